@@ -1,0 +1,355 @@
+"""Benchmark of the temporal-sieve hot path on B200 (contract: see DESIGN.md).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one DECIDE of the configured BASELINE workload: every repetition
+seed evaluates all 2^k_eff sieve points over the whole synthetic graph
+(default config 2 = BASELINE configs[1]: PathMotif k=6, n=1e5, m=1e6,
+4 repetitions).  Metric: GF(2^64) edge x level x sieve-point updates per
+second, updates = A * (k_eff - 1) * 2^k_eff per repetition.
+
+With N > 1 (torchrun) the 2^k_eff sieve points are sharded across ranks (no
+data-path collective); the per-vertex partial accumulators are XOR-combined
+once per step (NCCL all-gather + XOR kernel; NCCL has no XOR reduction).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+REPS = {1: 1, 2: 4, 3: 1, 4: 1, 5: 1}
+BYTES_PER_UPDATE = 16  # 8 B predecessor-state read + 8 B state write
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.stop = threading.Event()
+        self.proc = None
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi") is None:
+            return self
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        self.proc = subprocess.Popen(
+            ["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+             "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+        def reader():
+            for line in self.proc.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+        self.th = threading.Thread(target=reader, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def shard(P: int, rank: int, world: int):
+    """Contiguous sieve-point range of one rank."""
+    return rank * P // world, (rank + 1) * P // world
+
+
+# ------------------------------------------------------------------ CPU legs
+
+
+def cpu_sample(inst, k, colors, motif, anchor, seed=1, frac=0.1, threads=None):
+    """The reference's own eval_temporal_sieve (oracle/_ref) on a bounded
+    sample of the workload: the time prefix ts <= frac * t of the same graph
+    (all 2^k points, all levels).  Returns (updates/s, seconds, sample, kind, cores)."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count() or 1
+    max_ts = max(1, int(inst.t * frac))
+    arcs = int(np.count_nonzero(inst.ts <= max_ts)) * (1 if inst.directed else 2)
+    upd = arcs * (k - 1) * (1 << k)
+    sample = (f"ts <= {max_ts} of t={inst.t} ({arcs} arcs, all {1 << k} points, "
+              f"{k - 1} levels, seed {seed})")
+    if O.ref_available():
+        os.environ.setdefault("OMP_WAIT_POLICY", "active")
+        r = O.ref_eval(inst.n, inst.u, inst.v, inst.ts, inst.directed, colors, motif,
+                       max_ts=max_ts, seed=seed, lanes=8, threads=threads, anchor=anchor,
+                       t=inst.t, repeats=2)
+        return upd / r["seconds"], r["seconds"], sample, "reference", threads
+    cu, cv, ct = O.canonical_edges(inst.n, inst.u, inst.v, inst.ts, inst.directed)
+    from paper_2001_07158_b200.sieve import SieveConfig, build_shades
+    from paper_2001_07158_b200.graph import MotifQuery, VertexColoring
+    sh = build_shades(MotifQuery.from_multiset(motif), VertexColoring(colors, int(colors.max())),
+                      SieveConfig(seed=seed))
+    t0 = time.perf_counter()
+    O.eval_points(inst.n, cu, cv, ct, inst.directed, k, max_ts, sh.vertex_off, sh.vertex_shades,
+                  seed, anchor[0])
+    s = time.perf_counter() - t0
+    return upd / s, s, sample, "port", 1
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU implementation on the host cores."""
+    if rank != 0:
+        return
+    from paper_2001_07158_b200 import synth
+    inst = synth.make_config(args.config)
+    k, colors, motif, anchor = synth.effective_query(inst)
+    times, rates = [], []
+    info = None
+    for i in range(args.warmup + args.steps):
+        rate, sec, sample, kind, cores = cpu_sample(inst, k, colors, motif, anchor,
+                                                    frac=args.ref_frac)
+        info = (sample, kind, cores)
+        if i >= args.warmup:
+            times.append(sec)
+            rates.append(rate)
+    value = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64 (GF(2^64))",
+            "data": "synthetic", "config": config_json(inst, world, args),
+            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": info[2],
+                             "kind": info[1], "sample": info[0]},
+            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "GF(2^64) edge x level x sieve-pt updates/s (decide)"
+
+
+def config_json(inst, world, args):
+    k_eff = inst.k_eff
+    return {"workload": f"BASELINE configs[{args.config - 1}]: {inst.name}", "n": inst.n,
+            "m": inst.m, "t": inst.t, "directed": inst.directed, "k_eff": k_eff,
+            "sieve_points": 1 << k_eff, "repetitions": REPS[args.config],
+            "updates_per_step": inst.updates() * REPS[args.config],
+            "parallelism": f"sieve-point sharding x{world}",
+            "l2": "working set > L2 (state buffers 2*R*W*8 B, see DESIGN.md)"}
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-frac", type=float, default=0.1)
+    ap.add_argument("--points-per-batch", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2001_07158_b200 as T
+    from paper_2001_07158_b200 import _native, synth
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = local
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    inst = synth.make_config(args.config)
+    k, colors, motif, anchor = synth.effective_query(inst)
+    reps = REPS[args.config]
+    seeds = [1 + r for r in range(reps)]
+    P = 1 << k
+    p0, p1 = shard(P, rank, world)
+
+    g = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
+    col = T.VertexColoring(colors, int(colors.max()))
+    cfgs = [T.SieveConfig(seed=s, points_per_batch=args.points_per_batch) for s in seeds]
+    sh = T.build_shades(T.MotifQuery.from_multiset(motif), col, cfgs[0])
+    ds = T.DeviceShades(g, k, sh)
+    n = g.n()
+    acc = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
+    gathered = torch.zeros((world, reps, n), dtype=torch.int64, device="cuda") if world > 1 else None
+    total = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
+
+    def step():
+        acc.zero_()
+        for r in range(reps):
+            T.eval_points_device(g, ds, k, g.t(), cfgs[r], anchor[0], p0, p1,
+                                 acc[r].data_ptr(), sp)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered.view(-1), acc.view(-1))
+            T.xor_combine_device(gathered.data_ptr(), world, reps * n, total.data_ptr(), sp)
+            return total
+        return acc
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    _native.Profile.reset()
+    _native.Profile.enable(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _native.Profile.launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = _native.Profile.launches() - launches0
+    ms = e0.elapsed_time(e1) / args.steps
+    lvl_n, lvl_ms = _native.Profile.get("level")
+    all_n, all_ms = _native.Profile.get(None)
+    _native.Profile.enable(False)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    upd_step = inst.updates() * reps
+    value = upd_step / (ms * 1e-3)
+
+    # decision / checksum of the last step (finalize on the host)
+    host = res.cpu().numpy().view(np.uint64)
+    sink = anchor[1]
+    decisions, checksums = [], []
+    for r in range(reps):
+        a, nflag, cs = T.finalize(host[r], sink)
+        decisions.append(bool(nflag))
+        checksums.append(f"{cs:016x}")
+
+    # roofline of the dominant kernel (level, l >= 3): 16 B per (arc, point)
+    hbm, peak_kind = peaks()
+    W_eff = min(P // world if world > 1 else P, args.points_per_batch or 64)
+    roof = None
+    if lvl_n:
+        avg_ms = lvl_ms / lvl_n
+        alg_bytes = BYTES_PER_UPDATE * g.info.arcs * W_eff
+        achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                "kernel": "k_level (l>=3)", "avg_launch_ms": avg_ms,
+                "launch_share_of_step": lvl_ms / max(all_ms, 1e-9),
+                "alg_bytes_per_launch": alg_bytes}
+
+    # e2e through the public API with host buffers (graph build + shades +
+    # eval + accumulator read-back), same metric
+    e2e = None
+    if args.e2e_steps > 0:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            g2 = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
+            ds2 = T.DeviceShades(g2, k, sh)
+            a2 = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
+            for r in range(reps):
+                T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], p0, p1,
+                                     a2[r].data_ptr(), sp)
+            if world > 1:
+                dist.all_gather_into_tensor(gathered.view(-1), a2.view(-1))
+                T.xor_combine_device(gathered.data_ptr(), world, reps * n, total.data_ptr(), sp)
+                a2 = total
+            h = a2.cpu()
+            del g2, ds2
+        torch.cuda.synchronize()
+        sec = (time.perf_counter() - t0) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([sec], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        e2e = {"value": upd_step / sec, "unit": "updates/s",
+               "h2d_bytes_per_step": int(inst.m * 12 + sh.vertex_off.nbytes +
+                                         sh.vertex_shades.nbytes),
+               "d2h_bytes_per_step": int(reps * n * 8), "ms_per_step": sec * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            rate, sec, sample, kind, cores = cpu_sample(inst, k, colors, motif, anchor,
+                                                        frac=args.ref_frac)
+            cpu = {"value": rate, "unit": "updates/s", "cores": cores, "kind": kind,
+                   "sample": sample, "seconds": sec}
+        except Exception as e:  # reported, never fatal
+            cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable",
+                   "sample": str(e)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "u64 (GF(2^64) carry-less, integer pipes)", "data": "synthetic",
+                "config": config_json(inst, world, args), "roofline": roof, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
+                "decision": decisions, "checksums": checksums,
+                "graph": {"arcs": g.info.arcs, "runs": g.info.runs, "chunks": g.info.chunks,
+                          "split_chunks": g.info.split_chunks,
+                          "device_bytes": g.info.device_bytes},
+                "kernel_ms_per_step": {"level": lvl_ms / args.steps,
+                                       "all": all_ms / args.steps}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,149 @@
+/*
+ * tsv.h -- C-ABI of the B200 temporal-sieve engine (libtsv.so).
+ *
+ * Plain pointers and sizes only.  This is the boundary the host side of the
+ * reference would bind: the C++ drop-in (paper_2001_07158_b200/cpp, same API
+ * as /root/reference/proj/core/include/tsieve/{graph,sieve}.hpp) and the
+ * Python mirror (paper_2001_07158_b200/*.py, ctypes) both call it.  There is
+ * no CPU fallback: every compute entry point runs CUDA kernels for sm_100a or
+ * returns TSV_ERR_CUDA.
+ *
+ * Status codes: 0 ok; TSV_ERR_INVALID maps to the reference's
+ * std::invalid_argument, TSV_ERR_CAP to std::runtime_error (memory cap,
+ * sieve.cpp:161-166), TSV_ERR_CUDA to a device failure.  tsv_last_error()
+ * returns the message of the last failure on the calling thread.
+ */
+#ifndef TSV_H_
+#define TSV_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSV_OK 0
+#define TSV_ERR_INVALID 1
+#define TSV_ERR_CAP 2
+#define TSV_ERR_CUDA 3
+
+/* Opaque device-resident temporal graph: runs (head, ts) in vertex-major
+ * order, arcs grouped by run with their predecessor-state index, chunk table.
+ * Immutable after creation, so binary-search probes reuse it. */
+typedef struct tsv_graph tsv_graph;
+/* Opaque device-resident shade CSR (ShadeAssignment, sieve.hpp:39-56). */
+typedef struct tsv_shades tsv_shades;
+
+typedef struct {
+  int32_t n;          /* vertices */
+  int32_t t;          /* timestamp range [1..t] */
+  int32_t directed;
+  int32_t device;     /* CUDA ordinal the graph lives on */
+  int64_t m;          /* canonical edges (edge id = index) */
+  int64_t arcs;       /* m directed, 2m undirected */
+  int64_t runs;       /* distinct (ts, head) pairs */
+  int64_t chunks;     /* work chunks of the level kernel */
+  int64_t split_chunks; /* chunks that continue a vertex (carry fix-up) */
+  int64_t dropped_self_loops;
+  int64_t dropped_duplicates;
+  int64_t device_bytes; /* bytes of graph structure resident in HBM */
+} tsv_graph_info;
+
+/* Replaces TemporalGraph::build (graph.cpp:14-109) for the engine: drops
+ * self-loops, orients undirected edges u<v, sorts by (ts,u,v), removes
+ * duplicates (edge id = index), groups arcs into (ts, head) runs and uploads
+ * the layout to `device`.  t = 0 takes the max timestamp.  Errors: endpoint
+ * out of range, timestamp < 1 or > t (TSV_ERR_INVALID). */
+int tsv_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                    const int32_t* ts, int directed, int32_t t, int device,
+                    tsv_graph** out);
+
+/* Host-only canonicalization (no device): the edge list TemporalGraph::build
+ * keeps, in edge-id order.  Returns the kept count (<= m) or -1 on error. */
+int64_t tsv_canonical_edges(int32_t n, int64_t m, const int32_t* u,
+                            const int32_t* v, const int32_t* ts, int directed,
+                            int32_t* out_u, int32_t* out_v, int32_t* out_ts);
+
+void tsv_graph_free(tsv_graph* g);
+int tsv_graph_get_info(const tsv_graph* g, tsv_graph_info* out);
+
+/* Copies the canonical edge list (m entries each) back to the host. */
+int tsv_graph_edges(const tsv_graph* g, int32_t* u, int32_t* v, int32_t* ts);
+
+/* Uploads a shade CSR: vertex_off[n+1], vertex_shades[vertex_off[n]] with
+ * 1-based shade ids in [1..k] (build_shades, sieve.cpp:658-718). */
+int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
+                      const int32_t* vertex_shades, tsv_shades** out);
+void tsv_shades_free(tsv_shades* s);
+
+typedef struct {
+  uint64_t seed;             /* SieveConfig::seed */
+  int32_t field_bits;        /* must be 64 */
+  int32_t lane_width;        /* accepted, results independent of it */
+  int32_t edge_model;        /* 0 = instant (the only model on this path) */
+  int32_t points_per_batch;  /* 0 = engine choice; else power of two <= 128 */
+  uint64_t memory_cap_words; /* SieveConfig::memory_cap_words */
+} tsv_config;
+
+typedef struct {
+  int32_t global_nonzero;    /* decision (localize rule, sieve.cpp:149-150) */
+  int32_t pad;
+  int64_t flagged;           /* number of nonzero accumulators */
+  uint64_t checksum;         /* FNV-1a fold, sieve.cpp:35-49 */
+  uint64_t peak_field_words; /* field words resident during the evaluation */
+  double fn_bound;           /* (2k-1)/2^64 */
+} tsv_outcome;
+
+/* Replaces eval_temporal_sieve (sieve.hpp:84-87, sieve.cpp:720-732) for the
+ * instant edge model over GF(2^64).  accumulators: host buffer of n words
+ * (zero-extended, sink-only when anchor_sink >= 0).  Synchronous. */
+int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
+                            const int32_t* vertex_off,
+                            const int32_t* vertex_shades,
+                            const tsv_config* cfg, int32_t anchor_source,
+                            int32_t anchor_sink, uint64_t* accumulators,
+                            tsv_outcome* out);
+
+/* Sharded / device-resident form: XORs the contributions of sieve points
+ * A in [p_begin, p_end) into the DEVICE buffer d_acc (n words, caller-owned,
+ * not cleared) on `stream` (cudaStream_t, 0 = legacy default).  No finalize,
+ * no host copies.  Used for multi-GPU sieve-point sharding and timing. */
+int tsv_eval_points_device(const tsv_graph* g, const tsv_shades* s, int k,
+                           int32_t max_ts, const tsv_config* cfg,
+                           int32_t anchor_source, uint64_t p_begin,
+                           uint64_t p_end, uint64_t* d_acc, void* stream);
+
+/* d_out[i] = XOR_{p < nparts} d_parts[p*n + i] (multi-GPU combine). */
+int tsv_xor_combine_device(const uint64_t* d_parts, int nparts, int64_t n,
+                           uint64_t* d_out, void* stream);
+
+/* Host finalize of accumulators (sieve.cpp:136-159): sink restriction,
+ * flagged count, checksum.  Modifies acc in place when anchor_sink >= 0. */
+int tsv_finalize(int32_t n, uint64_t* acc, int32_t anchor_sink,
+                 tsv_outcome* out);
+
+/* Per-kernel device-time profile (CUDA events on the launching stream).
+ * names: "level", "level_first", "fixup", "readout", "zj" ... */
+int tsv_profile_enable(int on);
+int tsv_profile_get(const char* kernel, int64_t* launches, double* total_ms);
+int tsv_profile_reset(void);
+/* Number of engine kernels launched since the last reset. */
+int64_t tsv_kernel_launches(void);
+
+/* GF(2^64) on device: self-test of n products (a[i]*b[i] -> out[i], host
+ * buffers) with the production multiply (variant 0) or another variant. */
+int tsv_gf_mul_device(int variant, int64_t n, const uint64_t* a,
+                      const uint64_t* b, uint64_t* out);
+/* Throughput microbenchmark: products/s of a variant (device only). */
+int tsv_gf_bench(int variant, int64_t iters_per_thread, double* products_per_s);
+/* y draws on device (draw_nonzero(seed, role=3, edge, level-1, 0)). */
+int tsv_draw_edge_y_device(uint64_t seed, int32_t level, int64_t n,
+                           const int32_t* edges, uint64_t* out);
+
+const char* tsv_last_error(void);
+const char* tsv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSV_H_ */

@@ -1,0 +1,72 @@
+// engine.hpp -- device-side views and kernel launchers (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tsv {
+
+// Device pointers of a resident graph (layout.hpp describes the arrays).
+struct DevGraph {
+  int32_t n = 0;
+  int64_t A = 0, R = 0, C = 0;
+  const int32_t* arc_src = nullptr;
+  const uint32_t* arc_meta = nullptr;
+  const int32_t* arc_tail = nullptr;
+  const int32_t* run_head = nullptr;
+  const int32_t* run_ts = nullptr;
+  const int32_t* vtx_run_off = nullptr;
+  const int64_t* chunk_arc = nullptr;
+  const int32_t* chunk_run = nullptr;
+  const uint8_t* chunk_carry = nullptr;
+  const int32_t* carry_list = nullptr;
+  int32_t ncarry = 0;
+};
+
+// One sieve-point batch [pb, pe) of W = lanes * ppt consecutive points.
+struct Batch {
+  uint64_t pb = 0, pe = 0;
+  int lanes = 32, ppt = 1;
+#ifdef __CUDACC__
+  __host__ __device__
+#endif
+  int W() const { return lanes * ppt; }
+};
+
+struct LevelParams {
+  DevGraph g;
+  const uint64_t* zj = nullptr;  // n x k
+  int k = 0;
+  int ell = 2;                   // level being produced
+  uint64_t seed = 1;
+  int32_t anchor_source = -1;
+  Batch b;
+  const uint64_t* s_prev = nullptr;  // R x W (level ell-1), unused at ell=2
+  uint64_t* s_cur = nullptr;         // R x W (level ell)
+  uint64_t* agg = nullptr;           // C x W chunk tail aggregates
+};
+
+// Kernel launchers (kernels.cu).  All are asynchronous on `st`.
+void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
+               const int32_t* vertex_shades, const uint64_t* wtab, uint64_t* zj,
+               cudaStream_t st);
+void launch_level(const LevelParams& p, cudaStream_t st);
+void launch_fixup(const LevelParams& p, cudaStream_t st);
+void launch_readout(const DevGraph& g, int32_t max_ts, const uint64_t* s,
+                    int W, uint64_t* acc, cudaStream_t st);
+void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
+               uint64_t* acc, cudaStream_t st);
+void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n,
+                        uint64_t* out, cudaStream_t st);
+void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
+                   uint64_t* out, cudaStream_t st);
+void launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks,
+                     int threads, cudaStream_t st);
+void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,
+                   uint64_t* out, cudaStream_t st);
+
+// Profiling hooks (tsv_abi.cu).
+void prof_begin(const char* name, cudaStream_t st);
+void prof_end(cudaStream_t st);
+
+}  // namespace tsv

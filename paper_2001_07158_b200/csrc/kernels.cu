@@ -1,0 +1,401 @@
+// kernels.cu -- sm_100a kernels of the temporal sieve (instant edge model).
+//
+// The reference evaluates Eq. 3 time-major over dense n*W*(t+1) layers
+// (/root/reference/proj/core/src/sieve.cpp:170-307).  Here each level l is
+// ONE pass over the vertex-major arc stream (layout.hpp):
+//
+//   prod_a   = y(e_a, l-1) * S_{l-1}[src_a]            (gather, GF multiply)
+//   U_a      = XOR of prod over the head's arcs up to a  (segmented scan)
+//   S_l[run] = z_head^A * U_{last arc of run}           (at run ends)
+//
+// S_l[run] is P[l][head][ts(run)] of the reference: its stay term
+// (sieve.cpp:229-230) is the prefix over the head's earlier runs, and the
+// z_u multiply of sieve.cpp:255 commutes with that prefix because z_u is
+// constant along u's runs.  A warp owns one chunk of arcs; G = 32/LANES
+// arcs are in flight per step, each processed by LANES threads that hold
+// PPT sieve points apiece (W = LANES*PPT points per batch, contiguous in
+// HBM so every state gather/store is one coalesced W*8-byte segment).
+// Arc metadata and the y draws of 32 arcs are produced cooperatively (one
+// arc per thread) and staged in shared memory, so each draw costs one
+// thread, not W.
+#include <cuda_runtime.h>
+
+#include "engine.hpp"
+#include "gf_device.cuh"
+#include "layout.hpp"
+
+namespace tsv {
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr unsigned kFull = 0xffffffffu;
+
+template <int PPT>
+__device__ __forceinline__ void z_of(const uint64_t* __restrict__ zj, int k,
+                                     int32_t u, const uint32_t (&pt)[PPT],
+                                     const bool (&pv)[PPT],
+                                     uint64_t (&z)[PPT]) {
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) z[p] = 0;
+  const uint64_t* row = zj + static_cast<int64_t>(u) * k;
+  for (int j = 0; j < k; ++j) {
+    const uint64_t r = __ldg(row + j);
+#pragma unroll
+    for (int p = 0; p < PPT; ++p)
+      if ((pt[p] >> j) & 1u) z[p] ^= r;
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p)
+    if (!pv[p]) z[p] = 0;
+}
+
+__device__ __forceinline__ uint64_t z_single(const uint64_t* __restrict__ zj,
+                                             int k, int32_t u, uint64_t A) {
+  uint64_t z = 0;
+  const uint64_t* row = zj + static_cast<int64_t>(u) * k;
+  for (int j = 0; j < k; ++j)
+    if ((A >> j) & 1ull) z ^= __ldg(row + j);
+  return z;
+}
+
+template <int LANES, int PPT, bool FIRST>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+    k_level(const LevelParams P) {
+  constexpr int G = 32 / LANES;
+  constexpr int W = LANES * PPT;
+  constexpr int STEPS = 32 / G;  // steps per 32-arc batch
+  constexpr int UNR = (8 / PPT) < STEPS ? (8 / PPT) : STEPS;
+  __shared__ uint64_t s_y[kWarpsPerBlock][32];
+  __shared__ int32_t s_src[kWarpsPerBlock][32];
+  __shared__ uint32_t s_meta[kWarpsPerBlock][32];
+  __shared__ int32_t s_run[kWarpsPerBlock][32];
+
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
+  if (c >= P.g.C) return;  // warp-uniform
+  const int g = lane / LANES, li = lane % LANES;
+
+  uint32_t pt[PPT];
+  bool pv[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const uint64_t A = P.b.pb + li + LANES * p;
+    pt[p] = static_cast<uint32_t>(A);
+    pv[p] = A < P.b.pe;
+  }
+  const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
+  const uint64_t yb = static_cast<uint64_t>(P.ell - 1) + 0x165667b19e3779f9ull;
+  const int64_t a0 = P.g.chunk_arc[c], a1 = P.g.chunk_arc[c + 1];
+  int32_t run_ctr = P.g.chunk_run[c];
+  const int last_lane = (G - 1) * LANES + li;
+  uint64_t carry[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) carry[p] = 0;
+
+  for (int64_t base = a0; base < a1; base += 32) {
+    const int nb = static_cast<int>(a1 - base < 32 ? a1 - base : 32);
+    uint32_t meta = 0;
+    int32_t sidx = -1;
+    uint64_t y = 0;
+    if (lane < nb) {
+      meta = __ldg(P.g.arc_meta + base + lane);
+      sidx = FIRST ? __ldg(P.g.arc_tail + base + lane)
+                   : __ldg(P.g.arc_src + base + lane);
+      y = draw_edge_y(pre, yb, meta & kEdgeMask);
+    }
+    const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
+    s_y[wib][lane] = y;
+    s_src[wib][lane] = sidx;
+    s_meta[wib][lane] = meta;
+    s_run[wib][lane] = run_ctr + __popc(ends & ((1u << lane) - 1u));
+    run_ctr += __popc(ends);
+    __syncwarp();
+
+    for (int s0 = 0; s0 < STEPS; s0 += UNR) {
+      uint64_t val[UNR][PPT];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int i = (s0 + u) * G + g;
+        if (FIRST) {
+          if (i < nb) {
+            const int32_t tail = s_src[wib][i];
+            if (P.anchor_source >= 0 && tail != P.anchor_source) {
+#pragma unroll
+              for (int p = 0; p < PPT; ++p) val[u][p] = 0;
+            } else {
+              z_of<PPT>(P.zj, P.k, tail, pt, pv, val[u]);
+            }
+          } else {
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) val[u][p] = 0;
+          }
+        } else {
+          const int32_t src = i < nb ? s_src[wib][i] : -1;
+#pragma unroll
+          for (int p = 0; p < PPT; ++p)
+            val[u][p] = src >= 0
+                            ? __ldg(P.s_prev + static_cast<int64_t>(src) * W +
+                                    li + LANES * p)
+                            : 0ull;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int i = (s0 + u) * G + g;
+        const bool act = i < nb;
+        const uint32_t mt = act ? s_meta[wib][i] : 0u;
+        const uint64_t yy = act ? s_y[wib][i] : 0ull;
+        uint64_t v[PPT];
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) v[p] = gf_mul(yy, val[u][p]);
+        bool f = (mt & kVStart) != 0;
+        if (G > 1) {
+#pragma unroll
+          for (int d = 1; d < G; d <<= 1) {
+            const bool fo = __shfl_up_sync(kFull, f, d * LANES);
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) {
+              const uint64_t vo = __shfl_up_sync(kFull, v[p], d * LANES);
+              if (g >= d && !f) v[p] ^= vo;
+            }
+            if (g >= d) f = f || fo;
+          }
+        }
+        if (!f) {
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) v[p] ^= carry[p];
+        }
+        if (act && (mt & kRunEnd)) {
+          const int32_t run = s_run[wib][i];
+          const int32_t head = __ldg(P.g.run_head + run);
+          uint64_t z[PPT];
+          z_of<PPT>(P.zj, P.k, head, pt, pv, z);
+#pragma unroll
+          for (int p = 0; p < PPT; ++p)
+            P.s_cur[static_cast<int64_t>(run) * W + li + LANES * p] =
+                gf_mul(z[p], v[p]);
+        }
+#pragma unroll
+        for (int p = 0; p < PPT; ++p)
+          carry[p] = (G > 1) ? __shfl_sync(kFull, v[p], last_lane) : v[p];
+      }
+    }
+    __syncwarp();
+  }
+  if (g == 0) {
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) P.agg[c * W + li + LANES * p] = carry[p];
+  }
+}
+
+// Chunks that continue a long vertex receive the XOR of the preceding
+// pieces' tail aggregates, multiplied by z_head, on every run they end.
+__global__ void k_fixup(const LevelParams P) {
+  const int W = P.b.W();
+  const int32_t c = P.g.carry_list[blockIdx.x];
+  const int32_t r0 = P.g.chunk_run[c], r1 = P.g.chunk_run[c + 1];
+  if (r0 == r1) return;
+  const int32_t head = P.g.run_head[r0];
+  for (int w = threadIdx.x; w < W; w += blockDim.x) {
+    const uint64_t A = P.b.pb + static_cast<uint64_t>(w);
+    if (A >= P.b.pe) continue;
+    uint64_t carry = 0;
+    for (int64_t cc = c - 1;; --cc) {
+      carry ^= P.agg[cc * W + w];
+      if (!P.g.chunk_carry[cc]) break;
+    }
+    const uint64_t t = gf_mul(z_single(P.zj, P.k, head, A), carry);
+    for (int32_t r = r0; r < r1; ++r) P.s_cur[static_cast<int64_t>(r) * W + w] ^= t;
+  }
+}
+
+// acc[u] ^= XOR_w S_k[last run of u with ts <= max_ts][w]  (sieve.cpp:297-303)
+__global__ void k_readout(const DevGraph g, int32_t max_ts,
+                          const uint64_t* __restrict__ s, int W,
+                          uint64_t* __restrict__ acc) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= g.n) return;
+  int32_t lo = g.vtx_run_off[u], hi = g.vtx_run_off[u + 1];
+  while (lo < hi) {  // first run with ts > max_ts
+    const int32_t mid = lo + (hi - lo) / 2;
+    if (g.run_ts[mid] <= max_ts) lo = mid + 1;
+    else hi = mid;
+  }
+  const int32_t r = lo - 1;
+  if (r < g.vtx_run_off[u]) return;
+  uint64_t x = 0;
+  const uint64_t* row = s + static_cast<int64_t>(r) * W;
+  for (int w = 0; w < W; ++w) x ^= row[w];
+  acc[u] ^= x;
+}
+
+// k = 1: P_{u,1} = z_u^A, readout is the subset sum (sieve.cpp:203-213).
+__global__ void k_k1(int32_t n, const uint64_t* __restrict__ zj, Batch b,
+                     int32_t anchor_source, uint64_t* __restrict__ acc) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  if (anchor_source >= 0 && u != anchor_source) return;
+  uint64_t x = 0;
+  for (uint64_t A = b.pb; A < b.pe; ++A) x ^= z_single(zj, 1, static_cast<int32_t>(u), A);
+  acc[u] ^= x;
+}
+
+// z_{u,j} = XOR_{d in S(u)} v_{u,d} * w_{d,j}  (sieve.cpp:83-101)
+__global__ void k_zj(int32_t n, int k, uint64_t seed,
+                     const int32_t* __restrict__ vertex_off,
+                     const int32_t* __restrict__ vertex_shades,
+                     const uint64_t* __restrict__ wtab, uint64_t* __restrict__ zj) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const uint64_t pre = draw_prefix(seed, kRoleShadeV);
+  uint64_t row[32];
+  for (int j = 0; j < k; ++j) row[j] = 0;
+  for (int32_t s = vertex_off[u]; s < vertex_off[u + 1]; ++s) {
+    const int d = vertex_shades[s];
+    const uint64_t v = draw_nonzero_from(pre, static_cast<uint64_t>(u),
+                                         static_cast<uint64_t>(d), 0);
+    for (int j = 0; j < k; ++j) row[j] ^= gf_mul(v, wtab[(d - 1) * k + j]);
+  }
+  for (int j = 0; j < k; ++j) zj[u * k + j] = row[j];
+}
+
+__global__ void k_xor_combine(const uint64_t* __restrict__ parts, int nparts,
+                              int64_t n, uint64_t* __restrict__ out) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+       i < n; i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint64_t x = 0;
+    for (int p = 0; p < nparts; ++p) x ^= parts[p * n + i];
+    out[i] = x;
+  }
+}
+
+__device__ __forceinline__ uint64_t mul_variant(int variant, uint64_t a, uint64_t b) {
+  return variant == 1 ? gf_mul_serial(a, b) : gf_mul(a, b);
+}
+
+__global__ void k_gf_mul(int variant, int64_t n, const uint64_t* a,
+                         const uint64_t* b, uint64_t* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = mul_variant(variant, a[i], b[i]);
+}
+
+template <int VARIANT>
+__global__ void k_gf_bench(int64_t iters, uint64_t* sink) {
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t a0 = mix64(tid + 1), a1 = mix64(tid + 2), a2 = mix64(tid + 3),
+           a3 = mix64(tid + 4);
+  const uint64_t b = mix64(tid ^ 0x5555);
+  for (int64_t it = 0; it < iters; ++it) {
+    a0 = mul_variant(VARIANT, a0, b) ^ static_cast<uint64_t>(it);
+    a1 = mul_variant(VARIANT, a1, b) ^ static_cast<uint64_t>(it);
+    a2 = mul_variant(VARIANT, a2, b) ^ static_cast<uint64_t>(it);
+    a3 = mul_variant(VARIANT, a3, b) ^ static_cast<uint64_t>(it);
+  }
+  sink[tid] = a0 ^ a1 ^ a2 ^ a3;
+}
+
+__global__ void k_draw_y(uint64_t seed, int32_t level, int64_t n,
+                         const int32_t* edges, uint64_t* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t pre = draw_prefix(seed, kRoleEdgeY);
+  out[i] = draw_edge_y(pre, static_cast<uint64_t>(level - 1) + 0x165667b19e3779f9ull,
+                       static_cast<uint32_t>(edges[i]));
+}
+
+template <int LANES, int PPT>
+void level_dispatch(const LevelParams& p, cudaStream_t st) {
+  const dim3 grid(static_cast<unsigned>((p.g.C + kWarpsPerBlock - 1) / kWarpsPerBlock));
+  const dim3 block(kWarpsPerBlock * 32);
+  if (p.ell == 2)
+    k_level<LANES, PPT, true><<<grid, block, 0, st>>>(p);
+  else
+    k_level<LANES, PPT, false><<<grid, block, 0, st>>>(p);
+}
+
+unsigned blocks_for(int64_t n, int threads) {
+  return static_cast<unsigned>((n + threads - 1) / threads);
+}
+
+}  // namespace
+
+void launch_level(const LevelParams& p, cudaStream_t st) {
+  if (p.g.C == 0) return;
+  prof_begin(p.ell == 2 ? "level_first" : "level", st);
+  switch (p.b.lanes * 8 + p.b.ppt) {
+    case 1 * 8 + 1: level_dispatch<1, 1>(p, st); break;
+    case 2 * 8 + 1: level_dispatch<2, 1>(p, st); break;
+    case 4 * 8 + 1: level_dispatch<4, 1>(p, st); break;
+    case 8 * 8 + 1: level_dispatch<8, 1>(p, st); break;
+    case 16 * 8 + 1: level_dispatch<16, 1>(p, st); break;
+    case 32 * 8 + 1: level_dispatch<32, 1>(p, st); break;
+    case 32 * 8 + 2: level_dispatch<32, 2>(p, st); break;
+    case 32 * 8 + 4: level_dispatch<32, 4>(p, st); break;
+    default: break;
+  }
+  prof_end(st);
+}
+
+void launch_fixup(const LevelParams& p, cudaStream_t st) {
+  if (p.g.ncarry == 0) return;
+  prof_begin("fixup", st);
+  const int threads = p.b.W() < 128 ? ((p.b.W() + 31) / 32) * 32 : 128;
+  k_fixup<<<p.g.ncarry, threads, 0, st>>>(p);
+  prof_end(st);
+}
+
+void launch_readout(const DevGraph& g, int32_t max_ts, const uint64_t* s, int W,
+                    uint64_t* acc, cudaStream_t st) {
+  if (g.n == 0) return;
+  prof_begin("readout", st);
+  k_readout<<<blocks_for(g.n, 256), 256, 0, st>>>(g, max_ts, s, W, acc);
+  prof_end(st);
+}
+
+void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
+               uint64_t* acc, cudaStream_t st) {
+  if (n == 0) return;
+  prof_begin("k1", st);
+  k_k1<<<blocks_for(n, 256), 256, 0, st>>>(n, zj, b, anchor_source, acc);
+  prof_end(st);
+}
+
+void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
+               const int32_t* vertex_shades, const uint64_t* wtab, uint64_t* zj,
+               cudaStream_t st) {
+  if (n == 0) return;
+  prof_begin("zj", st);
+  k_zj<<<blocks_for(n, 128), 128, 0, st>>>(n, k, seed, vertex_off, vertex_shades, wtab, zj);
+  prof_end(st);
+}
+
+void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n, uint64_t* out,
+                        cudaStream_t st) {
+  if (n == 0) return;
+  prof_begin("xor_combine", st);
+  const unsigned blocks = blocks_for(n, 256) < 148 * 8 ? blocks_for(n, 256) : 148 * 8;
+  k_xor_combine<<<blocks, 256, 0, st>>>(parts, nparts, n, out);
+  prof_end(st);
+}
+
+void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
+                   uint64_t* out, cudaStream_t st) {
+  if (n == 0) return;
+  k_gf_mul<<<blocks_for(n, 256), 256, 0, st>>>(variant, n, a, b, out);
+}
+
+void launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks, int threads,
+                     cudaStream_t st) {
+  if (variant == 1)
+    k_gf_bench<1><<<blocks, threads, 0, st>>>(iters, sink);
+  else
+    k_gf_bench<0><<<blocks, threads, 0, st>>>(iters, sink);
+}
+
+void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,
+                   uint64_t* out, cudaStream_t st) {
+  if (n == 0) return;
+  k_draw_y<<<blocks_for(n, 256), 256, 0, st>>>(seed, level, n, edges, out);
+}
+
+}  // namespace tsv

@@ -1,0 +1,621 @@
+// tsv_abi.cu -- the extern "C" boundary of libtsv.so (declared in include/tsv.h).
+//
+// Host orchestration of the sieve: graph upload, shade upload, z-table build,
+// batch loop over sieve points, level passes, readout, finalize.  Errors are
+// reported as status codes plus a thread-local message; the C++ drop-in
+// rethrows them as the reference's exception types.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tsv.h"
+#include "engine.hpp"
+#include "gf_device.cuh"
+#include "layout.hpp"
+
+namespace {
+
+thread_local std::string g_error;
+
+struct CapError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define TSV_CUDA(x)                                                           \
+  do {                                                                        \
+    cudaError_t e_ = (x);                                                     \
+    if (e_ != cudaSuccess)                                                    \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return TSV_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return TSV_ERR_INVALID;
+  } catch (const CapError& e) {
+    g_error = e.what();
+    return TSV_ERR_CAP;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return TSV_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return TSV_ERR_CUDA;
+  }
+}
+
+// ---- profiling -------------------------------------------------------------
+
+struct ProfRec {
+  std::string name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_prof;
+thread_local const char* g_prof_open = nullptr;
+thread_local cudaEvent_t g_prof_open_ev = nullptr;
+std::atomic<int64_t> g_launches{0};
+
+template <typename T>
+T* dalloc(size_t count) {
+  T* p = nullptr;
+  if (count == 0) count = 1;
+  TSV_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+template <typename T>
+T* dupload(const std::vector<T>& v) {
+  T* p = dalloc<T>(v.size());
+  if (!v.empty())
+    TSV_CUDA(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t bytes, cudaStream_t s) : st(s) {
+    TSV_CUDA(cudaMallocAsync(&p, bytes ? bytes : 8, s));
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct DeviceGuard {
+  int prev = 0;
+  explicit DeviceGuard(int dev) {
+    TSV_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) TSV_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() { cudaSetDevice(prev); }
+};
+
+}  // namespace
+
+namespace tsv {
+
+void prof_begin(const char* name, cudaStream_t st) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof_on) return;
+  cudaEventCreate(&g_prof_open_ev);
+  cudaEventRecord(g_prof_open_ev, st);
+  g_prof_open = name;
+}
+
+void prof_end(cudaStream_t st) {
+  if (!g_prof_on || !g_prof_open) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof.push_back({g_prof_open, g_prof_open_ev, e});
+  g_prof_open = nullptr;
+}
+
+}  // namespace tsv
+
+struct tsv_graph {
+  tsv::HostLayout host;  // canonical edges kept; run/arc vectors released
+  tsv::DevGraph dev;
+  int device = 0;
+  int64_t device_bytes = 0;
+  std::vector<void*> owned;
+  ~tsv_graph() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (void* p : owned) cudaFree(p);
+    cudaSetDevice(prev);
+  }
+};
+
+struct tsv_shades {
+  int k = 0;
+  int32_t n = 0;
+  int device = 0;
+  int32_t* off = nullptr;
+  int32_t* shades = nullptr;
+  ~tsv_shades() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    cudaFree(off);
+    cudaFree(shades);
+    cudaSetDevice(prev);
+  }
+};
+
+namespace {
+
+template <typename T>
+const T* own_upload(tsv_graph* g, const std::vector<T>& v) {
+  T* p = dupload(v);
+  g->owned.push_back(p);
+  g->device_bytes += static_cast<int64_t>(std::max<size_t>(v.size(), 1) * sizeof(T));
+  return p;
+}
+
+void check_config(const tsv_config* cfg) {
+  if (!cfg) throw std::invalid_argument("null config");
+  if (cfg->field_bits != 8 && cfg->field_bits != 16 && cfg->field_bits != 32 &&
+      cfg->field_bits != 64)
+    throw std::invalid_argument("field_bits must be 8, 16, 32 or 64");
+  if (cfg->field_bits != 64)
+    throw std::invalid_argument(
+        "the B200 engine evaluates GF(2^64) only (field_bits must be 64)");
+  const int W = cfg->lane_width;
+  if (W < 1 || W > 256 || (W & (W - 1)))
+    throw std::invalid_argument("lane_width must be a power of two in [1,256]");
+  if (cfg->edge_model != 0)
+    throw std::invalid_argument("the B200 engine evaluates the instant edge model only");
+  const int ppb = cfg->points_per_batch;
+  if (ppb != 0 && (ppb < 1 || ppb > 128 || (ppb & (ppb - 1))))
+    throw std::invalid_argument("points_per_batch must be 0 or a power of two <= 128");
+}
+
+tsv::Batch batch_shape(int W) {
+  tsv::Batch b;
+  if (W >= 32) {
+    b.lanes = 32;
+    b.ppt = W / 32;
+  } else {
+    b.lanes = W;
+    b.ppt = 1;
+  }
+  return b;
+}
+
+// Points per batch: the largest power of two <= min(range, 64) whose
+// working set fits the word cap and free device memory.
+int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cfg,
+                 uint64_t* peak_words) {
+  const uint64_t R = static_cast<uint64_t>(g->dev.R), C = static_cast<uint64_t>(g->dev.C);
+  const uint64_t n = static_cast<uint64_t>(g->dev.n);
+  auto words = [&](uint64_t W) {
+    return (k >= 2 ? 2 * R * W + C * W : 0) + n * static_cast<uint64_t>(k) + n;
+  };
+  int W = cfg->points_per_batch ? cfg->points_per_batch : 64;
+  while (static_cast<uint64_t>(W) > range && W > 1) W >>= 1;
+  if (cfg->points_per_batch == 0) {
+    size_t free_b = 0, total_b = 0;
+    TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t budget = static_cast<uint64_t>(free_b * 0.85) / 8;
+    while (W > 1 && (words(W) > cfg->memory_cap_words || words(W) > budget)) W >>= 1;
+  }
+  *peak_words = words(W);
+  if (words(W) > cfg->memory_cap_words)
+    throw CapError("sieve memory cap exceeded: needs " + std::to_string(words(W)) +
+                   " field words, cap " + std::to_string(cfg->memory_cap_words));
+  return W;
+}
+
+void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
+                 const tsv_config* cfg, int32_t anchor_source, uint64_t p_begin,
+                 uint64_t p_end, uint64_t* d_acc, cudaStream_t st,
+                 uint64_t* peak_out) {
+  check_config(cfg);
+  if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
+  if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
+  if (!sh || sh->n != g->dev.n || sh->k != k)
+    throw std::invalid_argument("shade assignment built for a different graph");
+  const uint64_t P = 1ull << k;
+  p_end = std::min(p_end, P);
+  if (p_begin >= p_end) return;
+  uint64_t peak = 0;
+  const int W = choose_width(g, k, p_end - p_begin, cfg, &peak);
+  if (peak_out) *peak_out = peak;
+  const int32_t n = g->dev.n;
+
+  // w_{d,j} table on the host (k^2 draws), z_{u,j} on the device.
+  std::vector<uint64_t> wtab(static_cast<size_t>(k) * k);
+  for (int d = 1; d <= k; ++d)
+    for (int j = 1; j <= k; ++j)
+      wtab[(d - 1) * k + (j - 1)] = tsv::draw_nonzero(cfg->seed, tsv::kRoleShadeW, d, j, 0);
+  DevBuf d_w(wtab.size() * 8, st), d_zj(static_cast<size_t>(n) * k * 8, st);
+  TSV_CUDA(cudaMemcpyAsync(d_w.p, wtab.data(), wtab.size() * 8, cudaMemcpyHostToDevice, st));
+  tsv::launch_zj(n, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
+                 d_zj.as<uint64_t>(), st);
+  TSV_CUDA(cudaGetLastError());
+
+  if (k == 1) {
+    tsv::Batch b;
+    b.pb = p_begin;
+    b.pe = p_end;
+    tsv::launch_k1(n, d_zj.as<uint64_t>(), b, anchor_source, d_acc, st);
+    TSV_CUDA(cudaGetLastError());
+    return;
+  }
+  const size_t state_words = static_cast<size_t>(g->dev.R) * W;
+  DevBuf s0(state_words * 8, st), s1(state_words * 8, st),
+      agg(static_cast<size_t>(g->dev.C) * W * 8, st);
+  tsv::LevelParams lp;
+  lp.g = g->dev;
+  lp.zj = d_zj.as<uint64_t>();
+  lp.k = k;
+  lp.seed = cfg->seed;
+  lp.anchor_source = anchor_source;
+  lp.agg = agg.as<uint64_t>();
+  for (uint64_t pb = p_begin; pb < p_end; pb += W) {
+    lp.b = batch_shape(W);
+    lp.b.pb = pb;
+    lp.b.pe = std::min(p_end, pb + static_cast<uint64_t>(W));
+    uint64_t* cur = s0.as<uint64_t>();
+    uint64_t* prev = s1.as<uint64_t>();
+    for (int ell = 2; ell <= k; ++ell) {
+      lp.ell = ell;
+      lp.s_prev = prev;
+      lp.s_cur = cur;
+      tsv::launch_level(lp, st);
+      tsv::launch_fixup(lp, st);
+      std::swap(cur, prev);
+    }
+    tsv::launch_readout(g->dev, max_ts, prev, W, d_acc, st);
+    TSV_CUDA(cudaGetLastError());
+  }
+}
+
+void finalize_host(int32_t n, uint64_t* acc, int32_t sink, int k, tsv_outcome* out) {
+  int64_t flagged = 0;
+  uint64_t h = 1469598103934665603ull;
+  auto eat = [&](uint64_t x) {
+    for (int i = 0; i < 8; ++i) {
+      h ^= (x >> (8 * i)) & 0xff;
+      h *= 1099511628211ull;
+    }
+  };
+  for (int32_t u = 0; u < n; ++u) {
+    if (sink >= 0 && u != sink) acc[u] = 0;
+    if (!acc[u]) continue;
+    ++flagged;
+    eat(static_cast<uint64_t>(u));
+    eat(acc[u]);
+  }
+  out->flagged = flagged;
+  out->global_nonzero = flagged > 0;
+  out->checksum = h;
+  out->fn_bound = (2.0 * k - 1.0) / std::pow(2.0, 64);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tsv_last_error(void) { return g_error.c_str(); }
+const char* tsv_version(void) { return "tsv-b200 0.1 (sm_100a)"; }
+
+int tsv_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                    const int32_t* ts, int directed, int32_t t, int device,
+                    tsv_graph** out) {
+  return guard([&] {
+    if (!out) throw std::invalid_argument("null output handle");
+    *out = nullptr;
+    if (m < 0) throw std::invalid_argument("negative edge count");
+    if (m > 0 && (!u || !v || !ts)) throw std::invalid_argument("null edge arrays");
+    auto* g = new tsv_graph();
+    try {
+      g->device = device;
+      tsv::canonicalize(n, m, u, v, ts, directed != 0, t, g->host);
+      DeviceGuard dg(device);
+      cudaDeviceProp prop{};
+      TSV_CUDA(cudaGetDeviceProperties(&prop, device));
+      tsv::build_layout(g->host, 0, prop.multiProcessorCount);
+      tsv::HostLayout& L = g->host;
+      tsv::DevGraph& d = g->dev;
+      d.n = L.n;
+      d.A = static_cast<int64_t>(L.arc_src.size());
+      d.R = static_cast<int64_t>(L.run_head.size());
+      d.C = static_cast<int64_t>(L.chunk_carry.size());
+      d.arc_src = own_upload(g, L.arc_src);
+      d.arc_meta = own_upload(g, L.arc_meta);
+      d.arc_tail = own_upload(g, L.arc_tail);
+      d.run_head = own_upload(g, L.run_head);
+      d.run_ts = own_upload(g, L.run_ts);
+      d.vtx_run_off = own_upload(g, L.vtx_run_off);
+      d.chunk_arc = own_upload(g, L.chunk_arc);
+      d.chunk_run = own_upload(g, L.chunk_run);
+      d.chunk_carry = own_upload(g, L.chunk_carry);
+      d.carry_list = own_upload(g, L.carry_list);
+      d.ncarry = static_cast<int32_t>(L.carry_list.size());
+      // release the host copies of the device layout (keep canonical edges)
+      std::vector<int32_t>().swap(L.arc_src);
+      std::vector<int32_t>().swap(L.arc_tail);
+      std::vector<uint32_t>().swap(L.arc_meta);
+      std::vector<int32_t>().swap(L.run_head);
+      std::vector<int32_t>().swap(L.run_ts);
+      TSV_CUDA(cudaDeviceSynchronize());
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+  });
+}
+
+int64_t tsv_canonical_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                            const int32_t* ts, int directed, int32_t* out_u, int32_t* out_v,
+                            int32_t* out_ts) {
+  int64_t kept = -1;
+  int rc = guard([&] {
+    tsv::HostLayout L;
+    tsv::canonicalize(n, m, u, v, ts, directed != 0, 0, L);
+    kept = static_cast<int64_t>(L.eu.size());
+    for (int64_t i = 0; i < kept; ++i) {
+      out_u[i] = L.eu[i];
+      out_v[i] = L.ev[i];
+      out_ts[i] = L.ets[i];
+    }
+  });
+  return rc == TSV_OK ? kept : -1;
+}
+
+void tsv_graph_free(tsv_graph* g) { delete g; }
+
+int tsv_graph_get_info(const tsv_graph* g, tsv_graph_info* out) {
+  return guard([&] {
+    if (!g || !out) throw std::invalid_argument("null argument");
+    out->n = g->host.n;
+    out->t = g->host.t;
+    out->directed = g->host.directed ? 1 : 0;
+    out->device = g->device;
+    out->m = static_cast<int64_t>(g->host.eu.size());
+    out->arcs = g->dev.A;
+    out->runs = g->dev.R;
+    out->chunks = g->dev.C;
+    out->split_chunks = g->dev.ncarry;
+    out->dropped_self_loops = g->host.dropped_self_loops;
+    out->dropped_duplicates = g->host.dropped_duplicates;
+    out->device_bytes = g->device_bytes;
+  });
+}
+
+int tsv_graph_edges(const tsv_graph* g, int32_t* u, int32_t* v, int32_t* ts) {
+  return guard([&] {
+    if (!g) throw std::invalid_argument("null graph");
+    const size_t m = g->host.eu.size();
+    if (m && u) std::memcpy(u, g->host.eu.data(), m * 4);
+    if (m && v) std::memcpy(v, g->host.ev.data(), m * 4);
+    if (m && ts) std::memcpy(ts, g->host.ets.data(), m * 4);
+  });
+}
+
+int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
+                      const int32_t* vertex_shades, tsv_shades** out) {
+  return guard([&] {
+    if (!g || !out || !vertex_off) throw std::invalid_argument("null argument");
+    *out = nullptr;
+    if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
+    const int32_t n = g->host.n;
+    if (vertex_off[0] != 0) throw std::invalid_argument("vertex_off[0] must be 0");
+    for (int32_t i = 0; i < n; ++i)
+      if (vertex_off[i + 1] < vertex_off[i])
+        throw std::invalid_argument("vertex_off must be non-decreasing");
+    const int64_t cnt = vertex_off[n];
+    for (int64_t i = 0; i < cnt; ++i)
+      if (vertex_shades[i] < 1 || vertex_shades[i] > k)
+        throw std::invalid_argument("shade id outside [1..k]");
+    DeviceGuard dg(g->device);
+    auto* s = new tsv_shades();
+    s->k = k;
+    s->n = n;
+    s->device = g->device;
+    try {
+      s->off = dalloc<int32_t>(static_cast<size_t>(n) + 1);
+      s->shades = dalloc<int32_t>(static_cast<size_t>(cnt));
+      TSV_CUDA(cudaMemcpy(s->off, vertex_off, (static_cast<size_t>(n) + 1) * 4,
+                          cudaMemcpyHostToDevice));
+      if (cnt)
+        TSV_CUDA(cudaMemcpy(s->shades, vertex_shades, static_cast<size_t>(cnt) * 4,
+                            cudaMemcpyHostToDevice));
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+void tsv_shades_free(tsv_shades* s) { delete s; }
+
+int tsv_eval_points_device(const tsv_graph* g, const tsv_shades* s, int k,
+                           int32_t max_ts, const tsv_config* cfg,
+                           int32_t anchor_source, uint64_t p_begin, uint64_t p_end,
+                           uint64_t* d_acc, void* stream) {
+  return guard([&] {
+    if (!g || !d_acc) throw std::invalid_argument("null argument");
+    DeviceGuard dg(g->device);
+    eval_device(g, s, k, max_ts, cfg, anchor_source, p_begin, p_end, d_acc,
+                static_cast<cudaStream_t>(stream), nullptr);
+  });
+}
+
+int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
+                            const int32_t* vertex_off, const int32_t* vertex_shades,
+                            const tsv_config* cfg, int32_t anchor_source,
+                            int32_t anchor_sink, uint64_t* accumulators,
+                            tsv_outcome* out) {
+  tsv_shades* sh = nullptr;
+  int rc = guard([&] {
+    if (!g || !accumulators || !out) throw std::invalid_argument("null argument");
+    check_config(cfg);
+    if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
+    if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
+  });
+  if (rc) return rc;
+  rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
+  if (rc) return rc;
+  rc = guard([&] {
+    DeviceGuard dg(g->device);
+    const int32_t n = g->host.n;
+    cudaStream_t st = nullptr;
+    TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    uint64_t peak = 0;
+    try {
+      DevBuf acc(static_cast<size_t>(n) * 8, st);
+      TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8, st));
+      eval_device(g, sh, k, max_ts, cfg, anchor_source, 0, 1ull << k, acc.as<uint64_t>(),
+                  st, &peak);
+      if (n)
+        TSV_CUDA(cudaMemcpyAsync(accumulators, acc.p, static_cast<size_t>(n) * 8,
+                                 cudaMemcpyDeviceToHost, st));
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    TSV_CUDA(cudaStreamSynchronize(st));
+    TSV_CUDA(cudaStreamDestroy(st));
+    finalize_host(n, accumulators, anchor_sink, k, out);
+    out->peak_field_words = peak;
+  });
+  tsv_shades_free(sh);
+  return rc;
+}
+
+int tsv_xor_combine_device(const uint64_t* d_parts, int nparts, int64_t n,
+                           uint64_t* d_out, void* stream) {
+  return guard([&] {
+    if (nparts < 1 || n < 0) throw std::invalid_argument("bad combine shape");
+    tsv::launch_xor_combine(d_parts, nparts, n, d_out, static_cast<cudaStream_t>(stream));
+    TSV_CUDA(cudaGetLastError());
+  });
+}
+
+int tsv_finalize(int32_t n, uint64_t* acc, int32_t anchor_sink, tsv_outcome* out) {
+  return guard([&] {
+    if (!out || (n > 0 && !acc)) throw std::invalid_argument("null argument");
+    *out = tsv_outcome{};
+    finalize_host(n, acc, anchor_sink, 1, out);
+  });
+}
+
+int tsv_profile_enable(int on) {
+  g_prof_on = on != 0;
+  return TSV_OK;
+}
+
+int tsv_profile_get(const char* kernel, int64_t* launches, double* total_ms) {
+  return guard([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    int64_t cnt = 0;
+    double ms = 0;
+    for (auto& r : g_prof) {
+      if (kernel && r.name != kernel) continue;
+      TSV_CUDA(cudaEventSynchronize(r.b));
+      float x = 0;
+      TSV_CUDA(cudaEventElapsedTime(&x, r.a, r.b));
+      ms += x;
+      ++cnt;
+    }
+    if (launches) *launches = cnt;
+    if (total_ms) *total_ms = ms;
+  });
+}
+
+int tsv_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  g_prof.clear();
+  g_launches.store(0);
+  return TSV_OK;
+}
+
+int64_t tsv_kernel_launches(void) { return g_launches.load(); }
+
+int tsv_gf_mul_device(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
+                      uint64_t* out) {
+  return guard([&] {
+    if (n < 0) throw std::invalid_argument("negative count");
+    DevBuf da(n * 8, nullptr), db(n * 8, nullptr), dc(n * 8, nullptr);
+    if (n) {
+      TSV_CUDA(cudaMemcpy(da.p, a, n * 8, cudaMemcpyHostToDevice));
+      TSV_CUDA(cudaMemcpy(db.p, b, n * 8, cudaMemcpyHostToDevice));
+    }
+    tsv::launch_gf_mul(variant, n, da.as<uint64_t>(), db.as<uint64_t>(), dc.as<uint64_t>(),
+                       nullptr);
+    TSV_CUDA(cudaGetLastError());
+    if (n) TSV_CUDA(cudaMemcpy(out, dc.p, n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+int tsv_gf_bench(int variant, int64_t iters, double* products_per_s) {
+  return guard([&] {
+    int dev = 0, sms = 0;
+    TSV_CUDA(cudaGetDevice(&dev));
+    TSV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int threads = 256, blocks = sms * 8;
+    DevBuf sink(static_cast<size_t>(threads) * blocks * 8, nullptr);
+    tsv::launch_gf_bench(variant, 16, sink.as<uint64_t>(), blocks, threads, nullptr);
+    cudaEvent_t a, b;
+    TSV_CUDA(cudaEventCreate(&a));
+    TSV_CUDA(cudaEventCreate(&b));
+    TSV_CUDA(cudaEventRecord(a));
+    tsv::launch_gf_bench(variant, iters, sink.as<uint64_t>(), blocks, threads, nullptr);
+    TSV_CUDA(cudaEventRecord(b));
+    TSV_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    TSV_CUDA(cudaEventElapsedTime(&ms, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *products_per_s = 4.0 * iters * threads * blocks / (ms * 1e-3);
+  });
+}
+
+int tsv_draw_edge_y_device(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,
+                           uint64_t* out) {
+  return guard([&] {
+    DevBuf de(n * 4, nullptr), dy(n * 8, nullptr);
+    if (n) TSV_CUDA(cudaMemcpy(de.p, edges, n * 4, cudaMemcpyHostToDevice));
+    tsv::launch_draw_y(seed, level, n, de.as<int32_t>(), dy.as<uint64_t>(), nullptr);
+    TSV_CUDA(cudaGetLastError());
+    if (n) TSV_CUDA(cudaMemcpy(out, dy.p, n * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

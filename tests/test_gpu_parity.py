@@ -1,0 +1,213 @@
+"""GPU parity tests proper: the CUDA engine through the C-ABI (libtsv.so)
+against the golden vectors (reference outputs) and the CPU oracle.  Bit-exact
+everywhere: field arithmetic is integer work."""
+import numpy as np
+import pytest
+
+import paper_2001_07158_b200 as T
+from paper_2001_07158_b200 import _native, synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def u64(h):
+    return int(h, 16)
+
+
+def run_case(c, **cfgkw):
+    g = T.TemporalGraph.build(c["n"], (c["u"], c["v"], c["ts"]), c["directed"], c["t"])
+    col = T.VertexColoring(c["colors"], max(c["colors"]))
+    cfg = T.SieveConfig(seed=c["seed"], **cfgkw)
+    sh = T.build_shades(T.MotifQuery.from_multiset(c["motif"]), col, cfg)
+    if not sh.feasible:
+        return None
+    max_ts = c["max_ts"] or g.t()
+    return T.eval_temporal_sieve(g, len(c["motif"]), max_ts, sh, cfg,
+                                 T.AnchorSpec(*c["anchor"]))
+
+
+def test_gf_mul_device_matches_reference(cuda_device, golden):
+    a = np.array([u64(x[0]) for x in golden["gf_mul"]], np.uint64)
+    b = np.array([u64(x[1]) for x in golden["gf_mul"]], np.uint64)
+    want = [u64(x[2]) for x in golden["gf_mul"]]
+    for variant in (0, 1):
+        assert _native.gf_mul_device(a, b, variant).tolist() == want
+    assert _native.gf_mul_device([1 << 63], [2]).tolist() == [0x1B]
+
+
+def test_gf_mul_device_random_vs_oracle(cuda_device):
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 2**64 - 1, 200_000, dtype=np.uint64, endpoint=True)
+    b = rng.integers(0, 2**64 - 1, 200_000, dtype=np.uint64, endpoint=True)
+    a[:64] = 1 << np.arange(64, dtype=np.uint64)   # every single-bit operand
+    b[:64] = np.uint64(2**64 - 1)
+    got = _native.gf_mul_device(a, b)
+    idx = rng.choice(len(a), 3000, replace=False).tolist() + list(range(64))
+    for i in idx:
+        assert int(got[i]) == O.gf_mul(int(a[i]), int(b[i]))
+
+
+def test_edge_y_draws_device(cuda_device):
+    edges = np.arange(0, 5000, 7, dtype=np.int32)
+    for seed, level in ((1, 2), (99, 5)):
+        got = _native.draw_edge_y_device(seed, level, edges)
+        for e, y in zip(edges.tolist()[:200], got.tolist()[:200]):
+            assert y == O.draw_nonzero(seed, 3, e, level - 1, 0)
+
+
+def test_golden_sieve_cases(cuda_device, golden):
+    nz = 0
+    for c in golden["sieve"]:
+        out = run_case(c)
+        if out is None:
+            assert not c["feasible"]
+            continue
+        assert f"{out.checksum:016x}" == c["checksum"], c["name"]
+        assert out.flagged.tolist() == c["flagged"], c["name"]
+        assert out.global_nonzero == c["global"], c["name"]
+        if "acc" in c:
+            assert [f"{int(x):016x}" for x in out.accumulators] == c["acc"], c["name"]
+        nz += len(c["flagged"]) > 0
+    assert nz >= 20
+
+
+@pytest.mark.parametrize("ppb", [1, 2, 4, 8, 16, 32, 64, 128])
+def test_results_independent_of_batch_width(cuda_device, golden, ppb):
+    """test_sieve.cpp:291-308 (lane/thread invariance) for every kernel shape."""
+    by = {c["name"]: c for c in golden["sieve"]}
+    for name in ("fig2 seed5", "C1 k-TempPath k=5", "random 3", "random 7", "random 11"):
+        c = by[name]
+        out = run_case(c, points_per_batch=ppb)
+        if out is None:
+            continue
+        assert f"{out.checksum:016x}" == c["checksum"], (name, ppb)
+        if "acc" in c:
+            assert [f"{int(x):016x}" for x in out.accumulators] == c["acc"], (name, ppb)
+
+
+def test_decreasing_timestamps_no_for_every_seed(cuda_device):
+    # test_sieve.cpp:92-104: soundness holds for every seed
+    g = T.TemporalGraph.build(3, [(0, 1, 2), (1, 2, 1)], True)
+    col = T.VertexColoring([1, 2, 3], 3)
+    for seed in range(1, 21):
+        cfg = T.SieveConfig(seed=seed)
+        sh = T.build_shades(T.MotifQuery.from_multiset([1, 2, 3]), col, cfg)
+        assert not T.eval_temporal_sieve(g, 3, g.t(), sh, cfg).global_nonzero
+
+
+def _oracle_vs_gpu(n, u, v, ts, d, colors, motif, seed, anchor=(-1, -1), max_ts=None, ppb=0):
+    g = T.TemporalGraph.build(n, (u, v, ts), d)
+    col = T.VertexColoring(colors, int(max(colors)))
+    cfg = T.SieveConfig(seed=seed, points_per_batch=ppb)
+    sh = T.build_shades(T.MotifQuery.from_multiset(motif), col, cfg)
+    if not sh.feasible:
+        return None
+    mt = max_ts or g.t()
+    out = T.eval_temporal_sieve(g, len(motif), mt, sh, cfg, T.AnchorSpec(*anchor))
+    cu, cv, ct = g.edges()
+    acc, nf, cs = O.oracle_eval(n, cu, cv, ct, d, len(motif), mt, sh.vertex_off,
+                                sh.vertex_shades, seed, anchor)
+    assert np.array_equal(out.accumulators, acc)
+    assert out.checksum == cs
+    return nf
+
+
+def test_random_sweep_vs_oracle(cuda_device):
+    rng = np.random.default_rng(123)
+    nz = 0
+    for i in range(120):
+        n, u, v, ts, d, colors, motif = synth.random_small(rng, n_max=30, m_max=120, t_max=10,
+                                                           k_max=7)
+        anchor = (-1, -1)
+        if i % 3 == 0:
+            s, dd = rng.choice(n, 2, replace=False)
+            anchor = (int(s), int(dd))
+        cu, _, ct = O.canonical_edges(n, u, v, ts, d)
+        tmax = int(ct.max()) if len(ct) else 1
+        nf = _oracle_vs_gpu(n, u, v, ts, d, colors, motif, int(rng.integers(1, 1 << 40)), anchor,
+                            int(rng.integers(1, tmax + 1)), ppb=int(rng.choice([0, 1, 4, 32])))
+        nz += bool(nf)
+    assert nz > 15
+
+
+def test_hub_vertices_split_across_chunks(cuda_device):
+    """A head with far more in-arcs than a chunk holds is split into pieces
+    whose per-vertex prefix is repaired by the carry fix-up kernel."""
+    rng = np.random.default_rng(9)
+    n, m, t = 300, 12000, 60
+    u = rng.integers(0, n, m)
+    v = np.where(rng.random(m) < 0.5, 0, rng.integers(0, n, m))   # vertex 0 is a hub
+    v = np.where(rng.random(m) < 0.2, 1, v)                        # vertex 1 too
+    ts = rng.integers(1, t + 1, m)
+    colors = rng.integers(1, 4, n)
+    g = T.TemporalGraph.build(n, (u, v, ts), True)
+    assert g.info.split_chunks > 0
+    for motif in ([1, 1, 2, 3], [1, 2, 3, 1, 2]):
+        for seed in (1, 77):
+            assert _oracle_vs_gpu(n, u, v, ts, True, colors, motif, seed) >= 0
+    assert _oracle_vs_gpu(n, u, v, ts, False, colors, [1, 2, 3], 5) >= 0
+
+
+def test_c2_shape_small_scale_vs_oracle(cuda_device):
+    inst = synth.make_config(2, scale=0.01)   # n=1e3, m=1e4, k=6 PathMotif
+    k, col, motif, anchor = synth.effective_query(inst)
+    nf = _oracle_vs_gpu(inst.n, inst.u, inst.v, inst.ts, True, col, motif, 1)
+    assert nf > 0  # the planted path is found
+
+
+def test_sd_anchor_vs_oracle(cuda_device):
+    inst = synth.make_config(4, scale=0.0001)  # n=100, m=1e4, k_eff=12
+    k, col, motif, anchor = synth.effective_query(inst)
+    nf = _oracle_vs_gpu(inst.n, inst.u, inst.v, inst.ts, True, col, motif, 3, anchor)
+    assert nf == 1  # only the sink is kept
+
+
+def test_memory_cap_raises(cuda_device):
+    # test_sieve.cpp:364-371: cap -> std::runtime_error
+    rng = np.random.default_rng(5)
+    g = T.TemporalGraph.build(60, (rng.integers(0, 60, 240), rng.integers(0, 60, 240),
+                                   rng.integers(1, 13, 240)), False)
+    col = T.VertexColoring(rng.integers(1, 4, 60), 3)
+    cfg = T.SieveConfig(memory_cap_words=100)
+    sh = T.build_shades(T.MotifQuery.from_multiset([1, 2, 3]), col, cfg)
+    with pytest.raises(MemoryError, match="memory cap exceeded"):
+        T.eval_temporal_sieve(g, 3, g.t(), sh, cfg)
+
+
+def test_argument_errors(cuda_device):
+    g = T.TemporalGraph.build(3, [(0, 1, 1), (1, 2, 2)], True)
+    col = T.VertexColoring([1, 2, 3], 3)
+    sh = T.build_shades(T.MotifQuery.from_multiset([1, 2, 3]), col, T.SieveConfig())
+    with pytest.raises(ValueError, match="max_ts outside"):
+        T.eval_temporal_sieve(g, 3, 5, sh, T.SieveConfig())
+    with pytest.raises(ValueError, match="field_bits"):
+        T.eval_temporal_sieve(g, 3, 2, sh, T.SieveConfig(field_bits=12))
+    with pytest.raises(ValueError, match="GF\\(2\\^64\\) only"):
+        T.eval_temporal_sieve(g, 3, 2, sh, T.SieveConfig(field_bits=8))
+    with pytest.raises(ValueError, match="endpoint out of range"):
+        T.TemporalGraph.build(3, [(0, 4, 1)], True)
+
+
+def test_device_points_api_shards_xor_to_full(cuda_device, golden):
+    """tsv_eval_points_device over disjoint point ranges + tsv_xor_combine_device
+    reproduces the full evaluation (the multi-GPU sieve-point sharding path)."""
+    import torch
+    c = next(c for c in golden["sieve"] if c["name"] == "C1 k-TempPath k=5")
+    g = T.TemporalGraph.build(c["n"], (c["u"], c["v"], c["ts"]), True)
+    cfg = T.SieveConfig(seed=1)
+    sh = T.build_shades(T.MotifQuery.from_multiset(c["motif"]),
+                        T.VertexColoring(c["colors"], 1), cfg)
+    ds = T.DeviceShades(g, 5, sh)
+    parts = torch.zeros((4, g.n()), dtype=torch.int64, device="cuda")
+    bounds = [0, 5, 16, 17, 32]
+    stream = torch.cuda.current_stream().cuda_stream
+    for i in range(4):
+        T.eval_points_device(g, ds, 5, g.t(), cfg, -1, bounds[i], bounds[i + 1],
+                             parts[i].data_ptr(), stream)
+    total = torch.zeros(g.n(), dtype=torch.int64, device="cuda")
+    T.xor_combine_device(parts.data_ptr(), 4, g.n(), total.data_ptr(), stream)
+    acc = total.cpu().numpy().view(np.uint64)
+    acc, nflag, cs = T.finalize(acc)
+    assert f"{cs:016x}" == c["checksum"]
+    assert [f"{int(x):016x}" for x in acc] == c["acc"]
