@@ -44,6 +44,9 @@ struct LevelParams {
   const uint64_t* s_prev = nullptr;  // R x W (level ell-1), unused at ell=2
   uint64_t* s_cur = nullptr;         // R x W (level ell)
   uint64_t* agg = nullptr;           // C x W chunk tail aggregates
+  // y-multiply path for W >= 32: 0 = smem tables (default), 1 = holes in the
+  // wide kernel, 2 = grouped kernel.  Set from TSV_YMUL for measurements.
+  int ymul = 0;
 };
 
 // Kernel launchers (kernels.cu).  All are asynchronous on `st`.
@@ -60,8 +63,8 @@ void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n,
                         uint64_t* out, cudaStream_t st);
 void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
                    uint64_t* out, cudaStream_t st);
-void launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks,
-                     int threads, cudaStream_t st);
+double launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks,
+                       int threads, cudaStream_t st);
 void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,
                    uint64_t* out, cudaStream_t st);
 

@@ -1,0 +1,126 @@
+// gf_bench.cu -- GF(2^64) multiply variants: self-test and throughput
+// microbenchmarks (tsv_gf_mul_device / tsv_gf_bench).  The level kernels use
+// the variants these numbers select ("GF(2^64) multiply").
+//
+// variant 0  production general multiply (gf_mul)
+//         1  bit-serial reference
+//         2  holes + Karatsuba
+//         3  holes + schoolbook
+//         4  warp-uniform multiplier, smem tables, 1 product per lane per y
+//         5  ... 2 products per lane per y
+//         6  ... 4 products per lane per y
+#include <cuda_runtime.h>
+
+#include "engine.hpp"
+#include "gf_device.cuh"
+
+namespace tsv {
+namespace {
+
+template <int V>
+__device__ __forceinline__ uint64_t mul_v(uint64_t a, uint64_t b) {
+  if (V == 1) return gf_mul_serial(a, b);
+  if (V == 2) return gf_mul_kara(a, b);
+  if (V == 3) return gf_mul_school(a, b);
+  return gf_mul(a, b);
+}
+
+__global__ void k_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
+                         uint64_t* out) {
+  __shared__ uint64_t tabs[8][256];
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (variant >= 4) {
+    // products by a warp-uniform multiplier: every lane multiplies a[i] by
+    // each of the warp's 32 b values in turn and keeps the one of its own
+    // index, so all 32 tables are exercised.
+    const int64_t base = i - lane;
+    GfTable T{tabs[w]};
+    uint64_t mine = 0;
+    for (int j = 0; j < 32; ++j) {
+      const int64_t src = base + j < n ? base + j : n - 1;
+      const uint64_t y = b[src];
+      __syncwarp();
+      T.build(y, lane);
+      __syncwarp();
+      const uint64_t r = T.mul(i < n ? a[i] : 0);
+      if (j == lane) mine = r;
+    }
+    if (i < n) out[i] = mine;
+    return;
+  }
+  if (i >= n) return;
+  switch (variant) {
+    case 1: out[i] = mul_v<1>(a[i], b[i]); break;
+    case 2: out[i] = mul_v<2>(a[i], b[i]); break;
+    case 3: out[i] = mul_v<3>(a[i], b[i]); break;
+    default: out[i] = mul_v<0>(a[i], b[i]); break;
+  }
+}
+
+template <int V>
+__global__ void k_gf_bench(int64_t iters, uint64_t* sink) {
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t a0 = mix64(tid + 1), a1 = mix64(tid + 2), a2 = mix64(tid + 3), a3 = mix64(tid + 4);
+  const uint64_t b = mix64(tid ^ 0x5555);
+  for (int64_t it = 0; it < iters; ++it) {
+    a0 = mul_v<V>(a0, b) ^ static_cast<uint64_t>(it);
+    a1 = mul_v<V>(a1, b) ^ static_cast<uint64_t>(it);
+    a2 = mul_v<V>(a2, b) ^ static_cast<uint64_t>(it);
+    a3 = mul_v<V>(a3, b) ^ static_cast<uint64_t>(it);
+  }
+  sink[tid] = a0 ^ a1 ^ a2 ^ a3;
+}
+
+// Table products: per iteration the warp builds the table of a fresh y and
+// each lane multiplies PPT values by it.
+template <int PPT>
+__global__ void k_gf_bench_table(int64_t iters, uint64_t* sink) {
+  __shared__ uint64_t tabs[8][256];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  uint64_t a[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) a[p] = mix64(tid * 8 + p);
+  uint64_t y = mix64(blockIdx.x * 64 + w);
+  GfTable T{tabs[w]};
+  for (int64_t it = 0; it < iters; ++it) {
+    __syncwarp();
+    T.build(y, lane);
+    __syncwarp();
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) a[p] = T.mul(a[p]) ^ static_cast<uint64_t>(it);
+    y = y * 0x9e3779b97f4a7c15ull + 1;
+  }
+  uint64_t x = 0;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) x ^= a[p];
+  sink[tid] = x;
+}
+
+}  // namespace
+
+void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
+                   uint64_t* out, cudaStream_t st) {
+  if (n == 0) return;
+  const int threads = 256;
+  const int64_t blocks = (n + threads - 1) / threads;
+  k_gf_mul<<<static_cast<unsigned>(blocks), threads, 0, st>>>(variant, n, a, b, out);
+}
+
+// Returns products per launch for the given shape.
+double launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks, int threads,
+                       cudaStream_t st) {
+  const double lanes = static_cast<double>(blocks) * threads;
+  switch (variant) {
+    case 1: k_gf_bench<1><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
+    case 2: k_gf_bench<2><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
+    case 3: k_gf_bench<3><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
+    case 4: k_gf_bench_table<1><<<blocks, threads, 0, st>>>(iters, sink); return 1.0 * iters * lanes;
+    case 5: k_gf_bench_table<2><<<blocks, threads, 0, st>>>(iters, sink); return 2.0 * iters * lanes;
+    case 6: k_gf_bench_table<4><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
+    default: k_gf_bench<0><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
+  }
+}
+
+}  // namespace tsv

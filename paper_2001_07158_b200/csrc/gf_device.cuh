@@ -2,19 +2,23 @@
 //
 // Field: GF(2)[x] / (x^64 + x^4 + x^3 + x + 1), the reference's b = 64 field
 // (/root/reference/proj/core/include/tsieve/gf.hpp:37-42).  Addition is XOR.
-// Blackwell has no carry-less multiply instruction, so the 64x64 -> 128
-// carry-less product is emulated on the integer pipes.  Every variant below
-// returns the same field element as gf::mul<uint64_t> (gf.hpp:85-106); the
-// engine picks one by measurement (tsv_bench_gf / DESIGN.md).
+// Blackwell has no carry-less multiply instruction, so products are emulated
+// on the integer pipes.  Every routine returns the same field element as
+// gf::mul<uint64_t> (gf.hpp:85-106); the engine picks by measurement
+// (tsv_gf_bench, DESIGN.md section "GF(2^64) multiply"):
 //
-//  * clmul32_holes: 32x32 -> 64 via integer multiplies of operands masked to
-//    every 4th bit ("holes"): each IMAD.WIDE sums at most 8 one-bit products
-//    per output position, which fits in the 3 spare bits above it, so the
-//    parity bit of each position is the carry-less result.  16 IMAD.WIDE on
-//    the FMA pipe + LOP3 masking on the ALU pipe.
-//  * clmul64 = one Karatsuba level over clmul32 (3 products, not 4).
-//  * gf_reduce folds the high word: h*x^64 == h*(x^4+x^3+x+1), twice.
-//  * gf_mul_serial: bit-serial reference, used only by the self-test kernel.
+//  * gf_mul_kara  -- general product.  32x32 -> 64 carry-less products come
+//    from integer multiplies of operands masked to every 4th bit ("holes"):
+//    each mul.wide sums at most 8 one-bit products per output position, which
+//    fits below the next position of the same residue class, so bit p of the
+//    integer product is the carry-less bit p for its class.  Classes are XORed
+//    unmasked through one Karatsuba level and masked once at the end.
+//  * gf_mul_school -- same, schoolbook (4 sub-products, no operand sums).
+//  * GfTable -- product by a WARP-UNIFORM multiplier y: 16 tables of the 16
+//    multiples c * x^(4i) * y (fully reduced, 2 KB in shared memory, built
+//    cooperatively by the warp), then 16 nibble lookups per product.  Each
+//    table spans the 32 banks exactly once, so lookups are conflict-free.
+//  * gf_mul_serial -- bit-serial reference for the self-test kernel.
 #pragma once
 #include <cstdint>
 
@@ -24,61 +28,156 @@ struct u128 {
   uint64_t lo, hi;
 };
 
-__device__ __forceinline__ uint64_t clmul32_holes(uint32_t a, uint32_t b) {
-  const uint32_t m0 = 0x11111111u, m1 = 0x22222222u, m2 = 0x44444444u,
-                 m3 = 0x88888888u;
-  const uint32_t a0 = a & m0, a1 = a & m1, a2 = a & m2, a3 = a & m3;
-  const uint32_t b0 = b & m0, b1 = b & m1, b2 = b & m2, b3 = b & m3;
-#define TSV_P(x, y) ((uint64_t)(x) * (uint64_t)(y))
-  // Output class r collects the products whose mask classes sum to r mod 4.
-  const uint64_t c0 = TSV_P(a0, b0) ^ TSV_P(a1, b3) ^ TSV_P(a2, b2) ^ TSV_P(a3, b1);
-  const uint64_t c1 = TSV_P(a0, b1) ^ TSV_P(a1, b0) ^ TSV_P(a2, b3) ^ TSV_P(a3, b2);
-  const uint64_t c2 = TSV_P(a0, b2) ^ TSV_P(a1, b1) ^ TSV_P(a2, b0) ^ TSV_P(a3, b3);
-  const uint64_t c3 = TSV_P(a0, b3) ^ TSV_P(a1, b2) ^ TSV_P(a2, b1) ^ TSV_P(a3, b0);
-#undef TSV_P
+__device__ __forceinline__ uint64_t wmul(uint32_t a, uint32_t b) {
+  uint64_t r;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t lo32(uint64_t x) { return static_cast<uint32_t>(x); }
+__device__ __forceinline__ uint32_t hi32(uint64_t x) { return static_cast<uint32_t>(x >> 32); }
+__device__ __forceinline__ uint64_t pack(uint32_t lo, uint32_t hi) {
+  return (static_cast<uint64_t>(hi) << 32) | lo;
+}
+
+struct Split4 {
+  uint32_t c[4];
+};
+
+__device__ __forceinline__ Split4 split4(uint32_t a) {
+  Split4 s;
+  s.c[0] = a & 0x11111111u;
+  s.c[1] = a & 0x22222222u;
+  s.c[2] = a & 0x44444444u;
+  s.c[3] = a & 0x88888888u;
+  return s;
+}
+
+// Class-r raw product (unmasked): XOR over i of a_i * b_{(r-i) mod 4}.
+template <int R>
+__device__ __forceinline__ uint64_t class_prod(const Split4& a, const Split4& b) {
+  return wmul(a.c[0], b.c[R & 3]) ^ wmul(a.c[1], b.c[(R + 3) & 3]) ^
+         wmul(a.c[2], b.c[(R + 2) & 3]) ^ wmul(a.c[3], b.c[(R + 1) & 3]);
+}
+
+__device__ __forceinline__ uint64_t mask_class(uint64_t c0, uint64_t c1, uint64_t c2,
+                                               uint64_t c3) {
   return (c0 & 0x1111111111111111ull) | (c1 & 0x2222222222222222ull) |
          (c2 & 0x4444444444444444ull) | (c3 & 0x8888888888888888ull);
 }
 
-// 64x64 -> 128 carry-less product, one Karatsuba level.
-__device__ __forceinline__ u128 clmul64(uint64_t a, uint64_t b) {
-  const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32);
-  const uint32_t bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
-  const uint64_t L = clmul32_holes(al, bl);
-  const uint64_t H = clmul32_holes(ah, bh);
-  const uint64_t M = clmul32_holes(al ^ ah, bl ^ bh) ^ L ^ H;
-  u128 r;
-  r.lo = L ^ (M << 32);
-  r.hi = H ^ (M >> 32);
-  return r;
+// Karatsuba over 32-bit halves with deferred class masking.
+__device__ __forceinline__ u128 clmul64_kara(uint64_t a, uint64_t b) {
+  const Split4 al = split4(lo32(a)), ah = split4(hi32(a)), am = split4(lo32(a) ^ hi32(a));
+  const Split4 bl = split4(lo32(b)), bh = split4(hi32(b)), bm = split4(lo32(b) ^ hi32(b));
+  uint64_t lo[4], hi[4];
+#define TSV_KCLASS(R)                                          \
+  {                                                            \
+    const uint64_t L = class_prod<R>(al, bl);                  \
+    const uint64_t H = class_prod<R>(ah, bh);                  \
+    const uint64_t M = class_prod<R>(am, bm) ^ L ^ H;          \
+    lo[R] = L ^ (M << 32);                                     \
+    hi[R] = H ^ (M >> 32);                                     \
+  }
+  TSV_KCLASS(0) TSV_KCLASS(1) TSV_KCLASS(2) TSV_KCLASS(3)
+#undef TSV_KCLASS
+  return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
 }
 
-// Reduce a 128-bit carry-less product modulo x^64 + x^4 + x^3 + x + 1.
+// Schoolbook over 32-bit halves with deferred class masking.
+__device__ __forceinline__ u128 clmul64_school(uint64_t a, uint64_t b) {
+  const Split4 al = split4(lo32(a)), ah = split4(hi32(a));
+  const Split4 bl = split4(lo32(b)), bh = split4(hi32(b));
+  uint64_t lo[4], hi[4];
+#define TSV_SCLASS(R)                                                  \
+  {                                                                    \
+    const uint64_t L = class_prod<R>(al, bl);                          \
+    const uint64_t H = class_prod<R>(ah, bh);                          \
+    const uint64_t M = class_prod<R>(al, bh) ^ class_prod<R>(ah, bl);  \
+    lo[R] = L ^ (M << 32);                                             \
+    hi[R] = H ^ (M >> 32);                                             \
+  }
+  TSV_SCLASS(0) TSV_SCLASS(1) TSV_SCLASS(2) TSV_SCLASS(3)
+#undef TSV_SCLASS
+  return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
+}
+
+// Reduce a 128-bit carry-less product modulo x^64 + x^4 + x^3 + x + 1:
+// h * x^64 == h * (x^4 + x^3 + x + 1), folded twice.
 __device__ __forceinline__ uint64_t gf_reduce(u128 p) {
   const uint64_t h = p.hi;
   const uint64_t over = (h >> 63) ^ (h >> 61) ^ (h >> 60);
-  return p.lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4) ^ over ^ (over << 1) ^
-         (over << 3) ^ (over << 4);
+  return p.lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4) ^ over ^ (over << 1) ^ (over << 3) ^
+         (over << 4);
 }
 
+__device__ __forceinline__ uint64_t gf_mul_kara(uint64_t a, uint64_t b) {
+  return gf_reduce(clmul64_kara(a, b));
+}
+__device__ __forceinline__ uint64_t gf_mul_school(uint64_t a, uint64_t b) {
+  return gf_reduce(clmul64_school(a, b));
+}
+
+// Production general multiply (selected by tsv_gf_bench measurements).
 __device__ __forceinline__ uint64_t gf_mul(uint64_t a, uint64_t b) {
-  return gf_reduce(clmul64(a, b));
+  return gf_mul_kara(a, b);
 }
 
-__device__ __forceinline__ u128 u128_xor(u128 a, u128 b) {
-  return {a.lo ^ b.lo, a.hi ^ b.hi};
+// a * x in the field.
+__device__ __forceinline__ uint64_t gf_mulx(uint64_t a) {
+  return (a << 1) ^ ((a >> 63) * 0x1bull);
+}
+
+// a * x^s, 0 <= s <= 60, in one fold (the overflow has <= 60 bits).
+__device__ __forceinline__ uint64_t gf_mul_xpow(uint64_t a, int s) {
+  if (s == 0) return a;
+  const uint64_t h = a >> (64 - s);
+  return (a << s) ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4);
 }
 
 // Bit-serial product (Horner over the bits of b); independent check path.
 __device__ __forceinline__ uint64_t gf_mul_serial(uint64_t a, uint64_t b) {
   uint64_t r = 0;
   for (int i = 63; i >= 0; --i) {
-    const uint64_t top = r >> 63;
-    r = (r << 1) ^ (top ? 0x1bull : 0ull);
+    r = gf_mulx(r);
     if ((b >> i) & 1) r ^= a;
   }
   return r;
 }
+
+// ---- products by a warp-uniform multiplier --------------------------------
+
+// tab: 256 u64 in shared memory, private to one warp.  build() must be called
+// by all 32 lanes of the warp with the same y; mul() by any lane afterwards.
+struct GfTable {
+  uint64_t* tab;
+
+  __device__ __forceinline__ void build(uint64_t y, int lane) {
+    const int i = lane >> 1;          // window: multiples of x^(4i) * y
+    const uint64_t Y = gf_mul_xpow(y, 4 * i);
+    const uint64_t B0 = Y, B1 = gf_mulx(B0), B2 = gf_mulx(B1), B3 = gf_mulx(B2);
+    const uint64_t base = (lane & 1) ? B3 : 0ull;  // c = 8*(lane&1) + e
+    uint64_t* row = tab + i * 16 + (lane & 1) * 8;
+    row[0] = base;
+    row[1] = base ^ B0;
+    row[2] = base ^ B1;
+    row[3] = base ^ B1 ^ B0;
+    row[4] = base ^ B2;
+    row[5] = base ^ B2 ^ B0;
+    row[6] = base ^ B2 ^ B1;
+    row[7] = base ^ B2 ^ B1 ^ B0;
+  }
+
+  __device__ __forceinline__ uint64_t mul(uint64_t s) const {
+    uint64_t acc = 0;
+    const uint32_t w0 = lo32(s), w1 = hi32(s);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc ^= tab[i * 16 + ((w0 >> (4 * i)) & 15u)];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc ^= tab[(i + 8) * 16 + ((w1 >> (4 * i)) & 15u)];
+    return acc;
+  }
+};
 
 // ---- counter PRNG: gf.hpp:111-153 (splitmix64 finalizer rounds) ----------
 
@@ -94,16 +193,13 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 enum : uint64_t { kRoleShadeV = 1, kRoleShadeW = 2, kRoleEdgeY = 3 };
 
 // First two rounds of draw64 depend only on (seed, role): hoisted per launch.
-__host__ __device__ __forceinline__ uint64_t draw_prefix(uint64_t seed,
-                                                         uint64_t role) {
+__host__ __device__ __forceinline__ uint64_t draw_prefix(uint64_t seed, uint64_t role) {
   uint64_t h = seed + 0x9e3779b97f4a7c15ull;
   return mix64(h ^ (role * 0xff51afd7ed558ccdull));
 }
 
-__host__ __device__ __forceinline__ uint64_t draw_nonzero_from(uint64_t pre,
-                                                               uint64_t a,
-                                                               uint64_t b,
-                                                               uint64_t c) {
+__host__ __device__ __forceinline__ uint64_t draw_nonzero_from(uint64_t pre, uint64_t a,
+                                                               uint64_t b, uint64_t c) {
   uint64_t h = mix64(pre ^ (a + 0xc2b2ae3d27d4eb4full));
   h = mix64(h ^ (b + 0x165667b19e3779f9ull));
   h = mix64(h ^ (c + 0x27d4eb2f165667c5ull));
@@ -111,19 +207,15 @@ __host__ __device__ __forceinline__ uint64_t draw_nonzero_from(uint64_t pre,
   return h;
 }
 
-__host__ __device__ __forceinline__ uint64_t draw_nonzero(uint64_t seed,
-                                                          uint64_t role,
-                                                          uint64_t a,
-                                                          uint64_t b,
-                                                          uint64_t c) {
+__host__ __device__ __forceinline__ uint64_t draw_nonzero(uint64_t seed, uint64_t role,
+                                                          uint64_t a, uint64_t b, uint64_t c) {
   return draw_nonzero_from(draw_prefix(seed, role), a, b, c);
 }
 
-// Round 3 of a y draw: the c = 0 round and the (seed, role) prefix are fixed
-// per (level, launch); only the edge id varies.  yb = b + const for level l-1.
-__device__ __forceinline__ uint64_t draw_edge_y(uint64_t pre, uint64_t yb,
-                                                uint32_t edge) {
-  uint64_t h = mix64(pre ^ ((uint64_t)edge + 0xc2b2ae3d27d4eb4full));
+// y(e, l-1) = draw_nonzero(seed, edge_y, e, l-1, 0) with the (seed, role)
+// prefix hoisted; yb = (l-1) + the round-3 constant.
+__device__ __forceinline__ uint64_t draw_edge_y(uint64_t pre, uint64_t yb, uint32_t edge) {
+  uint64_t h = mix64(pre ^ (static_cast<uint64_t>(edge) + 0xc2b2ae3d27d4eb4full));
   h = mix64(h ^ yb);
   h = mix64(h ^ 0x27d4eb2f165667c5ull);  // c = 0
   while (h == 0) h = mix64(h + 0x9e3779b97f4a7c15ull);

@@ -188,6 +188,139 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   }
 }
 
+// The value multiplied by y(e, l-1) for one arc: the predecessor state
+// S_{l-1}[src] (gather), or z_tail^A at level 2 (only from the anchor
+// source in the (s,d) variant, sieve.cpp:241-242).
+template <int PPT, bool FIRST>
+__device__ __forceinline__ void fetch_src(const LevelParams& P, int32_t src,
+                                          const uint32_t (&pt)[PPT], const bool (&pv)[PPT],
+                                          uint64_t (&out)[PPT]) {
+  const int lane = threadIdx.x & 31;
+  if (FIRST) {
+    if (src >= 0 && (P.anchor_source < 0 || src == P.anchor_source)) {
+      z_of<PPT>(P.zj, P.k, src, pt, pv, out);
+    } else {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) out[p] = 0;
+    }
+  } else {
+#pragma unroll
+    for (int p = 0; p < PPT; ++p)
+      out[p] = src >= 0 ? __ldg(P.s_prev + static_cast<int64_t>(src) * (32 * PPT) + lane + 32 * p)
+                        : 0ull;
+  }
+}
+
+// Wide variant (W = 32*PPT >= 32): one arc per step for the whole warp, so
+// y is warp-uniform and its product with the gathered states goes through
+// the shared-memory multiple tables (GfTable) when YTAB; z_head^A is cached
+// across the consecutive runs of one head.
+template <int PPT, bool FIRST, bool YTAB>
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, PPT >= 4 ? 2 : 3)
+    k_level_wide(const LevelParams P) {
+  constexpr int W = 32 * PPT;
+  __shared__ uint64_t s_y[kWarpsPerBlock][32];
+  __shared__ int32_t s_src[kWarpsPerBlock][32];
+  __shared__ uint32_t s_meta[kWarpsPerBlock][32];
+  __shared__ int32_t s_run[kWarpsPerBlock][32];
+  __shared__ int32_t s_head[kWarpsPerBlock][32];
+  __shared__ uint64_t s_tab[YTAB ? kWarpsPerBlock : 1][256];
+
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
+  if (c >= P.g.C) return;  // warp-uniform
+
+  uint32_t pt[PPT];
+  bool pv[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const uint64_t A = P.b.pb + lane + 32 * p;
+    pt[p] = static_cast<uint32_t>(A);
+    pv[p] = A < P.b.pe;
+  }
+  GfTable T{s_tab[YTAB ? wib : 0]};
+  const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
+  const uint64_t yb = static_cast<uint64_t>(P.ell - 1) + 0x165667b19e3779f9ull;
+  const int64_t a0 = P.g.chunk_arc[c], a1 = P.g.chunk_arc[c + 1];
+  int32_t run_ctr = P.g.chunk_run[c];
+  uint64_t U[PPT], z[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) U[p] = z[p] = 0;
+  int32_t zhead = -1;
+
+  for (int64_t base = a0; base < a1; base += 32) {
+    const int nb = static_cast<int>(a1 - base < 32 ? a1 - base : 32);
+    uint32_t meta = 0;
+    int32_t sidx = -1, head = -1;
+    uint64_t y = 0;
+    if (lane < nb) {
+      meta = __ldg(P.g.arc_meta + base + lane);
+      sidx = FIRST ? __ldg(P.g.arc_tail + base + lane) : __ldg(P.g.arc_src + base + lane);
+      y = draw_edge_y(pre, yb, meta & kEdgeMask);
+    }
+    const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
+    const int32_t myrun = run_ctr + __popc(ends & ((1u << lane) - 1u));
+    if (lane < nb) head = __ldg(P.g.run_head + myrun);
+    s_y[wib][lane] = y;
+    s_src[wib][lane] = sidx;
+    s_meta[wib][lane] = meta;
+    s_run[wib][lane] = myrun;
+    s_head[wib][lane] = head;
+    run_ctr += __popc(ends);
+    __syncwarp();
+
+    // One step per arc; the predecessor states of the next arc are in flight
+    // while this one is multiplied (a step is thousands of cycles, so one
+    // step of look-ahead covers the HBM latency).  The loop is deliberately
+    // not unrolled: the step body is large and must stay in the I-cache.
+    uint64_t nxt[PPT];
+    fetch_src<PPT, FIRST>(P, s_src[wib][0], pt, pv, nxt);
+#pragma unroll 1
+    for (int i = 0; i < nb; ++i) {
+      uint64_t val[PPT];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) val[p] = nxt[p];
+      if (i + 1 < nb) fetch_src<PPT, FIRST>(P, s_src[wib][i + 1], pt, pv, nxt);
+      {
+        const uint32_t mt = s_meta[wib][i];
+        const uint64_t yy = s_y[wib][i];
+        uint64_t prod[PPT];
+        if (YTAB) {
+          __syncwarp();
+          T.build(yy, lane);
+          __syncwarp();
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) prod[p] = T.mul(val[p]);
+        } else {
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) prod[p] = gf_mul(yy, val[p]);
+        }
+        if (mt & kVStart) {
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) U[p] = prod[p];
+        } else {
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) U[p] ^= prod[p];
+        }
+        if (mt & kRunEnd) {
+          const int32_t h = s_head[wib][i];
+          if (h != zhead) {
+            z_of<PPT>(P.zj, P.k, h, pt, pv, z);
+            zhead = h;
+          }
+          const int64_t run = s_run[wib][i];
+#pragma unroll
+          for (int p = 0; p < PPT; ++p)
+            P.s_cur[run * W + lane + 32 * p] = gf_mul(z[p], U[p]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) P.agg[c * W + lane + 32 * p] = U[p];
+}
+
 // Chunks that continue a long vertex receive the XOR of the preceding
 // pieces' tail aggregates, multiplied by z_head, on every run they end.
 __global__ void k_fixup(const LevelParams P) {
@@ -269,31 +402,6 @@ __global__ void k_xor_combine(const uint64_t* __restrict__ parts, int nparts,
   }
 }
 
-__device__ __forceinline__ uint64_t mul_variant(int variant, uint64_t a, uint64_t b) {
-  return variant == 1 ? gf_mul_serial(a, b) : gf_mul(a, b);
-}
-
-__global__ void k_gf_mul(int variant, int64_t n, const uint64_t* a,
-                         const uint64_t* b, uint64_t* out) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = mul_variant(variant, a[i], b[i]);
-}
-
-template <int VARIANT>
-__global__ void k_gf_bench(int64_t iters, uint64_t* sink) {
-  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  uint64_t a0 = mix64(tid + 1), a1 = mix64(tid + 2), a2 = mix64(tid + 3),
-           a3 = mix64(tid + 4);
-  const uint64_t b = mix64(tid ^ 0x5555);
-  for (int64_t it = 0; it < iters; ++it) {
-    a0 = mul_variant(VARIANT, a0, b) ^ static_cast<uint64_t>(it);
-    a1 = mul_variant(VARIANT, a1, b) ^ static_cast<uint64_t>(it);
-    a2 = mul_variant(VARIANT, a2, b) ^ static_cast<uint64_t>(it);
-    a3 = mul_variant(VARIANT, a3, b) ^ static_cast<uint64_t>(it);
-  }
-  sink[tid] = a0 ^ a1 ^ a2 ^ a3;
-}
-
 __global__ void k_draw_y(uint64_t seed, int32_t level, int64_t n,
                          const int32_t* edges, uint64_t* out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -307,6 +415,16 @@ template <int LANES, int PPT>
 void level_dispatch(const LevelParams& p, cudaStream_t st) {
   const dim3 grid(static_cast<unsigned>((p.g.C + kWarpsPerBlock - 1) / kWarpsPerBlock));
   const dim3 block(kWarpsPerBlock * 32);
+  if (LANES == 32 && p.ymul != 2) {
+    if (p.ymul == 1) {
+      if (p.ell == 2) k_level_wide<PPT, true, false><<<grid, block, 0, st>>>(p);
+      else k_level_wide<PPT, false, false><<<grid, block, 0, st>>>(p);
+    } else {
+      if (p.ell == 2) k_level_wide<PPT, true, true><<<grid, block, 0, st>>>(p);
+      else k_level_wide<PPT, false, true><<<grid, block, 0, st>>>(p);
+    }
+    return;
+  }
   if (p.ell == 2)
     k_level<LANES, PPT, true><<<grid, block, 0, st>>>(p);
   else
@@ -376,20 +494,6 @@ void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n, uint64_t* 
   const unsigned blocks = blocks_for(n, 256) < 148 * 8 ? blocks_for(n, 256) : 148 * 8;
   k_xor_combine<<<blocks, 256, 0, st>>>(parts, nparts, n, out);
   prof_end(st);
-}
-
-void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
-                   uint64_t* out, cudaStream_t st) {
-  if (n == 0) return;
-  k_gf_mul<<<blocks_for(n, 256), 256, 0, st>>>(variant, n, a, b, out);
-}
-
-void launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks, int threads,
-                     cudaStream_t st) {
-  if (variant == 1)
-    k_gf_bench<1><<<blocks, threads, 0, st>>>(iters, sink);
-  else
-    k_gf_bench<0><<<blocks, threads, 0, st>>>(iters, sink);
 }
 
 void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -279,6 +280,8 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   lp.seed = cfg->seed;
   lp.anchor_source = anchor_source;
   lp.agg = agg.as<uint64_t>();
+  if (const char* e = std::getenv("TSV_YMUL"))
+    lp.ymul = std::strcmp(e, "holes") == 0 ? 1 : std::strcmp(e, "grouped") == 0 ? 2 : 0;
   for (uint64_t pb = p_begin; pb < p_end; pb += W) {
     lp.b = batch_shape(W);
     lp.b.pb = pb;
@@ -596,14 +599,15 @@ int tsv_gf_bench(int variant, int64_t iters, double* products_per_s) {
     TSV_CUDA(cudaEventCreate(&a));
     TSV_CUDA(cudaEventCreate(&b));
     TSV_CUDA(cudaEventRecord(a));
-    tsv::launch_gf_bench(variant, iters, sink.as<uint64_t>(), blocks, threads, nullptr);
+    const double products =
+        tsv::launch_gf_bench(variant, iters, sink.as<uint64_t>(), blocks, threads, nullptr);
     TSV_CUDA(cudaEventRecord(b));
     TSV_CUDA(cudaEventSynchronize(b));
     float ms = 0;
     TSV_CUDA(cudaEventElapsedTime(&ms, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    *products_per_s = 4.0 * iters * threads * blocks / (ms * 1e-3);
+    *products_per_s = products / (ms * 1e-3);
   });
 }
 
