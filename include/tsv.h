@@ -4,7 +4,7 @@
  * Plain pointers and sizes only.  This is the boundary the host side of the
  * reference would bind: the C++ drop-in (paper_2001_07158_b200/cpp, same API
  * as /root/reference/proj/core/include/tsieve/{graph,sieve}.hpp) and the
- * Python mirror (paper_2001_07158_b200/*.py, ctypes) both call it.  There is
+ * Python mirror (paper_2001_07158_b200 package, ctypes) both call it.  There is
  * no CPU fallback: every compute entry point runs CUDA kernels for sm_100a or
  * returns TSV_ERR_CUDA.
  *
@@ -57,6 +57,13 @@ typedef struct {
 int tsv_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                     const int32_t* ts, int directed, int32_t t, int device,
                     tsv_graph** out);
+
+/* Same, for an edge list that is ALREADY canonical (what a host-side
+ * TemporalGraph holds): validated in O(m) instead of re-sorted. */
+int tsv_graph_build_canonical(int32_t n, int64_t m, const int32_t* u,
+                              const int32_t* v, const int32_t* ts,
+                              int directed, int32_t t, int device,
+                              tsv_graph** out);
 
 /* Host-only canonicalization (no device): the edge list TemporalGraph::build
  * keeps, in edge-id order.  Returns the kept count (<= m) or -1 on error. */

@@ -1,0 +1,92 @@
+// capi.cpp -- a C entry point into the C++ drop-in solver, so the Python
+// tests can drive solve() on raw arrays exactly as oracle/ref_shim.cpp drives
+// the reference's (same argument meaning, same compact JSON record).
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <sstream>
+#include <string>
+
+#include "tsieve/solver.hpp"
+
+using namespace tsieve;
+
+namespace {
+thread_local std::string g_err;
+}
+
+extern "C" {
+
+const char* tsieve_last_error() { return g_err.c_str(); }
+
+// problem: CLI name; mode 0 decide, 1 optimum, 2 extract, 3 extract+optimum;
+// extraction 0 localized, 1 self-reducible; preprocess 0 none, 1 colors,
+// 2 static, 3 both.  Returns the JSON length or -1 (see tsieve_last_error).
+int64_t tsieve_solve_json(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                          const int32_t* ts, int directed, int32_t t, const int32_t* colors,
+                          const char* problem, const int32_t* motif, int32_t motif_len,
+                          int32_t k, int32_t source, int32_t dest, uint64_t seed, int32_t mode,
+                          int32_t extraction, int32_t preprocess, char* buf, int64_t cap) {
+  try {
+    std::vector<TemporalEdge> edges(static_cast<size_t>(m));
+    for (int64_t i = 0; i < m; ++i) edges[i] = {u[i], v[i], ts[i], 1};
+    TemporalGraph g = TemporalGraph::build(n, std::move(edges), directed != 0, t);
+    std::vector<Color> c(static_cast<size_t>(n), 1);
+    Color q = 1;
+    for (int32_t i = 0; colors && i < n; ++i) q = std::max(q, c[i] = colors[i]);
+    VertexColoring col(std::move(c), q);
+    SolveRequest req;
+    auto p = problem_from_name(problem);
+    if (!p) throw std::invalid_argument("unknown problem");
+    req.problem = *p;
+    req.query = motif_len > 0 ? MotifQuery::from_multiset(std::vector<Color>(motif, motif + motif_len))
+                              : MotifQuery::size_only(k);
+    req.source = source;
+    req.dest = dest;
+    req.config.seed = seed;
+    static const PreprocessLevel lv[] = {PreprocessLevel::none, PreprocessLevel::color_filter,
+                                         PreprocessLevel::static_sieve, PreprocessLevel::both};
+    req.preprocess = lv[preprocess & 3];
+    req.extraction = extraction ? ExtractionStrategy::self_reducible : ExtractionStrategy::localized;
+    static const SolveMode md[] = {SolveMode::decide, SolveMode::optimum, SolveMode::extract,
+                                   SolveMode::extract_optimum};
+    const SolveReport r = solve(g, col, req, md[mode & 3]);
+    std::ostringstream os;
+    char cs[32];
+    std::snprintf(cs, sizeof cs, "%016llx", static_cast<unsigned long long>(r.checksum));
+    os << "{\"decision\":" << (r.decision ? "true" : "false")
+       << ",\"certain\":" << (r.certain ? "true" : "false") << ",\"optimum_ts\":" << r.optimum_ts
+       << ",\"oracle_calls\":" << r.oracle_calls << ",\"checksum\":\"" << cs
+       << "\",\"extraction_failed\":" << (r.extraction_failed ? "true" : "false")
+       << ",\"flagged\":[";
+    for (size_t i = 0; i < r.flagged.size(); ++i) os << (i ? "," : "") << r.flagged[i];
+    os << "],\"witness\":";
+    if (r.witness) {
+      os << "{\"vertices\":[";
+      for (size_t i = 0; i < r.witness->vertices.size(); ++i)
+        os << (i ? "," : "") << r.witness->vertices[i];
+      os << "],\"edges\":[";
+      for (size_t i = 0; i < r.witness->edges.size(); ++i) {
+        const TemporalEdge& e = r.witness->edges[i];
+        os << (i ? "," : "") << "[" << e.u << "," << e.v << "," << e.ts << "]";
+      }
+      os << "]}";
+    } else {
+      os << "null";
+    }
+    os << ",\"preprocessed_n\":" << r.preprocessed_n << ",\"preprocessed_m\":" << r.preprocessed_m
+       << "}";
+    const std::string s = os.str();
+    if (buf && cap > 0) {
+      const size_t w = std::min<size_t>(static_cast<size_t>(cap - 1), s.size());
+      std::memcpy(buf, s.data(), w);
+      buf[w] = 0;
+    }
+    return static_cast<int64_t>(s.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,131 @@
+// sieve.cpp -- shade assignment (host) and the GPU-backed temporal sieve.
+// build_shades follows /root/reference/proj/core/src/sieve.cpp:658-718;
+// eval_temporal_sieve replaces sieve.cpp:720-732 by the C-ABI call.
+#include "tsieve/sieve.hpp"
+
+#include <algorithm>
+#include <bit>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+#include "tsv.h"
+
+namespace tsieve {
+
+namespace {
+
+void check_config(const SieveConfig& cfg) {
+  if (cfg.field_bits != 8 && cfg.field_bits != 16 && cfg.field_bits != 32 &&
+      cfg.field_bits != 64)
+    throw std::invalid_argument("field_bits must be 8, 16, 32 or 64");
+  if (cfg.lane_width < 1 || cfg.lane_width > 256 ||
+      !std::has_single_bit(static_cast<unsigned>(cfg.lane_width)))
+    throw std::invalid_argument("lane_width must be a power of two in [1,256]");
+  if (cfg.threads < 1) throw std::invalid_argument("threads must be >= 1");
+}
+
+}  // namespace
+
+double false_negative_bound(int k, int field_bits) {
+  return (2.0 * k - 1.0) / std::pow(2.0, field_bits);
+}
+
+ShadeAssignment build_shades(const MotifQuery& query, const VertexColoring& coloring,
+                             const SieveConfig& config) {
+  check_config(config);
+  if (query.multiset.empty()) throw std::invalid_argument("build_shades needs a color multiset");
+  int total = 0;
+  for (const auto& kv : query.multiset) total += kv.second;
+  if (total != query.k) throw std::invalid_argument("multiset multiplicities do not sum to k");
+
+  ShadeAssignment sh;
+  sh.k = query.k;
+  sh.seed = config.seed;
+  const int n = coloring.n();
+  std::vector<std::int64_t> count(static_cast<size_t>(coloring.q()) + 2, 0);
+  for (Vertex x = 0; x < n; ++x) ++count[coloring.primary(x)];
+  if (coloring.wildcard_active()) count[coloring.wildcard_color()] = n;
+
+  int next = 1;
+  for (const auto& [c, mu] : query.multiset) {
+    sh.colors.push_back(c);
+    std::vector<int> set(static_cast<size_t>(mu));
+    for (int& d : set) d = next++;
+    sh.shade_sets.push_back(std::move(set));
+    const bool present = c >= 1 && c < static_cast<Color>(count.size()) && count[c] > 0;
+    if (!present && sh.feasible) {
+      sh.feasible = false;
+      sh.missing_color = c;
+    }
+  }
+  auto set_of = [&](Color c) -> const std::vector<int>* {
+    auto it = std::lower_bound(sh.colors.begin(), sh.colors.end(), c);
+    return (it == sh.colors.end() || *it != c) ? nullptr : &sh.shade_sets[it - sh.colors.begin()];
+  };
+  sh.vertex_off.assign(static_cast<size_t>(n) + 1, 0);
+  for (Vertex x = 0; x < n; ++x) {
+    int cnt = 0;
+    if (auto* s = set_of(coloring.primary(x))) cnt += static_cast<int>(s->size());
+    if (coloring.wildcard_active())
+      if (auto* s = set_of(coloring.wildcard_color())) cnt += static_cast<int>(s->size());
+    sh.vertex_off[x + 1] = sh.vertex_off[x] + cnt;
+  }
+  sh.vertex_shades.resize(static_cast<size_t>(sh.vertex_off[n]));
+  for (Vertex x = 0; x < n; ++x) {
+    std::int32_t at = sh.vertex_off[x];
+    if (auto* s = set_of(coloring.primary(x)))
+      for (int d : *s) sh.vertex_shades[at++] = d;
+    if (coloring.wildcard_active())
+      if (auto* s = set_of(coloring.wildcard_color()))
+        for (int d : *s) sh.vertex_shades[at++] = d;
+  }
+  return sh;
+}
+
+SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts,
+                                 const ShadeAssignment& shades, const SieveConfig& config,
+                                 const AnchorSpec& anchor) {
+  check_config(config);
+  if (max_ts < 1 || max_ts > g.t()) throw std::invalid_argument("max_ts outside [1..t]");
+  if (static_cast<int>(shades.vertex_off.size()) != g.n() + 1)
+    throw std::invalid_argument("shade assignment built for a different graph");
+  if (config.edge_model != EdgeModel::instant)
+    throw std::invalid_argument("the B200 engine evaluates the instant edge model only");
+
+  tsv_config c{};
+  c.seed = config.seed;
+  c.field_bits = config.field_bits;
+  c.lane_width = config.lane_width;
+  c.edge_model = 0;
+  c.points_per_batch = 0;
+  c.memory_cap_words = config.memory_cap_words;
+
+  SieveOutcome out;
+  out.accumulators.assign(static_cast<size_t>(g.n()), 0);
+  std::uint64_t scratch = 0;
+  tsv_outcome o{};
+  static const std::int32_t kNoShade = 0;
+  const int rc = tsv_eval_temporal_sieve(
+      g.device_graph(config.device), k, max_ts, shades.vertex_off.data(),
+      shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c,
+      anchor.source, anchor.sink, g.n() ? out.accumulators.data() : &scratch, &o);
+  if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
+  if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
+
+  for (Vertex x = 0; x < g.n(); ++x)
+    if (out.accumulators[x]) out.flagged.push_back(x);
+  if (config.localize) {
+    out.global_nonzero = !out.flagged.empty();
+  } else {
+    std::uint64_t total = 0;
+    for (std::uint64_t a : out.accumulators) total ^= a;
+    out.global_nonzero = total != 0;
+  }
+  out.fn_bound = false_negative_bound(k, config.field_bits);
+  out.peak_field_words = o.peak_field_words;
+  out.checksum = o.checksum;
+  return out;
+}
+
+}  // namespace tsieve

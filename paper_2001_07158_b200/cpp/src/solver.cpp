@@ -1,0 +1,583 @@
+// solver.cpp -- problem drivers on top of the GPU temporal sieve.
+//
+// Semantics follow /root/reference/proj/core/src/solver.cpp: effective
+// instance (make_effective :42-126), preparation (prepare :499-546, color
+// filter of preprocess_mask :458-497), the decision / optimum / extraction
+// driver (solve_single :609-703: binary search :641-662, localized reverse
+// DFS :314-394, self-reduction shrink_to_core :557-607 + forward DFS
+// :398-452), and the rainbow / wildcard loops (:705-784).  Each probe is one
+// eval_temporal_sieve on the device.
+#include "tsieve/solver.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <deque>
+#include <functional>
+#include <map>
+#include <stdexcept>
+
+namespace tsieve {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+double since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+struct Prep {
+  Problem problem = Problem::path_motif;
+  SieveConfig cfg;
+  MotifQuery query;
+  VertexColoring coloring;
+  TemporalGraph graph;
+  AnchorSpec anchor;
+  ShadeAssignment shades;
+  int k = 0;
+  bool infeasible = false;
+  std::string why;
+  int kept = 0;
+  double pre_s = 0;
+  std::uint64_t peak = 0;
+};
+
+[[noreturn]] void unsupported(Problem p) {
+  throw std::invalid_argument(std::string(problem_name(p)) +
+                              " is not evaluated by the B200 temporal-sieve engine");
+}
+
+void make_effective(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req,
+                    Prep& p) {
+  p.problem = req.problem;
+  p.cfg = req.config;
+  p.anchor = {};
+  switch (req.problem) {
+    case Problem::k_temp_path:
+      if (req.query.kind != QueryKind::size_only)
+        throw std::invalid_argument("k-TempPath takes a size-only query");
+      p.query = MotifQuery::from_multiset(std::vector<Color>(static_cast<size_t>(
+                                              std::max(req.query.k, 0)), 1));
+      p.coloring = VertexColoring::uniform(g.n());
+      break;
+    case Problem::path_motif:
+    case Problem::colorful_path:
+      if (req.query.kind != QueryKind::multiset)
+        throw std::invalid_argument("expected a color-multiset query");
+      p.query = req.query;
+      p.coloring = col;
+      break;
+    case Problem::sd_colorful_path: {
+      if (req.query.kind != QueryKind::size_only)
+        throw std::invalid_argument("(s,d)-ColorfulPath takes --k (interior size)");
+      if (req.source < 0 || req.source >= g.n() || req.dest < 0 || req.dest >= g.n() ||
+          req.source == req.dest)
+        throw std::invalid_argument("invalid source/dest");
+      const int k = req.query.k;
+      std::vector<Color> c(static_cast<size_t>(g.n()));
+      for (Vertex x = 0; x < g.n(); ++x) {
+        const Color o = col.primary(x);
+        c[x] = (o >= 1 && o <= k) ? o : k + 3;  // sentinel for off-range colors
+      }
+      c[req.source] = k + 1;
+      c[req.dest] = k + 2;
+      p.coloring = VertexColoring(std::move(c), k + 3);
+      std::vector<Color> all;
+      for (Color x = 1; x <= k + 2; ++x) all.push_back(x);
+      p.query = MotifQuery::from_multiset(all);
+      p.anchor = {req.source, req.dest};
+      break;
+    }
+    case Problem::rainbow_path:
+      throw std::logic_error("rainbow handled by its own driver");
+    default:
+      unsupported(req.problem);
+  }
+  p.k = p.query.k;
+  if (p.k < 1) throw std::invalid_argument("k must be positive");
+}
+
+std::vector<bool> color_filter(const TemporalGraph& g, const Prep& p, PreprocessLevel level) {
+  std::vector<bool> keep(static_cast<size_t>(g.n()), true);
+  if (level == PreprocessLevel::color_filter || level == PreprocessLevel::both) {
+    for (Vertex x = 0; x < g.n(); ++x) {
+      bool hit = false;
+      for (const auto& kv : p.query.multiset)
+        if (p.coloring.has_color(x, kv.first)) {
+          hit = true;
+          break;
+        }
+      keep[x] = hit;
+    }
+  }
+  if ((level == PreprocessLevel::static_sieve || level == PreprocessLevel::both) &&
+      !p.query.multiset.empty())
+    throw std::invalid_argument(
+        "static-projection preprocessing (junction sieve) is not part of the B200 engine yet; "
+        "use --preprocess none or colors");
+  return keep;
+}
+
+Prep prepare(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req) {
+  Prep p;
+  make_effective(g, col, req, p);
+  const auto t0 = Clock::now();
+  if (p.k > g.n()) {
+    p.infeasible = true;
+    p.why = "k exceeds vertex count";
+    p.graph = g;
+    return p;
+  }
+  p.shades = build_shades(p.query, p.coloring, p.cfg);
+  if (!p.shades.feasible) {
+    p.infeasible = true;
+    p.why = "query color " + std::to_string(p.shades.missing_color) + " absent from the graph";
+    p.graph = g;
+    return p;
+  }
+  const std::vector<bool> keep = color_filter(g, p, req.preprocess);
+  p.graph = restrict_to(g, keep, g.t());
+  p.kept = static_cast<int>(std::count(keep.begin(), keep.end(), true));
+  if (p.kept < p.k) {
+    p.infeasible = true;
+    p.why = "fewer than k vertices remain after preprocessing";
+  }
+  p.pre_s = since(t0);
+  return p;
+}
+
+SieveOutcome probe(const Prep& p, const TemporalGraph& graph, Timestamp max_ts) {
+  return eval_temporal_sieve(graph, p.k, max_ts, p.shades, p.cfg, p.anchor);
+}
+
+// ---- witness extraction (host DFS over the incidence lists) ---------------
+
+struct Dfs {
+  const TemporalGraph& g;
+  const VertexColoring& col;
+  const MotifQuery& q;
+  AnchorSpec anchor;
+  Timestamp horizon;
+  std::map<Color, int> left;
+  std::vector<char> used;
+  std::vector<Vertex> chain;
+  std::vector<TemporalEdge> chain_edges;
+
+  Dfs(const TemporalGraph& g_, const VertexColoring& c_, const MotifQuery& q_, AnchorSpec a_,
+      Timestamp h_)
+      : g(g_), col(c_), q(q_), anchor(a_), horizon(h_), left(q_.multiset),
+        used(static_cast<size_t>(g_.n()), 0) {}
+
+  // Places v (consuming one unit of its color, or of the wildcard color) and
+  // runs fn; undoes the consumption unless fn succeeds.
+  template <typename Fn>
+  bool place(Vertex v, Fn&& fn) {
+    auto attempt = [&](Color c) {
+      auto it = left.find(c);
+      if (it == left.end() || it->second == 0) return false;
+      --it->second;
+      const bool ok = fn();
+      ++it->second;
+      return ok;
+    };
+    if (attempt(col.primary(v))) return true;
+    return col.wildcard_active() && attempt(col.wildcard_color());
+  }
+
+  bool allowed(Vertex v, int pos) const {
+    if (anchor.source >= 0 && ((v == anchor.source) != (pos == 1))) return false;
+    if (anchor.sink >= 0 && ((v == anchor.sink) != (pos == q.k))) return false;
+    return true;
+  }
+
+  bool step(Vertex v, const TemporalEdge& e, const std::function<bool()>& next) {
+    used[v] = 1;
+    chain.push_back(v);
+    chain_edges.push_back(e);
+    if (next()) return true;
+    chain_edges.pop_back();
+    chain.pop_back();
+    used[v] = 0;
+    return false;
+  }
+
+  // Reverse temporal DFS: fills position pos from the in-arcs of the current
+  // first vertex, descending timestamps, ascending neighbor within a stamp.
+  bool backward(int pos) {
+    if (pos == 0) return true;
+    const Vertex x = chain.back();
+    const Timestamp hi = chain_edges.empty() ? horizon : chain_edges.back().ts - 1;
+    auto arcs = g.in_arcs(x);
+    auto end = std::upper_bound(arcs.begin(), arcs.end(), hi,
+                                [](Timestamp t, const Incidence& a) { return t < a.ts; });
+    while (end != arcs.begin()) {
+      const Timestamp ts = std::prev(end)->ts;
+      auto beg = end;
+      while (beg != arcs.begin() && std::prev(beg)->ts == ts) --beg;
+      for (auto it = beg; it != end; ++it) {
+        const Vertex v = it->other;
+        if (used[v] || !allowed(v, pos)) continue;
+        const TemporalEdge& e = g.edge(it->edge);
+        if (place(v, [&] { return step(v, e, [&] { return backward(pos - 1); }); }))
+          return true;
+      }
+      end = beg;
+    }
+    return false;
+  }
+
+  // Forward temporal DFS: ascending timestamps, ascending neighbor.
+  bool forward(int pos) {
+    if (pos > q.k) return true;
+    const Vertex x = chain.back();
+    const Timestamp lo = chain_edges.empty() ? 1 : chain_edges.back().ts + 1;
+    auto arcs = g.out_arcs(x);
+    auto it = std::lower_bound(arcs.begin(), arcs.end(), lo,
+                               [](const Incidence& a, Timestamp t) { return a.ts < t; });
+    for (; it != arcs.end(); ++it) {
+      const Vertex v = it->other;
+      if (used[v] || it->ts > horizon || !allowed(v, pos)) continue;
+      const TemporalEdge& e = g.edge(it->edge);
+      if (place(v, [&] { return step(v, e, [&] { return forward(pos + 1); }); })) return true;
+    }
+    return false;
+  }
+};
+
+std::optional<TemporalPath> extract_backward(const Prep& p, Vertex end, Timestamp horizon) {
+  Dfs d(p.graph, p.coloring, p.query, p.anchor, horizon);
+  if (!d.allowed(end, p.query.k)) return std::nullopt;
+  const bool ok = d.place(end, [&] {
+    d.used[end] = 1;
+    d.chain.push_back(end);
+    if (d.backward(p.query.k - 1)) return true;
+    d.chain.pop_back();
+    d.used[end] = 0;
+    return false;
+  });
+  if (!ok) return std::nullopt;
+  TemporalPath path;
+  path.vertices.assign(d.chain.rbegin(), d.chain.rend());
+  path.edges.assign(d.chain_edges.rbegin(), d.chain_edges.rend());
+  return path;
+}
+
+std::optional<TemporalPath> extract_forward(const Prep& p, const TemporalGraph& core,
+                                            Vertex start, Timestamp horizon) {
+  Dfs d(core, p.coloring, p.query, p.anchor, horizon);
+  if (!d.allowed(start, 1)) return std::nullopt;
+  const bool ok = d.place(start, [&] {
+    d.used[start] = 1;
+    d.chain.push_back(start);
+    if (d.forward(2)) return true;
+    d.chain.pop_back();
+    d.used[start] = 0;
+    return false;
+  });
+  if (!ok) return std::nullopt;
+  TemporalPath path;
+  path.vertices = d.chain;
+  path.edges = d.chain_edges;
+  return path;
+}
+
+// Self-reduction, phase 1: shrink the vertex set with deletion probes on
+// restricted graphs (block halving, then a linear cleanup).
+std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
+                                 std::uint64_t& peak) {
+  std::vector<bool> keep(static_cast<size_t>(p.graph.n()), false);
+  for (const TemporalEdge& e : p.graph.edges()) keep[e.u] = keep[e.v] = true;
+  std::vector<Vertex> cand;
+  for (Vertex x = 0; x < p.graph.n(); ++x)
+    if (keep[x]) cand.push_back(x);
+
+  auto still_yes_without = [&](const std::vector<Vertex>& block) {
+    std::vector<bool> mask = keep;
+    for (Vertex x : block) mask[x] = false;
+    const TemporalGraph sub = restrict_to(p.graph, mask, horizon);
+    const SieveOutcome o = probe(p, sub, horizon);
+    ++calls;
+    peak = std::max(peak, o.peak_field_words);
+    return o.global_nonzero;
+  };
+
+  std::deque<std::vector<Vertex>> work{cand};
+  std::vector<Vertex> survivors;
+  while (!work.empty()) {
+    std::vector<Vertex> block = std::move(work.front());
+    work.pop_front();
+    if (block.empty()) continue;
+    if (still_yes_without(block)) {
+      for (Vertex x : block) keep[x] = false;
+    } else if (block.size() == 1) {
+      survivors.push_back(block[0]);
+    } else {
+      const size_t half = block.size() / 2;
+      work.emplace_back(block.begin(), block.begin() + half);
+      work.emplace_back(block.begin() + half, block.end());
+    }
+  }
+  for (Vertex x : survivors)
+    if (keep[x] && still_yes_without({x})) keep[x] = false;
+  return keep;
+}
+
+SolveReport solve_single(const TemporalGraph& g, const VertexColoring& col,
+                         const SolveRequest& req, SolveMode mode) {
+  SolveReport r;
+  const Prep p = prepare(g, col, req);
+  r.preprocessed_n = p.kept;
+  r.preprocessed_m = p.graph.m();
+  r.timings.preprocess_s = p.pre_s;
+  r.peak_field_words = p.peak;
+  if (p.infeasible) {
+    r.certain = true;
+    r.note = p.why;
+    return r;
+  }
+
+  const auto t0 = Clock::now();
+  const Timestamp full = p.graph.t();
+  const SieveOutcome whole = probe(p, p.graph, full);
+  r.oracle_calls = 1;
+  r.decision = whole.global_nonzero;
+  r.certain = r.decision;  // a nonzero accumulator certifies a match
+  r.flagged = whole.flagged;
+  r.checksum = whole.checksum;
+  r.peak_field_words = std::max(r.peak_field_words, whole.peak_field_words);
+  r.timings.sieve_s = since(t0);
+  if (!r.decision || mode == SolveMode::decide) {
+    r.fn_bound = whole.fn_bound * r.oracle_calls;
+    return r;
+  }
+
+  Timestamp horizon = full;
+  SieveOutcome at = whole;
+  if (mode == SolveMode::optimum || mode == SolveMode::extract_optimum) {
+    const auto ts0 = Clock::now();
+    Timestamp lo = 1, hi = full;
+    while (lo < hi) {
+      const Timestamp mid = lo + (hi - lo) / 2;
+      SieveOutcome o = probe(p, p.graph, mid);
+      ++r.oracle_calls;
+      r.peak_field_words = std::max(r.peak_field_words, o.peak_field_words);
+      if (o.global_nonzero) {
+        hi = mid;
+        at = std::move(o);
+      } else {
+        lo = mid + 1;
+      }
+    }
+    horizon = lo;
+    r.optimum_ts = horizon;
+    if (horizon == full) at = whole;
+    r.timings.sieve_s += since(ts0);
+  }
+
+  if (mode == SolveMode::extract || mode == SolveMode::extract_optimum) {
+    const auto te = Clock::now();
+    auto accept = [&](std::optional<TemporalPath> w) {
+      if (!w) return false;
+      if (!validate_path(p.graph, p.coloring, *w, p.query, EdgeModel::instant, p.anchor.source,
+                         p.anchor.sink))
+        return false;
+      r.witness = std::move(*w);
+      return true;
+    };
+    if (req.extraction == ExtractionStrategy::localized) {
+      for (Vertex u : at.flagged)
+        if (accept(extract_backward(p, u, horizon))) break;
+    } else {
+      int calls = 0;
+      const std::vector<bool> core = shrink_to_core(p, horizon, calls, r.peak_field_words);
+      r.oracle_calls += calls;
+      const TemporalGraph cg = restrict_to(p.graph, core, horizon);
+      for (Vertex u = 0; u < cg.n() && !r.witness; ++u)
+        if (core[u]) accept(extract_forward(p, cg, u, horizon));
+    }
+    r.extraction_failed = !r.witness;
+    r.timings.extract_s = since(te);
+  }
+  r.fn_bound = whole.fn_bound * r.oracle_calls;
+  return r;
+}
+
+void add_totals(SolveReport& into, const SolveReport& r) {
+  into.oracle_calls += r.oracle_calls;
+  into.fn_bound += r.fn_bound;
+  into.peak_field_words = std::max(into.peak_field_words, r.peak_field_words);
+  into.timings.preprocess_s += r.timings.preprocess_s;
+  into.timings.sieve_s += r.timings.sieve_s;
+  into.timings.extract_s += r.timings.extract_s;
+}
+
+// RainbowPath: ColorfulPath over the k-subsets of [1..q] in lexicographic order.
+SolveReport rainbow(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req,
+                    SolveMode mode) {
+  if (req.query.kind != QueryKind::size_only)
+    throw std::invalid_argument("RainbowPath takes --k");
+  const int k = req.query.k;
+  const Color q = col.q();
+  if (k >= q) throw std::invalid_argument("RainbowPath requires k < q");
+  SolveRequest sub = req;
+  sub.problem = Problem::colorful_path;
+  if (sub.preprocess == PreprocessLevel::none) sub.preprocess = PreprocessLevel::color_filter;
+  SolveReport total;
+  std::vector<Color> subset(static_cast<size_t>(k));
+  for (int i = 0; i < k; ++i) subset[i] = i + 1;
+  int tried = 0;
+  for (;;) {
+    ++tried;
+    sub.query = MotifQuery::from_multiset(subset);
+    SolveReport r = solve_single(g, col, sub, mode);
+    add_totals(total, r);
+    if (r.decision) {
+      r.oracle_calls = total.oracle_calls;
+      r.fn_bound = total.fn_bound;
+      r.peak_field_words = total.peak_field_words;
+      r.timings = total.timings;
+      r.note = "subset";
+      for (Color c : subset) r.note += " " + std::to_string(c);
+      r.note += " (" + std::to_string(tried) + " of C(q,k) tried)";
+      return r;
+    }
+    int i = k - 1;
+    while (i >= 0 && subset[i] == q - (k - 1 - i)) --i;
+    if (i < 0) break;
+    ++subset[i];
+    for (int j = i + 1; j < k; ++j) subset[j] = subset[j - 1] + 1;
+  }
+  total.note = "all " + std::to_string(tried) + " color subsets exhausted";
+  return total;
+}
+
+SolveReport wildcards(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req,
+                      SolveMode mode) {
+  if (req.query.kind != QueryKind::multiset)
+    throw std::invalid_argument("wildcards apply to color-multiset queries");
+  if (req.wildcard_max < req.query.k) throw std::invalid_argument("--wildcards-max below k");
+  const VertexColoring wc = col.with_wildcard();
+  SolveRequest sub = req;
+  sub.wildcard_max = 0;
+  SolveReport total;
+  for (int kk = req.query.k; kk <= req.wildcard_max; ++kk) {
+    SolveReport r = solve_single(g, wc, sub, mode);
+    total.oracle_calls += r.oracle_calls;
+    total.fn_bound += r.fn_bound;
+    if (r.decision) {
+      r.oracle_calls = total.oracle_calls;
+      r.fn_bound = total.fn_bound;
+      r.wildcards_used = kk - req.query.k;
+      return r;
+    }
+    ++sub.query.multiset[wc.wildcard_color()];
+    ++sub.query.k;
+  }
+  total.note = "no match up to k' = " + std::to_string(req.wildcard_max);
+  return total;
+}
+
+}  // namespace
+
+const char* problem_name(Problem p) {
+  switch (p) {
+    case Problem::k_temp_path: return "ktemppath";
+    case Problem::path_motif: return "pathmotif";
+    case Problem::colorful_path: return "colorfulpath";
+    case Problem::sd_colorful_path: return "sdcolorful";
+    case Problem::rainbow_path: return "rainbow";
+    case Problem::ec_temp_path: return "ectemppath";
+    case Problem::ec_path_motif: return "ecpathmotif";
+    case Problem::vc_path_motif: return "vcpathmotif";
+    case Problem::vc_colorful_path: return "vccolorfulpath";
+  }
+  return "?";
+}
+
+std::optional<Problem> problem_from_name(const std::string& name) {
+  for (int i = 0; i <= static_cast<int>(Problem::vc_colorful_path); ++i) {
+    const auto p = static_cast<Problem>(i);
+    if (name == problem_name(p)) return p;
+  }
+  return std::nullopt;
+}
+
+EffectiveInstance effective_instance(const TemporalGraph& g, const VertexColoring& coloring,
+                                     const SolveRequest& req) {
+  Prep p;
+  make_effective(g, coloring, req, p);
+  return {std::move(p.query), std::move(p.coloring), p.anchor, p.k};
+}
+
+SolveReport solve(const TemporalGraph& g, const VertexColoring& coloring,
+                  const SolveRequest& req, SolveMode mode) {
+  if (req.wildcard_max > 0) return wildcards(g, coloring, req, mode);
+  if (req.problem == Problem::rainbow_path) return rainbow(g, coloring, req, mode);
+  return solve_single(g, coloring, req, mode);
+}
+
+SolveReport decide(const TemporalGraph& g, const VertexColoring& coloring,
+                   const SolveRequest& req) {
+  return solve(g, coloring, req, SolveMode::decide);
+}
+
+SolveReport find_optimum_timestamp(const TemporalGraph& g, const VertexColoring& coloring,
+                                   const SolveRequest& req) {
+  return solve(g, coloring, req, SolveMode::optimum);
+}
+
+SolveReport extract_localized(const TemporalGraph& g, const VertexColoring& coloring,
+                              const SolveRequest& req, bool optimize) {
+  SolveRequest r = req;
+  r.extraction = ExtractionStrategy::localized;
+  return solve(g, coloring, r, optimize ? SolveMode::extract_optimum : SolveMode::extract);
+}
+
+SolveReport extract_self_reducible(const TemporalGraph& g, const VertexColoring& coloring,
+                                   const SolveRequest& req, bool optimize) {
+  SolveRequest r = req;
+  r.extraction = ExtractionStrategy::self_reducible;
+  return solve(g, coloring, r, optimize ? SolveMode::extract_optimum : SolveMode::extract);
+}
+
+SolveReport decide_sd_colorful(const TemporalGraph& g, const VertexColoring& coloring,
+                               Vertex source, Vertex dest, int k, const SieveConfig& config) {
+  SolveRequest req;
+  req.problem = Problem::sd_colorful_path;
+  req.query = MotifQuery::size_only(k);
+  req.source = source;
+  req.dest = dest;
+  req.config = config;
+  return decide(g, coloring, req);
+}
+
+SolveReport decide_rainbow(const TemporalGraph& g, const VertexColoring& coloring, int k,
+                           const SieveConfig& config) {
+  SolveRequest req;
+  req.problem = Problem::rainbow_path;
+  req.query = MotifQuery::size_only(k);
+  req.config = config;
+  return decide(g, coloring, req);
+}
+
+SolveReport solve_with_wildcards(const TemporalGraph& g, const VertexColoring& coloring,
+                                 const SolveRequest& req, int k_max) {
+  SolveRequest r = req;
+  r.wildcard_max = k_max;
+  return solve(g, coloring, r, SolveMode::decide);
+}
+
+PreprocessResult preprocess(const TemporalGraph& g, const VertexColoring& coloring,
+                            const SolveRequest& req, PreprocessLevel level) {
+  SolveRequest sub = req;
+  sub.preprocess = level;
+  Prep p;
+  make_effective(g, coloring, sub, p);
+  PreprocessResult out;
+  out.kept = color_filter(g, p, level);
+  out.graph = restrict_to(g, out.kept, g.t());
+  out.kept_count = static_cast<int>(std::count(out.kept.begin(), out.kept.end(), true));
+  return out;
+}
+
+}  // namespace tsieve

@@ -60,6 +60,36 @@ void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
   if (max_ts > L.t) throw std::invalid_argument("timestamp exceeds t");
 }
 
+void adopt_canonical(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                     const int32_t* ts, bool directed, int32_t t, HostLayout& L) {
+  if (n < 0 || m < 0) throw std::invalid_argument("negative size");
+  if (m >= static_cast<int64_t>(kEdgeMask))
+    throw std::invalid_argument("edge count exceeds the engine's 2^30 edge ids");
+  L.n = n;
+  L.directed = directed;
+  L.dropped_self_loops = L.dropped_duplicates = 0;
+  L.eu.assign(u, u + m);
+  L.ev.assign(v, v + m);
+  L.ets.assign(ts, ts + m);
+  int32_t max_ts = 0;
+  for (int64_t i = 0; i < m; ++i) {
+    if (u[i] < 0 || u[i] >= n || v[i] < 0 || v[i] >= n)
+      throw std::invalid_argument("edge endpoint out of range");
+    if (ts[i] < 1) throw std::invalid_argument("timestamp below 1");
+    if (u[i] == v[i] || (!directed && u[i] > v[i]))
+      throw std::invalid_argument("edge list is not canonical");
+    if (i > 0) {
+      const bool lt = ts[i - 1] != ts[i] ? ts[i - 1] < ts[i]
+                      : u[i - 1] != u[i] ? u[i - 1] < u[i]
+                                         : v[i - 1] < v[i];
+      if (!lt) throw std::invalid_argument("edge list is not canonical");
+    }
+    max_ts = std::max(max_ts, ts[i]);
+  }
+  L.t = t > 0 ? t : std::max<int32_t>(max_ts, 1);
+  if (max_ts > L.t) throw std::invalid_argument("timestamp exceeds t");
+}
+
 void build_layout(HostLayout& L, int64_t chunk_target, int sm_count) {
   const int32_t n = L.n;
   const int64_t m = static_cast<int64_t>(L.eu.size());

@@ -53,6 +53,12 @@ struct HostLayout {
 void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                   const int32_t* ts, bool directed, int32_t t, HostLayout& L);
 
+// Adopts an edge list that must already be canonical (strictly increasing
+// (ts,u,v), u != v, u < v when undirected); throws std::invalid_argument
+// otherwise.
+void adopt_canonical(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                     const int32_t* ts, bool directed, int32_t t, HostLayout& L);
+
 // Builds runs/arcs/chunks from L's canonical edges.  chunk_target = arcs per
 // chunk (0 = choose from the arc count and the SM count).
 void build_layout(HostLayout& L, int64_t chunk_target, int sm_count);

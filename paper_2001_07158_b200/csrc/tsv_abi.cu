@@ -330,9 +330,9 @@ extern "C" {
 const char* tsv_last_error(void) { return g_error.c_str(); }
 const char* tsv_version(void) { return "tsv-b200 0.1 (sm_100a)"; }
 
-int tsv_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
-                    const int32_t* ts, int directed, int32_t t, int device,
-                    tsv_graph** out) {
+static int graph_build_impl(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                            const int32_t* ts, int directed, int32_t t, int device,
+                            tsv_graph** out, bool canonical) {
   return guard([&] {
     if (!out) throw std::invalid_argument("null output handle");
     *out = nullptr;
@@ -341,7 +341,10 @@ int tsv_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
     auto* g = new tsv_graph();
     try {
       g->device = device;
-      tsv::canonicalize(n, m, u, v, ts, directed != 0, t, g->host);
+      if (canonical)
+        tsv::adopt_canonical(n, m, u, v, ts, directed != 0, t, g->host);
+      else
+        tsv::canonicalize(n, m, u, v, ts, directed != 0, t, g->host);
       DeviceGuard dg(device);
       cudaDeviceProp prop{};
       TSV_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -376,6 +379,18 @@ int tsv_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
     }
     *out = g;
   });
+}
+
+int tsv_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                    const int32_t* ts, int directed, int32_t t, int device,
+                    tsv_graph** out) {
+  return graph_build_impl(n, m, u, v, ts, directed, t, device, out, false);
+}
+
+int tsv_graph_build_canonical(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                              const int32_t* ts, int directed, int32_t t, int device,
+                              tsv_graph** out) {
+  return graph_build_impl(n, m, u, v, ts, directed, t, device, out, true);
 }
 
 int64_t tsv_canonical_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v,

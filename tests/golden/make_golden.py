@@ -152,6 +152,35 @@ def main():
                    "mode": 3, "result": r})
     out["solve_fig2"] = solves
 
+    # solver sweep: the four problems x decide / optimum / extract (both
+    # strategies) x preprocess none / colors on random small instances
+    sweep = []
+    srng = np.random.default_rng(777)
+    problems = ["ktemppath", "pathmotif", "colorfulpath", "sdcolorful"]
+    for i in range(64):
+        n, u, v, ts, d, colors, motif = synth.random_small(srng, n_max=14, m_max=60, t_max=6,
+                                                           k_max=5, q_max=3)
+        prob = problems[i % 4]
+        k, src, dst = 0, -1, -1
+        if prob == "ktemppath":
+            motif, k = [], int(srng.integers(2, 5))
+        elif prob == "colorfulpath":
+            motif = sorted(set(motif)) or [1]
+        elif prob == "sdcolorful":
+            motif, k = [], int(srng.integers(1, 3))
+            src, dst = (int(x) for x in srng.choice(n, 2, replace=False))
+        mode = [0, 1, 2, 3][(i // 4) % 4]
+        extraction = (i // 16) % 2
+        pre = (i // 32) % 2
+        seed = int(srng.integers(1, 1000))
+        r = O.ref_solve(n, u, v, ts, d, colors, prob, motif, k, source=src, dest=dst, seed=seed,
+                        mode=mode, extraction=extraction, preprocess=pre)
+        sweep.append({"n": n, "u": u.tolist(), "v": v.tolist(), "ts": ts.tolist(), "directed": d,
+                      "colors": colors.tolist(), "problem": prob, "motif": motif, "k": k,
+                      "source": src, "dest": dst, "seed": seed, "mode": mode,
+                      "extraction": extraction, "preprocess": pre, "result": r})
+    out["solve_sweep"] = sweep
+
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=0)
