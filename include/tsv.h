@@ -120,6 +120,18 @@ int tsv_eval_points_device(const tsv_graph* g, const tsv_shades* s, int k,
                            int32_t anchor_source, uint64_t p_begin,
                            uint64_t p_end, uint64_t* d_acc, void* stream);
 
+/* Static-projection engines over the projection's edge list (a[i], b[i]),
+ * i = static edge id (StaticProjection::project, graph.cpp:148-199):
+ * junction != 0 replaces eval_junction_sieve (sieve.cpp:376-473, the
+ * default `--preprocess both` pass), junction == 0 eval_static_sieve
+ * (sieve.cpp:311-369).  Synchronous; accumulators = n host words. */
+int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a,
+                               const int32_t* b, int directed, int junction,
+                               int k, const int32_t* vertex_off,
+                               const int32_t* vertex_shades,
+                               const tsv_config* cfg, int device,
+                               uint64_t* accumulators, tsv_outcome* out);
+
 /* d_out[i] = XOR_{p < nparts} d_parts[p*n + i] (multi-GPU combine). */
 int tsv_xor_combine_device(const uint64_t* d_parts, int nparts, int64_t n,
                            uint64_t* d_out, void* stream);

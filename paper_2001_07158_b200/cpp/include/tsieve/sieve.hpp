@@ -66,6 +66,13 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
                                  const ShadeAssignment& shades, const SieveConfig& config,
                                  const AnchorSpec& anchor = {});
 
+// Static-projection engines (sieve.hpp:90-102 of the reference), also on
+// the GPU: the junction sieve is the default preprocessing pass.
+SieveOutcome eval_static_sieve(const StaticProjection& gs, int k, const ShadeAssignment& shades,
+                               const SieveConfig& config);
+SieveOutcome eval_junction_sieve(const StaticProjection& gs, int k,
+                                 const ShadeAssignment& shades, const SieveConfig& config);
+
 double false_negative_bound(int k, int field_bits);
 
 }  // namespace tsieve

@@ -128,4 +128,60 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
   return out;
 }
 
+namespace {
+
+SieveOutcome eval_projection(const StaticProjection& gs, int k, const ShadeAssignment& shades,
+                             const SieveConfig& config, bool junction) {
+  check_config(config);
+  if (static_cast<int>(shades.vertex_off.size()) != gs.n() + 1)
+    throw std::invalid_argument("shade assignment built for a different graph");
+  std::vector<std::int32_t> a(static_cast<size_t>(gs.m()) + 1), b(a.size());
+  for (std::int64_t i = 0; i < gs.m(); ++i) {
+    a[i] = gs.edges()[i].first;
+    b[i] = gs.edges()[i].second;
+  }
+  tsv_config c{};
+  c.seed = config.seed;
+  c.field_bits = config.field_bits;
+  c.lane_width = config.lane_width;
+  c.memory_cap_words = config.memory_cap_words;
+  SieveOutcome out;
+  out.accumulators.assign(static_cast<size_t>(gs.n()), 0);
+  std::uint64_t scratch = 0;
+  static const std::int32_t kNoShade = 0;
+  tsv_outcome o{};
+  const int rc = tsv_eval_static_projection(
+      gs.n(), gs.m(), a.data(), b.data(), gs.directed() ? 1 : 0, junction ? 1 : 0, k,
+      shades.vertex_off.data(),
+      shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c, config.device,
+      gs.n() ? out.accumulators.data() : &scratch, &o);
+  if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
+  if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
+  for (Vertex x = 0; x < gs.n(); ++x)
+    if (out.accumulators[x]) out.flagged.push_back(x);
+  if (config.localize) {
+    out.global_nonzero = !out.flagged.empty();
+  } else {
+    std::uint64_t total = 0;
+    for (std::uint64_t v : out.accumulators) total ^= v;
+    out.global_nonzero = total != 0;
+  }
+  out.fn_bound = false_negative_bound(k, config.field_bits);
+  out.peak_field_words = o.peak_field_words;
+  out.checksum = o.checksum;
+  return out;
+}
+
+}  // namespace
+
+SieveOutcome eval_static_sieve(const StaticProjection& gs, int k, const ShadeAssignment& shades,
+                               const SieveConfig& config) {
+  return eval_projection(gs, k, shades, config, false);
+}
+
+SieveOutcome eval_junction_sieve(const StaticProjection& gs, int k,
+                                 const ShadeAssignment& shades, const SieveConfig& config) {
+  return eval_projection(gs, k, shades, config, true);
+}
+
 }  // namespace tsieve

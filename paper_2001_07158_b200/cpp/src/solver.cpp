@@ -97,7 +97,11 @@ void make_effective(const TemporalGraph& g, const VertexColoring& col, const Sol
   if (p.k < 1) throw std::invalid_argument("k must be positive");
 }
 
-std::vector<bool> color_filter(const TemporalGraph& g, const Prep& p, PreprocessLevel level) {
+// Kept-vertex mask (solver.cpp:458-497 of the reference): the exact color
+// filter, then the junction sieve on the static projection of what is left
+// (whp: flags exactly the vertices on a properly colored static k-path).
+std::vector<bool> preprocess_mask(const TemporalGraph& g, const Prep& p, PreprocessLevel level,
+                                  std::uint64_t& peak) {
   std::vector<bool> keep(static_cast<size_t>(g.n()), true);
   if (level == PreprocessLevel::color_filter || level == PreprocessLevel::both) {
     for (Vertex x = 0; x < g.n(); ++x) {
@@ -111,10 +115,20 @@ std::vector<bool> color_filter(const TemporalGraph& g, const Prep& p, Preprocess
     }
   }
   if ((level == PreprocessLevel::static_sieve || level == PreprocessLevel::both) &&
-      !p.query.multiset.empty())
-    throw std::invalid_argument(
-        "static-projection preprocessing (junction sieve) is not part of the B200 engine yet; "
-        "use --preprocess none or colors");
+      !p.query.multiset.empty()) {
+    MotifQuery relaxed;
+    relaxed.kind = QueryKind::multiset;
+    relaxed.k = p.k;
+    relaxed.multiset = p.query.multiset;
+    const ShadeAssignment sh = build_shades(relaxed, p.coloring, p.cfg);
+    if (!sh.feasible) return std::vector<bool>(static_cast<size_t>(g.n()), false);
+    const StaticProjection proj = StaticProjection::project(restrict_to(g, keep, g.t()));
+    const SieveOutcome jo = eval_junction_sieve(proj, p.k, sh, p.cfg);
+    peak = std::max(peak, jo.peak_field_words);
+    std::vector<bool> flagged(static_cast<size_t>(g.n()), false);
+    for (Vertex x : jo.flagged) flagged[x] = true;
+    for (Vertex x = 0; x < g.n(); ++x) keep[x] = keep[x] && flagged[x];
+  }
   return keep;
 }
 
@@ -135,7 +149,7 @@ Prep prepare(const TemporalGraph& g, const VertexColoring& col, const SolveReque
     p.graph = g;
     return p;
   }
-  const std::vector<bool> keep = color_filter(g, p, req.preprocess);
+  const std::vector<bool> keep = preprocess_mask(g, p, req.preprocess, p.peak);
   p.graph = restrict_to(g, keep, g.t());
   p.kept = static_cast<int>(std::count(keep.begin(), keep.end(), true));
   if (p.kept < p.k) {
@@ -574,7 +588,7 @@ PreprocessResult preprocess(const TemporalGraph& g, const VertexColoring& colori
   Prep p;
   make_effective(g, coloring, sub, p);
   PreprocessResult out;
-  out.kept = color_filter(g, p, level);
+  out.kept = preprocess_mask(g, p, level, out.peak_field_words);
   out.graph = restrict_to(g, out.kept, g.t());
   out.kept_count = static_cast<int>(std::count(out.kept.begin(), out.kept.end(), true));
   return out;

@@ -49,6 +49,32 @@ struct LevelParams {
   int ymul = 0;
 };
 
+// One level of a static-projection engine (static_kernels.cu).
+struct StaticLevel {
+  int64_t C = 0;                      // chunks
+  const int64_t* chunk_arc = nullptr; // C+1
+  const int32_t* arc_head = nullptr;  // head-sorted arcs
+  const int32_t* arc_tail = nullptr;
+  const int32_t* arc_edge = nullptr;  // static edge id
+  const uint64_t* zj = nullptr;
+  int k = 0;
+  uint64_t seed = 1;
+  uint64_t role = 3;                  // edge_y (ending) or edge_y2 (starting)
+  int level = 1;                      // second draw index
+  bool tail_times_z = false;          // walks-starting family
+  bool head_times_z = false;          // walks-ending family
+  const uint64_t* src = nullptr;      // n x W, nullptr = all-ones layer
+  uint64_t* out = nullptr;            // n x W, zeroed, XOR-accumulated
+  uint64_t pb = 0, pe = 0;
+  int ppt = 1;                        // W = 32 * ppt
+};
+
+void launch_static_level(const StaticLevel& p, cudaStream_t st);
+void launch_static_base(int32_t n, const uint64_t* zj, int k, uint64_t pb, uint64_t pe, int ppt,
+                        uint64_t* out, cudaStream_t st);
+void launch_static_readout(int32_t n, const uint64_t* a, const uint64_t* b, int ppt,
+                           uint64_t* acc, cudaStream_t st);
+
 // Kernel launchers (kernels.cu).  All are asynchronous on `st`.
 void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
                const int32_t* vertex_shades, const uint64_t* wtab, uint64_t* zj,

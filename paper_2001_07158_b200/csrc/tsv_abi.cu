@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <stdexcept>
 #include <string>
@@ -531,6 +532,171 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
   });
   tsv_shades_free(sh);
   return rc;
+}
+
+int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const int32_t* b,
+                               int directed, int junction, int k, const int32_t* vertex_off,
+                               const int32_t* vertex_shades, const tsv_config* cfg, int device,
+                               uint64_t* accumulators, tsv_outcome* out) {
+  return guard([&] {
+    if (!accumulators || !out || !vertex_off) throw std::invalid_argument("null argument");
+    check_config(cfg);
+    if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
+    if (n < 0 || ms < 0) throw std::invalid_argument("negative size");
+    // head-sorted arc lists of the projection: in-arcs (tail -> head) and
+    // out-arcs (head = the walk's current vertex, tail = the next one)
+    auto arcs = [&](bool incoming, std::vector<int32_t>& head, std::vector<int32_t>& tail,
+                    std::vector<int32_t>& edge) {
+      const int64_t A = directed ? ms : 2 * ms;
+      std::vector<int64_t> off(static_cast<size_t>(n) + 1, 0);
+      for (int64_t i = 0; i < ms; ++i) {
+        if (a[i] < 0 || a[i] >= n || b[i] < 0 || b[i] >= n)
+          throw std::invalid_argument("edge endpoint out of range");
+        ++off[(incoming ? b[i] : a[i]) + 1];
+        if (!directed) ++off[(incoming ? a[i] : b[i]) + 1];
+      }
+      for (int32_t x = 0; x < n; ++x) off[x + 1] += off[x];
+      head.resize(static_cast<size_t>(A));
+      tail.resize(static_cast<size_t>(A));
+      edge.resize(static_cast<size_t>(A));
+      auto put = [&](int32_t h, int32_t t, int64_t e) {
+        const int64_t p = off[h]++;
+        head[p] = h;
+        tail[p] = t;
+        edge[p] = static_cast<int32_t>(e);
+      };
+      for (int64_t i = 0; i < ms; ++i) {
+        if (incoming) put(b[i], a[i], i); else put(a[i], b[i], i);
+        if (!directed) { if (incoming) put(a[i], b[i], i); else put(b[i], a[i], i); }
+      }
+    };
+    DeviceGuard dg(device);
+    cudaStream_t st = nullptr;
+    TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    } sg{st};
+    const uint64_t P = 1ull << k;
+    const int ppt = P >= 64 ? 2 : 1;
+    const int W = 32 * ppt;
+    const uint64_t layers = junction ? static_cast<uint64_t>(k) + 2 : 2;
+    const uint64_t words = layers * static_cast<uint64_t>(n) * W +
+                           static_cast<uint64_t>(n) * (static_cast<uint64_t>(k) + 1);
+    if (words > cfg->memory_cap_words)
+      throw CapError("sieve memory cap exceeded: needs " + std::to_string(words) +
+                     " field words, cap " + std::to_string(cfg->memory_cap_words));
+
+    std::vector<int32_t> ih, it, ie, oh, ot, oe;
+    arcs(true, ih, it, ie);
+    if (junction) arcs(false, oh, ot, oe);
+    auto chunks = [](int64_t A) {
+      std::vector<int64_t> c;
+      const int64_t ch = 256;
+      for (int64_t s = 0; s < A; s += ch) c.push_back(s);
+      c.push_back(A);
+      return c;
+    };
+    const std::vector<int64_t> ic = chunks(static_cast<int64_t>(ih.size()));
+    const std::vector<int64_t> oc = chunks(static_cast<int64_t>(oh.size()));
+    auto up = [&](const auto& v) {
+      using T = typename std::decay_t<decltype(v)>::value_type;
+      auto* buf = new DevBuf(std::max<size_t>(v.size(), 1) * sizeof(T), st);
+      if (!v.empty())
+        TSV_CUDA(cudaMemcpyAsync(buf->p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, st));
+      return std::unique_ptr<DevBuf>(buf);
+    };
+    auto d_ih = up(ih), d_it = up(it), d_ie = up(ie), d_ic = up(ic);
+    auto d_oh = up(oh), d_ot = up(ot), d_oe = up(oe), d_oc = up(oc);
+    std::vector<int32_t> off(vertex_off, vertex_off + n + 1);
+    std::vector<int32_t> shv(vertex_shades, vertex_shades + vertex_off[n]);
+    for (int32_t s : shv)
+      if (s < 1 || s > k) throw std::invalid_argument("shade id outside [1..k]");
+    auto d_off = up(off), d_sh = up(shv);
+    std::vector<uint64_t> wtab(static_cast<size_t>(k) * k);
+    for (int d = 1; d <= k; ++d)
+      for (int j = 1; j <= k; ++j)
+        wtab[(d - 1) * k + (j - 1)] = tsv::draw_nonzero(cfg->seed, tsv::kRoleShadeW, d, j, 0);
+    auto d_w = up(wtab);
+    DevBuf zj(static_cast<size_t>(n) * k * 8, st), acc(static_cast<size_t>(n) * 8, st);
+    tsv::launch_zj(n, k, cfg->seed, d_off->as<int32_t>(), d_sh->as<int32_t>(),
+                   d_w->as<uint64_t>(), zj.as<uint64_t>(), st);
+    TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8, st));
+    const size_t layer = static_cast<size_t>(n) * W;
+    std::vector<std::unique_ptr<DevBuf>> ending;
+    for (uint64_t i = 0; i <= static_cast<uint64_t>(k); ++i)
+      ending.emplace_back(new DevBuf((junction || i <= 2 ? layer : 1) * 8, st));
+    DevBuf s0(layer * 8, st), s1(layer * 8, st);
+
+    tsv::StaticLevel in;
+    in.C = static_cast<int64_t>(ic.size()) - 1;
+    in.chunk_arc = d_ic->as<int64_t>();
+    in.arc_head = d_ih->as<int32_t>();
+    in.arc_tail = d_it->as<int32_t>();
+    in.arc_edge = d_ie->as<int32_t>();
+    in.zj = zj.as<uint64_t>();
+    in.k = k;
+    in.seed = cfg->seed;
+    in.role = tsv::kRoleEdgeY;
+    in.head_times_z = true;
+    in.ppt = ppt;
+    tsv::StaticLevel outl = in;
+    outl.C = static_cast<int64_t>(oc.size()) - 1;
+    outl.chunk_arc = d_oc->as<int64_t>();
+    outl.arc_head = d_oh->as<int32_t>();
+    outl.arc_tail = d_ot->as<int32_t>();
+    outl.arc_edge = d_oe->as<int32_t>();
+    outl.role = 4;  // edge_y2
+    outl.head_times_z = false;
+    outl.tail_times_z = true;
+
+    for (uint64_t pb = 0; pb < P; pb += W) {
+      const uint64_t pe = std::min(P, pb + W);
+      in.pb = outl.pb = pb;
+      in.pe = outl.pe = pe;
+      // walks-ending family E_1..E_k (static: only the last two layers kept)
+      auto E = [&](int l) -> uint64_t* {
+        return ending[junction ? l : (l % 2) + 1]->as<uint64_t>();
+      };
+      tsv::launch_static_base(n, zj.as<uint64_t>(), k, pb, pe, ppt, E(1), st);
+      for (int l = 2; l <= k; ++l) {
+        TSV_CUDA(cudaMemsetAsync(E(l), 0, layer * 8, st));
+        in.level = l - 1;
+        in.src = E(l - 1);
+        in.out = E(l);
+        tsv::launch_static_level(in, st);
+      }
+      if (!junction) {
+        tsv::launch_static_readout(n, E(k), nullptr, ppt, acc.as<uint64_t>(), st);
+        continue;
+      }
+      // walks-starting family S_1 = 1, S_b from S_{b-1}; readout E_{k+1-b} * S_b
+      tsv::launch_static_readout(n, E(k), nullptr, ppt, acc.as<uint64_t>(), st);
+      uint64_t* sp = nullptr;
+      uint64_t* sc = s0.as<uint64_t>();
+      for (int bb = 2; bb <= k; ++bb) {
+        TSV_CUDA(cudaMemsetAsync(sc, 0, layer * 8, st));
+        outl.level = bb - 1;
+        outl.src = sp;
+        outl.out = sc;
+        tsv::launch_static_level(outl, st);
+        tsv::launch_static_readout(n, E(k + 1 - bb), sc, ppt, acc.as<uint64_t>(), st);
+        sp = sc;
+        sc = (sc == s0.as<uint64_t>()) ? s1.as<uint64_t>() : s0.as<uint64_t>();
+      }
+    }
+    TSV_CUDA(cudaGetLastError());
+    if (n)
+      TSV_CUDA(cudaMemcpyAsync(accumulators, acc.p, static_cast<size_t>(n) * 8,
+                               cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    *out = tsv_outcome{};
+    finalize_host(n, accumulators, -1, k, out);
+    out->peak_field_words = words;
+  });
 }
 
 int tsv_xor_combine_device(const uint64_t* d_parts, int nparts, int64_t n,

@@ -181,6 +181,39 @@ def main():
                       "extraction": extraction, "preprocess": pre, "result": r})
     out["solve_sweep"] = sweep
 
+    # default preprocessing (junction sieve on the static projection): the
+    # kept-vertex set changes edge renumbering, so checksums pin it exactly
+    pre_sweep = []
+    for i in range(48):
+        n, u, v, ts, d, colors, motif = synth.random_small(srng, n_max=18, m_max=70, t_max=6,
+                                                           k_max=5, q_max=3)
+        prob = problems[i % 4]
+        k, src, dst = 0, -1, -1
+        if prob == "ktemppath":
+            motif, k = [], int(srng.integers(1, 5))
+        elif prob == "colorfulpath":
+            motif = sorted(set(motif)) or [1]
+        elif prob == "sdcolorful":
+            motif, k = [], int(srng.integers(1, 3))
+            src, dst = (int(x) for x in srng.choice(n, 2, replace=False))
+        mode = [0, 3][(i // 4) % 2]
+        pre = [3, 2][(i // 8) % 2]
+        seed = int(srng.integers(1, 1000))
+        r = O.ref_solve(n, u, v, ts, d, colors, prob, motif, k, source=src, dest=dst, seed=seed,
+                        mode=mode, extraction=(i // 16) % 2, preprocess=pre)
+        pre_sweep.append({"n": n, "u": u.tolist(), "v": v.tolist(), "ts": ts.tolist(),
+                          "directed": d, "colors": colors.tolist(), "problem": prob,
+                          "motif": motif, "k": k, "source": src, "dest": dst, "seed": seed,
+                          "mode": mode, "extraction": (i // 16) % 2, "preprocess": pre,
+                          "result": r})
+    out["solve_sweep_preprocess"] = pre_sweep
+    fig2_default = []
+    for prob, motif, k in (("pathmotif", [1, 1, 2, 3], 0), ("colorfulpath", [1, 2, 3, 4], 0),
+                           ("ktemppath", [], 4), ("pathmotif", [1, 1, 1, 3], 0)):
+        r = O.ref_solve(5, *fig2, False, fig2_col, prob, motif, k, seed=1, mode=3, preprocess=3)
+        fig2_default.append({"problem": prob, "motif": motif, "k": k, "result": r})
+    out["solve_fig2_default"] = fig2_default
+
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=0)

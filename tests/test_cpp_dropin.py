@@ -162,3 +162,42 @@ def test_cli_decide_extract_verify_optimum(cuda_device, fig2, tmp_path, golden):
                                         "--extraction", "self-reducible", "--format", "json"])
     assert rc == 0
     assert json.loads(out)["witness"]["vertex_names"][0] == "u4"
+
+
+@pytest.mark.gpu
+def test_default_preprocessing_matches_reference(cuda_device, golden):
+    """--preprocess both / static: the junction sieve on the static
+    projection runs on the GPU; the kept-vertex set (preprocessed_n/m), and
+    through the renumbered edge ids every checksum, equal the reference's."""
+    for c in golden["solve_sweep_preprocess"]:
+        got, want = solve(c), c["result"]
+        for key in ("decision", "certain", "optimum_ts", "checksum", "flagged", "witness",
+                    "extraction_failed", "oracle_calls", "preprocessed_n", "preprocessed_m"):
+            assert got[key] == want[key], (key, c["problem"], c["preprocess"], got, want)
+
+
+@pytest.mark.gpu
+def test_cli_reference_defaults(cuda_device, fig2, golden):
+    """The reference CLI tests (test_cli.cpp:41-84) with DEFAULT flags
+    (preprocess both, optimize on)."""
+    rc, out = cli(["decide"] + fig2 + ["--problem", "pathmotif", "--motif", "1,1,2,3",
+                                       "--format", "json"])
+    assert rc == 0 and '"decision": "YES"' in out
+    rc, _ = cli(["decide"] + fig2 + ["--problem", "pathmotif", "--motif", "1,1,1,3"])
+    assert rc == 1
+    rc, out = cli(["optimum"] + fig2 + ["--problem", "pathmotif", "--motif", "1,1,2,3",
+                                        "--format", "json"])
+    assert rc == 0 and '"optimum_ts": 3' in out
+    for case in golden["solve_fig2_default"]:
+        args = ["extract"] + fig2 + ["--problem", case["problem"], "--format", "json"]
+        args += ["--motif", ",".join(map(str, case["motif"]))] if case["motif"] else \
+            ["--k", str(case["k"])]
+        rc, out = cli(args)
+        rec = json.loads(out)
+        want = case["result"]
+        assert rec["decision"] == ("YES" if want["decision"] else "NO")
+        assert rec["accumulator_checksum"] == want["checksum"]
+        assert rec["preprocessed"]["n"] == want["preprocessed_n"]
+        got_w = None if rec["witness"] is None else {"vertices": rec["witness"]["vertices"],
+                                                     "edges": rec["witness"]["edges"]}
+        assert got_w == want["witness"]
