@@ -98,9 +98,6 @@ def dist_env():
     return rank, world, local
 
 
-def shard(P: int, rank: int, world: int):
-    """Contiguous sieve-point range of one rank."""
-    return rank * P // world, (rank + 1) * P // world
 
 
 # ------------------------------------------------------------------ CPU legs
@@ -202,6 +199,7 @@ def main():
 
     import paper_2001_07158_b200 as T
     from paper_2001_07158_b200 import _native, synth
+    from paper_2001_07158_b200.shard import point_range, xor_allreduce
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -215,7 +213,7 @@ def main():
     reps = REPS[args.config]
     seeds = [1 + r for r in range(reps)]
     P = 1 << k
-    p0, p1 = shard(P, rank, world)
+    p0, p1 = point_range(P, rank, world)
 
     g = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
     col = T.VertexColoring(colors, int(colors.max()))
@@ -224,7 +222,6 @@ def main():
     ds = T.DeviceShades(g, k, sh)
     n = g.n()
     acc = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
-    gathered = torch.zeros((world, reps, n), dtype=torch.int64, device="cuda") if world > 1 else None
     total = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
 
     def step():
@@ -233,9 +230,7 @@ def main():
             T.eval_points_device(g, ds, k, g.t(), cfgs[r], anchor[0], p0, p1,
                                  acc[r].data_ptr(), sp)
         if world > 1:
-            dist.all_gather_into_tensor(gathered.view(-1), acc.view(-1))
-            T.xor_combine_device(gathered.data_ptr(), world, reps * n, total.data_ptr(), sp)
-            return total
+            return xor_allreduce(acc, out=total)
         return acc
 
     for _ in range(args.warmup):
@@ -277,14 +272,23 @@ def main():
 
     # roofline of the dominant kernel (level, l >= 3): 16 B per (arc, point)
     hbm, peak_kind = peaks()
-    W_eff = min(P // world if world > 1 else P, args.points_per_batch or 64)
     roof = None
     if lvl_n:
+        # updates executed by the l >= 3 launches of this rank in the timed region
+        upd_lvl = g.info.arcs * (k - 2) * (p1 - p0) * reps * args.steps
+        alg_bytes = BYTES_PER_UPDATE * upd_lvl / lvl_n
         avg_ms = lvl_ms / lvl_n
-        alg_bytes = BYTES_PER_UPDATE * g.info.arcs * W_eff
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_level_traffic.json")) as f:
+                prof = json.load(f)
+            if prof["config"] == args.config and world == 1:
+                traffic = prof["traffic_bytes_per_launch"]
+        except Exception:
+            pass
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                 "kernel": "k_level (l>=3)", "avg_launch_ms": avg_ms,
                 "launch_share_of_step": lvl_ms / max(all_ms, 1e-9),
                 "alg_bytes_per_launch": alg_bytes}
@@ -305,9 +309,7 @@ def main():
                 T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], p0, p1,
                                      a2[r].data_ptr(), sp)
             if world > 1:
-                dist.all_gather_into_tensor(gathered.view(-1), a2.view(-1))
-                T.xor_combine_device(gathered.data_ptr(), world, reps * n, total.data_ptr(), sp)
-                a2 = total
+                a2 = xor_allreduce(a2, out=total)
             h = a2.cpu()
             del g2, ds2
         torch.cuda.synchronize()

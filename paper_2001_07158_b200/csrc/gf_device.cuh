@@ -102,13 +102,30 @@ __device__ __forceinline__ u128 clmul64_school(uint64_t a, uint64_t b) {
   return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
 }
 
+// Shifts issued on the FMA pipe (IMAD.SHL / IMAD.HI) instead of the ALU pipe,
+// which the carry-less XOR network already saturates.
+__device__ __forceinline__ uint32_t shl_f(uint32_t x, uint32_t pow2) {
+  uint32_t r;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(pow2));
+  return r;
+}
+__device__ __forceinline__ uint32_t shr_f(uint32_t x, uint32_t pow2_32ms) {
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(pow2_32ms));
+  return r;
+}
+
 // Reduce a 128-bit carry-less product modulo x^64 + x^4 + x^3 + x + 1:
-// h * x^64 == h * (x^4 + x^3 + x + 1), folded twice.
+// h * x^64 == h * (x^4 + x^3 + x + 1), folded twice.  Written on 32-bit
+// halves so every shift is a multiply (FMA pipe) and every combine an XOR.
 __device__ __forceinline__ uint64_t gf_reduce(u128 p) {
-  const uint64_t h = p.hi;
-  const uint64_t over = (h >> 63) ^ (h >> 61) ^ (h >> 60);
-  return p.lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4) ^ over ^ (over << 1) ^ (over << 3) ^
-         (over << 4);
+  const uint32_t hl = lo32(p.hi), hh = hi32(p.hi);
+  const uint32_t over = shr_f(hh, 2u) ^ shr_f(hh, 8u) ^ shr_f(hh, 16u);  // bits 63,61,60
+  const uint32_t lo = lo32(p.lo) ^ hl ^ shl_f(hl, 2u) ^ shl_f(hl, 8u) ^ shl_f(hl, 16u) ^ over ^
+                      shl_f(over, 2u) ^ shl_f(over, 8u) ^ shl_f(over, 16u);
+  const uint32_t hi = hi32(p.lo) ^ hh ^ shl_f(hh, 2u) ^ shl_f(hh, 8u) ^ shl_f(hh, 16u) ^
+                      shr_f(hl, 2u) ^ shr_f(hl, 8u) ^ shr_f(hl, 16u);
+  return pack(lo, hi);
 }
 
 __device__ __forceinline__ uint64_t gf_mul_kara(uint64_t a, uint64_t b) {
@@ -168,14 +185,34 @@ struct GfTable {
     row[7] = base ^ B2 ^ B1 ^ B0;
   }
 
+  // Lookups: nibble j of s, scaled by 8, is placed into the low byte of the
+  // table's shared-memory address with one byte permute (the table is
+  // 256-byte aligned); the window offset j*128 rides in the load immediate.
+  template <int OFF>
+  __device__ __forceinline__ static uint64_t lds(uint32_t addr) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1+%2];" : "=l"(v) : "r"(addr), "n"(OFF));
+    return v;
+  }
+
+  template <int WIN>
+  __device__ __forceinline__ static uint64_t word8(uint32_t w, uint32_t base) {
+    const uint32_t e = shl_f(w, 8u) & 0x78787878u;          // nibbles 0,2,4,6 (x8)
+    const uint32_t o = shr_f(w, 0x80000000u) & 0x78787878u; // nibbles 1,3,5,7 (x8)
+    uint64_t a = lds<(WIN + 0) * 128>(__byte_perm(e, base, 0x7650)) ^
+                 lds<(WIN + 1) * 128>(__byte_perm(o, base, 0x7650));
+    a ^= lds<(WIN + 2) * 128>(__byte_perm(e, base, 0x7651)) ^
+         lds<(WIN + 3) * 128>(__byte_perm(o, base, 0x7651));
+    a ^= lds<(WIN + 4) * 128>(__byte_perm(e, base, 0x7652)) ^
+         lds<(WIN + 5) * 128>(__byte_perm(o, base, 0x7652));
+    a ^= lds<(WIN + 6) * 128>(__byte_perm(e, base, 0x7653)) ^
+         lds<(WIN + 7) * 128>(__byte_perm(o, base, 0x7653));
+    return a;
+  }
+
   __device__ __forceinline__ uint64_t mul(uint64_t s) const {
-    uint64_t acc = 0;
-    const uint32_t w0 = lo32(s), w1 = hi32(s);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc ^= tab[i * 16 + ((w0 >> (4 * i)) & 15u)];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc ^= tab[(i + 8) * 16 + ((w1 >> (4 * i)) & 15u)];
-    return acc;
+    const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(tab));
+    return word8<0>(lo32(s), base) ^ word8<8>(hi32(s), base);
   }
 };
 

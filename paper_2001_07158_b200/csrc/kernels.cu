@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPT >= 4 ? 2 : 3)
   __shared__ uint32_t s_meta[kWarpsPerBlock][32];
   __shared__ int32_t s_run[kWarpsPerBlock][32];
   __shared__ int32_t s_head[kWarpsPerBlock][32];
-  __shared__ uint64_t s_tab[YTAB ? kWarpsPerBlock : 1][256];
+  __shared__ __align__(256) uint64_t s_tab[YTAB ? kWarpsPerBlock : 1][256];
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
