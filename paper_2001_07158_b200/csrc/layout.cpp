@@ -1,6 +1,8 @@
 // layout.cpp -- see layout.hpp.  Host C++ (OpenMP where it pays).
 #include "layout.hpp"
 
+#include <parallel/algorithm>
+
 #include <algorithm>
 #include <numeric>
 #include <stdexcept>
@@ -35,7 +37,11 @@ void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
     if (x.u != y.u) return x.u < y.u;
     return x.v < y.v;
   };
-  std::sort(kept.begin(), kept.end(), key_less);
+  // multiway-mergesort on all host cores for the 1e8-1e9-edge configs
+  if (kept.size() > (1u << 20))
+    __gnu_parallel::sort(kept.begin(), kept.end(), key_less);
+  else
+    std::sort(kept.begin(), kept.end(), key_less);
   auto same = [](const E& x, const E& y) {
     return x.ts == y.ts && x.u == y.u && x.v == y.v;
   };
