@@ -8,9 +8,11 @@ seed evaluates all 2^k_eff sieve points over the whole synthetic graph
 4 repetitions).  Metric: GF(2^64) edge x level x sieve-point updates per
 second, updates = A * (k_eff - 1) * 2^k_eff per repetition.
 
-With N > 1 (torchrun) the 2^k_eff sieve points are sharded across ranks (no
-data-path collective); the per-vertex partial accumulators are XOR-combined
-once per step (NCCL all-gather + XOR kernel; NCCL has no XOR reduction).
+With N > 1 (torchrun) the (repetition, sieve point) units of the decide are
+split into contiguous ranges (shard.work_units: whole repetitions while
+N <= reps, halves of one beyond), with no data-path collective; the
+per-vertex partial accumulators are XOR-combined once per step (NCCL
+all-gather + XOR kernel; NCCL has no XOR reduction).
 """
 from __future__ import annotations
 
@@ -210,7 +212,7 @@ def main():
 
     import paper_2001_07158_b200 as T
     from paper_2001_07158_b200 import _native, synth
-    from paper_2001_07158_b200.shard import point_range, xor_allreduce
+    from paper_2001_07158_b200.shard import work_units, xor_allreduce
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -224,7 +226,8 @@ def main():
     reps = REPS[args.config]
     seeds = [1 + r for r in range(reps)]
     P = 1 << k
-    p0, p1 = point_range(P, rank, world)
+    work = work_units(reps, P, rank, world)   # [(rep, p_begin, p_end)]
+    my_points = sum(b - a for _, a, b in work)
 
     g = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
     col = T.VertexColoring(colors, int(colors.max()))
@@ -237,8 +240,8 @@ def main():
 
     def step():
         acc.zero_()
-        for r in range(reps):
-            T.eval_points_device(g, ds, k, g.t(), cfgs[r], anchor[0], p0, p1,
+        for r, a, b in work:
+            T.eval_points_device(g, ds, k, g.t(), cfgs[r], anchor[0], a, b,
                                  acc[r].data_ptr(), sp)
         if world > 1:
             return xor_allreduce(acc, out=total)
@@ -286,7 +289,7 @@ def main():
     roof = None
     if lvl_n:
         # updates executed by the l >= 3 launches of this rank in the timed region
-        upd_lvl = g.info.arcs * (k - 2) * (p1 - p0) * reps * args.steps
+        upd_lvl = g.info.arcs * (k - 2) * my_points * args.steps
         alg_bytes = BYTES_PER_UPDATE * upd_lvl / lvl_n
         avg_ms = lvl_ms / lvl_n
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
@@ -316,8 +319,8 @@ def main():
             g2 = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
             ds2 = T.DeviceShades(g2, k, sh)
             a2 = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
-            for r in range(reps):
-                T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], p0, p1,
+            for r, a, b in work:
+                T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], a, b,
                                      a2[r].data_ptr(), sp)
             if world > 1:
                 a2 = xor_allreduce(a2, out=total)

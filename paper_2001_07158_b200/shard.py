@@ -19,6 +19,22 @@ def point_range(P: int, rank: int, world: int) -> tuple[int, int]:
     return rank * P // world, (rank + 1) * P // world
 
 
+def work_units(reps: int, P: int, rank: int, world: int) -> list[tuple[int, int, int]]:
+    """Share of one decide over `reps` repetitions x P sieve points.
+
+    The (repetition, point) units are split into contiguous ranges, so a rank
+    keeps whole repetitions while world <= reps (every batch stays as wide as
+    a single-GPU run) and splits a repetition's points only beyond that.
+    Returns [(rep, p_begin, p_end), ...]."""
+    u0, u1 = point_range(reps * P, rank, world)
+    out = []
+    for r in range(u0 // P, (u1 + P - 1) // P if u1 > u0 else u0 // P):
+        a, b = max(u0, r * P) - r * P, min(u1, (r + 1) * P) - r * P
+        if a < b:
+            out.append((r, a, b))
+    return out
+
+
 def xor_allreduce(t, group=None, out=None):
     """XOR-combine an int64 tensor across ranks; every rank receives the result.
 

@@ -50,6 +50,23 @@ def _worker(rank, world, port, case, q):
         dist.destroy_process_group()
 
 
+def test_work_units_cover_every_rep_point_once():
+    from paper_2001_07158_b200.shard import work_units
+    for reps, P in ((4, 64), (1, 32), (3, 8), (1, 4096)):
+        for world in (1, 2, 3, 4, 8):
+            seen = {}
+            for r in range(world):
+                for rep, a, b in work_units(reps, P, r, world):
+                    assert 0 <= a < b <= P
+                    for p in range(a, b):
+                        assert (rep, p) not in seen
+                        seen[(rep, p)] = r
+            assert len(seen) == reps * P
+    # C2 (4 reps x 64 points): up to 4 GPUs every rank keeps whole 64-point reps
+    assert work_units(4, 64, 1, 4) == [(1, 0, 64)]
+    assert work_units(4, 64, 5, 8) == [(2, 32, 64)]
+
+
 def test_point_ranges_partition():
     for P in (2, 32, 64, 4096):
         for world in (1, 2, 3, 4, 8):
