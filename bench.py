@@ -231,7 +231,10 @@ def main():
 
     g = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
     col = T.VertexColoring(colors, int(colors.max()))
-    cfgs = [T.SieveConfig(seed=s, points_per_batch=args.points_per_batch) for s in seeds]
+    # the reference's default cap (2^31 words) sizes ITS dense layers; the
+    # engine's batch width is bounded by device memory instead
+    cfgs = [T.SieveConfig(seed=s, points_per_batch=args.points_per_batch,
+                          memory_cap_words=1 << 62) for s in seeds]
     sh = T.build_shades(T.MotifQuery.from_multiset(motif), col, cfgs[0])
     ds = T.DeviceShades(g, k, sh)
     n = g.n()

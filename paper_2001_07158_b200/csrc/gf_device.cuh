@@ -84,6 +84,32 @@ __device__ __forceinline__ u128 clmul64_kara(uint64_t a, uint64_t b) {
   return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
 }
 
+// Operand pre-split for Karatsuba (lo, hi, lo^hi halves, 4 classes each):
+// a multiplier reused across products (z_head along a head's runs) is split
+// once and cached.
+struct KSplit {
+  Split4 l, h, m;
+};
+
+__device__ __forceinline__ KSplit ksplit(uint64_t a) {
+  return {split4(lo32(a)), split4(hi32(a)), split4(lo32(a) ^ hi32(a))};
+}
+
+__device__ __forceinline__ u128 clmul64_kara_s(const KSplit& A, const KSplit& B) {
+  uint64_t lo[4], hi[4];
+#define TSV_KSCLASS(R)                                         \
+  {                                                            \
+    const uint64_t L = class_prod<R>(A.l, B.l);                \
+    const uint64_t H = class_prod<R>(A.h, B.h);                \
+    const uint64_t M = class_prod<R>(A.m, B.m) ^ L ^ H;        \
+    lo[R] = L ^ (M << 32);                                     \
+    hi[R] = H ^ (M >> 32);                                     \
+  }
+  TSV_KSCLASS(0) TSV_KSCLASS(1) TSV_KSCLASS(2) TSV_KSCLASS(3)
+#undef TSV_KSCLASS
+  return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
+}
+
 // Schoolbook over 32-bit halves with deferred class masking.
 __device__ __forceinline__ u128 clmul64_school(uint64_t a, uint64_t b) {
   const Split4 al = split4(lo32(a)), ah = split4(hi32(a));
@@ -130,6 +156,9 @@ __device__ __forceinline__ uint64_t gf_reduce(u128 p) {
 
 __device__ __forceinline__ uint64_t gf_mul_kara(uint64_t a, uint64_t b) {
   return gf_reduce(clmul64_kara(a, b));
+}
+__device__ __forceinline__ uint64_t gf_mul_presplit(const KSplit& a, uint64_t b) {
+  return gf_reduce(clmul64_kara_s(a, ksplit(b)));
 }
 __device__ __forceinline__ uint64_t gf_mul_school(uint64_t a, uint64_t b) {
   return gf_reduce(clmul64_school(a, b));

@@ -28,6 +28,7 @@ namespace tsv {
 namespace {
 
 constexpr int kWarpsPerBlock = 8;
+constexpr int kWideWarps = 4;  // wide kernel: 4 warps per block (shared tables)
 constexpr unsigned kFull = 0xffffffffu;
 
 template <int PPT>
@@ -216,18 +217,19 @@ __device__ __forceinline__ void fetch_src(const LevelParams& P, int32_t src,
 // the shared-memory multiple tables (GfTable) when YTAB; z_head^A is cached
 // across the consecutive runs of one head.
 template <int PPT, bool FIRST, bool YTAB>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32, PPT >= 4 ? 2 : 3)
+__global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
     k_level_wide(const LevelParams P) {
   constexpr int W = 32 * PPT;
-  __shared__ uint64_t s_y[kWarpsPerBlock][32];
-  __shared__ int32_t s_src[kWarpsPerBlock][32];
-  __shared__ uint32_t s_meta[kWarpsPerBlock][32];
-  __shared__ int32_t s_run[kWarpsPerBlock][32];
-  __shared__ int32_t s_head[kWarpsPerBlock][32];
-  __shared__ __align__(256) uint64_t s_tab[YTAB ? kWarpsPerBlock : 1][256];
+  __shared__ uint64_t s_y[kWideWarps][32];
+  __shared__ int32_t s_src[kWideWarps][32];
+  __shared__ uint32_t s_meta[kWideWarps][32];
+  __shared__ int32_t s_run[kWideWarps][32];
+  __shared__ int32_t s_head[kWideWarps][32];
+  __shared__ __align__(256) uint64_t s_tab[YTAB ? kWideWarps : 1][256];
+  __shared__ uint32_t s_zs[kWideWarps][PPT][12][32];  // split z_head^A per lane
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kWideWarps + wib;
   if (c >= P.g.C) return;  // warp-uniform
 
   uint32_t pt[PPT];
@@ -304,14 +306,32 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, PPT >= 4 ? 2 : 3)
         }
         if (mt & kRunEnd) {
           const int32_t h = s_head[wib][i];
-          if (h != zhead) {
+          if (h != zhead) {  // new head: z_head^A and its Karatsuba split, cached
             z_of<PPT>(P.zj, P.k, h, pt, pv, z);
             zhead = h;
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) {
+              const KSplit ks = ksplit(z[p]);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                s_zs[wib][p][j][lane] = ks.l.c[j];
+                s_zs[wib][p][4 + j][lane] = ks.h.c[j];
+                s_zs[wib][p][8 + j][lane] = ks.m.c[j];
+              }
+            }
           }
           const int64_t run = s_run[wib][i];
 #pragma unroll
-          for (int p = 0; p < PPT; ++p)
-            P.s_cur[run * W + lane + 32 * p] = gf_mul(z[p], U[p]);
+          for (int p = 0; p < PPT; ++p) {
+            KSplit ks;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              ks.l.c[j] = s_zs[wib][p][j][lane];
+              ks.h.c[j] = s_zs[wib][p][4 + j][lane];
+              ks.m.c[j] = s_zs[wib][p][8 + j][lane];
+            }
+            P.s_cur[run * W + lane + 32 * p] = gf_mul_presplit(ks, U[p]);
+          }
         }
       }
     }
@@ -416,12 +436,14 @@ void level_dispatch(const LevelParams& p, cudaStream_t st) {
   const dim3 grid(static_cast<unsigned>((p.g.C + kWarpsPerBlock - 1) / kWarpsPerBlock));
   const dim3 block(kWarpsPerBlock * 32);
   if (LANES == 32 && p.ymul != 2) {
+    const dim3 wgrid(static_cast<unsigned>((p.g.C + kWideWarps - 1) / kWideWarps));
+    const dim3 wblock(kWideWarps * 32);
     if (p.ymul == 1) {
-      if (p.ell == 2) k_level_wide<PPT, true, false><<<grid, block, 0, st>>>(p);
-      else k_level_wide<PPT, false, false><<<grid, block, 0, st>>>(p);
+      if (p.ell == 2) k_level_wide<PPT, true, false><<<wgrid, wblock, 0, st>>>(p);
+      else k_level_wide<PPT, false, false><<<wgrid, wblock, 0, st>>>(p);
     } else {
-      if (p.ell == 2) k_level_wide<PPT, true, true><<<grid, block, 0, st>>>(p);
-      else k_level_wide<PPT, false, true><<<grid, block, 0, st>>>(p);
+      if (p.ell == 2) k_level_wide<PPT, true, true><<<wgrid, wblock, 0, st>>>(p);
+      else k_level_wide<PPT, false, true><<<wgrid, wblock, 0, st>>>(p);
     }
     return;
   }
