@@ -1,0 +1,409 @@
+// build_kernels.cu -- on-device construction of the engine's graph layout
+// (the host build of TemporalGraph does not scale to 1e9
+// edges).  Produces exactly the arrays of layout.cpp:
+//
+//   canonical edges  drop self-loops, orient u<v (undirected), sort by
+//                    (ts,u,v), drop duplicates: edge id = index
+//                    (/root/reference/proj/core/src/graph.cpp:22-43)
+//   arcs             (head, tail, edge) stably sorted by head over edge
+//                    order = (head, ts) order; runs = (head, ts) groups
+//   arc_src          tail's last run with ts' < ts (binary search)
+//   chunks           fixed arc ranges; a vertex split by a chunk boundary is
+//                    repaired by k_fixup, exactly like a split hub
+//
+// Sorting uses CUB's radix sort (library primitive shipped with the CUDA
+// toolkit); everything else is our own kernels.
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include "engine.hpp"
+#include "layout.hpp"
+
+namespace tsv {
+namespace {
+
+constexpr int kT = 256;
+
+unsigned nblk(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); }
+
+int bits_for(uint64_t x) {  // bits needed to represent values < x + 1
+  int b = 1;
+  while (b < 64 && (x >> b)) ++b;
+  return b;
+}
+
+__global__ void k_validate_orient(int64_t m, int32_t n, const int32_t* __restrict__ u,
+                                  const int32_t* __restrict__ v, const int32_t* __restrict__ ts,
+                                  int directed, uint64_t* __restrict__ key_uv,
+                                  uint32_t* __restrict__ key_ts, uint8_t* __restrict__ keep,
+                                  BuildStatus* st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int32_t a = u[i], b = v[i];
+  const int32_t t = ts[i];
+  if (a < 0 || a >= n || b < 0 || b >= n) {
+    atomicMin(reinterpret_cast<unsigned long long*>(&st->first_bad_endpoint),
+              static_cast<unsigned long long>(i));
+    keep[i] = 0;
+    return;
+  }
+  if (t < 1) {
+    atomicMin(reinterpret_cast<unsigned long long*>(&st->first_bad_ts),
+              static_cast<unsigned long long>(i));
+    keep[i] = 0;
+    return;
+  }
+  atomicMax(&st->max_ts, t);
+  if (a == b) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&st->self_loops), 1ull);
+    keep[i] = 0;
+    return;
+  }
+  if (!directed && a > b) {
+    const int32_t s = a;
+    a = b;
+    b = s;
+  }
+  key_uv[i] = static_cast<uint64_t>(a) * static_cast<uint64_t>(n) + static_cast<uint64_t>(b);
+  key_ts[i] = static_cast<uint32_t>(t);
+  keep[i] = 1;
+}
+
+// canonical-input variant: validate order instead of sorting
+__global__ void k_check_canonical(int64_t m, int32_t n, const int32_t* __restrict__ u,
+                                  const int32_t* __restrict__ v, const int32_t* __restrict__ ts,
+                                  int directed, BuildStatus* st) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int32_t a = u[i], b = v[i], t = ts[i];
+  if (a < 0 || a >= n || b < 0 || b >= n) {
+    atomicMin(reinterpret_cast<unsigned long long*>(&st->first_bad_endpoint),
+              static_cast<unsigned long long>(i));
+    return;
+  }
+  if (t < 1) {
+    atomicMin(reinterpret_cast<unsigned long long*>(&st->first_bad_ts),
+              static_cast<unsigned long long>(i));
+    return;
+  }
+  atomicMax(&st->max_ts, t);
+  bool ok = a != b && (directed || a < b);
+  if (i > 0) {
+    const int32_t pa = u[i - 1], pb = v[i - 1], pt = ts[i - 1];
+    ok = ok && (pt != t ? pt < t : pa != a ? pa < a : pb < b);
+  }
+  if (!ok) atomicExch(&st->not_canonical, 1);
+}
+
+__global__ void k_unique_flags(int64_t m, const uint32_t* __restrict__ kts,
+                               const uint64_t* __restrict__ kuv, uint8_t* __restrict__ flag) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  flag[i] = (i == 0 || kts[i] != kts[i - 1] || kuv[i] != kuv[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_unpack_edges(int64_t m, int32_t n, const uint32_t* __restrict__ kts,
+                               const uint64_t* __restrict__ kuv, int32_t* __restrict__ eu,
+                               int32_t* __restrict__ ev, int32_t* __restrict__ ets) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint64_t k = kuv[i];
+  eu[i] = static_cast<int32_t>(k / static_cast<uint64_t>(n));
+  ev[i] = static_cast<int32_t>(k % static_cast<uint64_t>(n));
+  ets[i] = static_cast<int32_t>(kts[i]);
+}
+
+// arcs in edge order: (head v, tail u) [+ (head u, tail v) when undirected]
+__global__ void k_make_arcs(int64_t m, int directed, const int32_t* __restrict__ eu,
+                            const int32_t* __restrict__ ev, uint32_t* __restrict__ head,
+                            uint32_t* __restrict__ idx) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  if (directed) {
+    head[i] = static_cast<uint32_t>(ev[i]);
+    idx[i] = static_cast<uint32_t>(i);
+  } else {
+    head[2 * i] = static_cast<uint32_t>(ev[i]);
+    idx[2 * i] = static_cast<uint32_t>(2 * i);
+    head[2 * i + 1] = static_cast<uint32_t>(eu[i]);
+    idx[2 * i + 1] = static_cast<uint32_t>(2 * i + 1);
+  }
+}
+
+// After the stable sort by head: tail/edge/ts of every arc, run starts.
+__global__ void k_arc_fields(int64_t A, int directed, const uint32_t* __restrict__ head,
+                             const uint32_t* __restrict__ idx, const int32_t* __restrict__ eu,
+                             const int32_t* __restrict__ ev, const int32_t* __restrict__ ets,
+                             int32_t* __restrict__ tail, int32_t* __restrict__ edge,
+                             int32_t* __restrict__ ats, int32_t* __restrict__ run_start) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= A) return;
+  const uint32_t a = idx[j];
+  const uint32_t e = directed ? a : (a >> 1);
+  const bool second = !directed && (a & 1u);
+  tail[j] = second ? ev[e] : eu[e];
+  edge[j] = static_cast<int32_t>(e);
+  const int32_t t = ets[e];
+  ats[j] = t;
+  int32_t start = 1;
+  if (j > 0) {
+    const uint32_t pa = idx[j - 1];
+    const int32_t pt = ets[directed ? pa : (pa >> 1)];
+    start = (head[j] != head[j - 1] || pt != t) ? 1 : 0;
+  }
+  run_start[j] = start;
+}
+
+// run_id = inclusive scan of run_start - 1; scatter run heads / timestamps
+__global__ void k_runs(int64_t A, const uint32_t* __restrict__ head,
+                       const int32_t* __restrict__ ats, const int32_t* __restrict__ run_start,
+                       const int32_t* __restrict__ run_incl, int32_t* __restrict__ run_head,
+                       int32_t* __restrict__ run_ts) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= A || !run_start[j]) return;
+  const int32_t r = run_incl[j] - 1;
+  run_head[r] = static_cast<int32_t>(head[j]);
+  run_ts[r] = ats[j];
+}
+
+// vtx_run_off[u] = first run with head >= u
+__global__ void k_vtx_off(int32_t n, int64_t R, const int32_t* __restrict__ run_head,
+                          int32_t* __restrict__ off) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u > n) return;
+  int64_t lo = 0, hi = R;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (run_head[mid] < u) lo = mid + 1;
+    else hi = mid;
+  }
+  off[u] = static_cast<int32_t>(lo);
+}
+
+__global__ void k_arc_src_meta(int64_t A, const uint32_t* __restrict__ head,
+                               const int32_t* __restrict__ tail, const int32_t* __restrict__ edge,
+                               const int32_t* __restrict__ ats,
+                               const int32_t* __restrict__ run_start,
+                               const int32_t* __restrict__ run_ts,
+                               const int32_t* __restrict__ vtx_run_off,
+                               int32_t* __restrict__ arc_src, uint32_t* __restrict__ arc_meta) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= A) return;
+  const int32_t x = tail[j], t = ats[j];
+  int32_t lo = vtx_run_off[x], hi = vtx_run_off[x + 1];
+  const int32_t base = lo;
+  while (lo < hi) {  // first run of x with ts >= t
+    const int32_t mid = lo + ((hi - lo) >> 1);
+    if (run_ts[mid] < t) lo = mid + 1;
+    else hi = mid;
+  }
+  arc_src[j] = lo == base ? -1 : lo - 1;
+  uint32_t meta = static_cast<uint32_t>(edge[j]);
+  if (j == 0 || head[j] != head[j - 1]) meta |= kVStart;
+  if (j + 1 == A || run_start[j + 1]) meta |= kRunEnd;
+  arc_meta[j] = meta;
+}
+
+// fixed chunks of ch arcs
+__global__ void k_chunks(int64_t C, int64_t A, int64_t ch, int64_t R,
+                         const int32_t* __restrict__ run_start,
+                         const int32_t* __restrict__ run_incl, const uint32_t* __restrict__ meta,
+                         int64_t* __restrict__ chunk_arc, int32_t* __restrict__ chunk_run,
+                         uint8_t* __restrict__ chunk_carry) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c > C) return;
+  const int64_t a = c * ch < A ? c * ch : A;
+  chunk_arc[c] = a;
+  if (c == C) {
+    chunk_run[c] = static_cast<int32_t>(R);
+    return;
+  }
+  // runs completed before arc a = id of a's run (0-based): earlier runs are
+  // complete, a's own run ends at or after a
+  chunk_run[c] = run_incl[a] - 1;
+  chunk_carry[c] = (meta[a] & kVStart) ? 0 : 1;
+}
+
+}  // namespace
+
+// Stable radix sort of (key, value) pairs with CUB; keys/values are swapped
+// into the DoubleBuffer's current buffers.
+template <typename K, typename V>
+static void radix_pairs(cub::DoubleBuffer<K>& k, cub::DoubleBuffer<V>& v, int64_t n, int end_bit,
+                        cudaStream_t st) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, k, v, n, 0, end_bit, st);
+  void* d_tmp = nullptr;
+  if (cudaMallocAsync(&d_tmp, tmp ? tmp : 8, st) != cudaSuccess)
+    throw std::runtime_error("device graph build: out of memory (sort)");
+  cub::DeviceRadixSort::SortPairs(d_tmp, tmp, k, v, n, 0, end_bit, st);
+  cudaFreeAsync(d_tmp, st);
+}
+
+void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, int64_t m,
+                  int32_t n, bool directed, bool canonical, DeviceLayout& out,
+                  BuildStatus* d_status, int sm_count, cudaStream_t st,
+                  const std::function<void*(size_t)>& alloc,
+                  const std::function<void(void*)>& release) {
+  auto A32 = [&](int64_t cnt) { return static_cast<int32_t*>(alloc(std::max<int64_t>(cnt, 1) * 4)); };
+  BuildStatus init{};
+  init.first_bad_endpoint = INT64_MAX;
+  init.first_bad_ts = INT64_MAX;
+  cudaMemcpyAsync(d_status, &init, sizeof(init), cudaMemcpyHostToDevice, st);
+
+  int32_t *eu = nullptr, *ev = nullptr, *ets = nullptr;
+  int64_t mc = m;
+  if (canonical) {
+    if (m) k_check_canonical<<<nblk(m), kT, 0, st>>>(m, n, d_u, d_v, d_ts, directed, d_status);
+    eu = A32(m);
+    ev = A32(m);
+    ets = A32(m);
+    cudaMemcpyAsync(eu, d_u, m * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(ev, d_v, m * 4, cudaMemcpyDeviceToDevice, st);
+    cudaMemcpyAsync(ets, d_ts, m * 4, cudaMemcpyDeviceToDevice, st);
+  } else {
+    // keys, drop loops/invalid, sort by (ts, u, v), unique
+    uint64_t* kuv[2] = {static_cast<uint64_t*>(alloc(std::max<int64_t>(m, 1) * 8)),
+                        static_cast<uint64_t*>(alloc(std::max<int64_t>(m, 1) * 8))};
+    uint32_t* kts[2] = {static_cast<uint32_t*>(alloc(std::max<int64_t>(m, 1) * 4)),
+                        static_cast<uint32_t*>(alloc(std::max<int64_t>(m, 1) * 4))};
+    uint8_t* keep = static_cast<uint8_t*>(alloc(std::max<int64_t>(m, 1)));
+    if (m)
+      k_validate_orient<<<nblk(m), kT, 0, st>>>(m, n, d_u, d_v, d_ts, directed ? 1 : 0, kuv[0],
+                                                kts[0], keep, d_status);
+    // compact kept edges
+    int64_t* d_cnt = static_cast<int64_t*>(alloc(8));
+    {
+      size_t tmp = 0;
+      cub::DeviceSelect::Flagged(nullptr, tmp, kuv[0], keep, kuv[1], d_cnt, m, st);
+      void* t = alloc(tmp ? tmp : 8);
+      cub::DeviceSelect::Flagged(t, tmp, kuv[0], keep, kuv[1], d_cnt, m, st);
+      cub::DeviceSelect::Flagged(t, tmp, kts[0], keep, kts[1], d_cnt, m, st);
+      release(t);
+    }
+    cudaMemcpyAsync(&mc, d_cnt, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    release(keep);
+    const uint64_t nn = static_cast<uint64_t>(n) * static_cast<uint64_t>(n);
+    BuildStatus hs{};
+    cudaMemcpy(&hs, d_status, sizeof(hs), cudaMemcpyDeviceToHost);
+    cub::DoubleBuffer<uint64_t> buv(kuv[1], kuv[0]);
+    cub::DoubleBuffer<uint32_t> bts(kts[1], kts[0]);
+    if (mc > 0 && hs.first_bad_endpoint == INT64_MAX && hs.first_bad_ts == INT64_MAX) {
+      // pass 1: by (u, v); pass 2 (stable): by ts
+      radix_pairs(buv, bts, mc, bits_for(nn ? nn - 1 : 0), st);
+      radix_pairs(bts, buv, mc, bits_for(static_cast<uint64_t>(hs.max_ts)), st);
+    }
+    uint8_t* flag = static_cast<uint8_t*>(alloc(std::max<int64_t>(mc, 1)));
+    if (mc) k_unique_flags<<<nblk(mc), kT, 0, st>>>(mc, bts.Current(), buv.Current(), flag);
+    {
+      size_t tmp = 0;
+      cub::DeviceSelect::Flagged(nullptr, tmp, buv.Current(), flag, buv.Alternate(), d_cnt, mc, st);
+      void* t = alloc(tmp ? tmp : 8);
+      cub::DeviceSelect::Flagged(t, tmp, buv.Current(), flag, buv.Alternate(), d_cnt, mc, st);
+      cub::DeviceSelect::Flagged(t, tmp, bts.Current(), flag, bts.Alternate(), d_cnt, mc, st);
+      release(t);
+    }
+    int64_t mu = 0;
+    cudaMemcpyAsync(&mu, d_cnt, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    out.dropped_duplicates = mc - mu;
+    mc = mu;
+    eu = A32(mc);
+    ev = A32(mc);
+    ets = A32(mc);
+    if (mc) k_unpack_edges<<<nblk(mc), kT, 0, st>>>(mc, n, bts.Alternate(), buv.Alternate(), eu, ev, ets);
+    release(flag);
+    release(d_cnt);
+    release(kuv[0]);
+    release(kuv[1]);
+    release(kts[0]);
+    release(kts[1]);
+  }
+  out.m = mc;
+  out.eu = eu;
+  out.ev = ev;
+  out.ets = ets;
+
+  // ---- arcs, runs -----------------------------------------------------------
+  const int64_t A = directed ? mc : 2 * mc;
+  out.A = A;
+  uint32_t* hd[2] = {static_cast<uint32_t*>(alloc(std::max<int64_t>(A, 1) * 4)),
+                     static_cast<uint32_t*>(alloc(std::max<int64_t>(A, 1) * 4))};
+  uint32_t* ix[2] = {static_cast<uint32_t*>(alloc(std::max<int64_t>(A, 1) * 4)),
+                     static_cast<uint32_t*>(alloc(std::max<int64_t>(A, 1) * 4))};
+  if (mc) k_make_arcs<<<nblk(mc), kT, 0, st>>>(mc, directed ? 1 : 0, eu, ev, hd[0], ix[0]);
+  cub::DoubleBuffer<uint32_t> bh(hd[0], hd[1]), bi(ix[0], ix[1]);
+  if (A) radix_pairs(bh, bi, A, bits_for(static_cast<uint64_t>(n)), st);
+  const uint32_t* head = bh.Current();
+  int32_t* tail = A32(A);
+  int32_t* edge = A32(A);
+  int32_t* ats = A32(A);
+  int32_t* run_start = A32(A + 1);
+  int32_t* run_incl = A32(A + 1);
+  if (A)
+    k_arc_fields<<<nblk(A), kT, 0, st>>>(A, directed ? 1 : 0, head, bi.Current(), eu, ev, ets,
+                                         tail, edge, ats, run_start);
+  {
+    size_t tmp = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tmp, run_start, run_incl, A, st);
+    void* t = alloc(tmp ? tmp : 8);
+    if (A) cub::DeviceScan::InclusiveSum(t, tmp, run_start, run_incl, A, st);
+    release(t);
+  }
+  int32_t R32 = 0;
+  if (A) cudaMemcpyAsync(&R32, run_incl + A - 1, 4, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  const int64_t R = R32;
+  out.R = R;
+  out.run_head = A32(R);
+  out.run_ts = A32(R);
+  if (A) k_runs<<<nblk(A), kT, 0, st>>>(A, head, ats, run_start, run_incl, out.run_head, out.run_ts);
+  out.vtx_run_off = A32(static_cast<int64_t>(n) + 1);
+  k_vtx_off<<<nblk(static_cast<int64_t>(n) + 1), kT, 0, st>>>(n, R, out.run_head, out.vtx_run_off);
+  out.arc_src = A32(A);
+  out.arc_meta = reinterpret_cast<uint32_t*>(A32(A));
+  if (A)
+    k_arc_src_meta<<<nblk(A), kT, 0, st>>>(A, head, tail, edge, ats, run_start, out.run_ts,
+                                           out.vtx_run_off, out.arc_src, out.arc_meta);
+  out.arc_tail = tail;
+
+  // ---- chunks ---------------------------------------------------------------
+  int64_t ch = A / (static_cast<int64_t>(std::max(sm_count, 1)) * 64);
+  ch = std::min<int64_t>(2048, std::max<int64_t>(64, ch));
+  const int64_t C = A ? (A + ch - 1) / ch : 0;
+  out.C = C;
+  out.chunk_arc = static_cast<int64_t*>(alloc((C + 1) * 8));
+  out.chunk_run = A32(C + 1);
+  out.chunk_carry = static_cast<uint8_t*>(alloc(std::max<int64_t>(C, 1)));
+  k_chunks<<<nblk(C + 1), kT, 0, st>>>(C, A, ch, R, run_start, run_incl, out.arc_meta,
+                                       out.chunk_arc, out.chunk_run, out.chunk_carry);
+  int32_t* cidx = A32(C);
+  int32_t* ccnt = A32(1);
+  out.carry_list = A32(C);
+  {
+    cub::CountingInputIterator<int32_t> it(0);
+    size_t tmp = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp, it, out.chunk_carry, out.carry_list, ccnt, C, st);
+    void* t = alloc(tmp ? tmp : 8);
+    if (C) cub::DeviceSelect::Flagged(t, tmp, it, out.chunk_carry, out.carry_list, ccnt, C, st);
+    release(t);
+  }
+  int32_t nc = 0;
+  if (C) cudaMemcpyAsync(&nc, ccnt, 4, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  out.ncarry = nc;
+  release(cidx);
+  release(ccnt);
+  release(edge);
+  release(ats);
+  release(run_start);
+  release(run_incl);
+  release(hd[0]);
+  release(hd[1]);
+  release(ix[0]);
+  release(ix[1]);
+}
+
+}  // namespace tsv

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 
 namespace tsv {
 
@@ -74,6 +75,41 @@ void launch_static_base(int32_t n, const uint64_t* zj, int k, uint64_t pb, uint6
                         uint64_t* out, cudaStream_t st);
 void launch_static_readout(int32_t n, const uint64_t* a, const uint64_t* b, int ppt,
                            uint64_t* acc, cudaStream_t st);
+
+// ---- on-device graph build (build_kernels.cu) ------------------------------
+
+struct BuildStatus {
+  long long first_bad_endpoint;  // smallest input index with an endpoint out of range
+  long long first_bad_ts;        // smallest input index with ts < 1
+  long long self_loops;
+  int max_ts;
+  int not_canonical;
+};
+
+struct DeviceLayout {
+  int64_t m = 0, A = 0, R = 0, C = 0;
+  int32_t ncarry = 0;
+  int64_t dropped_duplicates = 0;
+  int32_t *eu = nullptr, *ev = nullptr, *ets = nullptr;  // canonical edges
+  int32_t* arc_src = nullptr;
+  uint32_t* arc_meta = nullptr;
+  int32_t* arc_tail = nullptr;
+  int32_t *run_head = nullptr, *run_ts = nullptr, *vtx_run_off = nullptr;
+  int64_t* chunk_arc = nullptr;
+  int32_t* chunk_run = nullptr;
+  uint8_t* chunk_carry = nullptr;
+  int32_t* carry_list = nullptr;
+};
+
+// Builds the layout of layout.hpp on the device from device edge arrays.
+// canonical = the input is already canonical (validated, not re-sorted).
+// alloc/release manage device memory (stream-ordered); buffers still live at
+// return belong to `out`.  Errors are reported through *d_status.
+void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, int64_t m,
+                  int32_t n, bool directed, bool canonical, DeviceLayout& out,
+                  BuildStatus* d_status, int sm_count, cudaStream_t st,
+                  const std::function<void*(size_t)>& alloc,
+                  const std::function<void(void*)>& release);
 
 // Kernel launchers (kernels.cu).  All are asynchronous on `st`.
 void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,

@@ -141,10 +141,14 @@ void prof_end(cudaStream_t st) {
 }  // namespace tsv
 
 struct tsv_graph {
-  tsv::HostLayout host;  // canonical edges kept; run/arc vectors released
+  tsv::HostLayout host;  // n, t, directed, drop counts (+ canonical edges if host-built)
   tsv::DevGraph dev;
   int device = 0;
   int64_t device_bytes = 0;
+  int64_t m = 0;                      // canonical edge count
+  const int32_t* d_eu = nullptr;      // canonical edges on the device (device build)
+  const int32_t* d_ev = nullptr;
+  const int32_t* d_ets = nullptr;
   std::vector<void*> owned;
   ~tsv_graph() {
     int prev = 0;
@@ -324,6 +328,103 @@ void finalize_host(int32_t n, uint64_t* acc, int32_t sink, int k, tsv_outcome* o
   out->fn_bound = (2.0 * k - 1.0) / std::pow(2.0, 64);
 }
 
+// On-device build (build_kernels.cu): host edges -> HBM once, canonicalize,
+// sort and lay out on the GPU.  Every buffer still alive at the end belongs
+// to the graph.
+tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                              const int32_t* ts, bool directed, int32_t t, int device,
+                              bool canonical) {
+  DeviceGuard dg(device);
+  cudaDeviceProp prop{};
+  TSV_CUDA(cudaGetDeviceProperties(&prop, device));
+  cudaStream_t st = nullptr;
+  TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::vector<void*> live;
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+      throw CudaError("device graph build: out of device memory");
+    live.push_back(p);
+    return p;
+  };
+  auto release = [&](void* p) {
+    auto it = std::find(live.begin(), live.end(), p);
+    if (it != live.end()) live.erase(it);
+    cudaFreeAsync(p, st);
+  };
+  auto* g = new tsv_graph();
+  g->device = device;
+  g->host.n = n;
+  g->host.directed = directed;
+  try {
+    int32_t* du = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+    int32_t* dv = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+    int32_t* dts = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+    if (m) {
+      TSV_CUDA(cudaMemcpyAsync(du, u, m * 4, cudaMemcpyHostToDevice, st));
+      TSV_CUDA(cudaMemcpyAsync(dv, v, m * 4, cudaMemcpyHostToDevice, st));
+      TSV_CUDA(cudaMemcpyAsync(dts, ts, m * 4, cudaMemcpyHostToDevice, st));
+    }
+    auto* status = static_cast<tsv::BuildStatus*>(alloc(sizeof(tsv::BuildStatus)));
+    tsv::DeviceLayout L;
+    tsv::device_build(du, dv, dts, m, n, directed, canonical, L, status,
+                      prop.multiProcessorCount, st, alloc, release);
+    tsv::BuildStatus hs{};
+    TSV_CUDA(cudaMemcpyAsync(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    TSV_CUDA(cudaGetLastError());
+    release(du);
+    release(dv);
+    release(dts);
+    release(status);
+    if (hs.first_bad_endpoint != INT64_MAX || hs.first_bad_ts != INT64_MAX)
+      throw std::invalid_argument(hs.first_bad_endpoint <= hs.first_bad_ts
+                                      ? "edge endpoint out of range"
+                                      : "timestamp below 1");
+    if (hs.not_canonical) throw std::invalid_argument("edge list is not canonical");
+    if (L.m >= static_cast<int64_t>(tsv::kEdgeMask))
+      throw std::invalid_argument("edge count exceeds the engine's 2^30 edge ids");
+    const int32_t max_ts = hs.max_ts;
+    g->host.t = t > 0 ? t : std::max<int32_t>(max_ts, 1);
+    if (L.m > 0 && max_ts > g->host.t) throw std::invalid_argument("timestamp exceeds t");
+    g->host.dropped_self_loops = canonical ? 0 : hs.self_loops;
+    g->host.dropped_duplicates = L.dropped_duplicates;
+    g->m = L.m;
+    g->d_eu = L.eu;
+    g->d_ev = L.ev;
+    g->d_ets = L.ets;
+    tsv::DevGraph& d = g->dev;
+    d.n = n;
+    d.A = L.A;
+    d.R = L.R;
+    d.C = L.C;
+    d.arc_src = L.arc_src;
+    d.arc_meta = L.arc_meta;
+    d.arc_tail = L.arc_tail;
+    d.run_head = L.run_head;
+    d.run_ts = L.run_ts;
+    d.vtx_run_off = L.vtx_run_off;
+    d.chunk_arc = L.chunk_arc;
+    d.chunk_run = L.chunk_run;
+    d.chunk_carry = L.chunk_carry;
+    d.carry_list = L.carry_list;
+    d.ncarry = L.ncarry;
+    g->device_bytes = 12 * L.A + 8 * L.R + 4 * (static_cast<int64_t>(n) + 1) + 12 * L.m +
+                      17 * (L.C + 1);
+    TSV_CUDA(cudaStreamSynchronize(st));
+    g->owned = live;
+    live.clear();
+    cudaStreamDestroy(st);
+  } catch (...) {
+    for (void* p : live) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    delete g;
+    throw;
+  }
+  return g;
+}
+
 }  // namespace
 
 extern "C" {
@@ -339,6 +440,12 @@ static int graph_build_impl(int32_t n, int64_t m, const int32_t* u, const int32_
     *out = nullptr;
     if (m < 0) throw std::invalid_argument("negative edge count");
     if (m > 0 && (!u || !v || !ts)) throw std::invalid_argument("null edge arrays");
+    if (n < 0) throw std::invalid_argument("negative vertex count");
+    const char* hb = std::getenv("TSV_HOST_BUILD");
+    if (!(hb && hb[0] == '1')) {
+      *out = device_graph_build(n, m, u, v, ts, directed != 0, t, device, canonical);
+      return;
+    }
     auto* g = new tsv_graph();
     try {
       g->device = device;
@@ -346,6 +453,7 @@ static int graph_build_impl(int32_t n, int64_t m, const int32_t* u, const int32_
         tsv::adopt_canonical(n, m, u, v, ts, directed != 0, t, g->host);
       else
         tsv::canonicalize(n, m, u, v, ts, directed != 0, t, g->host);
+      g->m = static_cast<int64_t>(g->host.eu.size());
       DeviceGuard dg(device);
       cudaDeviceProp prop{};
       TSV_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -420,7 +528,7 @@ int tsv_graph_get_info(const tsv_graph* g, tsv_graph_info* out) {
     out->t = g->host.t;
     out->directed = g->host.directed ? 1 : 0;
     out->device = g->device;
-    out->m = static_cast<int64_t>(g->host.eu.size());
+    out->m = g->m;
     out->arcs = g->dev.A;
     out->runs = g->dev.R;
     out->chunks = g->dev.C;
@@ -434,7 +542,14 @@ int tsv_graph_get_info(const tsv_graph* g, tsv_graph_info* out) {
 int tsv_graph_edges(const tsv_graph* g, int32_t* u, int32_t* v, int32_t* ts) {
   return guard([&] {
     if (!g) throw std::invalid_argument("null graph");
-    const size_t m = g->host.eu.size();
+    const size_t m = static_cast<size_t>(g->m);
+    if (g->d_eu) {  // device-built: canonical edges live in HBM
+      DeviceGuard dg(g->device);
+      if (m && u) TSV_CUDA(cudaMemcpy(u, g->d_eu, m * 4, cudaMemcpyDeviceToHost));
+      if (m && v) TSV_CUDA(cudaMemcpy(v, g->d_ev, m * 4, cudaMemcpyDeviceToHost));
+      if (m && ts) TSV_CUDA(cudaMemcpy(ts, g->d_ets, m * 4, cudaMemcpyDeviceToHost));
+      return;
+    }
     if (m && u) std::memcpy(u, g->host.eu.data(), m * 4);
     if (m && v) std::memcpy(v, g->host.ev.data(), m * 4);
     if (m && ts) std::memcpy(ts, g->host.ets.data(), m * 4);

@@ -211,3 +211,39 @@ def test_device_points_api_shards_xor_to_full(cuda_device, golden):
     acc, nflag, cs = T.finalize(acc)
     assert f"{cs:016x}" == c["checksum"]
     assert [f"{int(x):016x}" for x in acc] == c["acc"]
+
+
+def test_device_build_matches_host_build(cuda_device):
+    """The on-device graph build (CUB sort + own kernels) yields the same
+    canonical edge ids, drop counts and sieve results as the host layout."""
+    import os
+    rng = np.random.default_rng(21)
+    for directed in (True, False):
+        n, m, t = 500, 6000, 30
+        u = rng.integers(0, n, m)
+        v = np.where(rng.random(m) < 0.3, 7, rng.integers(0, n, m))   # a hub + loops + dups
+        ts = rng.integers(1, t + 1, m)
+        u[:50], v[:50], ts[:50] = u[50:100], v[50:100], ts[50:100]    # duplicates
+        graphs = {}
+        for mode in ("0", "1"):
+            os.environ["TSV_HOST_BUILD"] = mode
+            try:
+                graphs[mode] = T.TemporalGraph.build(n, (u, v, ts), directed)
+            finally:
+                os.environ.pop("TSV_HOST_BUILD", None)
+        gd, gh = graphs["0"], graphs["1"]
+        for a, b in zip(gd.edges(), gh.edges()):
+            assert np.array_equal(a, b)
+        for f in ("m", "arcs", "runs", "dropped_self_loops", "dropped_duplicates", "t"):
+            assert getattr(gd.info, f) == getattr(gh.info, f), f
+        col = T.VertexColoring(rng.integers(1, 4, n), 3)
+        cfg = T.SieveConfig(seed=4)
+        sh = T.build_shades(T.MotifQuery.from_multiset([1, 2, 3, 1]), col, cfg)
+        od = T.eval_temporal_sieve(gd, 4, gd.t(), sh, cfg)
+        oh = T.eval_temporal_sieve(gh, 4, gh.t(), sh, cfg)
+        assert np.array_equal(od.accumulators, oh.accumulators) and od.checksum == oh.checksum
+        assert od.global_nonzero
+    with pytest.raises(ValueError, match="timestamp below 1"):
+        T.TemporalGraph.build(3, [(0, 1, 1), (1, 2, 0)], True)
+    g0 = T.TemporalGraph.build(4, np.zeros((0, 3), np.int64), True)
+    assert g0.m() == 0 and g0.info.arcs == 0
