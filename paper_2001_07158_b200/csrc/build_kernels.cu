@@ -205,16 +205,41 @@ __global__ void k_arc_src_meta(int64_t A, const uint32_t* __restrict__ head,
   arc_meta[j] = meta;
 }
 
-// fixed chunks of ch arcs
-__global__ void k_chunks(int64_t C, int64_t A, int64_t ch, int64_t R,
-                         const int32_t* __restrict__ run_start,
+__global__ void k_vstart_flags(int64_t A, const uint32_t* __restrict__ meta,
+                               uint8_t* __restrict__ f) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < A) f[j] = (meta[j] & kVStart) ? 1 : 0;
+}
+
+// Chunk boundary near c*ch: the next vertex start if it is within ch/2,
+// else c*ch itself (a long vertex is split; k_fixup repairs its prefix).
+// Strictly increasing in c except possibly at the final A.
+__global__ void k_chunk_bounds(int64_t C0, int64_t A, int64_t ch,
+                               const int64_t* __restrict__ vs, int64_t nv,
+                               int64_t* __restrict__ bounds) {
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (c > C0) return;
+  const int64_t t = c * ch < A ? c * ch : A;
+  if (c == C0 || t == A) {
+    bounds[c] = A;
+    return;
+  }
+  int64_t lo = 0, hi = nv;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (vs[mid] < t) lo = mid + 1;
+    else hi = mid;
+  }
+  const int64_t cand = lo < nv ? vs[lo] : A;
+  bounds[c] = (cand - t <= ch / 2) ? cand : t;
+}
+
+__global__ void k_chunks(int64_t C, int64_t R, const int64_t* __restrict__ chunk_arc,
                          const int32_t* __restrict__ run_incl, const uint32_t* __restrict__ meta,
-                         int64_t* __restrict__ chunk_arc, int32_t* __restrict__ chunk_run,
-                         uint8_t* __restrict__ chunk_carry) {
+                         int32_t* __restrict__ chunk_run, uint8_t* __restrict__ chunk_carry) {
   const int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (c > C) return;
-  const int64_t a = c * ch < A ? c * ch : A;
-  chunk_arc[c] = a;
+  const int64_t a = chunk_arc[c];
   if (c == C) {
     chunk_run[c] = static_cast<int32_t>(R);
     return;
@@ -372,13 +397,45 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
   // ---- chunks ---------------------------------------------------------------
   int64_t ch = A / (static_cast<int64_t>(std::max(sm_count, 1)) * 64);
   ch = std::min<int64_t>(2048, std::max<int64_t>(64, ch));
-  const int64_t C = A ? (A + ch - 1) / ch : 0;
+  const int64_t C0 = A ? (A + ch - 1) / ch : 0;
+  int64_t C = 0;
+  {
+    // vertex starts -> boundaries aligned to them where possible
+    uint8_t* vf = static_cast<uint8_t*>(alloc(std::max<int64_t>(A, 1)));
+    int64_t* vs = static_cast<int64_t*>(alloc(std::max<int64_t>(A, 1) * 8));
+    int64_t* cnt = static_cast<int64_t*>(alloc(8));
+    if (A) k_vstart_flags<<<nblk(A), kT, 0, st>>>(A, out.arc_meta, vf);
+    cub::CountingInputIterator<int64_t> it(0);
+    size_t tmp = 0;
+    cub::DeviceSelect::Flagged(nullptr, tmp, it, vf, vs, cnt, A, st);
+    void* t = alloc(tmp ? tmp : 8);
+    if (A) cub::DeviceSelect::Flagged(t, tmp, it, vf, vs, cnt, A, st);
+    release(t);
+    int64_t nv = 0;
+    if (A) cudaMemcpyAsync(&nv, cnt, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    int64_t* bounds = static_cast<int64_t*>(alloc((C0 + 1) * 8));
+    k_chunk_bounds<<<nblk(C0 + 1), kT, 0, st>>>(C0, A, ch, vs, nv, bounds);
+    out.chunk_arc = static_cast<int64_t*>(alloc((C0 + 1) * 8));
+    tmp = 0;
+    cub::DeviceSelect::Unique(nullptr, tmp, bounds, out.chunk_arc, cnt, C0 + 1, st);
+    t = alloc(tmp ? tmp : 8);
+    cub::DeviceSelect::Unique(t, tmp, bounds, out.chunk_arc, cnt, C0 + 1, st);
+    release(t);
+    int64_t nb = 1;
+    cudaMemcpyAsync(&nb, cnt, 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    C = A ? nb - 1 : 0;
+    release(vf);
+    release(vs);
+    release(cnt);
+    release(bounds);
+  }
   out.C = C;
-  out.chunk_arc = static_cast<int64_t*>(alloc((C + 1) * 8));
   out.chunk_run = A32(C + 1);
   out.chunk_carry = static_cast<uint8_t*>(alloc(std::max<int64_t>(C, 1)));
-  k_chunks<<<nblk(C + 1), kT, 0, st>>>(C, A, ch, R, run_start, run_incl, out.arc_meta,
-                                       out.chunk_arc, out.chunk_run, out.chunk_carry);
+  k_chunks<<<nblk(C + 1), kT, 0, st>>>(C, R, out.chunk_arc, run_incl, out.arc_meta,
+                                       out.chunk_run, out.chunk_carry);
   int32_t* cidx = A32(C);
   int32_t* ccnt = A32(1);
   out.carry_list = A32(C);

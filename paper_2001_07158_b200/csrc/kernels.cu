@@ -341,21 +341,25 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
   for (int p = 0; p < PPT; ++p) P.agg[c * W + lane + 32 * p] = U[p];
 }
 
-// Chunks that continue a long vertex receive the XOR of the preceding
-// pieces' tail aggregates, multiplied by z_head, on every run they end.
+// A chunk whose first arc continues vertex h (split across chunk
+// boundaries) computed h's prefix from zero; its runs of h receive the XOR
+// of the tail aggregates of the preceding chunks back to the one where h
+// starts, multiplied by z_h (the map U -> z*U is linear).
 __global__ void k_fixup(const LevelParams P) {
   const int W = P.b.W();
   const int32_t c = P.g.carry_list[blockIdx.x];
-  const int32_t r0 = P.g.chunk_run[c], r1 = P.g.chunk_run[c + 1];
-  if (r0 == r1) return;
+  const int32_t r0 = P.g.chunk_run[c];  // run of the chunk's first arc
+  if (r0 >= P.g.R) return;
   const int32_t head = P.g.run_head[r0];
+  const int32_t r1 = min(P.g.chunk_run[c + 1], P.g.vtx_run_off[head + 1]);
+  if (r0 >= r1) return;  // no run of h ends in this chunk
   for (int w = threadIdx.x; w < W; w += blockDim.x) {
     const uint64_t A = P.b.pb + static_cast<uint64_t>(w);
     if (A >= P.b.pe) continue;
     uint64_t carry = 0;
     for (int64_t cc = c - 1;; --cc) {
       carry ^= P.agg[cc * W + w];
-      if (!P.g.chunk_carry[cc]) break;
+      if (!P.g.chunk_carry[cc] || P.g.run_head[P.g.chunk_run[cc]] != head) break;
     }
     const uint64_t t = gf_mul(z_single(P.zj, P.k, head, A), carry);
     for (int32_t r = r0; r < r1; ++r) P.s_cur[static_cast<int64_t>(r) * W + w] ^= t;
