@@ -229,7 +229,7 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
   if (cfg->points_per_batch == 0) {
     size_t free_b = 0, total_b = 0;
     TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    const uint64_t budget = static_cast<uint64_t>(free_b * 0.85) / 8;
+    const uint64_t budget = static_cast<uint64_t>(free_b * 0.92) / 8;
     while (W > 1 && (words(W) > cfg->memory_cap_words || words(W) > budget)) W >>= 1;
   }
   *peak_words = words(W);
@@ -390,9 +390,23 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     g->host.dropped_self_loops = canonical ? 0 : hs.self_loops;
     g->host.dropped_duplicates = L.dropped_duplicates;
     g->m = L.m;
-    g->d_eu = L.eu;
-    g->d_ev = L.ev;
-    g->d_ets = L.ets;
+    if (L.m > (int64_t{1} << 26)) {
+      // large graphs: the canonical edge list is only needed on demand
+      // (tsv_graph_edges); keep it in host memory, not in HBM
+      g->host.eu.resize(L.m);
+      g->host.ev.resize(L.m);
+      g->host.ets.resize(L.m);
+      TSV_CUDA(cudaMemcpyAsync(g->host.eu.data(), L.eu, L.m * 4, cudaMemcpyDeviceToHost, st));
+      TSV_CUDA(cudaMemcpyAsync(g->host.ev.data(), L.ev, L.m * 4, cudaMemcpyDeviceToHost, st));
+      TSV_CUDA(cudaMemcpyAsync(g->host.ets.data(), L.ets, L.m * 4, cudaMemcpyDeviceToHost, st));
+      release(L.eu);
+      release(L.ev);
+      release(L.ets);
+    } else {
+      g->d_eu = L.eu;
+      g->d_ev = L.ev;
+      g->d_ets = L.ets;
+    }
     tsv::DevGraph& d = g->dev;
     d.n = n;
     d.A = L.A;
