@@ -126,7 +126,11 @@ def cpu_sample(inst, k, colors, motif, anchor, seed=1, frac=0.1, threads=None):
                        max_ts=max_ts, seed=seed, lanes=8, threads=threads, anchor=anchor,
                        t=inst.t, repeats=2)
         return upd / r["seconds"], r["seconds"], sample, "reference", threads
-    cu, cv, ct = O.canonical_edges(inst.n, inst.u, inst.v, inst.ts, inst.directed)
+    # port: the time-prefix subgraph itself, bounded to ~2e6 arcs
+    max_ts = max(1, min(max_ts, int(inst.t * 2e6 / max(arcs / max(frac, 1e-9), 1))))
+    sel = inst.ts <= max_ts
+    arcs = int(np.count_nonzero(sel)) * (1 if inst.directed else 2)
+    cu, cv, ct = O.canonical_edges(inst.n, inst.u[sel], inst.v[sel], inst.ts[sel], inst.directed)
     from paper_2001_07158_b200.sieve import SieveConfig, build_shades
     from paper_2001_07158_b200.graph import MotifQuery, VertexColoring
     sh = build_shades(MotifQuery.from_multiset(motif), VertexColoring(colors, int(colors.max())),

@@ -89,9 +89,10 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
   const int64_t a0 = P.g.chunk_arc[c], a1 = P.g.chunk_arc[c + 1];
   int32_t run_ctr = P.g.chunk_run[c];
   const int last_lane = (G - 1) * LANES + li;
-  uint64_t carry[PPT];
+  uint64_t carry[PPT], zc[PPT];
 #pragma unroll
-  for (int p = 0; p < PPT; ++p) carry[p] = 0;
+  for (int p = 0; p < PPT; ++p) carry[p] = zc[p] = 0;
+  int32_t zhead = -1;  // z_head^A cached per group across its consecutive runs
 
   for (int64_t base = a0; base < a1; base += 32) {
     const int nb = static_cast<int>(a1 - base < 32 ? a1 - base : 32);
@@ -169,12 +170,14 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
         if (act && (mt & kRunEnd)) {
           const int32_t run = s_run[wib][i];
           const int32_t head = __ldg(P.g.run_head + run);
-          uint64_t z[PPT];
-          z_of<PPT>(P.zj, P.k, head, pt, pv, z);
+          if (head != zhead) {
+            z_of<PPT>(P.zj, P.k, head, pt, pv, zc);
+            zhead = head;
+          }
 #pragma unroll
           for (int p = 0; p < PPT; ++p)
             P.s_cur[static_cast<int64_t>(run) * W + li + LANES * p] =
-                gf_mul(z[p], v[p]);
+                gf_mul(zc[p], v[p]);
         }
 #pragma unroll
         for (int p = 0; p < PPT; ++p)
