@@ -60,13 +60,11 @@ __device__ __forceinline__ uint64_t z_single(const uint64_t* __restrict__ zj,
 }
 
 template <int LANES, int PPT, bool FIRST>
-__global__ void __launch_bounds__(kWarpsPerBlock * 32)
+__global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     k_level(const LevelParams P) {
   constexpr int G = 32 / LANES;
   constexpr int W = LANES * PPT;
-  constexpr int STEPS = 32 / G;  // steps per 32-arc batch
-  constexpr int UNR = (8 / PPT) < STEPS ? (8 / PPT) : STEPS;
-  __shared__ uint64_t s_y[kWarpsPerBlock][32];
+  __shared__ uint32_t s_ys[kWarpsPerBlock][12][32];  // Karatsuba split of each arc's y
   __shared__ int32_t s_src[kWarpsPerBlock][32];
   __shared__ uint32_t s_meta[kWarpsPerBlock][32];
   __shared__ int32_t s_run[kWarpsPerBlock][32];
@@ -106,50 +104,65 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32)
       y = draw_edge_y(pre, yb, meta & kEdgeMask);
     }
     const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
-    s_y[wib][lane] = y;
+    {
+      const KSplit ks = ksplit(y);  // once per arc, not once per lane of its group
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s_ys[wib][j][lane] = ks.l.c[j];
+        s_ys[wib][4 + j][lane] = ks.h.c[j];
+        s_ys[wib][8 + j][lane] = ks.m.c[j];
+      }
+    }
     s_src[wib][lane] = sidx;
     s_meta[wib][lane] = meta;
     s_run[wib][lane] = run_ctr + __popc(ends & ((1u << lane) - 1u));
     run_ctr += __popc(ends);
     __syncwarp();
 
-    for (int s0 = 0; s0 < STEPS; s0 += UNR) {
-      uint64_t val[UNR][PPT];
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int i = (s0 + u) * G + g;
-        if (FIRST) {
-          if (i < nb) {
-            const int32_t tail = s_src[wib][i];
-            if (P.anchor_source >= 0 && tail != P.anchor_source) {
-#pragma unroll
-              for (int p = 0; p < PPT; ++p) val[u][p] = 0;
-            } else {
-              z_of<PPT>(P.zj, P.k, tail, pt, pv, val[u]);
-            }
-          } else {
-#pragma unroll
-            for (int p = 0; p < PPT; ++p) val[u][p] = 0;
-          }
+    // one step = G arcs (one per group); the next step's gathers are in
+    // flight during this one; the loop stays rolled to keep the I-cache warm
+    auto fetch = [&](int i, uint64_t (&out)[PPT]) {
+      if (FIRST) {
+        const int32_t tail = i < nb ? s_src[wib][i] : -1;
+        if (tail >= 0 && (P.anchor_source < 0 || tail == P.anchor_source)) {
+          z_of<PPT>(P.zj, P.k, tail, pt, pv, out);
         } else {
-          const int32_t src = i < nb ? s_src[wib][i] : -1;
 #pragma unroll
-          for (int p = 0; p < PPT; ++p)
-            val[u][p] = src >= 0
-                            ? __ldg(P.s_prev + static_cast<int64_t>(src) * W +
-                                    li + LANES * p)
-                            : 0ull;
+          for (int p = 0; p < PPT; ++p) out[p] = 0;
         }
-      }
+      } else {
+        const int32_t src = i < nb ? s_src[wib][i] : -1;
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int i = (s0 + u) * G + g;
+        for (int p = 0; p < PPT; ++p)
+          out[p] = src >= 0 ? __ldg(P.s_prev + static_cast<int64_t>(src) * W + li + LANES * p)
+                            : 0ull;
+      }
+    };
+    uint64_t nxt[PPT];
+    fetch(g, nxt);
+    const int steps = (nb + G - 1) / G;
+#pragma unroll 1
+    for (int s = 0; s < steps; ++s) {
+      uint64_t val[1][PPT];
+      const int u = 0;
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) val[0][p] = nxt[p];
+      if (s + 1 < steps) fetch((s + 1) * G + g, nxt);
+      {
+        const int i = s * G + g;
         const bool act = i < nb;
         const uint32_t mt = act ? s_meta[wib][i] : 0u;
-        const uint64_t yy = act ? s_y[wib][i] : 0ull;
+        const int ia = act ? i : 0;
+        KSplit ys;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          ys.l.c[j] = act ? s_ys[wib][j][ia] : 0u;
+          ys.h.c[j] = act ? s_ys[wib][4 + j][ia] : 0u;
+          ys.m.c[j] = act ? s_ys[wib][8 + j][ia] : 0u;
+        }
         uint64_t v[PPT];
 #pragma unroll
-        for (int p = 0; p < PPT; ++p) v[p] = gf_mul(yy, val[u][p]);
+        for (int p = 0; p < PPT; ++p) v[p] = gf_mul_presplit(ys, val[u][p]);
         bool f = (mt & kVStart) != 0;
         if (G > 1) {
 #pragma unroll

@@ -107,11 +107,28 @@ struct DevBuf {
   }
 };
 
+// The state buffers (2*R*W words, up to ~130 GB at 1e9 edges) are stream-
+// ordered allocations; keep freed pool memory mapped so repeated
+// evaluations (probes, repetitions, steps) do not re-map it every time.
+void keep_pool_memory(int dev) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done.push_back(dev);
+}
+
 struct DeviceGuard {
   int prev = 0;
   explicit DeviceGuard(int dev) {
     TSV_CUDA(cudaGetDevice(&prev));
     if (prev != dev) TSV_CUDA(cudaSetDevice(dev));
+    keep_pool_memory(dev);
   }
   ~DeviceGuard() { cudaSetDevice(prev); }
 };
@@ -229,6 +246,15 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
   if (cfg->points_per_batch == 0) {
     size_t free_b = 0, total_b = 0;
     TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    int dev = 0;
+    cudaMemPool_t pool = nullptr;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t reserved = 0, used = 0;  // freed pool memory is reusable
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+      if (reserved > used) free_b += reserved - used;
+    }
     const uint64_t budget = static_cast<uint64_t>(free_b * 0.92) / 8;
     while (W > 1 && (words(W) > cfg->memory_cap_words || words(W) > budget)) W >>= 1;
   }
