@@ -37,6 +37,7 @@ struct Batch {
 struct LevelParams {
   DevGraph g;
   const uint64_t* zj = nullptr;  // n x k
+  const uint64_t* zb = nullptr;  // n x W: z_u^A of the batch (wide kernel, optional)
   int k = 0;
   int ell = 2;                   // level being produced
   uint64_t seed = 1;
@@ -117,6 +118,8 @@ void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
                cudaStream_t st);
 void launch_level(const LevelParams& p, cudaStream_t st);
 void launch_fixup(const LevelParams& p, cudaStream_t st);
+void launch_zbatch(int32_t n, const uint64_t* zj, int k, const Batch& b, uint64_t* zb,
+                   cudaStream_t st);
 void launch_readout(const DevGraph& g, int32_t max_ts, const uint64_t* s,
                     int W, uint64_t* acc, cudaStream_t st);
 void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,

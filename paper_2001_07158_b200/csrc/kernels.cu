@@ -215,7 +215,13 @@ __device__ __forceinline__ void fetch_src(const LevelParams& P, int32_t src,
   const int lane = threadIdx.x & 31;
   if (FIRST) {
     if (src >= 0 && (P.anchor_source < 0 || src == P.anchor_source)) {
-      z_of<PPT>(P.zj, P.k, src, pt, pv, out);
+      if (P.zb) {  // batch z table materialized: one coalesced row per tail
+#pragma unroll
+        for (int p = 0; p < PPT; ++p)
+          out[p] = __ldg(P.zb + static_cast<int64_t>(src) * (32 * PPT) + lane + 32 * p);
+      } else {
+        z_of<PPT>(P.zj, P.k, src, pt, pv, out);
+      }
     } else {
 #pragma unroll
       for (int p = 0; p < PPT; ++p) out[p] = 0;
@@ -382,6 +388,19 @@ __global__ void k_fixup(const LevelParams P) {
   }
 }
 
+// zb[u][w] = z_u^{pb+w} for one batch (a warp per vertex row, W = 32*ppt)
+__global__ void k_zbatch(int32_t n, const uint64_t* __restrict__ zj, int k, Batch b,
+                         uint64_t* __restrict__ zb) {
+  const int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (u >= n) return;
+  const int lane = threadIdx.x & 31;
+  const int W = b.W();
+  for (int w = lane; w < W; w += 32) {
+    const uint64_t A = b.pb + static_cast<uint64_t>(w);
+    zb[u * W + w] = A < b.pe ? z_single(zj, k, static_cast<int32_t>(u), A) : 0ull;
+  }
+}
+
 // acc[u] ^= XOR_w S_k[last run of u with ts <= max_ts][w]  (sieve.cpp:297-303)
 __global__ void k_readout(const DevGraph g, int32_t max_ts,
                           const uint64_t* __restrict__ s, int W,
@@ -501,6 +520,15 @@ void launch_fixup(const LevelParams& p, cudaStream_t st) {
   prof_begin("fixup", st);
   const int threads = p.b.W() < 128 ? ((p.b.W() + 31) / 32) * 32 : 128;
   k_fixup<<<p.g.ncarry, threads, 0, st>>>(p);
+  prof_end(st);
+}
+
+void launch_zbatch(int32_t n, const uint64_t* zj, int k, const Batch& b, uint64_t* zb,
+                   cudaStream_t st) {
+  if (n == 0) return;
+  prof_begin("zbatch", st);
+  k_zbatch<<<static_cast<unsigned>((static_cast<int64_t>(n) * 32 + 255) / 256), 256, 0, st>>>(
+      n, zj, k, b, zb);
   prof_end(st);
 }
 

@@ -313,10 +313,21 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   lp.agg = agg.as<uint64_t>();
   if (const char* e = std::getenv("TSV_YMUL"))
     lp.ymul = std::strcmp(e, "holes") == 0 ? 1 : std::strcmp(e, "grouped") == 0 ? 2 : 0;
+  // The wide kernel's level-2 base case reads z_tail^A for every arc: when
+  // the per-batch table z[u][w] is small next to the state (n*W <= R*W/8,
+  // <= 4 GB) it is materialized once per batch and gathered like a state row.
+  const uint64_t zb_bytes = static_cast<uint64_t>(n) * W * 8;
+  const bool use_zb = W >= 32 && lp.ymul != 2 && zb_bytes <= (4ull << 30) &&
+                      static_cast<uint64_t>(n) * 8 <= static_cast<uint64_t>(g->dev.R);
+  DevBuf zb(use_zb ? zb_bytes : 8, st);
   for (uint64_t pb = p_begin; pb < p_end; pb += W) {
     lp.b = batch_shape(W);
     lp.b.pb = pb;
     lp.b.pe = std::min(p_end, pb + static_cast<uint64_t>(W));
+    if (use_zb) {
+      tsv::launch_zbatch(n, d_zj.as<uint64_t>(), k, lp.b, zb.as<uint64_t>(), st);
+      lp.zb = zb.as<uint64_t>();
+    }
     uint64_t* cur = s0.as<uint64_t>();
     uint64_t* prev = s1.as<uint64_t>();
     for (int ell = 2; ell <= k; ++ell) {
