@@ -71,6 +71,14 @@ int64_t tsv_canonical_edges(int32_t n, int64_t m, const int32_t* u,
                             const int32_t* v, const int32_t* ts, int directed,
                             int32_t* out_u, int32_t* out_v, int32_t* out_ts);
 
+/* Induced subgraph on the device (restrict_to, graph.cpp:483-494): edges with
+ * ts <= max_ts whose endpoints are both kept (keep_vertex: n host bytes);
+ * kept edges keep their relative order, so the rebuild's edge ids are their
+ * ranks, exactly as the reference renumbers.  t = min(max_ts, t).  Used by
+ * the self-reduction extraction probes. */
+int tsv_graph_restrict(const tsv_graph* g, const uint8_t* keep_vertex,
+                       int32_t max_ts, tsv_graph** out);
+
 void tsv_graph_free(tsv_graph* g);
 int tsv_graph_get_info(const tsv_graph* g, tsv_graph_info* out);
 

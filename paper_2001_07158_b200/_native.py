@@ -63,6 +63,8 @@ def lib():
     L.tsv_canonical_edges.restype = C.c_int64
     L.tsv_canonical_edges.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_int,
                                       _i32p, _i32p, _i32p]
+    L.tsv_graph_restrict.argtypes = [vp, np.ctypeslib.ndpointer(np.uint8, flags="C_CONTIGUOUS"),
+                                     C.c_int32, C.POINTER(vp)]
     L.tsv_graph_free.argtypes = [vp]
     L.tsv_graph_free.restype = None
     L.tsv_graph_get_info.argtypes = [vp, C.POINTER(GraphInfo)]

@@ -16,6 +16,8 @@
 #include <map>
 #include <stdexcept>
 
+#include "tsv.h"
+
 namespace tsieve {
 
 namespace {
@@ -305,14 +307,38 @@ std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
   for (Vertex x = 0; x < p.graph.n(); ++x)
     if (keep[x]) cand.push_back(x);
 
+  // Each deletion probe restricts the graph ON THE DEVICE (order-preserving
+  // filter + rebuild, tsv_graph_restrict) and evaluates there; no host graph
+  // is rebuilt per probe.
+  const tsv_graph* base = p.graph.device_graph(p.cfg.device);
+  tsv_config cfg{};
+  cfg.seed = p.cfg.seed;
+  cfg.field_bits = p.cfg.field_bits;
+  cfg.lane_width = p.cfg.lane_width;
+  cfg.memory_cap_words = p.cfg.memory_cap_words;
+  std::vector<std::uint8_t> mask8(static_cast<size_t>(p.graph.n()));
+  std::vector<std::uint64_t> acc(static_cast<size_t>(p.graph.n()) + 1);
+  static const std::int32_t kNoShade = 0;
   auto still_yes_without = [&](const std::vector<Vertex>& block) {
-    std::vector<bool> mask = keep;
-    for (Vertex x : block) mask[x] = false;
-    const TemporalGraph sub = restrict_to(p.graph, mask, horizon);
-    const SieveOutcome o = probe(p, sub, horizon);
+    for (Vertex x = 0; x < p.graph.n(); ++x) mask8[x] = keep[x] ? 1 : 0;
+    for (Vertex x : block) mask8[x] = 0;
+    tsv_graph* sub = nullptr;
+    if (tsv_graph_restrict(base, mask8.data(), horizon, &sub) != TSV_OK)
+      throw std::runtime_error(tsv_last_error());
+    tsv_outcome o{};
+    const int rc = tsv_eval_temporal_sieve(
+        sub, p.k, horizon, p.shades.vertex_off.data(),
+        p.shades.vertex_shades.empty() ? &kNoShade : p.shades.vertex_shades.data(), &cfg,
+        p.anchor.source, p.anchor.sink, acc.data(), &o);
+    tsv_graph_free(sub);
+    if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
+    if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
     ++calls;
     peak = std::max(peak, o.peak_field_words);
-    return o.global_nonzero;
+    if (p.cfg.localize) return o.global_nonzero != 0;
+    std::uint64_t total = 0;
+    for (Vertex x = 0; x < p.graph.n(); ++x) total ^= acc[x];
+    return total != 0;
   };
 
   std::deque<std::vector<Vertex>> work{cand};

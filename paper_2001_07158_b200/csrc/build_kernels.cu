@@ -250,7 +250,39 @@ __global__ void k_chunks(int64_t C, int64_t R, const int64_t* __restrict__ chunk
   chunk_carry[c] = (meta[a] & kVStart) ? 0 : 1;
 }
 
+__global__ void k_restrict_flags(int64_t m, const int32_t* __restrict__ eu,
+                                 const int32_t* __restrict__ ev, const int32_t* __restrict__ ets,
+                                 const uint8_t* __restrict__ keep, int32_t max_ts,
+                                 uint8_t* __restrict__ f) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) f[i] = (ets[i] <= max_ts && keep[eu[i]] && keep[ev[i]]) ? 1 : 0;
+}
+
 }  // namespace
+
+int64_t device_restrict(const int32_t* eu, const int32_t* ev, const int32_t* ets, int64_t m,
+                        const uint8_t* d_keep, int32_t max_ts, int32_t* ou, int32_t* ov,
+                        int32_t* ots, cudaStream_t st,
+                        const std::function<void*(size_t)>& alloc,
+                        const std::function<void(void*)>& release) {
+  if (m == 0) return 0;
+  uint8_t* f = static_cast<uint8_t*>(alloc(m));
+  int64_t* cnt = static_cast<int64_t*>(alloc(8));
+  k_restrict_flags<<<nblk(m), kT, 0, st>>>(m, eu, ev, ets, d_keep, max_ts, f);
+  size_t tmp = 0;
+  cub::DeviceSelect::Flagged(nullptr, tmp, eu, f, ou, cnt, m, st);
+  void* t = alloc(tmp ? tmp : 8);
+  cub::DeviceSelect::Flagged(t, tmp, eu, f, ou, cnt, m, st);
+  cub::DeviceSelect::Flagged(t, tmp, ev, f, ov, cnt, m, st);
+  cub::DeviceSelect::Flagged(t, tmp, ets, f, ots, cnt, m, st);
+  int64_t kept = 0;
+  cudaMemcpyAsync(&kept, cnt, 8, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  release(t);
+  release(cnt);
+  release(f);
+  return kept;
+}
 
 // Stable radix sort of (key, value) pairs with CUB; keys/values are swapped
 // into the DoubleBuffer's current buffers.

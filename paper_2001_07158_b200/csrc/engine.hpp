@@ -112,6 +112,14 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
                   const std::function<void*(size_t)>& alloc,
                   const std::function<void(void*)>& release);
 
+// Order-preserving filter of a canonical edge list (restrict_to): keeps
+// edges with ts <= max_ts and both endpoints kept; returns the kept count.
+int64_t device_restrict(const int32_t* eu, const int32_t* ev, const int32_t* ets, int64_t m,
+                        const uint8_t* d_keep, int32_t max_ts, int32_t* ou, int32_t* ov,
+                        int32_t* ots, cudaStream_t st,
+                        const std::function<void*(size_t)>& alloc,
+                        const std::function<void(void*)>& release);
+
 // Kernel launchers (kernels.cu).  All are asynchronous on `st`.
 void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
                const int32_t* vertex_shades, const uint64_t* wtab, uint64_t* zj,

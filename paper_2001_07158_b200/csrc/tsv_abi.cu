@@ -370,7 +370,8 @@ void finalize_host(int32_t n, uint64_t* acc, int32_t sink, int k, tsv_outcome* o
 // to the graph.
 tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                               const int32_t* ts, bool directed, int32_t t, int device,
-                              bool canonical) {
+                              bool canonical, bool on_device = false) {
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   DeviceGuard dg(device);
   cudaDeviceProp prop{};
   TSV_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -398,9 +399,9 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     int32_t* dv = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
     int32_t* dts = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
     if (m) {
-      TSV_CUDA(cudaMemcpyAsync(du, u, m * 4, cudaMemcpyHostToDevice, st));
-      TSV_CUDA(cudaMemcpyAsync(dv, v, m * 4, cudaMemcpyHostToDevice, st));
-      TSV_CUDA(cudaMemcpyAsync(dts, ts, m * 4, cudaMemcpyHostToDevice, st));
+      TSV_CUDA(cudaMemcpyAsync(du, u, m * 4, kind, st));
+      TSV_CUDA(cudaMemcpyAsync(dv, v, m * 4, kind, st));
+      TSV_CUDA(cudaMemcpyAsync(dts, ts, m * 4, kind, st));
     }
     auto* status = static_cast<tsv::BuildStatus*>(alloc(sizeof(tsv::BuildStatus)));
     tsv::DeviceLayout L;
@@ -568,6 +569,68 @@ int64_t tsv_canonical_edges(int32_t n, int64_t m, const int32_t* u, const int32_
     }
   });
   return rc == TSV_OK ? kept : -1;
+}
+
+int tsv_graph_restrict(const tsv_graph* g, const uint8_t* keep_vertex, int32_t max_ts,
+                       tsv_graph** out) {
+  return guard([&] {
+    if (!g || !out || (g->host.n > 0 && !keep_vertex))
+      throw std::invalid_argument("null argument");
+    *out = nullptr;
+    DeviceGuard dg(g->device);
+    cudaStream_t st = nullptr;
+    TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    std::vector<void*> tmp;
+    auto alloc = [&](size_t bytes) -> void* {
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+        throw CudaError("restrict: out of device memory");
+      tmp.push_back(p);
+      return p;
+    };
+    auto release = [&](void* p) {
+      auto it = std::find(tmp.begin(), tmp.end(), p);
+      if (it != tmp.end()) tmp.erase(it);
+      cudaFreeAsync(p, st);
+    };
+    try {
+      const int32_t n = g->host.n;
+      const int64_t m = g->m;
+      auto* keep = static_cast<uint8_t*>(alloc(std::max<int64_t>(n, 1)));
+      if (n) TSV_CUDA(cudaMemcpyAsync(keep, keep_vertex, n, cudaMemcpyHostToDevice, st));
+      const int32_t *eu = g->d_eu, *ev = g->d_ev, *ets = g->d_ets;
+      if (!eu) {  // canonical edges held on the host: stage them
+        auto* a = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        auto* b = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        auto* c = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        if (m) {
+          TSV_CUDA(cudaMemcpyAsync(a, g->host.eu.data(), m * 4, cudaMemcpyHostToDevice, st));
+          TSV_CUDA(cudaMemcpyAsync(b, g->host.ev.data(), m * 4, cudaMemcpyHostToDevice, st));
+          TSV_CUDA(cudaMemcpyAsync(c, g->host.ets.data(), m * 4, cudaMemcpyHostToDevice, st));
+        }
+        eu = a;
+        ev = b;
+        ets = c;
+      }
+      auto* ou = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      auto* ov = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      auto* ots = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      const int64_t kept =
+          tsv::device_restrict(eu, ev, ets, m, keep, max_ts, ou, ov, ots, st, alloc, release);
+      const int32_t t_new = std::min(max_ts, g->host.t);
+      TSV_CUDA(cudaStreamSynchronize(st));
+      *out = device_graph_build(n, kept, ou, ov, ots, g->host.directed, t_new, g->device,
+                                /*canonical=*/true, /*on_device=*/true);
+    } catch (...) {
+      for (void* p : tmp) cudaFreeAsync(p, st);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+      throw;
+    }
+    for (void* p : tmp) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  });
 }
 
 void tsv_graph_free(tsv_graph* g) { delete g; }

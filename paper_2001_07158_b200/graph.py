@@ -249,12 +249,19 @@ def restrict_to(g: TemporalGraph, keep_vertex, max_ts: int, device: int | None =
                 ) -> TemporalGraph:
     """Induced subgraph with ts <= max_ts (graph.cpp:483-494): kept edges keep
     their relative order, so the rebuild renumbers edge id = rank among them."""
+    keep = np.ascontiguousarray(np.asarray(keep_vertex, dtype=bool).astype(np.uint8))
+    if device is None or device == g.info.device:
+        # order-preserving filter + rebuild on the graph's device
+        h = C.c_void_p()
+        _native.check(_native.lib().tsv_graph_restrict(
+            g.handle, keep if len(keep) else np.zeros(1, np.uint8), int(max_ts), C.byref(h)))
+        info = _native.GraphInfo()
+        _native.check(_native.lib().tsv_graph_get_info(h, C.byref(info)))
+        return TemporalGraph(h, info)
     u, v, ts = g.edges()
-    keep = np.asarray(keep_vertex, dtype=bool)
-    sel = (ts <= max_ts) & keep[u] & keep[v]
+    sel = (ts <= max_ts) & keep.astype(bool)[u] & keep.astype(bool)[v]
     return TemporalGraph.build(g.n(), (u[sel], v[sel], ts[sel]), g.directed(),
-                               min(int(max_ts), g.t()),
-                               g.info.device if device is None else device)
+                               min(int(max_ts), g.t()), device)
 
 
 def save_graph(g: TemporalGraph) -> str:

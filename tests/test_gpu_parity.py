@@ -247,3 +247,30 @@ def test_device_build_matches_host_build(cuda_device):
         T.TemporalGraph.build(3, [(0, 1, 1), (1, 2, 0)], True)
     g0 = T.TemporalGraph.build(4, np.zeros((0, 3), np.int64), True)
     assert g0.m() == 0 and g0.info.arcs == 0
+
+
+def test_device_restrict_matches_reference_renumbering(cuda_device):
+    """tsv_graph_restrict (device, order-preserving) equals rebuilding the
+    kept edges from scratch (restrict_to, graph.cpp:483-494), and the sieve on
+    it equals the oracle on the restricted edge list."""
+    rng = np.random.default_rng(33)
+    for directed in (True, False):
+        n, m, t = 80, 900, 12
+        u, v, ts = rng.integers(0, n, m), rng.integers(0, n, m), rng.integers(1, t + 1, m)
+        g = T.TemporalGraph.build(n, (u, v, ts), directed)
+        keep = rng.random(n) < 0.7
+        for max_ts in (t, 7):
+            r = T.restrict_to(g, keep, max_ts)
+            cu, cv, ct = g.edges()
+            sel = (ct <= max_ts) & keep[cu] & keep[cv]
+            ref = T.TemporalGraph.build(n, (cu[sel], cv[sel], ct[sel]), directed, min(max_ts, g.t()))
+            for a, b in zip(r.edges(), ref.edges()):
+                assert np.array_equal(a, b)
+            assert r.t() == ref.t() and r.info.runs == ref.info.runs
+            col = T.VertexColoring(rng.integers(1, 3, n), 2)
+            cfg = T.SieveConfig(seed=9)
+            sh = T.build_shades(T.MotifQuery.from_multiset([1, 2, 1]), col, cfg)
+            o1 = T.eval_temporal_sieve(r, 3, r.t(), sh, cfg)
+            acc, nf, cs = O.oracle_eval(n, *r.edges(), directed, 3, r.t(), sh.vertex_off,
+                                        sh.vertex_shades, 9)
+            assert np.array_equal(o1.accumulators, acc) and o1.checksum == cs
