@@ -22,6 +22,7 @@ __device__ __forceinline__ uint64_t mul_v(uint64_t a, uint64_t b) {
   if (V == 1) return gf_mul_serial(a, b);
   if (V == 2) return gf_mul_kara(a, b);
   if (V == 3) return gf_mul_school(a, b);
+  if (V == 9) return gf_mul_p5(a, b);
   return gf_mul(a, b);
 }
 
@@ -30,7 +31,7 @@ __global__ void k_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64
   __shared__ __align__(256) uint64_t tabs[8][256];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (variant >= 4) {
+  if (variant >= 4 && variant <= 6) {
     // products by a warp-uniform multiplier: every lane multiplies a[i] by
     // each of the warp's 32 b values in turn and keeps the one of its own
     // index, so all 32 tables are exercised.
@@ -54,6 +55,7 @@ __global__ void k_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64
     case 1: out[i] = mul_v<1>(a[i], b[i]); break;
     case 2: out[i] = mul_v<2>(a[i], b[i]); break;
     case 3: out[i] = mul_v<3>(a[i], b[i]); break;
+    case 9: out[i] = mul_v<9>(a[i], b[i]); break;
     default: out[i] = mul_v<0>(a[i], b[i]); break;
   }
 }
@@ -98,6 +100,32 @@ __global__ void k_gf_bench_table(int64_t iters, uint64_t* sink) {
   sink[tid] = x;
 }
 
+// Pipe probes: 8 independent mul.wide.u32 (V=7) or 3-input XORs (V=8) per
+// iteration and thread, to calibrate the instruction costs of the variants.
+template <int V>
+__global__ void k_pipe_probe(int64_t iters, uint64_t* sink) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t a[8], b = tid * 0x9e3779b9u + 1;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = tid * (j + 3) + 7;
+  uint64_t acc = 0;
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (V == 7) {
+        const uint64_t p = wmul(a[j], b);
+        a[j] = static_cast<uint32_t>(p >> 32) ^ static_cast<uint32_t>(p);
+      } else {
+        a[j] = a[j] ^ b ^ a[(j + 1) & 7];
+      }
+    }
+    b += 0x7f4a7c15u;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc ^= a[j];
+  sink[tid] = acc;
+}
+
 }  // namespace
 
 void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
@@ -119,6 +147,9 @@ double launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks, i
     case 4: k_gf_bench_table<1><<<blocks, threads, 0, st>>>(iters, sink); return 1.0 * iters * lanes;
     case 5: k_gf_bench_table<2><<<blocks, threads, 0, st>>>(iters, sink); return 2.0 * iters * lanes;
     case 6: k_gf_bench_table<4><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
+    case 7: k_pipe_probe<7><<<blocks, threads, 0, st>>>(iters, sink); return 8.0 * iters * lanes;
+    case 8: k_pipe_probe<8><<<blocks, threads, 0, st>>>(iters, sink); return 8.0 * iters * lanes;
+    case 9: k_gf_bench<9><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
     default: k_gf_bench<0><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
   }
 }

@@ -128,6 +128,64 @@ __device__ __forceinline__ u128 clmul64_school(uint64_t a, uint64_t b) {
   return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
 }
 
+// ---- period-5 holes: class sums accumulate inside the multiplier ----------
+//
+// With operands masked to every 5th bit, a 32x32 product has at most
+// min(p+1, 63-p) <= 31 one-bit products at position p once all 5 products of
+// an output class are SUMMED, which fits the 5-bit field: the class sum is
+// one chain of mul.wide with accumulate (no XORs).  The single exception is
+// p = 31 with x = y = 0xffffffff (32 products): its field wraps to 0 (right
+// parity) and carries one unit into p = 36, which the correction undoes.
+
+__device__ __forceinline__ uint64_t wmad(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return r;
+}
+
+struct Split5 {
+  uint32_t c[5];
+};
+
+__device__ __forceinline__ Split5 split5(uint32_t a) {
+  return {{a & 0x42108421u, a & 0x84210842u, a & 0x08421084u, a & 0x10842108u,
+           a & 0x21084210u}};
+}
+
+// 32x32 -> 64 carry-less product (masked), period-5 holes.
+__device__ __forceinline__ uint64_t clmul32_p5(const Split5& x, const Split5& y, bool full) {
+  uint64_t c[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    uint64_t s = wmul(x.c[0], y.c[r]);
+#pragma unroll
+    for (int i = 1; i < 5; ++i) s = wmad(x.c[i], y.c[(r - i + 5) % 5], s);
+    c[r] = s;
+  }
+  if (full) c[1] ^= 1ull << 36;
+  return (c[0] & 0x1084210842108421ull) | (c[1] & 0x2108421084210842ull) |
+         (c[2] & 0x4210842108421084ull) | (c[3] & 0x8421084210842108ull) |
+         (c[4] & 0x0842108421084210ull);
+}
+
+struct KSplit5 {
+  Split5 l, h, m;
+  bool fl, fh, fm;  // operand half is all ones
+};
+
+__device__ __forceinline__ KSplit5 ksplit5(uint64_t a) {
+  const uint32_t l = lo32(a), h = hi32(a), m = l ^ h;
+  return {split5(l), split5(h), split5(m), l == 0xffffffffu, h == 0xffffffffu,
+          m == 0xffffffffu};
+}
+
+__device__ __forceinline__ u128 clmul64_p5(const KSplit5& A, const KSplit5& B) {
+  const uint64_t L = clmul32_p5(A.l, B.l, A.fl && B.fl);
+  const uint64_t H = clmul32_p5(A.h, B.h, A.fh && B.fh);
+  const uint64_t M = clmul32_p5(A.m, B.m, A.fm && B.fm) ^ L ^ H;
+  return {L ^ (M << 32), H ^ (M >> 32)};
+}
+
 // Shifts issued on the FMA pipe (IMAD.SHL / IMAD.HI) instead of the ALU pipe,
 // which the carry-less XOR network already saturates.
 __device__ __forceinline__ uint32_t shl_f(uint32_t x, uint32_t pow2) {
@@ -156,6 +214,12 @@ __device__ __forceinline__ uint64_t gf_reduce(u128 p) {
 
 __device__ __forceinline__ uint64_t gf_mul_kara(uint64_t a, uint64_t b) {
   return gf_reduce(clmul64_kara(a, b));
+}
+__device__ __forceinline__ uint64_t gf_mul_p5(uint64_t a, uint64_t b) {
+  return gf_reduce(clmul64_p5(ksplit5(a), ksplit5(b)));
+}
+__device__ __forceinline__ uint64_t gf_mul_presplit5(const KSplit5& a, uint64_t b) {
+  return gf_reduce(clmul64_p5(a, ksplit5(b)));
 }
 __device__ __forceinline__ uint64_t gf_mul_presplit(const KSplit& a, uint64_t b) {
   return gf_reduce(clmul64_kara_s(a, ksplit(b)));

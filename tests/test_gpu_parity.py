@@ -274,3 +274,49 @@ def test_device_restrict_matches_reference_renumbering(cuda_device):
             acc, nf, cs = O.oracle_eval(n, *r.edges(), directed, 3, r.t(), sh.vertex_off,
                                         sh.vertex_shades, 9)
             assert np.array_equal(o1.accumulators, acc) and o1.checksum == cs
+
+
+def _decide_points(g, ds, k, cfg, anchor_src, p0, p1):
+    import torch
+    acc = torch.zeros(g.n(), dtype=torch.int64, device="cuda")
+    T.eval_points_device(g, ds, k, g.t(), cfg, anchor_src, p0, p1, acc.data_ptr(),
+                         torch.cuda.current_stream().cuda_stream)
+    return acc.cpu().numpy().view(np.uint64)
+
+
+@pytest.mark.parametrize("cfgno,scale", [(2, 1.0), (5, 0.01)])
+def test_full_size_properties(cuda_device, cfgno, scale):
+    """BASELINE sizes, where the CPU oracle cannot follow, checked through
+    size-independent properties: (1) the accumulators do not depend on the
+    batch width (wide W=64/32 and grouped W=8/4 kernels agree bit for bit);
+    (2) sieve points are independent: XOR of disjoint point ranges = whole;
+    (3) the planted path is found; (4) restricted to the planted path's
+    vertices the engine equals the oracle exactly."""
+    inst = synth.make_config(cfgno, scale=scale)
+    k, col, motif, anchor = synth.effective_query(inst)
+    g = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed)
+    cfg = T.SieveConfig(seed=3, memory_cap_words=1 << 62)
+    sh = T.build_shades(T.MotifQuery.from_multiset(motif), T.VertexColoring(col, int(col.max())),
+                        cfg)
+    ds = T.DeviceShades(g, k, sh)
+    P = 1 << k
+    ref = None
+    for ppb in (64, 32, 8, 4):
+        c = T.SieveConfig(seed=3, points_per_batch=ppb, memory_cap_words=1 << 62)
+        acc = _decide_points(g, ds, k, c, anchor[0], 0, P)
+        if ref is None:
+            ref = acc
+        assert np.array_equal(acc, ref), ppb
+    parts = [_decide_points(g, ds, k, cfg, anchor[0], a, b)
+             for a, b in ((0, 5), (5, P // 2), (P // 2, P - 1), (P - 1, P))]
+    assert np.array_equal(parts[0] ^ parts[1] ^ parts[2] ^ parts[3], ref)
+    fin, nflag, cs = T.finalize(ref, anchor[1])
+    assert nflag > 0
+    keep = np.zeros(inst.n, bool)
+    keep[inst.planted] = True
+    r = T.restrict_to(g, keep, g.t())
+    out = T.eval_temporal_sieve(r, k, r.t(), sh, cfg, T.AnchorSpec(*anchor))
+    acc, nf, cs2 = O.oracle_eval(inst.n, *r.edges(), inst.directed, k, r.t(), sh.vertex_off,
+                                 sh.vertex_shades, 3, anchor)
+    assert np.array_equal(out.accumulators, acc) and out.checksum == cs2
+    assert int(inst.planted[-1]) in out.flagged.tolist()
