@@ -89,4 +89,39 @@ int64_t tsieve_solve_json(int32_t n, int64_t m, const int32_t* u, const int32_t*
   }
 }
 
+// load_graph on in-memory text (host only: ingestion + canonical build, no
+// device work).  Same argument meaning as oracle/ref_shim.cpp:ref_load_graph;
+// names are '\n'-joined.  Returns m or -1.
+int64_t tsieve_load_graph_text(const char* edge_text, const char* color_text, int directed,
+                               int32_t* n_out, int32_t* t_out, int32_t* out_u, int32_t* out_v,
+                               int32_t* out_ts, int64_t cap, int32_t* colors_out, int32_t ncap,
+                               char* names, int64_t names_cap) {
+  try {
+    std::istringstream es(edge_text);
+    std::istringstream cs(color_text ? color_text : "");
+    LoadResult lr = load_graph(es, color_text ? &cs : nullptr, directed != 0);
+    *n_out = lr.graph.n();
+    *t_out = lr.graph.t();
+    const auto& e = lr.graph.edges();
+    for (int64_t i = 0; i < lr.graph.m() && i < cap; ++i) {
+      out_u[i] = e[i].u;
+      out_v[i] = e[i].v;
+      out_ts[i] = e[i].ts;
+    }
+    for (int32_t i = 0; i < lr.graph.n() && i < ncap; ++i) colors_out[i] = lr.coloring.primary(i);
+    std::string joined;
+    for (size_t i = 0; i < lr.vertex_names.size(); ++i)
+      joined += (i ? "\n" : "") + lr.vertex_names[i];
+    if (names && names_cap > 0) {
+      const size_t w = std::min<size_t>(static_cast<size_t>(names_cap - 1), joined.size());
+      std::memcpy(names, joined.data(), w);
+      names[w] = 0;
+    }
+    return lr.graph.m();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 }  // extern "C"

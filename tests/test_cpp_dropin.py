@@ -93,6 +93,133 @@ def test_cli_certain_no_without_device(fig2):
 def test_dropin_exports():
     lib = dropin()
     assert hasattr(lib, "tsieve_solve_json")
+    assert hasattr(lib, "tsieve_load_graph_text")
+
+
+def dropin_load(edge_text, color_text, directed):
+    lib = dropin()
+    f = lib.tsieve_load_graph_text
+    f.restype = C.c_int64
+    f.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                  _i32p, _i32p, _i32p, C.c_int64, _i32p, C.c_int32, C.c_char_p, C.c_int64]
+    cap = edge_text.count("\n") + 2
+    ou, ov, ot = (np.empty(cap, np.int32) for _ in range(3))
+    n, t = C.c_int32(0), C.c_int32(0)
+    cols = np.empty(2 * cap + 2, np.int32)
+    names = C.create_string_buffer(1 << 22)
+    m = f(edge_text.encode(), None if color_text is None else color_text.encode(), int(directed),
+          C.byref(n), C.byref(t), ou, ov, ot, cap, cols, len(cols), names, len(names))
+    if m < 0:
+        raise ValueError(lib.tsieve_last_error().decode())
+    nm = names.value.decode().split("\n") if n.value else []
+    return {"n": n.value, "t": t.value, "u": ou[:m].copy(), "v": ov[:m].copy(),
+            "ts": ot[:m].copy(), "colors": cols[:n.value].copy(), "names": nm}
+
+
+def _random_text(rng):
+    """Edge/colour text exercising the tokenizer: numeric and symbolic names
+    (including non-canonical decimals like '007' and '+7'), comments, blank
+    lines, tabs, CRLF, sparse and dense timestamp spans, a missing final
+    newline, duplicates and self loops."""
+    pool = ["7", "007", "+7", "a", "b", "x_1", "12", "0", "00", "1073741824", "99999999999",
+            "-3", "v9", "3"]
+    names = [pool[i] for i in rng.choice(len(pool), size=rng.integers(2, len(pool)),
+                                         replace=False)]
+    span = int(rng.choice([5, 1000, 10**12]))
+    lines = []
+    for _ in range(int(rng.integers(0, 40))):
+        a, b = rng.choice(names), rng.choice(names)
+        ts = int(rng.integers(0, span))
+        sep = rng.choice([" ", "\t", "  "])
+        line = f"{a}{sep}{b}{sep}{ts}"
+        r = rng.random()
+        if r < 0.1:
+            line += " # comment"
+        elif r < 0.2:
+            line += "\r"
+        elif r < 0.25:
+            line += " 1"
+        lines.append(line)
+        if rng.random() < 0.1:
+            lines.append(rng.choice(["", "   ", "# only a comment"]))
+    text = "\n".join(lines) + ("\n" if rng.random() < 0.7 else "")
+    colors = None
+    if rng.random() < 0.7:
+        colors = "".join(f"{rng.choice(names + ['ghost'])} {int(rng.integers(1, 6))}\n"
+                         for _ in range(int(rng.integers(0, 10))))
+    return text, colors
+
+
+def test_load_graph_matches_reference_loader():
+    """load_graph (graph.cpp) against the reference's own load_graph
+    (oracle/_ref, graph.cpp:376-448): names, rank-normalized timestamps,
+    canonical edges, colours, and error messages on malformed lines."""
+    from oracle import oracle
+    try:
+        oracle.ref_lib()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"oracle/_ref not built: {e}")
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        text, colors = _random_text(rng)
+        directed = bool(rng.integers(0, 2))
+        want = oracle.ref_load_graph(text, colors, directed)
+        got = dropin_load(text, colors, directed)
+        assert got["n"] == want["n"] and got["t"] == want["t"], text
+        assert got["names"] == want["names"]
+        for key in ("u", "v", "ts", "colors"):
+            assert got[key].tolist() == want[key].tolist(), (key, text)
+    for bad in ["a b 3x\n", "a b\n", "a b 1\nb c -1\n", "a b 1 0\n", "a b 99999999999999999999\n",
+                "a b 1\n\n# c\na b 0x5\n", "a b --1\n", "a b +\n"]:
+        with pytest.raises(ValueError) as ref_err:
+            oracle.ref_load_graph(bad, None, False)
+        with pytest.raises(ValueError) as our_err:
+            dropin_load(bad, None, False)
+        assert str(our_err.value) == str(ref_err.value), bad
+    with pytest.raises(ValueError) as ref_err:
+        oracle.ref_load_graph("a b 1\n", "a 0\n", False)
+    with pytest.raises(ValueError) as our_err:
+        dropin_load("a b 1\n", "a 0\n", False)
+    assert str(our_err.value) == str(ref_err.value)
+
+
+def test_load_graph_multi_chunk_matches_reference_loader():
+    """A multi-megabyte edge file is parsed in parallel line-aligned chunks:
+    interning order, ranks and the line number of a late error must still be
+    those of the reference's sequential loader."""
+    from oracle import oracle
+    try:
+        oracle.ref_lib()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"oracle/_ref not built: {e}")
+    rng = np.random.default_rng(11)
+    L = 160_000
+    names = np.array([str(i) for i in range(3000)] + [f"n{i}" for i in range(500)] +
+                     ["007", "+3", "00"])
+    a = names[rng.integers(0, len(names), L)]
+    b = names[rng.integers(0, len(names), L)]
+    ts = rng.integers(0, 10**9, L)
+    lines = [f"{x} {y} {t}" for x, y, t in zip(a.tolist(), b.tolist(), ts.tolist())]
+    for i in rng.choice(L, 500, replace=False).tolist():
+        lines[i] = lines[i] + (" # note" if i % 2 else "\t1")
+    for i in rng.choice(L, 300, replace=False).tolist():
+        lines[i] = ""
+    text = "\n".join(lines) + "\n"
+    assert len(text) > 2 << 20  # several 1 MiB chunks
+    want = oracle.ref_load_graph(text, None, False)
+    got = dropin_load(text, None, False)
+    assert got["n"] == want["n"] and got["t"] == want["t"] and got["names"] == want["names"]
+    for key in ("u", "v", "ts"):
+        assert np.array_equal(got[key], want[key]), key
+    bad = lines[:]
+    bad[140_001] = "x y zz"
+    bad[150_000] = "x y"
+    text = "\n".join(bad) + "\n"
+    with pytest.raises(ValueError) as ref_err:
+        oracle.ref_load_graph(text, None, False)
+    with pytest.raises(ValueError) as our_err:
+        dropin_load(text, None, False)
+    assert str(our_err.value) == str(ref_err.value) == "line 140002: malformed integer 'zz'"
 
 
 # ------------------------------------------------------------------ GPU
