@@ -365,7 +365,8 @@ Instance load_instance(const Opts& o) {
     cf.emplace(o.colors_file);
     if (!*cf) throw std::invalid_argument("--colors: cannot open " + o.colors_file);
   }
-  inst.loaded = load_graph(ef, cf ? &*cf : nullptr, o.directed);
+  ef.close();
+  inst.loaded = load_graph_file(o.graph_file, cf ? &*cf : nullptr, o.directed);
   if (!o.delays_file.empty()) {
     std::ifstream df(o.delays_file);
     if (!df) throw std::invalid_argument("--delays: cannot open " + o.delays_file);

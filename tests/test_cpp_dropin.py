@@ -328,3 +328,28 @@ def test_cli_reference_defaults(cuda_device, fig2, golden):
         got_w = None if rec["witness"] is None else {"vertices": rec["witness"]["vertices"],
                                                      "edges": rec["witness"]["edges"]}
         assert got_w == want["witness"]
+
+
+@pytest.mark.gpu
+def test_large_build_canonicalizes_on_device_like_host(cuda_device):
+    """TemporalGraph::build sorts inputs of >= 2^22 edges on device 0 (and
+    keeps that HBM mirror); the canonical list must equal the host
+    canonicalizer's (TSV_HOST_BUILD=1), duplicates and self loops included."""
+    rng = np.random.default_rng(5)
+    m = (1 << 22) + 12345
+    u = rng.integers(0, 50_000, m)
+    v = rng.integers(0, 50_000, m)
+    ts = rng.integers(1, 3_000, m)
+    v[:1000] = u[:1000]                      # self loops
+    u[1000:3000], v[1000:3000], ts[1000:3000] = u[3000:5000], v[3000:5000], ts[3000:5000]
+    text = "".join(f"{a} {b} {t}\n" for a, b, t in zip(u.tolist(), v.tolist(), ts.tolist()))
+    for directed in (False, True):
+        os.environ["TSV_HOST_BUILD"] = "1"
+        try:
+            host = dropin_load(text, None, directed)
+        finally:
+            del os.environ["TSV_HOST_BUILD"]
+        dev = dropin_load(text, None, directed)
+        assert dev["n"] == host["n"] and dev["t"] == host["t"]
+        for key in ("u", "v", "ts"):
+            assert np.array_equal(dev[key], host[key]), key
