@@ -49,6 +49,11 @@ struct LevelParams {
   // y-multiply path for W >= 32: 0 = smem tables (default), 1 = holes in the
   // wide kernel, 2 = grouped kernel.  Set from TSV_YMUL for measurements.
   int ymul = 0;
+  // Level k fused with the readout (wide kernel only): no S_k is stored;
+  // acc[u] ^= XOR_w z_u * (XOR of u's arc products with ts <= max_ts).
+  bool last = false;
+  int32_t max_ts = 0;
+  uint64_t* acc = nullptr;
 };
 
 // One level of a static-projection engine (static_kernels.cu).

@@ -234,21 +234,49 @@ __device__ __forceinline__ void fetch_src(const LevelParams& P, int32_t src,
   }
 }
 
+// Level k fused with the readout: the XOR over the batch's points of
+// z_h^A * V, V = h's arc products with ts <= max_ts seen by this warp.  The
+// map V -> z*V is linear, so a vertex split across chunks simply contributes
+// once per piece (no fix-up), and only one general product per vertex piece
+// is needed instead of one per run.
+template <int PPT>
+__device__ __forceinline__ void flush_vertex(const LevelParams& P, int32_t h,
+                                             const uint32_t (&pt)[PPT], const bool (&pv)[PPT],
+                                             const uint64_t (&V)[PPT]) {
+  const int lane = threadIdx.x & 31;
+  uint64_t z[PPT];
+  if (P.zb) {
+#pragma unroll
+    for (int p = 0; p < PPT; ++p)
+      z[p] = __ldg(P.zb + static_cast<int64_t>(h) * (32 * PPT) + lane + 32 * p);
+  } else {
+    z_of<PPT>(P.zj, P.k, h, pt, pv, z);
+  }
+  uint64_t r = 0;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) r ^= gf_mul(z[p], V[p]);
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) r ^= __shfl_xor_sync(kFull, r, d);
+  if (lane == 0 && r) atomicXor(reinterpret_cast<unsigned long long*>(P.acc + h),
+                                static_cast<unsigned long long>(r));
+}
+
 // Wide variant (W = 32*PPT >= 32): one arc per step for the whole warp, so
 // y is warp-uniform and its product with the gathered states goes through
 // the shared-memory multiple tables (GfTable) when YTAB; z_head^A is cached
-// across the consecutive runs of one head.
-template <int PPT, bool FIRST, bool YTAB>
+// across the consecutive runs of one head.  LAST = level k fused with the
+// readout (flush_vertex).
+template <int PPT, bool FIRST, bool YTAB, bool LAST>
 __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
     k_level_wide(const LevelParams P) {
   constexpr int W = 32 * PPT;
   __shared__ uint64_t s_y[kWideWarps][32];
   __shared__ int32_t s_src[kWideWarps][32];
   __shared__ uint32_t s_meta[kWideWarps][32];
-  __shared__ int32_t s_run[kWideWarps][32];
+  __shared__ int32_t s_run[kWideWarps][32];  // LAST: the arc's timestamp
   __shared__ int32_t s_head[kWideWarps][32];
   __shared__ __align__(256) uint64_t s_tab[YTAB ? kWideWarps : 1][256];
-  __shared__ uint32_t s_zs[kWideWarps][PPT][12][32];  // split z_head^A per lane
+  __shared__ uint32_t s_zs[LAST ? 1 : kWideWarps][PPT][12][32];  // split z_head^A per lane
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * kWideWarps + wib;
@@ -270,7 +298,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
   uint64_t U[PPT], z[PPT];
 #pragma unroll
   for (int p = 0; p < PPT; ++p) U[p] = z[p] = 0;
-  int32_t zhead = -1;
+  int32_t zhead = -1;  // LAST: the vertex whose products U holds
 
   for (int64_t base = a0; base < a1; base += 32) {
     const int nb = static_cast<int>(a1 - base < 32 ? a1 - base : 32);
@@ -288,7 +316,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
     s_y[wib][lane] = y;
     s_src[wib][lane] = sidx;
     s_meta[wib][lane] = meta;
-    s_run[wib][lane] = myrun;
+    s_run[wib][lane] = LAST ? (lane < nb ? __ldg(P.g.run_ts + myrun) : 0) : myrun;
     s_head[wib][lane] = head;
     run_ctr += __popc(ends);
     __syncwarp();
@@ -319,14 +347,26 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
 #pragma unroll
           for (int p = 0; p < PPT; ++p) prod[p] = gf_mul(yy, val[p]);
         }
-        if (mt & kVStart) {
+        if (LAST) {
+          const int32_t h = s_head[wib][i];
+          if (h != zhead) {  // vertex boundary (warp-uniform)
+            if (zhead >= 0) flush_vertex<PPT>(P, zhead, pt, pv, U);
+            zhead = h;
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) U[p] = 0;
+          }
+          if (s_run[wib][i] <= P.max_ts) {
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) U[p] ^= prod[p];
+          }
+        } else if (mt & kVStart) {
 #pragma unroll
           for (int p = 0; p < PPT; ++p) U[p] = prod[p];
         } else {
 #pragma unroll
           for (int p = 0; p < PPT; ++p) U[p] ^= prod[p];
         }
-        if (mt & kRunEnd) {
+        if (!LAST && (mt & kRunEnd)) {
           const int32_t h = s_head[wib][i];
           if (h != zhead) {  // new head: z_head^A and its Karatsuba split, cached
             z_of<PPT>(P.zj, P.k, h, pt, pv, z);
@@ -358,6 +398,10 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
       }
     }
     __syncwarp();
+  }
+  if (LAST) {
+    if (zhead >= 0) flush_vertex<PPT>(P, zhead, pt, pv, U);
+    return;
   }
 #pragma unroll
   for (int p = 0; p < PPT; ++p) P.agg[c * W + lane + 32 * p] = U[p];
@@ -477,13 +521,20 @@ void level_dispatch(const LevelParams& p, cudaStream_t st) {
   if (LANES == 32 && p.ymul != 2) {
     const dim3 wgrid(static_cast<unsigned>((p.g.C + kWideWarps - 1) / kWideWarps));
     const dim3 wblock(kWideWarps * 32);
+    const bool first = p.ell == 2;
+#define TSV_WIDE(Y, L)                                                      \
+  do {                                                                      \
+    if (first) k_level_wide<PPT, true, Y, L><<<wgrid, wblock, 0, st>>>(p);  \
+    else k_level_wide<PPT, false, Y, L><<<wgrid, wblock, 0, st>>>(p);       \
+  } while (0)
     if (p.ymul == 1) {
-      if (p.ell == 2) k_level_wide<PPT, true, false><<<wgrid, wblock, 0, st>>>(p);
-      else k_level_wide<PPT, false, false><<<wgrid, wblock, 0, st>>>(p);
+      if (p.last) TSV_WIDE(false, true);
+      else TSV_WIDE(false, false);
     } else {
-      if (p.ell == 2) k_level_wide<PPT, true, true><<<wgrid, wblock, 0, st>>>(p);
-      else k_level_wide<PPT, false, true><<<wgrid, wblock, 0, st>>>(p);
+      if (p.last) TSV_WIDE(true, true);
+      else TSV_WIDE(true, false);
     }
+#undef TSV_WIDE
     return;
   }
   if (p.ell == 2)
@@ -500,7 +551,7 @@ unsigned blocks_for(int64_t n, int threads) {
 
 void launch_level(const LevelParams& p, cudaStream_t st) {
   if (p.g.C == 0) return;
-  prof_begin(p.ell == 2 ? "level_first" : "level", st);
+  prof_begin(p.last ? "level_last" : p.ell == 2 ? "level_first" : "level", st);
   switch (p.b.lanes * 8 + p.b.ppt) {
     case 1 * 8 + 1: level_dispatch<1, 1>(p, st); break;
     case 2 * 8 + 1: level_dispatch<2, 1>(p, st); break;

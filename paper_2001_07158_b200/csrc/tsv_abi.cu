@@ -330,15 +330,21 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
     }
     uint64_t* cur = s0.as<uint64_t>();
     uint64_t* prev = s1.as<uint64_t>();
+    // the wide kernel produces level k fused with the readout
+    const bool fuse_last = W >= 32 && lp.ymul != 2 && !std::getenv("TSV_NO_FUSED_READOUT");
     for (int ell = 2; ell <= k; ++ell) {
       lp.ell = ell;
       lp.s_prev = prev;
       lp.s_cur = cur;
+      lp.last = fuse_last && ell == k;
+      lp.max_ts = max_ts;
+      lp.acc = d_acc;
       tsv::launch_level(lp, st);
+      if (lp.last) break;
       tsv::launch_fixup(lp, st);
       std::swap(cur, prev);
     }
-    tsv::launch_readout(g->dev, max_ts, prev, W, d_acc, st);
+    if (!fuse_last) tsv::launch_readout(g->dev, max_ts, prev, W, d_acc, st);
     TSV_CUDA(cudaGetLastError());
   }
 }
