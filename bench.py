@@ -32,7 +32,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 REPS = {1: 1, 2: 4, 3: 1, 4: 1, 5: 1}
-BYTES_PER_UPDATE = 16  # 8 B predecessor-state read + 8 B state write
+# 8 B predecessor-state read per arc + 8 B state write per run
+# (runs no arc of the next level reads are not stored: graph.info.runs_referenced)
 
 
 def peaks():
@@ -299,9 +300,11 @@ def main():
         # updates executed by the middle-level launches (3 <= l < k when level
         # k is fused with the readout, else 3 <= l <= k) of this rank in the
         # timed region
+        # algorithmic bytes: one 8-B predecessor-state gather per arc with a
+        # src and one 8-B state store per referenced run, per sieve point
         mid_levels = (k - 2) - (1 if last_n else 0)
-        upd_lvl = g.info.arcs * mid_levels * my_points * args.steps
-        alg_bytes = BYTES_PER_UPDATE * upd_lvl / lvl_n
+        words = g.info.arcs_with_src + g.info.runs_referenced
+        alg_bytes = 8 * words * mid_levels * my_points * args.steps / lvl_n
         avg_ms = lvl_ms / lvl_n
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
         traffic = None
@@ -368,6 +371,8 @@ def main():
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
                 "decision": decisions, "checksums": checksums,
                 "graph": {"arcs": g.info.arcs, "runs": g.info.runs, "chunks": g.info.chunks,
+                          "arcs_with_src": g.info.arcs_with_src,
+                          "runs_referenced": g.info.runs_referenced,
                           "split_chunks": g.info.split_chunks,
                           "device_bytes": g.info.device_bytes},
                 "kernel_ms_per_step": {"level": lvl_ms / args.steps,

@@ -47,6 +47,8 @@ typedef struct {
   int64_t dropped_self_loops;
   int64_t dropped_duplicates;
   int64_t device_bytes; /* bytes of graph structure resident in HBM */
+  int64_t arcs_with_src;   /* arcs with a predecessor run (gathers per level) */
+  int64_t runs_referenced; /* runs some arc reads (stores per level < k) */
 } tsv_graph_info;
 
 /* Replaces TemporalGraph::build (graph.cpp:14-109) for the engine: drops

@@ -25,7 +25,8 @@ class GraphInfo(C.Structure):
                 ("device", C.c_int32), ("m", C.c_int64), ("arcs", C.c_int64),
                 ("runs", C.c_int64), ("chunks", C.c_int64), ("split_chunks", C.c_int64),
                 ("dropped_self_loops", C.c_int64), ("dropped_duplicates", C.c_int64),
-                ("device_bytes", C.c_int64)]
+                ("device_bytes", C.c_int64), ("arcs_with_src", C.c_int64),
+                ("runs_referenced", C.c_int64)]
 
 
 class Config(C.Structure):

@@ -22,6 +22,9 @@ struct DevGraph {
   const uint8_t* chunk_carry = nullptr;
   const int32_t* carry_list = nullptr;
   int32_t ncarry = 0;
+  // run_ref[r] = 1 iff some arc has arc_src == r: S_l of the other runs is
+  // never read by level l+1, so below level k it is neither formed nor stored
+  const uint8_t* run_ref = nullptr;
 };
 
 // One sieve-point batch [pb, pe) of W = lanes * ppt consecutive points.
@@ -52,6 +55,7 @@ struct LevelParams {
   // Level k fused with the readout (wide kernel only): no S_k is stored;
   // acc[u] ^= XOR_w z_u * (XOR of u's arc products with ts <= max_ts).
   bool last = false;
+  bool skip_unref = false;  // l < k: only runs in run_ref get S_l
   int32_t max_ts = 0;
   uint64_t* acc = nullptr;
 };
@@ -137,6 +141,10 @@ void launch_readout(const DevGraph& g, int32_t max_ts, const uint64_t* s,
                     int W, uint64_t* acc, cudaStream_t st);
 void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
                uint64_t* acc, cudaStream_t st);
+// Marks run_ref and counts (arcs with a src, referenced runs) into
+// counts[0..1] (device, zeroed here).
+void launch_run_ref(int64_t A, int64_t R, const int32_t* arc_src, uint8_t* run_ref,
+                    unsigned long long* counts, cudaStream_t st);
 void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n,
                         uint64_t* out, cudaStream_t st);
 void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,

@@ -315,7 +315,11 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
     if (lane < nb) head = __ldg(P.g.run_head + myrun);
     s_y[wib][lane] = y;
     s_src[wib][lane] = sidx;
-    s_meta[wib][lane] = meta;
+    // the edge id is consumed by the draw above; the staged meta keeps the
+    // flags plus bit 0 = "this run's S is read by the next level"
+    const uint32_t ref = (!LAST && lane < nb && (meta & kRunEnd) &&
+                          (!P.skip_unref || __ldg(P.g.run_ref + myrun))) ? 1u : 0u;
+    s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | ref;
     s_run[wib][lane] = LAST ? (lane < nb ? __ldg(P.g.run_ts + myrun) : 0) : myrun;
     s_head[wib][lane] = head;
     run_ctr += __popc(ends);
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
 #pragma unroll
           for (int p = 0; p < PPT; ++p) U[p] ^= prod[p];
         }
-        if (!LAST && (mt & kRunEnd)) {
+        if (!LAST && (mt & 1u)) {  // run end whose S is needed
           const int32_t h = s_head[wib][i];
           if (h != zhead) {  // new head: z_head^A and its Karatsuba split, cached
             z_of<PPT>(P.zj, P.k, h, pt, pv, z);
@@ -495,6 +499,22 @@ __global__ void k_zj(int32_t n, int k, uint64_t seed,
   for (int j = 0; j < k; ++j) zj[u * k + j] = row[j];
 }
 
+__global__ void k_run_ref(int64_t A, const int32_t* __restrict__ arc_src,
+                          uint8_t* __restrict__ run_ref, unsigned long long* counts) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int32_t s = a < A ? arc_src[a] : -1;
+  if (s >= 0) run_ref[s] = 1;
+  const unsigned c = __popc(__ballot_sync(kFull, s >= 0));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts, static_cast<unsigned long long>(c));
+}
+
+__global__ void k_count_ref(int64_t R, const uint8_t* __restrict__ run_ref,
+                            unsigned long long* counts) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const unsigned c = __popc(__ballot_sync(kFull, r < R && run_ref[r]));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts + 1, static_cast<unsigned long long>(c));
+}
+
 __global__ void k_xor_combine(const uint64_t* __restrict__ parts, int nparts,
                               int64_t n, uint64_t* __restrict__ out) {
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -615,6 +635,14 @@ void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n, uint64_t* 
   const unsigned blocks = blocks_for(n, 256) < 148 * 8 ? blocks_for(n, 256) : 148 * 8;
   k_xor_combine<<<blocks, 256, 0, st>>>(parts, nparts, n, out);
   prof_end(st);
+}
+
+void launch_run_ref(int64_t A, int64_t R, const int32_t* arc_src, uint8_t* run_ref,
+                    unsigned long long* counts, cudaStream_t st) {
+  cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
+  if (R > 0) cudaMemsetAsync(run_ref, 0, static_cast<size_t>(R), st);
+  if (A > 0) k_run_ref<<<blocks_for(A, 256), 256, 0, st>>>(A, arc_src, run_ref, counts);
+  if (R > 0) k_count_ref<<<blocks_for(R, 256), 256, 0, st>>>(R, run_ref, counts);
 }
 
 void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,

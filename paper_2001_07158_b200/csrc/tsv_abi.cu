@@ -163,6 +163,7 @@ struct tsv_graph {
   int device = 0;
   int64_t device_bytes = 0;
   int64_t m = 0;                      // canonical edge count
+  int64_t arcs_with_src = 0, runs_referenced = 0;
   const int32_t* d_eu = nullptr;      // canonical edges on the device (device build)
   const int32_t* d_ev = nullptr;
   const int32_t* d_ets = nullptr;
@@ -337,6 +338,7 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
       lp.s_prev = prev;
       lp.s_cur = cur;
       lp.last = fuse_last && ell == k;
+      lp.skip_unref = ell < k && !std::getenv("TSV_NO_SKIP_UNREF");
       lp.max_ts = max_ts;
       lp.acc = d_acc;
       tsv::launch_level(lp, st);
@@ -467,7 +469,17 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     d.chunk_carry = L.chunk_carry;
     d.carry_list = L.carry_list;
     d.ncarry = L.ncarry;
-    g->device_bytes = 12 * L.A + 8 * L.R + 4 * (static_cast<int64_t>(n) + 1) + 12 * L.m +
+    auto* rr = static_cast<uint8_t*>(alloc(std::max<int64_t>(L.R, 1)));
+    auto* cnt = static_cast<unsigned long long*>(alloc(16));
+    tsv::launch_run_ref(L.A, L.R, L.arc_src, rr, cnt, st);
+    unsigned long long hc[2] = {0, 0};
+    TSV_CUDA(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    release(cnt);
+    g->arcs_with_src = static_cast<int64_t>(hc[0]);
+    g->runs_referenced = static_cast<int64_t>(hc[1]);
+    d.run_ref = rr;
+    g->device_bytes = 12 * L.A + 9 * L.R + 4 * (static_cast<int64_t>(n) + 1) + 12 * L.m +
                       17 * (L.C + 1);
     TSV_CUDA(cudaStreamSynchronize(st));
     g->owned = live;
@@ -533,6 +545,17 @@ static int graph_build_impl(int32_t n, int64_t m, const int32_t* u, const int32_
       d.chunk_carry = own_upload(g, L.chunk_carry);
       d.carry_list = own_upload(g, L.carry_list);
       d.ncarry = static_cast<int32_t>(L.carry_list.size());
+      uint8_t* rr = dalloc<uint8_t>(std::max<size_t>(L.run_head.size(), 1));
+      g->owned.push_back(rr);
+      g->device_bytes += static_cast<int64_t>(std::max<size_t>(L.run_head.size(), 1));
+      auto* cnt = dalloc<unsigned long long>(2);
+      tsv::launch_run_ref(d.A, d.R, d.arc_src, rr, cnt, nullptr);
+      unsigned long long hc[2] = {0, 0};
+      TSV_CUDA(cudaMemcpy(hc, cnt, 16, cudaMemcpyDeviceToHost));
+      cudaFree(cnt);
+      g->arcs_with_src = static_cast<int64_t>(hc[0]);
+      g->runs_referenced = static_cast<int64_t>(hc[1]);
+      d.run_ref = rr;
       // release the host copies of the device layout (keep canonical edges)
       std::vector<int32_t>().swap(L.arc_src);
       std::vector<int32_t>().swap(L.arc_tail);
@@ -656,6 +679,8 @@ int tsv_graph_get_info(const tsv_graph* g, tsv_graph_info* out) {
     out->dropped_self_loops = g->host.dropped_self_loops;
     out->dropped_duplicates = g->host.dropped_duplicates;
     out->device_bytes = g->device_bytes;
+    out->arcs_with_src = g->arcs_with_src;
+    out->runs_referenced = g->runs_referenced;
   });
 }
 
