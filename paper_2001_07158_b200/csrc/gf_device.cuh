@@ -262,20 +262,35 @@ __device__ __forceinline__ uint64_t gf_mul_serial(uint64_t a, uint64_t b) {
 struct GfTable {
   uint64_t* tab;
 
+  template <int OFF>
+  __device__ __forceinline__ static void sts(uint32_t addr, uint64_t v) {
+    asm volatile("st.shared.u64 [%0+%1], %2;" ::"r"(addr), "n"(OFF), "l"(v) : "memory");
+  }
+
+  // Lane L writes entries 8*(L&1) .. 8*(L&1)+7 of window L>>1, i.e. the 64
+  // bytes at offset 64*L: c * x^(4i) * y for c = 8*(L&1) + e, e < 8.
+  // Branch-free (the window shift is a clamped PTX shift) and stored as
+  // eight 8-byte stores, so no register shuffling for vector stores.
   __device__ __forceinline__ void build(uint64_t y, int lane) {
-    const int i = lane >> 1;          // window: multiples of x^(4i) * y
-    const uint64_t Y = gf_mul_xpow(y, 4 * i);
-    const uint64_t B0 = Y, B1 = gf_mulx(B0), B2 = gf_mulx(B1), B3 = gf_mulx(B2);
-    const uint64_t base = (lane & 1) ? B3 : 0ull;  // c = 8*(lane&1) + e
-    uint64_t* row = tab + i * 16 + (lane & 1) * 8;
-    row[0] = base;
-    row[1] = base ^ B0;
-    row[2] = base ^ B1;
-    row[3] = base ^ B1 ^ B0;
-    row[4] = base ^ B2;
-    row[5] = base ^ B2 ^ B0;
-    row[6] = base ^ B2 ^ B1;
-    row[7] = base ^ B2 ^ B1 ^ B0;
+    const uint32_t s = 4u * static_cast<uint32_t>(lane >> 1);
+    uint64_t h, lo;
+    asm("shr.b64 %0, %1, %2;" : "=l"(h) : "l"(y), "r"(64u - s));  // 0 when s == 0
+    asm("shl.b64 %0, %1, %2;" : "=l"(lo) : "l"(y), "r"(s));
+    const uint64_t B0 = lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4);  // y * x^s (s <= 60)
+    const uint64_t B1 = gf_mulx(B0), B2 = gf_mulx(B1);
+    const uint64_t base = (lane & 1) ? gf_mulx(B2) : 0ull;
+    // (A lane-rotated Gray-code store order that avoids the 16-way bank
+    // conflicts of these stores was measured 3% slower: the kernel is bound
+    // by the ALU pipe, not by shared-memory wavefronts.)
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 64u * lane;
+    sts<0>(a, base);
+    sts<8>(a, base ^ B0);
+    sts<16>(a, base ^ B1);
+    sts<24>(a, base ^ B1 ^ B0);
+    sts<32>(a, base ^ B2);
+    sts<40>(a, base ^ B2 ^ B0);
+    sts<48>(a, base ^ B2 ^ B1);
+    sts<56>(a, base ^ B2 ^ B1 ^ B0);
   }
 
   // Lookups: nibble j of s, scaled by 8, is placed into the low byte of the

@@ -30,6 +30,9 @@ namespace {
 constexpr int kWarpsPerBlock = 8;
 constexpr int kWideWarps = 4;  // wide kernel: 4 warps per block (shared tables)
 constexpr unsigned kFull = 0xffffffffu;
+// staged per-arc flags of the wide kernel (kVStart / kRunEnd kept from meta)
+constexpr uint32_t kRef = 1u;   // run end whose S_l is read at level l+1
+constexpr uint32_t kLive = 2u;  // the arc's product can be nonzero
 
 template <int PPT>
 __device__ __forceinline__ void z_of(const uint64_t* __restrict__ zj, int k,
@@ -315,12 +318,17 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
     if (lane < nb) head = __ldg(P.g.run_head + myrun);
     s_y[wib][lane] = y;
     s_src[wib][lane] = sidx;
-    // the edge id is consumed by the draw above; the staged meta keeps the
-    // flags plus bit 0 = "this run's S is read by the next level"
+    // The edge id is consumed by the draw above; the staged meta keeps the
+    // flags plus kRef = "this run's S is read by the next level" and kLive =
+    // "this arc's product can be nonzero" (it has a predecessor state, comes
+    // from the anchor source at level 2, and at level k lies within max_ts).
     const uint32_t ref = (!LAST && lane < nb && (meta & kRunEnd) &&
-                          (!P.skip_unref || __ldg(P.g.run_ref + myrun))) ? 1u : 0u;
-    s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | ref;
-    s_run[wib][lane] = LAST ? (lane < nb ? __ldg(P.g.run_ts + myrun) : 0) : myrun;
+                          (!P.skip_unref || __ldg(P.g.run_ref + myrun))) ? kRef : 0u;
+    bool live = lane < nb && sidx >= 0;
+    if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
+    if (LAST) live = live && __ldg(P.g.run_ts + myrun) <= P.max_ts;
+    s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | ref | (live ? kLive : 0u);
+    s_run[wib][lane] = myrun;
     s_head[wib][lane] = head;
     run_ctr += __popc(ends);
     __syncwarp();
@@ -330,27 +338,18 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
     // step of look-ahead covers the HBM latency).  The loop is deliberately
     // not unrolled: the step body is large and must stay in the I-cache.
     uint64_t nxt[PPT];
-    fetch_src<PPT, FIRST>(P, s_src[wib][0], pt, pv, nxt);
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) nxt[p] = 0;
+    if (s_meta[wib][0] & kLive) fetch_src<PPT, FIRST>(P, s_src[wib][0], pt, pv, nxt);
 #pragma unroll 1
     for (int i = 0; i < nb; ++i) {
       uint64_t val[PPT];
 #pragma unroll
       for (int p = 0; p < PPT; ++p) val[p] = nxt[p];
-      if (i + 1 < nb) fetch_src<PPT, FIRST>(P, s_src[wib][i + 1], pt, pv, nxt);
+      if (i + 1 < nb && (s_meta[wib][i + 1] & kLive))
+        fetch_src<PPT, FIRST>(P, s_src[wib][i + 1], pt, pv, nxt);
       {
         const uint32_t mt = s_meta[wib][i];
-        const uint64_t yy = s_y[wib][i];
-        uint64_t prod[PPT];
-        if (YTAB) {
-          __syncwarp();
-          T.build(yy, lane);
-          __syncwarp();
-#pragma unroll
-          for (int p = 0; p < PPT; ++p) prod[p] = T.mul(val[p]);
-        } else {
-#pragma unroll
-          for (int p = 0; p < PPT; ++p) prod[p] = gf_mul(yy, val[p]);
-        }
         if (LAST) {
           const int32_t h = s_head[wib][i];
           if (h != zhead) {  // vertex boundary (warp-uniform)
@@ -359,21 +358,41 @@ __global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
 #pragma unroll
             for (int p = 0; p < PPT; ++p) U[p] = 0;
           }
-          if (s_run[wib][i] <= P.max_ts) {
+        }
+        if (mt & kLive) {  // warp-uniform: dead arcs contribute 0
+          const uint64_t yy = s_y[wib][i];
+          uint64_t prod[PPT];
+          if (YTAB) {
+            __syncwarp();
+            T.build(yy, lane);
+            __syncwarp();
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) prod[p] = T.mul(val[p]);
+          } else {
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) prod[p] = gf_mul(yy, val[p]);
+          }
+          if (!LAST && (mt & kVStart)) {
+#pragma unroll
+            for (int p = 0; p < PPT; ++p) U[p] = prod[p];
+          } else {
 #pragma unroll
             for (int p = 0; p < PPT; ++p) U[p] ^= prod[p];
           }
-        } else if (mt & kVStart) {
+        } else if (!LAST && (mt & kVStart)) {
 #pragma unroll
-          for (int p = 0; p < PPT; ++p) U[p] = prod[p];
-        } else {
-#pragma unroll
-          for (int p = 0; p < PPT; ++p) U[p] ^= prod[p];
+          for (int p = 0; p < PPT; ++p) U[p] = 0;
         }
-        if (!LAST && (mt & 1u)) {  // run end whose S is needed
+        if (!LAST && (mt & kRef)) {  // run end whose S is needed
           const int32_t h = s_head[wib][i];
           if (h != zhead) {  // new head: z_head^A and its Karatsuba split, cached
-            z_of<PPT>(P.zj, P.k, h, pt, pv, z);
+            if (P.zb) {
+#pragma unroll
+              for (int p = 0; p < PPT; ++p)
+                z[p] = __ldg(P.zb + static_cast<int64_t>(h) * W + lane + 32 * p);
+            } else {
+              z_of<PPT>(P.zj, P.k, h, pt, pv, z);
+            }
             zhead = h;
 #pragma unroll
             for (int p = 0; p < PPT; ++p) {
