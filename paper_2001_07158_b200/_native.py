@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtsv.so")
+LIB_PATH = os.environ.get("TSV_LIB") or os.path.join(HERE, "lib", "libtsv.so")
 
 TSV_OK, TSV_ERR_INVALID, TSV_ERR_CAP, TSV_ERR_CUDA = 0, 1, 2, 3
 

@@ -270,7 +270,10 @@ __device__ __forceinline__ void flush_vertex(const LevelParams& P, int32_t h,
 // across the consecutive runs of one head.  LAST = level k fused with the
 // readout (flush_vertex).
 template <int PPT, bool FIRST, bool YTAB, bool LAST>
-__global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : 6)
+#ifndef TSV_WIDE_MINB
+#define TSV_WIDE_MINB 5  // resident blocks per SM for PPT <= 2 (96-register cap; measured)
+#endif
+__global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : TSV_WIDE_MINB)
     k_level_wide(const LevelParams P) {
   constexpr int W = 32 * PPT;
   __shared__ uint64_t s_y[kWideWarps][32];
