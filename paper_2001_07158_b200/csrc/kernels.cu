@@ -270,10 +270,12 @@ __device__ __forceinline__ void flush_vertex(const LevelParams& P, int32_t h,
 // across the consecutive runs of one head.  LAST = level k fused with the
 // readout (flush_vertex).
 template <int PPT, bool FIRST, bool YTAB, bool LAST>
+// Resident blocks per SM (register cap 65536 / (128 * minB)), measured per
+// batch shape: PPT 1 -> 6 (80 regs), PPT 2 -> 5 (96 regs), PPT 4 -> 4.
 #ifndef TSV_WIDE_MINB
-#define TSV_WIDE_MINB 5  // resident blocks per SM for PPT <= 2 (96-register cap; measured)
+#define TSV_WIDE_MINB(PPT) ((PPT) >= 4 ? 4 : (PPT) == 2 ? 5 : 6)
 #endif
-__global__ void __launch_bounds__(kWideWarps * 32, PPT >= 4 ? 4 : TSV_WIDE_MINB)
+__global__ void __launch_bounds__(kWideWarps * 32, TSV_WIDE_MINB(PPT))
     k_level_wide(const LevelParams P) {
   constexpr int W = 32 * PPT;
   __shared__ uint64_t s_y[kWideWarps][32];

@@ -3,6 +3,7 @@
 # link it with the regular objects into exp_libs/libtsv_<name>.so; select it
 # at run time with TSV_LIB=exp_libs/libtsv_<name>.so.
 # Usage: tools/build_variant.sh <name> <nvcc flags...>
+#   e.g. tools/build_variant.sh m4 '-DTSV_WIDE_MINB(P)=4'
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
