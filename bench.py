@@ -196,7 +196,7 @@ def config_json(inst, world, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--scale", type=float, default=1.0,
@@ -307,19 +307,39 @@ def main():
         alg_bytes = 8 * words * mid_levels * my_points * args.steps / lvl_n
         avg_ms = lvl_ms / lvl_n
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
-        traffic = None
+        # per-launch DRAM traffic and instruction counts of the same kernel on
+        # the same workload, from the committed ncu capture (tools/ncu_level_json.py)
+        traffic, prof = None, None
         try:
-            with open(os.path.join(ROOT, "profiles", "r1_level_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", f"level_kernel_c{args.config}.json")) as f:
                 prof = json.load(f)
-            if prof["config"] == args.config and world == 1:
+            if prof["config"] != args.config or args.scale != 1.0 or world != 1:
+                prof = None
+            else:
                 traffic = prof["traffic_bytes_per_launch"]
         except Exception:
-            pass
+            prof = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                 "kernel": "k_level_wide (3 <= l < k)", "avg_launch_ms": avg_ms,
                 "launch_share_of_step": lvl_ms / max(all_ms, 1e-9),
                 "alg_bytes_per_launch": alg_bytes}
+        # The kernel is integer-pipe bound (GF(2^64) carry-less products), so
+        # the binding roofline is instruction issue: 4 warp-instructions per
+        # clock per SM.  achieved = the capture's executed warp-instructions
+        # per launch / this run's launch time; ALU-pipe utilization is the
+        # capture's own counter.
+        if prof is not None:
+            sm_mhz = clk.summary().get("sm_mhz") or prof["sm_clock_ghz"] * 1e3
+            peak_issue = 148 * 4 * sm_mhz * 1e6
+            ach = prof["warp_inst_per_launch"] / (avg_ms * 1e-3)
+            roof["int_pipe"] = {"bound": "issue", "unit": "warp-inst/s", "achieved": ach,
+                                "peak": peak_issue, "frac": ach / peak_issue,
+                                "alu_pipe_frac_ncu": prof["alu_pipe_pct_active"] / 100,
+                                "thread_inst_per_update": 32 * prof["warp_inst_per_launch"] /
+                                (alg_bytes / 8 / (g.info.arcs_with_src + g.info.runs_referenced)
+                                 * g.info.arcs),
+                                "capture": prof["capture"]}
 
     # e2e through the public API with host buffers (graph build + shades +
     # eval + accumulator read-back), same metric
