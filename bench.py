@@ -205,7 +205,7 @@ def main():
     ap.add_argument("--ref-frac", type=float, default=0.1)
     ap.add_argument("--points-per-batch", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -345,12 +345,16 @@ def main():
     # eval + accumulator read-back), same metric
     e2e = None
     if args.e2e_steps > 0:
+        # the step's inputs live in pinned host memory; every step copies them
+        # to the device, builds, evaluates and reads the accumulators back
+        pinned = tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+                       for a in (inst.u, inst.v, inst.ts))
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            g2 = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
+            g2 = T.TemporalGraph.build(inst.n, pinned, inst.directed, 0, dev)
             ds2 = T.DeviceShades(g2, k, sh)
             a2 = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
             for r, a, b in work:

@@ -381,8 +381,8 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
                               bool canonical, bool on_device = false) {
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   DeviceGuard dg(device);
-  cudaDeviceProp prop{};
-  TSV_CUDA(cudaGetDeviceProperties(&prop, device));
+  int sm_count = 0;  // (cudaGetDeviceProperties costs milliseconds per call)
+  TSV_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
   cudaStream_t st = nullptr;
   TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   std::vector<void*> live;
@@ -414,7 +414,7 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     auto* status = static_cast<tsv::BuildStatus*>(alloc(sizeof(tsv::BuildStatus)));
     tsv::DeviceLayout L;
     tsv::device_build(du, dv, dts, m, n, directed, canonical, L, status,
-                      prop.multiProcessorCount, st, alloc, release);
+                      sm_count, st, alloc, release);
     tsv::BuildStatus hs{};
     TSV_CUDA(cudaMemcpyAsync(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
     TSV_CUDA(cudaStreamSynchronize(st));
@@ -525,9 +525,9 @@ static int graph_build_impl(int32_t n, int64_t m, const int32_t* u, const int32_
         tsv::canonicalize(n, m, u, v, ts, directed != 0, t, g->host);
       g->m = static_cast<int64_t>(g->host.eu.size());
       DeviceGuard dg(device);
-      cudaDeviceProp prop{};
-      TSV_CUDA(cudaGetDeviceProperties(&prop, device));
-      tsv::build_layout(g->host, 0, prop.multiProcessorCount);
+      int sm_count = 0;
+      TSV_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device));
+      tsv::build_layout(g->host, 0, sm_count);
       tsv::HostLayout& L = g->host;
       tsv::DevGraph& d = g->dev;
       d.n = L.n;

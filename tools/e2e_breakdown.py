@@ -1,0 +1,54 @@
+"""Where the end-to-end step goes (C2 by default): graph build from host
+arrays (pageable vs pinned), shade upload, the sieve, accumulator read-back."""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--iters", type=int, default=5)
+    args = ap.parse_args()
+    import torch
+    import paper_2001_07158_b200 as T
+    from paper_2001_07158_b200 import synth
+    inst = synth.make_config(args.config, scale=args.scale)
+    k, colors, motif, anchor = synth.effective_query(inst)
+    col = T.VertexColoring(colors, int(colors.max()))
+    cfg = T.SieveConfig(seed=1, memory_cap_words=1 << 62)
+    sh = T.build_shades(T.MotifQuery.from_multiset(motif), col, cfg)
+    pin = [torch.from_numpy(a).pin_memory() for a in (inst.u, inst.v, inst.ts)]
+    arrs = {"pageable": (inst.u, inst.v, inst.ts), "pinned": tuple(p.numpy() for p in pin)}
+    acc = torch.zeros(inst.n, dtype=torch.int64, device="cuda")
+    sp = torch.cuda.current_stream().cuda_stream
+
+    def t(f):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = f()
+        torch.cuda.synchronize()
+        return r, (time.perf_counter() - t0) * 1e3
+
+    for kind, a in arrs.items():
+        rows = []
+        for _ in range(args.iters):
+            g, tb = t(lambda: T.TemporalGraph.build(inst.n, a, inst.directed, 0, 0))
+            ds, ts_ = t(lambda: T.DeviceShades(g, k, sh))
+            _, te = t(lambda: T.eval_points_device(g, ds, k, g.t(), cfg, anchor[0], 0, 1 << k,
+                                                   acc.data_ptr(), sp))
+            _, td = t(lambda: acc.cpu())
+            rows.append((tb, ts_, te, td))
+            del g, ds
+        best = [min(r[i] for r in rows) for i in range(4)]
+        print(f"{kind:9s} build {best[0]:.2f} ms  shades {best[1]:.2f}  eval(1 rep) {best[2]:.2f}"
+              f"  d2h {best[3]:.2f}")
+
+
+if __name__ == "__main__":
+    main()
