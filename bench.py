@@ -275,6 +275,10 @@ def main():
     ms = e0.elapsed_time(e1) / args.steps
     lvl_n, lvl_ms = _native.Profile.get("level")
     last_n, _ = _native.Profile.get("level_last")
+    grouped = False
+    if not lvl_n:  # W < 32: the grouped kernel (no fused readout, every run stored)
+        lvl_n, lvl_ms = _native.Profile.get("level_grouped")
+        grouped = bool(lvl_n)
     all_n, all_ms = _native.Profile.get(None)
     _native.Profile.enable(False)
     if world > 1:
@@ -303,7 +307,7 @@ def main():
         # algorithmic bytes: one 8-B predecessor-state gather per arc with a
         # src and one 8-B state store per referenced run, per sieve point
         mid_levels = (k - 2) - (1 if last_n else 0)
-        words = g.info.arcs_with_src + g.info.runs_referenced
+        words = g.info.arcs_with_src + (g.info.runs if grouped else g.info.runs_referenced)
         alg_bytes = 8 * words * mid_levels * my_points * args.steps / lvl_n
         avg_ms = lvl_ms / lvl_n
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
@@ -313,7 +317,7 @@ def main():
         try:
             with open(os.path.join(ROOT, "profiles", f"level_kernel_c{args.config}.json")) as f:
                 prof = json.load(f)
-            if prof["config"] != args.config or args.scale != 1.0 or world != 1:
+            if prof["config"] != args.config or args.scale != 1.0 or world != 1 or grouped:
                 prof = None
             else:
                 traffic = prof["traffic_bytes_per_launch"]
@@ -321,7 +325,8 @@ def main():
             prof = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": "k_level_wide (3 <= l < k)", "avg_launch_ms": avg_ms,
+                "kernel": ("k_level (grouped, W < 32, 3 <= l <= k)" if grouped
+                           else "k_level_wide (3 <= l < k)"), "avg_launch_ms": avg_ms,
                 "launch_share_of_step": lvl_ms / max(all_ms, 1e-9),
                 "alg_bytes_per_launch": alg_bytes}
         # The kernel is integer-pipe bound (GF(2^64) carry-less products), so

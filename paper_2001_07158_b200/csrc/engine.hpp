@@ -49,8 +49,8 @@ struct LevelParams {
   const uint64_t* s_prev = nullptr;  // R x W (level ell-1), unused at ell=2
   uint64_t* s_cur = nullptr;         // R x W (level ell)
   uint64_t* agg = nullptr;           // C x W chunk tail aggregates
-  // y-multiply path for W >= 32: 0 = smem tables (default), 1 = holes in the
-  // wide kernel, 2 = grouped kernel.  Set from TSV_YMUL for measurements.
+  // y-multiply path of the wide kernel: 0 = smem tables (default), 1 = holes
+  // general product.  Set from TSV_YMUL=holes for measurements.
   int ymul = 0;
   // Level k fused with the readout (wide kernel only): no S_k is stored;
   // acc[u] ^= XOR_w z_u * (XOR of u's arc products with ts <= max_ts).

@@ -62,51 +62,86 @@ __device__ __forceinline__ uint64_t z_single(const uint64_t* __restrict__ zj,
   return z;
 }
 
-template <int LANES, int PPT, bool FIRST>
+// Grouped variant (W = LANES < 32 points per batch): G = 32/LANES arcs are
+// in flight per warp step, one per group of LANES lanes (one point per lane);
+// y is split once per arc into shared memory and each group multiplies its
+// gathered states by its own arc's y (general product).  The per-vertex
+// prefix is a segmented XOR-scan across the groups (shuffles) plus a carry
+// across steps.  The z_head products at run ends are where the groups
+// diverge, so they go through a per-warp work queue: a group whose arc ends a
+// run that is needed (kPush) enqueues (run, head, prefix) and whenever G
+// entries are pending every group pops one, so each round of general
+// products runs with all 32 lanes busy.  Level k (LAST) enqueues one entry per
+// vertex piece (its last arc within max_ts) and the pop XORs the group's
+// z_head * prefix into acc[head] (fused readout, like flush_vertex).
+template <int LANES, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     k_level(const LevelParams P) {
   constexpr int G = 32 / LANES;
-  constexpr int W = LANES * PPT;
+  constexpr int W = LANES;
+  constexpr uint32_t kPush = 4u;  // staged: enqueue this arc's prefix
   __shared__ uint32_t s_ys[kWarpsPerBlock][12][32];  // Karatsuba split of each arc's y
   __shared__ int32_t s_src[kWarpsPerBlock][32];
   __shared__ uint32_t s_meta[kWarpsPerBlock][32];
   __shared__ int32_t s_run[kWarpsPerBlock][32];
+  __shared__ int32_t s_head[kWarpsPerBlock][32];
+  __shared__ int32_t q_run[kWarpsPerBlock][2 * G];
+  __shared__ int32_t q_head[kWarpsPerBlock][2 * G];
+  __shared__ uint64_t q_val[kWarpsPerBlock][2 * G][LANES];
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
   if (c >= P.g.C) return;  // warp-uniform
   const int g = lane / LANES, li = lane % LANES;
 
-  uint32_t pt[PPT];
-  bool pv[PPT];
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) {
-    const uint64_t A = P.b.pb + li + LANES * p;
-    pt[p] = static_cast<uint32_t>(A);
-    pv[p] = A < P.b.pe;
-  }
+  const uint64_t A = P.b.pb + li;
+  const bool pv = A < P.b.pe;
   const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
   const uint64_t yb = static_cast<uint64_t>(P.ell - 1) + 0x165667b19e3779f9ull;
   const int64_t a0 = P.g.chunk_arc[c], a1 = P.g.chunk_arc[c + 1];
   int32_t run_ctr = P.g.chunk_run[c];
   const int last_lane = (G - 1) * LANES + li;
-  uint64_t carry[PPT], zc[PPT];
+  uint64_t carry = 0;
+  int qn = 0;  // pending queue entries (warp-uniform)
+
+  // z_head^A for this lane's point
+  auto zval = [&](int32_t h) -> uint64_t {
+    if (P.zb) return __ldg(P.zb + static_cast<int64_t>(h) * W + li);
+    return pv ? z_single(P.zj, P.k, h, A) : 0ull;
+  };
+  // group gi pops entry e (all lanes of the warp call this together)
+  auto pop = [&](int e, bool on) {
+    uint64_t prod = 0;
+    int32_t h = -1;
+    if (on) {
+      h = q_head[wib][e];
+      prod = gf_mul(zval(h), q_val[wib][e][li]);
+    }
+    if (LAST) {  // XOR over the group's points (converged shuffles), one atomic
+      uint64_t r = prod;
 #pragma unroll
-  for (int p = 0; p < PPT; ++p) carry[p] = zc[p] = 0;
-  int32_t zhead = -1;  // z_head^A cached per group across its consecutive runs
+      for (int d = LANES / 2; d >= 1; d >>= 1) r ^= __shfl_xor_sync(kFull, r, d, LANES);
+      if (on && li == 0 && r)
+        atomicXor(reinterpret_cast<unsigned long long*>(P.acc + h),
+                  static_cast<unsigned long long>(r));
+    } else if (on) {
+      P.s_cur[static_cast<int64_t>(q_run[wib][e]) * W + li] = prod;
+    }
+  };
 
   for (int64_t base = a0; base < a1; base += 32) {
     const int nb = static_cast<int>(a1 - base < 32 ? a1 - base : 32);
     uint32_t meta = 0;
-    int32_t sidx = -1;
+    int32_t sidx = -1, head = -1;
     uint64_t y = 0;
     if (lane < nb) {
       meta = __ldg(P.g.arc_meta + base + lane);
-      sidx = FIRST ? __ldg(P.g.arc_tail + base + lane)
-                   : __ldg(P.g.arc_src + base + lane);
+      sidx = FIRST ? __ldg(P.g.arc_tail + base + lane) : __ldg(P.g.arc_src + base + lane);
       y = draw_edge_y(pre, yb, meta & kEdgeMask);
     }
     const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
+    const int32_t myrun = run_ctr + __popc(ends & ((1u << lane) - 1u));
+    if (lane < nb) head = __ldg(P.g.run_head + myrun);
     {
       const KSplit ks = ksplit(y);  // once per arc, not once per lane of its group
 #pragma unroll
@@ -116,96 +151,102 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
         s_ys[wib][8 + j][lane] = ks.m.c[j];
       }
     }
+    bool live = lane < nb && sidx >= 0;
+    if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
+    bool push;
+    if (LAST) {
+      // last arc of its vertex (within this chunk) with ts <= max_ts
+      const int32_t myts = lane < nb ? __ldg(P.g.run_ts + myrun) : 0;
+      const bool chunk_end = base + lane + 1 >= a1;
+      uint32_t nmeta = __shfl_down_sync(kFull, meta, 1);
+      int32_t nts = __shfl_down_sync(kFull, myts, 1);
+      if (lane == 31 && !chunk_end) {
+        nmeta = __ldg(P.g.arc_meta + base + 32);
+        nts = __ldg(P.g.run_ts + myrun + ((meta & kRunEnd) ? 1 : 0));
+      }
+      live = live && myts <= P.max_ts;
+      push = lane < nb && myts <= P.max_ts && (chunk_end || (nmeta & kVStart) || nts > P.max_ts);
+    } else {
+      push = lane < nb && (meta & kRunEnd) && (!P.skip_unref || __ldg(P.g.run_ref + myrun));
+    }
     s_src[wib][lane] = sidx;
-    s_meta[wib][lane] = meta;
-    s_run[wib][lane] = run_ctr + __popc(ends & ((1u << lane) - 1u));
+    s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | (live ? kLive : 0u) | (push ? kPush : 0u);
+    s_run[wib][lane] = myrun;
+    s_head[wib][lane] = head;
     run_ctr += __popc(ends);
     __syncwarp();
 
-    // one step = G arcs (one per group); the next step's gathers are in
-    // flight during this one; the loop stays rolled to keep the I-cache warm
-    auto fetch = [&](int i, uint64_t (&out)[PPT]) {
-      if (FIRST) {
-        const int32_t tail = i < nb ? s_src[wib][i] : -1;
-        if (tail >= 0 && (P.anchor_source < 0 || tail == P.anchor_source)) {
-          z_of<PPT>(P.zj, P.k, tail, pt, pv, out);
+    auto fetch = [&](int i, uint64_t& out) {
+      out = 0;
+      if (i < nb && (s_meta[wib][i] & kLive)) {
+        const int32_t src = s_src[wib][i];
+        if (FIRST) {
+          out = zval(src);
         } else {
-#pragma unroll
-          for (int p = 0; p < PPT; ++p) out[p] = 0;
+          out = __ldg(P.s_prev + static_cast<int64_t>(src) * W + li);
         }
-      } else {
-        const int32_t src = i < nb ? s_src[wib][i] : -1;
-#pragma unroll
-        for (int p = 0; p < PPT; ++p)
-          out[p] = src >= 0 ? __ldg(P.s_prev + static_cast<int64_t>(src) * W + li + LANES * p)
-                            : 0ull;
       }
     };
-    uint64_t nxt[PPT];
+    uint64_t nxt;
     fetch(g, nxt);
     const int steps = (nb + G - 1) / G;
 #pragma unroll 1
     for (int s = 0; s < steps; ++s) {
-      uint64_t val[1][PPT];
-      const int u = 0;
-#pragma unroll
-      for (int p = 0; p < PPT; ++p) val[0][p] = nxt[p];
+      const uint64_t val = nxt;
       if (s + 1 < steps) fetch((s + 1) * G + g, nxt);
-      {
-        const int i = s * G + g;
-        const bool act = i < nb;
-        const uint32_t mt = act ? s_meta[wib][i] : 0u;
-        const int ia = act ? i : 0;
+      const int i = s * G + g;
+      const bool act = i < nb;
+      const uint32_t mt = act ? s_meta[wib][i] : 0u;
+      uint64_t v = 0;
+      if (__any_sync(kFull, mt & kLive)) {
         KSplit ys;
+        const int ia = act ? i : 0;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          ys.l.c[j] = act ? s_ys[wib][j][ia] : 0u;
-          ys.h.c[j] = act ? s_ys[wib][4 + j][ia] : 0u;
-          ys.m.c[j] = act ? s_ys[wib][8 + j][ia] : 0u;
+          ys.l.c[j] = s_ys[wib][j][ia];
+          ys.h.c[j] = s_ys[wib][4 + j][ia];
+          ys.m.c[j] = s_ys[wib][8 + j][ia];
         }
-        uint64_t v[PPT];
+        v = (mt & kLive) ? gf_mul_presplit(ys, val) : 0ull;
+      }
+      // segmented inclusive XOR-scan over the G groups (vertex starts cut it)
+      bool f = (mt & kVStart) != 0;
+      if (G > 1) {
 #pragma unroll
-        for (int p = 0; p < PPT; ++p) v[p] = gf_mul_presplit(ys, val[u][p]);
-        bool f = (mt & kVStart) != 0;
-        if (G > 1) {
-#pragma unroll
-          for (int d = 1; d < G; d <<= 1) {
-            const bool fo = __shfl_up_sync(kFull, f, d * LANES);
-#pragma unroll
-            for (int p = 0; p < PPT; ++p) {
-              const uint64_t vo = __shfl_up_sync(kFull, v[p], d * LANES);
-              if (g >= d && !f) v[p] ^= vo;
-            }
-            if (g >= d) f = f || fo;
+        for (int d = 1; d < G; d <<= 1) {
+          const bool fo = __shfl_up_sync(kFull, f, d * LANES);
+          const uint64_t vo = __shfl_up_sync(kFull, v, d * LANES);
+          if (g >= d && !f) v ^= vo;
+          if (g >= d) f = f || fo;
+        }
+      }
+      if (!f) v ^= carry;
+      carry = (G > 1) ? __shfl_sync(kFull, v, last_lane) : v;
+      // enqueue the needed prefixes, pop whenever a full round is pending
+      const bool push = (mt & kPush) != 0;
+      const unsigned pm = __ballot_sync(kFull, push && li == 0);
+      if (pm) {
+        if (push) {
+          const int slot = qn + __popc(pm & ((1u << (g * LANES)) - 1u));
+          q_val[wib][slot][li] = v;
+          if (li == 0) {
+            q_run[wib][slot] = s_run[wib][i];
+            q_head[wib][slot] = s_head[wib][i];
           }
         }
-        if (!f) {
-#pragma unroll
-          for (int p = 0; p < PPT; ++p) v[p] ^= carry[p];
+        qn += __popc(pm);
+        __syncwarp();
+        if (qn >= G) {
+          pop(qn - G + g, true);
+          qn -= G;
         }
-        if (act && (mt & kRunEnd)) {
-          const int32_t run = s_run[wib][i];
-          const int32_t head = __ldg(P.g.run_head + run);
-          if (head != zhead) {
-            z_of<PPT>(P.zj, P.k, head, pt, pv, zc);
-            zhead = head;
-          }
-#pragma unroll
-          for (int p = 0; p < PPT; ++p)
-            P.s_cur[static_cast<int64_t>(run) * W + li + LANES * p] =
-                gf_mul(zc[p], v[p]);
-        }
-#pragma unroll
-        for (int p = 0; p < PPT; ++p)
-          carry[p] = (G > 1) ? __shfl_sync(kFull, v[p], last_lane) : v[p];
+        __syncwarp();
       }
     }
     __syncwarp();
   }
-  if (g == 0) {
-#pragma unroll
-    for (int p = 0; p < PPT; ++p) P.agg[c * W + li + LANES * p] = carry[p];
-  }
+  if (qn > 0) pop(g, g < qn);
+  if (!LAST && g == 0) P.agg[c * W + li] = carry;
 }
 
 // The value multiplied by y(e, l-1) for one arc: the predecessor state
@@ -562,7 +603,7 @@ template <int LANES, int PPT>
 void level_dispatch(const LevelParams& p, cudaStream_t st) {
   const dim3 grid(static_cast<unsigned>((p.g.C + kWarpsPerBlock - 1) / kWarpsPerBlock));
   const dim3 block(kWarpsPerBlock * 32);
-  if (LANES == 32 && p.ymul != 2) {
+  if (LANES == 32) {
     const dim3 wgrid(static_cast<unsigned>((p.g.C + kWideWarps - 1) / kWideWarps));
     const dim3 wblock(kWideWarps * 32);
     const bool first = p.ell == 2;
@@ -581,10 +622,16 @@ void level_dispatch(const LevelParams& p, cudaStream_t st) {
 #undef TSV_WIDE
     return;
   }
-  if (p.ell == 2)
-    k_level<LANES, PPT, true><<<grid, block, 0, st>>>(p);
-  else
-    k_level<LANES, PPT, false><<<grid, block, 0, st>>>(p);
+  if (LANES < 32 && PPT == 1) {
+    constexpr int L = LANES < 32 ? LANES : 16;  // (instantiated for LANES < 32 only)
+    if (p.ell == 2) {
+      if (p.last) k_level<L, true, true><<<grid, block, 0, st>>>(p);
+      else k_level<L, true, false><<<grid, block, 0, st>>>(p);
+    } else {
+      if (p.last) k_level<L, false, true><<<grid, block, 0, st>>>(p);
+      else k_level<L, false, false><<<grid, block, 0, st>>>(p);
+    }
+  }
 }
 
 unsigned blocks_for(int64_t n, int threads) {
@@ -595,7 +642,13 @@ unsigned blocks_for(int64_t n, int threads) {
 
 void launch_level(const LevelParams& p, cudaStream_t st) {
   if (p.g.C == 0) return;
-  prof_begin(p.last ? "level_last" : p.ell == 2 ? "level_first" : "level", st);
+  // profile names: the wide kernel's middle levels are "level"; the grouped
+  // kernel (W < 32) reports as "level_grouped[_first]"
+  const bool wide = p.b.lanes == 32;
+  prof_begin(p.last ? "level_last"
+             : p.ell == 2 ? (wide ? "level_first" : "level_grouped_first")
+                          : (wide ? "level" : "level_grouped"),
+             st);
   switch (p.b.lanes * 8 + p.b.ppt) {
     case 1 * 8 + 1: level_dispatch<1, 1>(p, st); break;
     case 2 * 8 + 1: level_dispatch<2, 1>(p, st); break;

@@ -235,8 +235,9 @@ tsv::Batch batch_shape(int W) {
 
 // Points per batch: the largest power of two <= min(range, 64) whose
 // working set fits the word cap and free device memory.
+// *zb_ok: the per-batch z table (n*W words) also fits next to that working set.
 int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cfg,
-                 uint64_t* peak_words) {
+                 uint64_t* peak_words, bool* zb_ok) {
   const uint64_t R = static_cast<uint64_t>(g->dev.R), C = static_cast<uint64_t>(g->dev.C);
   const uint64_t n = static_cast<uint64_t>(g->dev.n);
   auto words = [&](uint64_t W) {
@@ -244,7 +245,8 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
   };
   int W = cfg->points_per_batch ? cfg->points_per_batch : 64;
   while (static_cast<uint64_t>(W) > range && W > 1) W >>= 1;
-  if (cfg->points_per_batch == 0) {
+  uint64_t budget = UINT64_MAX;
+  {
     size_t free_b = 0, total_b = 0;
     TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
     int dev = 0;
@@ -256,10 +258,15 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
       cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
       if (reserved > used) free_b += reserved - used;
     }
-    const uint64_t budget = static_cast<uint64_t>(free_b * 0.92) / 8;
-    while (W > 1 && (words(W) > cfg->memory_cap_words || words(W) > budget)) W >>= 1;
+    budget = static_cast<uint64_t>(free_b * 0.92) / 8;
+    if (cfg->points_per_batch == 0)
+      while (W > 1 && (words(W) > cfg->memory_cap_words || words(W) > budget)) W >>= 1;
   }
-  *peak_words = words(W);
+  // z table only when small next to the state (n <= R/8) and it fits
+  const uint64_t zw = n * static_cast<uint64_t>(W);
+  *zb_ok = k >= 2 && n * 8 <= R && words(W) + zw <= budget &&
+           words(W) + zw <= cfg->memory_cap_words;
+  *peak_words = words(W) + (*zb_ok ? zw : 0);
   if (words(W) > cfg->memory_cap_words)
     throw CapError("sieve memory cap exceeded: needs " + std::to_string(words(W)) +
                    " field words, cap " + std::to_string(cfg->memory_cap_words));
@@ -279,7 +286,8 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   p_end = std::min(p_end, P);
   if (p_begin >= p_end) return;
   uint64_t peak = 0;
-  const int W = choose_width(g, k, p_end - p_begin, cfg, &peak);
+  bool zb_ok = false;
+  const int W = choose_width(g, k, p_end - p_begin, cfg, &peak, &zb_ok);
   if (peak_out) *peak_out = peak;
   const int32_t n = g->dev.n;
 
@@ -313,13 +321,12 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   lp.anchor_source = anchor_source;
   lp.agg = agg.as<uint64_t>();
   if (const char* e = std::getenv("TSV_YMUL"))
-    lp.ymul = std::strcmp(e, "holes") == 0 ? 1 : std::strcmp(e, "grouped") == 0 ? 2 : 0;
-  // The wide kernel's level-2 base case reads z_tail^A for every arc: when
-  // the per-batch table z[u][w] is small next to the state (n*W <= R*W/8,
-  // <= 4 GB) it is materialized once per batch and gathered like a state row.
+    lp.ymul = std::strcmp(e, "holes") == 0 ? 1 : 0;
+  // Level 2 reads z_tail^A for every arc and the run-end products z_head^A:
+  // when the per-batch table z[u][w] is small next to the state (n <= R/8)
+  // and fits, it is materialized once per batch and gathered like a state row.
   const uint64_t zb_bytes = static_cast<uint64_t>(n) * W * 8;
-  const bool use_zb = W >= 32 && lp.ymul != 2 && zb_bytes <= (4ull << 30) &&
-                      static_cast<uint64_t>(n) * 8 <= static_cast<uint64_t>(g->dev.R);
+  const bool use_zb = zb_ok;
   DevBuf zb(use_zb ? zb_bytes : 8, st);
   for (uint64_t pb = p_begin; pb < p_end; pb += W) {
     lp.b = batch_shape(W);
@@ -331,8 +338,9 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
     }
     uint64_t* cur = s0.as<uint64_t>();
     uint64_t* prev = s1.as<uint64_t>();
-    // the wide kernel produces level k fused with the readout
-    const bool fuse_last = W >= 32 && lp.ymul != 2 && !std::getenv("TSV_NO_FUSED_READOUT");
+    // level k is produced fused with the readout (TSV_NO_FUSED_READOUT=1
+    // keeps the separate readout, for cross-checks)
+    const bool fuse_last = !std::getenv("TSV_NO_FUSED_READOUT");
     for (int ell = 2; ell <= k; ++ell) {
       lp.ell = ell;
       lp.s_prev = prev;

@@ -149,6 +149,28 @@ def test_hub_vertices_split_across_chunks(cuda_device):
     assert _oracle_vs_gpu(n, u, v, ts, False, colors, [1, 2, 3], 5) >= 0
 
 
+@pytest.mark.parametrize("env", [{"TSV_NO_FUSED_READOUT": "1"}, {"TSV_NO_SKIP_UNREF": "1"},
+                                 {"TSV_YMUL": "holes"}])
+@pytest.mark.parametrize("ppb", [4, 16, 64])
+def test_engine_paths_agree(cuda_device, monkeypatch, env, ppb):
+    """The measurement switches (separate readout kernel instead of the
+    fused level k, storing every run's S, the holes product for y) give the
+    oracle's accumulators too, for the grouped and the wide kernel, with
+    hub vertices split across chunks and horizons below t."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    rng = np.random.default_rng(31)
+    n, m, t = 200, 6000, 40
+    u = rng.integers(0, n, m)
+    v = np.where(rng.random(m) < 0.4, 0, rng.integers(0, n, m))
+    ts = rng.integers(1, t + 1, m)
+    colors = rng.integers(1, 4, n)
+    for motif, seed, mt in (([1, 1, 2, 3], 3, None), ([1, 2, 3, 1, 2], 8, 25),
+                            ([1, 2, 3, 1, 2, 3], 11, 33)):
+        _oracle_vs_gpu(n, u, v, ts, True, colors, motif, seed, max_ts=mt, ppb=ppb)
+    _oracle_vs_gpu(n, u, v, ts, False, colors, [1, 2, 3], 5, max_ts=20, ppb=ppb)
+
+
 def test_c2_shape_small_scale_vs_oracle(cuda_device):
     inst = synth.make_config(2, scale=0.01)   # n=1e3, m=1e4, k=6 PathMotif
     k, col, motif, anchor = synth.effective_query(inst)
