@@ -187,7 +187,7 @@ def config_json(inst, world, args):
             "sieve_points": 1 << k_eff, "repetitions": REPS[args.config],
             "updates_per_step": inst.updates() * REPS[args.config],
             "parallelism": f"sieve-point sharding x{world}",
-            "l2": "working set > L2 (state buffers 2*R*W*8 B, see DESIGN.md)"}
+            "l2": "working set > L2 (state buffers 2*S*W*8 B, S = referenced runs, see DESIGN.md)"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -276,7 +276,7 @@ def main():
     lvl_n, lvl_ms = _native.Profile.get("level")
     last_n, _ = _native.Profile.get("level_last")
     grouped = False
-    if not lvl_n:  # W < 32: the grouped kernel (no fused readout, every run stored)
+    if not lvl_n:  # W < 32: the grouped kernel
         lvl_n, lvl_ms = _native.Profile.get("level_grouped")
         grouped = bool(lvl_n)
     all_n, all_ms = _native.Profile.get(None)
@@ -307,7 +307,7 @@ def main():
         # algorithmic bytes: one 8-B predecessor-state gather per arc with a
         # src and one 8-B state store per referenced run, per sieve point
         mid_levels = (k - 2) - (1 if last_n else 0)
-        words = g.info.arcs_with_src + (g.info.runs if grouped else g.info.runs_referenced)
+        words = g.info.arcs_with_src + g.info.runs_referenced
         alg_bytes = 8 * words * mid_levels * my_points * args.steps / lvl_n
         avg_ms = lvl_ms / lvl_n
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
@@ -325,7 +325,7 @@ def main():
             prof = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                "kernel": ("k_level (grouped, W < 32, 3 <= l <= k)" if grouped
+                "kernel": ("k_level (grouped, W < 32, 3 <= l < k)" if grouped
                            else "k_level_wide (3 <= l < k)"), "avg_launch_ms": avg_ms,
                 "launch_share_of_step": lvl_ms / max(all_ms, 1e-9),
                 "alg_bytes_per_launch": alg_bytes}

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <stdexcept>
 
 #include "engine.hpp"
 #include "layout.hpp"
@@ -493,6 +494,71 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
   release(hd[1]);
   release(ix[0]);
   release(ix[1]);
+}
+
+namespace {
+
+__global__ void k_mark_src(int64_t A, const int32_t* __restrict__ arc_src,
+                           int32_t* __restrict__ flag, unsigned long long* counts) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int32_t s = a < A ? arc_src[a] : -1;
+  if (s >= 0) flag[s] = 1;
+  const unsigned c = __popc(__ballot_sync(0xffffffffu, s >= 0));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts, static_cast<unsigned long long>(c));
+}
+
+__global__ void k_slots(int64_t R, const int32_t* __restrict__ flag,
+                        const int32_t* __restrict__ excl, int32_t* __restrict__ slot,
+                        unsigned long long* counts) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  slot[r] = flag[r] ? excl[r] : -1;
+  if (r == R - 1) counts[1] = static_cast<unsigned long long>(excl[r] + flag[r]);
+}
+
+__global__ void k_src_to_slot(int64_t A, int32_t* __restrict__ arc_src,
+                              const int32_t* __restrict__ slot) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  const int32_t s = arc_src[a];
+  if (s >= 0) arc_src[a] = slot[s];
+}
+
+}  // namespace
+
+SlotCounts build_run_slots(int64_t A, int64_t R, int32_t* arc_src, int32_t* run_slot,
+                           cudaStream_t st) {
+  SlotCounts out;
+  if (R == 0) return out;
+  constexpr int kT = 256;
+  auto nblk = [](int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); };
+  int32_t *flag = nullptr, *excl = nullptr;
+  unsigned long long* counts = nullptr;
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, flag, excl, R, st);
+  if (cudaMallocAsync(&flag, R * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&excl, R * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&counts, 16, st) != cudaSuccess ||
+      cudaMallocAsync(&tmp, tmp_bytes ? tmp_bytes : 8, st) != cudaSuccess)
+    throw std::runtime_error("state slots: out of device memory");
+  cudaMemsetAsync(flag, 0, R * 4, st);
+  cudaMemsetAsync(counts, 0, 16, st);
+  if (A) k_mark_src<<<nblk(A), kT, 0, st>>>(A, arc_src, flag, counts);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, excl, R, st);
+  k_slots<<<nblk(R), kT, 0, st>>>(R, flag, excl, run_slot, counts);
+  if (A) k_src_to_slot<<<nblk(A), kT, 0, st>>>(A, arc_src, run_slot);
+  unsigned long long hc[2] = {0, 0};
+  cudaMemcpyAsync(hc, counts, 16, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(flag, st);
+  cudaFreeAsync(excl, st);
+  cudaFreeAsync(counts, st);
+  cudaFreeAsync(tmp, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    throw std::runtime_error("state slots: device error");
+  out.arcs_with_src = static_cast<int64_t>(hc[0]);
+  out.slots = static_cast<int64_t>(hc[1]);
+  return out;
 }
 
 }  // namespace tsv

@@ -22,9 +22,11 @@ struct DevGraph {
   const uint8_t* chunk_carry = nullptr;
   const int32_t* carry_list = nullptr;
   int32_t ncarry = 0;
-  // run_ref[r] = 1 iff some arc has arc_src == r: S_l of the other runs is
-  // never read by level l+1, so below level k it is neither formed nor stored
-  const uint8_t* run_ref = nullptr;
+  // State slots: S_l of run r is read at level l+1 only through some arc's
+  // src, so only such runs get S_l, stored at row run_slot[r] (their rank in
+  // run order; -1 = never read).  arc_src holds SLOTS, not run indices.
+  const int32_t* run_slot = nullptr;
+  int64_t S = 0;  // state rows = referenced runs
 };
 
 // One sieve-point batch [pb, pe) of W = lanes * ppt consecutive points.
@@ -46,8 +48,8 @@ struct LevelParams {
   uint64_t seed = 1;
   int32_t anchor_source = -1;
   Batch b;
-  const uint64_t* s_prev = nullptr;  // R x W (level ell-1), unused at ell=2
-  uint64_t* s_cur = nullptr;         // R x W (level ell)
+  const uint64_t* s_prev = nullptr;  // S x W (level ell-1), unused at ell=2
+  uint64_t* s_cur = nullptr;         // S x W (level ell)
   uint64_t* agg = nullptr;           // C x W chunk tail aggregates
   // y-multiply path of the wide kernel: 0 = smem tables (default), 1 = holes
   // general product.  Set from TSV_YMUL=holes for measurements.
@@ -55,7 +57,6 @@ struct LevelParams {
   // Level k fused with the readout (wide kernel only): no S_k is stored;
   // acc[u] ^= XOR_w z_u * (XOR of u's arc products with ts <= max_ts).
   bool last = false;
-  bool skip_unref = false;  // l < k: only runs in run_ref get S_l
   int32_t max_ts = 0;
   uint64_t* acc = nullptr;
 };
@@ -137,14 +138,16 @@ void launch_level(const LevelParams& p, cudaStream_t st);
 void launch_fixup(const LevelParams& p, cudaStream_t st);
 void launch_zbatch(int32_t n, const uint64_t* zj, int k, const Batch& b, uint64_t* zb,
                    cudaStream_t st);
-void launch_readout(const DevGraph& g, int32_t max_ts, const uint64_t* s,
-                    int W, uint64_t* acc, cudaStream_t st);
 void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
                uint64_t* acc, cudaStream_t st);
-// Marks run_ref and counts (arcs with a src, referenced runs) into
-// counts[0..1] (device, zeroed here).
-void launch_run_ref(int64_t A, int64_t R, const int32_t* arc_src, uint8_t* run_ref,
-                    unsigned long long* counts, cudaStream_t st);
+// State slots (build_kernels.cu): run_slot[r] = rank of r among the runs
+// some arc reads (else -1) and arc_src rewritten from run indices to slots.
+// Returns {arcs with a src, referenced runs}; synchronizes `st`.
+struct SlotCounts {
+  int64_t arcs_with_src = 0, slots = 0;
+};
+SlotCounts build_run_slots(int64_t A, int64_t R, int32_t* arc_src, int32_t* run_slot,
+                           cudaStream_t st);
 void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n,
                         uint64_t* out, cudaStream_t st);
 void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,

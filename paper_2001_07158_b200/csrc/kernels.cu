@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     bool live = lane < nb && sidx >= 0;
     if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
     bool push;
+    int32_t slot = -1;
     if (LAST) {
       // last arc of its vertex (within this chunk) with ts <= max_ts
       const int32_t myts = lane < nb ? __ldg(P.g.run_ts + myrun) : 0;
@@ -167,11 +168,12 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
       live = live && myts <= P.max_ts;
       push = lane < nb && myts <= P.max_ts && (chunk_end || (nmeta & kVStart) || nts > P.max_ts);
     } else {
-      push = lane < nb && (meta & kRunEnd) && (!P.skip_unref || __ldg(P.g.run_ref + myrun));
+      slot = (lane < nb && (meta & kRunEnd)) ? __ldg(P.g.run_slot + myrun) : -1;
+      push = slot >= 0;
     }
     s_src[wib][lane] = sidx;
     s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | (live ? kLive : 0u) | (push ? kPush : 0u);
-    s_run[wib][lane] = myrun;
+    s_run[wib][lane] = slot;
     s_head[wib][lane] = head;
     run_ctr += __popc(ends);
     __syncwarp();
@@ -322,7 +324,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, TSV_WIDE_MINB(PPT))
   __shared__ uint64_t s_y[kWideWarps][32];
   __shared__ int32_t s_src[kWideWarps][32];
   __shared__ uint32_t s_meta[kWideWarps][32];
-  __shared__ int32_t s_run[kWideWarps][32];  // LAST: the arc's timestamp
+  __shared__ int32_t s_run[kWideWarps][32];  // state slot of the arc's run
   __shared__ int32_t s_head[kWideWarps][32];
   __shared__ __align__(256) uint64_t s_tab[YTAB ? kWideWarps : 1][256];
   __shared__ uint32_t s_zs[LAST ? 1 : kWideWarps][PPT][12][32];  // split z_head^A per lane
@@ -368,13 +370,14 @@ __global__ void __launch_bounds__(kWideWarps * 32, TSV_WIDE_MINB(PPT))
     // flags plus kRef = "this run's S is read by the next level" and kLive =
     // "this arc's product can be nonzero" (it has a predecessor state, comes
     // from the anchor source at level 2, and at level k lies within max_ts).
-    const uint32_t ref = (!LAST && lane < nb && (meta & kRunEnd) &&
-                          (!P.skip_unref || __ldg(P.g.run_ref + myrun))) ? kRef : 0u;
+    const int32_t slot = (!LAST && lane < nb && (meta & kRunEnd)) ? __ldg(P.g.run_slot + myrun)
+                                                                  : -1;
+    const uint32_t ref = slot >= 0 ? kRef : 0u;
     bool live = lane < nb && sidx >= 0;
     if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
     if (LAST) live = live && __ldg(P.g.run_ts + myrun) <= P.max_ts;
     s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | ref | (live ? kLive : 0u);
-    s_run[wib][lane] = myrun;
+    s_run[wib][lane] = slot;  // state row of this run's S (run ends only)
     s_head[wib][lane] = head;
     run_ctr += __popc(ends);
     __syncwarp();
@@ -497,7 +500,10 @@ __global__ void k_fixup(const LevelParams P) {
       if (!P.g.chunk_carry[cc] || P.g.run_head[P.g.chunk_run[cc]] != head) break;
     }
     const uint64_t t = gf_mul(z_single(P.zj, P.k, head, A), carry);
-    for (int32_t r = r0; r < r1; ++r) P.s_cur[static_cast<int64_t>(r) * W + w] ^= t;
+    for (int32_t r = r0; r < r1; ++r) {
+      const int32_t slot = P.g.run_slot[r];
+      if (slot >= 0) P.s_cur[static_cast<int64_t>(slot) * W + w] ^= t;
+    }
   }
 }
 
@@ -512,26 +518,6 @@ __global__ void k_zbatch(int32_t n, const uint64_t* __restrict__ zj, int k, Batc
     const uint64_t A = b.pb + static_cast<uint64_t>(w);
     zb[u * W + w] = A < b.pe ? z_single(zj, k, static_cast<int32_t>(u), A) : 0ull;
   }
-}
-
-// acc[u] ^= XOR_w S_k[last run of u with ts <= max_ts][w]  (sieve.cpp:297-303)
-__global__ void k_readout(const DevGraph g, int32_t max_ts,
-                          const uint64_t* __restrict__ s, int W,
-                          uint64_t* __restrict__ acc) {
-  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (u >= g.n) return;
-  int32_t lo = g.vtx_run_off[u], hi = g.vtx_run_off[u + 1];
-  while (lo < hi) {  // first run with ts > max_ts
-    const int32_t mid = lo + (hi - lo) / 2;
-    if (g.run_ts[mid] <= max_ts) lo = mid + 1;
-    else hi = mid;
-  }
-  const int32_t r = lo - 1;
-  if (r < g.vtx_run_off[u]) return;
-  uint64_t x = 0;
-  const uint64_t* row = s + static_cast<int64_t>(r) * W;
-  for (int w = 0; w < W; ++w) x ^= row[w];
-  acc[u] ^= x;
 }
 
 // k = 1: P_{u,1} = z_u^A, readout is the subset sum (sieve.cpp:203-213).
@@ -562,22 +548,6 @@ __global__ void k_zj(int32_t n, int k, uint64_t seed,
     for (int j = 0; j < k; ++j) row[j] ^= gf_mul(v, wtab[(d - 1) * k + j]);
   }
   for (int j = 0; j < k; ++j) zj[u * k + j] = row[j];
-}
-
-__global__ void k_run_ref(int64_t A, const int32_t* __restrict__ arc_src,
-                          uint8_t* __restrict__ run_ref, unsigned long long* counts) {
-  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int32_t s = a < A ? arc_src[a] : -1;
-  if (s >= 0) run_ref[s] = 1;
-  const unsigned c = __popc(__ballot_sync(kFull, s >= 0));
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts, static_cast<unsigned long long>(c));
-}
-
-__global__ void k_count_ref(int64_t R, const uint8_t* __restrict__ run_ref,
-                            unsigned long long* counts) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const unsigned c = __popc(__ballot_sync(kFull, r < R && run_ref[r]));
-  if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts + 1, static_cast<unsigned long long>(c));
 }
 
 __global__ void k_xor_combine(const uint64_t* __restrict__ parts, int nparts,
@@ -680,14 +650,6 @@ void launch_zbatch(int32_t n, const uint64_t* zj, int k, const Batch& b, uint64_
   prof_end(st);
 }
 
-void launch_readout(const DevGraph& g, int32_t max_ts, const uint64_t* s, int W,
-                    uint64_t* acc, cudaStream_t st) {
-  if (g.n == 0) return;
-  prof_begin("readout", st);
-  k_readout<<<blocks_for(g.n, 256), 256, 0, st>>>(g, max_ts, s, W, acc);
-  prof_end(st);
-}
-
 void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
                uint64_t* acc, cudaStream_t st) {
   if (n == 0) return;
@@ -712,14 +674,6 @@ void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n, uint64_t* 
   const unsigned blocks = blocks_for(n, 256) < 148 * 8 ? blocks_for(n, 256) : 148 * 8;
   k_xor_combine<<<blocks, 256, 0, st>>>(parts, nparts, n, out);
   prof_end(st);
-}
-
-void launch_run_ref(int64_t A, int64_t R, const int32_t* arc_src, uint8_t* run_ref,
-                    unsigned long long* counts, cudaStream_t st) {
-  cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), st);
-  if (R > 0) cudaMemsetAsync(run_ref, 0, static_cast<size_t>(R), st);
-  if (A > 0) k_run_ref<<<blocks_for(A, 256), 256, 0, st>>>(A, arc_src, run_ref, counts);
-  if (R > 0) k_count_ref<<<blocks_for(R, 256), 256, 0, st>>>(R, run_ref, counts);
 }
 
 void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,

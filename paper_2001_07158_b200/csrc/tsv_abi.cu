@@ -238,10 +238,12 @@ tsv::Batch batch_shape(int W) {
 // *zb_ok: the per-batch z table (n*W words) also fits next to that working set.
 int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cfg,
                  uint64_t* peak_words, bool* zb_ok) {
+  // state rows = referenced runs (slots); R is kept for the z-table rule
   const uint64_t R = static_cast<uint64_t>(g->dev.R), C = static_cast<uint64_t>(g->dev.C);
+  const uint64_t S = static_cast<uint64_t>(g->dev.S);
   const uint64_t n = static_cast<uint64_t>(g->dev.n);
   auto words = [&](uint64_t W) {
-    return (k >= 2 ? 2 * R * W + C * W : 0) + n * static_cast<uint64_t>(k) + n;
+    return (k >= 2 ? 2 * S * W + C * W : 0) + n * static_cast<uint64_t>(k) + n;
   };
   int W = cfg->points_per_batch ? cfg->points_per_batch : 64;
   while (static_cast<uint64_t>(W) > range && W > 1) W >>= 1;
@@ -310,7 +312,7 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
     TSV_CUDA(cudaGetLastError());
     return;
   }
-  const size_t state_words = static_cast<size_t>(g->dev.R) * W;
+  const size_t state_words = static_cast<size_t>(std::max<int64_t>(g->dev.S, 1)) * W;
   DevBuf s0(state_words * 8, st), s1(state_words * 8, st),
       agg(static_cast<size_t>(g->dev.C) * W * 8, st);
   tsv::LevelParams lp;
@@ -338,15 +340,12 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
     }
     uint64_t* cur = s0.as<uint64_t>();
     uint64_t* prev = s1.as<uint64_t>();
-    // level k is produced fused with the readout (TSV_NO_FUSED_READOUT=1
-    // keeps the separate readout, for cross-checks)
-    const bool fuse_last = !std::getenv("TSV_NO_FUSED_READOUT");
+    // level k is produced fused with the readout
     for (int ell = 2; ell <= k; ++ell) {
       lp.ell = ell;
       lp.s_prev = prev;
       lp.s_cur = cur;
-      lp.last = fuse_last && ell == k;
-      lp.skip_unref = ell < k && !std::getenv("TSV_NO_SKIP_UNREF");
+      lp.last = ell == k;
       lp.max_ts = max_ts;
       lp.acc = d_acc;
       tsv::launch_level(lp, st);
@@ -354,7 +353,6 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
       tsv::launch_fixup(lp, st);
       std::swap(cur, prev);
     }
-    if (!fuse_last) tsv::launch_readout(g->dev, max_ts, prev, W, d_acc, st);
     TSV_CUDA(cudaGetLastError());
   }
 }
@@ -477,17 +475,13 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     d.chunk_carry = L.chunk_carry;
     d.carry_list = L.carry_list;
     d.ncarry = L.ncarry;
-    auto* rr = static_cast<uint8_t*>(alloc(std::max<int64_t>(L.R, 1)));
-    auto* cnt = static_cast<unsigned long long*>(alloc(16));
-    tsv::launch_run_ref(L.A, L.R, L.arc_src, rr, cnt, st);
-    unsigned long long hc[2] = {0, 0};
-    TSV_CUDA(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, st));
-    TSV_CUDA(cudaStreamSynchronize(st));
-    release(cnt);
-    g->arcs_with_src = static_cast<int64_t>(hc[0]);
-    g->runs_referenced = static_cast<int64_t>(hc[1]);
-    d.run_ref = rr;
-    g->device_bytes = 12 * L.A + 9 * L.R + 4 * (static_cast<int64_t>(n) + 1) + 12 * L.m +
+    auto* slots = static_cast<int32_t*>(alloc(std::max<int64_t>(L.R, 1) * 4));
+    const tsv::SlotCounts sc = tsv::build_run_slots(L.A, L.R, L.arc_src, slots, st);
+    g->arcs_with_src = sc.arcs_with_src;
+    g->runs_referenced = sc.slots;
+    d.run_slot = slots;
+    d.S = sc.slots;
+    g->device_bytes = 12 * L.A + 12 * L.R + 4 * (static_cast<int64_t>(n) + 1) + 12 * L.m +
                       17 * (L.C + 1);
     TSV_CUDA(cudaStreamSynchronize(st));
     g->owned = live;
@@ -553,17 +547,15 @@ static int graph_build_impl(int32_t n, int64_t m, const int32_t* u, const int32_
       d.chunk_carry = own_upload(g, L.chunk_carry);
       d.carry_list = own_upload(g, L.carry_list);
       d.ncarry = static_cast<int32_t>(L.carry_list.size());
-      uint8_t* rr = dalloc<uint8_t>(std::max<size_t>(L.run_head.size(), 1));
-      g->owned.push_back(rr);
-      g->device_bytes += static_cast<int64_t>(std::max<size_t>(L.run_head.size(), 1));
-      auto* cnt = dalloc<unsigned long long>(2);
-      tsv::launch_run_ref(d.A, d.R, d.arc_src, rr, cnt, nullptr);
-      unsigned long long hc[2] = {0, 0};
-      TSV_CUDA(cudaMemcpy(hc, cnt, 16, cudaMemcpyDeviceToHost));
-      cudaFree(cnt);
-      g->arcs_with_src = static_cast<int64_t>(hc[0]);
-      g->runs_referenced = static_cast<int64_t>(hc[1]);
-      d.run_ref = rr;
+      int32_t* slots = dalloc<int32_t>(std::max<size_t>(L.run_head.size(), 1));
+      g->owned.push_back(slots);
+      g->device_bytes += 4 * static_cast<int64_t>(std::max<size_t>(L.run_head.size(), 1));
+      const tsv::SlotCounts sc =
+          tsv::build_run_slots(d.A, d.R, const_cast<int32_t*>(d.arc_src), slots, nullptr);
+      g->arcs_with_src = sc.arcs_with_src;
+      g->runs_referenced = sc.slots;
+      d.run_slot = slots;
+      d.S = sc.slots;
       // release the host copies of the device layout (keep canonical edges)
       std::vector<int32_t>().swap(L.arc_src);
       std::vector<int32_t>().swap(L.arc_tail);

@@ -149,14 +149,13 @@ def test_hub_vertices_split_across_chunks(cuda_device):
     assert _oracle_vs_gpu(n, u, v, ts, False, colors, [1, 2, 3], 5) >= 0
 
 
-@pytest.mark.parametrize("env", [{"TSV_NO_FUSED_READOUT": "1"}, {"TSV_NO_SKIP_UNREF": "1"},
-                                 {"TSV_YMUL": "holes"}])
+@pytest.mark.parametrize("env", [{}, {"TSV_YMUL": "holes"}])
 @pytest.mark.parametrize("ppb", [4, 16, 64])
 def test_engine_paths_agree(cuda_device, monkeypatch, env, ppb):
-    """The measurement switches (separate readout kernel instead of the
-    fused level k, storing every run's S, the holes product for y) give the
-    oracle's accumulators too, for the grouped and the wide kernel, with
-    hub vertices split across chunks and horizons below t."""
+    """Grouped and wide kernels (and the wide kernel's holes product for y
+    instead of the tables) give the oracle's accumulators with hub vertices
+    split across chunks (carry fix-up into state slots), horizons below t
+    (fused readout of the last run <= max_ts) and compacted state rows."""
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
     rng = np.random.default_rng(31)
