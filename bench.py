@@ -32,8 +32,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 REPS = {1: 1, 2: 4, 3: 1, 4: 1, 5: 1}
-# 8 B predecessor-state read per arc + 8 B state write per run
-# (runs no arc of the next level reads are not stored: graph.info.runs_referenced)
+BYTES_PER_UPDATE = 16  # 8 B predecessor-state read + 8 B state write
 
 
 def peaks():
@@ -304,11 +303,14 @@ def main():
         # updates executed by the middle-level launches (3 <= l < k when level
         # k is fused with the readout, else 3 <= l <= k) of this rank in the
         # timed region
-        # algorithmic bytes: one 8-B predecessor-state gather per arc with a
-        # src and one 8-B state store per referenced run, per sieve point
+        # algorithmic bytes: 16 B per (arc, point) update --
+        # one 8-B predecessor-state read plus one 8-B state write -- times the
+        # updates of one middle-level launch.  The engine moves less (no state
+        # for runs no arc reads, no read for arcs without a predecessor): that
+        # shows as ncu `traffic` below the algorithmic figure.
         mid_levels = (k - 2) - (1 if last_n else 0)
-        words = g.info.arcs_with_src + g.info.runs_referenced
-        alg_bytes = 8 * words * mid_levels * my_points * args.steps / lvl_n
+        upd_launch = g.info.arcs * mid_levels * my_points * args.steps / lvl_n
+        alg_bytes = BYTES_PER_UPDATE * upd_launch
         avg_ms = lvl_ms / lvl_n
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
         # per-launch DRAM traffic and instruction counts of the same kernel on
@@ -342,8 +344,7 @@ def main():
                                 "peak": peak_issue, "frac": ach / peak_issue,
                                 "alu_pipe_frac_ncu": prof["alu_pipe_pct_active"] / 100,
                                 "thread_inst_per_update": 32 * prof["warp_inst_per_launch"] /
-                                (alg_bytes / 8 / (g.info.arcs_with_src + g.info.runs_referenced)
-                                 * g.info.arcs),
+                                upd_launch,
                                 "capture": prof["capture"]}
 
     # e2e through the public API with host buffers (graph build + shades +
