@@ -28,7 +28,7 @@ __device__ __forceinline__ uint64_t mul_v(uint64_t a, uint64_t b) {
 
 __global__ void k_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
                          uint64_t* out) {
-  __shared__ __align__(256) uint64_t tabs[8][256];
+  __shared__ __align__(256) uint64_t tabs[8][GfTable::kWords];
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (variant >= 4 && variant <= 6) {
@@ -78,7 +78,7 @@ __global__ void k_gf_bench(int64_t iters, uint64_t* sink) {
 // each lane multiplies PPT values by it.
 template <int PPT>
 __global__ void k_gf_bench_table(int64_t iters, uint64_t* sink) {
-  __shared__ __align__(256) uint64_t tabs[8][256];
+  __shared__ __align__(256) uint64_t tabs[8][GfTable::kWords];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   uint64_t a[PPT];

@@ -260,6 +260,14 @@ __device__ __forceinline__ uint64_t gf_mul_serial(uint64_t a, uint64_t b) {
 // tab: 256 u64 in shared memory, private to one warp.  build() must be called
 // by all 32 lanes of the warp with the same y; mul() by any lane afterwards.
 struct GfTable {
+  // Window i (the 16 multiples c * x^(4i) * y) starts at byte 136*i: the
+  // 8-byte pad per window spreads the build's stores over all banks (two
+  // wavefronts per 8-byte store instead of sixteen) at no instruction cost,
+  // and a window's 16 entries still span 128 contiguous bytes, so lookups
+  // stay conflict-free.  Table footprint: kWords u64, a multiple of 256
+  // bytes so that consecutive tables stay 256-byte aligned.
+  static constexpr int kWinBytes = 136;
+  static constexpr int kWords = (16 * kWinBytes + 255) / 256 * 256 / 8;
   uint64_t* tab;
 
   template <int OFF>
@@ -267,10 +275,10 @@ struct GfTable {
     asm volatile("st.shared.u64 [%0+%1], %2;" ::"r"(addr), "n"(OFF), "l"(v) : "memory");
   }
 
-  // Lane L writes entries 8*(L&1) .. 8*(L&1)+7 of window L>>1, i.e. the 64
-  // bytes at offset 64*L: c * x^(4i) * y for c = 8*(L&1) + e, e < 8.
-  // Branch-free (the window shift is a clamped PTX shift) and stored as
-  // eight 8-byte stores, so no register shuffling for vector stores.
+  // Lane L writes entries 8*(L&1) .. 8*(L&1)+7 of window i = L>>1, i.e.
+  // the 64 bytes at offset 136*i + 64*(L&1): c * x^(4i) * y for
+  // c = 8*(L&1) + e, e < 8.  Branch-free (the window shift is a clamped PTX
+  // shift) and stored as 8-byte stores.
   __device__ __forceinline__ void build(uint64_t y, int lane) {
     const uint32_t s = 4u * static_cast<uint32_t>(lane >> 1);
     uint64_t h, lo;
@@ -279,10 +287,8 @@ struct GfTable {
     const uint64_t B0 = lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4);  // y * x^s (s <= 60)
     const uint64_t B1 = gf_mulx(B0), B2 = gf_mulx(B1);
     const uint64_t base = (lane & 1) ? gf_mulx(B2) : 0ull;
-    // (A lane-rotated Gray-code store order that avoids the 16-way bank
-    // conflicts of these stores was measured 3% slower: the kernel is bound
-    // by the ALU pipe, not by shared-memory wavefronts.)
-    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) + 64u * lane;
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) +
+                       kWinBytes * static_cast<uint32_t>(lane >> 1) + 64u * (lane & 1);
     sts<0>(a, base);
     sts<8>(a, base ^ B0);
     sts<16>(a, base ^ B1);
@@ -295,7 +301,7 @@ struct GfTable {
 
   // Lookups: nibble j of s, scaled by 8, is placed into the low byte of the
   // table's shared-memory address with one byte permute (the table is
-  // 256-byte aligned); the window offset j*128 rides in the load immediate.
+  // 256-byte aligned); the window offset j*136 rides in the load immediate.
   template <int OFF>
   __device__ __forceinline__ static uint64_t lds(uint32_t addr) {
     uint64_t v;
@@ -307,14 +313,14 @@ struct GfTable {
   __device__ __forceinline__ static uint64_t word8(uint32_t w, uint32_t base) {
     const uint32_t e = shl_f(w, 8u) & 0x78787878u;          // nibbles 0,2,4,6 (x8)
     const uint32_t o = shr_f(w, 0x80000000u) & 0x78787878u; // nibbles 1,3,5,7 (x8)
-    uint64_t a = lds<(WIN + 0) * 128>(__byte_perm(e, base, 0x7650)) ^
-                 lds<(WIN + 1) * 128>(__byte_perm(o, base, 0x7650));
-    a ^= lds<(WIN + 2) * 128>(__byte_perm(e, base, 0x7651)) ^
-         lds<(WIN + 3) * 128>(__byte_perm(o, base, 0x7651));
-    a ^= lds<(WIN + 4) * 128>(__byte_perm(e, base, 0x7652)) ^
-         lds<(WIN + 5) * 128>(__byte_perm(o, base, 0x7652));
-    a ^= lds<(WIN + 6) * 128>(__byte_perm(e, base, 0x7653)) ^
-         lds<(WIN + 7) * 128>(__byte_perm(o, base, 0x7653));
+    uint64_t a = lds<(WIN + 0) * kWinBytes>(__byte_perm(e, base, 0x7650)) ^
+                 lds<(WIN + 1) * kWinBytes>(__byte_perm(o, base, 0x7650));
+    a ^= lds<(WIN + 2) * kWinBytes>(__byte_perm(e, base, 0x7651)) ^
+         lds<(WIN + 3) * kWinBytes>(__byte_perm(o, base, 0x7651));
+    a ^= lds<(WIN + 4) * kWinBytes>(__byte_perm(e, base, 0x7652)) ^
+         lds<(WIN + 5) * kWinBytes>(__byte_perm(o, base, 0x7652));
+    a ^= lds<(WIN + 6) * kWinBytes>(__byte_perm(e, base, 0x7653)) ^
+         lds<(WIN + 7) * kWinBytes>(__byte_perm(o, base, 0x7653));
     return a;
   }
 

@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, TSV_WIDE_MINB(PPT))
   __shared__ uint32_t s_meta[kWideWarps][32];
   __shared__ int32_t s_run[kWideWarps][32];  // state slot of the arc's run
   __shared__ int32_t s_head[kWideWarps][32];
-  __shared__ __align__(256) uint64_t s_tab[YTAB ? kWideWarps : 1][256];
+  __shared__ __align__(256) uint64_t s_tab[YTAB ? kWideWarps : 1][GfTable::kWords];
   __shared__ uint32_t s_zs[LAST ? 1 : kWideWarps][PPT][12][32];  // split z_head^A per lane
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;

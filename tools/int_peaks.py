@@ -1,7 +1,8 @@
 """Measure the integer-pipe peaks the roofline needs on the GPU box (the
 driver's MEASURED_PEAKS.json has none): mul.wide.u32 and
 3-input LOP3 throughput (tsv_gf_bench pipe probes), and GF(2^64) product
-throughput per multiply variant.  Writes profiles/int_pipe_peaks.json."""
+throughput per multiply variant.  Writes gpurun_out/int_pipe_peaks.json
+(committed as profiles/int_pipe_peaks.json)."""
 import json
 import os
 import sys
@@ -29,7 +30,8 @@ def main():
     clk = 1.965e9
     out["per_sm_per_clock"] = {k: v / (sm * clk) for k, v in out.items() if "ops/s" in k}
     out["note"] = "best of 3 launches, full grid, SM clock assumed at its 1965 MHz maximum"
-    with open(os.path.join(ROOT, "profiles", "int_pipe_peaks.json"), "w") as f:
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)  # copied to profiles/ by hand
+    with open(os.path.join(ROOT, "gpurun_out", "int_pipe_peaks.json"), "w") as f:
         json.dump(out, f, indent=1)
 
 
