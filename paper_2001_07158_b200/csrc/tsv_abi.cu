@@ -233,7 +233,7 @@ tsv::Batch batch_shape(int W) {
   return b;
 }
 
-// Points per batch: the largest power of two <= min(range, 64) whose
+// Points per batch: the largest power of two <= min(range, 128) whose
 // working set fits the word cap and free device memory.
 // *zb_ok: the per-batch z table (n*W words) also fits next to that working set.
 int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cfg,
@@ -245,7 +245,7 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
   auto words = [&](uint64_t W) {
     return (k >= 2 ? 2 * S * W + C * W : 0) + n * static_cast<uint64_t>(k) + n;
   };
-  int W = cfg->points_per_batch ? cfg->points_per_batch : 64;
+  int W = cfg->points_per_batch ? cfg->points_per_batch : 128;
   while (static_cast<uint64_t>(W) > range && W > 1) W >>= 1;
   uint64_t budget = UINT64_MAX;
   {
