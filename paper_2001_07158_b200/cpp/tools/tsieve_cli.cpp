@@ -434,6 +434,12 @@ Instance load_instance(const Opts& o) {
   cfg.lane_width = o.lanes;
   cfg.threads = resolve_threads(o.threads);
   cfg.device = o.device;
+  // The reference CLI leaves memory_cap_words at its library default (2^31
+  // words), which bounds the reference's dense n*W*(t+1) layers.  The
+  // engine's working set is O(referenced runs * W) in HBM and the batch width
+  // is already fitted to free device memory, so the CLI lifts the cap rather
+  // than shrink the batch (a library caller's cap is still honoured).
+  cfg.memory_cap_words = std::uint64_t{1} << 62;
   const bool eps = inst.loaded.graph.has_transition_times();
   if (o.edge_model == "auto")
     cfg.edge_model = o.delays_file.empty()
