@@ -67,11 +67,32 @@ int tsv_graph_build_canonical(int32_t n, int64_t m, const int32_t* u,
                               int directed, int32_t t, int device,
                               tsv_graph** out);
 
+/* Device mirror of an ALREADY canonical edge list under an edge model
+ * (EdgeModel, graph.hpp:179; sieve.cpp:179-186, 257-291): 0 instant,
+ * 1 transition times eps[m] (NULL = all 1), 2 vertex delays delays[n]
+ * (NULL = all 0), 3 both.  An arc departing at ts lands in slot
+ * ts + eps - 1 of its head and reads its tail's state at ts - delta(tail)
+ * (delta = delay, or 1 without a delay model).  Evaluations must use the
+ * same config edge_model.  Errors: eps < 1, negative delays, as for
+ * tsv_graph_build_canonical. */
+int tsv_graph_build_model(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                          const int32_t* ts, const int32_t* eps, const int32_t* delays,
+                          int directed, int32_t t, int edge_model, int device,
+                          tsv_graph** out);
+
 /* Host-only canonicalization (no device): the edge list TemporalGraph::build
  * keeps, in edge-id order.  Returns the kept count (<= m) or -1 on error. */
 int64_t tsv_canonical_edges(int32_t n, int64_t m, const int32_t* u,
                             const int32_t* v, const int32_t* ts, int directed,
                             int32_t* out_u, int32_t* out_v, int32_t* out_ts);
+
+/* Same, carrying per-edge transition times (eps may be NULL; out_eps may be
+ * NULL).  Among duplicate (ts,u,v) edges the survivor is the reference's
+ * (same std::sort permutation, graph.cpp:34-41). */
+int64_t tsv_canonical_edges_eps(int32_t n, int64_t m, const int32_t* u,
+                                const int32_t* v, const int32_t* ts,
+                                const int32_t* eps, int directed, int32_t* out_u,
+                                int32_t* out_v, int32_t* out_ts, int32_t* out_eps);
 
 /* Induced subgraph on the device (restrict_to, graph.cpp:483-494): edges with
  * ts <= max_ts whose endpoints are both kept (keep_vertex: n host bytes);
@@ -97,7 +118,8 @@ typedef struct {
   uint64_t seed;             /* SieveConfig::seed */
   int32_t field_bits;        /* must be 64 */
   int32_t lane_width;        /* accepted, results independent of it */
-  int32_t edge_model;        /* 0 = instant (the only model on this path) */
+  int32_t edge_model;        /* 0 instant, 1 transition, 2 delay, 3 both (the
+                                graph must be built for it) */
   int32_t points_per_batch;  /* 0 = engine choice; else power of two <= 128 */
   uint64_t memory_cap_words; /* SieveConfig::memory_cap_words */
 } tsv_config;

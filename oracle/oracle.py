@@ -92,6 +92,11 @@ def ref_lib():
                                           C.c_int32, C.c_int32, _u64p,
                                           C.POINTER(C.c_uint64), C.POINTER(C.c_int64),
                                           C.POINTER(C.c_int32)]
+        lib.ref_eval_temporal_model.restype = C.c_int64
+        lib.ref_eval_temporal_model.argtypes = [
+            C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_void_p, C.c_void_p, C.c_int,
+            C.c_int32, _i32p, _i32p, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+            C.c_int32, C.c_int32, _u64p, C.POINTER(C.c_uint64), _i32p, _i32p, _i32p, _i32p]
         lib.ref_solve.restype = C.c_int64
         lib.ref_solve.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_int, C.c_int32,
                                   _i32p, C.c_char_p, _i32p, C.c_int32, C.c_int32, C.c_int32,
@@ -208,6 +213,31 @@ def ref_eval(n, u, v, ts, directed, colors, motif, max_ts=0, seed=1, lanes=8, th
         raise ValueError(ref_lib().ref_last_error().decode())
     return {"acc": acc[:n], "checksum": int(cs.value), "nflagged": int(nf.value),
             "global": bool(gl.value), "seconds": sec}
+
+
+def ref_eval_temporal_model(n, u, v, ts, eps, delays, directed, colors, motif, edge_model,
+                            seed=1, max_ts=0, lanes=8, anchor=(-1, -1), t=0):
+    """The reference's eval_temporal_sieve under an edge model (sieve.cpp:257-291).
+    Returns None when the query is infeasible, else accumulators, checksum and
+    the canonical edges (with transition times) of the reference's build."""
+    u, v, ts = _a32(u), _a32(v), _a32(ts)
+    m = len(u)
+    eps_a = _a32(eps) if eps is not None else None
+    del_a = _a32(delays) if delays is not None else None
+    acc = np.zeros(max(n, 1), np.uint64)
+    cs = C.c_uint64(0)
+    ou, ov, ot, oe = (np.zeros(max(m, 1), np.int32) for _ in range(4))
+    r = ref_lib().ref_eval_temporal_model(
+        n, m, u, v, ts, None if eps_a is None else eps_a.ctypes.data,
+        None if del_a is None else del_a.ctypes.data, int(directed), t, _a32(colors),
+        _a32(motif), len(motif), max_ts, seed, lanes, edge_model, anchor[0], anchor[1], acc,
+        C.byref(cs), ou, ov, ot, oe)
+    if r == -2:
+        return None
+    if r < 0:
+        raise ValueError(ref_lib().ref_last_error().decode())
+    return {"acc": acc[:n], "checksum": int(cs.value), "u": ou[:r], "v": ov[:r], "ts": ot[:r],
+            "eps": oe[:r]}
 
 
 def ref_solve(n, u, v, ts, directed, colors, problem, motif=(), k=0, source=-1, dest=-1,

@@ -76,6 +76,53 @@ uint64_t ref_draw_nonzero(uint64_t seed, uint64_t role, uint64_t a, uint64_t b,
 }
 
 // Canonical edge list of TemporalGraph::build; returns the kept count.
+// eval_temporal_sieve of the reference under an edge model: edges carry
+// transition times eps (NULL = 1), delays (NULL = none) are set on the
+// graph, edge_model 0..3 = instant / transition / delay / both.
+int64_t ref_eval_temporal_model(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                                const int32_t* ts, const int32_t* eps, const int32_t* delays,
+                                int directed, int32_t t, const int32_t* colors,
+                                const int32_t* motif, int32_t motif_len, int32_t max_ts,
+                                uint64_t seed, int32_t lanes, int32_t edge_model,
+                                int32_t anchor_source, int32_t anchor_sink, uint64_t* acc_out,
+                                uint64_t* checksum_out, int32_t* out_u, int32_t* out_v,
+                                int32_t* out_ts, int32_t* out_eps) {
+  try {
+    std::vector<TemporalEdge> edges(static_cast<size_t>(m));
+    for (int64_t i = 0; i < m; ++i) edges[i] = {u[i], v[i], ts[i], eps ? eps[i] : 1};
+    TemporalGraph g = TemporalGraph::build(n, std::move(edges), directed != 0, t);
+    if (delays) g.set_delays(std::vector<std::int32_t>(delays, delays + n));
+    for (int64_t i = 0; i < g.m(); ++i) {
+      const TemporalEdge& e = g.edge(static_cast<EdgeId>(i));
+      if (out_u) out_u[i] = e.u;
+      if (out_v) out_v[i] = e.v;
+      if (out_ts) out_ts[i] = e.ts;
+      if (out_eps) out_eps[i] = e.eps;
+    }
+    VertexColoring col = make_coloring(n, colors);
+    MotifQuery q = MotifQuery::from_multiset(std::vector<Color>(motif, motif + motif_len));
+    SieveConfig cfg;
+    cfg.seed = seed;
+    cfg.lane_width = lanes;
+    cfg.threads = 1;
+    cfg.memory_cap_words = ~std::uint64_t{0};
+    static const EdgeModel models[] = {EdgeModel::instant, EdgeModel::transition_only,
+                                       EdgeModel::delay_only, EdgeModel::transition_delay};
+    cfg.edge_model = models[edge_model & 3];
+    ShadeAssignment sh = build_shades(q, col, cfg);
+    if (!sh.feasible) return -2;
+    if (max_ts <= 0) max_ts = g.t();
+    SieveOutcome out = eval_temporal_sieve(g, motif_len, max_ts, sh, cfg,
+                                           AnchorSpec{anchor_source, anchor_sink});
+    for (int32_t i = 0; i < n; ++i) acc_out[i] = out.accumulators[i];
+    *checksum_out = out.checksum;
+    return g.m();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 int64_t ref_canonical_edges(int32_t n, int64_t m, const int32_t* u,
                             const int32_t* v, const int32_t* ts, int directed,
                             int32_t* out_u, int32_t* out_v, int32_t* out_ts) {

@@ -7,13 +7,13 @@ in include/tsv.h.  The C++ drop-in (same headers as the reference) and the
 """
 from .graph import (LoadResult, MotifQuery, TemporalGraph, VertexColoring,  # noqa: F401
                     load_graph, restrict_to, save_colors, save_graph)
-from .sieve import (AnchorSpec, DeviceShades, SieveConfig, SieveOutcome,  # noqa: F401
-                    ShadeAssignment, build_shades, eval_points_device, eval_temporal_sieve,
+from .sieve import (EDGE_MODELS, AnchorSpec, DeviceShades, SieveConfig,  # noqa: F401
+                    SieveOutcome, ShadeAssignment, build_shades, eval_points_device, eval_temporal_sieve,
                     false_negative_bound, finalize, xor_combine_device)
 
 __all__ = [
     "TemporalGraph", "VertexColoring", "MotifQuery", "LoadResult", "load_graph", "restrict_to",
     "save_graph", "save_colors", "SieveConfig", "ShadeAssignment", "AnchorSpec", "SieveOutcome",
     "build_shades", "eval_temporal_sieve", "false_negative_bound", "DeviceShades",
-    "eval_points_device", "xor_combine_device", "finalize",
+    "eval_points_device", "xor_combine_device", "finalize", "EDGE_MODELS",
 ]

@@ -61,6 +61,11 @@ def lib():
     L.tsv_version.restype = C.c_char_p
     L.tsv_graph_build.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_int,
                                   C.c_int32, C.c_int, C.POINTER(vp)]
+    L.tsv_graph_build_model.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, vp, vp,
+                                        C.c_int, C.c_int32, C.c_int, C.c_int, C.POINTER(vp)]
+    L.tsv_canonical_edges_eps.restype = C.c_int64
+    L.tsv_canonical_edges_eps.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, vp,
+                                          C.c_int, _i32p, _i32p, _i32p, _i32p]
     L.tsv_canonical_edges.restype = C.c_int64
     L.tsv_canonical_edges.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_int,
                                       _i32p, _i32p, _i32p]
@@ -113,6 +118,21 @@ def canonical_edges(n, u, v, ts, directed):
     if w < 0:
         raise ValueError(lib().tsv_last_error().decode())
     return ou[:w].copy(), ov[:w].copy(), ot[:w].copy()
+
+
+def canonical_edges_eps(n, u, v, ts, eps, directed):
+    """tsv_canonical_edges_eps: canonical edges plus their transition times."""
+    u = np.ascontiguousarray(u, dtype=np.int32)
+    v = np.ascontiguousarray(v, dtype=np.int32)
+    ts = np.ascontiguousarray(ts, dtype=np.int32)
+    e = None if eps is None else np.ascontiguousarray(eps, dtype=np.int32)
+    m = len(u)
+    ou, ov, ot, oe = (np.zeros(max(m, 1), np.int32) for _ in range(4))
+    w = lib().tsv_canonical_edges_eps(int(n), m, u, v, ts, None if e is None else e.ctypes.data,
+                                      int(bool(directed)), ou, ov, ot, oe)
+    if w < 0:
+        raise ValueError(lib().tsv_last_error().decode())
+    return ou[:w].copy(), ov[:w].copy(), ot[:w].copy(), oe[:w].copy()
 
 
 def gf_mul_device(a, b, variant: int = 0):

@@ -8,6 +8,11 @@
 //   arcs             (head, tail, edge) stably sorted by head over edge
 //                    order = (head, ts) order; runs = (head, ts) groups
 //   arc_src          tail's last run with ts' < ts (binary search)
+//
+// Non-instant edge models (sieve.cpp:257-291; canonical input only): an arc
+// departing at ts lands in slot ts + eps - 1 of its head (runs are (head,
+// slot) groups) and reads its tail's state at ts - delta(tail), delta = the
+// vertex delay (delay models) or 1; at level 2 it needs ts - delta >= 0.
 //   chunks           fixed arc ranges; a vertex split by a chunk boundary is
 //                    repaired by k_fixup, exactly like a split hub
 //
@@ -132,10 +137,45 @@ __global__ void k_make_arcs(int64_t m, int directed, const int32_t* __restrict__
   }
 }
 
-// After the stable sort by head: tail/edge/ts of every arc, run starts.
+// Landing slot of edge e: ts + eps - 1 under transition-time models.
+__device__ __forceinline__ int32_t slot_of(const int32_t* __restrict__ ets,
+                                           const int32_t* __restrict__ eps, uint32_t e) {
+  if (!eps) return ets[e];
+  const int64_t s = static_cast<int64_t>(ets[e]) + eps[e] - 1;
+  return s > INT32_MAX ? INT32_MAX : static_cast<int32_t>(s);
+}
+
+// (head << 32 | slot) keys of the arcs in edge order (transition models,
+// where slots are not monotone in edge order)
+__global__ void k_arc_keys(int64_t m, int directed, const int32_t* __restrict__ eu,
+                           const int32_t* __restrict__ ev, const int32_t* __restrict__ ets,
+                           const int32_t* __restrict__ eps, uint64_t* __restrict__ key,
+                           uint32_t* __restrict__ idx) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const uint64_t s = static_cast<uint32_t>(slot_of(ets, eps, static_cast<uint32_t>(i)));
+  if (directed) {
+    key[i] = (static_cast<uint64_t>(ev[i]) << 32) | s;
+    idx[i] = static_cast<uint32_t>(i);
+  } else {
+    key[2 * i] = (static_cast<uint64_t>(ev[i]) << 32) | s;
+    idx[2 * i] = static_cast<uint32_t>(2 * i);
+    key[2 * i + 1] = (static_cast<uint64_t>(eu[i]) << 32) | s;
+    idx[2 * i + 1] = static_cast<uint32_t>(2 * i + 1);
+  }
+}
+
+__global__ void k_key_heads(int64_t A, const uint64_t* __restrict__ key,
+                            uint32_t* __restrict__ head) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < A) head[j] = static_cast<uint32_t>(key[j] >> 32);
+}
+
+// After the sort by (head, slot): tail/edge/slot of every arc, run starts.
 __global__ void k_arc_fields(int64_t A, int directed, const uint32_t* __restrict__ head,
                              const uint32_t* __restrict__ idx, const int32_t* __restrict__ eu,
                              const int32_t* __restrict__ ev, const int32_t* __restrict__ ets,
+                             const int32_t* __restrict__ eps,
                              int32_t* __restrict__ tail, int32_t* __restrict__ edge,
                              int32_t* __restrict__ ats, int32_t* __restrict__ run_start) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -145,12 +185,12 @@ __global__ void k_arc_fields(int64_t A, int directed, const uint32_t* __restrict
   const bool second = !directed && (a & 1u);
   tail[j] = second ? ev[e] : eu[e];
   edge[j] = static_cast<int32_t>(e);
-  const int32_t t = ets[e];
+  const int32_t t = slot_of(ets, eps, e);
   ats[j] = t;
   int32_t start = 1;
   if (j > 0) {
     const uint32_t pa = idx[j - 1];
-    const int32_t pt = ets[directed ? pa : (pa >> 1)];
+    const int32_t pt = slot_of(ets, eps, directed ? pa : (pa >> 1));
     start = (head[j] != head[j - 1] || pt != t) ? 1 : 0;
   }
   run_start[j] = start;
@@ -183,23 +223,27 @@ __global__ void k_vtx_off(int32_t n, int64_t R, const int32_t* __restrict__ run_
 }
 
 __global__ void k_arc_src_meta(int64_t A, const uint32_t* __restrict__ head,
-                               const int32_t* __restrict__ tail, const int32_t* __restrict__ edge,
-                               const int32_t* __restrict__ ats,
+                               int32_t* __restrict__ tail, const int32_t* __restrict__ edge,
+                               const int32_t* __restrict__ ets,
+                               const int32_t* __restrict__ delay,
                                const int32_t* __restrict__ run_start,
                                const int32_t* __restrict__ run_ts,
                                const int32_t* __restrict__ vtx_run_off,
                                int32_t* __restrict__ arc_src, uint32_t* __restrict__ arc_meta) {
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= A) return;
-  const int32_t x = tail[j], t = ats[j];
+  const int32_t x = tail[j];
+  // the tail's state is read at ts - delta (instant: ts - 1)
+  const int64_t back = static_cast<int64_t>(ets[edge[j]]) - (delay ? delay[x] : 1);
   int32_t lo = vtx_run_off[x], hi = vtx_run_off[x + 1];
   const int32_t base = lo;
-  while (lo < hi) {  // first run of x with ts >= t
+  while (lo < hi) {  // first run of x with slot > back
     const int32_t mid = lo + ((hi - lo) >> 1);
-    if (run_ts[mid] < t) lo = mid + 1;
+    if (run_ts[mid] <= back) lo = mid + 1;
     else hi = mid;
   }
   arc_src[j] = lo == base ? -1 : lo - 1;
+  if (back < 0) tail[j] = -1;  // level 2 reads z_tail only at ts - delta >= 0
   uint32_t meta = static_cast<uint32_t>(edge[j]);
   if (j == 0 || head[j] != head[j - 1]) meta |= kVStart;
   if (j + 1 == A || run_start[j + 1]) meta |= kRunEnd;
@@ -303,7 +347,8 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
                   int32_t n, bool directed, bool canonical, DeviceLayout& out,
                   BuildStatus* d_status, int sm_count, cudaStream_t st,
                   const std::function<void*(size_t)>& alloc,
-                  const std::function<void(void*)>& release) {
+                  const std::function<void(void*)>& release, const int32_t* d_eps,
+                  const int32_t* d_delay) {
   auto A32 = [&](int64_t cnt) { return static_cast<int32_t*>(alloc(std::max<int64_t>(cnt, 1) * 4)); };
   BuildStatus init{};
   init.first_bad_endpoint = INT64_MAX;
@@ -391,9 +436,23 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
                      static_cast<uint32_t*>(alloc(std::max<int64_t>(A, 1) * 4))};
   uint32_t* ix[2] = {static_cast<uint32_t*>(alloc(std::max<int64_t>(A, 1) * 4)),
                      static_cast<uint32_t*>(alloc(std::max<int64_t>(A, 1) * 4))};
-  if (mc) k_make_arcs<<<nblk(mc), kT, 0, st>>>(mc, directed ? 1 : 0, eu, ev, hd[0], ix[0]);
   cub::DoubleBuffer<uint32_t> bh(hd[0], hd[1]), bi(ix[0], ix[1]);
-  if (A) radix_pairs(bh, bi, A, bits_for(static_cast<uint64_t>(n)), st);
+  if (!d_eps) {
+    // stable by head over edge order = (head, ts) order
+    if (mc) k_make_arcs<<<nblk(mc), kT, 0, st>>>(mc, directed ? 1 : 0, eu, ev, hd[0], ix[0]);
+    if (A) radix_pairs(bh, bi, A, bits_for(static_cast<uint64_t>(n)), st);
+  } else {
+    // transition times: sort by (head, slot)
+    uint64_t* ky[2] = {static_cast<uint64_t*>(alloc(std::max<int64_t>(A, 1) * 8)),
+                       static_cast<uint64_t*>(alloc(std::max<int64_t>(A, 1) * 8))};
+    if (mc) k_arc_keys<<<nblk(mc), kT, 0, st>>>(mc, directed ? 1 : 0, eu, ev, ets, d_eps, ky[0], ix[0]);
+    cub::DoubleBuffer<uint64_t> bk(ky[0], ky[1]);
+    if (A) radix_pairs(bk, bi, A, 32 + bits_for(static_cast<uint64_t>(n)), st);
+    if (A) k_key_heads<<<nblk(A), kT, 0, st>>>(A, bk.Current(), bh.Current());
+    cudaStreamSynchronize(st);
+    release(ky[0]);
+    release(ky[1]);
+  }
   const uint32_t* head = bh.Current();
   int32_t* tail = A32(A);
   int32_t* edge = A32(A);
@@ -402,7 +461,7 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
   int32_t* run_incl = A32(A + 1);
   if (A)
     k_arc_fields<<<nblk(A), kT, 0, st>>>(A, directed ? 1 : 0, head, bi.Current(), eu, ev, ets,
-                                         tail, edge, ats, run_start);
+                                         d_eps, tail, edge, ats, run_start);
   {
     size_t tmp = 0;
     cub::DeviceScan::InclusiveSum(nullptr, tmp, run_start, run_incl, A, st);
@@ -423,8 +482,9 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
   out.arc_src = A32(A);
   out.arc_meta = reinterpret_cast<uint32_t*>(A32(A));
   if (A)
-    k_arc_src_meta<<<nblk(A), kT, 0, st>>>(A, head, tail, edge, ats, run_start, out.run_ts,
-                                           out.vtx_run_off, out.arc_src, out.arc_meta);
+    k_arc_src_meta<<<nblk(A), kT, 0, st>>>(A, head, tail, edge, ets, d_delay, run_start,
+                                           out.run_ts, out.vtx_run_off, out.arc_src,
+                                           out.arc_meta);
   out.arc_tail = tail;
 
   // ---- chunks ---------------------------------------------------------------

@@ -116,11 +116,14 @@ struct DeviceLayout {
 // canonical = the input is already canonical (validated, not re-sorted).
 // alloc/release manage device memory (stream-ordered); buffers still live at
 // return belong to `out`.  Errors are reported through *d_status.
+// d_eps (m, canonical input only) / d_delay (n): transition times and vertex
+// delays of a non-instant edge model, or nullptr.
 void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, int64_t m,
                   int32_t n, bool directed, bool canonical, DeviceLayout& out,
                   BuildStatus* d_status, int sm_count, cudaStream_t st,
                   const std::function<void*(size_t)>& alloc,
-                  const std::function<void(void*)>& release);
+                  const std::function<void(void*)>& release, const int32_t* d_eps = nullptr,
+                  const int32_t* d_delay = nullptr);
 
 // Order-preserving filter of a canonical edge list (restrict_to): keeps
 // edges with ts <= max_ts and both endpoints kept; returns the kept count.

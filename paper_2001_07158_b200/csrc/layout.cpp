@@ -10,13 +10,14 @@
 namespace tsv {
 
 void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
-                  const int32_t* ts, bool directed, int32_t t, HostLayout& L) {
+                  const int32_t* ts, bool directed, int32_t t, HostLayout& L,
+                  const int32_t* eps) {
   if (n < 0) throw std::invalid_argument("negative vertex count");
   L.n = n;
   L.directed = directed;
   L.dropped_self_loops = 0;
   struct E {
-    int32_t ts, u, v;
+    int32_t ts, u, v, eps;
   };
   std::vector<E> kept;
   kept.reserve(static_cast<size_t>(m));
@@ -30,7 +31,7 @@ void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
       continue;
     }
     if (!directed && a > b) std::swap(a, b);
-    kept.push_back({ts[i], a, b});
+    kept.push_back({ts[i], a, b, eps ? eps[i] : 1});
   }
   auto key_less = [](const E& x, const E& y) {
     if (x.ts != y.ts) return x.ts < y.ts;
@@ -38,7 +39,8 @@ void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
     return x.v < y.v;
   };
   // multiway-mergesort on all host cores for the 1e8-1e9-edge configs
-  if (kept.size() > (1u << 20))
+  // (transition times need std::sort's exact permutation for duplicates)
+  if (kept.size() > (1u << 20) && !eps)
     __gnu_parallel::sort(kept.begin(), kept.end(), key_less);
   else
     std::sort(kept.begin(), kept.end(), key_less);
@@ -56,10 +58,12 @@ void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
   L.eu.resize(w);
   L.ev.resize(w);
   L.ets.resize(w);
+  L.eeps.assign(eps ? w : 0, 1);
   for (size_t i = 0; i < w; ++i) {
     L.eu[i] = kept[i].u;
     L.ev[i] = kept[i].v;
     L.ets[i] = kept[i].ts;
+    if (eps) L.eeps[i] = kept[i].eps;
     max_ts = std::max(max_ts, kept[i].ts);
   }
   L.t = t > 0 ? t : std::max<int32_t>(max_ts, 1);

@@ -33,8 +33,8 @@ struct HostLayout {
   int32_t n = 0, t = 0;
   bool directed = false;
   int64_t dropped_self_loops = 0, dropped_duplicates = 0;
-  // canonical edges (edge id = index)
-  std::vector<int32_t> eu, ev, ets;
+  // canonical edges (edge id = index); eeps only when transition times given
+  std::vector<int32_t> eu, ev, ets, eeps;
   // vertex-major runs
   std::vector<int32_t> run_head, run_ts;
   std::vector<int32_t> vtx_run_off;  // n+1
@@ -50,8 +50,12 @@ struct HostLayout {
 
 // Canonical edges per graph.cpp:14-43.  Throws std::invalid_argument with the
 // reference's messages on range errors.  t == 0 takes the max timestamp.
+// eps (nullable): per-edge transition times carried to L.eeps; among
+// duplicate (ts,u,v) edges the one std::sort leaves first is kept, as in
+// the reference (same comparator and input sequence => same permutation).
 void canonicalize(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
-                  const int32_t* ts, bool directed, int32_t t, HostLayout& L);
+                  const int32_t* ts, bool directed, int32_t t, HostLayout& L,
+                  const int32_t* eps = nullptr);
 
 // Adopts an edge list that must already be canonical (strictly increasing
 // (ts,u,v), u != v, u < v when undirected); throws std::invalid_argument

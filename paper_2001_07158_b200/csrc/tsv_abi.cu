@@ -163,6 +163,7 @@ struct tsv_graph {
   int device = 0;
   int64_t device_bytes = 0;
   int64_t m = 0;                      // canonical edge count
+  int model = 0;                      // edge model the layout was built for
   int64_t arcs_with_src = 0, runs_referenced = 0;
   const int32_t* d_eu = nullptr;      // canonical edges on the device (device build)
   const int32_t* d_ev = nullptr;
@@ -214,8 +215,8 @@ void check_config(const tsv_config* cfg) {
   const int W = cfg->lane_width;
   if (W < 1 || W > 256 || (W & (W - 1)))
     throw std::invalid_argument("lane_width must be a power of two in [1,256]");
-  if (cfg->edge_model != 0)
-    throw std::invalid_argument("the B200 engine evaluates the instant edge model only");
+  if (cfg->edge_model < 0 || cfg->edge_model > 3)
+    throw std::invalid_argument("edge_model must be 0..3");
   const int ppb = cfg->points_per_batch;
   if (ppb != 0 && (ppb < 1 || ppb > 128 || (ppb & (ppb - 1))))
     throw std::invalid_argument("points_per_batch must be 0 or a power of two <= 128");
@@ -284,6 +285,10 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
   if (!sh || sh->n != g->dev.n || sh->k != k)
     throw std::invalid_argument("shade assignment built for a different graph");
+  if (cfg->edge_model != g->model)
+    throw std::invalid_argument("graph was built for edge model " + std::to_string(g->model) +
+                                ", config asks for " + std::to_string(cfg->edge_model) +
+                                " (tsv_graph_build_model)");
   const uint64_t P = 1ull << k;
   p_end = std::min(p_end, P);
   if (p_begin >= p_end) return;
@@ -384,7 +389,9 @@ void finalize_host(int32_t n, uint64_t* acc, int32_t sink, int k, tsv_outcome* o
 // to the graph.
 tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                               const int32_t* ts, bool directed, int32_t t, int device,
-                              bool canonical, bool on_device = false) {
+                              bool canonical, bool on_device = false,
+                              const int32_t* eps = nullptr, const int32_t* delays = nullptr,
+                              int model = 0) {
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   DeviceGuard dg(device);
   int sm_count = 0;  // (cudaGetDeviceProperties costs milliseconds per call)
@@ -406,6 +413,7 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
   };
   auto* g = new tsv_graph();
   g->device = device;
+  g->model = model;
   g->host.n = n;
   g->host.directed = directed;
   try {
@@ -417,10 +425,30 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
       TSV_CUDA(cudaMemcpyAsync(dv, v, m * 4, kind, st));
       TSV_CUDA(cudaMemcpyAsync(dts, ts, m * 4, kind, st));
     }
+    // edge model (sieve.cpp:179-186): transition times when model 1/3,
+    // vertex delays (0 when none were given) when model 2/3
+    const bool use_eps = model == 1 || model == 3, use_delay = model == 2 || model == 3;
+    int32_t *deps = nullptr, *ddel = nullptr;
+    if (use_eps) {
+      deps = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      if (m && eps) TSV_CUDA(cudaMemcpyAsync(deps, eps, m * 4, kind, st));
+      else if (m) {
+        std::vector<int32_t> ones(static_cast<size_t>(m), 1);
+        TSV_CUDA(cudaMemcpyAsync(deps, ones.data(), m * 4, cudaMemcpyHostToDevice, st));
+        TSV_CUDA(cudaStreamSynchronize(st));
+      }
+    }
+    if (use_delay) {
+      ddel = static_cast<int32_t*>(alloc(std::max<int64_t>(n, 1) * 4));
+      if (n && delays) TSV_CUDA(cudaMemcpyAsync(ddel, delays, static_cast<size_t>(n) * 4, kind, st));
+      else if (n) TSV_CUDA(cudaMemsetAsync(ddel, 0, static_cast<size_t>(n) * 4, st));
+    }
     auto* status = static_cast<tsv::BuildStatus*>(alloc(sizeof(tsv::BuildStatus)));
     tsv::DeviceLayout L;
     tsv::device_build(du, dv, dts, m, n, directed, canonical, L, status,
-                      sm_count, st, alloc, release);
+                      sm_count, st, alloc, release, deps, ddel);
+    if (deps) release(deps);
+    if (ddel) release(ddel);
     tsv::BuildStatus hs{};
     TSV_CUDA(cudaMemcpyAsync(&hs, status, sizeof(hs), cudaMemcpyDeviceToHost, st));
     TSV_CUDA(cudaStreamSynchronize(st));
@@ -506,16 +534,19 @@ const char* tsv_version(void) { return "tsv-b200 0.1 (sm_100a)"; }
 
 static int graph_build_impl(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                             const int32_t* ts, int directed, int32_t t, int device,
-                            tsv_graph** out, bool canonical) {
+                            tsv_graph** out, bool canonical, const int32_t* eps = nullptr,
+                            const int32_t* delays = nullptr, int model = 0) {
   return guard([&] {
     if (!out) throw std::invalid_argument("null output handle");
     *out = nullptr;
     if (m < 0) throw std::invalid_argument("negative edge count");
     if (m > 0 && (!u || !v || !ts)) throw std::invalid_argument("null edge arrays");
     if (n < 0) throw std::invalid_argument("negative vertex count");
+    if (model < 0 || model > 3) throw std::invalid_argument("edge_model must be 0..3");
     const char* hb = std::getenv("TSV_HOST_BUILD");
-    if (!(hb && hb[0] == '1')) {
-      *out = device_graph_build(n, m, u, v, ts, directed != 0, t, device, canonical);
+    if (model != 0 || !(hb && hb[0] == '1')) {
+      *out = device_graph_build(n, m, u, v, ts, directed != 0, t, device, canonical, false, eps,
+                                delays, model);
       return;
     }
     auto* g = new tsv_graph();
@@ -583,18 +614,48 @@ int tsv_graph_build_canonical(int32_t n, int64_t m, const int32_t* u, const int3
   return graph_build_impl(n, m, u, v, ts, directed, t, device, out, true);
 }
 
+int tsv_graph_build_model(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                          const int32_t* ts, const int32_t* eps, const int32_t* delays,
+                          int directed, int32_t t, int edge_model, int device,
+                          tsv_graph** out) {
+  if (edge_model != 0 && delays) {
+    for (int32_t x = 0; x < n; ++x)
+      if (delays[x] < 0) {
+        g_error = "negative vertex delay";
+        return TSV_ERR_INVALID;
+      }
+  }
+  if (eps)
+    for (int64_t i = 0; i < m; ++i)
+      if (eps[i] < 1) {
+        g_error = "transition time below 1";
+        return TSV_ERR_INVALID;
+      }
+  return graph_build_impl(n, m, u, v, ts, directed, t, device, out, true, eps, delays,
+                          edge_model);
+}
+
 int64_t tsv_canonical_edges(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                             const int32_t* ts, int directed, int32_t* out_u, int32_t* out_v,
                             int32_t* out_ts) {
+  return tsv_canonical_edges_eps(n, m, u, v, ts, nullptr, directed, out_u, out_v, out_ts,
+                                 nullptr);
+}
+
+int64_t tsv_canonical_edges_eps(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                                const int32_t* ts, const int32_t* eps, int directed,
+                                int32_t* out_u, int32_t* out_v, int32_t* out_ts,
+                                int32_t* out_eps) {
   int64_t kept = -1;
   int rc = guard([&] {
     tsv::HostLayout L;
-    tsv::canonicalize(n, m, u, v, ts, directed != 0, 0, L);
+    tsv::canonicalize(n, m, u, v, ts, directed != 0, 0, L, eps);
     kept = static_cast<int64_t>(L.eu.size());
     for (int64_t i = 0; i < kept; ++i) {
       out_u[i] = L.eu[i];
       out_v[i] = L.ev[i];
       out_ts[i] = L.ets[i];
+      if (out_eps) out_eps[i] = eps ? L.eeps[i] : 1;
     }
   });
   return rc == TSV_OK ? kept : -1;
@@ -606,6 +667,10 @@ int tsv_graph_restrict(const tsv_graph* g, const uint8_t* keep_vertex, int32_t m
     if (!g || !out || (g->host.n > 0 && !keep_vertex))
       throw std::invalid_argument("null argument");
     *out = nullptr;
+    if (g->model != 0)
+      throw std::invalid_argument(
+          "tsv_graph_restrict: graphs of non-instant edge models are rebuilt from the host "
+          "(tsv_graph_build_model)");
     DeviceGuard dg(g->device);
     cudaStream_t st = nullptr;
     TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));

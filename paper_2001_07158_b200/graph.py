@@ -40,6 +40,34 @@ class TemporalGraph:
         _native.check(_native.lib().tsv_graph_get_info(h, C.byref(info)))
         return TemporalGraph(h, info)
 
+    @staticmethod
+    def build_model(n: int, edges, directed: bool, edge_model: str, eps=None, delays=None,
+                    t: int = 0, device: int = 0) -> "TemporalGraph":
+        """TemporalGraph::build with transition times + set_delays, mirrored on
+        the device for one edge model (tsv_graph_build_model): an arc
+        departing at ts lands at ts + eps - 1 and reads its tail at
+        ts - delta(tail) (sieve.cpp:257-291)."""
+        from .sieve import EDGE_MODELS
+        model = EDGE_MODELS[edge_model]
+        u, v, ts = _edge_arrays(edges)
+        cu, cv, ct, ce = _native.canonical_edges_eps(n, u, v, ts, eps, directed)
+        dl = None if delays is None else np.ascontiguousarray(delays, dtype=np.int32)
+        if dl is not None and len(dl) != n:
+            raise ValueError("delay vector size mismatch")
+        h = C.c_void_p()
+        _native.check(_native.lib().tsv_graph_build_model(
+            int(n), len(cu), cu if len(cu) else np.zeros(1, np.int32),
+            cv if len(cv) else np.zeros(1, np.int32), ct if len(ct) else np.zeros(1, np.int32),
+            ce.ctypes.data if (eps is not None and len(ce)) else None,
+            None if dl is None else dl.ctypes.data, int(bool(directed)), int(t), model,
+            int(device), C.byref(h)))
+        info = _native.GraphInfo()
+        _native.check(_native.lib().tsv_graph_get_info(h, C.byref(info)))
+        g = TemporalGraph(h, info)
+        g._eps = ce
+        g._keep = (ce, dl)  # host copies outlive the handle's build
+        return g
+
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:

@@ -18,6 +18,11 @@ from . import _native
 from .graph import MotifQuery, TemporalGraph, VertexColoring
 
 
+# EdgeModel (graph.hpp:179) -> tsv_config.edge_model; the graph must be
+# built for the same model (TemporalGraph.build_model)
+EDGE_MODELS = {"instant": 0, "transition": 1, "delay": 2, "transition_delay": 3}
+
+
 @dataclass
 class SieveConfig:
     seed: int = 1
@@ -32,13 +37,13 @@ class SieveConfig:
     def to_native(self) -> _native.Config:
         if self.threads < 1:
             raise ValueError("threads must be >= 1")
-        if self.edge_model != "instant":
-            raise ValueError("the B200 engine evaluates the instant edge model only")
+        if self.edge_model not in EDGE_MODELS:
+            raise ValueError(f"unknown edge model {self.edge_model!r}")
         c = _native.Config()
         c.seed = self.seed & (2**64 - 1)
         c.field_bits = self.field_bits
         c.lane_width = self.lane_width
-        c.edge_model = 0
+        c.edge_model = EDGE_MODELS[self.edge_model]
         c.points_per_batch = self.points_per_batch
         c.memory_cap_words = min(int(self.memory_cap_words), 2**64 - 1)
         return c

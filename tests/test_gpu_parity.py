@@ -341,3 +341,61 @@ def test_full_size_properties(cuda_device, cfgno, scale):
                                  sh.vertex_shades, 3, anchor)
     assert np.array_equal(out.accumulators, acc) and out.checksum == cs2
     assert int(inst.planted[-1]) in out.flagged.tolist()
+
+
+@pytest.mark.parametrize("model", ["transition", "delay", "transition_delay", "instant"])
+def test_edge_models_vs_reference(cuda_device, model):
+    """Transition-time and vertex-delay models (sieve.cpp:257-291) against the
+    reference itself (oracle/_ref): an arc departing at ts lands at
+    ts + eps - 1 and reads its tail's state at ts - delta(tail); every kernel
+    shape, anchors, horizons below t, duplicates and self loops."""
+    rng = np.random.default_rng({"transition": 1, "delay": 2, "transition_delay": 3,
+                                 "instant": 4}[model])
+    nz = 0
+    for i in range(60):
+        n = int(rng.integers(3, 25))
+        m = int(rng.integers(1, 90))
+        u = rng.integers(0, n, m)
+        v = rng.integers(0, n, m)
+        ts = rng.integers(1, 12, m)
+        eps = rng.integers(1, 4, m)
+        delays = rng.integers(0, 4, n) if i % 4 else None
+        directed = bool(rng.integers(0, 2))
+        k = int(rng.integers(1, 6))
+        q = int(rng.integers(1, 4))
+        colors = rng.integers(1, q + 1, n)
+        motif = sorted(rng.integers(1, q + 1, k).tolist())
+        anchor = (-1, -1)
+        if i % 5 == 0:
+            s, d = rng.choice(n, 2, replace=False)
+            anchor = (int(s), int(d))
+        seed = int(rng.integers(1, 1 << 30))
+        ppb = int(rng.choice([0, 1, 4, 32, 64]))
+        want = O.ref_eval_temporal_model(n, u, v, ts, eps, delays, directed, colors, motif,
+                                         T.EDGE_MODELS[model], seed=seed, anchor=anchor)
+        if want is None:
+            continue
+        tmax = int(want["ts"].max()) if len(want["ts"]) else 1
+        max_ts = int(rng.integers(1, tmax + 1))
+        want = O.ref_eval_temporal_model(n, u, v, ts, eps, delays, directed, colors, motif,
+                                         T.EDGE_MODELS[model], seed=seed, anchor=anchor,
+                                         max_ts=max_ts)
+        g = T.TemporalGraph.build_model(n, (u, v, ts), directed, model, eps=eps, delays=delays)
+        cfg = T.SieveConfig(seed=seed, edge_model=model, points_per_batch=ppb)
+        sh = T.build_shades(T.MotifQuery.from_multiset(motif), T.VertexColoring(colors, q), cfg)
+        out = T.eval_temporal_sieve(g, k, max_ts, sh, cfg, T.AnchorSpec(*anchor))
+        assert np.array_equal(out.accumulators, want["acc"]), (model, i)
+        assert out.checksum == want["checksum"], (model, i)
+        nz += bool(out.global_nonzero)
+    assert nz > 5
+
+
+def test_edge_model_mismatch_is_rejected(cuda_device):
+    g = T.TemporalGraph.build_model(3, [(0, 1, 1), (1, 2, 3)], True, "transition", eps=[2, 1])
+    col = T.VertexColoring([1, 2, 3], 3)
+    cfg = T.SieveConfig()
+    sh = T.build_shades(T.MotifQuery.from_multiset([1, 2, 3]), col, cfg)
+    with pytest.raises(ValueError, match="edge model"):
+        T.eval_temporal_sieve(g, 3, g.t(), sh, cfg)
+    with pytest.raises(ValueError, match="transition time below 1"):
+        T.TemporalGraph.build_model(3, [(0, 1, 1)], True, "transition", eps=[0])

@@ -118,3 +118,27 @@ def test_synthetic_configs_have_distinct_edges(cfg):
 def test_synthetic_updates_formula():
     c1 = synth.make_config(1)
     assert c1.updates() == 10_000 * 4 * 32  # A (k-1) 2^k = 1.28e6
+
+
+def test_canonical_edges_carry_transition_times_like_reference():
+    """Transition times ride through canonicalization; among duplicate
+    (ts,u,v) edges the survivor is the reference's (graph.cpp:34-41)."""
+    from oracle import oracle
+    try:
+        oracle.ref_lib()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"oracle/_ref not built: {e}")
+    rng = np.random.default_rng(17)
+    for it in range(60):
+        n = int(rng.integers(2, 12))
+        m = int(rng.integers(0, 60))
+        u = rng.integers(0, n, m)
+        v = rng.integers(0, n, m)
+        ts = rng.integers(1, 6, m)
+        eps = rng.integers(1, 4, m)
+        directed = bool(it % 2)
+        want = oracle.ref_eval_temporal_model(n, u, v, ts, eps, None, directed, [1] * n, [1],
+                                              edge_model=1)
+        cu, cv, ct, ce = _native.canonical_edges_eps(n, u, v, ts, eps, directed)
+        assert cu.tolist() == want["u"].tolist() and cv.tolist() == want["v"].tolist()
+        assert ct.tolist() == want["ts"].tolist() and ce.tolist() == want["eps"].tolist()
