@@ -97,6 +97,8 @@ def ref_lib():
             C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_void_p, C.c_void_p, C.c_int,
             C.c_int32, _i32p, _i32p, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
             C.c_int32, C.c_int32, _u64p, C.POINTER(C.c_uint64), _i32p, _i32p, _i32p, _i32p]
+        lib.ref_set_model.restype = None
+        lib.ref_set_model.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32]
         lib.ref_solve.restype = C.c_int64
         lib.ref_solve.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_int, C.c_int32,
                                   _i32p, C.c_char_p, _i32p, C.c_int32, C.c_int32, C.c_int32,
@@ -238,6 +240,19 @@ def ref_eval_temporal_model(n, u, v, ts, eps, delays, directed, colors, motif, e
         raise ValueError(ref_lib().ref_last_error().decode())
     return {"acc": acc[:n], "checksum": int(cs.value), "u": ou[:r], "v": ov[:r], "ts": ot[:r],
             "eps": oe[:r]}
+
+
+def ref_solve_model(n, u, v, ts, eps, delays, edge_model, *args, **kw):
+    """ref_solve with transition times / vertex delays under an edge model."""
+    e = _a32(eps) if eps is not None else None
+    d = _a32(delays) if delays is not None else None
+    ref_lib().ref_set_model(None if e is None else e.ctypes.data, 0 if e is None else len(e),
+                            None if d is None else d.ctypes.data, 0 if d is None else len(d),
+                            int(edge_model))
+    try:
+        return ref_solve(n, u, v, ts, *args, **kw)
+    finally:
+        ref_lib().ref_set_model(None, 0, None, 0, 0)
 
 
 def ref_solve(n, u, v, ts, directed, colors, problem, motif=(), k=0, source=-1, dest=-1,

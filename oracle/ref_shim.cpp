@@ -34,12 +34,20 @@ namespace {
 
 std::string g_err;
 
+// Edge-model overrides for the next ref_solve (ref_set_model; test driver
+// state, cleared by ref_set_model(NULL, NULL, 0, 0)).
+std::vector<std::int32_t> g_eps, g_delays;
+int g_model = 0;
+
 TemporalGraph make_graph(int32_t n, int64_t m, const int32_t* u,
                          const int32_t* v, const int32_t* ts, int directed,
                          int32_t t) {
   std::vector<TemporalEdge> edges(static_cast<size_t>(m));
-  for (int64_t i = 0; i < m; ++i) edges[i] = {u[i], v[i], ts[i], 1};
-  return TemporalGraph::build(n, std::move(edges), directed != 0, t);
+  const bool eps = static_cast<int64_t>(g_eps.size()) == m;
+  for (int64_t i = 0; i < m; ++i) edges[i] = {u[i], v[i], ts[i], eps ? g_eps[i] : 1};
+  TemporalGraph g = TemporalGraph::build(n, std::move(edges), directed != 0, t);
+  if (static_cast<int32_t>(g_delays.size()) == n && n > 0) g.set_delays(g_delays);
+  return g;
 }
 
 VertexColoring make_coloring(int32_t n, const int32_t* colors) {
@@ -67,6 +75,13 @@ size_t put(char* buf, size_t cap, const std::string& s) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_set_model(const int32_t* eps, int64_t m, const int32_t* delays, int32_t n,
+                   int32_t edge_model) {
+  g_eps.assign(eps ? eps : nullptr, eps ? eps + m : nullptr);
+  g_delays.assign(delays ? delays : nullptr, delays ? delays + n : nullptr);
+  g_model = edge_model;
+}
 
 // gf::mul<uint64_t> (gf.hpp:85-106) and gf::draw_nonzero (gf.hpp:147-153).
 uint64_t ref_gf_mul(uint64_t a, uint64_t b) { return gf::mul<std::uint64_t>(a, b); }
@@ -240,6 +255,9 @@ int64_t ref_solve(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
     req.dest = dest;
     req.config.seed = seed;
     req.config.threads = 1;
+    static const EdgeModel models[] = {EdgeModel::instant, EdgeModel::transition_only,
+                                       EdgeModel::delay_only, EdgeModel::transition_delay};
+    req.config.edge_model = models[g_model & 3];
     static const PreprocessLevel levels[] = {
         PreprocessLevel::none, PreprocessLevel::color_filter,
         PreprocessLevel::static_sieve, PreprocessLevel::both};

@@ -19,6 +19,14 @@ extern "C" {
 
 const char* tsieve_last_error() { return g_err.c_str(); }
 
+int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                             const int32_t* ts, const int32_t* eps, const int32_t* delays,
+                             int32_t edge_model, int directed, int32_t t, const int32_t* colors,
+                             const char* problem, const int32_t* motif, int32_t motif_len,
+                             int32_t k, int32_t source, int32_t dest, uint64_t seed,
+                             int32_t mode, int32_t extraction, int32_t preprocess, char* buf,
+                             int64_t cap);
+
 // problem: CLI name; mode 0 decide, 1 optimum, 2 extract, 3 extract+optimum;
 // extraction 0 localized, 1 self-reducible; preprocess 0 none, 1 colors,
 // 2 static, 3 both.  Returns the JSON length or -1 (see tsieve_last_error).
@@ -27,10 +35,25 @@ int64_t tsieve_solve_json(int32_t n, int64_t m, const int32_t* u, const int32_t*
                           const char* problem, const int32_t* motif, int32_t motif_len,
                           int32_t k, int32_t source, int32_t dest, uint64_t seed, int32_t mode,
                           int32_t extraction, int32_t preprocess, char* buf, int64_t cap) {
+  return tsieve_solve_json_ex(n, m, u, v, ts, nullptr, nullptr, 0, directed, t, colors, problem,
+                              motif, motif_len, k, source, dest, seed, mode, extraction,
+                              preprocess, buf, cap);
+}
+
+// Same, with transition times eps[m] / vertex delays delays[n] (either may be
+// NULL) and edge_model 0..3 (instant, transition, delay, transition-delay).
+int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                             const int32_t* ts, const int32_t* eps, const int32_t* delays,
+                             int32_t edge_model, int directed, int32_t t, const int32_t* colors,
+                             const char* problem, const int32_t* motif, int32_t motif_len,
+                             int32_t k, int32_t source, int32_t dest, uint64_t seed,
+                             int32_t mode, int32_t extraction, int32_t preprocess, char* buf,
+                             int64_t cap) {
   try {
     std::vector<TemporalEdge> edges(static_cast<size_t>(m));
-    for (int64_t i = 0; i < m; ++i) edges[i] = {u[i], v[i], ts[i], 1};
+    for (int64_t i = 0; i < m; ++i) edges[i] = {u[i], v[i], ts[i], eps ? eps[i] : 1};
     TemporalGraph g = TemporalGraph::build(n, std::move(edges), directed != 0, t);
+    if (delays && n > 0) g.set_delays(std::vector<std::int32_t>(delays, delays + n));
     std::vector<Color> c(static_cast<size_t>(n), 1);
     Color q = 1;
     for (int32_t i = 0; colors && i < n; ++i) q = std::max(q, c[i] = colors[i]);
@@ -44,6 +67,9 @@ int64_t tsieve_solve_json(int32_t n, int64_t m, const int32_t* u, const int32_t*
     req.source = source;
     req.dest = dest;
     req.config.seed = seed;
+    static const EdgeModel models[] = {EdgeModel::instant, EdgeModel::transition_only,
+                                       EdgeModel::delay_only, EdgeModel::transition_delay};
+    req.config.edge_model = models[edge_model & 3];
     static const PreprocessLevel lv[] = {PreprocessLevel::none, PreprocessLevel::color_filter,
                                          PreprocessLevel::static_sieve, PreprocessLevel::both};
     req.preprocess = lv[preprocess & 3];

@@ -90,14 +90,13 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
   if (max_ts < 1 || max_ts > g.t()) throw std::invalid_argument("max_ts outside [1..t]");
   if (static_cast<int>(shades.vertex_off.size()) != g.n() + 1)
     throw std::invalid_argument("shade assignment built for a different graph");
-  if (config.edge_model != EdgeModel::instant)
-    throw std::invalid_argument("the B200 engine evaluates the instant edge model only");
+  const int model = static_cast<int>(config.edge_model);  // enum order = tsv.h codes
 
   tsv_config c{};
   c.seed = config.seed;
   c.field_bits = config.field_bits;
   c.lane_width = config.lane_width;
-  c.edge_model = 0;
+  c.edge_model = model;
   c.points_per_batch = 0;
   c.memory_cap_words = config.memory_cap_words;
 
@@ -107,7 +106,7 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
   tsv_outcome o{};
   static const std::int32_t kNoShade = 0;
   const int rc = tsv_eval_temporal_sieve(
-      g.device_graph(config.device), k, max_ts, shades.vertex_off.data(),
+      g.device_graph(config.device, model), k, max_ts, shades.vertex_off.data(),
       shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c,
       anchor.source, anchor.sink, g.n() ? out.accumulators.data() : &scratch, &o);
   if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());

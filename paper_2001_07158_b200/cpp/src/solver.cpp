@@ -174,6 +174,7 @@ struct Dfs {
   const MotifQuery& q;
   AnchorSpec anchor;
   Timestamp horizon;
+  EdgeModel model = EdgeModel::instant;
   std::map<Color, int> left;
   std::vector<char> used;
   std::vector<Vertex> chain;
@@ -200,6 +201,17 @@ struct Dfs {
     return col.wildcard_active() && attempt(col.wildcard_color());
   }
 
+  // effective transition time / vertex delay (solver.cpp DfsCtx of the
+  // reference): 1 unless the edge model uses them
+  std::int32_t eps_eff(const TemporalEdge& e) const {
+    return (model == EdgeModel::transition_only || model == EdgeModel::transition_delay) ? e.eps
+                                                                                          : 1;
+  }
+  std::int32_t delta_eff(Vertex v) const {
+    return (model == EdgeModel::delay_only || model == EdgeModel::transition_delay) ? g.delay(v)
+                                                                                     : 1;
+  }
+
   bool allowed(Vertex v, int pos) const {
     if (anchor.source >= 0 && ((v == anchor.source) != (pos == 1))) return false;
     if (anchor.sink >= 0 && ((v == anchor.sink) != (pos == q.k))) return false;
@@ -222,7 +234,8 @@ struct Dfs {
   bool backward(int pos) {
     if (pos == 0) return true;
     const Vertex x = chain.back();
-    const Timestamp hi = chain_edges.empty() ? horizon : chain_edges.back().ts - 1;
+    const bool last_step = chain_edges.empty();
+    const Timestamp hi = last_step ? horizon : chain_edges.back().ts - delta_eff(x);
     auto arcs = g.in_arcs(x);
     auto end = std::upper_bound(arcs.begin(), arcs.end(), hi,
                                 [](Timestamp t, const Incidence& a) { return t < a.ts; });
@@ -232,8 +245,12 @@ struct Dfs {
       while (beg != arcs.begin() && std::prev(beg)->ts == ts) --beg;
       for (auto it = beg; it != end; ++it) {
         const Vertex v = it->other;
-        if (used[v] || !allowed(v, pos)) continue;
+        if (used[v]) continue;
         const TemporalEdge& e = g.edge(it->edge);
+        if (last_step ? it->ts + eps_eff(e) - 1 > horizon
+                      : chain_edges.back().ts - it->ts < eps_eff(e) + delta_eff(x) - 1)
+          continue;
+        if (!allowed(v, pos)) continue;
         if (place(v, [&] { return step(v, e, [&] { return backward(pos - 1); }); }))
           return true;
       }
@@ -246,14 +263,19 @@ struct Dfs {
   bool forward(int pos) {
     if (pos > q.k) return true;
     const Vertex x = chain.back();
-    const Timestamp lo = chain_edges.empty() ? 1 : chain_edges.back().ts + 1;
+    const Timestamp lo =
+        chain_edges.empty()
+            ? 1
+            : chain_edges.back().ts +
+                  std::max<std::int32_t>(0, eps_eff(chain_edges.back()) + delta_eff(x) - 1);
     auto arcs = g.out_arcs(x);
     auto it = std::lower_bound(arcs.begin(), arcs.end(), lo,
                                [](const Incidence& a, Timestamp t) { return a.ts < t; });
     for (; it != arcs.end(); ++it) {
       const Vertex v = it->other;
-      if (used[v] || it->ts > horizon || !allowed(v, pos)) continue;
+      if (used[v]) continue;
       const TemporalEdge& e = g.edge(it->edge);
+      if (it->ts + eps_eff(e) - 1 > horizon || !allowed(v, pos)) continue;
       if (place(v, [&] { return step(v, e, [&] { return forward(pos + 1); }); })) return true;
     }
     return false;
@@ -262,6 +284,7 @@ struct Dfs {
 
 std::optional<TemporalPath> extract_backward(const Prep& p, Vertex end, Timestamp horizon) {
   Dfs d(p.graph, p.coloring, p.query, p.anchor, horizon);
+  d.model = p.cfg.edge_model;
   if (!d.allowed(end, p.query.k)) return std::nullopt;
   const bool ok = d.place(end, [&] {
     d.used[end] = 1;
@@ -281,6 +304,7 @@ std::optional<TemporalPath> extract_backward(const Prep& p, Vertex end, Timestam
 std::optional<TemporalPath> extract_forward(const Prep& p, const TemporalGraph& core,
                                             Vertex start, Timestamp horizon) {
   Dfs d(core, p.coloring, p.query, p.anchor, horizon);
+  d.model = p.cfg.edge_model;
   if (!d.allowed(start, 1)) return std::nullopt;
   const bool ok = d.place(start, [&] {
     d.used[start] = 1;
@@ -310,11 +334,13 @@ std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
   // Each deletion probe restricts the graph ON THE DEVICE (order-preserving
   // filter + rebuild, tsv_graph_restrict) and evaluates there; no host graph
   // is rebuilt per probe.
-  const tsv_graph* base = p.graph.device_graph(p.cfg.device);
+  const int model = static_cast<int>(p.cfg.edge_model);
+  const tsv_graph* base = model == 0 ? p.graph.device_graph(p.cfg.device) : nullptr;
   tsv_config cfg{};
   cfg.seed = p.cfg.seed;
   cfg.field_bits = p.cfg.field_bits;
   cfg.lane_width = p.cfg.lane_width;
+  cfg.edge_model = model;
   cfg.memory_cap_words = p.cfg.memory_cap_words;
   std::vector<std::uint8_t> mask8(static_cast<size_t>(p.graph.n()));
   std::vector<std::uint64_t> acc(static_cast<size_t>(p.graph.n()) + 1);
@@ -323,14 +349,23 @@ std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
     for (Vertex x = 0; x < p.graph.n(); ++x) mask8[x] = keep[x] ? 1 : 0;
     for (Vertex x : block) mask8[x] = 0;
     tsv_graph* sub = nullptr;
-    if (tsv_graph_restrict(base, mask8.data(), horizon, &sub) != TSV_OK)
-      throw std::runtime_error(tsv_last_error());
+    std::optional<TemporalGraph> host_sub;
+    const tsv_graph* probe_graph = nullptr;
+    if (model == 0) {
+      if (tsv_graph_restrict(base, mask8.data(), horizon, &sub) != TSV_OK)
+        throw std::runtime_error(tsv_last_error());
+      probe_graph = sub;
+    } else {  // delay models: restrict on the host, mirror for the model
+      std::vector<bool> kb(mask8.begin(), mask8.end());
+      host_sub.emplace(restrict_to(p.graph, kb, horizon));
+      probe_graph = host_sub->device_graph(p.cfg.device, model);
+    }
     tsv_outcome o{};
     const int rc = tsv_eval_temporal_sieve(
-        sub, p.k, horizon, p.shades.vertex_off.data(),
+        probe_graph, p.k, horizon, p.shades.vertex_off.data(),
         p.shades.vertex_shades.empty() ? &kNoShade : p.shades.vertex_shades.data(), &cfg,
         p.anchor.source, p.anchor.sink, acc.data(), &o);
-    tsv_graph_free(sub);
+    if (sub) tsv_graph_free(sub);
     if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
     if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
     ++calls;
@@ -418,7 +453,7 @@ SolveReport solve_single(const TemporalGraph& g, const VertexColoring& col,
     const auto te = Clock::now();
     auto accept = [&](std::optional<TemporalPath> w) {
       if (!w) return false;
-      if (!validate_path(p.graph, p.coloring, *w, p.query, EdgeModel::instant, p.anchor.source,
+      if (!validate_path(p.graph, p.coloring, *w, p.query, p.cfg.edge_model, p.anchor.source,
                          p.anchor.sink))
         return false;
       r.witness = std::move(*w);

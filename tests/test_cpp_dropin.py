@@ -353,3 +353,66 @@ def test_large_build_canonicalizes_on_device_like_host(cuda_device):
         assert dev["n"] == host["n"] and dev["t"] == host["t"]
         for key in ("u", "v", "ts"):
             assert np.array_equal(dev[key], host[key]), key
+
+
+def solve_ex(c, eps, delays, model):
+    lib = dropin()
+    f = lib.tsieve_solve_json_ex
+    f.restype = C.c_int64
+    f.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_void_p, C.c_void_p, C.c_int32,
+                  C.c_int, C.c_int32, _i32p, C.c_char_p, _i32p, C.c_int32, C.c_int32, C.c_int32,
+                  C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int64]
+    a = lambda x: np.ascontiguousarray(np.asarray(x, dtype=np.int32))  # noqa: E731
+    e = a(eps) if eps is not None else None
+    d = a(delays) if delays is not None else None
+    buf = C.create_string_buffer(1 << 16)
+    motif = a(c["motif"]) if c["motif"] else np.zeros(1, np.int32)
+    r = f(c["n"], len(c["u"]), a(c["u"]), a(c["v"]), a(c["ts"]),
+          None if e is None else e.ctypes.data, None if d is None else d.ctypes.data, model,
+          int(c["directed"]), 0, a(c["colors"]), c["problem"].encode(), motif, len(c["motif"]),
+          c["k"], c["source"], c["dest"], c["seed"], c["mode"], c["extraction"], c["preprocess"],
+          buf, len(buf))
+    if r < 0:
+        raise ValueError(lib.tsieve_last_error().decode())
+    return json.loads(buf.value.decode())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", [1, 2, 3])
+def test_solver_edge_models_match_reference(cuda_device, model):
+    """solve() under the transition / delay / transition-delay models: the
+    sieve probes run on model-specific device layouts, the DFS uses the
+    reference's eps/delta gaps, self-reduction restricts on the host; every
+    field of the record equals the reference's."""
+    from oracle import oracle as O
+    from paper_2001_07158_b200 import synth
+    rng = np.random.default_rng(100 + model)
+    problems = ["pathmotif", "ktemppath", "colorfulpath", "sdcolorful"]
+    found = 0
+    for i in range(32):
+        n, u, v, ts, d, colors, motif = synth.random_small(rng, n_max=16, m_max=70, t_max=9,
+                                                           k_max=4, q_max=3)
+        eps = rng.integers(1, 3, len(u))
+        delays = rng.integers(0, 3, n) if i % 3 else None
+        prob = problems[i % 4]
+        k, src, dst = 0, -1, -1
+        if prob == "ktemppath":
+            motif, k = [], int(rng.integers(1, 4))
+        elif prob == "colorfulpath":
+            motif = sorted(set(motif)) or [1]
+        elif prob == "sdcolorful":
+            motif, k = [], int(rng.integers(1, 3))
+            src, dst = (int(x) for x in rng.choice(n, 2, replace=False))
+        c = {"n": n, "u": u.tolist(), "v": v.tolist(), "ts": ts.tolist(), "directed": d,
+             "colors": colors.tolist(), "problem": prob, "motif": motif, "k": k, "source": src,
+             "dest": dst, "seed": int(rng.integers(1, 1000)), "mode": [0, 1, 2, 3][(i // 4) % 4],
+             "extraction": (i // 16) % 2, "preprocess": [0, 1][(i // 8) % 2]}
+        want = O.ref_solve_model(n, u, v, ts, eps, delays, model, d, colors, prob, motif, k,
+                                 source=src, dest=dst, seed=c["seed"], mode=c["mode"],
+                                 extraction=c["extraction"], preprocess=c["preprocess"])
+        got = solve_ex(c, eps, delays, model)
+        for key in ("decision", "certain", "optimum_ts", "checksum", "flagged", "witness",
+                    "extraction_failed", "oracle_calls", "preprocessed_n", "preprocessed_m"):
+            assert got[key] == want[key], (key, model, i, got, want)
+        found += got["witness"] is not None
+    assert found > 3
