@@ -416,3 +416,45 @@ def test_solver_edge_models_match_reference(cuda_device, model):
             assert got[key] == want[key], (key, model, i, got, want)
         found += got["witness"] is not None
     assert found > 3
+
+
+@pytest.mark.gpu
+def test_cli_edge_models_from_files(cuda_device, tmp_path):
+    """The CLI reads transition times (4th column) and --delays files and
+    picks the model like the reference's --edge-model auto; results equal
+    the reference's solve() under the same model."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(8)
+    n, m = 12, 60
+    u, v = rng.integers(0, n, m), rng.integers(0, n, m)
+    ts, eps = rng.integers(1, 8, m), rng.integers(1, 3, m)
+    delays = rng.integers(0, 3, n)
+    colors = rng.integers(1, 3, n)
+    (tmp_path / "g.edges").write_text("".join(f"{a} {b} {t} {e}\n" for a, b, t, e in
+                                              zip(u.tolist(), v.tolist(), ts.tolist(),
+                                                  eps.tolist())))
+    (tmp_path / "g.colors").write_text("".join(f"{i} {c}\n" for i, c in enumerate(colors)))
+    (tmp_path / "g.delays").write_text("".join(f"{i} {d}\n" for i, d in enumerate(delays)))
+    # file tokens "0".."11" intern in first-appearance order: map ids
+    order = []
+    for a, b in zip(u.tolist(), v.tolist()):
+        for x in (a, b):
+            if x not in order:
+                order.append(x)
+    idx = {x: i for i, x in enumerate(order)}
+    nn = len(order)
+    uu = np.array([idx[x] for x in u.tolist()])
+    vv = np.array([idx[x] for x in v.tolist()])
+    col2 = np.array([colors[x] for x in order])
+    del2 = np.array([delays[x] for x in order])
+    for extra, model, dl in (([], 1, None), (["--delays", str(tmp_path / "g.delays")], 3, del2)):
+        args = ["decide", "--graph", str(tmp_path / "g.edges"), "--colors",
+                str(tmp_path / "g.colors"), "--problem", "pathmotif", "--motif", "1,2,1",
+                "--directed", "--preprocess", "none", "--format", "json"] + extra
+        rc, out = cli(args)
+        rec = json.loads(out)
+        want = O.ref_solve_model(nn, uu, vv, ts, eps, dl, model, True, col2, "pathmotif",
+                                 [1, 1, 2], 0, seed=1, mode=0)
+        assert rec["decision"] == ("YES" if want["decision"] else "NO"), (model, rec, want)
+        assert rec["accumulator_checksum"] == want["checksum"]
+        assert rec["config"]["edge_model"] == {1: "transition", 3: "transition-delay"}[model]
