@@ -152,6 +152,31 @@ int tsv_eval_points_device(const tsv_graph* g, const tsv_shades* s, int k,
                            int32_t anchor_source, uint64_t p_begin,
                            uint64_t p_end, uint64_t* d_acc, void* stream);
 
+/* Edge-constrained sieve (eval_edge_constrained_sieve, sieve.cpp:477-536,
+ * 758-780): level l uses only the edges with timestamp times[l-2]
+ * (times: k-1 strictly increasing stamps in [1..t]); per-vertex state, no
+ * anchor.  Instant model only. */
+int tsv_eval_edge_constrained(const tsv_graph* g, int k, const int32_t* times,
+                              const int32_t* vertex_off, const int32_t* vertex_shades,
+                              const tsv_config* cfg, uint64_t* accumulators,
+                              tsv_outcome* out);
+
+/* Vertex-ordered sieve (eval_vertex_ordered_sieve, sieve.cpp:540-635,
+ * 782-794): positional z (Role::label_z) and, at level l, only arcs whose
+ * tail has color order[l-2] and head order[l-1] (colors: n primary colors;
+ * wildcard_color matches every vertex, -1 = none). */
+int tsv_eval_vertex_ordered(const tsv_graph* g, int k, const int32_t* order,
+                            const int32_t* colors, int32_t wildcard_color,
+                            int32_t max_ts, const tsv_config* cfg,
+                            uint64_t* accumulators, tsv_outcome* out);
+
+/* VC-ColorfulPath's exact indicator DP (dp_probe, solver.cpp:146-191) in
+ * earliest-arrival form on the device; flagged[n] = 1 where a path realizing
+ * the order ends by max_ts. */
+int tsv_vc_colorful_dp(const tsv_graph* g, int k, const int32_t* order,
+                       const int32_t* colors, int32_t wildcard_color, int32_t max_ts,
+                       uint8_t* flagged);
+
 /* Static-projection engines over the projection's edge list (a[i], b[i]),
  * i = static edge id (StaticProjection::project, graph.cpp:148-199):
  * junction != 0 replaces eval_junction_sieve (sieve.cpp:376-473, the

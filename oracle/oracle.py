@@ -97,6 +97,8 @@ def ref_lib():
             C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_void_p, C.c_void_p, C.c_int,
             C.c_int32, _i32p, _i32p, C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
             C.c_int32, C.c_int32, _u64p, C.POINTER(C.c_uint64), _i32p, _i32p, _i32p, _i32p]
+        lib.ref_set_query.restype = None
+        lib.ref_set_query.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]
         lib.ref_set_model.restype = None
         lib.ref_set_model.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int32, C.c_int32]
         lib.ref_solve.restype = C.c_int64
@@ -240,6 +242,18 @@ def ref_eval_temporal_model(n, u, v, ts, eps, delays, directed, colors, motif, e
         raise ValueError(ref_lib().ref_last_error().decode())
     return {"acc": acc[:n], "checksum": int(cs.value), "u": ou[:r], "v": ov[:r], "ts": ot[:r],
             "eps": oe[:r]}
+
+
+def ref_solve_query(n, u, v, ts, times, order, *args, **kw):
+    """ref_solve with a timed (EC) or ordered (VC) query."""
+    t = _a32(times) if times else None
+    o = _a32(order) if order else None
+    ref_lib().ref_set_query(None if t is None else t.ctypes.data, 0 if t is None else len(t),
+                            None if o is None else o.ctypes.data, 0 if o is None else len(o))
+    try:
+        return ref_solve(n, u, v, ts, *args, **kw)
+    finally:
+        ref_lib().ref_set_query(None, 0, None, 0)
 
 
 def ref_solve_model(n, u, v, ts, eps, delays, edge_model, *args, **kw):

@@ -38,6 +38,7 @@ std::string g_err;
 // state, cleared by ref_set_model(NULL, NULL, 0, 0)).
 std::vector<std::int32_t> g_eps, g_delays;
 int g_model = 0;
+std::vector<std::int32_t> g_times, g_order;  // ref_set_query
 
 TemporalGraph make_graph(int32_t n, int64_t m, const int32_t* u,
                          const int32_t* v, const int32_t* ts, int directed,
@@ -75,6 +76,12 @@ size_t put(char* buf, size_t cap, const std::string& s) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+void ref_set_query(const int32_t* times, int32_t ntimes, const int32_t* order,
+                   int32_t norder) {
+  g_times.assign(times ? times : nullptr, times ? times + ntimes : nullptr);
+  g_order.assign(order ? order : nullptr, order ? order + norder : nullptr);
+}
 
 void ref_set_model(const int32_t* eps, int64_t m, const int32_t* delays, int32_t n,
                    int32_t edge_model) {
@@ -246,7 +253,13 @@ int64_t ref_solve(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
     auto p = problem_from_name(problem);
     if (!p) throw std::invalid_argument("unknown problem");
     req.problem = *p;
-    if (motif_len > 0)
+    if (!g_order.empty())
+      req.query = MotifQuery::from_order(std::vector<Color>(g_order.begin(), g_order.end()));
+    else if (!g_times.empty())
+      req.query = MotifQuery::from_times(
+          std::vector<Timestamp>(g_times.begin(), g_times.end()),
+          std::vector<Color>(motif, motif + std::max(motif_len, 0)));
+    else if (motif_len > 0)
       req.query = MotifQuery::from_multiset(
           std::vector<Color>(motif, motif + motif_len));
     else

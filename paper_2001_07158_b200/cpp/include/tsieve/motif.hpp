@@ -1,10 +1,10 @@
 // tsieve/motif.hpp -- query types of the B200 drop-in.
 //
 // Same names and meaning as the reference API
-// (/root/reference/proj/core/include/tsieve/motif.hpp:11-74).  The engine
-// evaluates the size-only and color-multiset kinds (k-TempPath, PathMotif,
-// ColorfulPath, (s,d)-ColorfulPath); the ordered/timed kinds are accepted as
-// values but rejected by the solver.
+// (/root/reference/proj/core/include/tsieve/motif.hpp:11-74).  Every kind
+// is evaluated on the device: size-only / multiset by the temporal sieve,
+// timed kinds by the edge-constrained sieve, ordered colors by the
+// vertex-ordered sieve (or the exact DP for VC-ColorfulPath).
 #pragma once
 
 #include <cstdint>

@@ -73,6 +73,24 @@ SieveOutcome eval_static_sieve(const StaticProjection& gs, int k, const ShadeAss
 SieveOutcome eval_junction_sieve(const StaticProjection& gs, int k,
                                  const ShadeAssignment& shades, const SieveConfig& config);
 
+// Delay-model entry (sieve.hpp of the reference): eval_temporal_sieve under
+// a non-instant config.edge_model.
+SieveOutcome eval_delay_sieve(const TemporalGraph& g, int k, Timestamp max_ts,
+                              const ShadeAssignment& shades, const SieveConfig& config);
+
+// Edge-constrained sieve: the l-th edge of the path must carry timestamp
+// times[l-2] (sieve.cpp:477-536, 758-780 of the reference); on the GPU.
+SieveOutcome eval_edge_constrained_sieve(const TemporalGraph& g,
+                                         const std::vector<Timestamp>& times,
+                                         const ShadeAssignment& shades,
+                                         const SieveConfig& config);
+
+// Vertex-ordered sieve: position l must carry color order[l-1]
+// (sieve.cpp:540-635, 782-794); on the GPU.
+SieveOutcome eval_vertex_ordered_sieve(const TemporalGraph& g, const std::vector<Color>& order,
+                                       const VertexColoring& coloring, Timestamp max_ts,
+                                       const SieveConfig& config);
+
 double false_negative_bound(int k, int field_bits);
 
 }  // namespace tsieve

@@ -25,7 +25,8 @@ int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32
                              const char* problem, const int32_t* motif, int32_t motif_len,
                              int32_t k, int32_t source, int32_t dest, uint64_t seed,
                              int32_t mode, int32_t extraction, int32_t preprocess, char* buf,
-                             int64_t cap);
+                             int64_t cap, const int32_t* times = nullptr, int32_t ntimes = 0,
+                             const int32_t* order = nullptr, int32_t norder = 0);
 
 // problem: CLI name; mode 0 decide, 1 optimum, 2 extract, 3 extract+optimum;
 // extraction 0 localized, 1 self-reducible; preprocess 0 none, 1 colors,
@@ -41,14 +42,17 @@ int64_t tsieve_solve_json(int32_t n, int64_t m, const int32_t* u, const int32_t*
 }
 
 // Same, with transition times eps[m] / vertex delays delays[n] (either may be
-// NULL) and edge_model 0..3 (instant, transition, delay, transition-delay).
+// NULL), edge_model 0..3 (instant, transition, delay, transition-delay), and
+// the timed / ordered query kinds: times[ntimes] (EC problems, with motif as
+// the color multiset) or order[norder] (VC problems).
 int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                              const int32_t* ts, const int32_t* eps, const int32_t* delays,
                              int32_t edge_model, int directed, int32_t t, const int32_t* colors,
                              const char* problem, const int32_t* motif, int32_t motif_len,
                              int32_t k, int32_t source, int32_t dest, uint64_t seed,
                              int32_t mode, int32_t extraction, int32_t preprocess, char* buf,
-                             int64_t cap) {
+                             int64_t cap, const int32_t* times, int32_t ntimes,
+                             const int32_t* order, int32_t norder) {
   try {
     std::vector<TemporalEdge> edges(static_cast<size_t>(m));
     for (int64_t i = 0; i < m; ++i) edges[i] = {u[i], v[i], ts[i], eps ? eps[i] : 1};
@@ -62,8 +66,13 @@ int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32
     auto p = problem_from_name(problem);
     if (!p) throw std::invalid_argument("unknown problem");
     req.problem = *p;
-    req.query = motif_len > 0 ? MotifQuery::from_multiset(std::vector<Color>(motif, motif + motif_len))
-                              : MotifQuery::size_only(k);
+    const std::vector<Color> mcol(motif, motif + std::max(motif_len, 0));
+    if (norder > 0)
+      req.query = MotifQuery::from_order(std::vector<Color>(order, order + norder));
+    else if (ntimes > 0)
+      req.query = MotifQuery::from_times(std::vector<Timestamp>(times, times + ntimes), mcol);
+    else
+      req.query = motif_len > 0 ? MotifQuery::from_multiset(mcol) : MotifQuery::size_only(k);
     req.source = source;
     req.dest = dest;
     req.config.seed = seed;

@@ -129,6 +129,105 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
 
 namespace {
 
+// Decision rule, fn bound and checksum of finalize (sieve.cpp:136-159)
+void finish(SieveOutcome& out, int k, const SieveConfig& config, const tsv_outcome& o) {
+  for (Vertex x = 0; x < static_cast<Vertex>(out.accumulators.size()); ++x)
+    if (out.accumulators[x]) out.flagged.push_back(x);
+  if (config.localize) {
+    out.global_nonzero = !out.flagged.empty();
+  } else {
+    std::uint64_t total = 0;
+    for (std::uint64_t a : out.accumulators) total ^= a;
+    out.global_nonzero = total != 0;
+  }
+  out.fn_bound = false_negative_bound(k, config.field_bits);
+  out.peak_field_words = o.peak_field_words;
+  out.checksum = o.checksum;
+}
+
+tsv_config to_abi(const SieveConfig& config) {
+  tsv_config c{};
+  c.seed = config.seed;
+  c.field_bits = config.field_bits;
+  c.lane_width = config.lane_width;
+  c.edge_model = 0;
+  c.memory_cap_words = config.memory_cap_words;
+  return c;
+}
+
+}  // namespace
+
+SieveOutcome eval_delay_sieve(const TemporalGraph& g, int k, Timestamp max_ts,
+                              const ShadeAssignment& shades, const SieveConfig& config) {
+  if (config.edge_model == EdgeModel::instant)
+    throw std::invalid_argument("eval_delay_sieve requires a delay edge model");
+  return eval_temporal_sieve(g, k, max_ts, shades, config);
+}
+
+SieveOutcome eval_edge_constrained_sieve(const TemporalGraph& g,
+                                         const std::vector<Timestamp>& times,
+                                         const ShadeAssignment& shades,
+                                         const SieveConfig& config) {
+  check_config(config);
+  if (times.empty()) throw std::invalid_argument("times must be nonempty");
+  for (std::size_t i = 0; i < times.size(); ++i) {
+    if (times[i] < 1 || times[i] > g.t())
+      throw std::invalid_argument("prescribed timestamp outside [1..t]");
+    if (i > 0 && times[i] <= times[i - 1])
+      throw std::invalid_argument("prescribed timestamps must strictly increase");
+  }
+  const int k = static_cast<int>(times.size()) + 1;
+  SieveOutcome out;
+  out.accumulators.assign(static_cast<size_t>(g.n()), 0);
+  // a prescribed timestamp with no edge is a certain NO (sieve.cpp:767-774)
+  for (Timestamp ts : times)
+    if (g.runs_at(ts).empty()) {
+      out.fn_bound = 0.0;
+      out.checksum = 1469598103934665603ull;  // FNV-1a basis: no nonzero entries
+      return out;
+    }
+  if (static_cast<int>(shades.vertex_off.size()) != g.n() + 1)
+    throw std::invalid_argument("shade assignment built for a different graph");
+  const tsv_config c = to_abi(config);
+  std::uint64_t scratch = 0;
+  static const std::int32_t kNoShade = 0;
+  tsv_outcome o{};
+  const int rc = tsv_eval_edge_constrained(
+      g.device_graph(config.device), k, times.data(), shades.vertex_off.data(),
+      shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c,
+      g.n() ? out.accumulators.data() : &scratch, &o);
+  if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
+  if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
+  finish(out, k, config, o);
+  return out;
+}
+
+SieveOutcome eval_vertex_ordered_sieve(const TemporalGraph& g, const std::vector<Color>& order,
+                                       const VertexColoring& coloring, Timestamp max_ts,
+                                       const SieveConfig& config) {
+  check_config(config);
+  if (order.empty()) throw std::invalid_argument("order must be nonempty");
+  if (max_ts < 1 || max_ts > g.t()) throw std::invalid_argument("max_ts outside [1..t]");
+  const int k = static_cast<int>(order.size());
+  const tsv_config c = to_abi(config);
+  SieveOutcome out;
+  out.accumulators.assign(static_cast<size_t>(g.n()), 0);
+  std::uint64_t scratch = 0;
+  static const std::int32_t kNoColor = 0;
+  tsv_outcome o{};
+  const int rc = tsv_eval_vertex_ordered(
+      g.device_graph(config.device), k, order.data(),
+      coloring.primaries().empty() ? &kNoColor : coloring.primaries().data(),
+      coloring.wildcard_active() ? coloring.wildcard_color() : -1, max_ts, &c,
+      g.n() ? out.accumulators.data() : &scratch, &o);
+  if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
+  if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
+  finish(out, k, config, o);
+  return out;
+}
+
+namespace {
+
 SieveOutcome eval_projection(const StaticProjection& gs, int k, const ShadeAssignment& shades,
                              const SieveConfig& config, bool junction) {
   check_config(config);

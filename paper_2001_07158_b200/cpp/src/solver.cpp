@@ -6,7 +6,9 @@
 // driver (solve_single :609-703: binary search :641-662, localized reverse
 // DFS :314-394, self-reduction shrink_to_core :557-607 + forward DFS
 // :398-452), and the rainbow / wildcard loops (:705-784).  Each probe is one
-// eval_temporal_sieve on the device.
+// engine call on the device: the temporal sieve (four problems, all edge
+// models), the edge-constrained sieve (EC problems), the vertex-ordered sieve
+// (VC-PathMotif) or the exact DP (VC-ColorfulPath).
 #include "tsieve/solver.hpp"
 
 #include <algorithm>
@@ -44,9 +46,8 @@ struct Prep {
   std::uint64_t peak = 0;
 };
 
-[[noreturn]] void unsupported(Problem p) {
-  throw std::invalid_argument(std::string(problem_name(p)) +
-                              " is not evaluated by the B200 temporal-sieve engine");
+bool uses_shades(Problem p) {
+  return p != Problem::vc_path_motif && p != Problem::vc_colorful_path;
 }
 
 void make_effective(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req,
@@ -90,13 +91,45 @@ void make_effective(const TemporalGraph& g, const VertexColoring& col, const Sol
       p.anchor = {req.source, req.dest};
       break;
     }
+    case Problem::ec_temp_path: {
+      if (req.query.kind != QueryKind::ordered_times_only)
+        throw std::invalid_argument("EC-TempPath takes a timestamp tuple");
+      p.query = MotifQuery::from_times(req.query.times,
+                                       std::vector<Color>(static_cast<size_t>(req.query.k), 1));
+      p.coloring = VertexColoring::uniform(g.n());
+      break;
+    }
+    case Problem::ec_path_motif:
+      if (req.query.kind != QueryKind::ordered_times_multiset)
+        throw std::invalid_argument(
+            "EC-PathMotif takes a timestamp tuple plus a color multiset");
+      p.query = req.query;
+      p.coloring = col;
+      break;
+    case Problem::vc_path_motif:
+    case Problem::vc_colorful_path:
+      if (req.query.kind != QueryKind::ordered_colors)
+        throw std::invalid_argument("VC variants take an ordered color tuple");
+      if (req.problem == Problem::vc_colorful_path) {
+        std::vector<Color> sorted = req.query.order;
+        std::sort(sorted.begin(), sorted.end());
+        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+          throw std::invalid_argument("VC-ColorfulPath needs distinct colors");
+      }
+      p.query = req.query;
+      p.coloring = col;
+      break;
     case Problem::rainbow_path:
       throw std::logic_error("rainbow handled by its own driver");
-    default:
-      unsupported(req.problem);
   }
   p.k = p.query.k;
   if (p.k < 1) throw std::invalid_argument("k must be positive");
+  if (p.query.has_times()) {
+    const auto& ts = p.query.times;
+    for (size_t i = 1; i < ts.size(); ++i)
+      if (ts[i] <= ts[i - 1])
+        throw std::invalid_argument("prescribed timestamps must strictly increase");
+  }
 }
 
 // Kept-vertex mask (solver.cpp:458-497 of the reference): the exact color
@@ -144,14 +177,28 @@ Prep prepare(const TemporalGraph& g, const VertexColoring& col, const SolveReque
     p.graph = g;
     return p;
   }
-  p.shades = build_shades(p.query, p.coloring, p.cfg);
-  if (!p.shades.feasible) {
+  if (p.query.has_times() &&
+      (p.query.times.front() < 1 || p.query.times.back() > g.t())) {
     p.infeasible = true;
-    p.why = "query color " + std::to_string(p.shades.missing_color) + " absent from the graph";
+    p.why = "prescribed timestamp outside [1..t]";
     p.graph = g;
     return p;
   }
-  const std::vector<bool> keep = preprocess_mask(g, p, req.preprocess, p.peak);
+  if (uses_shades(p.problem)) {
+    p.shades = build_shades(p.query, p.coloring, p.cfg);
+    if (!p.shades.feasible) {
+      p.infeasible = true;
+      p.why = "query color " + std::to_string(p.shades.missing_color) + " absent from the graph";
+      p.graph = g;
+      return p;
+    }
+  }
+  PreprocessLevel level = req.preprocess;
+  // the exact DP stays exact: only the lossless filter applies to it
+  if (p.problem == Problem::vc_colorful_path &&
+      (level == PreprocessLevel::static_sieve || level == PreprocessLevel::both))
+    level = PreprocessLevel::color_filter;
+  const std::vector<bool> keep = preprocess_mask(g, p, level, p.peak);
   p.graph = restrict_to(g, keep, g.t());
   p.kept = static_cast<int>(std::count(keep.begin(), keep.end(), true));
   if (p.kept < p.k) {
@@ -162,8 +209,55 @@ Prep prepare(const TemporalGraph& g, const VertexColoring& col, const SolveReque
   return p;
 }
 
-SieveOutcome probe(const Prep& p, const TemporalGraph& graph, Timestamp max_ts) {
-  return eval_temporal_sieve(graph, p.k, max_ts, p.shades, p.cfg, p.anchor);
+struct Probe {
+  SieveOutcome out;
+  bool exact = false;  // holds for every seed
+};
+
+// One oracle call of the problem's engine (solver.cpp:199-230 of the
+// reference); every engine runs on the device.
+Probe probe(const Prep& p, const TemporalGraph& graph, Timestamp max_ts) {
+  Probe pr;
+  switch (p.problem) {
+    case Problem::ec_temp_path:
+    case Problem::ec_path_motif:
+      if (p.query.times.back() > max_ts) {
+        pr.out.accumulators.assign(static_cast<size_t>(graph.n()), 0);
+        pr.exact = true;
+      } else {
+        pr.out = eval_edge_constrained_sieve(graph, p.query.times, p.shades, p.cfg);
+      }
+      break;
+    case Problem::vc_path_motif:
+      pr.out = eval_vertex_ordered_sieve(graph, p.query.order, p.coloring, max_ts, p.cfg);
+      break;
+    case Problem::vc_colorful_path: {  // exact indicator DP (dp_probe)
+      std::vector<std::uint8_t> f(static_cast<size_t>(graph.n()) + 1, 0);
+      const int rc = tsv_vc_colorful_dp(
+          graph.device_graph(p.cfg.device), p.k, p.query.order.data(),
+          p.coloring.primaries().empty() ? nullptr : p.coloring.primaries().data(),
+          p.coloring.wildcard_active() ? p.coloring.wildcard_color() : -1, max_ts, f.data());
+      if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
+      if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
+      pr.exact = true;
+      pr.out.accumulators.assign(static_cast<size_t>(graph.n()), 0);
+      std::uint64_t h = 1469598103934665603ull;
+      for (Vertex u = 0; u < graph.n(); ++u)
+        if (f[u]) {
+          pr.out.accumulators[u] = 1;
+          pr.out.flagged.push_back(u);
+          h ^= static_cast<std::uint64_t>(u);
+          h *= 1099511628211ull;
+        }
+      pr.out.global_nonzero = !pr.out.flagged.empty();
+      pr.out.fn_bound = 0.0;
+      pr.out.checksum = h;
+      break;
+    }
+    default:
+      pr.out = eval_temporal_sieve(graph, p.k, max_ts, p.shades, p.cfg, p.anchor);
+  }
+  return pr;
 }
 
 // ---- witness extraction (host DFS over the incidence lists) ---------------
@@ -185,10 +279,13 @@ struct Dfs {
       : g(g_), col(c_), q(q_), anchor(a_), horizon(h_), left(q_.multiset),
         used(static_cast<size_t>(g_.n()), 0) {}
 
-  // Places v (consuming one unit of its color, or of the wildcard color) and
-  // runs fn; undoes the consumption unless fn succeeds.
+  // Places v at 1-based position pos (consuming one unit of its color, or of
+  // the wildcard color; ordered queries need the position's color) and runs
+  // fn; undoes the consumption unless fn succeeds.
   template <typename Fn>
-  bool place(Vertex v, Fn&& fn) {
+  bool place(Vertex v, int pos, Fn&& fn) {
+    if (q.kind == QueryKind::ordered_colors)
+      return col.has_color(v, q.order[static_cast<size_t>(pos - 1)]) && fn();
     auto attempt = [&](Color c) {
       auto it = left.find(c);
       if (it == left.end() || it->second == 0) return false;
@@ -235,7 +332,9 @@ struct Dfs {
     if (pos == 0) return true;
     const Vertex x = chain.back();
     const bool last_step = chain_edges.empty();
-    const Timestamp hi = last_step ? horizon : chain_edges.back().ts - delta_eff(x);
+    Timestamp hi = last_step ? horizon : chain_edges.back().ts - delta_eff(x);
+    const bool timed = q.has_times();
+    if (timed) hi = std::min(hi, q.times[static_cast<size_t>(pos - 1)]);
     auto arcs = g.in_arcs(x);
     auto end = std::upper_bound(arcs.begin(), arcs.end(), hi,
                                 [](Timestamp t, const Incidence& a) { return t < a.ts; });
@@ -247,11 +346,12 @@ struct Dfs {
         const Vertex v = it->other;
         if (used[v]) continue;
         const TemporalEdge& e = g.edge(it->edge);
+        if (timed && it->ts != q.times[static_cast<size_t>(pos - 1)]) continue;
         if (last_step ? it->ts + eps_eff(e) - 1 > horizon
                       : chain_edges.back().ts - it->ts < eps_eff(e) + delta_eff(x) - 1)
           continue;
         if (!allowed(v, pos)) continue;
-        if (place(v, [&] { return step(v, e, [&] { return backward(pos - 1); }); }))
+        if (place(v, pos, [&] { return step(v, e, [&] { return backward(pos - 1); }); }))
           return true;
       }
       end = beg;
@@ -275,8 +375,10 @@ struct Dfs {
       const Vertex v = it->other;
       if (used[v]) continue;
       const TemporalEdge& e = g.edge(it->edge);
+      if (q.has_times() && it->ts != q.times[static_cast<size_t>(pos - 2)]) continue;
       if (it->ts + eps_eff(e) - 1 > horizon || !allowed(v, pos)) continue;
-      if (place(v, [&] { return step(v, e, [&] { return forward(pos + 1); }); })) return true;
+      if (place(v, pos, [&] { return step(v, e, [&] { return forward(pos + 1); }); }))
+        return true;
     }
     return false;
   }
@@ -286,7 +388,7 @@ std::optional<TemporalPath> extract_backward(const Prep& p, Vertex end, Timestam
   Dfs d(p.graph, p.coloring, p.query, p.anchor, horizon);
   d.model = p.cfg.edge_model;
   if (!d.allowed(end, p.query.k)) return std::nullopt;
-  const bool ok = d.place(end, [&] {
+  const bool ok = d.place(end, p.query.k, [&] {
     d.used[end] = 1;
     d.chain.push_back(end);
     if (d.backward(p.query.k - 1)) return true;
@@ -306,7 +408,7 @@ std::optional<TemporalPath> extract_forward(const Prep& p, const TemporalGraph& 
   Dfs d(core, p.coloring, p.query, p.anchor, horizon);
   d.model = p.cfg.edge_model;
   if (!d.allowed(start, 1)) return std::nullopt;
-  const bool ok = d.place(start, [&] {
+  const bool ok = d.place(start, 1, [&] {
     d.used[start] = 1;
     d.chain.push_back(start);
     if (d.forward(2)) return true;
@@ -335,7 +437,13 @@ std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
   // filter + rebuild, tsv_graph_restrict) and evaluates there; no host graph
   // is rebuilt per probe.
   const int model = static_cast<int>(p.cfg.edge_model);
-  const tsv_graph* base = model == 0 ? p.graph.device_graph(p.cfg.device) : nullptr;
+  // the temporal sieve under the instant model restricts on the device; the
+  // other engines / models restrict on the host and probe the result
+  const bool temporal = p.problem == Problem::k_temp_path || p.problem == Problem::path_motif ||
+                        p.problem == Problem::colorful_path ||
+                        p.problem == Problem::sd_colorful_path;
+  const bool on_device = temporal && model == 0;
+  const tsv_graph* base = on_device ? p.graph.device_graph(p.cfg.device) : nullptr;
   tsv_config cfg{};
   cfg.seed = p.cfg.seed;
   cfg.field_bits = p.cfg.field_bits;
@@ -348,6 +456,14 @@ std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
   auto still_yes_without = [&](const std::vector<Vertex>& block) {
     for (Vertex x = 0; x < p.graph.n(); ++x) mask8[x] = keep[x] ? 1 : 0;
     for (Vertex x : block) mask8[x] = 0;
+    if (!temporal) {
+      std::vector<bool> kb(mask8.begin(), mask8.end());
+      const TemporalGraph sub = restrict_to(p.graph, kb, horizon);
+      const Probe pr = probe(p, sub, horizon);
+      ++calls;
+      peak = std::max(peak, pr.out.peak_field_words);
+      return pr.out.global_nonzero;
+    }
     tsv_graph* sub = nullptr;
     std::optional<TemporalGraph> host_sub;
     const tsv_graph* probe_graph = nullptr;
@@ -413,10 +529,13 @@ SolveReport solve_single(const TemporalGraph& g, const VertexColoring& col,
 
   const auto t0 = Clock::now();
   const Timestamp full = p.graph.t();
-  const SieveOutcome whole = probe(p, p.graph, full);
+  const Probe whole_probe = probe(p, p.graph, full);
+  const SieveOutcome& whole = whole_probe.out;
   r.oracle_calls = 1;
   r.decision = whole.global_nonzero;
-  r.certain = r.decision;  // a nonzero accumulator certifies a match
+  // a nonzero accumulator certifies a match; NO is exact only for the
+  // deterministic paths
+  r.certain = whole_probe.exact || r.decision;
   r.flagged = whole.flagged;
   r.checksum = whole.checksum;
   r.peak_field_words = std::max(r.peak_field_words, whole.peak_field_words);
@@ -433,7 +552,7 @@ SolveReport solve_single(const TemporalGraph& g, const VertexColoring& col,
     Timestamp lo = 1, hi = full;
     while (lo < hi) {
       const Timestamp mid = lo + (hi - lo) / 2;
-      SieveOutcome o = probe(p, p.graph, mid);
+      SieveOutcome o = probe(p, p.graph, mid).out;
       ++r.oracle_calls;
       r.peak_field_words = std::max(r.peak_field_words, o.peak_field_words);
       if (o.global_nonzero) {

@@ -59,6 +59,11 @@ struct LevelParams {
   bool last = false;
   int32_t max_ts = 0;
   uint64_t* acc = nullptr;
+  // Vertex-ordered sieve (vc_impl, sieve.cpp:540-635): an arc is live at
+  // this level only when its tail has color vc_tail and its head vc_head
+  // (has_color: primary color, or any color when it is the wildcard).
+  const int32_t* vc_color = nullptr;  // n primary colors, nullptr = not VC
+  int32_t vc_head = 0, vc_tail = 0, vc_wild = -1;
 };
 
 // One level of a static-projection engine (static_kernels.cu).
@@ -142,7 +147,25 @@ void launch_fixup(const LevelParams& p, cudaStream_t st);
 void launch_zbatch(int32_t n, const uint64_t* zj, int k, const Batch& b, uint64_t* zb,
                    cudaStream_t st);
 void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
-               uint64_t* acc, cudaStream_t st);
+               uint64_t* acc, cudaStream_t st, const int32_t* colors = nullptr,
+               int32_t color = -1, int32_t wild = -1);
+// positional z_{u,j} = draw(seed, label_z, u, j+1) (build_zj_positional, sieve.cpp:103-113)
+void launch_zj_positional(int32_t n, int k, uint64_t seed, uint64_t* zj, cudaStream_t st);
+// Edge-constrained level (ec_impl, sieve.cpp:477-536): the arcs of edges
+// [e0, e1) (one timestamp) add z_head * y(e, l-1) * prev[tail] into cur[head]
+// (n x W rows, W = 32*ppt; prev of level 1 = the batch z table).
+void launch_ec_level(int64_t e0, int64_t e1, int directed, const int32_t* eu,
+                     const int32_t* ev, const uint64_t* zb, int W, uint64_t seed, int ell,
+                     const uint64_t* prev, uint64_t* cur, cudaStream_t st);
+// acc[u] ^= XOR_w rows[u][w]
+void launch_row_xor(int32_t n, int W, const uint64_t* rows, uint64_t* acc, cudaStream_t st);
+// VC-ColorfulPath exact DP (dp_probe, solver.cpp:146-191) in earliest-arrival
+// form: e_next[head] = min(ts + 1) over edges ts <= max_ts whose tail/head
+// colors match the order step and with e_prev[tail] <= ts.
+void launch_vc_dp_level(int64_t m, int directed, const int32_t* eu, const int32_t* ev,
+                        const int32_t* ets, int32_t max_ts, const int32_t* colors,
+                        int32_t tail_color, int32_t head_color, int32_t wild,
+                        const int32_t* e_prev, int32_t* e_next, cudaStream_t st);
 // State slots (build_kernels.cu): run_slot[r] = rank of r among the runs
 // some arc reads (else -1) and arc_src rewritten from run indices to slots.
 // Returns {arcs with a src, referenced runs}; synchronizes `st`.

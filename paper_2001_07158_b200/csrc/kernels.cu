@@ -53,6 +53,12 @@ __device__ __forceinline__ void z_of(const uint64_t* __restrict__ zj, int k,
     if (!pv[p]) z[p] = 0;
 }
 
+// has_color of the reference (graph.hpp:129-131) on the device
+__device__ __forceinline__ bool has_color(const int32_t* __restrict__ colors, int32_t x,
+                                          int32_t c, int32_t wild) {
+  return c == wild || __ldg(colors + x) == c;
+}
+
 __device__ __forceinline__ uint64_t z_single(const uint64_t* __restrict__ zj,
                                              int k, int32_t u, uint64_t A) {
   uint64_t z = 0;
@@ -153,6 +159,11 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     }
     bool live = lane < nb && sidx >= 0;
     if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
+    if (P.vc_color && live) {
+      const int32_t tl = FIRST ? sidx : __ldg(P.g.arc_tail + base + lane);
+      live = tl >= 0 && has_color(P.vc_color, tl, P.vc_tail, P.vc_wild) &&
+             has_color(P.vc_color, head, P.vc_head, P.vc_wild);
+    }
     bool push;
     int32_t slot = -1;
     if (LAST) {
@@ -376,6 +387,11 @@ __global__ void __launch_bounds__(kWideWarps * 32, TSV_WIDE_MINB(PPT))
     bool live = lane < nb && sidx >= 0;
     if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
     if (LAST) live = live && __ldg(P.g.run_ts + myrun) <= P.max_ts;
+    if (P.vc_color && live) {  // vertex-ordered sieve: per-level color filter
+      const int32_t tl = FIRST ? sidx : __ldg(P.g.arc_tail + base + lane);
+      live = tl >= 0 && has_color(P.vc_color, tl, P.vc_tail, P.vc_wild) &&
+             has_color(P.vc_color, head, P.vc_head, P.vc_wild);
+    }
     s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | ref | (live ? kLive : 0u);
     s_run[wib][lane] = slot;  // state row of this run's S (run ends only)
     s_head[wib][lane] = head;
@@ -522,10 +538,12 @@ __global__ void k_zbatch(int32_t n, const uint64_t* __restrict__ zj, int k, Batc
 
 // k = 1: P_{u,1} = z_u^A, readout is the subset sum (sieve.cpp:203-213).
 __global__ void k_k1(int32_t n, const uint64_t* __restrict__ zj, Batch b,
-                     int32_t anchor_source, uint64_t* __restrict__ acc) {
+                     int32_t anchor_source, uint64_t* __restrict__ acc,
+                     const int32_t* __restrict__ colors, int32_t color, int32_t wild) {
   const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u >= n) return;
   if (anchor_source >= 0 && u != anchor_source) return;
+  if (colors && !has_color(colors, static_cast<int32_t>(u), color, wild)) return;
   uint64_t x = 0;
   for (uint64_t A = b.pb; A < b.pe; ++A) x ^= z_single(zj, 1, static_cast<int32_t>(u), A);
   acc[u] ^= x;
@@ -548,6 +566,64 @@ __global__ void k_zj(int32_t n, int k, uint64_t seed,
     for (int j = 0; j < k; ++j) row[j] ^= gf_mul(v, wtab[(d - 1) * k + j]);
   }
   for (int j = 0; j < k; ++j) zj[u * k + j] = row[j];
+}
+
+__global__ void k_zj_positional(int32_t n, int k, uint64_t seed, uint64_t* __restrict__ zj) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const uint64_t pre = draw_prefix(seed, 5);  // Role::label_z (gf.hpp:116)
+  for (int j = 0; j < k; ++j)
+    zj[u * k + j] = draw_nonzero_from(pre, static_cast<uint64_t>(u), static_cast<uint64_t>(j + 1), 0);
+}
+
+// One warp per arc of the timestamp's edges; each lane owns W/32 points.
+__global__ void k_ec_level(int64_t e0, int64_t e1, int directed, const int32_t* __restrict__ eu,
+                           const int32_t* __restrict__ ev, const uint64_t* __restrict__ zb,
+                           int W, uint64_t seed, int ell, const uint64_t* __restrict__ prev,
+                           uint64_t* __restrict__ cur) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t arcs = (e1 - e0) * (directed ? 1 : 2);
+  if (warp >= arcs) return;
+  const int64_t e = e0 + (directed ? warp : (warp >> 1));
+  const bool rev = !directed && (warp & 1);
+  const int32_t tail = rev ? ev[e] : eu[e], head = rev ? eu[e] : ev[e];
+  const uint64_t pre = draw_prefix(seed, kRoleEdgeY);
+  const uint64_t y = draw_edge_y(pre, static_cast<uint64_t>(ell - 1) + 0x165667b19e3779f9ull,
+                                 static_cast<uint32_t>(e));
+  for (int w = lane; w < W; w += 32) {
+    const uint64_t s = __ldg(prev + static_cast<int64_t>(tail) * W + w);
+    const uint64_t v = gf_mul(__ldg(zb + static_cast<int64_t>(head) * W + w), gf_mul(y, s));
+    if (v)
+      atomicXor(reinterpret_cast<unsigned long long*>(cur + static_cast<int64_t>(head) * W + w),
+                static_cast<unsigned long long>(v));
+  }
+}
+
+__global__ void k_row_xor(int32_t n, int W, const uint64_t* __restrict__ rows,
+                          uint64_t* __restrict__ acc) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  uint64_t x = 0;
+  for (int w = 0; w < W; ++w) x ^= rows[u * W + w];
+  acc[u] ^= x;
+}
+
+__global__ void k_vc_dp_level(int64_t m, int directed, const int32_t* __restrict__ eu,
+                              const int32_t* __restrict__ ev, const int32_t* __restrict__ ets,
+                              int32_t max_ts, const int32_t* __restrict__ colors,
+                              int32_t tail_c, int32_t head_c, int32_t wild,
+                              const int32_t* __restrict__ e_prev, int32_t* __restrict__ e_next) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int32_t t = ets[i];
+  if (t > max_ts) return;
+  auto relax = [&](int32_t head, int32_t tail) {
+    if (!has_color(colors, head, head_c, wild) || !has_color(colors, tail, tail_c, wild)) return;
+    if (e_prev[tail] <= t) atomicMin(e_next + head, t + 1);
+  };
+  relax(ev[i], eu[i]);
+  if (!directed) relax(eu[i], ev[i]);
 }
 
 __global__ void k_xor_combine(const uint64_t* __restrict__ parts, int nparts,
@@ -651,10 +727,11 @@ void launch_zbatch(int32_t n, const uint64_t* zj, int k, const Batch& b, uint64_
 }
 
 void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
-               uint64_t* acc, cudaStream_t st) {
+               uint64_t* acc, cudaStream_t st, const int32_t* colors, int32_t color,
+               int32_t wild) {
   if (n == 0) return;
   prof_begin("k1", st);
-  k_k1<<<blocks_for(n, 256), 256, 0, st>>>(n, zj, b, anchor_source, acc);
+  k_k1<<<blocks_for(n, 256), 256, 0, st>>>(n, zj, b, anchor_source, acc, colors, color, wild);
   prof_end(st);
 }
 
@@ -674,6 +751,38 @@ void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n, uint64_t* 
   const unsigned blocks = blocks_for(n, 256) < 148 * 8 ? blocks_for(n, 256) : 148 * 8;
   k_xor_combine<<<blocks, 256, 0, st>>>(parts, nparts, n, out);
   prof_end(st);
+}
+
+void launch_zj_positional(int32_t n, int k, uint64_t seed, uint64_t* zj, cudaStream_t st) {
+  if (n == 0) return;
+  prof_begin("zj", st);
+  k_zj_positional<<<blocks_for(n, 128), 128, 0, st>>>(n, k, seed, zj);
+  prof_end(st);
+}
+
+void launch_ec_level(int64_t e0, int64_t e1, int directed, const int32_t* eu,
+                     const int32_t* ev, const uint64_t* zb, int W, uint64_t seed, int ell,
+                     const uint64_t* prev, uint64_t* cur, cudaStream_t st) {
+  const int64_t arcs = (e1 - e0) * (directed ? 1 : 2);
+  if (arcs <= 0) return;
+  prof_begin("ec_level", st);
+  k_ec_level<<<blocks_for(arcs * 32, 256), 256, 0, st>>>(e0, e1, directed, eu, ev, zb, W, seed,
+                                                        ell, prev, cur);
+  prof_end(st);
+}
+
+void launch_row_xor(int32_t n, int W, const uint64_t* rows, uint64_t* acc, cudaStream_t st) {
+  if (n == 0) return;
+  k_row_xor<<<blocks_for(n, 256), 256, 0, st>>>(n, W, rows, acc);
+}
+
+void launch_vc_dp_level(int64_t m, int directed, const int32_t* eu, const int32_t* ev,
+                        const int32_t* ets, int32_t max_ts, const int32_t* colors,
+                        int32_t tail_color, int32_t head_color, int32_t wild,
+                        const int32_t* e_prev, int32_t* e_next, cudaStream_t st) {
+  if (m == 0) return;
+  k_vc_dp_level<<<blocks_for(m, 256), 256, 0, st>>>(m, directed, eu, ev, ets, max_ts, colors,
+                                                   tail_color, head_color, wild, e_prev, e_next);
 }
 
 void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges,

@@ -276,15 +276,24 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
   return W;
 }
 
+// Vertex-ordered sieve (vc_impl): positional z, per-level color filter.
+struct VcSpec {
+  const int32_t* d_colors = nullptr;  // n primary colors (device)
+  std::vector<int32_t> order;         // k colors, position-exact
+  int32_t wild = -1;                  // wildcard color, -1 = none
+};
+
 void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                  const tsv_config* cfg, int32_t anchor_source, uint64_t p_begin,
                  uint64_t p_end, uint64_t* d_acc, cudaStream_t st,
-                 uint64_t* peak_out) {
+                 uint64_t* peak_out, const VcSpec* vc = nullptr) {
   check_config(cfg);
   if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
   if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
-  if (!sh || sh->n != g->dev.n || sh->k != k)
+  if (!vc && (!sh || sh->n != g->dev.n || sh->k != k))
     throw std::invalid_argument("shade assignment built for a different graph");
+  if (vc && static_cast<int>(vc->order.size()) != k)
+    throw std::invalid_argument("order must have k colors");
   if (cfg->edge_model != g->model)
     throw std::invalid_argument("graph was built for edge model " + std::to_string(g->model) +
                                 ", config asks for " + std::to_string(cfg->edge_model) +
@@ -305,15 +314,22 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
       wtab[(d - 1) * k + (j - 1)] = tsv::draw_nonzero(cfg->seed, tsv::kRoleShadeW, d, j, 0);
   DevBuf d_w(wtab.size() * 8, st), d_zj(static_cast<size_t>(n) * k * 8, st);
   TSV_CUDA(cudaMemcpyAsync(d_w.p, wtab.data(), wtab.size() * 8, cudaMemcpyHostToDevice, st));
-  tsv::launch_zj(n, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
-                 d_zj.as<uint64_t>(), st);
+  if (vc)
+    tsv::launch_zj_positional(n, k, cfg->seed, d_zj.as<uint64_t>(), st);
+  else
+    tsv::launch_zj(n, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
+                   d_zj.as<uint64_t>(), st);
   TSV_CUDA(cudaGetLastError());
 
   if (k == 1) {
     tsv::Batch b;
     b.pb = p_begin;
     b.pe = p_end;
-    tsv::launch_k1(n, d_zj.as<uint64_t>(), b, anchor_source, d_acc, st);
+    if (vc)
+      tsv::launch_k1(n, d_zj.as<uint64_t>(), b, -1, d_acc, st, vc->d_colors, vc->order[0],
+                     vc->wild);
+    else
+      tsv::launch_k1(n, d_zj.as<uint64_t>(), b, anchor_source, d_acc, st);
     TSV_CUDA(cudaGetLastError());
     return;
   }
@@ -353,6 +369,12 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
       lp.last = ell == k;
       lp.max_ts = max_ts;
       lp.acc = d_acc;
+      if (vc) {
+        lp.vc_color = vc->d_colors;
+        lp.vc_head = vc->order[ell - 1];
+        lp.vc_tail = vc->order[ell - 2];
+        lp.vc_wild = vc->wild;
+      }
       tsv::launch_level(lp, st);
       if (lp.last) break;
       tsv::launch_fixup(lp, st);
@@ -857,6 +879,209 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
   });
   tsv_shades_free(sh);
   return rc;
+}
+
+namespace {
+
+// The canonical edges on the graph's device: the resident copy of a device
+// build, else a staged copy of the host-held list.
+struct DeviceEdges {
+  const int32_t *u = nullptr, *v = nullptr, *ts = nullptr;
+  std::vector<int32_t> host_ts;  // canonical timestamps on the host
+  std::unique_ptr<DevBuf> bu, bv, bt;
+  DeviceEdges(const tsv_graph* g, cudaStream_t st) {
+    const int64_t m = g->m;
+    if (g->d_eu) {
+      u = g->d_eu;
+      v = g->d_ev;
+      ts = g->d_ets;
+      host_ts.resize(static_cast<size_t>(m));
+      if (m) TSV_CUDA(cudaMemcpyAsync(host_ts.data(), ts, m * 4, cudaMemcpyDeviceToHost, st));
+      TSV_CUDA(cudaStreamSynchronize(st));
+    } else {
+      bu = std::make_unique<DevBuf>(std::max<int64_t>(m, 1) * 4, st);
+      bv = std::make_unique<DevBuf>(std::max<int64_t>(m, 1) * 4, st);
+      bt = std::make_unique<DevBuf>(std::max<int64_t>(m, 1) * 4, st);
+      if (m) {
+        TSV_CUDA(cudaMemcpyAsync(bu->p, g->host.eu.data(), m * 4, cudaMemcpyHostToDevice, st));
+        TSV_CUDA(cudaMemcpyAsync(bv->p, g->host.ev.data(), m * 4, cudaMemcpyHostToDevice, st));
+        TSV_CUDA(cudaMemcpyAsync(bt->p, g->host.ets.data(), m * 4, cudaMemcpyHostToDevice, st));
+      }
+      u = bu->as<int32_t>();
+      v = bv->as<int32_t>();
+      ts = bt->as<int32_t>();
+      host_ts = g->host.ets;
+    }
+  }
+};
+
+struct StreamGuard {
+  cudaStream_t st = nullptr;
+  StreamGuard() { TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); }
+  ~StreamGuard() {
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  }
+};
+
+}  // namespace
+
+int tsv_eval_edge_constrained(const tsv_graph* g, int k, const int32_t* times,
+                              const int32_t* vertex_off, const int32_t* vertex_shades,
+                              const tsv_config* cfg, uint64_t* accumulators, tsv_outcome* out) {
+  tsv_shades* sh = nullptr;
+  int rc = guard([&] {
+    if (!g || !accumulators || !out || (k > 1 && !times))
+      throw std::invalid_argument("null argument");
+    check_config(cfg);
+    if (k < 2 || k > 30) throw std::invalid_argument("k out of range [2,30]");
+    for (int i = 0; i + 1 < k; ++i) {
+      if (times[i] < 1 || times[i] > g->host.t)
+        throw std::invalid_argument("prescribed timestamp outside [1..t]");
+      if (i > 0 && times[i] <= times[i - 1])
+        throw std::invalid_argument("prescribed timestamps must strictly increase");
+    }
+    if (cfg->edge_model != 0)
+      throw std::invalid_argument("the edge-constrained sieve uses the instant model");
+  });
+  if (rc) return rc;
+  rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
+  if (rc) return rc;
+  rc = guard([&] {
+    DeviceGuard dg(g->device);
+    const int32_t n = g->host.n;
+    StreamGuard sg;
+    cudaStream_t st = sg.st;
+    DeviceEdges E(g, st);
+    const uint64_t P = 1ull << k;
+    // batch width: the n x W state pair plus the z table must fit
+    size_t free_b = 0, total_b = 0;
+    TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    int W = static_cast<int>(std::min<uint64_t>(P, 128));
+    while (W > 1 && 3ull * n * W * 8 > free_b * 0.8) W >>= 1;
+    std::vector<uint64_t> wtab(static_cast<size_t>(k) * k);
+    for (int d = 1; d <= k; ++d)
+      for (int j = 1; j <= k; ++j)
+        wtab[(d - 1) * k + (j - 1)] = tsv::draw_nonzero(cfg->seed, tsv::kRoleShadeW, d, j, 0);
+    DevBuf d_w(wtab.size() * 8, st), d_zj(static_cast<size_t>(n) * k * 8 + 8, st),
+        acc(static_cast<size_t>(n) * 8 + 8, st), zb(static_cast<size_t>(n) * W * 8 + 8, st),
+        s0(static_cast<size_t>(n) * W * 8 + 8, st), s1(static_cast<size_t>(n) * W * 8 + 8, st);
+    TSV_CUDA(cudaMemcpyAsync(d_w.p, wtab.data(), wtab.size() * 8, cudaMemcpyHostToDevice, st));
+    tsv::launch_zj(n, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
+                   d_zj.as<uint64_t>(), st);
+    TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8 + 8, st));
+    // edge range of each prescribed timestamp (edges are sorted by ts)
+    std::vector<std::pair<int64_t, int64_t>> range(static_cast<size_t>(k - 1));
+    for (int i = 0; i + 1 < k; ++i) {
+      auto lo = std::lower_bound(E.host_ts.begin(), E.host_ts.end(), times[i]);
+      auto hi = std::upper_bound(E.host_ts.begin(), E.host_ts.end(), times[i]);
+      range[i] = {lo - E.host_ts.begin(), hi - E.host_ts.begin()};
+    }
+    for (uint64_t pb = 0; pb < P; pb += W) {
+      tsv::Batch b = batch_shape(W);
+      b.pb = pb;
+      b.pe = std::min(P, pb + static_cast<uint64_t>(W));
+      tsv::launch_zbatch(n, d_zj.as<uint64_t>(), k, b, zb.as<uint64_t>(), st);
+      const uint64_t* prev = zb.as<uint64_t>();
+      uint64_t* bufs[2] = {s0.as<uint64_t>(), s1.as<uint64_t>()};
+      for (int ell = 2; ell <= k; ++ell) {
+        uint64_t* cur = bufs[ell & 1];
+        TSV_CUDA(cudaMemsetAsync(cur, 0, static_cast<size_t>(n) * W * 8, st));
+        tsv::launch_ec_level(range[ell - 2].first, range[ell - 2].second, g->host.directed,
+                             E.u, E.v, zb.as<uint64_t>(), W, cfg->seed, ell, prev, cur, st);
+        prev = cur;
+      }
+      tsv::launch_row_xor(n, W, prev, acc.as<uint64_t>(), st);
+    }
+    TSV_CUDA(cudaGetLastError());
+    if (n)
+      TSV_CUDA(cudaMemcpyAsync(accumulators, acc.p, static_cast<size_t>(n) * 8,
+                               cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    finalize_host(n, accumulators, -1, k, out);
+    out->peak_field_words = 3ull * n * W + static_cast<uint64_t>(n) * k + n;
+  });
+  tsv_shades_free(sh);
+  return rc;
+}
+
+int tsv_eval_vertex_ordered(const tsv_graph* g, int k, const int32_t* order,
+                            const int32_t* colors, int32_t wildcard_color, int32_t max_ts,
+                            const tsv_config* cfg, uint64_t* accumulators, tsv_outcome* out) {
+  return guard([&] {
+    if (!g || !order || !accumulators || !out || (g->host.n > 0 && !colors))
+      throw std::invalid_argument("null argument");
+    check_config(cfg);
+    if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
+    if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
+    DeviceGuard dg(g->device);
+    const int32_t n = g->host.n;
+    StreamGuard sg;
+    cudaStream_t st = sg.st;
+    VcSpec vc;
+    DevBuf dcol(static_cast<size_t>(n) * 4 + 4, st), acc(static_cast<size_t>(n) * 8 + 8, st);
+    if (n) TSV_CUDA(cudaMemcpyAsync(dcol.p, colors, static_cast<size_t>(n) * 4,
+                                    cudaMemcpyHostToDevice, st));
+    TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8 + 8, st));
+    vc.d_colors = dcol.as<int32_t>();
+    vc.order.assign(order, order + k);
+    vc.wild = wildcard_color;
+    uint64_t peak = 0;
+    eval_device(g, nullptr, k, max_ts, cfg, -1, 0, 1ull << k, acc.as<uint64_t>(), st, &peak,
+                &vc);
+    if (n)
+      TSV_CUDA(cudaMemcpyAsync(accumulators, acc.p, static_cast<size_t>(n) * 8,
+                               cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    finalize_host(n, accumulators, -1, k, out);
+    out->peak_field_words = peak;
+  });
+}
+
+int tsv_vc_colorful_dp(const tsv_graph* g, int k, const int32_t* order, const int32_t* colors,
+                       int32_t wildcard_color, int32_t max_ts, uint8_t* flagged) {
+  return guard([&] {
+    if (!g || !order || !flagged || (g->host.n > 0 && !colors))
+      throw std::invalid_argument("null argument");
+    if (k < 1) throw std::invalid_argument("k must be positive");
+    DeviceGuard dg(g->device);
+    const int32_t n = g->host.n;
+    StreamGuard sg;
+    cudaStream_t st = sg.st;
+    DeviceEdges E(g, st);
+    constexpr int32_t kInf = INT32_MAX;
+    std::vector<int32_t> e1(static_cast<size_t>(n));
+    for (int32_t u = 0; u < n; ++u)
+      e1[u] = (colors[u] == order[0] || order[0] == wildcard_color) ? 0 : kInf;
+    DevBuf dcol(static_cast<size_t>(n) * 4 + 4, st), a(static_cast<size_t>(n) * 4 + 4, st),
+        b(static_cast<size_t>(n) * 4 + 4, st);
+    if (n) {
+      TSV_CUDA(cudaMemcpyAsync(dcol.p, colors, static_cast<size_t>(n) * 4,
+                               cudaMemcpyHostToDevice, st));
+      TSV_CUDA(cudaMemcpyAsync(a.p, e1.data(), static_cast<size_t>(n) * 4,
+                               cudaMemcpyHostToDevice, st));
+    }
+    int32_t* prev = a.as<int32_t>();
+    int32_t* cur = b.as<int32_t>();
+    for (int ell = 2; ell <= k; ++ell) {
+      // fill with "unreached"
+      std::vector<int32_t> inf(static_cast<size_t>(n), kInf);
+      if (n) TSV_CUDA(cudaMemcpyAsync(cur, inf.data(), static_cast<size_t>(n) * 4,
+                                      cudaMemcpyHostToDevice, st));
+      TSV_CUDA(cudaStreamSynchronize(st));
+      tsv::launch_vc_dp_level(g->m, g->host.directed, E.u, E.v, E.ts, max_ts,
+                              dcol.as<int32_t>(), order[ell - 2], order[ell - 1],
+                              wildcard_color, prev, cur, st);
+      std::swap(prev, cur);
+    }
+    std::vector<int32_t> e(static_cast<size_t>(n));
+    if (n) TSV_CUDA(cudaMemcpyAsync(e.data(), prev, static_cast<size_t>(n) * 4,
+                                    cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    TSV_CUDA(cudaGetLastError());
+    for (int32_t u = 0; u < n; ++u)
+      flagged[u] = (e[u] != kInf && e[u] <= static_cast<int64_t>(max_ts) + 1) ? 1 : 0;
+  });
 }
 
 int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const int32_t* b,

@@ -355,23 +355,27 @@ def test_large_build_canonicalizes_on_device_like_host(cuda_device):
             assert np.array_equal(dev[key], host[key]), key
 
 
-def solve_ex(c, eps, delays, model):
+def solve_ex(c, eps, delays, model, times=(), order=()):
     lib = dropin()
     f = lib.tsieve_solve_json_ex
     f.restype = C.c_int64
     f.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_void_p, C.c_void_p, C.c_int32,
                   C.c_int, C.c_int32, _i32p, C.c_char_p, _i32p, C.c_int32, C.c_int32, C.c_int32,
-                  C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int64]
+                  C.c_int32, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_char_p, C.c_int64,
+                  C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]
     a = lambda x: np.ascontiguousarray(np.asarray(x, dtype=np.int32))  # noqa: E731
     e = a(eps) if eps is not None else None
     d = a(delays) if delays is not None else None
+    tm = a(times) if len(times) else None
+    od = a(order) if len(order) else None
     buf = C.create_string_buffer(1 << 16)
     motif = a(c["motif"]) if c["motif"] else np.zeros(1, np.int32)
     r = f(c["n"], len(c["u"]), a(c["u"]), a(c["v"]), a(c["ts"]),
           None if e is None else e.ctypes.data, None if d is None else d.ctypes.data, model,
           int(c["directed"]), 0, a(c["colors"]), c["problem"].encode(), motif, len(c["motif"]),
           c["k"], c["source"], c["dest"], c["seed"], c["mode"], c["extraction"], c["preprocess"],
-          buf, len(buf))
+          buf, len(buf), None if tm is None else tm.ctypes.data, len(times),
+          None if od is None else od.ctypes.data, len(order))
     if r < 0:
         raise ValueError(lib.tsieve_last_error().decode())
     return json.loads(buf.value.decode())
@@ -458,3 +462,55 @@ def test_cli_edge_models_from_files(cuda_device, tmp_path):
         assert rec["decision"] == ("YES" if want["decision"] else "NO"), (model, rec, want)
         assert rec["accumulator_checksum"] == want["checksum"]
         assert rec["config"]["edge_model"] == {1: "transition", 3: "transition-delay"}[model]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("problem", ["ectemppath", "ecpathmotif", "vcpathmotif",
+                                     "vccolorfulpath"])
+def test_solver_ec_vc_problems_match_reference(cuda_device, problem):
+    """Edge-constrained (prescribed timestamps) and vertex-ordered (position
+    colors) problems: the EC and VC sieves and the VC-ColorfulPath exact DP on
+    the device, the DFS with timed / ordered constraints; every record field
+    equals the reference's (decide / optimum / extract, both strategies,
+    preprocess none / colors / both)."""
+    from oracle import oracle as O
+    from paper_2001_07158_b200 import synth
+    rng = np.random.default_rng(sum(map(ord, problem)))
+    found = 0
+    for i in range(28):
+        n, u, v, ts, d, colors, _ = synth.random_small(rng, n_max=14, m_max=60, t_max=8,
+                                                       k_max=4, q_max=3)
+        k = int(rng.integers(2, 5))
+        times, order, motif = [], [], []
+        if problem.startswith("ec"):
+            # prescribed stamps: often those of an existing increasing walk
+            if i % 3 and len(ts):
+                cand = sorted(set(ts.tolist()))
+                pick = sorted(rng.choice(cand, min(k - 1, len(cand)), replace=False).tolist())
+                times = pick
+            else:
+                times = sorted(rng.choice(np.arange(1, 9), k - 1, replace=False).tolist())
+            k = len(times) + 1
+            if problem == "ecpathmotif":
+                motif = sorted(rng.integers(1, int(colors.max()) + 1, k).tolist())
+        else:
+            q = int(colors.max())
+            if problem == "vccolorfulpath":
+                k = min(k, q)
+                order = rng.permutation(np.arange(1, q + 1))[:k].tolist()
+            else:
+                order = rng.integers(1, q + 1, k).tolist()
+        c = {"n": n, "u": u.tolist(), "v": v.tolist(), "ts": ts.tolist(), "directed": d,
+             "colors": colors.tolist(), "problem": problem, "motif": motif, "k": 0,
+             "source": -1, "dest": -1, "seed": int(rng.integers(1, 1000)),
+             "mode": [0, 1, 2, 3][i % 4], "extraction": (i // 4) % 2,
+             "preprocess": [0, 1, 3][(i // 8) % 3]}
+        want = O.ref_solve_query(n, u, v, ts, times, order, d, colors, problem, motif, 0,
+                                 seed=c["seed"], mode=c["mode"], extraction=c["extraction"],
+                                 preprocess=c["preprocess"])
+        got = solve_ex(c, None, None, 0, times=times, order=order)
+        for key in ("decision", "certain", "optimum_ts", "checksum", "flagged", "witness",
+                    "extraction_failed", "oracle_calls", "preprocessed_n", "preprocessed_m"):
+            assert got[key] == want[key], (key, problem, i, times, order, got, want)
+        found += got["witness"] is not None
+    assert found >= 2
