@@ -139,6 +139,8 @@ int64_t device_restrict(const int32_t* eu, const int32_t* ev, const int32_t* ets
                         const std::function<void(void*)>& release);
 
 // Kernel launchers (kernels.cu).  All are asynchronous on `st`.
+// w_{d,j} table (k x k) of the constrained substitution, on the device
+void launch_wtab(int k, uint64_t seed, uint64_t* wtab, cudaStream_t st);
 void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
                const int32_t* vertex_shades, const uint64_t* wtab, uint64_t* zj,
                cudaStream_t st);

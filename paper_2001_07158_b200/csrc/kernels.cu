@@ -549,6 +549,16 @@ __global__ void k_k1(int32_t n, const uint64_t* __restrict__ zj, Batch b,
   acc[u] ^= x;
 }
 
+// w_{d,j} = draw(seed, shade_w, d, j) for d, j in [1..k] (sieve.cpp:85-89),
+// drawn on the device so no pageable host copy stalls the stream
+__global__ void k_wtab(int k, uint64_t seed, uint64_t* __restrict__ wtab) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= k * k) return;
+  const uint64_t pre = draw_prefix(seed, kRoleShadeW);
+  wtab[i] = draw_nonzero_from(pre, static_cast<uint64_t>(i / k + 1),
+                              static_cast<uint64_t>(i % k + 1), 0);
+}
+
 // z_{u,j} = XOR_{d in S(u)} v_{u,d} * w_{d,j}  (sieve.cpp:83-101)
 __global__ void k_zj(int32_t n, int k, uint64_t seed,
                      const int32_t* __restrict__ vertex_off,
@@ -733,6 +743,10 @@ void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
   prof_begin("k1", st);
   k_k1<<<blocks_for(n, 256), 256, 0, st>>>(n, zj, b, anchor_source, acc, colors, color, wild);
   prof_end(st);
+}
+
+void launch_wtab(int k, uint64_t seed, uint64_t* wtab, cudaStream_t st) {
+  k_wtab<<<blocks_for(static_cast<int64_t>(k) * k, 256), 256, 0, st>>>(k, seed, wtab);
 }
 
 void launch_zj(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,

@@ -237,8 +237,10 @@ tsv::Batch batch_shape(int W) {
 // Points per batch: the largest power of two <= min(range, 128) whose
 // working set fits the word cap and free device memory.
 // *zb_ok: the per-batch z table (n*W words) also fits next to that working set.
+// *lanes: 2 when there are several batches and two working sets fit, so that
+// consecutive batches run on two streams (their kernels overlap), else 1.
 int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cfg,
-                 uint64_t* peak_words, bool* zb_ok) {
+                 uint64_t* peak_words, bool* zb_ok, int* lanes) {
   // state rows = referenced runs (slots); R is kept for the z-table rule
   const uint64_t R = static_cast<uint64_t>(g->dev.R), C = static_cast<uint64_t>(g->dev.C);
   const uint64_t S = static_cast<uint64_t>(g->dev.S);
@@ -270,6 +272,13 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
   *zb_ok = k >= 2 && n * 8 <= R && words(W) + zw <= budget &&
            words(W) + zw <= cfg->memory_cap_words;
   *peak_words = words(W) + (*zb_ok ? zw : 0);
+  *lanes = 1;
+  const uint64_t lane_words = words(W) - n * static_cast<uint64_t>(k) - n + (*zb_ok ? zw : 0);
+  if (range > static_cast<uint64_t>(W) && *peak_words + lane_words <= budget &&
+      *peak_words + lane_words <= cfg->memory_cap_words && !std::getenv("TSV_ONE_LANE")) {
+    *lanes = 2;
+    *peak_words += lane_words;
+  }
   if (words(W) > cfg->memory_cap_words)
     throw CapError("sieve memory cap exceeded: needs " + std::to_string(words(W)) +
                    " field words, cap " + std::to_string(cfg->memory_cap_words));
@@ -303,17 +312,14 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   if (p_begin >= p_end) return;
   uint64_t peak = 0;
   bool zb_ok = false;
-  const int W = choose_width(g, k, p_end - p_begin, cfg, &peak, &zb_ok);
+  int nlanes = 1;
+  const int W = choose_width(g, k, p_end - p_begin, cfg, &peak, &zb_ok, &nlanes);
   if (peak_out) *peak_out = peak;
   const int32_t n = g->dev.n;
 
   // w_{d,j} table on the host (k^2 draws), z_{u,j} on the device.
-  std::vector<uint64_t> wtab(static_cast<size_t>(k) * k);
-  for (int d = 1; d <= k; ++d)
-    for (int j = 1; j <= k; ++j)
-      wtab[(d - 1) * k + (j - 1)] = tsv::draw_nonzero(cfg->seed, tsv::kRoleShadeW, d, j, 0);
-  DevBuf d_w(wtab.size() * 8, st), d_zj(static_cast<size_t>(n) * k * 8, st);
-  TSV_CUDA(cudaMemcpyAsync(d_w.p, wtab.data(), wtab.size() * 8, cudaMemcpyHostToDevice, st));
+  DevBuf d_w(static_cast<size_t>(k) * k * 8, st), d_zj(static_cast<size_t>(n) * k * 8, st);
+  tsv::launch_wtab(k, cfg->seed, d_w.as<uint64_t>(), st);
   if (vc)
     tsv::launch_zj_positional(n, k, cfg->seed, d_zj.as<uint64_t>(), st);
   else
@@ -334,29 +340,59 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
     return;
   }
   const size_t state_words = static_cast<size_t>(std::max<int64_t>(g->dev.S, 1)) * W;
-  DevBuf s0(state_words * 8, st), s1(state_words * 8, st),
-      agg(static_cast<size_t>(g->dev.C) * W * 8, st);
-  tsv::LevelParams lp;
-  lp.g = g->dev;
-  lp.zj = d_zj.as<uint64_t>();
-  lp.k = k;
-  lp.seed = cfg->seed;
-  lp.anchor_source = anchor_source;
-  lp.agg = agg.as<uint64_t>();
-  if (const char* e = std::getenv("TSV_YMUL"))
-    lp.ymul = std::strcmp(e, "holes") == 0 ? 1 : 0;
   // Level 2 reads z_tail^A for every arc and the run-end products z_head^A:
   // when the per-batch table z[u][w] is small next to the state (n <= R/8)
   // and fits, it is materialized once per batch and gathered like a state row.
   const uint64_t zb_bytes = static_cast<uint64_t>(n) * W * 8;
   const bool use_zb = zb_ok;
-  DevBuf zb(use_zb ? zb_bytes : 8, st);
-  for (uint64_t pb = p_begin; pb < p_end; pb += W) {
+  // One or two lanes (stream + private working set); batch i runs on lane
+  // i % lanes, the second lane's stream forked from / joined to `st`.
+  struct Lane {
+    cudaStream_t st = nullptr;
+    std::unique_ptr<DevBuf> s0, s1, agg, zb;
+  };
+  std::vector<Lane> lanes(static_cast<size_t>(nlanes));
+  cudaEvent_t fork = nullptr, join = nullptr;
+  for (int l = 0; l < nlanes; ++l) {
+    Lane& L = lanes[l];
+    if (l == 0) {
+      L.st = st;
+    } else {
+      TSV_CUDA(cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking));
+    }
+    L.s0 = std::make_unique<DevBuf>(state_words * 8, st);
+    L.s1 = std::make_unique<DevBuf>(state_words * 8, st);
+    L.agg = std::make_unique<DevBuf>(static_cast<size_t>(g->dev.C) * W * 8, st);
+    L.zb = std::make_unique<DevBuf>(use_zb ? zb_bytes : 8, st);
+  }
+  if (nlanes > 1) {  // lane 1 starts after z and the buffers exist on `st`
+    TSV_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    TSV_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    TSV_CUDA(cudaEventRecord(fork, st));
+    TSV_CUDA(cudaStreamWaitEvent(lanes[1].st, fork, 0));
+  }
+  tsv::LevelParams base_lp;
+  base_lp.g = g->dev;
+  base_lp.zj = d_zj.as<uint64_t>();
+  base_lp.k = k;
+  base_lp.seed = cfg->seed;
+  base_lp.anchor_source = anchor_source;
+  if (const char* e = std::getenv("TSV_YMUL"))
+    base_lp.ymul = std::strcmp(e, "holes") == 0 ? 1 : 0;
+  uint64_t batch_no = 0;
+  for (uint64_t pb = p_begin; pb < p_end; pb += W, ++batch_no) {
+    Lane& L = lanes[batch_no % lanes.size()];
+    const cudaStream_t bst = L.st;
+    tsv::LevelParams lp = base_lp;
+    lp.agg = L.agg->as<uint64_t>();
+    DevBuf& zb = *L.zb;
+    DevBuf& s0 = *L.s0;
+    DevBuf& s1 = *L.s1;
     lp.b = batch_shape(W);
     lp.b.pb = pb;
     lp.b.pe = std::min(p_end, pb + static_cast<uint64_t>(W));
     if (use_zb) {
-      tsv::launch_zbatch(n, d_zj.as<uint64_t>(), k, lp.b, zb.as<uint64_t>(), st);
+      tsv::launch_zbatch(n, d_zj.as<uint64_t>(), k, lp.b, zb.as<uint64_t>(), bst);
       lp.zb = zb.as<uint64_t>();
     }
     uint64_t* cur = s0.as<uint64_t>();
@@ -375,12 +411,19 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
         lp.vc_tail = vc->order[ell - 2];
         lp.vc_wild = vc->wild;
       }
-      tsv::launch_level(lp, st);
+      tsv::launch_level(lp, bst);
       if (lp.last) break;
-      tsv::launch_fixup(lp, st);
+      tsv::launch_fixup(lp, bst);
       std::swap(cur, prev);
     }
     TSV_CUDA(cudaGetLastError());
+  }
+  if (nlanes > 1) {  // join lane 1 back into `st` before its buffers are freed
+    TSV_CUDA(cudaEventRecord(join, lanes[1].st));
+    TSV_CUDA(cudaStreamWaitEvent(st, join, 0));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    cudaStreamDestroy(lanes[1].st);  // released once its work completes
   }
 }
 
@@ -959,14 +1002,10 @@ int tsv_eval_edge_constrained(const tsv_graph* g, int k, const int32_t* times,
     TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
     int W = static_cast<int>(std::min<uint64_t>(P, 128));
     while (W > 1 && 3ull * n * W * 8 > free_b * 0.8) W >>= 1;
-    std::vector<uint64_t> wtab(static_cast<size_t>(k) * k);
-    for (int d = 1; d <= k; ++d)
-      for (int j = 1; j <= k; ++j)
-        wtab[(d - 1) * k + (j - 1)] = tsv::draw_nonzero(cfg->seed, tsv::kRoleShadeW, d, j, 0);
-    DevBuf d_w(wtab.size() * 8, st), d_zj(static_cast<size_t>(n) * k * 8 + 8, st),
+    DevBuf d_w(static_cast<size_t>(k) * k * 8, st), d_zj(static_cast<size_t>(n) * k * 8 + 8, st),
         acc(static_cast<size_t>(n) * 8 + 8, st), zb(static_cast<size_t>(n) * W * 8 + 8, st),
         s0(static_cast<size_t>(n) * W * 8 + 8, st), s1(static_cast<size_t>(n) * W * 8 + 8, st);
-    TSV_CUDA(cudaMemcpyAsync(d_w.p, wtab.data(), wtab.size() * 8, cudaMemcpyHostToDevice, st));
+    tsv::launch_wtab(k, cfg->seed, d_w.as<uint64_t>(), st);
     tsv::launch_zj(n, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
                    d_zj.as<uint64_t>(), st);
     TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8 + 8, st));
