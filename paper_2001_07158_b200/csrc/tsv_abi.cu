@@ -1182,9 +1182,11 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
     std::vector<int32_t> ih, it, ie, oh, ot, oe;
     arcs(true, ih, it, ie);
     if (junction) arcs(false, oh, ot, oe);
+    // chunks sized to give every SM several warps (a 256-arc chunk left the
+    // C2 projection with 191 blocks, 16% of the warp slots busy)
     auto chunks = [](int64_t A) {
       std::vector<int64_t> c;
-      const int64_t ch = 256;
+      const int64_t ch = std::min<int64_t>(256, std::max<int64_t>(32, A / (148 * 64)));
       for (int64_t s = 0; s < A; s += ch) c.push_back(s);
       c.push_back(A);
       return c;
