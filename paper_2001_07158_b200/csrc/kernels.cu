@@ -80,6 +80,38 @@ __device__ __forceinline__ uint64_t z_single(const uint64_t* __restrict__ zj,
 // products runs with all 32 lanes busy.  Level k (LAST) enqueues one entry per
 // vertex piece (its last arc within max_ts) and the pop XORs the group's
 // z_head * prefix into acc[head] (fused readout, like flush_vertex).
+// Window w of a GfTable (the 16 multiples c * x^(4w) * y) written by one
+// lane: 16 lanes build a whole table (the half-warp variant of
+// GfTable::build).  With the 136-byte window stride the 16 lanes' stores of
+// one entry hit 16 distinct bank pairs.
+__device__ __forceinline__ void build_window16(uint64_t* tab, uint64_t y, int w) {
+  const uint32_t s = 4u * static_cast<uint32_t>(w);
+  uint64_t h, lo;
+  asm("shr.b64 %0, %1, %2;" : "=l"(h) : "l"(y), "r"(64u - s));  // 0 when s == 0
+  asm("shl.b64 %0, %1, %2;" : "=l"(lo) : "l"(y), "r"(s));
+  const uint64_t B0 = lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4);
+  const uint64_t B1 = gf_mulx(B0), B2 = gf_mulx(B1), B3 = gf_mulx(B2);
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) +
+                     GfTable::kWinBytes * static_cast<uint32_t>(w);
+  const uint64_t v3 = B1 ^ B0, v5 = B2 ^ B0, v6 = B2 ^ B1, v7 = v6 ^ B0;
+  GfTable::sts<0>(a, 0ull);
+  GfTable::sts<8>(a, B0);
+  GfTable::sts<16>(a, B1);
+  GfTable::sts<24>(a, v3);
+  GfTable::sts<32>(a, B2);
+  GfTable::sts<40>(a, v5);
+  GfTable::sts<48>(a, v6);
+  GfTable::sts<56>(a, v7);
+  GfTable::sts<64>(a, B3);
+  GfTable::sts<72>(a, B3 ^ B0);
+  GfTable::sts<80>(a, B3 ^ B1);
+  GfTable::sts<88>(a, B3 ^ v3);
+  GfTable::sts<96>(a, B3 ^ B2);
+  GfTable::sts<104>(a, B3 ^ v5);
+  GfTable::sts<112>(a, B3 ^ v6);
+  GfTable::sts<120>(a, B3 ^ v7);
+}
+
 template <int LANES, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     k_level(const LevelParams P) {
@@ -94,6 +126,13 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
   __shared__ int32_t q_run[kWarpsPerBlock][2 * G];
   __shared__ int32_t q_head[kWarpsPerBlock][2 * G];
   __shared__ uint64_t q_val[kWarpsPerBlock][2 * G][LANES];
+  // LANES == 16: each half-warp multiplies by its own arc's y through a
+  // shared-memory table it builds (16 lanes x one window each) instead of
+  // the general product
+  constexpr bool kHalfTab = LANES == 16;
+  __shared__ __align__(256) uint64_t s_gtab[kHalfTab ? kWarpsPerBlock : 1][kHalfTab ? 2 : 1]
+                                           [GfTable::kWords];
+  __shared__ uint64_t s_yraw[kHalfTab ? kWarpsPerBlock : 1][32];
 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t c = static_cast<int64_t>(blockIdx.x) * kWarpsPerBlock + wib;
@@ -148,7 +187,9 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
     const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
     const int32_t myrun = run_ctr + __popc(ends & ((1u << lane) - 1u));
     if (lane < nb) head = __ldg(P.g.run_head + myrun);
-    {
+    if (kHalfTab) {
+      s_yraw[kHalfTab ? wib : 0][lane] = y;
+    } else {
       const KSplit ks = ksplit(y);  // once per arc, not once per lane of its group
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -212,15 +253,23 @@ __global__ void __launch_bounds__(kWarpsPerBlock * 32, 3)
       const uint32_t mt = act ? s_meta[wib][i] : 0u;
       uint64_t v = 0;
       if (__any_sync(kFull, mt & kLive)) {
-        KSplit ys;
         const int ia = act ? i : 0;
+        if (kHalfTab) {
+          uint64_t* tab = s_gtab[kHalfTab ? wib : 0][kHalfTab ? g : 0];
+          __syncwarp();
+          build_window16(tab, s_yraw[kHalfTab ? wib : 0][ia], li);
+          __syncwarp();
+          v = (mt & kLive) ? GfTable{tab}.mul(val) : 0ull;
+        } else {
+          KSplit ys;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          ys.l.c[j] = s_ys[wib][j][ia];
-          ys.h.c[j] = s_ys[wib][4 + j][ia];
-          ys.m.c[j] = s_ys[wib][8 + j][ia];
+          for (int j = 0; j < 4; ++j) {
+            ys.l.c[j] = s_ys[wib][j][ia];
+            ys.h.c[j] = s_ys[wib][4 + j][ia];
+            ys.m.c[j] = s_ys[wib][8 + j][ia];
+          }
+          v = (mt & kLive) ? gf_mul_presplit(ys, val) : 0ull;
         }
-        v = (mt & kLive) ? gf_mul_presplit(ys, val) : 0ull;
       }
       // segmented inclusive XOR-scan over the G groups (vertex starts cut it)
       bool f = (mt & kVStart) != 0;
