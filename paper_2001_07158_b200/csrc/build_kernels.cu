@@ -21,6 +21,9 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "engine.hpp"
@@ -30,6 +33,24 @@ namespace tsv {
 namespace {
 
 constexpr int kT = 256;
+
+// TSV_TRACE_BUILD=1: phase times of the device build on stderr
+struct BuildTrace {
+  bool on = false;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit BuildTrace(cudaStream_t s) : st(s), t0(std::chrono::steady_clock::now()) {
+    const char* e = std::getenv("TSV_TRACE_BUILD");
+    on = e && e[0] == '1';
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const double ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, "[build] %-28s %9.1f ms\n", what, ms);
+  }
+};
 
 unsigned nblk(int64_t n) { return static_cast<unsigned>((n + kT - 1) / kT); }
 
@@ -349,6 +370,7 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
                   const std::function<void*(size_t)>& alloc,
                   const std::function<void(void*)>& release, const int32_t* d_eps,
                   const int32_t* d_delay) {
+  BuildTrace tr(st);
   auto A32 = [&](int64_t cnt) { return static_cast<int32_t*>(alloc(std::max<int64_t>(cnt, 1) * 4)); };
   BuildStatus init{};
   init.first_bad_endpoint = INT64_MAX;
@@ -395,8 +417,11 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
     cub::DoubleBuffer<uint32_t> bts(kts[1], kts[0]);
     if (mc > 0 && hs.first_bad_endpoint == INT64_MAX && hs.first_bad_ts == INT64_MAX) {
       // pass 1: by (u, v); pass 2 (stable): by ts
+      tr.mark("validate + compact");
       radix_pairs(buv, bts, mc, bits_for(nn ? nn - 1 : 0), st);
+      tr.mark("sort by (u, v)");
       radix_pairs(bts, buv, mc, bits_for(static_cast<uint64_t>(hs.max_ts)), st);
+      tr.mark("sort by ts");
     }
     uint8_t* flag = static_cast<uint8_t*>(alloc(std::max<int64_t>(mc, 1)));
     if (mc) k_unique_flags<<<nblk(mc), kT, 0, st>>>(mc, bts.Current(), buv.Current(), flag);
@@ -424,6 +449,7 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
     release(kts[0]);
     release(kts[1]);
   }
+  tr.mark("unique + unpack");
   out.m = mc;
   out.eu = eu;
   out.ev = ev;
@@ -487,6 +513,7 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
                                            out.arc_meta);
   out.arc_tail = tail;
 
+  tr.mark("arcs: sort, runs, sources");
   // ---- chunks ---------------------------------------------------------------
   int64_t ch = A / (static_cast<int64_t>(std::max(sm_count, 1)) * 64);
   ch = std::min<int64_t>(2048, std::max<int64_t>(64, ch));
@@ -552,6 +579,7 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
   release(run_incl);
   release(hd[0]);
   release(hd[1]);
+  tr.mark("chunks");
   release(ix[0]);
   release(ix[1]);
 }
@@ -585,6 +613,58 @@ __global__ void k_src_to_slot(int64_t A, int32_t* __restrict__ arc_src,
 }
 
 }  // namespace
+
+namespace {
+
+__global__ void k_run_end_flags(int64_t A, const uint32_t* __restrict__ meta,
+                                int32_t* __restrict__ f) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a < A) f[a] = (meta[a] & kRunEnd) ? 1 : 0;
+}
+
+// arc a lies in run (number of run ends before it); its edge (u, v, ts):
+// directed -> (tail, head); undirected -> the arc with tail < head writes
+__global__ void k_edges_from_arcs(int64_t A, int directed, const uint32_t* __restrict__ meta,
+                                  const int32_t* __restrict__ tail,
+                                  const int32_t* __restrict__ ends_before,
+                                  const int32_t* __restrict__ run_head,
+                                  const int32_t* __restrict__ run_ts, int32_t* __restrict__ eu,
+                                  int32_t* __restrict__ ev, int32_t* __restrict__ ets) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  const int32_t r = ends_before[a];
+  const int32_t h = run_head[r], t = tail[a];
+  if (!directed && t > h) return;
+  const uint32_t e = meta[a] & kEdgeMask;
+  eu[e] = t;
+  ev[e] = h;
+  ets[e] = run_ts[r];
+}
+
+}  // namespace
+
+void edges_from_layout(const DevGraph& g, bool directed, int32_t* eu, int32_t* ev, int32_t* ets,
+                       cudaStream_t st) {
+  const int64_t A = g.A;
+  if (A == 0) return;
+  constexpr int kTb = 256;
+  const unsigned blocks = static_cast<unsigned>((A + kTb - 1) / kTb);
+  int32_t *f = nullptr, *ex = nullptr;
+  void* tmp = nullptr;
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, f, ex, A, st);
+  if (cudaMallocAsync(&f, A * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&ex, A * 4, st) != cudaSuccess ||
+      cudaMallocAsync(&tmp, tb ? tb : 8, st) != cudaSuccess)
+    throw std::runtime_error("edge reconstruction: out of device memory");
+  k_run_end_flags<<<blocks, kTb, 0, st>>>(A, g.arc_meta, f);
+  cub::DeviceScan::ExclusiveSum(tmp, tb, f, ex, A, st);
+  k_edges_from_arcs<<<blocks, kTb, 0, st>>>(A, directed ? 1 : 0, g.arc_meta, g.arc_tail, ex,
+                                            g.run_head, g.run_ts, eu, ev, ets);
+  cudaFreeAsync(f, st);
+  cudaFreeAsync(ex, st);
+  cudaFreeAsync(tmp, st);
+}
 
 SlotCounts build_run_slots(int64_t A, int64_t R, int32_t* arc_src, int32_t* run_slot,
                            cudaStream_t st) {

@@ -168,6 +168,12 @@ void launch_vc_dp_level(int64_t m, int directed, const int32_t* eu, const int32_
                         const int32_t* ets, int32_t max_ts, const int32_t* colors,
                         int32_t tail_color, int32_t head_color, int32_t wild,
                         const int32_t* e_prev, int32_t* e_next, cudaStream_t st);
+// Canonical edges (edge id order) rebuilt from an instant-model layout: the
+// arc carrying edge id e knows its tail, its run's head and timestamp
+// (build_kernels.cu).  Outputs are device arrays of m entries.
+void edges_from_layout(const DevGraph& g, bool directed, int32_t* eu, int32_t* ev, int32_t* ets,
+                       cudaStream_t st);
+
 // State slots (build_kernels.cu): run_slot[r] = rank of r among the runs
 // some arc reads (else -1) and arc_src rewritten from run indices to slots.
 // Returns {arcs with a src, referenced runs}; synchronizes `st`.

@@ -6,6 +6,9 @@
 // rethrows them as the reference's exception types.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -164,6 +167,7 @@ struct tsv_graph {
   int64_t device_bytes = 0;
   int64_t m = 0;                      // canonical edge count
   int model = 0;                      // edge model the layout was built for
+  bool edges_in_layout = false;       // canonical edges only implied by the layout
   int64_t arcs_with_src = 0, runs_referenced = 0;
   const int32_t* d_eu = nullptr;      // canonical edges on the device (device build)
   const int32_t* d_ev = nullptr;
@@ -508,6 +512,17 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
       if (n && delays) TSV_CUDA(cudaMemcpyAsync(ddel, delays, static_cast<size_t>(n) * 4, kind, st));
       else if (n) TSV_CUDA(cudaMemsetAsync(ddel, 0, static_cast<size_t>(n) * 4, st));
     }
+    const char* tre = std::getenv("TSV_TRACE_BUILD");
+    const bool trace = tre && tre[0] == '1';
+    const auto tb0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+      if (!trace) return;
+      cudaStreamSynchronize(st);
+      std::fprintf(stderr, "[build] %-28s %9.1f ms (total)\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                             tb0).count());
+    };
+    mark("uploads");
     auto* status = static_cast<tsv::BuildStatus*>(alloc(sizeof(tsv::BuildStatus)));
     tsv::DeviceLayout L;
     tsv::device_build(du, dv, dts, m, n, directed, canonical, L, status,
@@ -535,15 +550,12 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     g->host.dropped_self_loops = canonical ? 0 : hs.self_loops;
     g->host.dropped_duplicates = L.dropped_duplicates;
     g->m = L.m;
-    if (L.m > (int64_t{1} << 26)) {
-      // large graphs: the canonical edge list is only needed on demand
-      // (tsv_graph_edges); keep it in host memory, not in HBM
-      g->host.eu.resize(L.m);
-      g->host.ev.resize(L.m);
-      g->host.ets.resize(L.m);
-      TSV_CUDA(cudaMemcpyAsync(g->host.eu.data(), L.eu, L.m * 4, cudaMemcpyDeviceToHost, st));
-      TSV_CUDA(cudaMemcpyAsync(g->host.ev.data(), L.ev, L.m * 4, cudaMemcpyDeviceToHost, st));
-      TSV_CUDA(cudaMemcpyAsync(g->host.ets.data(), L.ets, L.m * 4, cudaMemcpyDeviceToHost, st));
+    const char* eil = std::getenv("TSV_EDGES_IN_LAYOUT");  // (tests: force the mode)
+    if ((L.m > (int64_t{1} << 26) || (eil && eil[0] == '1')) && model == 0) {
+      // large graphs: the canonical edge list is needed only on demand
+      // (tsv_graph_edges, restriction, EC/VC); it is rebuilt from the layout
+      // then (edges_from_layout), so neither HBM nor a host copy holds it
+      g->edges_in_layout = true;
       release(L.eu);
       release(L.ev);
       release(L.ets);
@@ -574,6 +586,7 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     g->runs_referenced = sc.slots;
     d.run_slot = slots;
     d.S = sc.slots;
+    mark("state slots");
     g->device_bytes = 12 * L.A + 12 * L.R + 4 * (static_cast<int64_t>(n) + 1) + 12 * L.m +
                       17 * (L.C + 1);
     TSV_CUDA(cudaStreamSynchronize(st));
@@ -758,7 +771,15 @@ int tsv_graph_restrict(const tsv_graph* g, const uint8_t* keep_vertex, int32_t m
       auto* keep = static_cast<uint8_t*>(alloc(std::max<int64_t>(n, 1)));
       if (n) TSV_CUDA(cudaMemcpyAsync(keep, keep_vertex, n, cudaMemcpyHostToDevice, st));
       const int32_t *eu = g->d_eu, *ev = g->d_ev, *ets = g->d_ets;
-      if (!eu) {  // canonical edges held on the host: stage them
+      if (!eu && g->edges_in_layout) {  // rebuilt on the device from the layout
+        auto* a = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        auto* b = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        auto* c = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        tsv::edges_from_layout(g->dev, g->host.directed, a, b, c, st);
+        eu = a;
+        ev = b;
+        ets = c;
+      } else if (!eu) {  // canonical edges held on the host: stage them
         auto* a = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
         auto* b = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
         auto* c = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
@@ -825,6 +846,16 @@ int tsv_graph_edges(const tsv_graph* g, int32_t* u, int32_t* v, int32_t* ts) {
       if (m && ts) TSV_CUDA(cudaMemcpy(ts, g->d_ets, m * 4, cudaMemcpyDeviceToHost));
       return;
     }
+    if (g->edges_in_layout) {  // large device-built graph: rebuild from the layout
+      DeviceGuard dg(g->device);
+      DevBuf a(m * 4 + 4, nullptr), b(m * 4 + 4, nullptr), c(m * 4 + 4, nullptr);
+      tsv::edges_from_layout(g->dev, g->host.directed, a.as<int32_t>(), b.as<int32_t>(),
+                             c.as<int32_t>(), nullptr);
+      if (m && u) TSV_CUDA(cudaMemcpy(u, a.p, m * 4, cudaMemcpyDeviceToHost));
+      if (m && v) TSV_CUDA(cudaMemcpy(v, b.p, m * 4, cudaMemcpyDeviceToHost));
+      if (m && ts) TSV_CUDA(cudaMemcpy(ts, c.p, m * 4, cudaMemcpyDeviceToHost));
+      return;
+    }
     if (m && u) std::memcpy(u, g->host.eu.data(), m * 4);
     if (m && v) std::memcpy(v, g->host.ev.data(), m * 4);
     if (m && ts) std::memcpy(ts, g->host.ets.data(), m * 4);
@@ -839,13 +870,14 @@ int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
     if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
     const int32_t n = g->host.n;
     if (vertex_off[0] != 0) throw std::invalid_argument("vertex_off[0] must be 0");
-    for (int32_t i = 0; i < n; ++i)
-      if (vertex_off[i + 1] < vertex_off[i])
-        throw std::invalid_argument("vertex_off must be non-decreasing");
+    int bad_off = 0, bad_shade = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad_off)
+    for (int32_t i = 0; i < n; ++i) bad_off |= vertex_off[i + 1] < vertex_off[i];
+    if (bad_off) throw std::invalid_argument("vertex_off must be non-decreasing");
     const int64_t cnt = vertex_off[n];
-    for (int64_t i = 0; i < cnt; ++i)
-      if (vertex_shades[i] < 1 || vertex_shades[i] > k)
-        throw std::invalid_argument("shade id outside [1..k]");
+#pragma omp parallel for schedule(static) reduction(| : bad_shade)
+    for (int64_t i = 0; i < cnt; ++i) bad_shade |= vertex_shades[i] < 1 || vertex_shades[i] > k;
+    if (bad_shade) throw std::invalid_argument("shade id outside [1..k]");
     DeviceGuard dg(g->device);
     auto* s = new tsv_shades();
     s->k = k;
@@ -939,10 +971,21 @@ struct DeviceEdges {
   std::unique_ptr<DevBuf> bu, bv, bt;
   DeviceEdges(const tsv_graph* g, cudaStream_t st) {
     const int64_t m = g->m;
-    if (g->d_eu) {
-      u = g->d_eu;
-      v = g->d_ev;
-      ts = g->d_ets;
+    if (g->d_eu || g->edges_in_layout) {
+      if (g->d_eu) {
+        u = g->d_eu;
+        v = g->d_ev;
+        ts = g->d_ets;
+      } else {  // rebuilt from the layout
+        bu = std::make_unique<DevBuf>(std::max<int64_t>(m, 1) * 4, st);
+        bv = std::make_unique<DevBuf>(std::max<int64_t>(m, 1) * 4, st);
+        bt = std::make_unique<DevBuf>(std::max<int64_t>(m, 1) * 4, st);
+        tsv::edges_from_layout(g->dev, g->host.directed, bu->as<int32_t>(), bv->as<int32_t>(),
+                               bt->as<int32_t>(), st);
+        u = bu->as<int32_t>();
+        v = bv->as<int32_t>();
+        ts = bt->as<int32_t>();
+      }
       host_ts.resize(static_cast<size_t>(m));
       if (m) TSV_CUDA(cudaMemcpyAsync(host_ts.data(), ts, m * 4, cudaMemcpyDeviceToHost, st));
       TSV_CUDA(cudaStreamSynchronize(st));

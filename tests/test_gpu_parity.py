@@ -399,3 +399,27 @@ def test_edge_model_mismatch_is_rejected(cuda_device):
         T.eval_temporal_sieve(g, 3, g.t(), sh, cfg)
     with pytest.raises(ValueError, match="transition time below 1"):
         T.TemporalGraph.build_model(3, [(0, 1, 1)], True, "transition", eps=[0])
+
+
+def test_edges_rebuilt_from_layout(cuda_device, monkeypatch):
+    """Large device-built graphs keep no canonical edge list (neither in HBM
+    nor on the host): edges(), restriction and the EC engine rebuild it from
+    the arc layout.  Forced here on small graphs (TSV_EDGES_IN_LAYOUT=1) and
+    compared with the stored-list build."""
+    rng = np.random.default_rng(44)
+    for directed in (True, False):
+        n, m, t = 300, 5000, 40
+        u = rng.integers(0, n, m)
+        v = np.where(rng.random(m) < 0.3, 3, rng.integers(0, n, m))
+        ts = rng.integers(1, t + 1, m)
+        ref = T.TemporalGraph.build(n, (u, v, ts), directed)
+        monkeypatch.setenv("TSV_EDGES_IN_LAYOUT", "1")
+        g = T.TemporalGraph.build(n, (u, v, ts), directed)
+        monkeypatch.delenv("TSV_EDGES_IN_LAYOUT")
+        for a, b in zip(g.edges(), ref.edges()):
+            assert np.array_equal(a, b)
+        keep = rng.random(n) < 0.8
+        r1 = T.restrict_to(g, keep, 30)
+        r2 = T.restrict_to(ref, keep, 30)
+        for a, b in zip(r1.edges(), r2.edges()):
+            assert np.array_equal(a, b)
