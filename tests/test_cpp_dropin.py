@@ -514,3 +514,31 @@ def test_solver_ec_vc_problems_match_reference(cuda_device, problem):
             assert got[key] == want[key], (key, problem, i, times, order, got, want)
         found += got["witness"] is not None
     assert found >= 2
+
+
+@pytest.mark.gpu
+def test_solver_larger_instances_match_reference(cuda_device):
+    """Solver records on larger random graphs (hubs split across warp chunks,
+    several batches per evaluation, both extraction strategies, default
+    junction preprocessing) against the reference."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(2024)
+    for i in range(6):
+        n, m, t = 400, 6000, 25
+        u = rng.integers(0, n, m)
+        v = np.where(rng.random(m) < 0.2, 7, rng.integers(0, n, m))   # a hub head
+        ts = rng.integers(1, t + 1, m)
+        d = bool(i % 2)
+        colors = rng.integers(1, 4, n)
+        prob, motif, k = [("pathmotif", [1, 1, 2, 3, 1], 0), ("ktemppath", [], 6),
+                          ("colorfulpath", [1, 2, 3], 0)][i % 3]
+        c = {"n": n, "u": u.tolist(), "v": v.tolist(), "ts": ts.tolist(), "directed": d,
+             "colors": colors.tolist(), "problem": prob, "motif": motif, "k": k,
+             "source": -1, "dest": -1, "seed": 7 + i, "mode": 3, "extraction": i // 3,
+             "preprocess": 3}
+        want = O.ref_solve(n, u, v, ts, d, colors, prob, motif, k, seed=c["seed"], mode=3,
+                           extraction=c["extraction"], preprocess=3)
+        got = solve(c)
+        for key in ("decision", "certain", "optimum_ts", "checksum", "flagged", "witness",
+                    "extraction_failed", "oracle_calls", "preprocessed_n", "preprocessed_m"):
+            assert got[key] == want[key], (key, i, got, want)
