@@ -424,7 +424,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "u64 (GF(2^64) carry-less, integer pipes)", "data": "synthetic",
+                "dtype": "u64", "data": "synthetic",
                 "config": config_json(inst, world, args), "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(),
                 "decision": decisions, "checksums": checksums,
