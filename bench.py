@@ -166,7 +166,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64 (GF(2^64))",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic", "config": config_json(inst, world, args),
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": info[2],
                              "kind": info[1], "sample": info[0]},
