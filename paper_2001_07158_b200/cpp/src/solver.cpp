@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <deque>
 #include <functional>
 #include <map>
@@ -552,7 +554,11 @@ SolveReport solve_single(const TemporalGraph& g, const VertexColoring& col,
     Timestamp lo = 1, hi = full;
     while (lo < hi) {
       const Timestamp mid = lo + (hi - lo) / 2;
+      const auto tp = Clock::now();
       SieveOutcome o = probe(p, p.graph, mid).out;
+      if (std::getenv("TSIEVE_TRACE"))
+        std::fprintf(stderr, "probe max_ts=%d %s %.3f ms\n", mid,
+                     o.global_nonzero ? "YES" : "NO", 1e3 * since(tp));
       ++r.oracle_calls;
       r.peak_field_words = std::max(r.peak_field_words, o.peak_field_words);
       if (o.global_nonzero) {

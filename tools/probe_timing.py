@@ -1,0 +1,44 @@
+"""Wall time of single eval_temporal_sieve calls (one repetition, one horizon)
+on a BASELINE config, through the Python mirror of the C-ABI: what one
+binary-search probe of `tsieve extract` costs.
+`python tools/probe_timing.py --config 2`."""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_2001_07158_b200 as T  # noqa: E402
+from paper_2001_07158_b200 import synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cap", type=int, default=62, help="log2 memory_cap_words")
+    args = ap.parse_args()
+    inst = synth.make_config(args.config, scale=args.scale)
+    k, colors, motif, anchor = synth.effective_query(inst)
+    t0 = time.perf_counter()
+    g = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, 0)
+    t_build = time.perf_counter() - t0
+    col = T.VertexColoring(colors, int(colors.max()))
+    cfg = T.SieveConfig(seed=1, memory_cap_words=1 << args.cap)
+    sh = T.build_shades(T.MotifQuery.from_multiset(motif), col, cfg)
+    an = T.AnchorSpec(*anchor)
+    full = g.t()
+    rows = []
+    for max_ts in [full, full, full // 2, full // 4, full // 2 + full // 8, full, full // 3]:
+        t0 = time.perf_counter()
+        o = T.eval_temporal_sieve(g, k, max_ts, sh, cfg, an)
+        rows.append({"max_ts": max_ts, "s": round(time.perf_counter() - t0, 5),
+                     "yes": bool(o.global_nonzero)})
+    print(json.dumps({"config": args.config, "build_s": t_build, "probes": rows}))
+
+
+if __name__ == "__main__":
+    main()
