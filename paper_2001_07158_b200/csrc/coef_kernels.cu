@@ -1,0 +1,452 @@
+// coef_kernels.cu -- the temporal sieve in coefficient (top-degree) form.
+//
+// For a fixed graph and seed, S_l(A) of every run is a polynomial in the
+// bits a_1..a_k of the sieve point A: z_u(A) = XOR_j a_j z_{u,j} is linear,
+// y and XOR are constants and sums.  At 0/1 points it equals its multilinear
+// reduction, and over GF(2) the sum over all 2^k points of a multilinear
+// monomial a_T is 2^(k-|T|) copies of it: nonzero only for T = [k].  So the
+// reference's accumulator acc[u] = XOR_A P[u][k][max_ts](A)
+// (/root/reference/proj/core/src/sieve.cpp:294-306) is the coefficient of
+// a_1..a_k in the level-k polynomial, and only the degree-l part of level l
+// can reach it (S_l has degree <= l; each level raises the degree by at most
+// one).  The degree-l part of S_l[run] is indexed by the l-subsets T of [k]:
+//
+//   U_l[run][T'] = XOR_{arcs a of head up to run} y(e_a, l-1) * S_{l-1}[src_a][T']
+//   S_l[run][T]  = XOR_{j in T} z_{head,j} * U_l[run][T \ {j}]     (|T| = l)
+//
+// with S_1[v][{j}] = z_{v,j}.  Bit-identical accumulators for C(k, l-1)
+// products per arc at level l instead of 2^k (C2: 62 vs 320 per arc over
+// all levels).  The engine runs two kernels per level:
+//
+//   k_coef_arcs   one pass over the vertex-major arc stream (layout.hpp):
+//                 products y * S_{l-1}[src] for the C(k,l-1) entries of
+//                 each arc (a lane group per arc, entries across its lanes),
+//                 segmented prefix XOR per head, U stored at the ends of runs
+//                 some arc of the next level reads (state slots); level k
+//                 XORs each vertex piece's U into ulast[head].
+//   k_coef_ztrans S_l[slot][T] from U[slot] (l products per entry, one
+//                 thread per (slot, T)); k_coef_readout applies the same map
+//                 to ulast for level k and XORs into acc.
+//
+// Subsets of a level are numbered in colex order (= increasing bit mask):
+// entry e of level 1 is {e}, so S_1 rows are the z_{u,.} rows as stored.
+#include <cuda_runtime.h>
+
+#include "coef.hpp"
+#include "gf_device.cuh"
+#include "layout.hpp"
+
+namespace tsv {
+namespace {
+
+constexpr int kCoefWarps = 4;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kLive = 2u;  // staged: the arc's products can be nonzero
+constexpr uint32_t kPush = 4u;  // staged: store / flush this arc's prefix
+
+__device__ __forceinline__ bool has_color_c(const int32_t* __restrict__ colors, int32_t x,
+                                            int32_t c, int32_t wild) {
+  return c == wild || __ldg(colors + x) == c;
+}
+
+// One half-warp's GfTable window (16 lanes build a whole table).
+__device__ __forceinline__ void build_window16_c(uint64_t* tab, uint64_t y, int w) {
+  const uint32_t s = 4u * static_cast<uint32_t>(w);
+  uint64_t h, lo;
+  asm("shr.b64 %0, %1, %2;" : "=l"(h) : "l"(y), "r"(64u - s));
+  asm("shl.b64 %0, %1, %2;" : "=l"(lo) : "l"(y), "r"(s));
+  const uint64_t B0 = lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4);
+  const uint64_t B1 = gf_mulx(B0), B2 = gf_mulx(B1), B3 = gf_mulx(B2);
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(tab)) +
+                     GfTable::kWinBytes * static_cast<uint32_t>(w);
+  const uint64_t v3 = B1 ^ B0, v5 = B2 ^ B0, v6 = B2 ^ B1, v7 = v6 ^ B0;
+  GfTable::sts<0>(a, 0ull);
+  GfTable::sts<8>(a, B0);
+  GfTable::sts<16>(a, B1);
+  GfTable::sts<24>(a, v3);
+  GfTable::sts<32>(a, B2);
+  GfTable::sts<40>(a, v5);
+  GfTable::sts<48>(a, v6);
+  GfTable::sts<56>(a, v7);
+  GfTable::sts<64>(a, B3);
+  GfTable::sts<72>(a, B3 ^ B0);
+  GfTable::sts<80>(a, B3 ^ B1);
+  GfTable::sts<88>(a, B3 ^ v3);
+  GfTable::sts<96>(a, B3 ^ B2);
+  GfTable::sts<104>(a, B3 ^ v5);
+  GfTable::sts<112>(a, B3 ^ v6);
+  GfTable::sts<120>(a, B3 ^ v7);
+}
+
+// One level's arc pass over the entry slice [e0, e0 + ne) of the C(k, l-1)
+// input entries.  A warp owns a chunk; G = 32/LG arcs are in flight per step,
+// one per group of LG lanes, and lane li of a group holds entries
+// e0 + li + LG*p (p < PPT).  The y product: LG = 32 -> a warp table
+// (GfTable), LG = 16 -> a half-warp table per arc, LG <= 8 -> general
+// product with y split once per arc in shared memory.
+template <int LG, int PPT, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kCoefWarps * 32)
+    k_coef_arcs(const CoefParams P) {
+  constexpr int G = 32 / LG;
+  constexpr bool kWarpTab = LG == 32;
+  constexpr bool kHalfTab = LG == 16;
+  constexpr bool kGeneral = LG <= 8;
+  __shared__ uint32_t s_ys[kGeneral ? kCoefWarps : 1][12][32];
+  __shared__ uint64_t s_yraw[kCoefWarps][32];
+  __shared__ int32_t s_src[kCoefWarps][32];
+  __shared__ uint32_t s_meta[kCoefWarps][32];
+  __shared__ int32_t s_slot[kCoefWarps][32];
+  __shared__ int32_t s_head[kCoefWarps][32];
+  __shared__ __align__(256) uint64_t s_tab[kGeneral ? 1 : kCoefWarps][kHalfTab ? 2 : 1]
+                                          [GfTable::kWords];
+
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kCoefWarps + wib;
+  if (c >= P.g.C) return;  // warp-uniform
+  const int g = lane / LG, li = lane % LG;
+  bool ev[PPT];  // entry li + LG*p of the slice exists
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) ev[p] = li + LG * p < P.ne;
+  const int64_t E = P.E;
+
+  const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
+  const uint64_t yb = static_cast<uint64_t>(P.ell - 1) + 0x165667b19e3779f9ull;
+  const int64_t a0 = P.g.chunk_arc[c], a1 = P.g.chunk_arc[c + 1];
+  int32_t run_ctr = P.g.chunk_run[c];
+  const int last_lane = (G - 1) * LG + li;
+  uint64_t carry[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) carry[p] = 0;
+
+  for (int64_t base = a0; base < a1; base += 32) {
+    const int nb = static_cast<int>(a1 - base < 32 ? a1 - base : 32);
+    uint32_t meta = 0;
+    int32_t sidx = -1, head = -1;
+    uint64_t y = 0;
+    if (lane < nb) {
+      meta = __ldg(P.g.arc_meta + base + lane);
+      sidx = FIRST ? __ldg(P.g.arc_tail + base + lane) : __ldg(P.g.arc_src + base + lane);
+      y = draw_edge_y(pre, yb, meta & kEdgeMask);
+    }
+    const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
+    const int32_t myrun = run_ctr + __popc(ends & ((1u << lane) - 1u));
+    if (lane < nb) head = __ldg(P.g.run_head + myrun);
+    s_yraw[wib][lane] = y;
+    if (kGeneral) {
+      const KSplit ks = ksplit(y);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s_ys[kGeneral ? wib : 0][j][lane] = ks.l.c[j];
+        s_ys[kGeneral ? wib : 0][4 + j][lane] = ks.h.c[j];
+        s_ys[kGeneral ? wib : 0][8 + j][lane] = ks.m.c[j];
+      }
+    }
+    bool live = lane < nb && sidx >= 0;
+    if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
+    if (LAST) live = live && __ldg(P.g.run_ts + myrun) <= P.max_ts;
+    if (P.vc_color && live) {
+      const int32_t tl = FIRST ? sidx : __ldg(P.g.arc_tail + base + lane);
+      live = tl >= 0 && has_color_c(P.vc_color, tl, P.vc_tail, P.vc_wild) &&
+             has_color_c(P.vc_color, head, P.vc_head, P.vc_wild);
+    }
+    bool push;
+    int32_t slot = -1;
+    if (LAST) {  // last arc of its vertex within this chunk: flush the piece
+      const bool chunk_end = base + lane + 1 >= a1;
+      uint32_t nmeta = __shfl_down_sync(kFull, meta, 1);
+      if (lane == 31 && !chunk_end) nmeta = __ldg(P.g.arc_meta + base + 32);
+      push = lane < nb && (chunk_end || (nmeta & kVStart));
+    } else {
+      slot = (lane < nb && (meta & kRunEnd)) ? __ldg(P.g.run_slot + myrun) : -1;
+      push = slot >= 0;
+    }
+    s_src[wib][lane] = sidx;
+    s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | (live ? kLive : 0u) | (push ? kPush : 0u);
+    s_slot[wib][lane] = slot;
+    s_head[wib][lane] = head;
+    run_ctr += __popc(ends);
+    __syncwarp();
+
+    auto fetch = [&](int i, uint64_t (&out)[PPT]) {
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) out[p] = 0;
+      if (i < nb && (s_meta[wib][i] & kLive)) {
+        const int64_t src = s_src[wib][i];
+        const uint64_t* row = FIRST ? P.zj + src * P.k + P.e0 : P.s_prev + src * E + P.e0;
+#pragma unroll
+        for (int p = 0; p < PPT; ++p)
+          if (ev[p]) out[p] = __ldg(row + li + LG * p);
+      }
+    };
+    uint64_t nxt[PPT];
+    fetch(g, nxt);
+    const int steps = (nb + G - 1) / G;
+#pragma unroll 1
+    for (int s = 0; s < steps; ++s) {
+      uint64_t v[PPT];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) v[p] = nxt[p];
+      if (s + 1 < steps) fetch((s + 1) * G + g, nxt);
+      const int i = s * G + g;
+      const bool act = i < nb;
+      const uint32_t mt = act ? s_meta[wib][i] : 0u;
+      const bool lv = (mt & kLive) != 0;
+      if (__any_sync(kFull, lv)) {
+        const int ia = act ? i : 0;
+        if (kWarpTab) {
+          GfTable T{s_tab[kGeneral ? 0 : wib][0]};
+          __syncwarp();
+          T.build(s_yraw[wib][ia], lane);
+          __syncwarp();
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) v[p] = lv ? T.mul(v[p]) : 0ull;
+        } else if (kHalfTab) {
+          uint64_t* tab = s_tab[kGeneral ? 0 : wib][kHalfTab ? g : 0];
+          __syncwarp();
+          build_window16_c(tab, s_yraw[wib][ia], li);
+          __syncwarp();
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) v[p] = lv ? GfTable{tab}.mul(v[p]) : 0ull;
+        } else {
+          KSplit ys;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            ys.l.c[j] = s_ys[kGeneral ? wib : 0][j][ia];
+            ys.h.c[j] = s_ys[kGeneral ? wib : 0][4 + j][ia];
+            ys.m.c[j] = s_ys[kGeneral ? wib : 0][8 + j][ia];
+          }
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) v[p] = lv ? gf_mul_presplit(ys, v[p]) : 0ull;
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < PPT; ++p) v[p] = 0;
+      }
+      // segmented inclusive XOR-scan over the G groups (vertex starts cut it)
+      bool f = (mt & kVStart) != 0;
+      if (G > 1) {
+#pragma unroll
+        for (int d = 1; d < G; d <<= 1) {
+          const bool fo = __shfl_up_sync(kFull, f, d * LG);
+#pragma unroll
+          for (int p = 0; p < PPT; ++p) {
+            const uint64_t vo = __shfl_up_sync(kFull, v[p], d * LG);
+            if (g >= d && !f) v[p] ^= vo;
+          }
+          if (g >= d) f = f || fo;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        if (!f) v[p] ^= carry[p];
+        carry[p] = (G > 1) ? __shfl_sync(kFull, v[p], last_lane) : v[p];
+      }
+      if (mt & kPush) {
+        if (LAST) {
+          const int64_t row = static_cast<int64_t>(s_head[wib][i]) * E + P.e0;
+#pragma unroll
+          for (int p = 0; p < PPT; ++p)
+            if (ev[p] && v[p])
+              atomicXor(reinterpret_cast<unsigned long long*>(P.ulast + row + li + LG * p),
+                        static_cast<unsigned long long>(v[p]));
+        } else {
+          const int64_t row = static_cast<int64_t>(s_slot[wib][i]) * E + P.e0;
+#pragma unroll
+          for (int p = 0; p < PPT; ++p)
+            if (ev[p]) P.ubuf[row + li + LG * p] = v[p];
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (!LAST && g == 0) {
+#pragma unroll
+    for (int p = 0; p < PPT; ++p)
+      if (ev[p]) P.agg[c * E + P.e0 + li + LG * p] = carry[p];
+  }
+}
+
+// A chunk whose first arc continues vertex h (split across chunks) started
+// h's prefix from zero: its runs of h receive the XOR of the tail aggregates
+// of the preceding chunks back to the one where h starts (U space, before
+// the z map, so no product is needed).
+__global__ void k_coef_fixup(const CoefParams P) {
+  const int32_t c = P.g.carry_list[blockIdx.x];
+  const int32_t r0 = P.g.chunk_run[c];
+  if (r0 >= P.g.R) return;
+  const int32_t head = P.g.run_head[r0];
+  const int32_t r1 = min(P.g.chunk_run[c + 1], P.g.vtx_run_off[head + 1]);
+  if (r0 >= r1) return;
+  const int64_t E = P.E;
+  for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+    uint64_t carry = 0;
+    for (int64_t cc = c - 1;; --cc) {
+      carry ^= P.agg[cc * E + e];
+      if (!P.g.chunk_carry[cc] || P.g.run_head[P.g.chunk_run[cc]] != head) break;
+    }
+    if (!carry) continue;
+    for (int32_t r = r0; r < r1; ++r) {
+      const int32_t slot = P.g.run_slot[r];
+      if (slot >= 0) P.ubuf[static_cast<int64_t>(slot) * E + e] ^= carry;
+    }
+  }
+}
+
+// S_l[slot][o] = XOR_{c < l} z_{head, j_c} * U[slot][in_c], (in_c, j_c) =
+// pairs[o*l + c]: one thread per (slot, output entry).
+__global__ void k_coef_ztrans(int64_t S, int F, int l, const int32_t* __restrict__ slot_head,
+                              const uint64_t* __restrict__ zj, int k, int E,
+                              const uint64_t* __restrict__ ubuf, const int2* __restrict__ pairs,
+                              uint64_t* __restrict__ out) {
+  const int64_t total = S * F;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = idx / F;
+    const int o = static_cast<int>(idx - s * F);
+    const uint64_t* U = ubuf + s * E;
+    const uint64_t* z = zj + static_cast<int64_t>(__ldg(slot_head + s)) * k;
+    uint64_t r = 0;
+    for (int cc = 0; cc < l; ++cc) {
+      const int2 pr = __ldg(pairs + o * l + cc);
+      const uint64_t u = __ldg(U + pr.x);
+      if (u) r ^= gf_mul(__ldg(z + pr.y), u);
+    }
+    out[idx] = r;
+  }
+}
+
+// Level k: acc[h] ^= XOR_{c < k} z_{h, j_c} * ulast[h][in_c].
+__global__ void k_coef_readout(int32_t n, const uint64_t* __restrict__ zj, int k,
+                               const uint64_t* __restrict__ ulast,
+                               const int2* __restrict__ pairs, uint64_t* __restrict__ acc) {
+  const int64_t h = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (h >= n) return;
+  const uint64_t* U = ulast + h * k;
+  const uint64_t* z = zj + h * k;
+  uint64_t r = 0;
+  for (int cc = 0; cc < k; ++cc) {
+    const int2 pr = __ldg(pairs + cc);
+    const uint64_t u = __ldg(U + pr.x);
+    if (u) r ^= gf_mul(__ldg(z + pr.y), u);
+  }
+  if (r) acc[h] ^= r;
+}
+
+__global__ void k_slot_head(int64_t R, const int32_t* __restrict__ run_slot,
+                            const int32_t* __restrict__ run_head, int32_t* __restrict__ slot_head) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= R) return;
+  const int32_t s = run_slot[r];
+  if (s >= 0) slot_head[s] = run_head[r];
+}
+
+template <int LG, int PPT>
+void arcs_dispatch(const CoefParams& p, cudaStream_t st) {
+  const unsigned blocks = static_cast<unsigned>((p.g.C + kCoefWarps - 1) / kCoefWarps);
+  const bool first = p.ell == 2, last = p.last;
+  if (first && last)
+    k_coef_arcs<LG, PPT, true, true><<<blocks, kCoefWarps * 32, 0, st>>>(p);
+  else if (first)
+    k_coef_arcs<LG, PPT, true, false><<<blocks, kCoefWarps * 32, 0, st>>>(p);
+  else if (last)
+    k_coef_arcs<LG, PPT, false, true><<<blocks, kCoefWarps * 32, 0, st>>>(p);
+  else
+    k_coef_arcs<LG, PPT, false, false><<<blocks, kCoefWarps * 32, 0, st>>>(p);
+}
+
+}  // namespace
+
+CoefTables coef_tables(int k) {
+  CoefTables t;
+  t.k = k;
+  std::vector<std::vector<int64_t>> C(static_cast<size_t>(k) + 1,
+                                      std::vector<int64_t>(static_cast<size_t>(k) + 2, 0));
+  for (int a = 0; a <= k; ++a) {
+    C[a][0] = 1;
+    for (int b = 1; b <= a; ++b) C[a][b] = C[a - 1][b - 1] + (b <= a - 1 ? C[a - 1][b] : 0);
+  }
+  t.count.resize(static_cast<size_t>(k) + 1);
+  for (int l = 0; l <= k; ++l) t.count[l] = C[k][l];
+  // colex rank of a subset: sum over its i-th smallest element x of C(x, i+1)
+  auto rank = [&](uint64_t mask) {
+    int64_t r = 0;
+    int i = 0;
+    for (int x = 0; x < k; ++x)
+      if ((mask >> x) & 1ull) r += (x >= i + 1 ? C[x][i + 1] : 0), ++i;
+    return r;
+  };
+  t.pairs.resize(static_cast<size_t>(k) + 1);
+  for (int l = 2; l <= k; ++l) {
+    std::vector<int2>& v = t.pairs[l];
+    v.reserve(static_cast<size_t>(t.count[l] * l));
+    uint64_t T = (1ull << l) - 1;  // l-subsets in increasing mask order (Gosper)
+    const uint64_t end = 1ull << k;
+    while (T < end) {
+      for (int j = 0; j < k; ++j)
+        if ((T >> j) & 1ull)
+          v.push_back(make_int2(static_cast<int>(rank(T & ~(1ull << j))), j));
+      const uint64_t cbit = T & (~T + 1), rr = T + cbit;
+      T = (((rr ^ T) >> 2) / cbit) | rr;
+    }
+  }
+  return t;
+}
+
+int coef_group_lanes(int ne) { return ne <= 4 ? 4 : ne <= 8 ? 8 : ne <= 16 ? 16 : 32; }
+
+void launch_coef_arcs(const CoefParams& p, cudaStream_t st) {
+  if (p.g.C == 0 || p.ne <= 0) return;
+  prof_begin(p.last ? "coef_arcs_last" : p.ell == 2 ? "coef_arcs_first" : "coef_arcs", st);
+  const int lg = coef_group_lanes(p.ne);
+  if (lg == 4) {
+    arcs_dispatch<4, 1>(p, st);
+  } else if (lg == 8) {
+    arcs_dispatch<8, 1>(p, st);
+  } else if (lg == 16) {
+    arcs_dispatch<16, 1>(p, st);
+  } else if (p.ne <= 32) {
+    arcs_dispatch<32, 1>(p, st);
+  } else if (p.ne <= 64) {
+    arcs_dispatch<32, 2>(p, st);
+  } else {
+    arcs_dispatch<32, 4>(p, st);
+  }
+  prof_end(st);
+}
+
+void launch_coef_fixup(const CoefParams& p, cudaStream_t st) {
+  if (p.g.ncarry == 0) return;
+  prof_begin("coef_fixup", st);
+  k_coef_fixup<<<p.g.ncarry, 128, 0, st>>>(p);
+  prof_end(st);
+}
+
+void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const uint64_t* zj,
+                        int k, int E, const uint64_t* ubuf, const int2* pairs, uint64_t* out,
+                        int sm_count, cudaStream_t st) {
+  if (S == 0) return;
+  prof_begin("coef_ztrans", st);
+  const int64_t total = S * F;
+  const int64_t want = (total + 255) / 256;
+  const int64_t cap = static_cast<int64_t>(sm_count) * 64;
+  k_coef_ztrans<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, st>>>(
+      S, F, l, slot_head, zj, k, E, ubuf, pairs, out);
+  prof_end(st);
+}
+
+void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* ulast,
+                         const int2* pairs, uint64_t* acc, cudaStream_t st) {
+  if (n == 0) return;
+  prof_begin("coef_readout", st);
+  k_coef_readout<<<(n + 255) / 256, 256, 0, st>>>(n, zj, k, ulast, pairs, acc);
+  prof_end(st);
+}
+
+void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_head,
+                      int32_t* slot_head, cudaStream_t st) {
+  if (R == 0) return;
+  k_slot_head<<<static_cast<unsigned>((R + 255) / 256), 256, 0, st>>>(R, run_slot, run_head,
+                                                                       slot_head);
+}
+
+}  // namespace tsv

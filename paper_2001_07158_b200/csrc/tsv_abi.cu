@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/tsv.h"
+#include "coef.hpp"
 #include "engine.hpp"
 #include "gf_device.cuh"
 #include "layout.hpp"
@@ -238,6 +239,23 @@ tsv::Batch batch_shape(int W) {
   return b;
 }
 
+// Device words an evaluation may allocate: 92% of free memory plus freed
+// (reusable) pool memory.
+uint64_t device_budget_words() {
+  size_t free_b = 0, total_b = 0;
+  TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  int dev = 0;
+  cudaMemPool_t pool = nullptr;
+  if (cudaGetDevice(&dev) == cudaSuccess &&
+      cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t reserved = 0, used = 0;  // freed pool memory is reusable
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    if (reserved > used) free_b += reserved - used;
+  }
+  return static_cast<uint64_t>(free_b * 0.92) / 8;
+}
+
 // Points per batch: the largest power of two <= min(range, 128) whose
 // working set fits the word cap and free device memory.
 // *zb_ok: the per-batch z table (n*W words) also fits next to that working set.
@@ -254,23 +272,9 @@ int choose_width(const tsv_graph* g, int k, uint64_t range, const tsv_config* cf
   };
   int W = cfg->points_per_batch ? cfg->points_per_batch : 128;
   while (static_cast<uint64_t>(W) > range && W > 1) W >>= 1;
-  uint64_t budget = UINT64_MAX;
-  {
-    size_t free_b = 0, total_b = 0;
-    TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
-    int dev = 0;
-    cudaMemPool_t pool = nullptr;
-    if (cudaGetDevice(&dev) == cudaSuccess &&
-        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t reserved = 0, used = 0;  // freed pool memory is reusable
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-      if (reserved > used) free_b += reserved - used;
-    }
-    budget = static_cast<uint64_t>(free_b * 0.92) / 8;
-    if (cfg->points_per_batch == 0)
-      while (W > 1 && (words(W) > cfg->memory_cap_words || words(W) > budget)) W >>= 1;
-  }
+  const uint64_t budget = device_budget_words();
+  if (cfg->points_per_batch == 0)
+    while (W > 1 && (words(W) > cfg->memory_cap_words || words(W) > budget)) W >>= 1;
   // z table only when small next to the state (n <= R/8) and it fits
   const uint64_t zw = n * static_cast<uint64_t>(W);
   *zb_ok = k >= 2 && n * 8 <= R && words(W) + zw <= budget &&
@@ -296,6 +300,92 @@ struct VcSpec {
   int32_t wild = -1;                  // wildcard color, -1 = none
 };
 
+// The coefficient (top-degree) engine, coef_kernels.cu: the XOR over ALL
+// 2^k sieve points in one pass per level, bit-identical to the point engine.
+// Used for full-range evaluations when its working set (two S x M state
+// buffers, M = max_l C(k, l)) fits; TSV_ENGINE=points disables it.
+// Returns false (nothing launched) when not applicable.
+bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
+               const tsv_config* cfg, int32_t anchor_source, uint64_t* d_acc, cudaStream_t st,
+               uint64_t* peak_out, const VcSpec* vc) {
+  const char* eng = std::getenv("TSV_ENGINE");
+  if (eng && std::strcmp(eng, "points") == 0) return false;
+  if (k < 2 || k > 16) return false;
+  const tsv::CoefTables T = tsv::coef_tables(k);
+  int64_t M = 1;
+  for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, T.count[l]);
+  const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
+  const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
+  const uint64_t n = static_cast<uint64_t>(g->dev.n);
+  const uint64_t words = 2 * S * M + C * M + 2 * n * k + n + S / 2 + 1;
+  if (words > cfg->memory_cap_words || words > device_budget_words()) return false;
+  if (peak_out) *peak_out = words;
+  const int32_t nn = g->dev.n;
+  int dev = 0, sms = 148;
+  TSV_CUDA(cudaGetDevice(&dev));
+  TSV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+
+  DevBuf d_w(static_cast<size_t>(k) * k * 8, st), d_zj(static_cast<size_t>(n) * k * 8, st);
+  tsv::launch_wtab(k, cfg->seed, d_w.as<uint64_t>(), st);
+  if (vc)
+    tsv::launch_zj_positional(nn, k, cfg->seed, d_zj.as<uint64_t>(), st);
+  else
+    tsv::launch_zj(nn, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
+                   d_zj.as<uint64_t>(), st);
+  DevBuf X(S * M * 8, st), Y(S * M * 8, st), agg(C * M * 8, st);
+  DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(S * 4, st);
+  TSV_CUDA(cudaMemsetAsync(ulast.p, 0, std::max<uint64_t>(n, 1) * k * 8, st));
+  std::vector<int2> pairs;
+  std::vector<size_t> poff(static_cast<size_t>(k) + 1, 0);
+  for (int l = 2; l <= k; ++l) {
+    poff[l] = pairs.size();
+    pairs.insert(pairs.end(), T.pairs[l].begin(), T.pairs[l].end());
+  }
+  DevBuf d_pairs(pairs.size() * sizeof(int2), st);
+  TSV_CUDA(cudaMemcpyAsync(d_pairs.p, pairs.data(), pairs.size() * sizeof(int2),
+                           cudaMemcpyHostToDevice, st));
+  tsv::launch_slot_head(g->dev.R, g->dev.run_slot, g->dev.run_head, slot_head.as<int32_t>(), st);
+  const int2* dp = d_pairs.as<int2>();
+  for (int l = 2; l <= k; ++l) {
+    tsv::CoefParams cp;
+    cp.g = g->dev;
+    cp.zj = d_zj.as<uint64_t>();
+    cp.k = k;
+    cp.ell = l;
+    cp.last = l == k;
+    cp.seed = cfg->seed;
+    cp.anchor_source = anchor_source;
+    cp.E = static_cast<int>(T.count[l - 1]);
+    cp.s_prev = X.as<uint64_t>();
+    cp.ubuf = Y.as<uint64_t>();
+    cp.agg = agg.as<uint64_t>();
+    cp.ulast = ulast.as<uint64_t>();
+    cp.max_ts = max_ts;
+    if (vc) {
+      cp.vc_color = vc->d_colors;
+      cp.vc_head = vc->order[l - 1];
+      cp.vc_tail = vc->order[l - 2];
+      cp.vc_wild = vc->wild;
+    }
+    for (int e0 = 0; e0 < cp.E; e0 += tsv::kCoefSlice) {
+      cp.e0 = e0;
+      cp.ne = std::min(tsv::kCoefSlice, cp.E - e0);
+      tsv::launch_coef_arcs(cp, st);
+    }
+    if (cp.last) {
+      tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k],
+                               d_acc, st);
+    } else {
+      tsv::launch_coef_fixup(cp, st);
+      tsv::launch_coef_ztrans(g->dev.S, static_cast<int>(T.count[l]), l,
+                              slot_head.as<int32_t>(), d_zj.as<uint64_t>(), k, cp.E,
+                              Y.as<uint64_t>(), dp + poff[l], X.as<uint64_t>(), sms, st);
+    }
+    TSV_CUDA(cudaGetLastError());
+  }
+  return true;
+}
+
 void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                  const tsv_config* cfg, int32_t anchor_source, uint64_t p_begin,
                  uint64_t p_end, uint64_t* d_acc, cudaStream_t st,
@@ -314,6 +404,9 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   const uint64_t P = 1ull << k;
   p_end = std::min(p_end, P);
   if (p_begin >= p_end) return;
+  if (p_begin == 0 && p_end == P &&
+      eval_coef(g, sh, k, max_ts, cfg, anchor_source, d_acc, st, peak_out, vc))
+    return;
   uint64_t peak = 0;
   bool zb_ok = false;
   int nlanes = 1;

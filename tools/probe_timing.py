@@ -37,7 +37,25 @@ def main():
         o = T.eval_temporal_sieve(g, k, max_ts, sh, cfg, an)
         rows.append({"max_ts": max_ts, "s": round(time.perf_counter() - t0, 5),
                      "yes": bool(o.global_nonzero)})
-    print(json.dumps({"config": args.config, "build_s": t_build, "probes": rows}))
+    # per-kernel CUDA-event times of 3 full evaluations
+    from paper_2001_07158_b200 import _native
+    _native.Profile.reset()
+    _native.Profile.enable(True)
+    for _ in range(3):
+        T.eval_temporal_sieve(g, k, full, sh, cfg, an)
+    names = ["coef_arcs_first", "coef_arcs", "coef_arcs_last", "coef_ztrans", "coef_fixup",
+             "coef_readout", "level_first", "level", "level_last", "level_grouped_first",
+             "level_grouped", "zbatch", "zj", "fixup"]
+    kern = {}
+    for nm in names:
+        cnt, ms = _native.Profile.get(nm)
+        if cnt:
+            kern[nm] = {"launches": cnt // 3, "ms_per_eval": round(ms / 3, 4)}
+    cnt, ms = _native.Profile.get(None)
+    kern["all"] = {"launches": cnt // 3, "ms_per_eval": round(ms / 3, 4)}
+    _native.Profile.enable(False)
+    print(json.dumps({"config": args.config, "scale": args.scale, "build_s": t_build,
+                      "probes": rows, "kernels": kern}))
 
 
 if __name__ == "__main__":
