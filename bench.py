@@ -192,6 +192,58 @@ def config_json(inst, world, args):
 # ---------------------------------------------------------------- our arm
 
 
+
+def coef_roofline(coef, k, info, evals, hbm, peak_kind, args, world, sm_mhz):
+    """Roofline of the coefficient engine's dominant kernel.
+
+    Algorithmic bytes, per evaluation:
+      k_coef_arcs, middle levels 3 <= l < k: 16 B per (arc, input entry) --
+        one 8-B read of S_{l-1}[src][T'] and one 8-B U write, the point
+        engine's SURVEY 8(d) figure with sieve points replaced by the
+        C(k, l-1) coefficient entries an arc carries;
+      k_coef_ztrans, levels 2 <= l < k: 8 B per (state slot, input entry)
+        read + 8 B per (state slot, output entry) written.
+    achieved = those bytes / the kernel's CUDA-event time in the bench's
+    profile pass; int_pipe from the committed ncu capture of the same kernel."""
+    from math import comb
+    A, S = info.arcs, info.runs_referenced
+    alg = {"coef_arcs": evals * sum(16 * A * comb(k, l - 1) for l in range(3, k)),
+           "coef_ztrans": evals * sum(8 * S * (comb(k, l - 1) + comb(k, l))
+                                      for l in range(2, k))}
+    name = max(coef, key=lambda nm: coef[nm][1])
+    n_launch, tot_ms = coef[name]
+    if not n_launch or not alg[name]:
+        return None
+    achieved = alg[name] / (tot_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+            "kernel": {"coef_arcs": "k_coef_arcs (3 <= l < k)",
+                       "coef_ztrans": "k_coef_ztrans_tab (2 <= l < k)"}[name],
+            "engine": "coefficient (top-degree) form, DESIGN.md 6b",
+            "avg_launch_ms": tot_ms / n_launch,
+            "alg_bytes_per_launch": alg[name] / n_launch,
+            "kernel_ms_per_eval": {nm: coef[nm][1] / max(evals, 1) for nm in coef}}
+    try:
+        with open(os.path.join(ROOT, "profiles", f"coef_kernels_c{args.config}.json")) as f:
+            prof = json.load(f)
+        if prof["config"] != args.config or args.scale != 1.0 or world != 1:
+            prof = None
+        else:
+            prof = prof["kernels"][name]
+    except Exception:
+        prof = None
+    if prof is not None:
+        roof["traffic"] = prof["traffic_bytes_per_launch"]
+        clk = sm_mhz or prof["sm_clock_ghz"] * 1e3
+        peak_issue = 148 * 4 * clk * 1e6
+        ach = prof["warp_inst_per_launch"] / (roof["avg_launch_ms"] * 1e-3)
+        roof["int_pipe"] = {"bound": "issue", "unit": "warp-inst/s", "achieved": ach,
+                            "peak": peak_issue, "frac": ach / peak_issue,
+                            "alu_pipe_frac_ncu": prof["alu_pipe_pct_active"] / 100,
+                            "capture": prof["capture"]}
+    return roof
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -301,6 +353,7 @@ def main():
     if not lvl_n:  # W < 32: the grouped kernel
         lvl_n, lvl_ms = _native.Profile.get("level_grouped")
         grouped = bool(lvl_n)
+    coef = {nm: _native.Profile.get(nm) for nm in ("coef_arcs", "coef_ztrans")}
     all_n, all_ms = _native.Profile.get(None)
     _native.Profile.enable(False)
     if world > 1:
@@ -319,10 +372,15 @@ def main():
         decisions.append(bool(nflag))
         checksums.append(f"{cs:016x}")
 
-    # roofline of the dominant kernel (level, l >= 3): 16 B per (arc, point)
+    # roofline of the dominant kernel
     hbm, peak_kind = peaks()
     roof = None
-    if lvl_n:
+    # full-range evaluations in the profile pass (the coefficient engine's)
+    evals = sum(1 for _, a, b in work if a == 0 and b == P) * prof_steps
+    if any(c for c, _ in coef.values()):
+        roof = coef_roofline(coef, k, g.info, evals, hbm, peak_kind, args, world,
+                             clk.summary().get("sm_mhz"))
+    elif lvl_n:
         # updates executed by the middle-level launches (3 <= l < k when level
         # k is fused with the readout, else 3 <= l <= k) of this rank in the
         # timed region
@@ -433,7 +491,10 @@ def main():
                           "runs_referenced": g.info.runs_referenced,
                           "split_chunks": g.info.split_chunks,
                           "device_bytes": g.info.device_bytes},
+                "engine": "coefficient" if any(c for c, _ in coef.values()) else "points",
                 "kernel_ms_per_step": {"level": lvl_ms / prof_steps,
+                                       "coef_arcs": coef["coef_arcs"][1] / prof_steps,
+                                       "coef_ztrans": coef["coef_ztrans"][1] / prof_steps,
                                        "all": all_ms / prof_steps,
                                        "source": f"{prof_steps}-step single-stream profile pass"}}
         print(json.dumps(line), flush=True)

@@ -26,6 +26,8 @@ struct CoefParams {
   uint64_t* agg = nullptr;           // C x E: chunk tail prefixes
   uint64_t* ulast = nullptr;         // n x k: level-k vertex sums (zeroed)
   int32_t max_ts = 0;
+  const uint8_t* vflag = nullptr;  // n: vertex has a nonzero S_1 row (nullptr: no skipping)
+  const uint8_t* sflag = nullptr;  // S: S_{ell-1}[slot] row is nonzero (ell > 2)
   const int32_t* vc_color = nullptr;  // vertex-ordered sieve filter (as LevelParams)
   int32_t vc_head = 0, vc_tail = 0, vc_wild = -1;
 };
@@ -38,10 +40,13 @@ constexpr int kCoefSlice = 128;
 void launch_coef_arcs(const CoefParams& p, cudaStream_t st);
 void launch_coef_fixup(const CoefParams& p, cudaStream_t st);
 void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const uint64_t* zj,
-                        int k, int E, const uint64_t* ubuf, const int2* pairs, uint64_t* out,
-                        int sm_count, cudaStream_t st);
+                        int k, int E, const uint64_t* ubuf, const int2* pairs,
+                        const int2* jpairs, uint64_t* out, uint8_t* sflag, int sm_count,
+                        cudaStream_t st);
+// vflag[u] = row u of the n x k table is nonzero
+void launch_row_nonzero(int32_t n, int k, const uint64_t* rows, uint8_t* vflag, cudaStream_t st);
 void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* ulast,
-                         const int2* pairs, uint64_t* acc, cudaStream_t st);
+                         const int2* pairs, uint64_t scale, uint64_t* acc, cudaStream_t st);
 void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_head,
                       int32_t* slot_head, cudaStream_t st);
 
@@ -52,6 +57,9 @@ struct CoefTables {
   // pairs of level l (2..k): for output o (an l-subset T) and c < l,
   // (rank of T minus its c-th element among the (l-1)-subsets, that element)
   std::vector<std::vector<int2>> pairs;
+  // jpairs of level l: for each j < k, the C(k-1, l-1) pairs (rank of an
+  // (l-1)-subset T' without j, rank of T' + {j}) in increasing T' order
+  std::vector<std::vector<int2>> jpairs;
 };
 CoefTables coef_tables(int k);
 

@@ -32,6 +32,10 @@
 // entry e of level 1 is {e}, so S_1 rows are the z_{u,.} rows as stored.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 #include "coef.hpp"
 #include "gf_device.cuh"
 #include "layout.hpp"
@@ -97,6 +101,7 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
   __shared__ uint32_t s_meta[kCoefWarps][32];
   __shared__ int32_t s_slot[kCoefWarps][32];
   __shared__ int32_t s_head[kCoefWarps][32];
+  __shared__ int8_t s_idx[kCoefWarps][32];
   __shared__ __align__(256) uint64_t s_tab[kGeneral ? 1 : kCoefWarps][kHalfTab ? 2 : 1]
                                           [GfTable::kWords];
 
@@ -149,15 +154,20 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
       live = tl >= 0 && has_color_c(P.vc_color, tl, P.vc_tail, P.vc_wild) &&
              has_color_c(P.vc_color, head, P.vc_head, P.vc_wild);
     }
+    // zero states: a head without shades has S = 0 (its products and stores
+    // are never read), and a source whose state row is all zero adds nothing
+    const bool hz = lane < nb && P.vflag && !__ldg(P.vflag + head);
+    if (live && P.vflag)
+      live = !hz && (FIRST ? __ldg(P.vflag + sidx) : __ldg(P.sflag + sidx)) != 0;
     bool push;
     int32_t slot = -1;
     if (LAST) {  // last arc of its vertex within this chunk: flush the piece
       const bool chunk_end = base + lane + 1 >= a1;
       uint32_t nmeta = __shfl_down_sync(kFull, meta, 1);
       if (lane == 31 && !chunk_end) nmeta = __ldg(P.g.arc_meta + base + 32);
-      push = lane < nb && (chunk_end || (nmeta & kVStart));
+      push = lane < nb && !hz && (chunk_end || (nmeta & kVStart));
     } else {
-      slot = (lane < nb && (meta & kRunEnd)) ? __ldg(P.g.run_slot + myrun) : -1;
+      slot = (lane < nb && !hz && (meta & kRunEnd)) ? __ldg(P.g.run_slot + myrun) : -1;
       push = slot >= 0;
     }
     s_src[wib][lane] = sidx;
@@ -165,12 +175,17 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
     s_slot[wib][lane] = slot;
     s_head[wib][lane] = head;
     run_ctr += __popc(ends);
+    // only arcs with a product, a store or a prefix reset are stepped through
+    const unsigned actm = __ballot_sync(kFull, lane < nb && (live || push || (meta & kVStart)));
+    const int nact = __popc(actm);
+    if ((actm >> lane) & 1u) s_idx[wib][__popc(actm & ((1u << lane) - 1u))] = lane;
     __syncwarp();
 
-    auto fetch = [&](int i, uint64_t (&out)[PPT]) {
+    auto fetch = [&](int q, uint64_t (&out)[PPT]) {
 #pragma unroll
       for (int p = 0; p < PPT; ++p) out[p] = 0;
-      if (i < nb && (s_meta[wib][i] & kLive)) {
+      const int i = q < nact ? s_idx[wib][q] : 0;
+      if (q < nact && (s_meta[wib][i] & kLive)) {
         const int64_t src = s_src[wib][i];
         const uint64_t* row = FIRST ? P.zj + src * P.k + P.e0 : P.s_prev + src * E + P.e0;
 #pragma unroll
@@ -180,15 +195,15 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
     };
     uint64_t nxt[PPT];
     fetch(g, nxt);
-    const int steps = (nb + G - 1) / G;
+    const int steps = (nact + G - 1) / G;
 #pragma unroll 1
     for (int s = 0; s < steps; ++s) {
       uint64_t v[PPT];
 #pragma unroll
       for (int p = 0; p < PPT; ++p) v[p] = nxt[p];
       if (s + 1 < steps) fetch((s + 1) * G + g, nxt);
-      const int i = s * G + g;
-      const bool act = i < nb;
+      const bool act = s * G + g < nact;
+      const int i = act ? s_idx[wib][s * G + g] : 0;
       const uint32_t mt = act ? s_meta[wib][i] : 0u;
       const bool lv = (mt & kLive) != 0;
       if (__any_sync(kFull, lv)) {
@@ -297,7 +312,7 @@ __global__ void k_coef_fixup(const CoefParams P) {
 __global__ void k_coef_ztrans(int64_t S, int F, int l, const int32_t* __restrict__ slot_head,
                               const uint64_t* __restrict__ zj, int k, int E,
                               const uint64_t* __restrict__ ubuf, const int2* __restrict__ pairs,
-                              uint64_t* __restrict__ out) {
+                              uint64_t* __restrict__ out, uint8_t* __restrict__ sflag) {
   const int64_t total = S * F;
   for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -312,13 +327,97 @@ __global__ void k_coef_ztrans(int64_t S, int F, int l, const int32_t* __restrict
       if (u) r ^= gf_mul(__ldg(z + pr.y), u);
     }
     out[idx] = r;
+    if (r) sflag[s] = 1;
   }
 }
 
-// Level k: acc[h] ^= XOR_{c < k} z_{h, j_c} * ulast[h][in_c].
+// The same map with shared-memory multiple tables of the multipliers.  Each
+// z_{h,j} multiplies C(k-1, l-1) entries of every slot of head h, so a warp
+// takes a window of 32 consecutive slots (slot_head is nondecreasing: slots
+// are ranks in vertex-major run order) and, per head segment of the window
+// and per j, builds the table of z_{h,j} (GfTable, all 32 lanes) and spreads
+// the (slot, T' without j) items of the segment over its lanes, XORing
+// z_{h,j} * U[T'] into output T' + {j} of a shared-memory accumulator.  The
+// multiplier is warp-uniform, so every lookup of a warp hits one 128-byte
+// table window (conflict-free); within one j the outputs are distinct, so
+// the accumulator needs no atomics.  ~45 instructions per product instead of
+// ~170 for the general product.  Segments with more than kZAcc / F slots are
+// processed in sub-batches.
+constexpr int kZWarps = 4;
+constexpr int kZAcc = 1024;  // accumulator words per warp
+constexpr int kZWarpWords = GfTable::kWords + kZAcc;
+__global__ void __launch_bounds__(kZWarps * 32)
+    k_coef_ztrans_tab(int64_t S, int F, int K1, const int32_t* __restrict__ slot_head,
+                      const uint64_t* __restrict__ zj, int k, int E,
+                      const uint64_t* __restrict__ ubuf, const int2* __restrict__ jpairs,
+                      uint64_t* __restrict__ out, uint8_t* __restrict__ sflag) {
+  __shared__ __align__(256) uint64_t sm[kZWarps][kZWarpWords];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint64_t* const tab = sm[wib];
+  uint64_t* const acc = sm[wib] + GfTable::kWords;
+  GfTable T{tab};
+  const int qmax = kZAcc / F < 32 ? kZAcc / F : 32;  // slots per sub-batch (F <= kZAcc)
+  const float invK1 = 1.0f / static_cast<float>(K1);
+  const int64_t nwin = (S + 31) / 32;
+  for (int64_t w = static_cast<int64_t>(blockIdx.x) * kZWarps + wib; w < nwin;
+       w += static_cast<int64_t>(gridDim.x) * kZWarps) {
+    const int64_t w0 = w * 32;
+    const int nsl = static_cast<int>(S - w0 < 32 ? S - w0 : 32);
+    const int32_t myh = lane < nsl ? __ldg(slot_head + w0 + lane) : -1;
+    const int32_t prevh = __shfl_up_sync(kFull, myh, 1);
+    unsigned starts = __ballot_sync(kFull, lane < nsl && (lane == 0 || myh != prevh));
+    while (starts) {
+      const int a = __ffs(starts) - 1;
+      starts &= starts - 1;
+      const int b = starts ? __ffs(starts) - 1 : nsl;
+      const int32_t h = __shfl_sync(kFull, myh, a);
+      const uint64_t zl = lane < k ? __ldg(zj + static_cast<int64_t>(h) * k + lane) : 0ull;
+      for (int q0 = a; q0 < b; q0 += qmax) {
+        const int qb = b - q0 < qmax ? b - q0 : qmax;
+        const int64_t s0 = w0 + q0;
+        const uint64_t* U0 = ubuf + s0 * E;
+        __syncwarp();
+        for (int i = lane; i < qb * F; i += 32) acc[i] = 0;
+        const int items = qb * K1;
+        for (int j = 0; j < k; ++j) {
+          const uint64_t zv = __shfl_sync(kFull, zl, j);
+          if (zv == 0) continue;  // warp-uniform: shade j not in S(h)
+          __syncwarp();
+          T.build(zv, lane);
+          __syncwarp();
+          const int2* jp = jpairs + j * K1;
+          for (int it = lane; it < items; it += 32) {
+            int qq = __float2int_rz(static_cast<float>(it) * invK1);
+            if ((qq + 1) * K1 <= it) ++qq;
+            if (qq * K1 > it) --qq;
+            const int2 p = __ldg(jp + (it - qq * K1));
+            const uint64_t u = __ldg(U0 + static_cast<int64_t>(qq) * E + p.x);
+            if (u) acc[qq * F + p.y] ^= T.mul(u);
+          }
+        }
+        __syncwarp();
+        const float invF = 1.0f / static_cast<float>(F);
+        for (int i = lane; i < qb * F; i += 32) {
+          const uint64_t r = acc[i];
+          out[s0 * F + i] = r;
+          if (r) {  // sflag was cleared before the launch
+            int qq = __float2int_rz(static_cast<float>(i) * invF);
+            if ((qq + 1) * F <= i) ++qq;
+            if (qq * F > i) --qq;
+            sflag[s0 + qq] = 1;
+          }
+        }
+      }
+    }
+  }
+}
+
+// Level k: acc[h] ^= scale * XOR_{c < k} z_{h, j_c} * ulast[h][in_c]
+// (scale = det(W) in the shade basis, 1 for positional z).
 __global__ void k_coef_readout(int32_t n, const uint64_t* __restrict__ zj, int k,
                                const uint64_t* __restrict__ ulast,
-                               const int2* __restrict__ pairs, uint64_t* __restrict__ acc) {
+                               const int2* __restrict__ pairs, uint64_t scale,
+                               uint64_t* __restrict__ acc) {
   const int64_t h = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (h >= n) return;
   const uint64_t* U = ulast + h * k;
@@ -329,7 +428,17 @@ __global__ void k_coef_readout(int32_t n, const uint64_t* __restrict__ zj, int k
     const uint64_t u = __ldg(U + pr.x);
     if (u) r ^= gf_mul(__ldg(z + pr.y), u);
   }
+  if (r && scale != 1) r = gf_mul(scale, r);
   if (r) acc[h] ^= r;
+}
+
+__global__ void k_row_nonzero(int32_t n, int k, const uint64_t* __restrict__ rows,
+                              uint8_t* __restrict__ vflag) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  uint64_t a = 0;
+  for (int j = 0; j < k; ++j) a |= __ldg(rows + u * k + j);
+  vflag[u] = a != 0;
 }
 
 __global__ void k_slot_head(int64_t R, const int32_t* __restrict__ run_slot,
@@ -389,6 +498,18 @@ CoefTables coef_tables(int k) {
       T = (((rr ^ T) >> 2) / cbit) | rr;
     }
   }
+  t.jpairs.resize(static_cast<size_t>(k) + 1);
+  for (int l = 2; l <= k; ++l) {
+    std::vector<std::vector<int2>> per(static_cast<size_t>(k));
+    const std::vector<int2>& v = t.pairs[l];
+    for (size_t i = 0; i < v.size(); ++i)  // output o = i / l, pair (in, j)
+      per[v[i].y].push_back(make_int2(v[i].x, static_cast<int>(i / l)));
+    for (int j = 0; j < k; ++j) {
+      std::sort(per[j].begin(), per[j].end(),
+                [](const int2& x, const int2& y) { return x.x < y.x; });
+      t.jpairs[l].insert(t.jpairs[l].end(), per[j].begin(), per[j].end());
+    }
+  }
   return t;
 }
 
@@ -422,24 +543,49 @@ void launch_coef_fixup(const CoefParams& p, cudaStream_t st) {
 }
 
 void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const uint64_t* zj,
-                        int k, int E, const uint64_t* ubuf, const int2* pairs, uint64_t* out,
-                        int sm_count, cudaStream_t st) {
+                        int k, int E, const uint64_t* ubuf, const int2* pairs,
+                        const int2* jpairs, uint64_t* out, uint8_t* sflag, int sm_count,
+                        cudaStream_t st) {
   if (S == 0) return;
   prof_begin("coef_ztrans", st);
-  const int64_t total = S * F;
-  const int64_t want = (total + 255) / 256;
-  const int64_t cap = static_cast<int64_t>(sm_count) * 64;
-  k_coef_ztrans<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, st>>>(
-      S, F, l, slot_head, zj, k, E, ubuf, pairs, out);
+  cudaMemsetAsync(sflag, 0, static_cast<size_t>(S), st);
+  static const bool general = [] {
+    const char* e = std::getenv("TSV_ZTRANS");
+    return e && std::strcmp(e, "general") == 0;
+  }();
+  if (!general && F <= kZAcc) {
+    static int per_sm = 0;
+    if (!per_sm &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coef_ztrans_tab, kZWarps * 32,
+                                                      0) != cudaSuccess)
+      per_sm = 1;
+    const int K1 = static_cast<int>(static_cast<int64_t>(F) * l / k);  // C(k-1, l-1)
+    const int64_t nwin = (S + 31) / 32;
+    const int64_t want = (nwin + kZWarps - 1) / kZWarps;
+    const int64_t cap = static_cast<int64_t>(sm_count) * (per_sm > 0 ? per_sm : 1);
+    k_coef_ztrans_tab<<<static_cast<unsigned>(want < cap ? want : cap), kZWarps * 32, 0, st>>>(
+        S, F, K1, slot_head, zj, k, E, ubuf, jpairs, out, sflag);
+  } else {
+    const int64_t total = S * F;
+    const int64_t want = (total + 255) / 256;
+    const int64_t cap = static_cast<int64_t>(sm_count) * 64;
+    k_coef_ztrans<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, st>>>(
+        S, F, l, slot_head, zj, k, E, ubuf, pairs, out, sflag);
+  }
   prof_end(st);
 }
 
 void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* ulast,
-                         const int2* pairs, uint64_t* acc, cudaStream_t st) {
+                         const int2* pairs, uint64_t scale, uint64_t* acc, cudaStream_t st) {
   if (n == 0) return;
   prof_begin("coef_readout", st);
-  k_coef_readout<<<(n + 255) / 256, 256, 0, st>>>(n, zj, k, ulast, pairs, acc);
+  k_coef_readout<<<(n + 255) / 256, 256, 0, st>>>(n, zj, k, ulast, pairs, scale, acc);
   prof_end(st);
+}
+
+void launch_row_nonzero(int32_t n, int k, const uint64_t* rows, uint8_t* vflag, cudaStream_t st) {
+  if (n == 0) return;
+  k_row_nonzero<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, k, rows, vflag);
 }
 
 void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_head,

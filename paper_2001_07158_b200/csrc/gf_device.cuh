@@ -21,6 +21,7 @@
 //  * gf_mul_serial -- bit-serial reference for the self-test kernel.
 #pragma once
 #include <cstdint>
+#include <utility>
 
 namespace tsv {
 
@@ -329,6 +330,51 @@ struct GfTable {
     return word8<0>(lo32(s), base) ^ word8<8>(hi32(s), base);
   }
 };
+
+// ---- host field arithmetic (a handful of products per evaluation) -------
+
+// GF(2^64) product mod x^64 + x^4 + x^3 + x + 1, bit-serial (gf.hpp:55-65, 85-106).
+inline uint64_t gf_mul_host(uint64_t a, uint64_t b) {
+  uint64_t r = 0;
+  for (int i = 0; i < 64; ++i) {
+    if ((b >> i) & 1ull) r ^= a;
+    a = (a << 1) ^ ((a >> 63) ? 0x1bull : 0ull);
+  }
+  return r;
+}
+
+// a^(2^64 - 2) = a^-1 (a != 0).
+inline uint64_t gf_inv_host(uint64_t a) {
+  uint64_t r = 1, sq = a;
+  for (int i = 1; i < 64; ++i) {  // exponent bits 1..63 are set, bit 0 is not
+    sq = gf_mul_host(sq, sq);
+    r = gf_mul_host(r, sq);
+  }
+  return r;
+}
+
+// Determinant of the row-major k x k matrix m (Gaussian elimination; in
+// characteristic 2 it equals the permanent).
+inline uint64_t gf_det_host(const uint64_t* m, int k) {
+  uint64_t a[32 * 32];
+  for (int i = 0; i < k * k; ++i) a[i] = m[i];
+  uint64_t det = 1;
+  for (int c = 0; c < k; ++c) {
+    int p = c;
+    while (p < k && a[p * k + c] == 0) ++p;
+    if (p == k) return 0;
+    if (p != c)
+      for (int j = 0; j < k; ++j) std::swap(a[p * k + j], a[c * k + j]);
+    det = gf_mul_host(det, a[c * k + c]);
+    const uint64_t inv = gf_inv_host(a[c * k + c]);
+    for (int r = c + 1; r < k; ++r) {
+      const uint64_t f = gf_mul_host(a[r * k + c], inv);
+      if (f)
+        for (int j = c; j < k; ++j) a[r * k + j] ^= gf_mul_host(f, a[c * k + j]);
+    }
+  }
+  return det;
+}
 
 // ---- counter PRNG: gf.hpp:111-153 (splitmix64 finalizer rounds) ----------
 

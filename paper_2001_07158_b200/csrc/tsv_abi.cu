@@ -317,7 +317,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
   const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
   const uint64_t n = static_cast<uint64_t>(g->dev.n);
-  const uint64_t words = 2 * S * M + C * M + 2 * n * k + n + S / 2 + 1;
+  const uint64_t words = 2 * S * M + C * M + 2 * n * k + n + S / 2 + (n + S) / 8 + 2;
   if (words > cfg->memory_cap_words || words > device_budget_words()) return false;
   if (peak_out) *peak_out = words;
   const int32_t nn = g->dev.n;
@@ -325,21 +325,43 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   TSV_CUDA(cudaGetDevice(&dev));
   TSV_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
 
+  // Shade basis (coef_kernels.cu, top): z_u(x) = XOR_d v_{u,d} w_d(x), so the
+  // engine runs on the n x k table of v_{u,d} (0 for d not in S(u); k_zj
+  // with the identity for w) and the readout multiplies by det(W) = per(W)
+  // (char 2).  Vertex-ordered sieves keep their positional z_{u,j}.
+  uint64_t scale = 1;
   DevBuf d_w(static_cast<size_t>(k) * k * 8, st), d_zj(static_cast<size_t>(n) * k * 8, st);
-  tsv::launch_wtab(k, cfg->seed, d_w.as<uint64_t>(), st);
-  if (vc)
+  if (vc) {
     tsv::launch_zj_positional(nn, k, cfg->seed, d_zj.as<uint64_t>(), st);
-  else
+  } else {
+    std::vector<uint64_t> W(static_cast<size_t>(k) * k), I(static_cast<size_t>(k) * k, 0);
+    const uint64_t pre = tsv::draw_prefix(cfg->seed, tsv::kRoleShadeW);
+    for (int d = 0; d < k; ++d) {
+      I[static_cast<size_t>(d) * k + d] = 1;
+      for (int j = 0; j < k; ++j)
+        W[static_cast<size_t>(d) * k + j] = tsv::draw_nonzero_from(pre, d + 1, j + 1, 0);
+    }
+    scale = tsv::gf_det_host(W.data(), k);
+    // pageable source: staged before the call returns
+    TSV_CUDA(cudaMemcpyAsync(d_w.p, I.data(), I.size() * 8, cudaMemcpyHostToDevice, st));
     tsv::launch_zj(nn, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
                    d_zj.as<uint64_t>(), st);
+  }
   DevBuf X(S * M * 8, st), Y(S * M * 8, st), agg(C * M * 8, st);
   DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(S * 4, st);
+  DevBuf vflag(std::max<uint64_t>(n, 1), st), sflag(S, st);
+  tsv::launch_row_nonzero(nn, k, d_zj.as<uint64_t>(), vflag.as<uint8_t>(), st);
   TSV_CUDA(cudaMemsetAsync(ulast.p, 0, std::max<uint64_t>(n, 1) * k * 8, st));
   std::vector<int2> pairs;
   std::vector<size_t> poff(static_cast<size_t>(k) + 1, 0);
   for (int l = 2; l <= k; ++l) {
     poff[l] = pairs.size();
     pairs.insert(pairs.end(), T.pairs[l].begin(), T.pairs[l].end());
+  }
+  std::vector<size_t> joff(static_cast<size_t>(k) + 1, 0);  // jpairs after pairs
+  for (int l = 2; l <= k; ++l) {
+    joff[l] = pairs.size();
+    pairs.insert(pairs.end(), T.jpairs[l].begin(), T.jpairs[l].end());
   }
   DevBuf d_pairs(pairs.size() * sizeof(int2), st);
   TSV_CUDA(cudaMemcpyAsync(d_pairs.p, pairs.data(), pairs.size() * sizeof(int2),
@@ -361,6 +383,8 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     cp.agg = agg.as<uint64_t>();
     cp.ulast = ulast.as<uint64_t>();
     cp.max_ts = max_ts;
+    cp.vflag = vflag.as<uint8_t>();
+    cp.sflag = sflag.as<uint8_t>();
     if (vc) {
       cp.vc_color = vc->d_colors;
       cp.vc_head = vc->order[l - 1];
@@ -373,13 +397,14 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
       tsv::launch_coef_arcs(cp, st);
     }
     if (cp.last) {
-      tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k],
+      tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k], scale,
                                d_acc, st);
     } else {
       tsv::launch_coef_fixup(cp, st);
       tsv::launch_coef_ztrans(g->dev.S, static_cast<int>(T.count[l]), l,
                               slot_head.as<int32_t>(), d_zj.as<uint64_t>(), k, cp.E,
-                              Y.as<uint64_t>(), dp + poff[l], X.as<uint64_t>(), sms, st);
+                              Y.as<uint64_t>(), dp + poff[l], dp + joff[l], X.as<uint64_t>(),
+                              sflag.as<uint8_t>(), sms, st);
     }
     TSV_CUDA(cudaGetLastError());
   }
