@@ -13,21 +13,31 @@ namespace tsv {
 // One level l of the coefficient engine (kernel k_coef_arcs).
 struct CoefParams {
   DevGraph g;
-  const uint64_t* zj = nullptr;  // n x k: z_{u,j} = S_1[u][{j}]
+  const uint64_t* zj = nullptr;  // n x k: S_1 rows (v_{u,d} in the shade basis)
   int k = 0;
   int ell = 2;                   // level being produced
   bool last = false;             // ell == k: flush vertex pieces into ulast
   uint64_t seed = 1;
   int32_t anchor_source = -1;
-  int E = 0;                     // input entries C(k, ell-1) = row stride
+  int E = 0;                     // input entries C(k, ell-1)
   int e0 = 0, ne = 0;            // entry slice of this launch
-  const uint64_t* s_prev = nullptr;  // S x E: S_{ell-1} (ell > 2)
-  uint64_t* ubuf = nullptr;          // S x E: U at referenced run ends
+  const uint64_t* s_prev = nullptr;  // S rows of level ell-1 (ell > 2), stride rs_in
+  uint64_t* ubuf = nullptr;          // S rows of level ell, stride rs_out (see below)
+  int rs_in = 0, rs_out = 0;
   uint64_t* agg = nullptr;           // C x E: chunk tail prefixes
   uint64_t* ulast = nullptr;         // n x k: level-k vertex sums (zeroed)
   int32_t max_ts = 0;
-  const uint8_t* vflag = nullptr;  // n: vertex has a nonzero S_1 row (nullptr: no skipping)
-  const uint8_t* sflag = nullptr;  // S: S_{ell-1}[slot] row is nonzero (ell > 2)
+  // per vertex: -1 no shade (S = 0), d = its only shade, -2 several
+  // (nullptr: no zero skipping, no single-shade form)
+  const int8_t* vsh = nullptr;
+  const uint64_t* vsv = nullptr;   // n: v_{u,d} of a single-shade vertex, else 1
+  const uint8_t* sflag = nullptr;  // S: row of level ell-1 is nonzero (ell > 2)
+  uint8_t* sflag_out = nullptr;    // S: row of level ell is nonzero (cleared)
+  // A single-shade vertex's rows keep U_l (the S_l entries are
+  // S_l[T] = v_h * U_l[T - {d}] for T containing its shade d, else 0; v_h
+  // rides on the next arc's y): for a source with shade d the level-ell arcs
+  // read entry e (an (ell-1)-subset) at smap[d * E + e] of its U row (-1: zero).
+  const int32_t* smap = nullptr;
   const int32_t* vc_color = nullptr;  // vertex-ordered sieve filter (as LevelParams)
   int32_t vc_head = 0, vc_tail = 0, vc_wild = -1;
 };
@@ -39,12 +49,15 @@ constexpr int kCoefSlice = 128;
 
 void launch_coef_arcs(const CoefParams& p, cudaStream_t st);
 void launch_coef_fixup(const CoefParams& p, cudaStream_t st);
+// Multi-shade heads: S_l[slot] from the U row stored at the same place
+// (in place, row stride rs).  F = C(k, l) <= kZAcc.
 void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const uint64_t* zj,
-                        int k, int E, const uint64_t* ubuf, const int2* pairs,
-                        const int2* jpairs, uint64_t* out, uint8_t* sflag, int sm_count,
-                        cudaStream_t st);
-// vflag[u] = row u of the n x k table is nonzero
-void launch_row_nonzero(int32_t n, int k, const uint64_t* rows, uint8_t* vflag, cudaStream_t st);
+                        int k, int E, uint64_t* rows, int rs, const int2* jpairs,
+                        const int8_t* vsh, uint8_t* sflag, int sm_count, cudaStream_t st);
+constexpr int kZAcc = 1024;  // largest F the in-place z map handles (k <= 12)
+// vsh / vsv of the rows of the n x k shade table (CoefParams)
+void launch_vshade(int32_t n, int k, const uint64_t* rows, int8_t* vsh, uint64_t* vsv,
+                   cudaStream_t st);
 void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* ulast,
                          const int2* pairs, uint64_t scale, uint64_t* acc, cudaStream_t st);
 void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_head,
@@ -57,6 +70,9 @@ struct CoefTables {
   // pairs of level l (2..k): for output o (an l-subset T) and c < l,
   // (rank of T minus its c-th element among the (l-1)-subsets, that element)
   std::vector<std::vector<int2>> pairs;
+  // smap of level l: smap[d * C(k,l) + o] = rank of T_o - {d} among the
+  // (l-1)-subsets, -1 if d is not in T_o
+  std::vector<std::vector<int32_t>> smap;
   // jpairs of level l: for each j < k, the C(k-1, l-1) pairs (rank of an
   // (l-1)-subset T' without j, rank of T' + {j}) in increasing T' order
   std::vector<std::vector<int2>> jpairs;

@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
   __shared__ int32_t s_slot[kCoefWarps][32];
   __shared__ int32_t s_head[kCoefWarps][32];
   __shared__ int8_t s_idx[kCoefWarps][32];
+  __shared__ int8_t s_hd[kCoefWarps][32];
   __shared__ __align__(256) uint64_t s_tab[kGeneral ? 1 : kCoefWarps][kHalfTab ? 2 : 1]
                                           [GfTable::kWords];
 
@@ -136,16 +137,6 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
     const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
     const int32_t myrun = run_ctr + __popc(ends & ((1u << lane) - 1u));
     if (lane < nb) head = __ldg(P.g.run_head + myrun);
-    s_yraw[wib][lane] = y;
-    if (kGeneral) {
-      const KSplit ks = ksplit(y);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        s_ys[kGeneral ? wib : 0][j][lane] = ks.l.c[j];
-        s_ys[kGeneral ? wib : 0][4 + j][lane] = ks.h.c[j];
-        s_ys[kGeneral ? wib : 0][8 + j][lane] = ks.m.c[j];
-      }
-    }
     bool live = lane < nb && sidx >= 0;
     if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
     if (LAST) live = live && __ldg(P.g.run_ts + myrun) <= P.max_ts;
@@ -156,9 +147,27 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
     }
     // zero states: a head without shades has S = 0 (its products and stores
     // are never read), and a source whose state row is all zero adds nothing
-    const bool hz = lane < nb && P.vflag && !__ldg(P.vflag + head);
-    if (live && P.vflag)
-      live = !hz && (FIRST ? __ldg(P.vflag + sidx) : __ldg(P.sflag + sidx)) != 0;
+    const bool hz = lane < nb && P.vsh && __ldg(P.vsh + head) == -1;
+    if (live && P.vsh)
+      live = !hz && (FIRST ? __ldg(P.vsh + sidx) != -1 : __ldg(P.sflag + sidx) != 0);
+    // a single-shade tail's state is stored without its v (k_coef_zshift):
+    // the arc multiplies by y * v_tail instead
+    int8_t td = -2;  // the source's shade when it keeps its U row
+    if (!FIRST && live && P.vsv) {
+      const int32_t tl = __ldg(P.g.arc_tail + base + lane);
+      td = __ldg(P.vsh + tl);
+      if (td >= 0) y = gf_mul(y, __ldg(P.vsv + tl));
+    }
+    s_yraw[wib][lane] = y;
+    if (kGeneral) {
+      const KSplit ks = ksplit(y);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s_ys[kGeneral ? wib : 0][j][lane] = ks.l.c[j];
+        s_ys[kGeneral ? wib : 0][4 + j][lane] = ks.h.c[j];
+        s_ys[kGeneral ? wib : 0][8 + j][lane] = ks.m.c[j];
+      }
+    }
     bool push;
     int32_t slot = -1;
     if (LAST) {  // last arc of its vertex within this chunk: flush the piece
@@ -170,6 +179,7 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
       slot = (lane < nb && !hz && (meta & kRunEnd)) ? __ldg(P.g.run_slot + myrun) : -1;
       push = slot >= 0;
     }
+    s_hd[wib][lane] = td;
     s_src[wib][lane] = sidx;
     s_meta[wib][lane] = (meta & (kVStart | kRunEnd)) | (live ? kLive : 0u) | (push ? kPush : 0u);
     s_slot[wib][lane] = slot;
@@ -187,10 +197,28 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
       const int i = q < nact ? s_idx[wib][q] : 0;
       if (q < nact && (s_meta[wib][i] & kLive)) {
         const int64_t src = s_src[wib][i];
-        const uint64_t* row = FIRST ? P.zj + src * P.k + P.e0 : P.s_prev + src * E + P.e0;
+        if (FIRST) {
+          const uint64_t* row = P.zj + src * P.k + P.e0;
 #pragma unroll
-        for (int p = 0; p < PPT; ++p)
-          if (ev[p]) out[p] = __ldg(row + li + LG * p);
+          for (int p = 0; p < PPT; ++p)
+            if (ev[p]) out[p] = __ldg(row + li + LG * p);
+        } else {
+          const uint64_t* row = P.s_prev + src * P.rs_in;
+          const int td = s_hd[wib][i];
+          if (td >= 0) {  // U row of a single-shade source
+            const int32_t* sm = P.smap + td * E + P.e0;
+#pragma unroll
+            for (int p = 0; p < PPT; ++p)
+              if (ev[p]) {
+                const int in = __ldg(sm + li + LG * p);
+                if (in >= 0) out[p] = __ldg(row + in);
+              }
+          } else {
+#pragma unroll
+            for (int p = 0; p < PPT; ++p)
+              if (ev[p]) out[p] = __ldg(row + P.e0 + li + LG * p);
+          }
+        }
       }
     };
     uint64_t nxt[PPT];
@@ -256,20 +284,29 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
         if (!f) v[p] ^= carry[p];
         carry[p] = (G > 1) ? __shfl_sync(kFull, v[p], last_lane) : v[p];
       }
-      if (mt & kPush) {
-        if (LAST) {
+      if (LAST) {
+        if (mt & kPush) {
           const int64_t row = static_cast<int64_t>(s_head[wib][i]) * E + P.e0;
 #pragma unroll
           for (int p = 0; p < PPT; ++p)
             if (ev[p] && v[p])
               atomicXor(reinterpret_cast<unsigned long long*>(P.ulast + row + li + LG * p),
                         static_cast<unsigned long long>(v[p]));
-        } else {
-          const int64_t row = static_cast<int64_t>(s_slot[wib][i]) * E + P.e0;
+        }
+      } else {
+        bool nzr = false;
+        if (mt & kPush) {
+          const int64_t row = static_cast<int64_t>(s_slot[wib][i]) * P.rs_out + P.e0;
 #pragma unroll
           for (int p = 0; p < PPT; ++p)
-            if (ev[p]) P.ubuf[row + li + LG * p] = v[p];
+            if (ev[p]) {
+              P.ubuf[row + li + LG * p] = v[p];
+              nzr = nzr || v[p] != 0;
+            }
         }
+        const unsigned bm = __ballot_sync(kFull, nzr);
+        const unsigned gm = LG == 32 ? kFull : ((1u << LG) - 1u) << (g * LG);
+        if ((mt & kPush) && li == 0 && (bm & gm)) P.sflag_out[s_slot[wib][i]] = 1;
       }
     }
     __syncwarp();
@@ -292,6 +329,8 @@ __global__ void k_coef_fixup(const CoefParams P) {
   const int32_t head = P.g.run_head[r0];
   const int32_t r1 = min(P.g.chunk_run[c + 1], P.g.vtx_run_off[head + 1]);
   if (r0 >= r1) return;
+  const int dh = P.vsh ? P.vsh[head] : -2;
+  if (dh == -1) return;  // shadeless: rows never read
   const int64_t E = P.E;
   for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
     uint64_t carry = 0;
@@ -302,55 +341,35 @@ __global__ void k_coef_fixup(const CoefParams P) {
     if (!carry) continue;
     for (int32_t r = r0; r < r1; ++r) {
       const int32_t slot = P.g.run_slot[r];
-      if (slot >= 0) P.ubuf[static_cast<int64_t>(slot) * E + e] ^= carry;
+      if (slot >= 0) {
+        P.ubuf[static_cast<int64_t>(slot) * P.rs_out + e] ^= carry;
+        P.sflag_out[slot] = 1;
+      }
     }
   }
 }
 
-// S_l[slot][o] = XOR_{c < l} z_{head, j_c} * U[slot][in_c], (in_c, j_c) =
-// pairs[o*l + c]: one thread per (slot, output entry).
-__global__ void k_coef_ztrans(int64_t S, int F, int l, const int32_t* __restrict__ slot_head,
-                              const uint64_t* __restrict__ zj, int k, int E,
-                              const uint64_t* __restrict__ ubuf, const int2* __restrict__ pairs,
-                              uint64_t* __restrict__ out, uint8_t* __restrict__ sflag) {
-  const int64_t total = S * F;
-  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t s = idx / F;
-    const int o = static_cast<int>(idx - s * F);
-    const uint64_t* U = ubuf + s * E;
-    const uint64_t* z = zj + static_cast<int64_t>(__ldg(slot_head + s)) * k;
-    uint64_t r = 0;
-    for (int cc = 0; cc < l; ++cc) {
-      const int2 pr = __ldg(pairs + o * l + cc);
-      const uint64_t u = __ldg(U + pr.x);
-      if (u) r ^= gf_mul(__ldg(z + pr.y), u);
-    }
-    out[idx] = r;
-    if (r) sflag[s] = 1;
-  }
-}
-
-// The same map with shared-memory multiple tables of the multipliers.  Each
-// z_{h,j} multiplies C(k-1, l-1) entries of every slot of head h, so a warp
-// takes a window of 32 consecutive slots (slot_head is nondecreasing: slots
-// are ranks in vertex-major run order) and, per head segment of the window
-// and per j, builds the table of z_{h,j} (GfTable, all 32 lanes) and spreads
-// the (slot, T' without j) items of the segment over its lanes, XORing
-// z_{h,j} * U[T'] into output T' + {j} of a shared-memory accumulator.  The
-// multiplier is warp-uniform, so every lookup of a warp hits one 128-byte
-// table window (conflict-free); within one j the outputs are distinct, so
-// the accumulator needs no atomics.  ~45 instructions per product instead of
-// ~170 for the general product.  Segments with more than kZAcc / F slots are
-// processed in sub-batches.
+// S_l[slot][T] = XOR_{j in T} z_{h,j} * U[slot][T - {j}] for the slots of
+// heads with several shades (the others are stored mapped by k_coef_arcs),
+// in place: the U row (C(k, l-1) entries) is replaced by the S row
+// (C(k, l) entries) at the same row (stride rs).  Each z_{h,j} multiplies
+// C(k-1, l-1) entries of every slot of head h, so a warp takes a window of
+// 32 consecutive slots (slot_head is nondecreasing: slots are ranks in
+// vertex-major run order) and, per head segment of the window and per j
+// with z_{h,j} != 0, builds the table of z_{h,j} (GfTable, all 32 lanes)
+// and spreads the (slot, T' without j) items of the segment over its lanes,
+// XORing z_{h,j} * U[T'] into output T' + {j} of a shared-memory
+// accumulator.  The multiplier is warp-uniform, so every lookup of a warp
+// hits one 128-byte table window (conflict-free); within one j the outputs
+// are distinct, so the accumulator needs no atomics.  A sub-batch's U rows
+// are all read before its S rows are written.
 constexpr int kZWarps = 4;
-constexpr int kZAcc = 1024;  // accumulator words per warp
 constexpr int kZWarpWords = GfTable::kWords + kZAcc;
 __global__ void __launch_bounds__(kZWarps * 32)
     k_coef_ztrans_tab(int64_t S, int F, int K1, const int32_t* __restrict__ slot_head,
-                      const uint64_t* __restrict__ zj, int k, int E,
-                      const uint64_t* __restrict__ ubuf, const int2* __restrict__ jpairs,
-                      uint64_t* __restrict__ out, uint8_t* __restrict__ sflag) {
+                      const uint64_t* __restrict__ zj, int k, uint64_t* rows, int rs,
+                      const int2* __restrict__ jpairs, const int8_t* __restrict__ vsh,
+                      uint8_t* __restrict__ sflag) {
   __shared__ __align__(256) uint64_t sm[kZWarps][kZWarpWords];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint64_t* const tab = sm[wib];
@@ -358,6 +377,7 @@ __global__ void __launch_bounds__(kZWarps * 32)
   GfTable T{tab};
   const int qmax = kZAcc / F < 32 ? kZAcc / F : 32;  // slots per sub-batch (F <= kZAcc)
   const float invK1 = 1.0f / static_cast<float>(K1);
+  const float invF = 1.0f / static_cast<float>(F);
   const int64_t nwin = (S + 31) / 32;
   for (int64_t w = static_cast<int64_t>(blockIdx.x) * kZWarps + wib; w < nwin;
        w += static_cast<int64_t>(gridDim.x) * kZWarps) {
@@ -371,11 +391,12 @@ __global__ void __launch_bounds__(kZWarps * 32)
       starts &= starts - 1;
       const int b = starts ? __ffs(starts) - 1 : nsl;
       const int32_t h = __shfl_sync(kFull, myh, a);
+      if (vsh && __ldg(vsh + h) != -2) continue;  // stored mapped by k_coef_arcs
       const uint64_t zl = lane < k ? __ldg(zj + static_cast<int64_t>(h) * k + lane) : 0ull;
       for (int q0 = a; q0 < b; q0 += qmax) {
         const int qb = b - q0 < qmax ? b - q0 : qmax;
         const int64_t s0 = w0 + q0;
-        const uint64_t* U0 = ubuf + s0 * E;
+        const uint64_t* U0 = rows + s0 * rs;
         __syncwarp();
         for (int i = lane; i < qb * F; i += 32) acc[i] = 0;
         const int items = qb * K1;
@@ -391,21 +412,18 @@ __global__ void __launch_bounds__(kZWarps * 32)
             if ((qq + 1) * K1 <= it) ++qq;
             if (qq * K1 > it) --qq;
             const int2 p = __ldg(jp + (it - qq * K1));
-            const uint64_t u = __ldg(U0 + static_cast<int64_t>(qq) * E + p.x);
+            const uint64_t u = U0[static_cast<int64_t>(qq) * rs + p.x];
             if (u) acc[qq * F + p.y] ^= T.mul(u);
           }
         }
         __syncwarp();
-        const float invF = 1.0f / static_cast<float>(F);
         for (int i = lane; i < qb * F; i += 32) {
+          int qq = __float2int_rz(static_cast<float>(i) * invF);
+          if ((qq + 1) * F <= i) ++qq;
+          if (qq * F > i) --qq;
           const uint64_t r = acc[i];
-          out[s0 * F + i] = r;
-          if (r) {  // sflag was cleared before the launch
-            int qq = __float2int_rz(static_cast<float>(i) * invF);
-            if ((qq + 1) * F <= i) ++qq;
-            if (qq * F > i) --qq;
-            sflag[s0 + qq] = 1;
-          }
+          rows[(s0 + qq) * rs + (i - qq * F)] = r;
+          if (r) sflag[s0 + qq] = 1;
         }
       }
     }
@@ -432,13 +450,18 @@ __global__ void k_coef_readout(int32_t n, const uint64_t* __restrict__ zj, int k
   if (r) acc[h] ^= r;
 }
 
-__global__ void k_row_nonzero(int32_t n, int k, const uint64_t* __restrict__ rows,
-                              uint8_t* __restrict__ vflag) {
+__global__ void k_vshade(int32_t n, int k, const uint64_t* __restrict__ rows,
+                         int8_t* __restrict__ vsh, uint64_t* __restrict__ vsv) {
   const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u >= n) return;
-  uint64_t a = 0;
-  for (int j = 0; j < k; ++j) a |= __ldg(rows + u * k + j);
-  vflag[u] = a != 0;
+  int cnt = 0, d = -1;
+  uint64_t v = 1;
+  for (int j = 0; j < k; ++j) {
+    const uint64_t x = __ldg(rows + u * k + j);
+    if (x) ++cnt, d = j, v = x;
+  }
+  vsh[u] = static_cast<int8_t>(cnt == 0 ? -1 : cnt == 1 ? d : -2);
+  vsv[u] = cnt == 1 ? v : 1ull;
 }
 
 __global__ void k_slot_head(int64_t R, const int32_t* __restrict__ run_slot,
@@ -510,6 +533,15 @@ CoefTables coef_tables(int k) {
       t.jpairs[l].insert(t.jpairs[l].end(), per[j].begin(), per[j].end());
     }
   }
+  t.smap.resize(static_cast<size_t>(k) + 1);
+  for (int l = 2; l <= k; ++l) {
+    const int64_t F = t.count[l];
+    std::vector<int32_t>& m = t.smap[l];
+    m.assign(static_cast<size_t>(k * F), -1);
+    const std::vector<int2>& v = t.pairs[l];
+    for (size_t i = 0; i < v.size(); ++i)  // output o = i / l, pair (in, j)
+      m[static_cast<size_t>(v[i].y * F) + i / l] = v[i].x;
+  }
   return t;
 }
 
@@ -543,35 +575,22 @@ void launch_coef_fixup(const CoefParams& p, cudaStream_t st) {
 }
 
 void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const uint64_t* zj,
-                        int k, int E, const uint64_t* ubuf, const int2* pairs,
-                        const int2* jpairs, uint64_t* out, uint8_t* sflag, int sm_count,
-                        cudaStream_t st) {
+                        int k, int E, uint64_t* rows, int rs, const int2* jpairs,
+                        const int8_t* vsh, uint8_t* sflag, int sm_count, cudaStream_t st) {
+  (void)E;
   if (S == 0) return;
   prof_begin("coef_ztrans", st);
-  cudaMemsetAsync(sflag, 0, static_cast<size_t>(S), st);
-  static const bool general = [] {
-    const char* e = std::getenv("TSV_ZTRANS");
-    return e && std::strcmp(e, "general") == 0;
-  }();
-  if (!general && F <= kZAcc) {
-    static int per_sm = 0;
-    if (!per_sm &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coef_ztrans_tab, kZWarps * 32,
-                                                      0) != cudaSuccess)
-      per_sm = 1;
-    const int K1 = static_cast<int>(static_cast<int64_t>(F) * l / k);  // C(k-1, l-1)
-    const int64_t nwin = (S + 31) / 32;
-    const int64_t want = (nwin + kZWarps - 1) / kZWarps;
-    const int64_t cap = static_cast<int64_t>(sm_count) * (per_sm > 0 ? per_sm : 1);
-    k_coef_ztrans_tab<<<static_cast<unsigned>(want < cap ? want : cap), kZWarps * 32, 0, st>>>(
-        S, F, K1, slot_head, zj, k, E, ubuf, jpairs, out, sflag);
-  } else {
-    const int64_t total = S * F;
-    const int64_t want = (total + 255) / 256;
-    const int64_t cap = static_cast<int64_t>(sm_count) * 64;
-    k_coef_ztrans<<<static_cast<unsigned>(want < cap ? want : cap), 256, 0, st>>>(
-        S, F, l, slot_head, zj, k, E, ubuf, pairs, out, sflag);
-  }
+  static int per_sm = 0;
+  if (!per_sm &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coef_ztrans_tab, kZWarps * 32,
+                                                    0) != cudaSuccess)
+    per_sm = 1;
+  const int K1 = static_cast<int>(static_cast<int64_t>(F) * l / k);  // C(k-1, l-1)
+  const int64_t nwin = (S + 31) / 32;
+  const int64_t want = (nwin + kZWarps - 1) / kZWarps;
+  const int64_t cap = static_cast<int64_t>(sm_count) * (per_sm > 0 ? per_sm : 1);
+  k_coef_ztrans_tab<<<static_cast<unsigned>(want < cap ? want : cap), kZWarps * 32, 0, st>>>(
+      S, F, K1, slot_head, zj, k, rows, rs, jpairs, vsh, sflag);
   prof_end(st);
 }
 
@@ -583,9 +602,10 @@ void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* u
   prof_end(st);
 }
 
-void launch_row_nonzero(int32_t n, int k, const uint64_t* rows, uint8_t* vflag, cudaStream_t st) {
+void launch_vshade(int32_t n, int k, const uint64_t* rows, int8_t* vsh, uint64_t* vsv,
+                   cudaStream_t st) {
   if (n == 0) return;
-  k_row_nonzero<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, k, rows, vflag);
+  k_vshade<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(n, k, rows, vsh, vsv);
 }
 
 void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_head,

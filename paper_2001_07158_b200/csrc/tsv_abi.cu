@@ -310,14 +310,14 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                uint64_t* peak_out, const VcSpec* vc) {
   const char* eng = std::getenv("TSV_ENGINE");
   if (eng && std::strcmp(eng, "points") == 0) return false;
-  if (k < 2 || k > 16) return false;
+  if (k < 2 || k > 12) return false;  // C(k, l) <= tsv::kZAcc
   const tsv::CoefTables T = tsv::coef_tables(k);
   int64_t M = 1;
   for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, T.count[l]);
   const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
   const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
   const uint64_t n = static_cast<uint64_t>(g->dev.n);
-  const uint64_t words = 2 * S * M + C * M + 2 * n * k + n + S / 2 + (n + S) / 8 + 2;
+  const uint64_t words = 2 * S * M + C * M + 2 * n * k + 2 * n + S / 2 + (n + S) / 8 + 2;
   if (words > cfg->memory_cap_words || words > device_budget_words()) return false;
   if (peak_out) *peak_out = words;
   const int32_t nn = g->dev.n;
@@ -349,25 +349,40 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   }
   DevBuf X(S * M * 8, st), Y(S * M * 8, st), agg(C * M * 8, st);
   DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(S * 4, st);
-  DevBuf vflag(std::max<uint64_t>(n, 1), st), sflag(S, st);
-  tsv::launch_row_nonzero(nn, k, d_zj.as<uint64_t>(), vflag.as<uint8_t>(), st);
+  // zero skipping and the single-shade form (CoefParams::vsh); positional z
+  // keeps the plain z map
+  DevBuf vsh(std::max<uint64_t>(n, 1), st), vsv(std::max<uint64_t>(n, 1) * 8, st);
+  DevBuf fl0(S, st), fl1(S, st);
+  if (!vc) tsv::launch_vshade(nn, k, d_zj.as<uint64_t>(), vsh.as<int8_t>(), vsv.as<uint64_t>(), st);
   TSV_CUDA(cudaMemsetAsync(ulast.p, 0, std::max<uint64_t>(n, 1) * k * 8, st));
+  // host tables, one upload: pairs (readout), jpairs (z map), smap
   std::vector<int2> pairs;
-  std::vector<size_t> poff(static_cast<size_t>(k) + 1, 0);
+  std::vector<size_t> poff(static_cast<size_t>(k) + 1, 0), joff = poff;
   for (int l = 2; l <= k; ++l) {
     poff[l] = pairs.size();
     pairs.insert(pairs.end(), T.pairs[l].begin(), T.pairs[l].end());
   }
-  std::vector<size_t> joff(static_cast<size_t>(k) + 1, 0);  // jpairs after pairs
   for (int l = 2; l <= k; ++l) {
     joff[l] = pairs.size();
     pairs.insert(pairs.end(), T.jpairs[l].begin(), T.jpairs[l].end());
   }
-  DevBuf d_pairs(pairs.size() * sizeof(int2), st);
+  std::vector<int32_t> maps;
+  std::vector<size_t> moff(static_cast<size_t>(k) + 1, 0);
+  for (int l = 2; l <= k; ++l) {
+    moff[l] = maps.size();
+    maps.insert(maps.end(), T.smap[l].begin(), T.smap[l].end());
+  }
+  DevBuf d_pairs(pairs.size() * sizeof(int2), st), d_maps(std::max<size_t>(maps.size(), 1) * 4, st);
+  // pageable sources: staged before the calls return
   TSV_CUDA(cudaMemcpyAsync(d_pairs.p, pairs.data(), pairs.size() * sizeof(int2),
                            cudaMemcpyHostToDevice, st));
+  TSV_CUDA(cudaMemcpyAsync(d_maps.p, maps.data(), maps.size() * 4, cudaMemcpyHostToDevice, st));
   tsv::launch_slot_head(g->dev.R, g->dev.run_slot, g->dev.run_head, slot_head.as<int32_t>(), st);
   const int2* dp = d_pairs.as<int2>();
+  // row strides: level l's rows hold its U row (C(k, l-1)) and then its S row (C(k, l))
+  auto rs = [&](int l) { return static_cast<int>(std::max(T.count[l - 1], T.count[l])); };
+  uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
+  uint8_t *fa = fl0.as<uint8_t>(), *fb = fl1.as<uint8_t>();
   for (int l = 2; l <= k; ++l) {
     tsv::CoefParams cp;
     cp.g = g->dev;
@@ -378,33 +393,40 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     cp.seed = cfg->seed;
     cp.anchor_source = anchor_source;
     cp.E = static_cast<int>(T.count[l - 1]);
-    cp.s_prev = X.as<uint64_t>();
-    cp.ubuf = Y.as<uint64_t>();
+    cp.s_prev = A;
+    cp.rs_in = l > 2 ? rs(l - 1) : 0;
+    cp.ubuf = B;
+    cp.rs_out = l < k ? rs(l) : 0;
     cp.agg = agg.as<uint64_t>();
     cp.ulast = ulast.as<uint64_t>();
     cp.max_ts = max_ts;
-    cp.vflag = vflag.as<uint8_t>();
-    cp.sflag = sflag.as<uint8_t>();
+    cp.vsh = vc ? nullptr : vsh.as<int8_t>();
+    cp.vsv = vc ? nullptr : vsv.as<uint64_t>();
+    cp.sflag = fa;
+    cp.sflag_out = fb;
+    cp.smap = l > 2 ? d_maps.as<int32_t>() + moff[l - 1] : nullptr;
     if (vc) {
       cp.vc_color = vc->d_colors;
       cp.vc_head = vc->order[l - 1];
       cp.vc_tail = vc->order[l - 2];
       cp.vc_wild = vc->wild;
     }
+    if (!cp.last) TSV_CUDA(cudaMemsetAsync(fb, 0, S, st));
     for (int e0 = 0; e0 < cp.E; e0 += tsv::kCoefSlice) {
       cp.e0 = e0;
       cp.ne = std::min(tsv::kCoefSlice, cp.E - e0);
       tsv::launch_coef_arcs(cp, st);
     }
     if (cp.last) {
-      tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k], scale,
-                               d_acc, st);
+      tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k],
+                               scale, d_acc, st);
     } else {
       tsv::launch_coef_fixup(cp, st);
       tsv::launch_coef_ztrans(g->dev.S, static_cast<int>(T.count[l]), l,
-                              slot_head.as<int32_t>(), d_zj.as<uint64_t>(), k, cp.E,
-                              Y.as<uint64_t>(), dp + poff[l], dp + joff[l], X.as<uint64_t>(),
-                              sflag.as<uint8_t>(), sms, st);
+                              slot_head.as<int32_t>(), d_zj.as<uint64_t>(), k, cp.E, B, rs(l),
+                              dp + joff[l], cp.vsh, fb, sms, st);
+      std::swap(A, B);
+      std::swap(fa, fb);
     }
     TSV_CUDA(cudaGetLastError());
   }
