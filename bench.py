@@ -229,7 +229,7 @@ def coef_roofline(coef, k, info, evals, hbm, peak_kind, args, world, sm_mhz):
         if prof["config"] != args.config or args.scale != 1.0 or world != 1:
             prof = None
         else:
-            prof = prof["kernels"][name]
+            prof = dict(prof["kernels"][name], capture=prof["capture"])
     except Exception:
         prof = None
     if prof is not None:
