@@ -38,6 +38,16 @@ struct CoefParams {
   // rides on the next arc's y): for a source with shade d the level-ell arcs
   // read entry e (an (ell-1)-subset) at smap[d * E + e] of its U row (-1: zero).
   const int32_t* smap = nullptr;
+  // item-stream kernel (coef_items.cu): compact frames, per (tail class,
+  // head class) item lists of (input index, output index); class = the
+  // vertex's shade, or k for several shades
+  const int2* items = nullptr;
+  const int32_t* item_off = nullptr;  // (k+1) x (k+1)
+  const int32_t* item_cnt = nullptr;
+  int frame_single = 0;  // C(k-1, ell-1) (0: full frames everywhere)
+  int frame_multi = 0;   // C(k, ell-1)
+  int frame_max = 0;     // accumulator words (frame_multi, or frame_single without multi-shade vertices)
+  int warp_words = 0;    // shared words per warp (table + frame accumulator)
   const int32_t* vc_color = nullptr;  // vertex-ordered sieve filter (as LevelParams)
   int32_t vc_head = 0, vc_tail = 0, vc_wild = -1;
 };
@@ -49,6 +59,14 @@ constexpr int kCoefSlice = 128;
 
 void launch_coef_arcs(const CoefParams& p, cudaStream_t st);
 void launch_coef_fixup(const CoefParams& p, cudaStream_t st);
+void launch_coef_items(const CoefParams& p, cudaStream_t st);
+// Item lists of level l (2..k) for CoefParams::items: per (tail class tc,
+// head class hc), tc/hc = shade d or k (several shades).
+struct CoefItems {
+  std::vector<int2> items;
+  std::vector<int32_t> off, cnt;  // (k+1) x (k+1)
+};
+CoefItems coef_items(int k, int l);
 // Multi-shade heads: S_l[slot] from the U row stored at the same place
 // (in place, row stride rs).  F = C(k, l) <= kZAcc.
 void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const uint64_t* zj,
@@ -58,8 +76,11 @@ constexpr int kZAcc = 1024;  // largest F the in-place z map handles (k <= 12)
 // vsh / vsv of the rows of the n x k shade table (CoefParams)
 void launch_vshade(int32_t n, int k, const uint64_t* rows, int8_t* vsh, uint64_t* vsv,
                    cudaStream_t st);
+// vsh / vsv non-null: single-shade vertices hold their one compact level-k
+// entry in ulast[h * k] (item-stream kernel)
 void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* ulast,
-                         const int2* pairs, uint64_t scale, uint64_t* acc, cudaStream_t st);
+                         const int2* pairs, uint64_t scale, const int8_t* vsh,
+                         const uint64_t* vsv, uint64_t* acc, cudaStream_t st);
 void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_head,
                       int32_t* slot_head, cudaStream_t st);
 

@@ -331,11 +331,12 @@ __global__ void k_coef_fixup(const CoefParams P) {
   if (r0 >= r1) return;
   const int dh = P.vsh ? P.vsh[head] : -2;
   if (dh == -1) return;  // shadeless: rows never read
-  const int64_t E = P.E;
+  // entries of the head's rows: its compact frame in the item-stream layout
+  const int64_t E = (P.frame_single && dh >= 0) ? P.frame_single : P.E;
   for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
     uint64_t carry = 0;
     for (int64_t cc = c - 1;; --cc) {
-      carry ^= P.agg[cc * E + e];
+      carry ^= P.agg[cc * P.E + e];
       if (!P.g.chunk_carry[cc] || P.g.run_head[P.g.chunk_run[cc]] != head) break;
     }
     if (!carry) continue;
@@ -435,12 +436,19 @@ __global__ void __launch_bounds__(kZWarps * 32)
 __global__ void k_coef_readout(int32_t n, const uint64_t* __restrict__ zj, int k,
                                const uint64_t* __restrict__ ulast,
                                const int2* __restrict__ pairs, uint64_t scale,
-                               uint64_t* __restrict__ acc) {
+                               const int8_t* __restrict__ vsh,
+                               const uint64_t* __restrict__ vsv, uint64_t* __restrict__ acc) {
   const int64_t h = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (h >= n) return;
   const uint64_t* U = ulast + h * k;
   const uint64_t* z = zj + h * k;
   uint64_t r = 0;
+  const int d = vsh ? __ldg(vsh + h) : -2;
+  if (d == -1) return;
+  if (d >= 0) {  // compact frame: the one entry [k] - {d}
+    const uint64_t u = __ldg(U);
+    if (u) r = gf_mul(__ldg(vsv + h), u);
+  } else
   for (int cc = 0; cc < k; ++cc) {
     const int2 pr = __ldg(pairs + cc);
     const uint64_t u = __ldg(U + pr.x);
@@ -545,6 +553,49 @@ CoefTables coef_tables(int k) {
   return t;
 }
 
+CoefItems coef_items(int k, int l) {
+  // binomials and colex ranks (compact frame d: the bit d removed)
+  int64_t C[33][33] = {};
+  for (int a = 0; a <= 32; ++a) {
+    C[a][0] = 1;
+    for (int b = 1; b <= a; ++b) C[a][b] = C[a - 1][b - 1] + C[a - 1][b];
+  }
+  auto rank = [&](uint64_t mask) {
+    int64_t r = 0;
+    int i = 0;
+    for (int x = 0; mask; ++x, mask >>= 1)
+      if (mask & 1ull) r += C[x][i + 1], ++i;
+    return static_cast<int32_t>(r);
+  };
+  auto squeeze = [](uint64_t mask, int d) {  // drop bit d
+    const uint64_t lo = mask & ((1ull << d) - 1ull);
+    return lo | ((mask >> (d + 1)) << d);
+  };
+  CoefItems t;
+  const int K1 = k + 1;
+  t.off.assign(static_cast<size_t>(K1 * K1), 0);
+  t.cnt.assign(static_cast<size_t>(K1 * K1), 0);
+  for (int tc = 0; tc <= k; ++tc)
+    for (int hc = 0; hc <= k; ++hc) {
+      t.off[tc * K1 + hc] = static_cast<int32_t>(t.items.size());
+      if (tc < k && tc == hc) continue;  // same single shade twice: zero
+      // U entries T of the head: (l-1)-subsets, in increasing mask order
+      for (uint64_t T = (1ull << (l - 1)) - 1; T < (1ull << k);) {
+        const bool ok = (tc == k || ((T >> tc) & 1ull)) && (hc == k || !((T >> hc) & 1ull));
+        if (ok) {
+          const int32_t in = tc == k ? rank(T) : rank(squeeze(T & ~(1ull << tc), tc));
+          const int32_t out = hc == k ? rank(T) : rank(squeeze(T, hc));
+          t.items.push_back(make_int2(in, out));
+        }
+        if (T == 0) break;
+        const uint64_t cbit = T & (~T + 1), rr = T + cbit;
+        T = (((rr ^ T) >> 2) / cbit) | rr;
+      }
+      t.cnt[tc * K1 + hc] = static_cast<int32_t>(t.items.size()) - t.off[tc * K1 + hc];
+    }
+  return t;
+}
+
 int coef_group_lanes(int ne) { return ne <= 4 ? 4 : ne <= 8 ? 8 : ne <= 16 ? 16 : 32; }
 
 void launch_coef_arcs(const CoefParams& p, cudaStream_t st) {
@@ -595,10 +646,11 @@ void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const
 }
 
 void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* ulast,
-                         const int2* pairs, uint64_t scale, uint64_t* acc, cudaStream_t st) {
+                         const int2* pairs, uint64_t scale, const int8_t* vsh,
+                         const uint64_t* vsv, uint64_t* acc, cudaStream_t st) {
   if (n == 0) return;
   prof_begin("coef_readout", st);
-  k_coef_readout<<<(n + 255) / 256, 256, 0, st>>>(n, zj, k, ulast, pairs, scale, acc);
+  k_coef_readout<<<(n + 255) / 256, 256, 0, st>>>(n, zj, k, ulast, pairs, scale, vsh, vsv, acc);
   prof_end(st);
 }
 

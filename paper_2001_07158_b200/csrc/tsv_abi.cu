@@ -186,6 +186,8 @@ struct tsv_graph {
 struct tsv_shades {
   int k = 0;
   int32_t n = 0;
+  int64_t single = 0;  // vertices with exactly one shade (engine choice)
+  int64_t multi = 0;   // vertices with several shades
   int device = 0;
   int32_t* off = nullptr;
   int32_t* shades = nullptr;
@@ -372,6 +374,25 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     moff[l] = maps.size();
     maps.insert(maps.end(), T.smap[l].begin(), T.smap[l].end());
   }
+  // item-stream kernel (coef_items.cu) unless the vertex-ordered sieve's
+  // positional z (no shade structure) or TSV_ITEMS=0
+  const char* it_env = std::getenv("TSV_ITEMS");
+  // (measured: C3/C4, all single-shade, 1.3x faster; C5, no single-shade
+  // vertex, 1.2x slower than k_coef_arcs)
+  const bool use_items = !vc && !(it_env && std::strcmp(it_env, "0") == 0) &&
+                         ((it_env && std::strcmp(it_env, "1") == 0) || sh->single * 4 >= n);
+  std::vector<size_t> ioff(static_cast<size_t>(k) + 1, 0), icoff = ioff;
+  if (use_items) {
+    for (int l = 2; l <= k; ++l) {
+      tsv::CoefItems ci = tsv::coef_items(k, l);
+      for (int32_t& o : ci.off) o += static_cast<int32_t>(pairs.size());  // absolute
+      ioff[l] = pairs.size();
+      pairs.insert(pairs.end(), ci.items.begin(), ci.items.end());
+      icoff[l] = maps.size();
+      maps.insert(maps.end(), ci.off.begin(), ci.off.end());
+      maps.insert(maps.end(), ci.cnt.begin(), ci.cnt.end());
+    }
+  }
   DevBuf d_pairs(pairs.size() * sizeof(int2), st), d_maps(std::max<size_t>(maps.size(), 1) * 4, st);
   // pageable sources: staged before the calls return
   TSV_CUDA(cudaMemcpyAsync(d_pairs.p, pairs.data(), pairs.size() * sizeof(int2),
@@ -405,6 +426,16 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     cp.sflag = fa;
     cp.sflag_out = fb;
     cp.smap = l > 2 ? d_maps.as<int32_t>() + moff[l - 1] : nullptr;
+    if (use_items) {
+      const int K1 = k + 1;
+      cp.items = dp;  // offsets are absolute in d_pairs
+      cp.item_off = d_maps.as<int32_t>() + icoff[l];
+      cp.item_cnt = cp.item_off + K1 * K1;
+      cp.frame_multi = static_cast<int>(T.count[l - 1]);
+      cp.frame_single = static_cast<int>(T.count[l - 1] * (k - l + 1) / k);  // C(k-1, l-1)
+      cp.frame_max = sh->multi ? cp.frame_multi : cp.frame_single;
+      cp.warp_words = tsv::GfTable::kWords + (cp.frame_max + 31) / 32 * 32;
+    }
     if (vc) {
       cp.vc_color = vc->d_colors;
       cp.vc_head = vc->order[l - 1];
@@ -412,14 +443,19 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
       cp.vc_wild = vc->wild;
     }
     if (!cp.last) TSV_CUDA(cudaMemsetAsync(fb, 0, S, st));
-    for (int e0 = 0; e0 < cp.E; e0 += tsv::kCoefSlice) {
-      cp.e0 = e0;
-      cp.ne = std::min(tsv::kCoefSlice, cp.E - e0);
-      tsv::launch_coef_arcs(cp, st);
+    if (use_items) {
+      tsv::launch_coef_items(cp, st);
+    } else {
+      for (int e0 = 0; e0 < cp.E; e0 += tsv::kCoefSlice) {
+        cp.e0 = e0;
+        cp.ne = std::min(tsv::kCoefSlice, cp.E - e0);
+        tsv::launch_coef_arcs(cp, st);
+      }
     }
     if (cp.last) {
       tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k],
-                               scale, d_acc, st);
+                               scale, use_items ? cp.vsh : nullptr,
+                               use_items ? cp.vsv : nullptr, d_acc, st);
     } else {
       tsv::launch_coef_fixup(cp, st);
       tsv::launch_coef_ztrans(g->dev.S, static_cast<int>(T.count[l]), l,
@@ -1018,10 +1054,18 @@ int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
 #pragma omp parallel for schedule(static) reduction(| : bad_shade)
     for (int64_t i = 0; i < cnt; ++i) bad_shade |= vertex_shades[i] < 1 || vertex_shades[i] > k;
     if (bad_shade) throw std::invalid_argument("shade id outside [1..k]");
+    int64_t single = 0, multi = 0;
+#pragma omp parallel for schedule(static) reduction(+ : single, multi)
+    for (int32_t i = 0; i < n; ++i) {
+      single += vertex_off[i + 1] - vertex_off[i] == 1;
+      multi += vertex_off[i + 1] - vertex_off[i] > 1;
+    }
     DeviceGuard dg(g->device);
     auto* s = new tsv_shades();
     s->k = k;
     s->n = n;
+    s->single = single;
+    s->multi = multi;
     s->device = g->device;
     try {
       // pool allocations (cudaMalloc costs ~0.1 ms per call); the copies from
