@@ -161,28 +161,6 @@ void prof_end(cudaStream_t st) {
 
 }  // namespace tsv
 
-struct tsv_graph {
-  tsv::HostLayout host;  // n, t, directed, drop counts (+ canonical edges if host-built)
-  tsv::DevGraph dev;
-  int device = 0;
-  int64_t device_bytes = 0;
-  int64_t m = 0;                      // canonical edge count
-  int model = 0;                      // edge model the layout was built for
-  bool edges_in_layout = false;       // canonical edges only implied by the layout
-  int64_t arcs_with_src = 0, runs_referenced = 0;
-  const int32_t* d_eu = nullptr;      // canonical edges on the device (device build)
-  const int32_t* d_ev = nullptr;
-  const int32_t* d_ets = nullptr;
-  std::vector<void*> owned;
-  ~tsv_graph() {
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(device);
-    for (void* p : owned) cudaFree(p);
-    cudaSetDevice(prev);
-  }
-};
-
 struct tsv_shades {
   int k = 0;
   int32_t n = 0;
@@ -197,6 +175,34 @@ struct tsv_shades {
     cudaSetDevice(device);
     cudaFree(off);
     cudaFree(shades);
+    cudaSetDevice(prev);
+  }
+};
+
+struct tsv_graph {
+  tsv::HostLayout host;  // n, t, directed, drop counts (+ canonical edges if host-built)
+  tsv::DevGraph dev;
+  int device = 0;
+  int64_t device_bytes = 0;
+  int64_t m = 0;                      // canonical edge count
+  int model = 0;                      // edge model the layout was built for
+  bool edges_in_layout = false;       // canonical edges only implied by the layout
+  int64_t arcs_with_src = 0, runs_referenced = 0;
+  const int32_t* d_eu = nullptr;      // canonical edges on the device (device build)
+  const int32_t* d_ev = nullptr;
+  const int32_t* d_ets = nullptr;
+  std::vector<void*> owned;
+  // last shade table evaluated on this graph (binary-search and self-
+  // reduction probes repeat it): reused when its content fingerprint matches
+  mutable std::mutex shade_mu;
+  mutable std::shared_ptr<tsv_shades> shade_cache;
+  mutable uint64_t shade_fp = 0;
+  mutable int shade_k = 0;
+  ~tsv_graph() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (void* p : owned) cudaFree(p);
     cudaSetDevice(prev);
   }
 };
@@ -1115,8 +1121,32 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
   });
   if (rc) return rc;
-  rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
-  if (rc) return rc;
+  // content fingerprint of the shade CSR: a repeated table is not uploaded again
+  const int32_t n0 = g->host.n;
+  const int64_t cnt = vertex_off[n0];
+  uint64_t fp = tsv::mix64(static_cast<uint64_t>(k) * 0x9e3779b97f4a7c15ull ^ static_cast<uint64_t>(cnt));
+#pragma omp parallel for schedule(static) reduction(+ : fp)
+  for (int64_t i = 0; i <= n0; ++i)
+    fp += tsv::mix64(static_cast<uint64_t>(i) * 0xff51afd7ed558ccdull ^ static_cast<uint32_t>(vertex_off[i]));
+#pragma omp parallel for schedule(static) reduction(+ : fp)
+  for (int64_t i = 0; i < cnt; ++i)
+    fp += tsv::mix64(static_cast<uint64_t>(i) * 0xc4ceb9fe1a85ec53ull + 1 ^
+                     static_cast<uint32_t>(vertex_shades[i]));
+  std::shared_ptr<tsv_shades> hold;
+  {
+    std::lock_guard<std::mutex> lk(g->shade_mu);
+    if (g->shade_cache && g->shade_fp == fp && g->shade_k == k) hold = g->shade_cache;
+  }
+  if (!hold) {
+    rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
+    if (rc) return rc;
+    hold = std::shared_ptr<tsv_shades>(sh, tsv_shades_free);
+    std::lock_guard<std::mutex> lk(g->shade_mu);
+    g->shade_cache = hold;
+    g->shade_fp = fp;
+    g->shade_k = k;
+  }
+  sh = hold.get();
   rc = guard([&] {
     DeviceGuard dg(g->device);
     const int32_t n = g->host.n;
@@ -1141,7 +1171,6 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     finalize_host(n, accumulators, anchor_sink, k, out);
     out->peak_field_words = peak;
   });
-  tsv_shades_free(sh);
   return rc;
 }
 
