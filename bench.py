@@ -193,23 +193,64 @@ def config_json(inst, world, args):
 
 
 
-def coef_roofline(coef, k, info, evals, hbm, peak_kind, args, world, sm_mhz):
+def coef_alg_bytes(g, sh, k):
+    """Algorithmic bytes of one full evaluation by the coefficient engine, per
+    kernel family ("Roofline"), from the graph and the
+    shade classes: a vertex with no shade is dead, one shade d keeps the
+    (l-1)-subsets without d (frame C(k-1, l-1)), several shades keep all
+    C(k, l-1).
+      coef_arcs, middle levels 3 <= l < k: 8 B per (live arc with a
+        predecessor run, entry it carries) read -- C(k-2, l-2) for single ->
+        single shades d_t != d_h, C(k-1, l-2) single -> multi, C(k-1, l-1)
+        multi -> single, C(k, l-1) multi -> multi -- plus 8 B per (referenced
+        run of a live head, frame entry) written;
+      coef_ztrans, levels 2 <= l < k: 8 B per (referenced run of a
+        multi-shade head, C(k, l-1) entry) read + C(k, l) written."""
+    from math import comb
+    n = g.n()
+    cu, cv, ct = (np.asarray(x, dtype=np.int64) for x in g.edges())
+    if not g.directed():
+        cu, cv, ct = np.concatenate([cu, cv]), np.concatenate([cv, cu]), np.concatenate([ct, ct])
+    cnt = np.diff(np.asarray(sh.vertex_off, dtype=np.int64))
+    d1 = np.full(n, -1, np.int64)
+    one = cnt == 1
+    d1[one] = np.asarray(sh.vertex_shades, dtype=np.int64)[np.asarray(sh.vertex_off)[:-1][one]]
+    multi = cnt >= 2
+    # predecessor run: the tail has an in-arc with an earlier timestamp
+    first_in = np.full(n, np.iinfo(np.int64).max, np.int64)
+    np.minimum.at(first_in, cv, ct)
+    live = (cnt[cu] > 0) & (cnt[cv] > 0) & (first_in[cu] < ct)
+    tu, hv = cu[live], cv[live]
+    ss = one[tu] & one[hv] & (d1[tu] != d1[hv])
+    sm = one[tu] & multi[hv]
+    ms = multi[tu] & one[hv]
+    mm = multi[tu] & multi[hv]
+    n_ss, n_sm, n_ms, n_mm = (int(x.sum()) for x in (ss, sm, ms, mm))
+    # referenced runs (tail, its last in-timestamp < ts) of live heads
+    key_in = np.unique(cv * (1 << 32) + ct)          # runs (head, ts), sorted
+    q = cu * (1 << 32) + ct                           # an arc's source lies before (tail, ts)
+    pos = np.searchsorted(key_in, q, side="left") - 1
+    ok = (pos >= 0) & (cnt[cu] > 0)
+    src = key_in[np.clip(pos, 0, None)]
+    ok &= (src >> 32) == cu
+    ref = np.unique(src[ok])
+    rh = ref >> 32
+    r_single, r_multi = int(one[rh].sum()), int(multi[rh].sum())
+    arcs = sum(8 * (n_ss * comb(k - 2, l - 2) + n_sm * comb(k - 1, l - 2) +
+                    n_ms * comb(k - 1, l - 1) + n_mm * comb(k, l - 1) +
+                    r_single * comb(k - 1, l - 1) + r_multi * comb(k, l - 1))
+               for l in range(3, k))
+    ztrans = sum(8 * r_multi * (comb(k, l - 1) + comb(k, l)) for l in range(2, k))
+    return {"coef_arcs": arcs, "coef_ztrans": ztrans}
+
+
+def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
     """Roofline of the coefficient engine's dominant kernel.
 
-    Algorithmic bytes, per evaluation:
-      k_coef_arcs, middle levels 3 <= l < k: 16 B per (arc, input entry) --
-        one 8-B read of S_{l-1}[src][T'] and one 8-B U write, the point
-        engine's SURVEY 8(d) figure with sieve points replaced by the
-        C(k, l-1) coefficient entries an arc carries;
-      k_coef_ztrans, levels 2 <= l < k: 8 B per (state slot, input entry)
-        read + 8 B per (state slot, output entry) written.
-    achieved = those bytes / the kernel's CUDA-event time in the bench's
-    profile pass; int_pipe from the committed ncu capture of the same kernel."""
-    from math import comb
-    A, S = info.arcs, info.runs_referenced
-    alg = {"coef_arcs": evals * sum(16 * A * comb(k, l - 1) for l in range(3, k)),
-           "coef_ztrans": evals * sum(8 * S * (comb(k, l - 1) + comb(k, l))
-                                      for l in range(2, k))}
+    alg1 = coef_alg_bytes() of one evaluation; achieved = those bytes x the
+    evaluations of the profile pass / the kernel family's CUDA-event time in
+    that pass; int_pipe from the committed ncu capture of the same kernel."""
+    alg = {nm: evals * b for nm, b in alg1.items()}
     name = max(coef, key=lambda nm: coef[nm][1])
     n_launch, tot_ms = coef[name]
     if not n_launch or not alg[name]:
@@ -217,7 +258,7 @@ def coef_roofline(coef, k, info, evals, hbm, peak_kind, args, world, sm_mhz):
     achieved = alg[name] / (tot_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
-            "kernel": {"coef_arcs": "k_coef_arcs (3 <= l < k)",
+            "kernel": {"coef_arcs": "k_coef_items / k_coef_arcs (3 <= l < k)",
                        "coef_ztrans": "k_coef_ztrans_tab (2 <= l < k)"}[name],
             "engine": "coefficient (top-degree) form, DESIGN.md 6b",
             "avg_launch_ms": tot_ms / n_launch,
@@ -378,7 +419,7 @@ def main():
     # full-range evaluations in the profile pass (the coefficient engine's)
     evals = sum(1 for _, a, b in work if a == 0 and b == P) * prof_steps
     if any(c for c, _ in coef.values()):
-        roof = coef_roofline(coef, k, g.info, evals, hbm, peak_kind, args, world,
+        roof = coef_roofline(coef, k, coef_alg_bytes(g, sh, k), evals, hbm, peak_kind, args, world,
                              clk.summary().get("sm_mhz"))
     elif lvl_n:
         # updates executed by the middle-level launches (3 <= l < k when level

@@ -308,6 +308,77 @@ struct VcSpec {
   int32_t wild = -1;                  // wildcard color, -1 = none
 };
 
+// Subset-index tables of the coefficient engine for one k (host).
+const tsv::CoefTables& coef_const_tables(int k) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<tsv::CoefTables>> tabs(31);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!tabs[k]) tabs[k] = std::make_unique<tsv::CoefTables>(tsv::coef_tables(k));
+  return *tabs[k];
+}
+
+// Device copies of the index tables (they depend on k and the arc kernel
+// only): built and uploaded once per (device, k, kernel) for the process, so
+// an evaluation issues no pageable host->device copy (a pageable copy stalls
+// the host and serialises the streams of concurrent evaluations).
+struct CoefConst {
+  int2* pairs = nullptr;      // pairs (readout), jpairs (z map), items
+  int32_t* maps = nullptr;    // smap, item offsets/counts
+  uint64_t* ident = nullptr;  // k x k identity (w of the shade basis)
+  std::vector<size_t> poff, joff, moff, icoff;
+};
+const CoefConst& coef_const(int dev, int k, bool items) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<CoefConst>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  const size_t key = (static_cast<size_t>(dev) * 31 + k) * 2 + (items ? 1 : 0);
+  if (cache.size() <= key) cache.resize(key + 1);
+  if (cache[key]) return *cache[key];
+  const tsv::CoefTables& T = coef_const_tables(k);
+  auto c = std::make_unique<CoefConst>();
+  std::vector<int2> pairs;
+  c->poff.assign(static_cast<size_t>(k) + 1, 0);
+  c->joff = c->moff = c->icoff = c->poff;
+  for (int l = 2; l <= k; ++l) {
+    c->poff[l] = pairs.size();
+    pairs.insert(pairs.end(), T.pairs[l].begin(), T.pairs[l].end());
+  }
+  for (int l = 2; l <= k; ++l) {
+    c->joff[l] = pairs.size();
+    pairs.insert(pairs.end(), T.jpairs[l].begin(), T.jpairs[l].end());
+  }
+  std::vector<int32_t> maps;
+  for (int l = 2; l <= k; ++l) {
+    c->moff[l] = maps.size();
+    maps.insert(maps.end(), T.smap[l].begin(), T.smap[l].end());
+  }
+  if (items) {
+    for (int l = 2; l <= k; ++l) {
+      tsv::CoefItems ci = tsv::coef_items(k, l);
+      for (int32_t& o : ci.off) o += static_cast<int32_t>(pairs.size());  // absolute
+      pairs.insert(pairs.end(), ci.items.begin(), ci.items.end());
+      c->icoff[l] = maps.size();
+      maps.insert(maps.end(), ci.off.begin(), ci.off.end());
+      maps.insert(maps.end(), ci.cnt.begin(), ci.cnt.end());
+    }
+  }
+  std::vector<uint64_t> I(static_cast<size_t>(k) * k, 0);
+  for (int d = 0; d < k; ++d) I[static_cast<size_t>(d) * k + d] = 1;
+  int cur = 0;
+  TSV_CUDA(cudaGetDevice(&cur));
+  TSV_CUDA(cudaSetDevice(dev));
+  TSV_CUDA(cudaMalloc(&c->pairs, std::max<size_t>(pairs.size(), 1) * sizeof(int2)));
+  TSV_CUDA(cudaMalloc(&c->maps, std::max<size_t>(maps.size(), 1) * 4));
+  TSV_CUDA(cudaMalloc(&c->ident, I.size() * 8));
+  TSV_CUDA(cudaMemcpy(c->pairs, pairs.data(), pairs.size() * sizeof(int2),
+                      cudaMemcpyHostToDevice));
+  TSV_CUDA(cudaMemcpy(c->maps, maps.data(), maps.size() * 4, cudaMemcpyHostToDevice));
+  TSV_CUDA(cudaMemcpy(c->ident, I.data(), I.size() * 8, cudaMemcpyHostToDevice));
+  TSV_CUDA(cudaSetDevice(cur));
+  cache[key] = std::move(c);
+  return *cache[key];
+}
+
 // The coefficient (top-degree) engine, coef_kernels.cu: the XOR over ALL
 // 2^k sieve points in one pass per level, bit-identical to the point engine.
 // Used for full-range evaluations when its working set (two S x M state
@@ -319,7 +390,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const char* eng = std::getenv("TSV_ENGINE");
   if (eng && std::strcmp(eng, "points") == 0) return false;
   if (k < 2 || k > 12) return false;  // C(k, l) <= tsv::kZAcc
-  const tsv::CoefTables T = tsv::coef_tables(k);
+  const tsv::CoefTables& T = coef_const_tables(k);
   int64_t M = 1;
   for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, T.count[l]);
   const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
@@ -338,21 +409,18 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   // with the identity for w) and the readout multiplies by det(W) = per(W)
   // (char 2).  Vertex-ordered sieves keep their positional z_{u,j}.
   uint64_t scale = 1;
-  DevBuf d_w(static_cast<size_t>(k) * k * 8, st), d_zj(static_cast<size_t>(n) * k * 8, st);
+  DevBuf d_zj(static_cast<size_t>(n) * k * 8, st);
   if (vc) {
     tsv::launch_zj_positional(nn, k, cfg->seed, d_zj.as<uint64_t>(), st);
   } else {
-    std::vector<uint64_t> W(static_cast<size_t>(k) * k), I(static_cast<size_t>(k) * k, 0);
+    std::vector<uint64_t> W(static_cast<size_t>(k) * k);
     const uint64_t pre = tsv::draw_prefix(cfg->seed, tsv::kRoleShadeW);
     for (int d = 0; d < k; ++d) {
-      I[static_cast<size_t>(d) * k + d] = 1;
       for (int j = 0; j < k; ++j)
         W[static_cast<size_t>(d) * k + j] = tsv::draw_nonzero_from(pre, d + 1, j + 1, 0);
     }
     scale = tsv::gf_det_host(W.data(), k);
-    // pageable source: staged before the call returns
-    TSV_CUDA(cudaMemcpyAsync(d_w.p, I.data(), I.size() * 8, cudaMemcpyHostToDevice, st));
-    tsv::launch_zj(nn, k, cfg->seed, sh->off, sh->shades, d_w.as<uint64_t>(),
+    tsv::launch_zj(nn, k, cfg->seed, sh->off, sh->shades, coef_const(dev, k, false).ident,
                    d_zj.as<uint64_t>(), st);
   }
   DevBuf X(S * M * 8, st), Y(S * M * 8, st), agg(C * M * 8, st);
@@ -363,23 +431,6 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   DevBuf fl0(S, st), fl1(S, st);
   if (!vc) tsv::launch_vshade(nn, k, d_zj.as<uint64_t>(), vsh.as<int8_t>(), vsv.as<uint64_t>(), st);
   TSV_CUDA(cudaMemsetAsync(ulast.p, 0, std::max<uint64_t>(n, 1) * k * 8, st));
-  // host tables, one upload: pairs (readout), jpairs (z map), smap
-  std::vector<int2> pairs;
-  std::vector<size_t> poff(static_cast<size_t>(k) + 1, 0), joff = poff;
-  for (int l = 2; l <= k; ++l) {
-    poff[l] = pairs.size();
-    pairs.insert(pairs.end(), T.pairs[l].begin(), T.pairs[l].end());
-  }
-  for (int l = 2; l <= k; ++l) {
-    joff[l] = pairs.size();
-    pairs.insert(pairs.end(), T.jpairs[l].begin(), T.jpairs[l].end());
-  }
-  std::vector<int32_t> maps;
-  std::vector<size_t> moff(static_cast<size_t>(k) + 1, 0);
-  for (int l = 2; l <= k; ++l) {
-    moff[l] = maps.size();
-    maps.insert(maps.end(), T.smap[l].begin(), T.smap[l].end());
-  }
   // item-stream kernel (coef_items.cu) unless the vertex-ordered sieve's
   // positional z (no shade structure) or TSV_ITEMS=0
   const char* it_env = std::getenv("TSV_ITEMS");
@@ -387,25 +438,11 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   // vertex, 1.2x slower than k_coef_arcs)
   const bool use_items = !vc && !(it_env && std::strcmp(it_env, "0") == 0) &&
                          ((it_env && std::strcmp(it_env, "1") == 0) || sh->single * 4 >= n);
-  std::vector<size_t> ioff(static_cast<size_t>(k) + 1, 0), icoff = ioff;
-  if (use_items) {
-    for (int l = 2; l <= k; ++l) {
-      tsv::CoefItems ci = tsv::coef_items(k, l);
-      for (int32_t& o : ci.off) o += static_cast<int32_t>(pairs.size());  // absolute
-      ioff[l] = pairs.size();
-      pairs.insert(pairs.end(), ci.items.begin(), ci.items.end());
-      icoff[l] = maps.size();
-      maps.insert(maps.end(), ci.off.begin(), ci.off.end());
-      maps.insert(maps.end(), ci.cnt.begin(), ci.cnt.end());
-    }
-  }
-  DevBuf d_pairs(pairs.size() * sizeof(int2), st), d_maps(std::max<size_t>(maps.size(), 1) * 4, st);
-  // pageable sources: staged before the calls return
-  TSV_CUDA(cudaMemcpyAsync(d_pairs.p, pairs.data(), pairs.size() * sizeof(int2),
-                           cudaMemcpyHostToDevice, st));
-  TSV_CUDA(cudaMemcpyAsync(d_maps.p, maps.data(), maps.size() * 4, cudaMemcpyHostToDevice, st));
+  // the index tables depend on (k, use_items) only: uploaded once per device
+  const CoefConst& cc = coef_const(dev, k, use_items);
+  const std::vector<size_t>&poff = cc.poff, &joff = cc.joff, &moff = cc.moff, &icoff = cc.icoff;
   tsv::launch_slot_head(g->dev.R, g->dev.run_slot, g->dev.run_head, slot_head.as<int32_t>(), st);
-  const int2* dp = d_pairs.as<int2>();
+  const int2* dp = cc.pairs;
   // row strides: level l's rows hold its U row (C(k, l-1)) and then its S row (C(k, l))
   auto rs = [&](int l) { return static_cast<int>(std::max(T.count[l - 1], T.count[l])); };
   uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
@@ -431,11 +468,11 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     cp.vsv = vc ? nullptr : vsv.as<uint64_t>();
     cp.sflag = fa;
     cp.sflag_out = fb;
-    cp.smap = l > 2 ? d_maps.as<int32_t>() + moff[l - 1] : nullptr;
+    cp.smap = l > 2 ? cc.maps + moff[l - 1] : nullptr;
     if (use_items) {
       const int K1 = k + 1;
       cp.items = dp;  // offsets are absolute in d_pairs
-      cp.item_off = d_maps.as<int32_t>() + icoff[l];
+      cp.item_off = cc.maps + icoff[l];
       cp.item_cnt = cp.item_off + K1 * K1;
       cp.frame_multi = static_cast<int>(T.count[l - 1]);
       cp.frame_single = static_cast<int>(T.count[l - 1] * (k - l + 1) / k);  // C(k-1, l-1)

@@ -36,6 +36,11 @@ def family(name):
         first = m.group(3) in ("1", "true")
         last = m.group(4) in ("1", "true")
         return "coef_arcs_first" if first else "coef_arcs_last" if last else "coef_arcs"
+    m = re.search(r"k_coef_items<(\w+), (\w+), (\d+)>", name)
+    if m:
+        first = m.group(1) in ("1", "true")
+        last = m.group(2) in ("1", "true")
+        return "coef_arcs_first" if first else "coef_arcs_last" if last else "coef_arcs"
     for f in ("k_coef_ztrans_tab", "k_coef_ztrans", "k_coef_readout", "k_coef_fixup"):
         if f in name:
             return {"k_coef_ztrans_tab": "coef_ztrans"}.get(f, f[2:])
