@@ -298,8 +298,9 @@ def main():
     ap.add_argument("--points-per-batch", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--streams", type=int, default=2,
-                    help="concurrent CUDA streams for the repetitions of a step")
+    ap.add_argument("--streams", type=int, default=4,
+                    help="concurrent CUDA streams for the repetitions of a step "
+                         "(at most one per work unit)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -342,7 +343,7 @@ def main():
 
     # repetitions (independent evaluations) may run on concurrent streams so
     # one evaluation's tail wave overlaps the next one's launches
-    side = [torch.cuda.Stream() for _ in range(max(1, args.streams) - 1)]
+    side = [torch.cuda.Stream() for _ in range(max(1, min(args.streams, len(work))) - 1)]
 
     def step(concurrent=True):
         acc.zero_()

@@ -72,6 +72,14 @@ CoefItems coef_items(int k, int l);
 void launch_coef_ztrans(int64_t S, int F, int l, const int32_t* slot_head, const uint64_t* zj,
                         int k, int E, uint64_t* rows, int rs, const int2* jpairs,
                         const int8_t* vsh, uint8_t* sflag, int sm_count, cudaStream_t st);
+// Direct form (k_coef_ztrans_direct): one thread per (listed row, T),
+// general products, over the (slot, head) list of k_multi_slots.
+void launch_multi_slots(int64_t R, const int32_t* run_slot, const int32_t* run_head,
+                        const int8_t* vsh, int2* list, int32_t* count, cudaStream_t st);
+void launch_coef_ztrans_direct(int64_t S, int F, int l, const int2* list, const int32_t* count,
+                               const uint64_t* zj, int k, uint64_t* rows, int rs,
+                               const int2* pairs, const uint8_t* sflag, int sm_count,
+                               cudaStream_t st);
 constexpr int kZAcc = 1024;  // largest F the in-place z map handles (k <= 12)
 // vsh / vsv of the rows of the n x k shade table (CoefParams)
 void launch_vshade(int32_t n, int k, const uint64_t* rows, int8_t* vsh, uint64_t* vsv,

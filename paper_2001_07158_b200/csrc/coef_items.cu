@@ -29,6 +29,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <utility>
+#include <vector>
 
 #include "coef.hpp"
 #include "gf_device.cuh"
@@ -294,6 +299,234 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items(const CoefParams P) {
   }
 }
 
+
+// Small frames (frame_max <= 32 * NO, i.e. k <= 7): the same item stream,
+// but a batch's products are first stored to per-arc rows in shared memory
+// (prow[arc][entry]; items of one arc have distinct outputs, so a plain
+// store) and the head prefixes are then walked arc by arc with lane o
+// holding entry o (and o + 32) of the prefix in registers.  The walk visits
+// only the arcs with an event (vertex start, live products, referenced run
+// end), taken from warp ballots, and needs no shared accumulator or
+// per-arc warp barrier: the serial part of k_coef_items costs ~10
+// instructions per event instead of ~40.
+template <bool FIRST, bool LAST, int NO>
+__global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P, int fmp) {
+  extern __shared__ uint64_t dsm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  uint64_t* const prow = dsm + static_cast<size_t>(wib) * 32 * fmp;
+  __shared__ uint32_t s_ys[kIW][12][32];
+  __shared__ int64_t s_row[kIW][32];   // source row offset (-1: the value 1)
+  __shared__ int32_t s_start[kIW][33]; // item stream offsets of the live arcs
+  __shared__ int32_t s_poff[kIW][32];  // item list offset
+  __shared__ int8_t s_lane[kIW][32];   // the live arc's lane (its prow row)
+
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kIW + wib;
+  if (c >= P.g.C) return;  // warp-uniform
+  const int k = P.k;
+  const int fm = P.frame_max;
+  const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
+  const uint64_t yb = static_cast<uint64_t>(P.ell - 1) + 0x165667b19e3779f9ull;
+  const int64_t a0 = P.g.chunk_arc[c], a1 = P.g.chunk_arc[c + 1];
+  int32_t run_ctr = P.g.chunk_run[c];
+  int frame = fm;  // frame of the current head
+  uint64_t acc0 = 0, acc1 = 0;  // prefix entries lane, lane + 32
+
+  for (int64_t base = a0; base < a1; base += 32) {
+    const int nb = static_cast<int>(a1 - base < 32 ? a1 - base : 32);
+    uint32_t meta = 0;
+    int32_t sidx = -1, head = -1, tail = -1;
+    uint64_t y = 0;
+    if (lane < nb) {
+      meta = __ldg(P.g.arc_meta + base + lane);
+      sidx = FIRST ? __ldg(P.g.arc_tail + base + lane) : __ldg(P.g.arc_src + base + lane);
+      tail = FIRST ? sidx : __ldg(P.g.arc_tail + base + lane);
+    }
+    const unsigned ends = __ballot_sync(kFull, lane < nb && (meta & kRunEnd));
+    const int32_t myrun = run_ctr + __popc(ends & ((1u << lane) - 1u));
+    run_ctr += __popc(ends);
+    if (lane < nb) head = __ldg(P.g.run_head + myrun);
+    const int hs = lane < nb ? __ldg(P.vsh + head) : -1;  // head shade class
+    bool live = lane < nb && sidx >= 0 && hs != -1;
+    if (FIRST) live = live && (P.anchor_source < 0 || sidx == P.anchor_source);
+    if (LAST) live = live && __ldg(P.g.run_ts + myrun) <= P.max_ts;
+    int ts = -1;
+    if (live) {
+      ts = __ldg(P.vsh + tail);
+      live = ts != -1 && (FIRST || __ldg(P.sflag + sidx) != 0);
+    }
+    int nitem = 0, poff = 0;
+    if (live) {
+      const int pt = (ts >= 0 ? ts : k) * (k + 1) + (hs >= 0 ? hs : k);
+      nitem = __ldg(P.item_cnt + pt);
+      poff = __ldg(P.item_off + pt);
+      live = nitem > 0;
+      if (!live) nitem = 0;
+    }
+    if (live) y = draw_edge_y(pre, yb, meta & kEdgeMask);
+    if (live && ts >= 0) y = gf_mul(y, __ldg(P.vsv + tail));  // v_tail rides on y
+    bool push;
+    int32_t dst = -1;
+    if (LAST) {  // last arc of its vertex within this chunk: flush the piece
+      const bool chunk_end = base + lane + 1 >= a1;
+      uint32_t nmeta = __shfl_down_sync(kFull, meta, 1);
+      if (lane == 31 && !chunk_end) nmeta = __ldg(P.g.arc_meta + base + 32);
+      push = lane < nb && hs != -1 && (chunk_end || (nmeta & kVStart));
+      dst = head;
+    } else {
+      dst = (lane < nb && hs != -1 && (meta & kRunEnd)) ? __ldg(P.g.run_slot + myrun) : -1;
+      push = dst >= 0;
+    }
+    const int myfr = hs >= 0 ? P.frame_single : P.frame_multi;
+    const unsigned vstm = __ballot_sync(kFull, lane < nb && (meta & kVStart));
+    const unsigned livem = __ballot_sync(kFull, live);
+    const unsigned pushm = __ballot_sync(kFull, push);
+
+    // compact the live arcs; exclusive scan of their item counts
+    int incl = nitem;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(kFull, incl, d);
+      if (lane >= d) incl += o;
+    }
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int nlive = __popc(livem);
+    __syncwarp();  // the previous batch's readers of the staging arrays are done
+    if (live) {
+      const int ai = __popc(livem & ((1u << lane) - 1u));
+      s_start[wib][ai] = incl - nitem;
+      s_poff[wib][ai] = poff;
+      s_lane[wib][ai] = static_cast<int8_t>(lane);
+      s_row[wib][ai] = FIRST ? (ts >= 0 ? -1 : static_cast<int64_t>(sidx) * k)
+                             : static_cast<int64_t>(sidx) * P.rs_in;
+      const KSplit ks = ksplit(y);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s_ys[wib][j][ai] = ks.l.c[j];
+        s_ys[wib][4 + j][ai] = ks.h.c[j];
+        s_ys[wib][8 + j][ai] = ks.m.c[j];
+      }
+    }
+    // rows of the live arcs start at zero (entries no item of the arc reaches)
+    {
+      unsigned m = livem;
+      while (m) {
+        const int a = __ffs(m) - 1;
+        m &= m - 1;
+        for (int o = lane; o < fm; o += 32) prow[a * fmp + o] = 0;
+      }
+    }
+    if (lane == 0) s_start[wib][nlive] = total;
+    __syncwarp();
+
+    // item q -> live arc j with s_start[j] <= q < s_start[j + 1]
+    for (int q0 = 0; q0 < total; q0 += 64) {
+      int jj[2], out[2];
+      uint64_t u[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int q = q0 + 32 * r + lane;
+        jj[r] = -1;
+        out[r] = 0;
+        u[r] = 0;
+        if (q < total) {
+          int j = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1)
+            if (j + st < nlive && s_start[wib][j + st] <= q) j += st;
+          jj[r] = j;
+          const int2 it = __ldg(P.items + s_poff[wib][j] + (q - s_start[wib][j]));
+          out[r] = it.y;
+          const int64_t row = s_row[wib][j];
+          u[r] = row < 0 ? 1ull : FIRST ? __ldg(P.zj + row + it.x) : __ldg(P.s_prev + row + it.x);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        if (jj[r] >= 0 && u[r]) {
+          const int j = jj[r];
+          KSplit ys;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            ys.l.c[i] = s_ys[wib][i][j];
+            ys.h.c[i] = s_ys[wib][4 + i][j];
+            ys.m.c[i] = s_ys[wib][8 + i][j];
+          }
+          prow[s_lane[wib][j] * fmp + out[r]] = gf_mul_presplit(ys, u[r]);
+        }
+      }
+    }
+    __syncwarp();
+
+    // walk the arcs with events in stream order
+    unsigned ev = vstm | livem | pushm;
+    while (ev) {
+      const int a = __ffs(ev) - 1;
+      ev &= ev - 1;
+      const unsigned bit = 1u << a;
+      if (vstm & bit) {
+        acc0 = 0;
+        if (NO > 1) acc1 = 0;
+        frame = __shfl_sync(kFull, myfr, a);
+      }
+      if (livem & bit) {
+        if (lane < fm) acc0 ^= prow[a * fmp + lane];
+        if (NO > 1 && lane + 32 < fm) acc1 ^= prow[a * fmp + 32 + lane];
+      }
+      if (pushm & bit) {
+        const int32_t d = __shfl_sync(kFull, dst, a);
+        const int fr = __shfl_sync(kFull, myfr, a);
+        if (LAST) {
+          uint64_t* up = P.ulast + static_cast<int64_t>(d) * k;
+          if (lane < fr && acc0)
+            atomicXor(reinterpret_cast<unsigned long long*>(up + lane),
+                      static_cast<unsigned long long>(acc0));
+          if (NO > 1 && lane + 32 < fr && acc1)
+            atomicXor(reinterpret_cast<unsigned long long*>(up + 32 + lane),
+                      static_cast<unsigned long long>(acc1));
+        } else {
+          uint64_t* rowp = P.ubuf + static_cast<int64_t>(d) * P.rs_out;
+          bool nz = false;
+          if (lane < fr) {
+            rowp[lane] = acc0;
+            nz = acc0 != 0;
+          }
+          if (NO > 1 && lane + 32 < fr) {
+            rowp[32 + lane] = acc1;
+            nz = nz || acc1 != 0;
+          }
+          if (__any_sync(kFull, nz) && lane == 0) P.sflag_out[d] = 1;
+        }
+      }
+    }
+  }
+  if (!LAST) {  // chunk tail prefix for k_coef_fixup (frame of the last vertex)
+    if (lane < frame) P.agg[c * P.E + lane] = acc0;
+    if (NO > 1 && lane + 32 < frame) P.agg[c * P.E + 32 + lane] = acc1;
+  }
+}
+
+// Opt a kernel into `bytes` of dynamic shared memory (raised only, per
+// kernel and device).
+void allow_smem(const void* f, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_pair(f, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& d : done)
+    if (d.first == key) {
+      if (bytes > d.second) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+        d.second = bytes;
+      }
+      return;
+    }
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  done.emplace_back(key, bytes);
+}
+
 }  // namespace
 
 void launch_coef_items(const CoefParams& p, cudaStream_t st) {
@@ -301,16 +534,33 @@ void launch_coef_items(const CoefParams& p, cudaStream_t st) {
   prof_begin(p.last ? "coef_arcs_last" : p.ell == 2 ? "coef_arcs_first" : "coef_arcs", st);
   const size_t smem = static_cast<size_t>(kIW) * p.warp_words * 8 + 256;
   const unsigned blocks = static_cast<unsigned>((p.g.C + kIW - 1) / kIW);
+  // (every instantiation has the same signature, so a static inside the
+  // generic lambda would be shared by all of them: keep the size per kernel)
   auto go = [&](auto kern) {
-    static size_t configured = 0;
-    if (smem > configured) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
-      configured = smem;
-    }
+    allow_smem(reinterpret_cast<const void*>(kern), smem);
     kern<<<blocks, kIW * 32, smem, st>>>(p);
   };
   const bool first = p.ell == 2, last = p.last;
+  const char* reg_env = std::getenv("TSV_ITEMS_REG");
+  if (p.frame_max <= 64 && !(reg_env && std::strcmp(reg_env, "0") == 0)) {
+    const int fmp = p.frame_max | 1;  // odd row stride: conflict-free 8-byte column reads
+    const size_t rsm = static_cast<size_t>(kIW) * 32 * fmp * 8;
+    auto go2 = [&](auto kern) {
+      allow_smem(reinterpret_cast<const void*>(kern), rsm);
+      kern<<<blocks, kIW * 32, rsm, st>>>(p, fmp);
+    };
+    const bool two = p.frame_max > 32;
+    if (first && last)
+      two ? go2(k_coef_items_reg<true, true, 2>) : go2(k_coef_items_reg<true, true, 1>);
+    else if (first)
+      two ? go2(k_coef_items_reg<true, false, 2>) : go2(k_coef_items_reg<true, false, 1>);
+    else if (last)
+      two ? go2(k_coef_items_reg<false, true, 2>) : go2(k_coef_items_reg<false, true, 1>);
+    else
+      two ? go2(k_coef_items_reg<false, false, 2>) : go2(k_coef_items_reg<false, false, 1>);
+    prof_end(st);
+    return;
+  }
   // items of a single -> single arc: C(k-2, ell-2)
   const int64_t ss = static_cast<int64_t>(p.frame_single) * (p.ell - 1) / (p.k - 1);
   const bool deep = ss >= 32 || (p.frame_max == p.frame_multi && p.frame_multi >= 64);

@@ -480,6 +480,92 @@ __global__ void k_slot_head(int64_t R, const int32_t* __restrict__ run_slot,
   if (s >= 0) slot_head[s] = run_head[r];
 }
 
+
+// Multi-shade rows (or every row with positional z) in a compact list of
+// (slot, head), built once per evaluation: the direct z map below then runs
+// over exactly the rows it transforms (C2: 1/8 of the state slots).
+__global__ void k_multi_slots(int64_t R, const int32_t* __restrict__ run_slot,
+                              const int32_t* __restrict__ run_head,
+                              const int8_t* __restrict__ vsh, int2* __restrict__ list,
+                              int32_t* __restrict__ count) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int32_t s = -1, h = -1;
+  if (r < R) {
+    s = run_slot[r];
+    if (s >= 0) {
+      h = run_head[r];
+      if (vsh && __ldg(vsh + h) != -2) s = -1;
+    }
+  }
+  const unsigned m = __ballot_sync(kFull, s >= 0);
+  if (!m) return;
+  int base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(kFull, base, __ffs(m) - 1);
+  if (s >= 0) list[base + __popc(m & ((1u << lane) - 1u))] = make_int2(s, h);
+}
+
+// Direct z map of the listed rows, in place: S_l[slot][T] =
+// XOR_{j in T} z_{head,j} * U_l[slot][T - {j}] (pairs of level l: for each
+// l-subset T its l pairs (rank of T - {j}, j)).  A block takes a tile of
+// rows, forms every entry of the tile in shared memory (one thread per
+// (row, T), general products), then -- after all of the tile's U entries
+// are read -- writes the tile back.  Rows whose U is zero (sflag clear) are
+// skipped: their S is zero and no arc reads them (the arc kernels test the
+// flag whenever zero skipping is on; sflag = nullptr transforms every row,
+// as the vertex-ordered sieve's arcs read rows without the test).
+constexpr int kZdThreads = 256;
+constexpr int kZdWords = 2048;  // shared output words per tile
+__global__ void __launch_bounds__(kZdThreads)
+    k_coef_ztrans_direct(const int2* __restrict__ list, const int32_t* __restrict__ count,
+                         int F, int l, int spt, const uint64_t* __restrict__ zj, int k,
+                         uint64_t* rows, int rs, const int2* __restrict__ pairs,
+                         const uint8_t* __restrict__ sflag) {
+  __shared__ uint64_t out[kZdWords];
+  __shared__ int2 tile[kZdWords / 2];  // F >= 2 below level k
+  const int64_t nrows = *count;
+  const int64_t ntiles = (nrows + spt - 1) / spt;
+  const float invF = 1.0f / static_cast<float>(F);
+  for (int64_t tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+    const int64_t r0 = tl * spt;
+    const int nr = static_cast<int>(nrows - r0 < spt ? nrows - r0 : spt);
+    for (int i = threadIdx.x; i < nr; i += kZdThreads) {
+      int2 e = list[r0 + i];
+      if (sflag && !sflag[e.x]) e.x = -1;
+      tile[i] = e;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * F; i += kZdThreads) {
+      int q = __float2int_rz(static_cast<float>(i) * invF);
+      if ((q + 1) * F <= i) ++q;
+      if (q * F > i) --q;
+      const int2 e = tile[q];
+      if (e.x < 0) continue;
+      const int t = i - q * F;
+      const uint64_t* U = rows + static_cast<int64_t>(e.x) * rs;
+      const uint64_t* z = zj + static_cast<int64_t>(e.y) * k;
+      uint64_t r = 0;
+      for (int c = 0; c < l; ++c) {
+        const int2 pr = __ldg(pairs + t * l + c);
+        const uint64_t u = U[pr.x];
+        const uint64_t zv = __ldg(z + pr.y);
+        if (u && zv) r ^= gf_mul(zv, u);
+      }
+      out[i] = r;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * F; i += kZdThreads) {
+      int q = __float2int_rz(static_cast<float>(i) * invF);
+      if ((q + 1) * F <= i) ++q;
+      if (q * F > i) --q;
+      const int2 e = tile[q];
+      if (e.x >= 0) rows[static_cast<int64_t>(e.x) * rs + (i - q * F)] = out[i];
+    }
+    __syncthreads();
+  }
+}
+
 template <int LG, int PPT>
 void arcs_dispatch(const CoefParams& p, cudaStream_t st) {
   const unsigned blocks = static_cast<unsigned>((p.g.C + kCoefWarps - 1) / kCoefWarps);
@@ -665,6 +751,32 @@ void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_hea
   if (R == 0) return;
   k_slot_head<<<static_cast<unsigned>((R + 255) / 256), 256, 0, st>>>(R, run_slot, run_head,
                                                                        slot_head);
+}
+
+void launch_multi_slots(int64_t R, const int32_t* run_slot, const int32_t* run_head,
+                        const int8_t* vsh, int2* list, int32_t* count, cudaStream_t st) {
+  cudaMemsetAsync(count, 0, 4, st);
+  if (R == 0) return;
+  k_multi_slots<<<static_cast<unsigned>((R + 255) / 256), 256, 0, st>>>(R, run_slot, run_head,
+                                                                         vsh, list, count);
+}
+
+void launch_coef_ztrans_direct(int64_t S, int F, int l, const int2* list, const int32_t* count,
+                               const uint64_t* zj, int k, uint64_t* rows, int rs,
+                               const int2* pairs, const uint8_t* sflag, int sm_count,
+                               cudaStream_t st) {
+  if (S == 0) return;
+  prof_begin("coef_ztrans", st);
+  const int spt = F <= kZdWords ? kZdWords / F : 1;  // rows per tile (F <= kZAcc < kZdWords)
+  static int per_sm = 0;
+  if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coef_ztrans_direct,
+                                                               kZdThreads, 0) != cudaSuccess)
+    per_sm = 1;
+  const int64_t tiles = (S + spt - 1) / spt;  // upper bound (the list is <= S)
+  const int64_t cap = static_cast<int64_t>(sm_count) * (per_sm > 0 ? per_sm : 1);
+  k_coef_ztrans_direct<<<static_cast<unsigned>(tiles < cap ? tiles : cap), kZdThreads, 0, st>>>(
+      list, count, F, l, spt, zj, k, rows, rs, pairs, sflag);
+  prof_end(st);
 }
 
 }  // namespace tsv

@@ -396,7 +396,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
   const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
   const uint64_t n = static_cast<uint64_t>(g->dev.n);
-  const uint64_t words = 2 * S * M + C * M + 2 * n * k + 2 * n + S / 2 + (n + S) / 8 + 2;
+  const uint64_t words = 2 * S * M + C * M + 2 * n * k + 2 * n + S + (n + S) / 8 + 2;
   if (words > cfg->memory_cap_words || words > device_budget_words()) return false;
   if (peak_out) *peak_out = words;
   const int32_t nn = g->dev.n;
@@ -424,7 +424,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                    d_zj.as<uint64_t>(), st);
   }
   DevBuf X(S * M * 8, st), Y(S * M * 8, st), agg(C * M * 8, st);
-  DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(S * 4, st);
+  DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(std::getenv("TSV_ZTRANS") ? S * 4 : 8, st);
   // zero skipping and the single-shade form (CoefParams::vsh); positional z
   // keeps the plain z map
   DevBuf vsh(std::max<uint64_t>(n, 1), st), vsv(std::max<uint64_t>(n, 1) * 8, st);
@@ -441,7 +441,17 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   // the index tables depend on (k, use_items) only: uploaded once per device
   const CoefConst& cc = coef_const(dev, k, use_items);
   const std::vector<size_t>&poff = cc.poff, &joff = cc.joff, &moff = cc.moff, &icoff = cc.icoff;
-  tsv::launch_slot_head(g->dev.R, g->dev.run_slot, g->dev.run_head, slot_head.as<int32_t>(), st);
+  // multi-shade rows: the direct z map over a (slot, head) list, or
+  // (TSV_ZTRANS=tab) the warp-per-window table map over slot_head
+  const char* zt_env = std::getenv("TSV_ZTRANS");
+  const bool zt_tab = zt_env && std::strcmp(zt_env, "tab") == 0;
+  DevBuf mlist(S * 8, st), mcount(4, st);
+  if (zt_tab)
+    tsv::launch_slot_head(g->dev.R, g->dev.run_slot, g->dev.run_head, slot_head.as<int32_t>(), st);
+  else if (k > 2)
+    tsv::launch_multi_slots(g->dev.R, g->dev.run_slot, g->dev.run_head,
+                            vc ? nullptr : vsh.as<int8_t>(), mlist.as<int2>(),
+                            mcount.as<int32_t>(), st);
   const int2* dp = cc.pairs;
   // row strides: level l's rows hold its U row (C(k, l-1)) and then its S row (C(k, l))
   auto rs = [&](int l) { return static_cast<int>(std::max(T.count[l - 1], T.count[l])); };
@@ -501,9 +511,15 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                                use_items ? cp.vsv : nullptr, d_acc, st);
     } else {
       tsv::launch_coef_fixup(cp, st);
-      tsv::launch_coef_ztrans(g->dev.S, static_cast<int>(T.count[l]), l,
-                              slot_head.as<int32_t>(), d_zj.as<uint64_t>(), k, cp.E, B, rs(l),
-                              dp + joff[l], cp.vsh, fb, sms, st);
+      if (zt_tab)
+        tsv::launch_coef_ztrans(g->dev.S, static_cast<int>(T.count[l]), l,
+                                slot_head.as<int32_t>(), d_zj.as<uint64_t>(), k, cp.E, B, rs(l),
+                                dp + joff[l], cp.vsh, fb, sms, st);
+      else
+        tsv::launch_coef_ztrans_direct(g->dev.S, static_cast<int>(T.count[l]), l,
+                                       mlist.as<int2>(), mcount.as<int32_t>(),
+                                       d_zj.as<uint64_t>(), k, B, rs(l), dp + poff[l],
+                                       vc ? nullptr : fb, sms, st);
       std::swap(A, B);
       std::swap(fa, fb);
     }

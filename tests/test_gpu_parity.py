@@ -170,6 +170,44 @@ def test_engine_paths_agree(cuda_device, monkeypatch, env, ppb):
     _oracle_vs_gpu(n, u, v, ts, False, colors, [1, 2, 3], 5, max_ts=20, ppb=ppb)
 
 
+@pytest.mark.parametrize("env", [{"TSV_ENGINE": "points"}, {"TSV_ITEMS": "0"},
+                                 {"TSV_ITEMS": "1", "TSV_ITEMS_REG": "0"}, {"TSV_ITEMS": "1"},
+                                 {"TSV_ZTRANS": "tab"}])
+def test_coefficient_engine_kernels_agree(cuda_device, monkeypatch, env):
+    """Every arc kernel of the coefficient engine (k_coef_arcs, the item
+    stream k_coef_items, its register-walk form k_coef_items_reg for frames
+    <= 64 words, one and two entries per lane), both z maps of multi-shade
+    rows (direct and table) and the point engine give the
+    oracle's accumulators: single-shade, multi-shade and shadeless vertices,
+    hubs split across chunks, horizons below t, (s,d) anchors, undirected
+    graphs, k = 2..8."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    rng = np.random.default_rng(47)
+    n, m, t = 200, 6000, 40
+    u = rng.integers(0, n, m)
+    v = np.where(rng.random(m) < 0.3, 0, rng.integers(0, n, m))
+    ts = rng.integers(1, t + 1, m)
+    colors = rng.integers(1, 6, n)            # color 5 is in no motif: shadeless vertices
+    nz = 0
+    for motif, seed, mt, anchor in (([1, 2], 2, None, (-1, -1)),
+                                     ([1, 2, 3], 4, 30, (-1, -1)),
+                                     ([1, 1, 2, 3], 3, None, (-1, -1)),
+                                     ([1, 2, 3, 4, 1], 8, 25, (-1, -1)),
+                                     ([1, 1, 2, 3, 4, 2], 11, None, (-1, -1)),
+                                     ([1, 2, 3, 4, 1, 2, 3], 13, 35, (-1, -1)),
+                                     ([1, 2, 3, 4, 1, 2, 3, 4], 17, None, (-1, -1)),
+                                     ([1, 2, 3, 4], 19, None, (3, 0)),
+                                     ([1, 2, 3, 4, 2, 3], 23, 31, (5, 7))):
+        nz += bool(_oracle_vs_gpu(n, u, v, ts, True, colors, motif, seed, anchor, mt))
+    # every vertex carries every shade (k-TempPath): multi-shade frames only
+    one = np.ones(n, np.int64)
+    for k_ in (5, 6, 7):
+        nz += bool(_oracle_vs_gpu(n, u, v, ts, True, one, [1] * k_, 29 + k_))
+    nz += bool(_oracle_vs_gpu(n, u, v, ts, False, colors, [1, 1, 2, 3, 4, 2], 31, max_ts=20))
+    assert nz >= 8
+
+
 def test_c2_shape_small_scale_vs_oracle(cuda_device):
     inst = synth.make_config(2, scale=0.01)   # n=1e3, m=1e4, k=6 PathMotif
     k, col, motif, anchor = synth.effective_query(inst)
