@@ -193,7 +193,7 @@ def config_json(inst, world, args):
 
 
 
-def coef_alg_bytes(g, sh, k):
+def coef_alg_bytes(g, sh, k, info):
     """Algorithmic bytes of one full evaluation by the coefficient engine, per
     kernel family ("Roofline"), from the graph and the
     shade classes: a vertex with no shade is dead, one shade d keeps the
@@ -203,7 +203,8 @@ def coef_alg_bytes(g, sh, k):
         predecessor run, entry it carries) read -- C(k-2, l-2) for single ->
         single shades d_t != d_h, C(k-1, l-2) single -> multi, C(k-1, l-1)
         multi -> single, C(k, l-1) multi -> multi -- plus 8 B per (referenced
-        run of a live head, frame entry) written;
+        run of a live head, frame entry) written, plus 12 B per arc and 4 B
+        per run of graph metadata;
       coef_ztrans, levels 2 <= l < k: 8 B per (referenced run of a
         multi-shade head, C(k, l-1) entry) read + C(k, l) written."""
     from math import comb
@@ -236,9 +237,12 @@ def coef_alg_bytes(g, sh, k):
     ref = np.unique(src[ok])
     rh = ref >> 32
     r_single, r_multi = int(one[rh].sum()), int(multi[rh].sum())
+    # + the graph itself: 12 B per arc (edge id, predecessor slot, tail) and
+    # 4 B per run (head) at every middle level
+    meta = 12 * len(cu) + 4 * int(info.runs)
     arcs = sum(8 * (n_ss * comb(k - 2, l - 2) + n_sm * comb(k - 1, l - 2) +
                     n_ms * comb(k - 1, l - 1) + n_mm * comb(k, l - 1) +
-                    r_single * comb(k - 1, l - 1) + r_multi * comb(k, l - 1))
+                    r_single * comb(k - 1, l - 1) + r_multi * comb(k, l - 1)) + meta
                for l in range(3, k))
     ztrans = sum(8 * r_multi * (comb(k, l - 1) + comb(k, l)) for l in range(2, k))
     return {"coef_arcs": arcs, "coef_ztrans": ztrans}
@@ -420,7 +424,7 @@ def main():
     # full-range evaluations in the profile pass (the coefficient engine's)
     evals = sum(1 for _, a, b in work if a == 0 and b == P) * prof_steps
     if any(c for c, _ in coef.values()):
-        roof = coef_roofline(coef, k, coef_alg_bytes(g, sh, k), evals, hbm, peak_kind, args, world,
+        roof = coef_roofline(coef, k, coef_alg_bytes(g, sh, k, g.info), evals, hbm, peak_kind, args, world,
                              clk.summary().get("sm_mhz"))
     elif lvl_n:
         # updates executed by the middle-level launches (3 <= l < k when level

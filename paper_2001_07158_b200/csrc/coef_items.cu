@@ -309,8 +309,12 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items(const CoefParams P) {
 // end), taken from warp ballots, and needs no shared accumulator or
 // per-arc warp barrier: the serial part of k_coef_items costs ~10
 // instructions per event instead of ~40.
+#ifndef TSV_REG_MINB
+#define TSV_REG_MINB 7  // <= 72 registers: 7 blocks of 4 warps per SM
+#endif
 template <bool FIRST, bool LAST, int NO>
-__global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P, int fmp) {
+__global__ void __launch_bounds__(kIW * 32, TSV_REG_MINB)
+    k_coef_items_reg(const CoefParams P, int fmp) {
   extern __shared__ uint64_t dsm[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   uint64_t* const prow = dsm + static_cast<size_t>(wib) * 32 * fmp;
@@ -319,6 +323,7 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P,
   __shared__ int32_t s_start[kIW][33]; // item stream offsets of the live arcs
   __shared__ int32_t s_poff[kIW][32];  // item list offset
   __shared__ int8_t s_lane[kIW][32];   // the live arc's lane (its prow row)
+  __shared__ uint64_t s_om[kIW][32];   // by lane: outputs the arc's items reach
 
   const int64_t c = static_cast<int64_t>(blockIdx.x) * kIW + wib;
   if (c >= P.g.C) return;  // warp-uniform
@@ -355,10 +360,12 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P,
       live = ts != -1 && (FIRST || __ldg(P.sflag + sidx) != 0);
     }
     int nitem = 0, poff = 0;
+    uint64_t omask = 0;  // outputs the arc's items reach (its prow entries)
     if (live) {
       const int pt = (ts >= 0 ? ts : k) * (k + 1) + (hs >= 0 ? hs : k);
       nitem = __ldg(P.item_cnt + pt);
       poff = __ldg(P.item_off + pt);
+      omask = __ldg(P.item_omask + pt);
       live = nitem > 0;
       if (!live) nitem = 0;
     }
@@ -391,6 +398,7 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P,
     const int total = __shfl_sync(kFull, incl, 31);
     const int nlive = __popc(livem);
     __syncwarp();  // the previous batch's readers of the staging arrays are done
+    s_om[wib][lane] = omask;
     if (live) {
       const int ai = __popc(livem & ((1u << lane) - 1u));
       s_start[wib][ai] = incl - nitem;
@@ -406,15 +414,8 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P,
         s_ys[wib][8 + j][ai] = ks.m.c[j];
       }
     }
-    // rows of the live arcs start at zero (entries no item of the arc reaches)
-    {
-      unsigned m = livem;
-      while (m) {
-        const int a = __ffs(m) - 1;
-        m &= m - 1;
-        for (int o = lane; o < fm; o += 32) prow[a * fmp + o] = 0;
-      }
-    }
+    // a live arc's row holds exactly the outputs its items reach (omask);
+    // the walk reads no other entry, so the rows need no clearing
     if (lane == 0) s_start[wib][nlive] = total;
     __syncwarp();
 
@@ -442,6 +443,7 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P,
       }
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
+        if (jj[r] >= 0 && !u[r]) prow[s_lane[wib][jj[r]] * fmp + out[r]] = 0ull;
         if (jj[r] >= 0 && u[r]) {
           const int j = jj[r];
           KSplit ys;
@@ -469,8 +471,9 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items_reg(const CoefParams P,
         frame = __shfl_sync(kFull, myfr, a);
       }
       if (livem & bit) {
-        if (lane < fm) acc0 ^= prow[a * fmp + lane];
-        if (NO > 1 && lane + 32 < fm) acc1 ^= prow[a * fmp + 32 + lane];
+        const uint64_t om = s_om[wib][a];
+        if ((om >> lane) & 1u) acc0 ^= prow[a * fmp + lane];
+        if (NO > 1 && ((om >> (32 + lane)) & 1u)) acc1 ^= prow[a * fmp + 32 + lane];
       }
       if (pushm & bit) {
         const int32_t d = __shfl_sync(kFull, dst, a);

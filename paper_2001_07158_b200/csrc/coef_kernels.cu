@@ -323,6 +323,8 @@ __global__ void __launch_bounds__(kCoefWarps * 32)
 // of the preceding chunks back to the one where h starts (U space, before
 // the z map, so no product is needed).
 __global__ void k_coef_fixup(const CoefParams P) {
+  __shared__ uint64_t carry_s[kZAcc];  // E = C(k, l-1) <= kZAcc (k <= 12)
+  __shared__ int any;
   const int32_t c = P.g.carry_list[blockIdx.x];
   const int32_t r0 = P.g.chunk_run[c];
   if (r0 >= P.g.R) return;
@@ -332,20 +334,30 @@ __global__ void k_coef_fixup(const CoefParams P) {
   const int dh = P.vsh ? P.vsh[head] : -2;
   if (dh == -1) return;  // shadeless: rows never read
   // entries of the head's rows: its compact frame in the item-stream layout
-  const int64_t E = (P.frame_single && dh >= 0) ? P.frame_single : P.E;
-  for (int64_t e = threadIdx.x; e < E; e += blockDim.x) {
+  const int E = (P.frame_single && dh >= 0) ? P.frame_single : P.E;
+  if (threadIdx.x == 0) any = 0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
     uint64_t carry = 0;
     for (int64_t cc = c - 1;; --cc) {
       carry ^= P.agg[cc * P.E + e];
       if (!P.g.chunk_carry[cc] || P.g.run_head[P.g.chunk_run[cc]] != head) break;
     }
+    carry_s[e] = carry;
+    if (carry) any = 1;
+  }
+  __syncthreads();
+  if (!any) return;
+  // every (run, entry) of the piece in parallel (hub pieces hold ~1e3 runs)
+  const int n = (r1 - r0) * E;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int q = i / E, e = i - q * E;
+    const uint64_t carry = carry_s[e];
     if (!carry) continue;
-    for (int32_t r = r0; r < r1; ++r) {
-      const int32_t slot = P.g.run_slot[r];
-      if (slot >= 0) {
-        P.ubuf[static_cast<int64_t>(slot) * P.rs_out + e] ^= carry;
-        P.sflag_out[slot] = 1;
-      }
+    const int32_t slot = P.g.run_slot[r0 + q];
+    if (slot >= 0) {
+      P.ubuf[static_cast<int64_t>(slot) * P.rs_out + e] ^= carry;
+      P.sflag_out[slot] = 1;
     }
   }
 }
@@ -707,7 +719,7 @@ void launch_coef_arcs(const CoefParams& p, cudaStream_t st) {
 void launch_coef_fixup(const CoefParams& p, cudaStream_t st) {
   if (p.g.ncarry == 0) return;
   prof_begin("coef_fixup", st);
-  k_coef_fixup<<<p.g.ncarry, 128, 0, st>>>(p);
+  k_coef_fixup<<<p.g.ncarry, 256, 0, st>>>(p);
   prof_end(st);
 }
 

@@ -325,7 +325,8 @@ struct CoefConst {
   int2* pairs = nullptr;      // pairs (readout), jpairs (z map), items
   int32_t* maps = nullptr;    // smap, item offsets/counts
   uint64_t* ident = nullptr;  // k x k identity (w of the shade basis)
-  std::vector<size_t> poff, joff, moff, icoff;
+  uint64_t* omask = nullptr;  // per level, (k+1)^2 output masks of the item lists
+  std::vector<size_t> poff, joff, moff, icoff, omoff;
 };
 const CoefConst& coef_const(int dev, int k, bool items) {
   static std::mutex mu;
@@ -338,7 +339,8 @@ const CoefConst& coef_const(int dev, int k, bool items) {
   auto c = std::make_unique<CoefConst>();
   std::vector<int2> pairs;
   c->poff.assign(static_cast<size_t>(k) + 1, 0);
-  c->joff = c->moff = c->icoff = c->poff;
+  c->joff = c->moff = c->icoff = c->omoff = c->poff;
+  std::vector<uint64_t> om;
   for (int l = 2; l <= k; ++l) {
     c->poff[l] = pairs.size();
     pairs.insert(pairs.end(), T.pairs[l].begin(), T.pairs[l].end());
@@ -355,6 +357,15 @@ const CoefConst& coef_const(int dev, int k, bool items) {
   if (items) {
     for (int l = 2; l <= k; ++l) {
       tsv::CoefItems ci = tsv::coef_items(k, l);
+      c->omoff[l] = om.size();
+      for (size_t pt = 0; pt < ci.off.size(); ++pt) {
+        uint64_t msk = 0;
+        for (int32_t i = 0; i < ci.cnt[pt]; ++i) {
+          const int32_t o = ci.items[static_cast<size_t>(ci.off[pt] + i)].y;
+          if (o < 64) msk |= 1ull << o;
+        }
+        om.push_back(msk);
+      }
       for (int32_t& o : ci.off) o += static_cast<int32_t>(pairs.size());  // absolute
       pairs.insert(pairs.end(), ci.items.begin(), ci.items.end());
       c->icoff[l] = maps.size();
@@ -370,6 +381,9 @@ const CoefConst& coef_const(int dev, int k, bool items) {
   TSV_CUDA(cudaMalloc(&c->pairs, std::max<size_t>(pairs.size(), 1) * sizeof(int2)));
   TSV_CUDA(cudaMalloc(&c->maps, std::max<size_t>(maps.size(), 1) * 4));
   TSV_CUDA(cudaMalloc(&c->ident, I.size() * 8));
+  TSV_CUDA(cudaMalloc(&c->omask, std::max<size_t>(om.size(), 1) * 8));
+  if (!om.empty())
+    TSV_CUDA(cudaMemcpy(c->omask, om.data(), om.size() * 8, cudaMemcpyHostToDevice));
   TSV_CUDA(cudaMemcpy(c->pairs, pairs.data(), pairs.size() * sizeof(int2),
                       cudaMemcpyHostToDevice));
   TSV_CUDA(cudaMemcpy(c->maps, maps.data(), maps.size() * 4, cudaMemcpyHostToDevice));
@@ -484,6 +498,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
       cp.items = dp;  // offsets are absolute in d_pairs
       cp.item_off = cc.maps + icoff[l];
       cp.item_cnt = cp.item_off + K1 * K1;
+      cp.item_omask = cc.omask + cc.omoff[l];
       cp.frame_multi = static_cast<int>(T.count[l - 1]);
       cp.frame_single = static_cast<int>(T.count[l - 1] * (k - l + 1) / k);  // C(k-1, l-1)
       cp.frame_max = sh->multi ? cp.frame_multi : cp.frame_single;

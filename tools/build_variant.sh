@@ -1,5 +1,6 @@
 #!/bin/bash
-# Experimental engine variant: recompile kernels.cu with extra nvcc flags and
+# Experimental engine variant: recompile kernels.cu (or SRC=<name> of another
+# csrc/*.cu) with extra nvcc flags and
 # link it with the regular objects into exp_libs/libtsv_<name>.so; select it
 # at run time with TSV_LIB=exp_libs/libtsv_<name>.so.
 # Usage: tools/build_variant.sh <name> <nvcc flags...>
@@ -10,10 +11,14 @@ name=$1; shift
 P=paper_2001_07158_b200
 make -s -C $P >/dev/null
 mkdir -p exp_libs build_exp
+src=${SRC:-kernels}
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xptxas -v \
-  -Xcompiler -fPIC,-fopenmp -ccbin g++ "$@" -c $P/csrc/kernels.cu -o build_exp/kernels_$name.o \
-  2> build_exp/kernels_$name.ptxas.log
+  -Xcompiler -fPIC,-fopenmp -ccbin g++ "$@" -c $P/csrc/$src.cu -o build_exp/${src}_$name.o \
+  2> build_exp/${src}_$name.ptxas.log
+objs=""
+for o in $P/build/*.o; do
+  [ "$(basename $o .o)" = "$src" ] && objs="$objs build_exp/${src}_$name.o" || objs="$objs $o"
+done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o exp_libs/libtsv_$name.so \
-  build_exp/kernels_$name.o $P/build/static_kernels.o $P/build/build_kernels.o \
-  $P/build/gf_bench.o $P/build/tsv_abi.o $P/build/layout.o -Xcompiler -fopenmp -lgomp
-grep -A2 "k_level_wideILi2ELb0ELb1ELb0" build_exp/kernels_$name.ptxas.log | grep -E "registers|spill" | head -2
+  $objs -Xcompiler -fopenmp -lgomp
+grep -A2 "k_level_wideILi2ELb0ELb1ELb0" build_exp/${src}_$name.ptxas.log | grep -E "registers|spill" | head -2
