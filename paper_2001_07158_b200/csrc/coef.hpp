@@ -45,6 +45,8 @@ struct CoefParams {
   const int32_t* item_off = nullptr;  // (k+1) x (k+1)
   const int32_t* item_cnt = nullptr;
   const uint64_t* item_omask = nullptr;  // (k+1) x (k+1): outputs < 64 an item list reaches
+  int32_t* chunk_ctr = nullptr;  // zeroed: persistent warps take chunks from it (nullptr: one per warp)
+  int sms = 148;
   int frame_single = 0;  // C(k-1, ell-1) (0: full frames everywhere)
   int frame_multi = 0;   // C(k, ell-1)
   int frame_max = 0;     // accumulator words (frame_multi, or frame_single without multi-shade vertices)

@@ -325,12 +325,14 @@ __global__ void __launch_bounds__(kIW * 32, TSV_REG_MINB)
   __shared__ int8_t s_lane[kIW][32];   // the live arc's lane (its prow row)
   __shared__ uint64_t s_om[kIW][32];   // by lane: outputs the arc's items reach
 
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * kIW + wib;
-  if (c >= P.g.C) return;  // warp-uniform
   const int k = P.k;
   const int fm = P.frame_max;
   const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
   const uint64_t yb = static_cast<uint64_t>(P.ell - 1) + 0x165667b19e3779f9ull;
+  // persistent warps: the first chunk by warp id, then from the counter
+  // (chunks hold ~A / 9500 arcs, so one chunk per warp left a 30% tail wave)
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * kIW;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * kIW + wib; c < P.g.C;) {
   const int64_t a0 = P.g.chunk_arc[c], a1 = P.g.chunk_arc[c + 1];
   int32_t run_ctr = P.g.chunk_run[c];
   int frame = fm;  // frame of the current head
@@ -506,6 +508,28 @@ __global__ void __launch_bounds__(kIW * 32, TSV_REG_MINB)
     if (lane < frame) P.agg[c * P.E + lane] = acc0;
     if (NO > 1 && lane + 32 < frame) P.agg[c * P.E + 32 + lane] = acc1;
   }
+  if (!P.chunk_ctr) break;
+  int64_t nx = 0;
+  if (lane == 0) nx = atomicAdd(P.chunk_ctr, 1) + nwarps;
+  c = __shfl_sync(kFull, nx, 0);
+  }
+}
+
+// Resident blocks per SM of a kernel at (threads, dynamic shared bytes),
+// cached: the occupancy query is not free and runs once per launch otherwise.
+int resident_blocks(const void* f, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, size_t>, int>> done;
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(f, smem);
+  for (auto& d : done)
+    if (d.first == key) return d.second;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  done.emplace_back(key, per_sm);
+  return per_sm;
 }
 
 // Opt a kernel into `bytes` of dynamic shared memory (raised only, per
@@ -550,7 +574,13 @@ void launch_coef_items(const CoefParams& p, cudaStream_t st) {
     const size_t rsm = static_cast<size_t>(kIW) * 32 * fmp * 8;
     auto go2 = [&](auto kern) {
       allow_smem(reinterpret_cast<const void*>(kern), rsm);
-      kern<<<blocks, kIW * 32, rsm, st>>>(p, fmp);
+      unsigned nb = blocks;
+      if (p.chunk_ctr) {  // persistent grid: every resident block slot once
+        const int per_sm = resident_blocks(reinterpret_cast<const void*>(kern), kIW * 32, rsm);
+        const unsigned cap = static_cast<unsigned>(p.sms * per_sm);
+        if (cap < nb) nb = cap;
+      }
+      kern<<<nb, kIW * 32, rsm, st>>>(p, fmp);
     };
     const bool two = p.frame_max > 32;
     if (first && last)

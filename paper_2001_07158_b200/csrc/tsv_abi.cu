@@ -123,6 +123,11 @@ void keep_pool_memory(int dev) {
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t keep = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    // evaluations on concurrent streams (repetitions, probes) must not be
+    // chained by the pool: no new stream dependencies to reuse a block freed
+    // on another stream (same-stream reuse and completed frees still apply)
+    int no = 0;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
   }
   done.push_back(dev);
 }
@@ -262,6 +267,29 @@ uint64_t device_budget_words() {
     if (reserved > used) free_b += reserved - used;
   }
   return static_cast<uint64_t>(free_b * 0.92) / 8;
+}
+
+// Does a working set of `words` fit next to what is allocated?  A set below
+// 1/8 of the device is taken as fitting without a cudaMemGetInfo query (the
+// query is not free: on the bench's deep stream queues it blocked the host).
+bool fits_device(uint64_t words) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, size_t>> total;
+  int dev = 0;
+  TSV_CUDA(cudaGetDevice(&dev));
+  size_t tb = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& t : total)
+      if (t.first == dev) tb = t.second;
+    if (!tb) {
+      size_t f = 0;
+      TSV_CUDA(cudaMemGetInfo(&f, &tb));
+      total.emplace_back(dev, tb);
+    }
+  }
+  if (words * 8 <= tb / 8) return true;
+  return words <= device_budget_words();
 }
 
 // Points per batch: the largest power of two <= min(range, 128) whose
@@ -411,7 +439,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
   const uint64_t n = static_cast<uint64_t>(g->dev.n);
   const uint64_t words = 2 * S * M + C * M + 2 * n * k + 2 * n + S + (n + S) / 8 + 2;
-  if (words > cfg->memory_cap_words || words > device_budget_words()) return false;
+  if (words > cfg->memory_cap_words || !fits_device(words)) return false;
   if (peak_out) *peak_out = words;
   const int32_t nn = g->dev.n;
   int dev = 0, sms = 148;
@@ -471,6 +499,11 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   auto rs = [&](int l) { return static_cast<int>(std::max(T.count[l - 1], T.count[l])); };
   uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
   uint8_t *fa = fl0.as<uint8_t>(), *fb = fl1.as<uint8_t>();
+  // chunk counters of the persistent item kernel, one per level
+  const char* ps_env = std::getenv("TSV_PERSIST");
+  const bool persist = !(ps_env && std::strcmp(ps_env, "0") == 0);
+  DevBuf ctrs(static_cast<size_t>(k + 1) * 4, st);
+  if (persist) TSV_CUDA(cudaMemsetAsync(ctrs.p, 0, static_cast<size_t>(k + 1) * 4, st));
   for (int l = 2; l <= k; ++l) {
     tsv::CoefParams cp;
     cp.g = g->dev;
@@ -493,6 +526,8 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     cp.sflag = fa;
     cp.sflag_out = fb;
     cp.smap = l > 2 ? cc.maps + moff[l - 1] : nullptr;
+    cp.chunk_ctr = persist ? ctrs.as<int32_t>() + l : nullptr;
+    cp.sms = sms;
     if (use_items) {
       const int K1 = k + 1;
       cp.items = dp;  // offsets are absolute in d_pairs

@@ -35,6 +35,22 @@ def work_units(reps: int, P: int, rank: int, world: int) -> list[tuple[int, int,
     return out
 
 
+def plan_units(reps: int, P: int, k: int, rank: int, world: int) -> list[tuple[int, int, int]]:
+    """Work of `rank` for one decide, choosing between the two engines.
+
+    A unit covering all P points of a repetition runs the coefficient engine
+    (DESIGN.md 2b), which costs about as much as the point engine on P / r
+    points, r ~ 4 at k = 6 (C2: 0.71 vs 2.87 ms per evaluation) and ~1.3 at
+    k = 5 (C5, whose point engine multiplies by y tables).  Fixing some of the
+    k variables per rank does not shrink the coefficient form, so when there
+    are more ranks than repetitions and a rank's point share would still be
+    >= P / 4 (k >= 6), the repetitions stay whole on ranks 0..reps-1 and the
+    other ranks idle; otherwise the points are split (work_units)."""
+    if k >= 6 and world > reps and reps * P >= world * (P // 4):
+        return [(rank, 0, P)] if rank < reps else []
+    return work_units(reps, P, rank, world)
+
+
 def xor_allreduce(t, group=None, out=None):
     """XOR-combine an int64 tensor across ranks; every rank receives the result.
 

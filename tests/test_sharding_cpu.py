@@ -67,6 +67,24 @@ def test_work_units_cover_every_rep_point_once():
     assert work_units(4, 64, 5, 8) == [(2, 32, 64)]
 
 
+def test_plan_units_keeps_coefficient_reps_whole():
+    from paper_2001_07158_b200.shard import plan_units
+    for reps, P, k in ((4, 64, 6), (1, 32, 5), (1, 256, 8), (1, 4096, 12), (3, 64, 6)):
+        for world in (1, 2, 4, 8):
+            seen = set()
+            for r in range(world):
+                for rep, a, b in plan_units(reps, P, k, r, world):
+                    for p in range(a, b):
+                        assert (rep, p) not in seen
+                        seen.add((rep, p))
+            assert len(seen) == reps * P
+    # C2 at 8 GPUs: four whole repetitions, four idle ranks
+    assert plan_units(4, 64, 6, 3, 8) == [(3, 0, 64)]
+    assert plan_units(4, 64, 6, 5, 8) == []
+    # C5 (k = 5, one repetition): points split over the ranks
+    assert plan_units(1, 32, 5, 1, 2) == [(0, 16, 32)]
+
+
 def test_point_ranges_partition():
     for P in (2, 32, 64, 4096):
         for world in (1, 2, 3, 4, 8):

@@ -36,7 +36,7 @@ def family(name):
         first = m.group(3) in ("1", "true")
         last = m.group(4) in ("1", "true")
         return "coef_arcs_first" if first else "coef_arcs_last" if last else "coef_arcs"
-    m = re.search(r"k_coef_items<(\w+), (\w+), (\d+)>", name)
+    m = re.search(r"k_coef_items(?:_reg)?<(\w+), (\w+), (\d+)>", name)
     if m:
         first = m.group(1) in ("1", "true")
         last = m.group(2) in ("1", "true")
