@@ -324,13 +324,35 @@ __global__ void k_restrict_flags(int64_t m, const int32_t* __restrict__ eu,
   if (i < m) f[i] = (ets[i] <= max_ts && keep[eu[i]] && keep[ev[i]]) ? 1 : 0;
 }
 
+__global__ void k_shaded_mask(int32_t n, const int32_t* __restrict__ off,
+                              uint8_t* __restrict__ keep) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u < n) keep[u] = off[u + 1] > off[u] ? 1 : 0;
+}
+
+__global__ void k_remap_edge_ids(int64_t A, uint32_t* __restrict__ meta,
+                                 const int32_t* __restrict__ oid) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  const uint32_t mt = meta[a];
+  meta[a] = (mt & ~kEdgeMask) | static_cast<uint32_t>(oid[mt & kEdgeMask]);
+}
+
 }  // namespace
+
+void launch_shaded_mask(int32_t n, const int32_t* off, uint8_t* keep, cudaStream_t st) {
+  if (n > 0) k_shaded_mask<<<nblk(n), kT, 0, st>>>(n, off, keep);
+}
+
+void launch_remap_edge_ids(int64_t A, uint32_t* meta, const int32_t* oid, cudaStream_t st) {
+  if (A > 0) k_remap_edge_ids<<<nblk(A), kT, 0, st>>>(A, meta, oid);
+}
 
 int64_t device_restrict(const int32_t* eu, const int32_t* ev, const int32_t* ets, int64_t m,
                         const uint8_t* d_keep, int32_t max_ts, int32_t* ou, int32_t* ov,
                         int32_t* ots, cudaStream_t st,
                         const std::function<void*(size_t)>& alloc,
-                        const std::function<void(void*)>& release) {
+                        const std::function<void(void*)>& release, int32_t* oid) {
   if (m == 0) return 0;
   uint8_t* f = static_cast<uint8_t*>(alloc(m));
   int64_t* cnt = static_cast<int64_t*>(alloc(8));
@@ -341,6 +363,8 @@ int64_t device_restrict(const int32_t* eu, const int32_t* ev, const int32_t* ets
   cub::DeviceSelect::Flagged(t, tmp, eu, f, ou, cnt, m, st);
   cub::DeviceSelect::Flagged(t, tmp, ev, f, ov, cnt, m, st);
   cub::DeviceSelect::Flagged(t, tmp, ets, f, ots, cnt, m, st);
+  if (oid) cub::DeviceSelect::Flagged(t, tmp, cub::CountingInputIterator<int32_t>(0), f, oid, cnt,
+                                      m, st);
   int64_t kept = 0;
   cudaMemcpyAsync(&kept, cnt, 8, cudaMemcpyDeviceToHost, st);
   cudaStreamSynchronize(st);

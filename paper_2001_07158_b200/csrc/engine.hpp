@@ -132,11 +132,17 @@ void device_build(const int32_t* d_u, const int32_t* d_v, const int32_t* d_ts, i
 
 // Order-preserving filter of a canonical edge list (restrict_to): keeps
 // edges with ts <= max_ts and both endpoints kept; returns the kept count.
+// oid (optional): the kept edges' indices in the input list.
 int64_t device_restrict(const int32_t* eu, const int32_t* ev, const int32_t* ets, int64_t m,
                         const uint8_t* d_keep, int32_t max_ts, int32_t* ou, int32_t* ov,
                         int32_t* ots, cudaStream_t st,
                         const std::function<void*(size_t)>& alloc,
-                        const std::function<void(void*)>& release);
+                        const std::function<void(void*)>& release, int32_t* oid = nullptr);
+// keep[u] = vertex u has at least one shade (shade CSR offsets, device)
+void launch_shaded_mask(int32_t n, const int32_t* off, uint8_t* keep, cudaStream_t st);
+// arc_meta edge ids of a layout built from a filtered list -> the ids of the
+// unfiltered list (oid[filtered id])
+void launch_remap_edge_ids(int64_t A, uint32_t* meta, const int32_t* oid, cudaStream_t st);
 
 // Kernel launchers (kernels.cu).  All are asynchronous on `st`.
 // w_{d,j} table (k x k) of the constrained substitution, on the device

@@ -174,6 +174,13 @@ struct tsv_shades {
   int device = 0;
   int32_t* off = nullptr;
   int32_t* shades = nullptr;
+  // the graph restricted to vertices with a shade (same vertex and edge ids),
+  // built once per graph by shaded_subgraph(); state: 0 not tried, 1 built,
+  // 2 not worth it (most arcs kept) or not applicable
+  mutable std::mutex sub_mu;
+  mutable int sub_state = 0;
+  mutable const tsv_graph* sub_of = nullptr;
+  mutable std::shared_ptr<tsv_graph> sub;
   ~tsv_shades() {
     int prev = 0;
     cudaGetDevice(&prev);
@@ -336,6 +343,8 @@ struct VcSpec {
   int32_t wild = -1;                  // wildcard color, -1 = none
 };
 
+const tsv_graph* shaded_subgraph(const tsv_graph* g, const tsv_shades* sh);
+
 // Subset-index tables of the coefficient engine for one k (host).
 const tsv::CoefTables& coef_const_tables(int k) {
   static std::mutex mu;
@@ -432,6 +441,10 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const char* eng = std::getenv("TSV_ENGINE");
   if (eng && std::strcmp(eng, "points") == 0) return false;
   if (k < 2 || k > 12) return false;  // C(k, l) <= tsv::kZAcc
+  // arcs touching a shadeless vertex never carry a nonzero product (its z,
+  // hence every S row, is zero): evaluate the shaded subgraph, which keeps
+  // the vertex and edge ids (y draws) and gives the same accumulators
+  if (!vc && sh) g = shaded_subgraph(g, sh);
   const tsv::CoefTables& T = coef_const_tables(k);
   int64_t M = 1;
   for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, T.count[l]);
@@ -887,6 +900,100 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
   }
   return g;
 }
+
+// Graph restricted to the vertices with at least one shade, keeping vertex ids
+// and the original edge ids in arc_meta (so every y draw is the full graph's).
+// An arc with a shadeless endpoint adds nothing in the full graph: a
+// shadeless tail's rows are zero at every level (z = 0), a shadeless head's
+// rows are never read and its accumulator is zero; a run whose arcs all came
+// from shadeless tails only repeats its vertex's prefix, so an arc's source
+// (the tail's last run before it) has the same prefix in both graphs.  Built
+// once per (graph, shades) on the graph's device; used by the coefficient
+// engine when it drops >= 15% of the arcs (C2: 61%), else the graph itself.
+const tsv_graph* shaded_subgraph(const tsv_graph* g, const tsv_shades* sh) {
+  const char* env = std::getenv("TSV_SUBGRAPH");
+  if (g->model != 0 || (env && env[0] == '0') || g->host.n == 0) return g;
+  std::lock_guard<std::mutex> lk(sh->sub_mu);
+  if (sh->sub_of == g) {
+    if (sh->sub_state == 1) return sh->sub.get();
+    if (sh->sub_state == 2) return g;
+  }
+  sh->sub.reset();
+  sh->sub_of = g;
+  sh->sub_state = 2;
+  DeviceGuard dg(g->device);
+  cudaStream_t st = nullptr;
+  TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::vector<void*> tmp;
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+      throw CudaError("shaded subgraph: out of device memory");
+    tmp.push_back(p);
+    return p;
+  };
+  auto release = [&](void* p) {
+    auto it = std::find(tmp.begin(), tmp.end(), p);
+    if (it != tmp.end()) tmp.erase(it);
+    cudaFreeAsync(p, st);
+  };
+  auto done = [&] {
+    for (void* p : tmp) cudaFreeAsync(p, st);
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  };
+  try {
+    const int32_t n = g->host.n;
+    const int64_t m = g->m;
+    auto* keep = static_cast<uint8_t*>(alloc(static_cast<size_t>(n)));
+    tsv::launch_shaded_mask(n, sh->off, keep, st);
+    const int32_t *eu = g->d_eu, *ev = g->d_ev, *ets = g->d_ets;
+    if (!eu && g->edges_in_layout) {
+      auto* a = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      auto* b = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      auto* c = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      tsv::edges_from_layout(g->dev, g->host.directed, a, b, c, st);
+      eu = a;
+      ev = b;
+      ets = c;
+    } else if (!eu) {
+      auto* a = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      auto* b = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      auto* c = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+      if (m) {
+        TSV_CUDA(cudaMemcpyAsync(a, g->host.eu.data(), m * 4, cudaMemcpyHostToDevice, st));
+        TSV_CUDA(cudaMemcpyAsync(b, g->host.ev.data(), m * 4, cudaMemcpyHostToDevice, st));
+        TSV_CUDA(cudaMemcpyAsync(c, g->host.ets.data(), m * 4, cudaMemcpyHostToDevice, st));
+      }
+      eu = a;
+      ev = b;
+      ets = c;
+    }
+    auto* ou = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+    auto* ov = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+    auto* ots = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+    auto* oid = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+    const int64_t kept = tsv::device_restrict(eu, ev, ets, m, keep, g->host.t, ou, ov, ots, st,
+                                              alloc, release, oid);
+    if (kept * 100 > m * 85) {
+      done();
+      return g;
+    }
+    TSV_CUDA(cudaStreamSynchronize(st));
+    tsv_graph* s = device_graph_build(n, kept, ou, ov, ots, g->host.directed, g->host.t,
+                                      g->device, /*canonical=*/true, /*on_device=*/true);
+    tsv::launch_remap_edge_ids(s->dev.A, const_cast<uint32_t*>(s->dev.arc_meta), oid, st);
+    TSV_CUDA(cudaGetLastError());
+    done();
+    sh->sub.reset(s);
+    sh->sub_state = 1;
+    return s;
+  } catch (...) {
+    done();
+    throw;
+  }
+}
+
 
 }  // namespace
 
