@@ -235,14 +235,15 @@ def config_json(inst, world, args):
             "sieve_points": 1 << k_eff, "repetitions": REPS[args.config],
             "updates_per_step": inst.updates() * REPS[args.config],
             "parallelism": f"sieve-point sharding x{world}",
-            "l2": "working set > L2 (state buffers 2*S*W*8 B, S = referenced runs, see DESIGN.md)"}
+            "l2": "flushed before every step: a 256 MB buffer (2x the 126 MB L2) is "
+                  "zeroed on the bench stream inside the timed region"}
 
 
 # ---------------------------------------------------------------- our arm
 
 
 
-def coef_alg_bytes(g, sh, k, info):
+def coef_alg_bytes(g, sh, k):
     """Algorithmic bytes of one full evaluation by the coefficient engine, per
     kernel family ("Roofline"), from the graph and the
     shade classes: a vertex with no shade is dead, one shade d keeps the
@@ -253,7 +254,7 @@ def coef_alg_bytes(g, sh, k, info):
         single shades d_t != d_h, C(k-1, l-2) single -> multi, C(k-1, l-1)
         multi -> single, C(k, l-1) multi -> multi -- plus 8 B per (referenced
         run of a live head, frame entry) written, plus 12 B per arc and 4 B
-        per run of graph metadata;
+        per run of the shaded subgraph (graph metadata);
       coef_ztrans, levels 2 <= l < k: 8 B per (referenced run of a
         multi-shade head, C(k, l-1) entry) read + C(k, l) written."""
     from math import comb
@@ -286,9 +287,12 @@ def coef_alg_bytes(g, sh, k, info):
     ref = np.unique(src[ok])
     rh = ref >> 32
     r_single, r_multi = int(one[rh].sum()), int(multi[rh].sum())
-    # + the graph itself: 12 B per arc (edge id, predecessor slot, tail) and
-    # 4 B per run (head) at every middle level
-    meta = 12 * len(cu) + 4 * int(info.runs)
+    # + the graph itself at every middle level: 12 B per arc (edge id,
+    # predecessor slot, tail) and 4 B per run (head) of the shaded subgraph
+    # the engine walks (arcs with both endpoints shaded)
+    kept = (cnt[cu] > 0) & (cnt[cv] > 0)
+    runs_kept = len(np.unique(cv[kept] * (1 << 32) + ct[kept]))
+    meta = 12 * int(kept.sum()) + 4 * runs_kept
     arcs = sum(8 * (n_ss * comb(k - 2, l - 2) + n_sm * comb(k - 1, l - 2) +
                     n_ms * comb(k - 1, l - 1) + n_mm * comb(k, l - 1) +
                     r_single * comb(k - 1, l - 1) + r_multi * comb(k, l - 1)) + meta
@@ -398,7 +402,13 @@ def main():
     # one evaluation's tail wave overlaps the next one's launches
     side = [torch.cuda.Stream() for _ in range(max(1, min(args.streams, len(work))) - 1)]
 
+    # L2 flush between steps (inside the timed region, counted against us):
+    # the coefficient engine's working set at C2 (~70 MB per evaluation,
+    # ~15 MB of graph) would otherwise partly survive in L2 across steps
+    l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
     def step(concurrent=True):
+        l2_flush.zero_()
         acc.zero_()
         if not side or not concurrent:
             for r, a, b in work:
@@ -476,7 +486,7 @@ def main():
     # full-range evaluations in the profile pass (the coefficient engine's)
     evals = sum(1 for _, a, b in work if a == 0 and b == P) * prof_steps
     if any(c for c, _ in coef.values()):
-        roof = coef_roofline(coef, k, coef_alg_bytes(g, sh, k, g.info), evals, hbm, peak_kind, args, world,
+        roof = coef_roofline(coef, k, coef_alg_bytes(g, sh, k), evals, hbm, peak_kind, args, world,
                              clk.summary().get("sm_mhz"))
     elif lvl_n:
         # updates executed by the middle-level launches (3 <= l < k when level
