@@ -82,7 +82,7 @@ void launch_multi_slots(int64_t R, const int32_t* run_slot, const int32_t* run_h
 void launch_coef_ztrans_direct(int64_t S, int F, int l, const int2* list, const int32_t* count,
                                const uint64_t* zj, int k, uint64_t* rows, int rs,
                                const int2* pairs, const uint8_t* sflag, int sm_count,
-                               cudaStream_t st);
+                               int64_t rows_hint, cudaStream_t st);
 constexpr int kZAcc = 1024;  // largest F the in-place z map handles (k <= 12)
 // vsh / vsv of the rows of the n x k shade table (CoefParams)
 void launch_vshade(int32_t n, int k, const uint64_t* rows, int8_t* vsh, uint64_t* vsv,

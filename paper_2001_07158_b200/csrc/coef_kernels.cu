@@ -776,10 +776,14 @@ void launch_multi_slots(int64_t R, const int32_t* run_slot, const int32_t* run_h
 void launch_coef_ztrans_direct(int64_t S, int F, int l, const int2* list, const int32_t* count,
                                const uint64_t* zj, int k, uint64_t* rows, int rs,
                                const int2* pairs, const uint8_t* sflag, int sm_count,
-                               cudaStream_t st) {
+                               int64_t rows_hint, cudaStream_t st) {
   if (S == 0) return;
   prof_begin("coef_ztrans", st);
-  const int spt = F <= kZdWords ? kZdWords / F : 1;  // rows per tile (F <= kZAcc < kZdWords)
+  // rows per tile: as many as the shared tile holds, but few enough that the
+  // expected rows (rows_hint) still give every SM ~8 blocks -- C2 lists a
+  // few 10^4 rows (latency-bound, dependent gathers), C5 every slot
+  const int64_t want = std::max<int64_t>(1, rows_hint / (static_cast<int64_t>(sm_count) * 8));
+  const int spt = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kZdWords / F, want)));
   static int per_sm = 0;
   if (!per_sm && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coef_ztrans_direct,
                                                                kZdThreads, 0) != cudaSuccess)

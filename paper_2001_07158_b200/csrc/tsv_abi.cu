@@ -501,6 +501,11 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const char* zt_env = std::getenv("TSV_ZTRANS");
   const bool zt_tab = zt_env && std::strcmp(zt_env, "tab") == 0;
   DevBuf mlist(S * 8, st), mcount(4, st);
+  // expected listed rows: slots x the multi-shade share of the shaded vertices
+  const int64_t rows_hint =
+      vc ? static_cast<int64_t>(S)
+         : static_cast<int64_t>(static_cast<double>(S) * static_cast<double>(sh->multi) /
+                                static_cast<double>(std::max<int64_t>(sh->multi + sh->single, 1)));
   if (zt_tab)
     tsv::launch_slot_head(g->dev.R, g->dev.run_slot, g->dev.run_head, slot_head.as<int32_t>(), st);
   else if (k > 2)
@@ -582,7 +587,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
         tsv::launch_coef_ztrans_direct(g->dev.S, static_cast<int>(T.count[l]), l,
                                        mlist.as<int2>(), mcount.as<int32_t>(),
                                        d_zj.as<uint64_t>(), k, B, rs(l), dp + poff[l],
-                                       vc ? nullptr : fb, sms, st);
+                                       vc ? nullptr : fb, sms, rows_hint, st);
       std::swap(A, B);
       std::swap(fa, fb);
     }
