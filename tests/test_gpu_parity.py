@@ -211,6 +211,29 @@ def test_coefficient_engine_kernels_agree(cuda_device, monkeypatch, env):
     assert nz >= 8
 
 
+@pytest.mark.parametrize("env", [{}, {"TSV_ENGINE": "points"}])
+def test_coefficient_engine_large_k_vs_oracle(cuda_device, monkeypatch, env):
+    """k = 9..12 (C4's k_eff is 12): frames above 64 words take the shared-
+    memory item kernel, multi-shade rows the direct z map with up to 924
+    entries per row; colorful, repeated-color and anchored queries, hubs."""
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    rng = np.random.default_rng(61)
+    n, m, t = 90, 2500, 60
+    u = rng.integers(0, n, m)
+    v = np.where(rng.random(m) < 0.25, 0, rng.integers(0, n, m))
+    ts = rng.integers(1, t + 1, m)
+    colors = rng.integers(1, 13, n)                # 12 colors; 13+ absent
+    nz = 0
+    for motif, seed, mt, anchor in ((list(range(1, 10)), 3, None, (-1, -1)),
+                                     ([1, 1, 2, 3, 4, 5, 6, 7, 8, 9], 5, 50, (-1, -1)),
+                                     (list(range(1, 12)), 7, None, (2, 5)),
+                                     ([1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12], 9, None, (-1, -1)),
+                                     ([1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6], 11, 45, (-1, -1))):
+        nz += bool(_oracle_vs_gpu(n, u, v, ts, True, colors, motif, seed, anchor, mt))
+    assert nz == 5
+
+
 def test_c2_shape_small_scale_vs_oracle(cuda_device):
     inst = synth.make_config(2, scale=0.01)   # n=1e3, m=1e4, k=6 PathMotif
     k, col, motif, anchor = synth.effective_query(inst)
