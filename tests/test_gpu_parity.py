@@ -173,14 +173,15 @@ def test_engine_paths_agree(cuda_device, monkeypatch, env, ppb):
 @pytest.mark.parametrize("env", [{"TSV_ENGINE": "points"}, {"TSV_ITEMS": "0"},
                                  {"TSV_ITEMS": "1", "TSV_ITEMS_REG": "0"}, {"TSV_ITEMS": "1"},
                                  {"TSV_ZTRANS": "tab"}, {"TSV_SUBGRAPH": "0"},
-                                 {"TSV_PERSIST": "0"}])
+                                 {"TSV_PERSIST": "0"}, {"TSV_WALK_SPLIT": "0"}])
 def test_coefficient_engine_kernels_agree(cuda_device, monkeypatch, env):
     """Every arc kernel of the coefficient engine (k_coef_arcs, the item
     stream k_coef_items, its register-walk form k_coef_items_reg for frames
     <= 64 words, one and two entries per lane), both z maps of multi-shade
     rows (direct and table), with and without the shaded subgraph (arcs
     touching shadeless vertices dropped, edge ids kept) and the persistent
-    chunk loop, and the point engine give the
+    chunk loop, with and without the half-warp split walk (frames <= 16),
+    and the point engine give the
     oracle's accumulators: single-shade, multi-shade and shadeless vertices,
     hubs split across chunks, horizons below t, (s,d) anchors, undirected
     graphs, k = 2..8."""
