@@ -158,6 +158,9 @@ void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
                uint64_t* acc, cudaStream_t st, const int32_t* colors = nullptr,
                int32_t color = -1, int32_t wild = -1);
 // positional z_{u,j} = draw(seed, label_z, u, j+1) (build_zj_positional, sieve.cpp:103-113)
+// launch_zj with w = identity (the coefficient engine's shade basis)
+void launch_zj_ident(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
+                     const int32_t* vertex_shades, uint64_t* zj, cudaStream_t st);
 void launch_zj_positional(int32_t n, int k, uint64_t seed, uint64_t* zj, cudaStream_t st);
 // Edge-constrained level (ec_impl, sieve.cpp:477-536): the arcs of edges
 // [e0, e1) (one timestamp) add z_head * y(e, l-1) * prev[tail] into cur[head]

@@ -627,6 +627,25 @@ __global__ void k_zj(int32_t n, int k, uint64_t seed,
   for (int j = 0; j < k; ++j) zj[u * k + j] = row[j];
 }
 
+// The shade basis (coefficient engine): w = identity, so z_{u,d} = v_{u,d}
+// for d in S(u) and 0 otherwise -- no products, no per-thread row array.
+__global__ void k_zj_ident(int32_t n, int k, uint64_t seed,
+                           const int32_t* __restrict__ vertex_off,
+                           const int32_t* __restrict__ vertex_shades, uint64_t* __restrict__ zj) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const uint64_t pre = draw_prefix(seed, kRoleShadeV);
+  const int32_t s0 = vertex_off[u], s1 = vertex_off[u + 1];
+  uint32_t have = 0;
+  for (int32_t s = s0; s < s1; ++s) have |= 1u << (vertex_shades[s] - 1);
+  for (int j = 0; j < k; ++j)
+    if (!((have >> j) & 1u)) zj[u * k + j] = 0;
+  for (int32_t s = s0; s < s1; ++s) {
+    const int d = vertex_shades[s];
+    zj[u * k + d - 1] = draw_nonzero_from(pre, static_cast<uint64_t>(u), static_cast<uint64_t>(d), 0);
+  }
+}
+
 __global__ void k_zj_positional(int32_t n, int k, uint64_t seed, uint64_t* __restrict__ zj) {
   const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u >= n) return;
@@ -813,6 +832,14 @@ void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n, uint64_t* 
   prof_begin("xor_combine", st);
   const unsigned blocks = blocks_for(n, 256) < 148 * 8 ? blocks_for(n, 256) : 148 * 8;
   k_xor_combine<<<blocks, 256, 0, st>>>(parts, nparts, n, out);
+  prof_end(st);
+}
+
+void launch_zj_ident(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
+                     const int32_t* vertex_shades, uint64_t* zj, cudaStream_t st) {
+  if (n == 0) return;
+  prof_begin("zj", st);
+  k_zj_ident<<<blocks_for(n, 256), 256, 0, st>>>(n, k, seed, vertex_off, vertex_shades, zj);
   prof_end(st);
 }
 

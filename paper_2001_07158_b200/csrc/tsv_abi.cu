@@ -475,8 +475,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
         W[static_cast<size_t>(d) * k + j] = tsv::draw_nonzero_from(pre, d + 1, j + 1, 0);
     }
     scale = tsv::gf_det_host(W.data(), k);
-    tsv::launch_zj(nn, k, cfg->seed, sh->off, sh->shades, coef_const(dev, k, false).ident,
-                   d_zj.as<uint64_t>(), st);
+    tsv::launch_zj_ident(nn, k, cfg->seed, sh->off, sh->shades, d_zj.as<uint64_t>(), st);
   }
   DevBuf X(S * M * 8, st), Y(S * M * 8, st), agg(C * M * 8, st);
   DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(std::getenv("TSV_ZTRANS") ? S * 4 : 8, st);
