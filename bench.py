@@ -216,7 +216,7 @@ def run_reference(args, rank, world):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic", "config": config_json(inst, world, args),
+            "data": "synthetic", "config": config_json(inst, world, args, cpu=True),
             "cpu_baseline": {"value": value, "unit": "updates/s", "cores": info[2],
                              "kind": info[1], "sample": info[0]},
             "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
@@ -227,16 +227,20 @@ def run_reference(args, rank, world):
 METRIC = "GF(2^64) edge x level x sieve-pt updates/s (decide)"
 
 
-def config_json(inst, world, args):
+def config_json(inst, world, args, cpu=False):
     k_eff = inst.k_eff
+    l2 = ("host arm: the reference's CPU code, no device cache involved" if cpu else
+          "flushed before every step: a 256 MB buffer (2x the 126 MB L2) is "
+          "zeroed on the bench stream inside the timed region")
     return {"workload": f"BASELINE configs[{args.config - 1}]: {inst.name}"
                         + ("" if args.scale == 1.0 else f" (scaled x{args.scale})"), "n": inst.n,
             "m": inst.m, "t": inst.t, "directed": inst.directed, "k_eff": k_eff,
             "sieve_points": 1 << k_eff, "repetitions": REPS[args.config],
             "updates_per_step": inst.updates() * REPS[args.config],
-            "parallelism": f"sieve-point sharding x{world}",
-            "l2": "flushed before every step: a 256 MB buffer (2x the 126 MB L2) is "
-                  "zeroed on the bench stream inside the timed region"}
+            "parallelism": (f"repetitions / sieve points over {world} GPU(s) (shard.plan_units)"
+                            if not cpu else
+                            "reference CPU code on all host threads (rank 0)"),
+            "l2": l2}
 
 
 # ---------------------------------------------------------------- our arm
