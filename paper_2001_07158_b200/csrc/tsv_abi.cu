@@ -166,6 +166,11 @@ void prof_end(cudaStream_t st) {
 
 }  // namespace tsv
 
+inline uint64_t next_graph_uid() {
+  static std::atomic<uint64_t> ctr{1};
+  return ctr.fetch_add(1);
+}
+
 struct tsv_shades {
   int k = 0;
   int32_t n = 0;
@@ -179,7 +184,7 @@ struct tsv_shades {
   // 2 not worth it (most arcs kept) or not applicable
   mutable std::mutex sub_mu;
   mutable int sub_state = 0;
-  mutable const tsv_graph* sub_of = nullptr;
+  mutable uint64_t sub_of = 0;  // uid of the graph the subgraph was built from
   mutable std::shared_ptr<tsv_graph> sub;
   ~tsv_shades() {
     int prev = 0;
@@ -192,6 +197,8 @@ struct tsv_shades {
 };
 
 struct tsv_graph {
+  // process-unique id (a freed graph's address may be reused by a new one)
+  const uint64_t uid = next_graph_uid();
   tsv::HostLayout host;  // n, t, directed, drop counts (+ canonical edges if host-built)
   tsv::DevGraph dev;
   int device = 0;
@@ -918,12 +925,12 @@ const tsv_graph* shaded_subgraph(const tsv_graph* g, const tsv_shades* sh) {
   const char* env = std::getenv("TSV_SUBGRAPH");
   if (g->model != 0 || (env && env[0] == '0') || g->host.n == 0) return g;
   std::lock_guard<std::mutex> lk(sh->sub_mu);
-  if (sh->sub_of == g) {
+  if (sh->sub_of == g->uid) {
     if (sh->sub_state == 1) return sh->sub.get();
     if (sh->sub_state == 2) return g;
   }
   sh->sub.reset();
-  sh->sub_of = g;
+  sh->sub_of = g->uid;
   sh->sub_state = 2;
   DeviceGuard dg(g->device);
   cudaStream_t st = nullptr;
