@@ -321,7 +321,7 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
             "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
             "kernel": {"coef_arcs": "k_coef_items / k_coef_arcs (3 <= l < k)",
                        "coef_ztrans": "k_coef_ztrans_tab (2 <= l < k)"}[name],
-            "engine": "coefficient (top-degree) form, DESIGN.md 6b",
+            "engine": "coefficient (top-degree) form on the shaded subgraph, DESIGN.md 2b",
             "avg_launch_ms": tot_ms / n_launch,
             "alg_bytes_per_launch": alg[name] / n_launch,
             "kernel_ms_per_eval": {nm: coef[nm][1] / max(evals, 1) for nm in coef}}

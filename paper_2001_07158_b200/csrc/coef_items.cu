@@ -1,6 +1,6 @@
 // coef_items.cu -- the coefficient engine's arc pass as an item stream over
 // compact shade frames (used whenever the shade table has vertices with a
-// single shade; DESIGN.md section 6b).
+// single shade; DESIGN.md section 2b).
 //
 // In the shade basis (coef_kernels.cu, top) the level-l state of a run is
 // indexed by the l-subsets T of the k shades.  A vertex h with exactly one
