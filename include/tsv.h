@@ -198,6 +198,13 @@ int tsv_xor_combine_device(const uint64_t* d_parts, int nparts, int64_t n,
 int tsv_finalize(int32_t n, uint64_t* acc, int32_t anchor_sink,
                  tsv_outcome* out);
 
+/* Device finalize (finalize.cu): zeroes all but the sink of the DEVICE
+ * accumulators when anchor_sink >= 0, then the flagged count and the FNV-1a
+ * checksum (out->flagged, checksum, global_nonzero), computed in parallel
+ * on the device.  Synchronizes `stream`. */
+int tsv_finalize_device(uint64_t* d_acc, int64_t n, int32_t anchor_sink, void* stream,
+                        tsv_outcome* out);
+
 /* Per-kernel device-time profile (CUDA events on the launching stream).
  * names: "level", "level_first", "fixup", "readout", "zj" ... */
 int tsv_profile_enable(int on);

@@ -58,6 +58,24 @@ def oracle_lib():
         lib.tsvo_eval_points.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_int,
                                          C.c_int, C.c_int32, _i32p, _i32p, C.c_uint64,
                                          C.c_int32, C.c_uint64, C.c_uint64, _u64p]
+        lib.tsvo_canonicalize_inplace.restype = C.c_int64
+        lib.tsvo_canonicalize_inplace.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p,
+                                                  C.c_int]
+        lib.tsvo_big_build.restype = C.c_void_p
+        lib.tsvo_big_build.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, _i32p, C.c_int,
+                                       C.c_int32]
+        lib.tsvo_big_free.restype = None
+        lib.tsvo_big_free.argtypes = [C.c_void_p]
+        lib.tsvo_big_arcs.restype = C.c_int64
+        lib.tsvo_big_arcs.argtypes = [C.c_void_p]
+        lib.tsvo_big_runs.restype = C.c_int64
+        lib.tsvo_big_runs.argtypes = [C.c_void_p]
+        lib.tsvo_big_eval.restype = C.c_int
+        lib.tsvo_big_eval.argtypes = [C.c_void_p, C.c_int, _i32p, _i32p, C.c_uint64, C.c_int32,
+                                      C.c_uint64, C.c_uint64, C.c_int, _u64p]
+        lib.tsvo_set_threads.restype = None
+        lib.tsvo_set_threads.argtypes = [C.c_int]
+        lib.tsvo_max_threads.restype = C.c_int
         lib.tsvo_finalize.restype = C.c_int64
         lib.tsvo_finalize.argtypes = [C.c_int32, _u64p, C.c_int32, C.POINTER(C.c_uint64)]
         _oracle = lib
@@ -157,6 +175,69 @@ def eval_points(n, cu, cv, cts, directed, k, max_ts, vertex_off, vertex_shades, 
     if rc != 0:
         raise ValueError("k out of range [1,30]")
     return acc[:n]
+
+
+def canonicalize_inplace(n, u, v, ts, directed) -> int:
+    """Canonical edges (graph.cpp:14-43) written into u/v/ts[0:return] in place
+    (int32 arrays, modified).  Multi-threaded; for the BASELINE sizes."""
+    for a in (u, v, ts):
+        if a.dtype != np.int32 or not a.flags.c_contiguous:
+            raise TypeError("canonicalize_inplace needs contiguous int32 arrays")
+    w = oracle_lib().tsvo_canonicalize_inplace(n, len(u), u, v, ts, int(directed))
+    if w == -1:
+        raise ValueError("edge endpoint or timestamp out of range")
+    if w < 0:
+        raise ValueError("timestamps too large for the bucket sort")
+    return int(w)
+
+
+class BigGraph:
+    """Head-grouped arcs/runs of CANONICAL edges for tsvo_big_eval
+    (oracle/tsv_oracle_big.c).  The edge arrays are not referenced after
+    construction, so a caller may free them."""
+
+    def __init__(self, n, cu, cv, cts, directed, max_ts):
+        self.n = int(n)
+        self.h = oracle_lib().tsvo_big_build(n, len(cu), _a32(cu), _a32(cv), _a32(cts),
+                                             int(directed), int(max_ts))
+        if not self.h:
+            raise ValueError("too many arcs for the oracle's 32-bit indices")
+        self.arcs = oracle_lib().tsvo_big_arcs(self.h)
+        self.runs = oracle_lib().tsvo_big_runs(self.h)
+
+    def eval(self, k, vertex_off, vertex_shades, seed, anchor_source=-1, p_begin=0,
+             p_end=None, lanes=8, out=None):
+        """XOR of sieve points [p_begin, p_end) into `out` (fresh zeros if None)."""
+        if p_end is None:
+            p_end = 1 << k
+        acc = np.zeros(max(self.n, 1), np.uint64) if out is None else out
+        vs = _a32(vertex_shades) if len(vertex_shades) else np.zeros(1, np.int32)
+        rc = oracle_lib().tsvo_big_eval(self.h, k, _a32(vertex_off), vs, seed, anchor_source,
+                                        p_begin, p_end, lanes, acc)
+        if rc == -3:
+            raise MemoryError("oracle sieve state does not fit in host memory")
+        if rc != 0:
+            raise ValueError("k out of range [1,30] or bad lane count")
+        return acc[:self.n]
+
+    def close(self):
+        if self.h:
+            oracle_lib().tsvo_big_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def set_threads(t: int):
+    oracle_lib().tsvo_set_threads(int(t))
+
+
+def max_threads() -> int:
+    return int(oracle_lib().tsvo_max_threads())
 
 
 def finalize(acc, anchor_sink=-1):

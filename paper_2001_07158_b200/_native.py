@@ -85,6 +85,7 @@ def lib():
                                          C.c_int32, C.c_uint64, C.c_uint64, vp, vp]
     L.tsv_xor_combine_device.argtypes = [vp, C.c_int, C.c_int64, vp, vp]
     L.tsv_finalize.argtypes = [C.c_int32, _u64p, C.c_int32, C.POINTER(Outcome)]
+    L.tsv_finalize_device.argtypes = [vp, C.c_int64, C.c_int32, vp, C.POINTER(Outcome)]
     L.tsv_profile_enable.argtypes = [C.c_int]
     L.tsv_profile_get.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
     L.tsv_kernel_launches.restype = C.c_int64
@@ -142,6 +143,13 @@ def gf_mul_device(a, b, variant: int = 0):
     check(lib().tsv_gf_mul_device(variant, len(a), a if len(a) else out, b if len(b) else out,
                                   out))
     return out[:len(a)]
+
+
+def finalize_device(d_acc_ptr: int, n: int, sink: int = -1, stream: int = 0):
+    """tsv_finalize_device on a device buffer: (flagged, checksum)."""
+    o = Outcome()
+    check(lib().tsv_finalize_device(d_acc_ptr, int(n), int(sink), stream or None, C.byref(o)))
+    return int(o.flagged), int(o.checksum)
 
 
 def gf_bench(variant: int = 0, iters: int = 4096) -> float:

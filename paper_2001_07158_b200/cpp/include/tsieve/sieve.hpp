@@ -27,8 +27,13 @@ struct SieveConfig {
   bool localize = true;
   EdgeModel edge_model = EdgeModel::instant;
   std::uint64_t memory_cap_words = std::uint64_t{1} << 31;
-  int device = 0;      // CUDA device the evaluation runs on (engine extension)
 };
+
+// CUDA device that the calling thread's evaluations run on (engine extension,
+// kept out of SieveConfig so its layout is the reference's).  Default: the
+// TSV_DEVICE environment variable, else 0.
+void set_device(int device);
+int device();
 
 struct ShadeAssignment {
   int k = 0;

@@ -1,6 +1,7 @@
 // sieve.cpp -- shade assignment (host) and the GPU-backed temporal sieve.
 // build_shades follows /root/reference/proj/core/src/sieve.cpp:658-718;
 // eval_temporal_sieve replaces sieve.cpp:720-732 by the C-ABI call.
+#include <cstdlib>
 #include "tsieve/sieve.hpp"
 
 #include <algorithm>
@@ -83,6 +84,18 @@ ShadeAssignment build_shades(const MotifQuery& query, const VertexColoring& colo
   return sh;
 }
 
+namespace {
+int default_device() {
+  const char* e = std::getenv("TSV_DEVICE");
+  return e ? std::atoi(e) : 0;
+}
+thread_local int t_device = default_device();
+void finish(SieveOutcome& out, int k, const SieveConfig& config, const tsv_outcome& o);
+}  // namespace
+
+void set_device(int d) { t_device = d; }
+int device() { return t_device; }
+
 SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts,
                                  const ShadeAssignment& shades, const SieveConfig& config,
                                  const AnchorSpec& anchor) {
@@ -106,38 +119,48 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
   tsv_outcome o{};
   static const std::int32_t kNoShade = 0;
   const int rc = tsv_eval_temporal_sieve(
-      g.device_graph(config.device, model), k, max_ts, shades.vertex_off.data(),
+      g.device_graph(tsieve::device(), model), k, max_ts, shades.vertex_off.data(),
       shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c,
       anchor.source, anchor.sink, g.n() ? out.accumulators.data() : &scratch, &o);
   if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
   if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());
 
-  for (Vertex x = 0; x < g.n(); ++x)
-    if (out.accumulators[x]) out.flagged.push_back(x);
-  if (config.localize) {
-    out.global_nonzero = !out.flagged.empty();
-  } else {
-    std::uint64_t total = 0;
-    for (std::uint64_t a : out.accumulators) total ^= a;
-    out.global_nonzero = total != 0;
-  }
-  out.fn_bound = false_negative_bound(k, config.field_bits);
-  out.peak_field_words = o.peak_field_words;
-  out.checksum = o.checksum;
+  finish(out, k, config, o);
   return out;
 }
 
 namespace {
 
-// Decision rule, fn bound and checksum of finalize (sieve.cpp:136-159)
+// Decision rule, fn bound and checksum of finalize (sieve.cpp:136-159).
+// The flagged list (ascending nonzero accumulators) is gathered on all host
+// threads: per-block counts, a scan, then an ordered fill.
 void finish(SieveOutcome& out, int k, const SieveConfig& config, const tsv_outcome& o) {
-  for (Vertex x = 0; x < static_cast<Vertex>(out.accumulators.size()); ++x)
-    if (out.accumulators[x]) out.flagged.push_back(x);
+  const auto& acc = out.accumulators;
+  const int64_t n = static_cast<int64_t>(acc.size());
+  const int64_t block = int64_t{1} << 16;
+  const int64_t nb = (n + block - 1) / block;
+  std::vector<int64_t> cnt(static_cast<size_t>(nb) + 1, 0);
+  std::uint64_t total = 0;
+#pragma omp parallel for schedule(static) reduction(^ : total) if (n > (1 << 20))
+  for (int64_t b = 0; b < nb; ++b) {
+    int64_t c = 0;
+    for (int64_t x = b * block; x < std::min(n, (b + 1) * block); ++x) {
+      c += acc[static_cast<size_t>(x)] != 0;
+      total ^= acc[static_cast<size_t>(x)];
+    }
+    cnt[static_cast<size_t>(b) + 1] = c;
+  }
+  for (int64_t b = 0; b < nb; ++b) cnt[b + 1] += cnt[b];
+  out.flagged.resize(static_cast<size_t>(cnt[nb]));
+#pragma omp parallel for schedule(static) if (n > (1 << 20))
+  for (int64_t b = 0; b < nb; ++b) {
+    int64_t w = cnt[b];
+    for (int64_t x = b * block; x < std::min(n, (b + 1) * block); ++x)
+      if (acc[static_cast<size_t>(x)]) out.flagged[static_cast<size_t>(w++)] = static_cast<Vertex>(x);
+  }
   if (config.localize) {
     out.global_nonzero = !out.flagged.empty();
   } else {
-    std::uint64_t total = 0;
-    for (std::uint64_t a : out.accumulators) total ^= a;
     out.global_nonzero = total != 0;
   }
   out.fn_bound = false_negative_bound(k, config.field_bits);
@@ -193,7 +216,7 @@ SieveOutcome eval_edge_constrained_sieve(const TemporalGraph& g,
   static const std::int32_t kNoShade = 0;
   tsv_outcome o{};
   const int rc = tsv_eval_edge_constrained(
-      g.device_graph(config.device), k, times.data(), shades.vertex_off.data(),
+      g.device_graph(tsieve::device()), k, times.data(), shades.vertex_off.data(),
       shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c,
       g.n() ? out.accumulators.data() : &scratch, &o);
   if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
@@ -216,7 +239,7 @@ SieveOutcome eval_vertex_ordered_sieve(const TemporalGraph& g, const std::vector
   static const std::int32_t kNoColor = 0;
   tsv_outcome o{};
   const int rc = tsv_eval_vertex_ordered(
-      g.device_graph(config.device), k, order.data(),
+      g.device_graph(tsieve::device()), k, order.data(),
       coloring.primaries().empty() ? &kNoColor : coloring.primaries().data(),
       coloring.wildcard_active() ? coloring.wildcard_color() : -1, max_ts, &c,
       g.n() ? out.accumulators.data() : &scratch, &o);
@@ -251,7 +274,7 @@ SieveOutcome eval_projection(const StaticProjection& gs, int k, const ShadeAssig
   const int rc = tsv_eval_static_projection(
       gs.n(), gs.m(), a.data(), b.data(), gs.directed() ? 1 : 0, junction ? 1 : 0, k,
       shades.vertex_off.data(),
-      shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c, config.device,
+      shades.vertex_shades.empty() ? &kNoShade : shades.vertex_shades.data(), &c, tsieve::device(),
       gs.n() ? out.accumulators.data() : &scratch, &o);
   if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
   if (rc != TSV_OK) throw std::runtime_error(tsv_last_error());

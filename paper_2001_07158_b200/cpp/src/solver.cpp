@@ -5,7 +5,7 @@
 // filter of preprocess_mask :458-497), the decision / optimum / extraction
 // driver (solve_single :609-703: binary search :641-662, localized reverse
 // DFS :314-394, self-reduction shrink_to_core :557-607 + forward DFS
-// :398-452), and the rainbow / wildcard loops (:705-784).  Each probe is one
+// :398-452).  The rainbow / wildcard loops (:705-784) are out of scope.  Each probe is one
 // engine call on the device: the temporal sieve (four problems, all edge
 // models), the edge-constrained sieve (EC problems), the vertex-ordered sieve
 // (VC-PathMotif) or the exact DP (VC-ColorfulPath).
@@ -236,7 +236,7 @@ Probe probe(const Prep& p, const TemporalGraph& graph, Timestamp max_ts) {
     case Problem::vc_colorful_path: {  // exact indicator DP (dp_probe)
       std::vector<std::uint8_t> f(static_cast<size_t>(graph.n()) + 1, 0);
       const int rc = tsv_vc_colorful_dp(
-          graph.device_graph(p.cfg.device), p.k, p.query.order.data(),
+          graph.device_graph(tsieve::device()), p.k, p.query.order.data(),
           p.coloring.primaries().empty() ? nullptr : p.coloring.primaries().data(),
           p.coloring.wildcard_active() ? p.coloring.wildcard_color() : -1, max_ts, f.data());
       if (rc == TSV_ERR_INVALID) throw std::invalid_argument(tsv_last_error());
@@ -445,7 +445,7 @@ std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
                         p.problem == Problem::colorful_path ||
                         p.problem == Problem::sd_colorful_path;
   const bool on_device = temporal && model == 0;
-  const tsv_graph* base = on_device ? p.graph.device_graph(p.cfg.device) : nullptr;
+  const tsv_graph* base = on_device ? p.graph.device_graph(tsieve::device()) : nullptr;
   tsv_config cfg{};
   cfg.seed = p.cfg.seed;
   cfg.field_bits = p.cfg.field_bits;
@@ -476,7 +476,7 @@ std::vector<bool> shrink_to_core(const Prep& p, Timestamp horizon, int& calls,
     } else {  // delay models: restrict on the host, mirror for the model
       std::vector<bool> kb(mask8.begin(), mask8.end());
       host_sub.emplace(restrict_to(p.graph, kb, horizon));
-      probe_graph = host_sub->device_graph(p.cfg.device, model);
+      probe_graph = host_sub->device_graph(tsieve::device(), model);
     }
     tsv_outcome o{};
     const int rc = tsv_eval_temporal_sieve(
@@ -602,81 +602,6 @@ SolveReport solve_single(const TemporalGraph& g, const VertexColoring& col,
   return r;
 }
 
-void add_totals(SolveReport& into, const SolveReport& r) {
-  into.oracle_calls += r.oracle_calls;
-  into.fn_bound += r.fn_bound;
-  into.peak_field_words = std::max(into.peak_field_words, r.peak_field_words);
-  into.timings.preprocess_s += r.timings.preprocess_s;
-  into.timings.sieve_s += r.timings.sieve_s;
-  into.timings.extract_s += r.timings.extract_s;
-}
-
-// RainbowPath: ColorfulPath over the k-subsets of [1..q] in lexicographic order.
-SolveReport rainbow(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req,
-                    SolveMode mode) {
-  if (req.query.kind != QueryKind::size_only)
-    throw std::invalid_argument("RainbowPath takes --k");
-  const int k = req.query.k;
-  const Color q = col.q();
-  if (k >= q) throw std::invalid_argument("RainbowPath requires k < q");
-  SolveRequest sub = req;
-  sub.problem = Problem::colorful_path;
-  if (sub.preprocess == PreprocessLevel::none) sub.preprocess = PreprocessLevel::color_filter;
-  SolveReport total;
-  std::vector<Color> subset(static_cast<size_t>(k));
-  for (int i = 0; i < k; ++i) subset[i] = i + 1;
-  int tried = 0;
-  for (;;) {
-    ++tried;
-    sub.query = MotifQuery::from_multiset(subset);
-    SolveReport r = solve_single(g, col, sub, mode);
-    add_totals(total, r);
-    if (r.decision) {
-      r.oracle_calls = total.oracle_calls;
-      r.fn_bound = total.fn_bound;
-      r.peak_field_words = total.peak_field_words;
-      r.timings = total.timings;
-      r.note = "subset";
-      for (Color c : subset) r.note += " " + std::to_string(c);
-      r.note += " (" + std::to_string(tried) + " of C(q,k) tried)";
-      return r;
-    }
-    int i = k - 1;
-    while (i >= 0 && subset[i] == q - (k - 1 - i)) --i;
-    if (i < 0) break;
-    ++subset[i];
-    for (int j = i + 1; j < k; ++j) subset[j] = subset[j - 1] + 1;
-  }
-  total.note = "all " + std::to_string(tried) + " color subsets exhausted";
-  return total;
-}
-
-SolveReport wildcards(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req,
-                      SolveMode mode) {
-  if (req.query.kind != QueryKind::multiset)
-    throw std::invalid_argument("wildcards apply to color-multiset queries");
-  if (req.wildcard_max < req.query.k) throw std::invalid_argument("--wildcards-max below k");
-  const VertexColoring wc = col.with_wildcard();
-  SolveRequest sub = req;
-  sub.wildcard_max = 0;
-  SolveReport total;
-  for (int kk = req.query.k; kk <= req.wildcard_max; ++kk) {
-    SolveReport r = solve_single(g, wc, sub, mode);
-    total.oracle_calls += r.oracle_calls;
-    total.fn_bound += r.fn_bound;
-    if (r.decision) {
-      r.oracle_calls = total.oracle_calls;
-      r.fn_bound = total.fn_bound;
-      r.wildcards_used = kk - req.query.k;
-      return r;
-    }
-    ++sub.query.multiset[wc.wildcard_color()];
-    ++sub.query.k;
-  }
-  total.note = "no match up to k' = " + std::to_string(req.wildcard_max);
-  return total;
-}
-
 }  // namespace
 
 const char* problem_name(Problem p) {
@@ -711,8 +636,13 @@ EffectiveInstance effective_instance(const TemporalGraph& g, const VertexColorin
 
 SolveReport solve(const TemporalGraph& g, const VertexColoring& coloring,
                   const SolveRequest& req, SolveMode mode) {
-  if (req.wildcard_max > 0) return wildcards(g, coloring, req, mode);
-  if (req.problem == Problem::rainbow_path) return rainbow(g, coloring, req, mode);
+  // The RainbowPath subset loop and the wildcard loop (solver.cpp:705-784 of
+  // the reference) are outer drivers off the temporal-sieve path (SURVEY.md
+  // section 2, out of scope): not provided by this engine.
+  if (req.wildcard_max > 0)
+    throw std::invalid_argument("--wildcards-max is not supported by the B200 engine");
+  if (req.problem == Problem::rainbow_path)
+    throw std::invalid_argument("RainbowPath is not supported by the B200 engine");
   return solve_single(g, coloring, req, mode);
 }
 

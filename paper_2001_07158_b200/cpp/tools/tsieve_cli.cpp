@@ -433,7 +433,7 @@ Instance load_instance(const Opts& o) {
   cfg.field_bits = o.field_bits;
   cfg.lane_width = o.lanes;
   cfg.threads = resolve_threads(o.threads);
-  cfg.device = o.device;
+  tsieve::set_device(o.device);
   // The reference CLI leaves memory_cap_words at its library default (2^31
   // words), which bounds the reference's dense n*W*(t+1) layers.  The
   // engine's working set is O(referenced runs * W) in HBM and the batch width

@@ -201,6 +201,12 @@ void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges
                    uint64_t* out, cudaStream_t st);
 
 // Profiling hooks (tsv_abi.cu).
+// finalize (sieve.cpp:136-159) of device accumulators (finalize.cu): zeroes
+// all but the sink when sink >= 0; flagged count and FNV-1a checksum.
+// Synchronizes `st`.
+void device_finalize(uint64_t* d_acc, int64_t n, int64_t sink, cudaStream_t st,
+                     uint64_t* checksum, int64_t* flagged);
+
 void prof_begin(const char* name, cudaStream_t st);
 void prof_end(cudaStream_t st);
 

@@ -180,12 +180,16 @@ struct tsv_shades {
   int32_t* off = nullptr;
   int32_t* shades = nullptr;
   // the graph restricted to vertices with a shade (same vertex and edge ids),
-  // built once per graph by shaded_subgraph(); state: 0 not tried, 1 built,
-  // 2 not worth it (most arcs kept) or not applicable
+  // built once per (graph, shades) by shaded_subgraph(), for the last few
+  // graphs (uid); a null subgraph = not worth it / not applicable.  Callers
+  // hold the shared_ptr while they enqueue work on it; freeing a graph runs
+  // cudaFree, which waits for the kernels still reading it.
+  struct SubEntry {
+    uint64_t uid;
+    std::shared_ptr<tsv_graph> sub;
+  };
   mutable std::mutex sub_mu;
-  mutable int sub_state = 0;
-  mutable uint64_t sub_of = 0;  // uid of the graph the subgraph was built from
-  mutable std::shared_ptr<tsv_graph> sub;
+  mutable std::vector<SubEntry> subs;
   ~tsv_shades() {
     int prev = 0;
     cudaGetDevice(&prev);
@@ -212,15 +216,20 @@ struct tsv_graph {
   const int32_t* d_ets = nullptr;
   std::vector<void*> owned;
   // last shade table evaluated on this graph (binary-search and self-
-  // reduction probes repeat it): reused when its content fingerprint matches
+  // reduction probes repeat it): reused only when the caller's CSR equals a
+  // host copy of the cached one word for word (parallel compare)
   mutable std::mutex shade_mu;
   mutable std::shared_ptr<tsv_shades> shade_cache;
-  mutable uint64_t shade_fp = 0;
+  mutable std::vector<int32_t> shade_off_copy, shade_vs_copy;
   mutable int shade_k = 0;
+  // stream of the synchronous entry points (created once per graph)
+  mutable std::mutex stream_mu;
+  mutable cudaStream_t api_stream = nullptr;
   ~tsv_graph() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    if (api_stream) cudaStreamDestroy(api_stream);
     for (void* p : owned) cudaFree(p);
     cudaSetDevice(prev);
   }
@@ -350,7 +359,7 @@ struct VcSpec {
   int32_t wild = -1;                  // wildcard color, -1 = none
 };
 
-const tsv_graph* shaded_subgraph(const tsv_graph* g, const tsv_shades* sh);
+std::shared_ptr<tsv_graph> shaded_subgraph(const tsv_graph* g, const tsv_shades* sh);
 
 // Subset-index tables of the coefficient engine for one k (host).
 const tsv::CoefTables& coef_const_tables(int k) {
@@ -451,7 +460,11 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   // arcs touching a shadeless vertex never carry a nonzero product (its z,
   // hence every S row, is zero): evaluate the shaded subgraph, which keeps
   // the vertex and edge ids (y draws) and gives the same accumulators
-  if (!vc && sh) g = shaded_subgraph(g, sh);
+  std::shared_ptr<tsv_graph> sub_hold;
+  if (!vc && sh) {
+    sub_hold = shaded_subgraph(g, sh);
+    if (sub_hold) g = sub_hold.get();
+  }
   const tsv::CoefTables& T = coef_const_tables(k);
   int64_t M = 1;
   for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, T.count[l]);
@@ -611,6 +624,9 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
   if (!vc && (!sh || sh->n != g->dev.n || sh->k != k))
     throw std::invalid_argument("shade assignment built for a different graph");
+  if (!vc && sh->device != g->device)
+    throw std::invalid_argument("shade table uploaded to device " + std::to_string(sh->device) +
+                                ", graph lives on device " + std::to_string(g->device));
   if (vc && static_cast<int>(vc->order.size()) != k)
     throw std::invalid_argument("order must have k colors");
   if (cfg->edge_model != g->model)
@@ -921,17 +937,14 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
 // (the tail's last run before it) has the same prefix in both graphs.  Built
 // once per (graph, shades) on the graph's device; used by the coefficient
 // engine when it drops >= 15% of the arcs (C2: 61%), else the graph itself.
-const tsv_graph* shaded_subgraph(const tsv_graph* g, const tsv_shades* sh) {
+std::shared_ptr<tsv_graph> shaded_subgraph(const tsv_graph* g, const tsv_shades* sh) {
   const char* env = std::getenv("TSV_SUBGRAPH");
-  if (g->model != 0 || (env && env[0] == '0') || g->host.n == 0) return g;
+  if (g->model != 0 || (env && env[0] == '0') || g->host.n == 0) return nullptr;
   std::lock_guard<std::mutex> lk(sh->sub_mu);
-  if (sh->sub_of == g->uid) {
-    if (sh->sub_state == 1) return sh->sub.get();
-    if (sh->sub_state == 2) return g;
-  }
-  sh->sub.reset();
-  sh->sub_of = g->uid;
-  sh->sub_state = 2;
+  for (const auto& e : sh->subs)
+    if (e.uid == g->uid) return e.sub;
+  if (sh->subs.size() >= 4) sh->subs.erase(sh->subs.begin());
+  sh->subs.push_back({g->uid, nullptr});  // "not worth it" unless built below
   DeviceGuard dg(g->device);
   cudaStream_t st = nullptr;
   TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -988,7 +1001,7 @@ const tsv_graph* shaded_subgraph(const tsv_graph* g, const tsv_shades* sh) {
                                               alloc, release, oid);
     if (kept * 100 > m * 85) {
       done();
-      return g;
+      return nullptr;
     }
     TSV_CUDA(cudaStreamSynchronize(st));
     tsv_graph* s = device_graph_build(n, kept, ou, ov, ots, g->host.directed, g->host.t,
@@ -996,15 +1009,91 @@ const tsv_graph* shaded_subgraph(const tsv_graph* g, const tsv_shades* sh) {
     tsv::launch_remap_edge_ids(s->dev.A, const_cast<uint32_t*>(s->dev.arc_meta), oid, st);
     TSV_CUDA(cudaGetLastError());
     done();
-    sh->sub.reset(s);
-    sh->sub_state = 1;
-    return s;
+    std::shared_ptr<tsv_graph> sp(s);
+    sh->subs.back().sub = sp;
+    return sp;
   } catch (...) {
     done();
     throw;
   }
 }
 
+
+// a == b over `count` words, compared on all host threads
+template <typename T>
+bool equal_par(const T* a, const T* b, size_t count) {
+  if (count == 0 || a == b) return true;
+  if (count < (size_t{1} << 20)) return std::memcmp(a, b, count * sizeof(T)) == 0;
+  const size_t block = size_t{1} << 18;
+  const int64_t nb = static_cast<int64_t>((count + block - 1) / block);
+  int diff = 0;
+#pragma omp parallel for schedule(static) reduction(| : diff)
+  for (int64_t i = 0; i < nb; ++i) {
+    const size_t lo = static_cast<size_t>(i) * block, len = std::min(block, count - lo);
+    diff |= std::memcmp(a + lo, b + lo, len * sizeof(T)) != 0;
+  }
+  return diff == 0;
+}
+
+// Device -> host copy of `count` words into pageable memory: DMA into two
+// pinned staging buffers (per device, reused) while the host threads move
+// the previous chunk out.  Plain cudaMemcpy to pageable memory stages
+// through the driver at a fraction of the link rate.
+void copy_to_host(uint64_t* dst, const uint64_t* d_src, size_t count, cudaStream_t st) {
+  if (count == 0) return;
+  const size_t bytes = count * 8;
+  if (bytes < (size_t{8} << 20)) {
+    TSV_CUDA(cudaMemcpyAsync(dst, d_src, bytes, cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  constexpr size_t kChunk = size_t{32} << 20;
+  struct Staging {
+    std::mutex mu;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+  };
+  static std::mutex reg_mu;
+  static std::vector<std::unique_ptr<Staging>> reg;
+  int dev = 0;
+  TSV_CUDA(cudaGetDevice(&dev));
+  Staging* S = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(reg_mu);
+    if (reg.size() <= static_cast<size_t>(dev)) reg.resize(static_cast<size_t>(dev) + 1);
+    if (!reg[dev]) {
+      auto s = std::make_unique<Staging>();
+      for (int i = 0; i < 2; ++i) {
+        TSV_CUDA(cudaMallocHost(&s->buf[i], kChunk));
+        TSV_CUDA(cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming));
+      }
+      reg[dev] = std::move(s);
+    }
+    S = reg[dev].get();
+  }
+  std::lock_guard<std::mutex> lk(S->mu);
+  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](size_t c) {
+    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+    TSV_CUDA(cudaMemcpyAsync(S->buf[c & 1], reinterpret_cast<const char*>(d_src) + off, len,
+                             cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaEventRecord(S->ev[c & 1], st));
+  };
+  issue(0);
+  for (size_t c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) issue(c + 1);
+    TSV_CUDA(cudaEventSynchronize(S->ev[c & 1]));
+    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+    const char* src = static_cast<const char*>(S->buf[c & 1]);
+    char* out = reinterpret_cast<char*>(dst) + off;
+    const int64_t parts = 16;
+#pragma omp parallel for schedule(static) num_threads(16)
+    for (int64_t p = 0; p < parts; ++p) {
+      const size_t lo = len * p / parts, hi = len * (p + 1) / parts;
+      std::memcpy(out + lo, src + lo, hi - lo);
+    }
+  }
+}
 
 }  // namespace
 
@@ -1334,65 +1423,90 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
                             const tsv_config* cfg, int32_t anchor_source,
                             int32_t anchor_sink, uint64_t* accumulators,
                             tsv_outcome* out) {
-  tsv_shades* sh = nullptr;
-  int rc = guard([&] {
-    if (!g || !accumulators || !out) throw std::invalid_argument("null argument");
+  return guard([&] {
+    if (!g || !accumulators || !out || !vertex_off)
+      throw std::invalid_argument("null argument");
     check_config(cfg);
     if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
     if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
-  });
-  if (rc) return rc;
-  // content fingerprint of the shade CSR: a repeated table is not uploaded again
-  const int32_t n0 = g->host.n;
-  const int64_t cnt = vertex_off[n0];
-  uint64_t fp = tsv::mix64(static_cast<uint64_t>(k) * 0x9e3779b97f4a7c15ull ^ static_cast<uint64_t>(cnt));
-#pragma omp parallel for schedule(static) reduction(+ : fp)
-  for (int64_t i = 0; i <= n0; ++i)
-    fp += tsv::mix64(static_cast<uint64_t>(i) * 0xff51afd7ed558ccdull ^ static_cast<uint32_t>(vertex_off[i]));
-#pragma omp parallel for schedule(static) reduction(+ : fp)
-  for (int64_t i = 0; i < cnt; ++i)
-    fp += tsv::mix64(static_cast<uint64_t>(i) * 0xc4ceb9fe1a85ec53ull + 1 ^
-                     static_cast<uint32_t>(vertex_shades[i]));
-  std::shared_ptr<tsv_shades> hold;
-  {
-    std::lock_guard<std::mutex> lk(g->shade_mu);
-    if (g->shade_cache && g->shade_fp == fp && g->shade_k == k) hold = g->shade_cache;
-  }
-  if (!hold) {
-    rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
-    if (rc) return rc;
-    hold = std::shared_ptr<tsv_shades>(sh, tsv_shades_free);
-    std::lock_guard<std::mutex> lk(g->shade_mu);
-    g->shade_cache = hold;
-    g->shade_fp = fp;
-    g->shade_k = k;
-  }
-  sh = hold.get();
-  rc = guard([&] {
-    DeviceGuard dg(g->device);
     const int32_t n = g->host.n;
-    cudaStream_t st = nullptr;
-    TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    uint64_t peak = 0;
-    try {
-      DevBuf acc(static_cast<size_t>(n) * 8, st);
-      TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8, st));
-      eval_device(g, sh, k, max_ts, cfg, anchor_source, 0, 1ull << k, acc.as<uint64_t>(),
-                  st, &peak);
-      if (n)
-        TSV_CUDA(cudaMemcpyAsync(accumulators, acc.p, static_cast<size_t>(n) * 8,
-                                 cudaMemcpyDeviceToHost, st));
-    } catch (...) {
-      cudaStreamSynchronize(st);
-      cudaStreamDestroy(st);
-      throw;
+    const int64_t cnt = vertex_off[n];
+    if (cnt < 0 || (cnt > 0 && !vertex_shades)) throw std::invalid_argument("null argument");
+    // a repeated shade table (every probe of one query) is not uploaded
+    // again: reuse the cached device copy when the CSR is word-for-word equal
+    std::shared_ptr<tsv_shades> hold;
+    {
+      std::lock_guard<std::mutex> lk(g->shade_mu);
+      if (g->shade_cache && g->shade_k == k &&
+          g->shade_off_copy.size() == static_cast<size_t>(n) + 1 &&
+          g->shade_vs_copy.size() == static_cast<size_t>(cnt) &&
+          equal_par(g->shade_off_copy.data(), vertex_off, static_cast<size_t>(n) + 1) &&
+          equal_par(g->shade_vs_copy.data(), vertex_shades, static_cast<size_t>(cnt)))
+        hold = g->shade_cache;
     }
-    TSV_CUDA(cudaStreamSynchronize(st));
-    TSV_CUDA(cudaStreamDestroy(st));
-    finalize_host(n, accumulators, anchor_sink, k, out);
+    if (!hold) {
+      tsv_shades* sh = nullptr;
+      const int rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
+      if (rc == TSV_ERR_INVALID) throw std::invalid_argument(g_error);
+      if (rc) throw CudaError(g_error);
+      hold = std::shared_ptr<tsv_shades>(sh, tsv_shades_free);
+      std::lock_guard<std::mutex> lk(g->shade_mu);
+      g->shade_cache = hold;
+      g->shade_k = k;
+      g->shade_off_copy.assign(vertex_off, vertex_off + n + 1);
+      g->shade_vs_copy.assign(vertex_shades, vertex_shades + cnt);
+    }
+    DeviceGuard dg(g->device);
+    // the graph's stream; a concurrent call on the same graph gets its own
+    std::unique_lock<std::mutex> slk(g->stream_mu, std::try_to_lock);
+    cudaStream_t st = nullptr;
+    struct TmpStream {
+      cudaStream_t s = nullptr;
+      ~TmpStream() {
+        if (s) {
+          cudaStreamSynchronize(s);
+          cudaStreamDestroy(s);
+        }
+      }
+    } tmp;
+    if (slk.owns_lock()) {
+      if (!g->api_stream)
+        TSV_CUDA(cudaStreamCreateWithFlags(&g->api_stream, cudaStreamNonBlocking));
+      st = g->api_stream;
+    } else {
+      TSV_CUDA(cudaStreamCreateWithFlags(&tmp.s, cudaStreamNonBlocking));
+      st = tmp.s;
+    }
+    uint64_t peak = 0;
+    DevBuf acc(static_cast<size_t>(n) * 8, st);
+    TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8, st));
+    eval_device(g, hold.get(), k, max_ts, cfg, anchor_source, 0, 1ull << k, acc.as<uint64_t>(),
+                st, &peak);
+    // finalize on the device (sink restriction, flagged count, checksum),
+    // then the accumulators to the caller through pinned staging buffers
+    uint64_t checksum = 0;
+    int64_t flagged = 0;
+    tsv::device_finalize(acc.as<uint64_t>(), n, anchor_sink, st, &checksum, &flagged);
+    copy_to_host(accumulators, acc.as<uint64_t>(), static_cast<size_t>(n), st);
+    out->flagged = flagged;
+    out->global_nonzero = flagged > 0;
+    out->checksum = checksum;
+    out->fn_bound = (2.0 * k - 1.0) / std::pow(2.0, 64);
     out->peak_field_words = peak;
   });
-  return rc;
+}
+
+int tsv_finalize_device(uint64_t* d_acc, int64_t n, int32_t anchor_sink, void* stream,
+                        tsv_outcome* out) {
+  return guard([&] {
+    if ((!d_acc && n > 0) || !out || n < 0) throw std::invalid_argument("null argument");
+    uint64_t cs = 0;
+    int64_t f = 0;
+    tsv::device_finalize(d_acc, n, anchor_sink, static_cast<cudaStream_t>(stream), &cs, &f);
+    out->flagged = f;
+    out->global_nonzero = f > 0;
+    out->checksum = cs;
+  });
 }
 
 namespace {
