@@ -3,16 +3,20 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
 A step is one DECIDE of the configured BASELINE workload: every repetition
-seed evaluates all 2^k_eff sieve points over the whole synthetic graph
-(default config 2 = BASELINE configs[1]: PathMotif k=6, n=1e5, m=1e6,
-4 repetitions).  Metric: GF(2^64) edge x level x sieve-point updates per
-second, updates = A * (k_eff - 1) * 2^k_eff per repetition.
+seed evaluates all 2^k_eff sieve points over the whole synthetic graph.
+Default: config 5 = BASELINE configs[4], the config the metric is quoted on
+(k-TempPath k=5, n=1e8, m=1e9, ts in [1,1e6], one repetition).  Metric:
+GF(2^64) edge x level x sieve-point updates per second, updates =
+A * (k_eff - 1) * 2^k_eff per repetition, and the decide wall time.  The
+coefficient engine computes the same sieve sums without visiting points,
+so for it the rate is an EQUIVALENT point-form rate (`value_kind`).
+
+Every run checks its decide against the committed full-size golden
+(tests/golden/full_size.json) and reports `parity`.
 
 With N > 1 (torchrun) the (repetition, sieve point) units of the decide are
-split into contiguous ranges (shard.work_units: whole repetitions while
-N <= reps, halves of one beyond), with no data-path collective; the
-per-vertex partial accumulators are XOR-combined once per step (NCCL
-all-gather + XOR kernel; NCCL has no XOR reduction).
+split (shard.plan_units), with no data-path collective; the per-vertex
+partial accumulators are XOR-combined once per step (shard.xor_allreduce).
 """
 from __future__ import annotations
 
@@ -151,102 +155,6 @@ def dist_env():
 
 
 
-# ------------------------------------------------------------------ CPU legs
-
-
-def cpu_sample(inst, k, colors, motif, anchor, seed=1, frac=0.1, threads=None):
-    """The reference's own eval_temporal_sieve (oracle/_ref) on a bounded
-    sample of the workload: the time prefix ts <= frac * t of the same graph
-    (all 2^k points, all levels).  Returns (updates/s, seconds, sample, kind, cores)."""
-    from oracle import oracle as O
-    threads = threads or os.cpu_count() or 1
-    max_ts = max(1, int(inst.t * frac))
-    arcs = int(np.count_nonzero(inst.ts <= max_ts)) * (1 if inst.directed else 2)
-    upd = arcs * (k - 1) * (1 << k)
-    sample = (f"ts <= {max_ts} of t={inst.t} ({arcs} arcs, all {1 << k} points, "
-              f"{k - 1} levels, seed {seed})")
-    # The reference's dense layers (2 n W (max_ts+1) words, sieve.cpp:188-192)
-    # only fit for configs 1-2; beyond that the validated sparse restatement
-    # (oracle port) stands in, on 2 of the sieve points.
-    dense_bytes = 2 * inst.n * 8 * (max_ts + 1) * 8
-    if O.ref_available() and dense_bytes < 24e9:
-        os.environ.setdefault("OMP_WAIT_POLICY", "active")
-        r = O.ref_eval(inst.n, inst.u, inst.v, inst.ts, inst.directed, colors, motif,
-                       max_ts=max_ts, seed=seed, lanes=8, threads=threads, anchor=anchor,
-                       t=inst.t, repeats=2)
-        return upd / r["seconds"], r["seconds"], sample, "reference", threads
-    # port: the time-prefix subgraph itself, bounded to ~2e6 arcs
-    max_ts = max(1, min(max_ts, int(inst.t * 2e6 / max(arcs / max(frac, 1e-9), 1))))
-    sel = inst.ts <= max_ts
-    arcs = int(np.count_nonzero(sel)) * (1 if inst.directed else 2)
-    cu, cv, ct = O.canonical_edges(inst.n, inst.u[sel], inst.v[sel], inst.ts[sel], inst.directed)
-    from paper_2001_07158_b200.sieve import SieveConfig, build_shades
-    from paper_2001_07158_b200.graph import MotifQuery, VertexColoring
-    sh = build_shades(MotifQuery.from_multiset(motif), VertexColoring(colors, int(colors.max())),
-                      SieveConfig(seed=seed))
-    npts = min(2, 1 << k)
-    upd = arcs * (k - 1) * npts
-    sample = (f"ts <= {max_ts} of t={inst.t} ({arcs} arcs, sieve points 0..{npts - 1}, "
-              f"{k - 1} levels, seed {seed}; sparse oracle port)")
-    t0 = time.perf_counter()
-    O.eval_points(inst.n, cu, cv, ct, inst.directed, k, max_ts, sh.vertex_off, sh.vertex_shades,
-                  seed, anchor[0], 0, npts)
-    s = time.perf_counter() - t0
-    return upd / s, s, sample, "port", 1
-
-
-def run_reference(args, rank, world):
-    """--impl reference: the reference CPU implementation on the host cores."""
-    if rank != 0:
-        return
-    from paper_2001_07158_b200 import synth
-    inst = synth.make_config(args.config, scale=args.scale)
-    k, colors, motif, anchor = synth.effective_query(inst)
-    times, rates = [], []
-    info = None
-    for i in range(args.warmup + args.steps):
-        rate, sec, sample, kind, cores = cpu_sample(inst, k, colors, motif, anchor,
-                                                    frac=args.ref_frac)
-        info = (sample, kind, cores)
-        if i >= args.warmup:
-            times.append(sec)
-            rates.append(rate)
-    value = statistics.median(rates)
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic", "config": config_json(inst, world, args, cpu=True),
-            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": info[2],
-                             "kind": info[1], "sample": info[0]},
-            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-
-
-METRIC = "GF(2^64) edge x level x sieve-pt updates/s (decide)"
-
-
-def config_json(inst, world, args, cpu=False):
-    k_eff = inst.k_eff
-    l2 = ("host arm: the reference's CPU code, no device cache involved" if cpu else
-          "flushed before every step: a 256 MB buffer (2x the 126 MB L2) is "
-          "zeroed on the bench stream inside the timed region")
-    return {"workload": f"BASELINE configs[{args.config - 1}]: {inst.name}"
-                        + ("" if args.scale == 1.0 else f" (scaled x{args.scale})"), "n": inst.n,
-            "m": inst.m, "t": inst.t, "directed": inst.directed, "k_eff": k_eff,
-            "sieve_points": 1 << k_eff, "repetitions": REPS[args.config],
-            "updates_per_step": inst.updates() * REPS[args.config],
-            "parallelism": (f"repetitions / sieve points over {world} GPU(s) (shard.plan_units)"
-                            if not cpu else
-                            "reference CPU code on all host threads (rank 0)"),
-            "l2": l2}
-
-
-# ---------------------------------------------------------------- our arm
-
-
-
 def coef_alg_bytes(g, sh, k):
     """Algorithmic bytes of one full evaluation by the coefficient engine, per
     kernel family ("Roofline"), from the graph and the
@@ -263,10 +171,20 @@ def coef_alg_bytes(g, sh, k):
         multi-shade head, C(k, l-1) entry) read + C(k, l) written."""
     from math import comb
     n = g.n()
+    cnt = np.diff(np.asarray(sh.vertex_off, dtype=np.int64))
+    if n and int(cnt.min()) >= 2:
+        # every vertex carries several shades (k-TempPath: all k): every
+        # arc with a predecessor run is live and carries C(k, l-1) entries,
+        # every referenced run is a multi-shade row -- closed form from the
+        # graph's own counts (no host pass over 1e9 edges)
+        a_src, S = g.info.arcs_with_src, g.info.runs_referenced
+        meta = 12 * g.info.arcs + 4 * g.info.runs
+        arcs = sum(8 * (a_src + S) * comb(k, l - 1) + meta for l in range(3, k))
+        ztrans = sum(8 * S * (comb(k, l - 1) + comb(k, l)) for l in range(2, k))
+        return {"coef_arcs": arcs, "coef_ztrans": ztrans}
     cu, cv, ct = (np.asarray(x, dtype=np.int64) for x in g.edges())
     if not g.directed():
         cu, cv, ct = np.concatenate([cu, cv]), np.concatenate([cv, cu]), np.concatenate([ct, ct])
-    cnt = np.diff(np.asarray(sh.vertex_off, dtype=np.int64))
     d1 = np.full(n, -1, np.int64)
     one = cnt == 1
     d1[one] = np.asarray(sh.vertex_shades, dtype=np.int64)[np.asarray(sh.vertex_off)[:-1][one]]
@@ -320,8 +238,9 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
             "kernel": {"coef_arcs": "k_coef_items / k_coef_arcs (3 <= l < k)",
-                       "coef_ztrans": "k_coef_ztrans_tab (2 <= l < k)"}[name],
+                       "coef_ztrans": "k_coef_ztrans_direct (2 <= l < k)"}[name],
             "engine": "coefficient (top-degree) form on the shaded subgraph, DESIGN.md 2b",
+            "family": name,
             "avg_launch_ms": tot_ms / n_launch,
             "alg_bytes_per_launch": alg[name] / n_launch,
             "kernel_ms_per_eval": {nm: coef[nm][1] / max(evals, 1) for nm in coef}}
@@ -346,19 +265,175 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
     return roof
 
 
+# ------------------------------------------------------------------ CPU legs
+
+METRIC = "GF(2^64) edge x level x sieve-pt updates/s (decide)"
+GOLDEN_FULL = os.path.join(ROOT, "tests", "golden", "full_size.json")
+DEFAULT_STEPS = {1: 50, 2: 20, 3: 10, 4: 3, 5: 5}
+DEFAULT_E2E = {1: 5, 2: 5, 3: 3, 4: 1, 5: 2}
+# CPU sample per config: the time prefix ts <= frac * t (10-30 s of host work)
+CPU_FRAC = {1: 1.0, 2: 0.1, 3: 0.1, 4: 0.002, 5: 0.01}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_sample(inst, k, colors, motif, anchor, seed=1, frac=None, threads=None, gpu_check=None):
+    """The reference's CPU implementation of the path on a BOUNDED sample of
+    the workload (the time prefix ts <= frac * t of the same graph, all 2^k
+    points, all levels), on all host threads.  Returns a dict.
+
+    Configs 1-2: the reference's own eval_temporal_sieve (oracle/_ref, the
+    unmodified core compiled by oracle/Makefile; kind "reference").  Configs
+    3-5: its dense layers (2 n W (t+1) words, sieve.cpp:188-192) cannot be
+    allocated, so the validated multi-threaded restatement stands in
+    (oracle/tsv_oracle_big.c; kind "port").  gpu_check(max_ts) -> the GPU's
+    accumulators on the same window, compared word for word."""
+    from oracle import oracle as O
+    threads = threads or os.cpu_count() or 1
+    if frac is None:
+        frac = CPU_FRAC[inst_cfg(inst)]
+    max_ts = max(1, int(inst.t * frac))
+    sel = inst.ts <= max_ts
+    arcs = int(np.count_nonzero(sel)) * (1 if inst.directed else 2)
+    upd = arcs * (k - 1) * (1 << k)
+    dense_bytes = 2 * inst.n * 8 * (max_ts + 1) * 8
+    res = {"threads": threads, "max_ts": max_ts, "arcs": arcs, "updates": upd}
+    if O.ref_available() and dense_bytes < 24e9:
+        os.environ.setdefault("OMP_WAIT_POLICY", "active")
+        r = O.ref_eval(inst.n, inst.u, inst.v, inst.ts, inst.directed, colors, motif,
+                       max_ts=max_ts, seed=seed, lanes=8, threads=threads, anchor=anchor,
+                       t=inst.t, repeats=2)
+        res.update(seconds=r["seconds"], kind="reference", acc=r["acc"],
+                   sample=f"ts <= {max_ts} of t={inst.t} ({arcs} arcs, all {1 << k} points, "
+                          f"{k - 1} levels, seed {seed}; reference eval_temporal_sieve, "
+                          f"best of 2)")
+    else:
+        from paper_2001_07158_b200.graph import MotifQuery, VertexColoring
+        from paper_2001_07158_b200.sieve import SieveConfig, build_shades
+        u = np.ascontiguousarray(inst.u[sel], dtype=np.int32)
+        v = np.ascontiguousarray(inst.v[sel], dtype=np.int32)
+        ts = np.ascontiguousarray(inst.ts[sel], dtype=np.int32)
+        O.set_threads(threads)
+        w = O.canonicalize_inplace(inst.n, u, v, ts, inst.directed)
+        G = O.BigGraph(inst.n, u[:w], v[:w], ts[:w], inst.directed, max_ts)
+        sh = build_shades(MotifQuery.from_multiset(motif),
+                          VertexColoring(colors, int(colors.max())), SieveConfig(seed=seed))
+        t0 = time.perf_counter()
+        acc = G.eval(k, sh.vertex_off, sh.vertex_shades, seed, anchor[0], lanes=16)
+        sec = time.perf_counter() - t0
+        G.close()
+        res.update(seconds=sec, kind="port", acc=acc,
+                   sample=f"ts <= {max_ts} of t={inst.t} ({arcs} arcs, all {1 << k} points, "
+                          f"{k - 1} levels, seed {seed}; oracle/tsv_oracle_big.c, the "
+                          f"reference's dense layers do not fit at this size)")
+    res["value"] = upd / res["seconds"]
+    if gpu_check is not None:
+        try:
+            res["window_parity"] = bool(np.array_equal(gpu_check(max_ts), res["acc"]))
+        except Exception as e:  # reported, never fatal
+            res["window_parity"] = f"unchecked: {e}"
+    return res
+
+
+def inst_cfg(inst):
+    return int(inst.name[1])
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU implementation on the host cores
+    (rank 0 only; other ranks exit without work)."""
+    if rank != 0:
+        return
+    from paper_2001_07158_b200 import synth
+    inst = synth.make_config(args.config, scale=args.scale)
+    k, colors, motif, anchor = synth.effective_query(inst)
+    times, rates = [], []
+    info = None
+    steps = args.steps or DEFAULT_STEPS[args.config]
+    for i in range(args.warmup + steps):
+        r = cpu_sample(inst, k, colors, motif, anchor, frac=args.ref_frac)
+        info = r
+        if i >= args.warmup:
+            times.append(r["seconds"])
+            rates.append(r["value"])
+    value = statistics.median(rates)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "updates/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * statistics.median(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic", "config": config_json(inst, world, args, cpu=True),
+            "cpu_baseline": {"value": value, "unit": "updates/s", "cores": info["threads"],
+                             "kind": info["kind"], "sample": info["sample"],
+                             "cpu_model": cpu_model()},
+            "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(inst, world, args, cpu=False):
+    k_eff = inst.k_eff
+    reps = REPS[args.config]
+    l2 = ("host arm: the reference's CPU code, no device cache involved" if cpu else
+          "flushed before every step: a 256 MB buffer (2x the 126 MB L2) is "
+          "zeroed on the bench stream inside the timed region")
+    return {"workload": f"BASELINE configs[{args.config - 1}]: {inst.name}"
+                        + ("" if args.scale == 1.0 else f" (scaled x{args.scale})"), "n": inst.n,
+            "m": inst.m, "t": inst.t, "directed": inst.directed, "k_eff": k_eff,
+            "sieve_points": 1 << k_eff, "repetitions": reps,
+            "updates_per_step": inst.updates() * reps,
+            "parallelism": (f"repetitions / sieve points over {world} GPU(s) (shard.plan_units)"
+                            if not cpu else
+                            "reference CPU code on all host threads (rank 0)"),
+            "l2": l2}
+
+
+def golden_for(args, reps):
+    """Committed full-size golden decide outputs for this config (seed 1+r,
+    max_ts = t), or None."""
+    if args.scale != 1.0 and not (args.config == 5 and args.scale == 0.1):
+        return None
+    key = f"C{args.config}" + ("x0.1" if args.scale != 1.0 else "")
+    try:
+        with open(GOLDEN_FULL) as f:
+            rec = json.load(f).get(key)
+    except Exception:
+        return None
+    if not rec or "evals" not in rec:
+        return None
+    want = {}
+    for e in rec["evals"]:
+        if e["max_ts"] == rec["t_canonical"]:
+            want[e["seed"]] = e
+    if not all((1 + r) in want for r in range(reps)):
+        return None
+    return key, [want[1 + r] for r in range(reps)]
+
+
+# ---------------------------------------------------------------- our arm
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=0, help="0 = per-config default")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--scale", type=float, default=1.0,
                     help="shrink n and m of the config (not a bench line unless 1.0)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-frac", type=float, default=0.1)
+    ap.add_argument("--ref-frac", type=float, default=None,
+                    help="CPU sample: time prefix ts <= frac * t (default per config)")
     ap.add_argument("--points-per-batch", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=-1, help="-1 = per-config default")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent CUDA streams for the repetitions of a step "
                          "(at most one per work unit)")
@@ -367,6 +442,8 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    steps = args.steps or DEFAULT_STEPS[args.config]
+    e2e_steps = DEFAULT_E2E[args.config] if args.e2e_steps < 0 else args.e2e_steps
 
     import torch
     import torch.distributed as dist
@@ -388,27 +465,28 @@ def main():
     seeds = [1 + r for r in range(reps)]
     P = 1 << k
     work = plan_units(reps, P, k, rank, world)   # [(rep, p_begin, p_end)]
-    my_points = sum(b - a for _, a, b in work)
 
     g = T.TemporalGraph.build(inst.n, (inst.u, inst.v, inst.ts), inst.directed, 0, dev)
     col = T.VertexColoring(colors, int(colors.max()))
     # the reference's default cap (2^31 words) sizes ITS dense layers; the
-    # engine's batch width is bounded by device memory instead
+    # engine's working set is bounded by device memory instead
     cfgs = [T.SieveConfig(seed=s, points_per_batch=args.points_per_batch,
                           memory_cap_words=1 << 62) for s in seeds]
     sh = T.build_shades(T.MotifQuery.from_multiset(motif), col, cfgs[0])
     ds = T.DeviceShades(g, k, sh)
     n = g.n()
+    graph_info = {"arcs": g.info.arcs, "runs": g.info.runs, "chunks": g.info.chunks,
+                  "arcs_with_src": g.info.arcs_with_src,
+                  "runs_referenced": g.info.runs_referenced,
+                  "split_chunks": g.info.split_chunks, "device_bytes": g.info.device_bytes}
     acc = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
-    total = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
+    total = torch.zeros((reps, n), dtype=torch.int64, device="cuda") if world > 1 else None
 
     # repetitions (independent evaluations) may run on concurrent streams so
     # one evaluation's tail wave overlaps the next one's launches
     side = [torch.cuda.Stream() for _ in range(max(1, min(args.streams, len(work))) - 1)]
 
-    # L2 flush between steps (inside the timed region, counted against us):
-    # the coefficient engine's working set at C2 (~70 MB per evaluation,
-    # ~15 MB of graph) would otherwise partly survive in L2 across steps
+    # L2 flush between steps (inside the timed region, counted against us)
     l2_flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def step(concurrent=True):
@@ -443,17 +521,17 @@ def main():
     with clk:
         e0.record(stream)
         h0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(steps):
             res = step()
-        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # enqueue time per step
+        host_ms = (time.perf_counter() - h0) * 1e3 / steps   # enqueue time per step
         e1.record(stream)
         torch.cuda.synchronize()
     launches = _native.Profile.launches() - launches0
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = e0.elapsed_time(e1) / steps
     # Per-kernel CUDA-event timing (roofline) from a separate single-stream
     # pass after the timed region: with concurrent streams a launch's events
     # would also cover the other stream's kernels.
-    prof_steps = max(1, min(args.steps, 3))
+    prof_steps = max(1, min(steps, 3))
     _native.Profile.reset()
     _native.Profile.enable(True)
     for _ in range(prof_steps):
@@ -475,14 +553,21 @@ def main():
     upd_step = inst.updates() * reps
     value = upd_step / (ms * 1e-3)
 
-    # decision / checksum of the last step (finalize on the host)
-    host = res.cpu().numpy().view(np.uint64)
-    sink = anchor[1]
-    decisions, checksums = [], []
+    # decision / checksum of the last timed step, finalized on the device
+    decisions, checksums, nflagged = [], [], []
     for r in range(reps):
-        a, nflag, cs = T.finalize(host[r], sink)
-        decisions.append(bool(nflag))
+        f, cs = _native.finalize_device(res[r].data_ptr(), n, anchor[1], sp)
+        decisions.append(f > 0)
         checksums.append(f"{cs:016x}")
+        nflagged.append(f)
+    gold = golden_for(args, reps)
+    parity = None
+    if gold is not None:
+        key, evals = gold
+        parity = {"golden": f"tests/golden/full_size.json {key}",
+                  "source": evals[0]["source"],
+                  "match": all(checksums[r] == evals[r]["checksum"] and
+                               nflagged[r] == evals[r]["nflagged"] for r in range(reps))}
 
     # roofline of the dominant kernel
     hbm, peak_kind = peaks()
@@ -490,119 +575,139 @@ def main():
     # full-range evaluations in the profile pass (the coefficient engine's)
     evals = sum(1 for _, a, b in work if a == 0 and b == P) * prof_steps
     if any(c for c, _ in coef.values()):
-        roof = coef_roofline(coef, k, coef_alg_bytes(g, sh, k), evals, hbm, peak_kind, args, world,
-                             clk.summary().get("sm_mhz"))
+        roof = coef_roofline(coef, k, coef_alg_bytes(g, sh, k), evals, hbm, peak_kind, args,
+                             world, clk.summary().get("sm_mhz"))
+        if roof is not None:
+            roof["launch_share_of_step"] = coef[roof["family"]][1] / max(all_ms, 1e-9)
     elif lvl_n:
-        # updates executed by the middle-level launches (3 <= l < k when level
-        # k is fused with the readout, else 3 <= l <= k) of this rank in the
-        # timed region
-        # algorithmic bytes: 16 B per (arc, point) update --
-        # one 8-B predecessor-state read plus one 8-B state write -- times the
-        # updates of one middle-level launch.  The engine moves less (no state
-        # for runs no arc reads, no read for arcs without a predecessor): that
-        # shows as ncu `traffic` below the algorithmic figure.
         mid_levels = (k - 2) - (1 if last_n else 0)
+        my_points = sum(b - a for _, a, b in work)
         upd_launch = g.info.arcs * mid_levels * my_points * prof_steps / lvl_n
         alg_bytes = BYTES_PER_UPDATE * upd_launch
         avg_ms = lvl_ms / lvl_n
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
-        # per-launch DRAM traffic and instruction counts of the same kernel on
-        # the same workload, from the committed ncu capture (tools/ncu_level_json.py)
-        traffic, prof = None, None
-        try:
-            with open(os.path.join(ROOT, "profiles", f"level_kernel_c{args.config}.json")) as f:
-                prof = json.load(f)
-            if prof["config"] != args.config or args.scale != 1.0 or world != 1 or grouped:
-                prof = None
-            else:
-                traffic = prof["traffic_bytes_per_launch"]
-        except Exception:
-            prof = None
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
                 "kernel": ("k_level (grouped, W < 32, 3 <= l < k)" if grouped
                            else "k_level_wide (3 <= l < k)"), "avg_launch_ms": avg_ms,
                 "launch_share_of_step": lvl_ms / max(all_ms, 1e-9),
                 "alg_bytes_per_launch": alg_bytes}
-        # The kernel is integer-pipe bound (GF(2^64) carry-less products), so
-        # the binding roofline is instruction issue: 4 warp-instructions per
-        # clock per SM.  achieved = the capture's executed warp-instructions
-        # per launch / this run's launch time; ALU-pipe utilization is the
-        # capture's own counter.
-        if prof is not None:
-            sm_mhz = clk.summary().get("sm_mhz") or prof["sm_clock_ghz"] * 1e3
-            peak_issue = 148 * 4 * sm_mhz * 1e6
-            ach = prof["warp_inst_per_launch"] / (avg_ms * 1e-3)
-            roof["int_pipe"] = {"bound": "issue", "unit": "warp-inst/s", "achieved": ach,
-                                "peak": peak_issue, "frac": ach / peak_issue,
-                                "alu_pipe_frac_ncu": prof["alu_pipe_pct_active"] / 100,
-                                "thread_inst_per_update": 32 * prof["warp_inst_per_launch"] /
-                                upd_launch,
-                                "capture": prof["capture"]}
 
-    # e2e through the public API with host buffers (graph build + shades +
-    # eval + accumulator read-back), same metric
+    # the GPU's accumulators on the CPU sample's window (horizon max_ts on the
+    # same graph), checked word for word against the CPU arm below
+    gpu_window = None
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    if want_cpu:
+        frac = args.ref_frac if args.ref_frac is not None else CPU_FRAC[args.config]
+        wts = max(1, int(inst.t * frac))
+        if wts <= g.t():
+            o = T.eval_temporal_sieve(g, k, wts, sh, cfgs[0], T.AnchorSpec(*anchor))
+            gpu_window = (wts, o.accumulators)
+
+    # e2e through the C-ABI with HOST buffers: every step copies the edge
+    # arrays from pinned host memory (tsv_graph_build: device canonicalize +
+    # layout), uploads the host shade CSR, evaluates, finalizes and copies the
+    # accumulators back into a host buffer (tsv_eval_temporal_sieve).  The
+    # timed graph is freed first so both fit in HBM.
+    del ds, g
+    acc = total = None
+    torch.cuda.synchronize()
     e2e = None
-    if args.e2e_steps > 0:
-        # the step's inputs live in pinned host memory; every step copies them
-        # to the device, builds, evaluates and reads the accumulators back
-        pinned = tuple(torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    e2e_parity = None
+    if e2e_steps > 0:
+        import ctypes as C
+        pinned = tuple(torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).pin_memory()
                        for a in (inst.u, inst.v, inst.ts))
+        pu, pv, pt = (x.numpy() for x in pinned)
+        host_acc = np.zeros((reps, max(n, 1)), np.uint64)
+        vs = sh.vertex_shades if len(sh.vertex_shades) else np.zeros(1, np.int32)
+        voff = np.ascontiguousarray(sh.vertex_off, np.int32)
+        L = _native.lib()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
+        outs = []
         t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            g2 = T.TemporalGraph.build(inst.n, pinned, inst.directed, 0, dev)
-            ds2 = T.DeviceShades(g2, k, sh)
-            a2 = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
-            lanes = [stream] + side
-            for s in side:
-                s.wait_stream(stream)
-            for i, (r, a, b) in enumerate(work):
-                T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], a, b,
-                                     a2[r].data_ptr(), lanes[i % len(lanes)].cuda_stream)
-            for s in side:
-                stream.wait_stream(s)
-            if world > 1:
-                a2 = xor_allreduce(a2, out=total)
-            h = a2.cpu()
-            del g2, ds2
+        for _ in range(e2e_steps):
+            h = C.c_void_p()
+            _native.check(L.tsv_graph_build(inst.n, len(pu), pu, pv, pt, int(inst.directed), 0,
+                                             dev, C.byref(h)))
+            info = _native.GraphInfo()
+            _native.check(L.tsv_graph_get_info(h, C.byref(info)))
+            outs = []
+            if world == 1:
+                for r in range(reps):
+                    o = _native.Outcome()
+                    cfg = cfgs[r].to_native()
+                    _native.check(L.tsv_eval_temporal_sieve(
+                        h, k, info.t, voff, vs, C.byref(cfg), anchor[0], anchor[1],
+                        host_acc[r], C.byref(o)))
+                    outs.append((int(o.flagged), f"{o.checksum:016x}"))
+            else:
+                g2 = T.TemporalGraph(h, info)
+                ds2 = T.DeviceShades(g2, k, sh)
+                a2 = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
+                for r, a, b in work:
+                    T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], a, b,
+                                         a2[r].data_ptr(), sp)
+                a2 = xor_allreduce(a2)
+                host_acc[:] = a2.cpu().numpy().view(np.uint64)
+                del ds2, g2
+                h = None
+            if h is not None:
+                L.tsv_graph_free(h)
         torch.cuda.synchronize()
-        sec = (time.perf_counter() - t0) / args.e2e_steps
+        sec = (time.perf_counter() - t0) / e2e_steps
         if world > 1:
             t = torch.tensor([sec], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             sec = float(t.item())
+        if gold is not None and outs:
+            e2e_parity = all(outs[r] == (gold[1][r]["nflagged"], gold[1][r]["checksum"])
+                             for r in range(reps))
         e2e = {"value": upd_step / sec, "unit": "updates/s",
-               "h2d_bytes_per_step": int(inst.m * 12 + sh.vertex_off.nbytes +
-                                         sh.vertex_shades.nbytes),
-               "d2h_bytes_per_step": int(reps * n * 8), "ms_per_step": sec * 1e3}
+               "h2d_bytes_per_step": int(pu.nbytes + pv.nbytes + pt.nbytes + voff.nbytes +
+                                         (vs.nbytes if len(sh.vertex_shades) else 0)),
+               "d2h_bytes_per_step": int(reps * n * 8), "ms_per_step": sec * 1e3,
+               "path": ("C-ABI: tsv_graph_build (pinned host edges) + tsv_eval_temporal_sieve "
+                        "(host shade CSR, host accumulators, device finalize) per repetition"
+                        if world == 1 else "tsv_graph_build + tsv_eval_points_device + "
+                        "XOR combine + D2H"),
+               "parity": e2e_parity}
+        del pinned, pu, pv, pt
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if want_cpu:
+        def gpu_check(mt):
+            if gpu_window is None or gpu_window[0] != mt:
+                raise ValueError("no GPU evaluation at this horizon")
+            return gpu_window[1]
         try:
-            rate, sec, sample, kind, cores = cpu_sample(inst, k, colors, motif, anchor,
-                                                        frac=args.ref_frac)
-            cpu = {"value": rate, "unit": "updates/s", "cores": cores, "kind": kind,
-                   "sample": sample, "seconds": sec}
+            r = cpu_sample(inst, k, colors, motif, anchor, frac=args.ref_frac,
+                           gpu_check=gpu_check)
+            cpu = {"value": r["value"], "unit": "updates/s", "cores": r["threads"],
+                   "kind": r["kind"], "sample": r["sample"], "seconds": r["seconds"],
+                   "cpu_model": cpu_model(), "window_parity": r.get("window_parity")}
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "updates/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "u64", "data": "synthetic",
-                "config": config_json(inst, world, args), "roofline": roof, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "host_enqueue_ms_per_step": host_ms, "clocks": clk.summary(),
-                "decision": decisions, "checksums": checksums,
-                "graph": {"arcs": g.info.arcs, "runs": g.info.runs, "chunks": g.info.chunks,
-                          "arcs_with_src": g.info.arcs_with_src,
-                          "runs_referenced": g.info.runs_referenced,
-                          "split_chunks": g.info.split_chunks,
-                          "device_bytes": g.info.device_bytes},
+                "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+                "decide_ms": ms / reps if reps > 1 else ms,
+                "value_kind": ("equivalent point-form updates/s: A*(k_eff-1)*2^k_eff per decide "
+                               "/ decide time; the coefficient engine computes the same sieve "
+                               "sums without visiting points (DESIGN.md 2b)"
+                               if any(c for c, _ in coef.values()) else
+                               "point-form updates/s (point engine)"),
+                "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+                "config": config_json(inst, world, args), "parity": parity,
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "host_enqueue_ms_per_step": host_ms,
+                "clocks": clk.summary(), "decision": decisions, "checksums": checksums,
+                "nflagged": nflagged, "graph": graph_info,
                 "engine": "coefficient" if any(c for c, _ in coef.values()) else "points",
                 "kernel_ms_per_step": {"level": lvl_ms / prof_steps,
                                        "coef_arcs": coef["coef_arcs"][1] / prof_steps,
