@@ -72,9 +72,27 @@ def test_golden_sieve_cases(cuda_device, golden):
     assert nz >= 20
 
 
+def level_kernels_ran():
+    """Launches of the point engine's level kernels since the last reset."""
+    return sum(_native.Profile.get(nm)[0] for nm in
+               ("level", "level_first", "level_last", "level_grouped", "level_grouped_first"))
+
+
+@pytest.fixture
+def point_engine(monkeypatch):
+    """Full-range calls on the point engine (TSV_ENGINE=points), with the
+    per-kernel profile on so a test can assert which kernels ran."""
+    monkeypatch.setenv("TSV_ENGINE", "points")
+    _native.Profile.reset()
+    _native.Profile.enable(True)
+    yield
+    _native.Profile.enable(False)
+
+
 @pytest.mark.parametrize("ppb", [1, 2, 4, 8, 16, 32, 64, 128])
-def test_results_independent_of_batch_width(cuda_device, golden, ppb):
-    """test_sieve.cpp:291-308 (lane/thread invariance) for every kernel shape."""
+def test_results_independent_of_batch_width(cuda_device, golden, ppb, point_engine):
+    """test_sieve.cpp:291-308 (lane/thread invariance) for every kernel shape
+    of the point engine (grouped W < 32, wide W >= 32)."""
     by = {c["name"]: c for c in golden["sieve"]}
     for name in ("fig2 seed5", "C1 k-TempPath k=5", "random 3", "random 7", "random 11"):
         c = by[name]
@@ -84,6 +102,9 @@ def test_results_independent_of_batch_width(cuda_device, golden, ppb):
         assert f"{out.checksum:016x}" == c["checksum"], (name, ppb)
         if "acc" in c:
             assert [f"{int(x):016x}" for x in out.accumulators] == c["acc"], (name, ppb)
+    assert level_kernels_ran() > 0
+    assert _native.Profile.get("coef_arcs_last")[0] == 0
+    assert _native.Profile.get("level_last")[0] > 0
 
 
 def test_decreasing_timestamps_no_for_every_seed(cuda_device):
@@ -151,11 +172,12 @@ def test_hub_vertices_split_across_chunks(cuda_device):
 
 @pytest.mark.parametrize("env", [{}, {"TSV_YMUL": "holes"}])
 @pytest.mark.parametrize("ppb", [4, 16, 64])
-def test_engine_paths_agree(cuda_device, monkeypatch, env, ppb):
-    """Grouped and wide kernels (and the wide kernel's holes product for y
-    instead of the tables) give the oracle's accumulators with hub vertices
-    split across chunks (carry fix-up into state slots), horizons below t
-    (fused readout of the last run <= max_ts) and compacted state rows."""
+def test_engine_paths_agree(cuda_device, monkeypatch, env, ppb, point_engine):
+    """Grouped and wide kernels of the point engine (and the wide kernel's
+    holes product for y instead of the tables) give the oracle's
+    accumulators with hub vertices split across chunks (carry fix-up into
+    state slots), horizons below t (fused readout of the last run <= max_ts)
+    and compacted state rows."""
     for k_, v_ in env.items():
         monkeypatch.setenv(k_, v_)
     rng = np.random.default_rng(31)
@@ -168,6 +190,53 @@ def test_engine_paths_agree(cuda_device, monkeypatch, env, ppb):
                             ([1, 2, 3, 1, 2, 3], 11, 33)):
         _oracle_vs_gpu(n, u, v, ts, True, colors, motif, seed, max_ts=mt, ppb=ppb)
     _oracle_vs_gpu(n, u, v, ts, False, colors, [1, 2, 3], 5, max_ts=20, ppb=ppb)
+    assert _native.Profile.get("level_grouped" if ppb < 32 else "level")[0] > 0
+    assert _native.Profile.get("fixup")[0] > 0
+
+
+@pytest.mark.parametrize("ppb", [1, 2, 4, 8, 16, 32, 64, 128])
+def test_partial_point_ranges_vs_oracle(cuda_device, ppb):
+    """The multi-GPU path: partial sieve-point ranges [a, b) (every call on
+    the point engine) equal the oracle's partial sums for the same range, at
+    every batch width; hubs split across chunks, anchors, horizons below t,
+    undirected graphs.  Ranges that are not multiples of the width exercise
+    the idle lanes of the last batch."""
+    import torch
+    rng = np.random.default_rng(100 + ppb)
+    n, m, t = 160, 5000, 30
+    u = rng.integers(0, n, m)
+    v = np.where(rng.random(m) < 0.35, 0, rng.integers(0, n, m))     # hub
+    ts = rng.integers(1, t + 1, m)
+    colors = rng.integers(1, 5, n)
+    _native.Profile.reset()
+    _native.Profile.enable(True)
+    try:
+        for directed, motif, seed, mt, anchor in (
+                (True, [1, 1, 2, 3, 4], 3, None, (-1, -1)),
+                (True, [1, 2, 3, 4, 1, 2], 5, 22, (-1, -1)),
+                (True, [1, 2, 3, 4, 4, 3, 2], 7, None, (4, 9)),
+                (False, [1, 2, 3, 1], 9, 17, (-1, -1))):
+            g = T.TemporalGraph.build(n, (u, v, ts), directed)
+            col = T.VertexColoring(colors, int(colors.max()))
+            cfg = T.SieveConfig(seed=seed, points_per_batch=ppb)
+            sh = T.build_shades(T.MotifQuery.from_multiset(motif), col, cfg)
+            ds = T.DeviceShades(g, len(motif), sh)
+            k = len(motif)
+            P = 1 << k
+            cu, cv, ct = g.edges()
+            mt = mt or g.t()
+            for a, b in ((0, 1), (3, 3 + ppb), (1, P // 2 + 3), (P // 2, P), (P - 1, P), (5, P - 2)):
+                acc = torch.zeros(n, dtype=torch.int64, device="cuda")
+                T.eval_points_device(g, ds, k, mt, cfg, anchor[0], a, b, acc.data_ptr(),
+                                     torch.cuda.current_stream().cuda_stream)
+                got = acc.cpu().numpy().view(np.uint64)
+                want = O.eval_points(n, cu, cv, ct, directed, k, mt, sh.vertex_off,
+                                     sh.vertex_shades, seed, anchor[0], a, b)
+                assert np.array_equal(got, want), (directed, motif, a, b)
+        assert level_kernels_ran() > 0
+        assert _native.Profile.get("coef_arcs_last")[0] == 0
+    finally:
+        _native.Profile.enable(False)
 
 
 @pytest.mark.parametrize("env", [{"TSV_ENGINE": "points"}, {"TSV_ITEMS": "0"},
@@ -371,10 +440,11 @@ def _decide_points(g, ds, k, cfg, anchor_src, p0, p1):
 
 
 @pytest.mark.parametrize("cfgno,scale", [(2, 1.0), (5, 0.01)])
-def test_full_size_properties(cuda_device, cfgno, scale):
-    """BASELINE sizes, where the CPU oracle cannot follow, checked through
-    size-independent properties: (1) the accumulators do not depend on the
-    batch width (wide W=64/32 and grouped W=8/4 kernels agree bit for bit);
+def test_full_size_properties(cuda_device, monkeypatch, cfgno, scale):
+    """Size-independent properties at BASELINE sizes (the bit-exact full-size
+    goldens are test_gpu_full.py's): (1) the point engine's accumulators do
+    not depend on the batch width (wide W=64/32 and grouped W=8/4 kernels
+    agree bit for bit) and equal the coefficient engine's;
     (2) sieve points are independent: XOR of disjoint point ranges = whole;
     (3) the planted path is found; (4) restricted to the planted path's
     vertices the engine equals the oracle exactly."""
@@ -387,12 +457,16 @@ def test_full_size_properties(cuda_device, cfgno, scale):
     ds = T.DeviceShades(g, k, sh)
     P = 1 << k
     ref = None
+    monkeypatch.setenv("TSV_ENGINE", "points")      # the width loop is the point engine's
     for ppb in (64, 32, 8, 4):
         c = T.SieveConfig(seed=3, points_per_batch=ppb, memory_cap_words=1 << 62)
         acc = _decide_points(g, ds, k, c, anchor[0], 0, P)
         if ref is None:
             ref = acc
         assert np.array_equal(acc, ref), ppb
+    monkeypatch.delenv("TSV_ENGINE")
+    # the coefficient engine (full range) equals the point engine
+    assert np.array_equal(_decide_points(g, ds, k, cfg, anchor[0], 0, P), ref)
     parts = [_decide_points(g, ds, k, cfg, anchor[0], a, b)
              for a, b in ((0, 5), (5, P // 2), (P // 2, P - 1), (P - 1, P))]
     assert np.array_equal(parts[0] ^ parts[1] ^ parts[2] ^ parts[3], ref)

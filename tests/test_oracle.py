@@ -123,3 +123,87 @@ def test_oracle_vs_reference_random():
         assert np.array_equal(acc, r["acc"]) and cs == r["checksum"]
         nz += nf > 0
     assert nz > 10
+
+
+def _big_eval(n, u, v, ts, directed, k, max_ts, off, shades, seed, anchor_src, lanes,
+              p0=0, p1=None):
+    """The multi-threaded restatement (tsv_oracle_big.c): in-place
+    canonicalization, head-grouped runs, `lanes` points per pass."""
+    u2, v2, t2 = (np.array(x, dtype=np.int32) for x in (u, v, ts))
+    w = O.canonicalize_inplace(n, u2, v2, t2, directed)
+    G = O.BigGraph(n, u2[:w], v2[:w], t2[:w], directed, max_ts)
+    return (u2[:w], v2[:w], t2[:w]), G.eval(k, off, shades, seed, anchor_src, p0, p1, lanes)
+
+
+def test_big_oracle_sieve_golden(golden):
+    """tsv_oracle_big.c (the checker of the full-size goldens) pinned to the
+    reference's golden sieve cases: accumulators, flagged set, checksum."""
+    from paper_2001_07158_b200 import sieve as S
+    from paper_2001_07158_b200.graph import MotifQuery, VertexColoring
+    nz = 0
+    for i, c in enumerate(golden["sieve"]):
+        sh = S.build_shades(MotifQuery.from_multiset(c["motif"]),
+                            VertexColoring(c["colors"], max(c["colors"])),
+                            S.SieveConfig(seed=c["seed"]))
+        if not sh.feasible:
+            continue
+        cu, cv, ct = O.canonical_edges(c["n"], c["u"], c["v"], c["ts"], c["directed"])
+        t = c["t"] or (int(ct.max()) if len(ct) else 1)
+        max_ts = c["max_ts"] or t
+        canon, acc = _big_eval(c["n"], c["u"], c["v"], c["ts"], c["directed"], len(c["motif"]),
+                               max_ts, sh.vertex_off, sh.vertex_shades, c["seed"],
+                               c["anchor"][0], lanes=(1, 3, 8, 16)[i % 4])
+        assert all(np.array_equal(a, b) for a, b in zip(canon, (cu, cv, ct))), c["name"]
+        a, nflag, cs = O.finalize(acc, c["anchor"][1])
+        assert f"{cs:016x}" == c["checksum"], c["name"]
+        assert np.nonzero(a)[0].tolist() == c["flagged"], c["name"]
+        nz += nflag > 0
+    assert nz >= 20
+
+
+def test_big_oracle_matches_restatement_random():
+    """Random small instances (loops, duplicates, undirected, anchors,
+    horizons below t, partial point ranges, every lane count)."""
+    from paper_2001_07158_b200 import sieve as S
+    from paper_2001_07158_b200 import synth
+    from paper_2001_07158_b200.graph import MotifQuery, VertexColoring
+    rng = np.random.default_rng(21)
+    for it in range(200):
+        n, u, v, ts, d, colors, motif = synth.random_small(rng, k_max=7)
+        k = len(motif)
+        sh = S.build_shades(MotifQuery.from_multiset(motif),
+                            VertexColoring(colors, int(colors.max())), S.SieveConfig(seed=5))
+        if not sh.feasible:
+            continue
+        cu, cv, ct = O.canonical_edges(n, u, v, ts, d)
+        max_ts = int(rng.integers(1, (int(ct.max()) if len(ct) else 1) + 1))
+        anchor = -1 if rng.random() < 0.6 else int(rng.integers(0, n))
+        P = 1 << k
+        p0 = int(rng.integers(0, P))
+        p1 = int(rng.integers(p0 + 1, P + 1))
+        want = O.eval_points(n, cu, cv, ct, d, k, max_ts, sh.vertex_off, sh.vertex_shades, 5,
+                             anchor, p0, p1)
+        _, got = _big_eval(n, u, v, ts, d, k, max_ts, sh.vertex_off, sh.vertex_shades, 5, anchor,
+                           int(rng.choice([1, 2, 5, 8, 16])), p0, p1)
+        assert np.array_equal(got, want), it
+
+
+def test_full_size_goldens_recorded():
+    """tests/golden/full_size.json covers every BASELINE config at full size
+    (C1's full-size case lives in golden.json) and C2's entries come from
+    the reference itself."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "full_size.json")) as f:
+        full = json.load(f)
+    assert len(full["C2"]["evals"]) == 5
+    assert all(e["source"].startswith("reference") for e in full["C2"]["evals"])
+    assert full["C3"]["evals"][0]["nflagged"] > 0
+    assert full["C5x0.1"]["evals"][0]["nflagged"] > 0
+    assert len(full["C4"]["points"]) >= 3
+    if "C5" in full:
+        assert len(full["C5"]["points"]) == 32
+        x = 0
+        for p in full["C5"]["points"]:
+            x ^= int(p["xor_total"], 16)
+        assert f"{x:016x}" == full["C5"]["evals"][0]["xor_total"]
