@@ -360,6 +360,8 @@ struct VcSpec {
 };
 
 std::shared_ptr<tsv_graph> shaded_subgraph(const tsv_graph* g, const tsv_shades* sh);
+void copy_to_host(void* dst, const void* d_src, size_t bytes, cudaStream_t st);
+void copy_to_device(void* d_dst, const void* src, size_t bytes, cudaStream_t st);
 
 // Subset-index tables of the coefficient engine for one k (host).
 const tsv::CoefTables& coef_const_tables(int k) {
@@ -815,9 +817,21 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     int32_t* dv = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
     int32_t* dts = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
     if (m) {
-      TSV_CUDA(cudaMemcpyAsync(du, u, m * 4, kind, st));
-      TSV_CUDA(cudaMemcpyAsync(dv, v, m * 4, kind, st));
-      TSV_CUDA(cudaMemcpyAsync(dts, ts, m * 4, kind, st));
+      // pageable host arrays go through the pinned staging buffers
+      cudaPointerAttributes pa{};
+      const bool pageable = kind == cudaMemcpyHostToDevice &&
+                            (cudaPointerGetAttributes(&pa, u) != cudaSuccess ||
+                             pa.type == cudaMemoryTypeUnregistered);
+      cudaGetLastError();  // (clear a failed attribute query)
+      if (pageable) {
+        copy_to_device(du, u, m * 4, st);
+        copy_to_device(dv, v, m * 4, st);
+        copy_to_device(dts, ts, m * 4, st);
+      } else {
+        TSV_CUDA(cudaMemcpyAsync(du, u, m * 4, kind, st));
+        TSV_CUDA(cudaMemcpyAsync(dv, v, m * 4, kind, st));
+        TSV_CUDA(cudaMemcpyAsync(dts, ts, m * 4, kind, st));
+      }
     }
     // edge model (sieve.cpp:179-186): transition times when model 1/3,
     // vertex delays (0 when none were given) when model 2/3
@@ -940,6 +954,8 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
 std::shared_ptr<tsv_graph> shaded_subgraph(const tsv_graph* g, const tsv_shades* sh) {
   const char* env = std::getenv("TSV_SUBGRAPH");
   if (g->model != 0 || (env && env[0] == '0') || g->host.n == 0) return nullptr;
+  // every vertex has a shade (k-TempPath, C5): nothing to drop
+  if (sh->single + sh->multi >= static_cast<int64_t>(g->host.n)) return nullptr;
   std::lock_guard<std::mutex> lk(sh->sub_mu);
   for (const auto& e : sh->subs)
     if (e.uid == g->uid) return e.sub;
@@ -1035,64 +1051,103 @@ bool equal_par(const T* a, const T* b, size_t count) {
   return diff == 0;
 }
 
-// Device -> host copy of `count` words into pageable memory: DMA into two
-// pinned staging buffers (per device, reused) while the host threads move
-// the previous chunk out.  Plain cudaMemcpy to pageable memory stages
-// through the driver at a fraction of the link rate.
-void copy_to_host(uint64_t* dst, const uint64_t* d_src, size_t count, cudaStream_t st) {
-  if (count == 0) return;
-  const size_t bytes = count * 8;
+// dst = src[0..count), copied on all host threads
+void copy_par(std::vector<int32_t>& dst, const int32_t* src, size_t count) {
+  dst.resize(count);
+  const size_t block = size_t{1} << 20;
+  const int64_t nb = static_cast<int64_t>((count + block - 1) / block);
+#pragma omp parallel for schedule(static) if (nb > 4)
+  for (int64_t i = 0; i < nb; ++i) {
+    const size_t lo = static_cast<size_t>(i) * block, len = std::min(block, count - lo);
+    std::memcpy(dst.data() + lo, src + lo, len * sizeof(int32_t));
+  }
+}
+
+// Copies between device memory and pageable host memory through two pinned
+// staging buffers per device (reused by every call): the DMA of one chunk
+// overlaps the host threads moving the neighbouring chunk.  Plain cudaMemcpy
+// from/to pageable memory stages through the driver at a fraction of the
+// link rate (C5: 800 MB of accumulators, 2.4 GB of shade CSR).
+struct Staging {
+  static constexpr size_t kChunk = size_t{32} << 20;
+  std::mutex mu;
+  void* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+
+Staging& staging() {
+  static std::mutex reg_mu;
+  static std::vector<std::unique_ptr<Staging>> reg;
+  int dev = 0;
+  TSV_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(reg_mu);
+  if (reg.size() <= static_cast<size_t>(dev)) reg.resize(static_cast<size_t>(dev) + 1);
+  if (!reg[dev]) {
+    auto st = std::make_unique<Staging>();
+    for (int i = 0; i < 2; ++i) {
+      TSV_CUDA(cudaMallocHost(&st->buf[i], Staging::kChunk));
+      TSV_CUDA(cudaEventCreateWithFlags(&st->ev[i], cudaEventDisableTiming));
+    }
+    reg[dev] = std::move(st);
+  }
+  return *reg[dev];
+}
+
+void memcpy_par(char* dst, const char* src, size_t len) {
+  const int64_t parts = len >= (size_t{4} << 20) ? 16 : 1;
+#pragma omp parallel for schedule(static) num_threads(16) if (parts > 1)
+  for (int64_t p = 0; p < parts; ++p) {
+    const size_t lo = len * p / parts, hi = len * (p + 1) / parts;
+    std::memcpy(dst + lo, src + lo, hi - lo);
+  }
+}
+
+void copy_to_host(void* dst, const void* d_src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
   if (bytes < (size_t{8} << 20)) {
     TSV_CUDA(cudaMemcpyAsync(dst, d_src, bytes, cudaMemcpyDeviceToHost, st));
     TSV_CUDA(cudaStreamSynchronize(st));
     return;
   }
-  constexpr size_t kChunk = size_t{32} << 20;
-  struct Staging {
-    std::mutex mu;
-    void* buf[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
-  };
-  static std::mutex reg_mu;
-  static std::vector<std::unique_ptr<Staging>> reg;
-  int dev = 0;
-  TSV_CUDA(cudaGetDevice(&dev));
-  Staging* S = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(reg_mu);
-    if (reg.size() <= static_cast<size_t>(dev)) reg.resize(static_cast<size_t>(dev) + 1);
-    if (!reg[dev]) {
-      auto s = std::make_unique<Staging>();
-      for (int i = 0; i < 2; ++i) {
-        TSV_CUDA(cudaMallocHost(&s->buf[i], kChunk));
-        TSV_CUDA(cudaEventCreateWithFlags(&s->ev[i], cudaEventDisableTiming));
-      }
-      reg[dev] = std::move(s);
-    }
-    S = reg[dev].get();
-  }
-  std::lock_guard<std::mutex> lk(S->mu);
-  const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+  Staging& S = staging();
+  std::lock_guard<std::mutex> lk(S.mu);
+  const size_t K = Staging::kChunk, nchunks = (bytes + K - 1) / K;
   auto issue = [&](size_t c) {
-    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-    TSV_CUDA(cudaMemcpyAsync(S->buf[c & 1], reinterpret_cast<const char*>(d_src) + off, len,
+    const size_t off = c * K, len = std::min(K, bytes - off);
+    TSV_CUDA(cudaMemcpyAsync(S.buf[c & 1], static_cast<const char*>(d_src) + off, len,
                              cudaMemcpyDeviceToHost, st));
-    TSV_CUDA(cudaEventRecord(S->ev[c & 1], st));
+    TSV_CUDA(cudaEventRecord(S.ev[c & 1], st));
   };
   issue(0);
   for (size_t c = 0; c < nchunks; ++c) {
-    if (c + 1 < nchunks) issue(c + 1);
-    TSV_CUDA(cudaEventSynchronize(S->ev[c & 1]));
-    const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
-    const char* src = static_cast<const char*>(S->buf[c & 1]);
-    char* out = reinterpret_cast<char*>(dst) + off;
-    const int64_t parts = 16;
-#pragma omp parallel for schedule(static) num_threads(16)
-    for (int64_t p = 0; p < parts; ++p) {
-      const size_t lo = len * p / parts, hi = len * (p + 1) / parts;
-      std::memcpy(out + lo, src + lo, hi - lo);
-    }
+    if (c + 1 < nchunks) issue(c + 1);  // buffer (c+1)&1 was drained in step c-1
+    TSV_CUDA(cudaEventSynchronize(S.ev[c & 1]));
+    const size_t off = c * K, len = std::min(K, bytes - off);
+    memcpy_par(static_cast<char*>(dst) + off, static_cast<const char*>(S.buf[c & 1]), len);
   }
+}
+
+// Host -> device; returns once the source may be reused (the last DMAs are
+// complete).
+void copy_to_device(void* d_dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return;
+  if (bytes < (size_t{8} << 20)) {
+    TSV_CUDA(cudaMemcpyAsync(d_dst, src, bytes, cudaMemcpyHostToDevice, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  Staging& S = staging();
+  std::lock_guard<std::mutex> lk(S.mu);
+  const size_t K = Staging::kChunk, nchunks = (bytes + K - 1) / K;
+  for (size_t c = 0; c < nchunks; ++c) {
+    if (c >= 2) TSV_CUDA(cudaEventSynchronize(S.ev[c & 1]));  // DMA of chunk c-2 done
+    const size_t off = c * K, len = std::min(K, bytes - off);
+    memcpy_par(static_cast<char*>(S.buf[c & 1]), static_cast<const char*>(src) + off, len);
+    TSV_CUDA(cudaMemcpyAsync(static_cast<char*>(d_dst) + off, S.buf[c & 1], len,
+                             cudaMemcpyHostToDevice, st));
+    TSV_CUDA(cudaEventRecord(S.ev[c & 1], st));
+  }
+  TSV_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace
@@ -1384,18 +1439,15 @@ int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
     s->multi = multi;
     s->device = g->device;
     try {
-      // pool allocations (cudaMalloc costs ~0.1 ms per call); the copies from
-      // pageable memory are synchronous, so the arrays are ready on return
+      // pool allocations (cudaMalloc costs ~0.1 ms per call); the copies go
+      // through the pinned staging buffers and are complete on return
       TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->off),
                                (static_cast<size_t>(n) + 1) * 4, nullptr));
       TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->shades),
                                std::max<size_t>(static_cast<size_t>(cnt), 1) * 4, nullptr));
-      TSV_CUDA(cudaMemcpyAsync(s->off, vertex_off, (static_cast<size_t>(n) + 1) * 4,
-                               cudaMemcpyHostToDevice, nullptr));
-      if (cnt)
-        TSV_CUDA(cudaMemcpyAsync(s->shades, vertex_shades, static_cast<size_t>(cnt) * 4,
-                                 cudaMemcpyHostToDevice, nullptr));
       TSV_CUDA(cudaStreamSynchronize(nullptr));
+      copy_to_device(s->off, vertex_off, (static_cast<size_t>(n) + 1) * 4, nullptr);
+      copy_to_device(s->shades, vertex_shades, static_cast<size_t>(cnt) * 4, nullptr);
     } catch (...) {
       delete s;
       throw;
@@ -1453,8 +1505,8 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
       std::lock_guard<std::mutex> lk(g->shade_mu);
       g->shade_cache = hold;
       g->shade_k = k;
-      g->shade_off_copy.assign(vertex_off, vertex_off + n + 1);
-      g->shade_vs_copy.assign(vertex_shades, vertex_shades + cnt);
+      copy_par(g->shade_off_copy, vertex_off, static_cast<size_t>(n) + 1);
+      copy_par(g->shade_vs_copy, vertex_shades, static_cast<size_t>(cnt));
     }
     DeviceGuard dg(g->device);
     // the graph's stream; a concurrent call on the same graph gets its own
@@ -1487,7 +1539,7 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     uint64_t checksum = 0;
     int64_t flagged = 0;
     tsv::device_finalize(acc.as<uint64_t>(), n, anchor_sink, st, &checksum, &flagged);
-    copy_to_host(accumulators, acc.as<uint64_t>(), static_cast<size_t>(n), st);
+    copy_to_host(accumulators, acc.p, static_cast<size_t>(n) * 8, st);
     out->flagged = flagged;
     out->global_nonzero = flagged > 0;
     out->checksum = checksum;

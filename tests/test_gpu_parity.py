@@ -225,7 +225,8 @@ def test_partial_point_ranges_vs_oracle(cuda_device, ppb):
             P = 1 << k
             cu, cv, ct = g.edges()
             mt = mt or g.t()
-            for a, b in ((0, 1), (3, 3 + ppb), (1, P // 2 + 3), (P // 2, P), (P - 1, P), (5, P - 2)):
+            for a, b in ((0, 1), (3, min(P, 3 + ppb)), (1, P // 2 + 3), (P // 2, P), (P - 1, P),
+                         (5, P - 2)):
                 acc = torch.zeros(n, dtype=torch.int64, device="cuda")
                 T.eval_points_device(g, ds, k, mt, cfg, anchor[0], a, b, acc.data_ptr(),
                                      torch.cuda.current_stream().cuda_stream)
