@@ -15,6 +15,10 @@
 #   launches:TAG[,ARGS]      ncu launch list of `bench.py --steps 1 --warmup 3 ARGS`
 #   ncu:TAG,REGEX,SKIP,COUNT[,ARGS]
 #                            ncu --set full of the matching launches of the same command
+#   ncueval:TAG,REGEX,SKIP,COUNT,CFG[,SCALE]
+#                            ncu --set full of `tools/one_eval.py CFG SCALE 2`
+#   launcheval:TAG,CFG[,SCALE]
+#                            ncu launch list (gpu__time_duration) of the same
 #   sanitize:TOOL[,K]        compute-sanitizer --tool TOOL over pytest -m gpu -k K
 #   py:SCRIPT[,ARGS]         python SCRIPT ARGS                          -> py_<i>.log
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
@@ -25,6 +29,8 @@ for job in "$@"; do
   name=${job%%:*}
   arg=""; [[ "$job" == *:* ]] && arg=${job#*:}
   IFS=',' read -r -a A <<< "$arg"
+  # ENV=VALUE jobs set an environment variable for the jobs after them
+  if [[ "$name" == *=* ]]; then export "$job"; echo "env $job"; continue; fi
   case $name in
     box)
       (nproc; lscpu | grep -E "Model name|Socket|Thread|Core|NUMA node\(s\)"; free -g;
@@ -37,7 +43,7 @@ for job in "$@"; do
       timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
       echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log ;;
     timings)
-      out=gpurun_out/timings_${A[0]}_${A[1]:-1}.log
+      out=gpurun_out/timings_${A[0]}_${A[1]:-1}_$i.log
       timeout 1800 python tools/probe_timing.py --config "${A[0]}" --scale "${A[1]:-1.0}" > $out 2>&1
       echo "timings ${A[*]} rc=$?"; tail -c 1200 $out; echo ;;
     bench)
@@ -62,6 +68,19 @@ for job in "$@"; do
       timeout 3000 ncu --set full --clock-control none --import-source on -k "regex:$rx" \
           -s "$skip" -c "$cnt" -o gpurun_out/prof_$tag $CMD > gpurun_out/ncu_full_$tag.log 2>&1
       echo "ncu $tag rc=$?"; tail -2 gpurun_out/ncu_full_$tag.log ;;
+    ncueval)
+      tag=${A[0]}; rx=${A[1]}; skip=${A[2]}; cnt=${A[3]}
+      CMD="python tools/one_eval.py ${A[4]} ${A[5]:-1.0} 2"
+      $CMD > gpurun_out/plain_ncu_$tag.log 2>&1 && echo "plain rc=0" && tail -2 gpurun_out/plain_ncu_$tag.log &&
+      timeout 3000 ncu --set full --clock-control none --import-source on -k "regex:$rx" \
+          -s "$skip" -c "$cnt" -o gpurun_out/prof_$tag $CMD > gpurun_out/ncu_full_$tag.log 2>&1
+      echo "ncueval $tag rc=$?"; tail -2 gpurun_out/ncu_full_$tag.log ;;
+    launcheval)
+      tag=${A[0]}
+      CMD="python tools/one_eval.py ${A[1]} ${A[2]:-1.0} 2"
+      timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+          --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1
+      echo "launcheval $tag rc=$?"; tail -3 gpurun_out/ncu_launch_$tag.log ;;
     sanitize)
       tool=${A[0]}; k=${A[1]:-small}
       timeout 2400 compute-sanitizer --tool "$tool" --print-limit 20 \
