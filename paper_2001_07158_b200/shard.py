@@ -5,9 +5,10 @@ accumulators are XOR sums over points (/root/reference/proj/core/src/
 sieve.cpp:297-303), so rank r of N evaluates the contiguous point range
 ``point_range(P, r, N)`` over the full graph it holds, and the per-vertex
 partial accumulators are combined once per evaluation by an exclusive-or.
-NCCL has no XOR reduction: the combine is an all-gather followed by the
-engine's XOR kernel (on CUDA tensors) or torch.bitwise_xor (CPU / gloo).
-There is no other data-path communication.
+NCCL has no XOR reduction: the combine is a reduce-scatter built from an
+all-to-all, the engine's XOR kernel (CUDA tensors; torch.bitwise_xor on
+CPU / gloo) and an all-gather (xor_allreduce).  There is no other data-path
+communication.
 """
 from __future__ import annotations
 
@@ -51,30 +52,54 @@ def plan_units(reps: int, P: int, k: int, rank: int, world: int) -> list[tuple[i
     return work_units(reps, P, rank, world)
 
 
+def _xor_parts(parts, out):
+    """out = XOR of the rows of parts ([N, L]); CUDA: tsv_xor_combine_device."""
+    import torch
+    if parts.is_cuda:
+        from .sieve import xor_combine_device
+        xor_combine_device(parts.data_ptr(), parts.shape[0], parts.shape[1], out.data_ptr(),
+                           torch.cuda.current_stream(parts.device).cuda_stream)
+        return out
+    out.copy_(parts[0])
+    for i in range(1, parts.shape[0]):
+        torch.bitwise_xor(out, parts[i], out=out)
+    return out
+
+
 def xor_allreduce(t, group=None, out=None):
     """XOR-combine an int64 tensor across ranks; every rank receives the result.
 
-    CUDA tensors: NCCL all-gather into one buffer + tsv_xor_combine_device;
-    CPU tensors (gloo): all_gather + torch.bitwise_xor."""
+    NCCL (and gloo) have no XOR reduction, so this is a reduce-scatter /
+    all-gather built from primitives: the flattened tensor is cut into
+    `world` slices, an all-to-all sends slice j of every rank to rank j,
+    rank j XORs the `world` copies of its slice (tsv_xor_combine_device on
+    the device), and an all-gather returns the combined slices.  Each rank
+    moves 2 (world-1)/world of the tensor (an all-gather of whole tensors
+    moves world-1 of it and needs world copies in memory)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     if world == 1:
         return t if out is None else out.copy_(t)
-    if t.is_cuda:
-        from .sieve import xor_combine_device
-        gathered = torch.empty((world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(gathered.view(-1), t.contiguous().view(-1), group=group)
-        res = out if out is not None else torch.empty_like(t)
-        xor_combine_device(gathered.data_ptr(), world, t.numel(), res.data_ptr(),
-                           torch.cuda.current_stream(t.device).cuda_stream)
-        return res
-    parts = [torch.empty_like(t) for _ in range(world)]
-    dist.all_gather(parts, t.contiguous(), group=group)
-    res = parts[0].clone()
-    for p in parts[1:]:
-        torch.bitwise_xor(res, p, out=res)
+    flat = t.contiguous().view(-1)
+    L = flat.numel()
+    sl = (L + world - 1) // world
+    if sl * world != L:
+        src = torch.zeros(sl * world, dtype=flat.dtype, device=flat.device)
+        src[:L] = flat
+    else:
+        src = flat
+    recv = torch.empty(world, sl, dtype=flat.dtype, device=flat.device)
+    dist.all_to_all_single(recv.view(-1), src, group=group)
+    mine = torch.empty(sl, dtype=flat.dtype, device=flat.device)
+    _xor_parts(recv, mine)
+    full = torch.empty(world * sl, dtype=flat.dtype, device=flat.device)
+    if flat.is_cuda:
+        dist.all_gather_into_tensor(full, mine, group=group)
+    else:
+        dist.all_gather(list(full.view(world, sl).unbind(0)), mine, group=group)
+    res = full[:L].view(t.shape)
     if out is not None:
         out.copy_(res)
         return out

@@ -115,3 +115,44 @@ def test_two_rank_gloo_sharding_reproduces_golden(golden, name):
     assert f"{cs:016x}" == case["checksum"]
     if "acc" in case:
         assert [f"{int(x):016x}" for x in acc_fin] == case["acc"]
+
+
+def _xor_worker(rank, world, port, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2001_07158_b200.shard import xor_allreduce
+        rng = np.random.default_rng(1000 + rank)
+        part = rng.integers(-2**63, 2**63 - 1, size=(3, n), dtype=np.int64)
+        res = xor_allreduce(torch.from_numpy(part))
+        out = torch.zeros(3, n, dtype=torch.int64)
+        xor_allreduce(torch.from_numpy(part), out=out)
+        q.put((rank, res.numpy().tolist(), out.numpy().tolist()))
+    finally:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 1), (2, 1001), (4, 7), (4, 4096), (3, 10)])
+def test_xor_reduce_scatter_combine(world, n):
+    """shard.xor_allreduce (all-to-all of slices + XOR + all-gather) returns
+    on EVERY rank the XOR of all ranks' tensors, for sizes that do not split
+    evenly and tensors smaller than the world."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_xor_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    want = np.zeros((3, n), np.int64)
+    for r in range(world):
+        want ^= np.random.default_rng(1000 + r).integers(-2**63, 2**63 - 1, size=(3, n),
+                                                         dtype=np.int64)
+    for rank, res, out in got:
+        assert np.array_equal(np.array(res, np.int64), want), rank
+        assert np.array_equal(np.array(out, np.int64), want), rank
