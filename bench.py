@@ -181,7 +181,12 @@ def coef_alg_bytes(g, sh, k):
         meta = 12 * g.info.arcs + 4 * g.info.runs
         arcs = sum(8 * (a_src + S) * comb(k, l - 1) + meta for l in range(3, k))
         ztrans = sum(8 * S * (comb(k, l - 1) + comb(k, l)) for l in range(2, k))
-        return {"coef_arcs": arcs, "coef_ztrans": ztrans}
+        # vertex-lane engine (z map fused): per middle level 8 B per (live
+        # arc, input entry) + 8 B per (referenced run, output entry) + 8 B of
+        # metadata per arc (edge id, source slot) + 4 B per run (slot)
+        vertex = sum(8 * (a_src * comb(k, l - 1) + S * comb(k, l)) + 8 * g.info.arcs +
+                     4 * g.info.runs for l in range(3, k))
+        return {"coef_arcs": arcs, "coef_ztrans": ztrans, "coef_vertex": vertex}
     cu, cv, ct = (np.asarray(x, dtype=np.int64) for x in g.edges())
     if not g.directed():
         cu, cv, ct = np.concatenate([cu, cv]), np.concatenate([cv, cu]), np.concatenate([ct, ct])
@@ -229,16 +234,17 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
     alg1 = coef_alg_bytes() of one evaluation; achieved = those bytes x the
     evaluations of the profile pass / the kernel family's CUDA-event time in
     that pass; int_pipe from the committed ncu capture of the same kernel."""
-    alg = {nm: evals * b for nm, b in alg1.items()}
+    alg = {nm: evals * b for nm, b in alg1.items() if nm in coef}
     name = max(coef, key=lambda nm: coef[nm][1])
     n_launch, tot_ms = coef[name]
-    if not n_launch or not alg[name]:
+    if not n_launch or not alg.get(name):
         return None
     achieved = alg[name] / (tot_ms * 1e-3) / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
             "kernel": {"coef_arcs": "k_coef_items / k_coef_arcs (3 <= l < k)",
-                       "coef_ztrans": "k_coef_ztrans_direct (2 <= l < k)"}[name],
+                       "coef_ztrans": "k_coef_ztrans_direct (2 <= l < k)",
+                       "coef_vertex": "k_coef_vertex (3 <= l < k; z map fused)"}[name],
             "engine": "coefficient (top-degree) form on the shaded subgraph, DESIGN.md 2b",
             "family": name,
             "avg_launch_ms": tot_ms / n_launch,
@@ -544,6 +550,11 @@ def main():
         lvl_n, lvl_ms = _native.Profile.get("level_grouped")
         grouped = bool(lvl_n)
     coef = {nm: _native.Profile.get(nm) for nm in ("coef_arcs", "coef_ztrans")}
+    # the vertex-lane engine (coef_vertex.cu) fuses the z map into the level:
+    # one family, "coef_vertex" (middle levels)
+    vx = _native.Profile.get("coef_vertex")
+    if vx[0]:
+        coef = {"coef_vertex": vx}
     all_n, all_ms = _native.Profile.get(None)
     _native.Profile.enable(False)
     if world > 1:
@@ -710,8 +721,7 @@ def main():
                 "nflagged": nflagged, "graph": graph_info,
                 "engine": "coefficient" if any(c for c, _ in coef.values()) else "points",
                 "kernel_ms_per_step": {"level": lvl_ms / prof_steps,
-                                       "coef_arcs": coef["coef_arcs"][1] / prof_steps,
-                                       "coef_ztrans": coef["coef_ztrans"][1] / prof_steps,
+                                       **{nm: c[1] / prof_steps for nm, c in coef.items()},
                                        "all": all_ms / prof_steps,
                                        "source": f"{prof_steps}-step single-stream profile pass"}}
         print(json.dumps(line), flush=True)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <vector>
 
 #include "engine.hpp"
@@ -94,6 +95,26 @@ void launch_coef_readout(int32_t n, const uint64_t* zj, int k, const uint64_t* u
                          const uint64_t* vsv, uint64_t* acc, cudaStream_t st);
 void launch_slot_head(int64_t R, const int32_t* run_slot, const int32_t* run_head,
                       int32_t* slot_head, cudaStream_t st);
+
+// Vertex-lane form of the coefficient engine (coef_vertex.cu): every vertex
+// multi-shade, k <= kVertexMaxK.  Work list = the vertices with arcs sorted
+// by arc count (descending), built once per graph.
+constexpr int kVertexMaxK = 5;
+struct VertList {
+  int64_t nv = 0;
+  int32_t* head = nullptr;   // vertex
+  int64_t* start = nullptr;  // its first arc (vertex-major arc order)
+  int32_t* count = nullptr;  // its arcs
+};
+bool vertex_engine_supports(int k);
+void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
+                       const std::function<void*(size_t)>& alloc,
+                       const std::function<void(void*)>& release);
+// One level l of the vertex-lane engine: S_l rows (stride C(k, l)) at the
+// referenced slots into p.ubuf from p.s_prev (stride C(k, l-1)) or zj (l = 2);
+// at l = k the readout acc[h] ^= det * ... (no ulast).
+void launch_coef_vertex(const CoefParams& p, const VertList& vl, uint64_t det, uint64_t* acc,
+                        cudaStream_t st);
 
 // Host tables (colex order = increasing bit mask within a level).
 struct CoefTables {

@@ -1,0 +1,422 @@
+// coef_vertex.cu -- the coefficient engine (coef_kernels.cu) in VERTEX-LANE
+// form, for the case the BASELINE headline runs: every vertex carries several
+// shades (k-TempPath: all k of them), small k, bounded in-degree (C5: n=1e8,
+// m=1e9, k=5).
+//
+// Same algebra as coef_kernels.cu (derivation at its top):
+//
+//   U_l[run][T'] = XOR_{arcs a of head up to run} y(e_a, l-1) * S_{l-1}[src_a][T']
+//   S_l[run][T]  = XOR_{j in T} z_{head,j} * U_l[run][T \ {j}]
+//
+// but organised for instruction count, not for arc parallelism:
+//
+//  * one LANE owns one head vertex and walks its arcs in time order, so the
+//    per-vertex prefix XOR is a register accumulation -- no segmented scan,
+//    no shuffles, no chunk carry fix-up, no per-arc staging;
+//  * lanes of a warp take vertices of equal in-degree (a work list sorted by
+//    arc count, built once per graph), so they step together;
+//  * the arc product y * x multiplies by the arc's y split once (Karatsuba
+//    holes, gf_device.cuh) and the products of a run accumulate UNREDUCED
+//    (128-bit, class-masked): one reduction per referenced run end instead of
+//    one per product;
+//  * the z map S = z_h ^ U is fused: a referenced run end pushes its U row to
+//    a per-warp shared-memory queue; whenever 32 rows are queued, every lane
+//    maps one row (z_{h,j} split once per j, L products per output summed
+//    unreduced, one reduction per output) and stores the S row -- the rows
+//    never make a round trip through HBM as U, and no lane idles while
+//    others map;
+//  * level k is fused with the readout: acc[h] ^= det(W) * XOR_j z_{h,j} *
+//    U_k[h][[k] - {j}] from the lane's own accumulator (no ulast buffer).
+//
+// Reads per live arc: its metadata and one row of C(k, l-1) words.  Writes:
+// one row of C(k, l) words per referenced run.  Bit-identical to the other
+// engines (tests/test_gpu_parity.py, tests/test_gpu_full.py).
+#include <cuda_runtime.h>
+
+#include <cub/cub.cuh>
+
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+
+#include "coef.hpp"
+#include "gf_device.cuh"
+#include "layout.hpp"
+
+namespace tsv {
+namespace {
+
+constexpr unsigned kFullV = 0xffffffffu;
+constexpr int kVWarps = 2;   // warps per block
+constexpr int kQCap = 64;    // queued rows per warp (ring)
+
+__host__ __device__ constexpr int binom_c(int n, int r) {
+  if (r < 0 || r > n) return 0;
+  int v = 1;
+  for (int i = 0; i < r; ++i) v = v * (n - i) / (i + 1);
+  return v;
+}
+
+// Colex rank of a subset mask (the order of CoefTables: increasing mask
+// within a level): sum over its i-th smallest element x of C(x, i+1).
+__host__ __device__ constexpr int colex_rank(unsigned mask) {
+  int r = 0, i = 0;
+  for (int x = 0; x < 32; ++x)
+    if ((mask >> x) & 1u) {
+      r += binom_c(x, i + 1);
+      ++i;
+    }
+  return r;
+}
+
+// For the l-subsets T of [k] in colex order: T's mask, and for each j in T
+// the rank of T - {j} among the (l-1)-subsets.
+template <int K, int L>
+struct SubsetTab {
+  static constexpr int F = binom_c(K, L);
+  unsigned mask[F > 0 ? F : 1] = {};
+  int less[F > 0 ? F : 1][K] = {};  // less[o][j] = rank(T_o - {j}) if j in T_o, else -1
+  constexpr SubsetTab() {
+    int o = 0;
+    for (unsigned T = 0; T < (1u << K); ++T) {
+      int pc = 0;
+      for (int x = 0; x < K; ++x) pc += (T >> x) & 1u;
+      if (pc != L) continue;
+      mask[o] = T;
+      for (int j = 0; j < K; ++j) less[o][j] = ((T >> j) & 1u) ? colex_rank(T & ~(1u << j)) : -1;
+      ++o;
+    }
+  }
+};
+
+// 128-bit unreduced carry-less product accumulation (class-masked).
+__device__ __forceinline__ void clmul_acc(const KSplit& a, uint64_t b, u128& acc) {
+  const u128 p = clmul64_kara_s(a, ksplit(b));
+  acc.lo ^= p.lo;
+  acc.hi ^= p.hi;
+}
+
+// Reduction with ALU shifts (the FMA pipe carries the wide multiplies).
+__device__ __forceinline__ uint64_t gf_reduce_alu(u128 p) {
+  const uint64_t h = p.hi;
+  const uint64_t over = (h >> 60) ^ (h >> 61) ^ (h >> 63);  // x^64.. terms of the first fold
+  const uint64_t f1 = h ^ (h << 1) ^ (h << 3) ^ (h << 4);
+  return p.lo ^ f1 ^ over ^ (over << 1) ^ (over << 3) ^ (over << 4);
+}
+
+struct VertArgs {
+  CoefParams P;              // graph, seed, levels, rows (s_prev, ubuf), max_ts, anchor
+  const int32_t* wl_head;    // work list sorted by arc count (descending)
+  const int64_t* wl_start;   // first arc of the vertex
+  const int32_t* wl_count;   // arcs of the vertex
+  int64_t nv;                // vertices in the list
+  uint64_t det;              // det(W) of the shade basis (readout)
+  uint64_t* acc;             // level k: per-vertex accumulators (XORed into)
+};
+
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// Per-warp shared state.  Lane-minor layouts ([entry][lane], [entry][slot])
+// keep every access conflict-free.
+template <int E, int F, int L, bool LAST>
+struct VertSmem {
+  uint64_t x[2][E][32];                 // the next / current arc's source row (cp.async)
+  uint64_t u[E][32];                    // the lane's running prefix U_L
+  uint64_t q[LAST ? 1 : E][kQCap];      // queued U rows (ring)
+  int32_t q_slot[kQCap], q_head[kQCap];
+  uint8_t pin[F > 0 ? F : 1][L], pj[F > 0 ? F : 1][L];  // output o: (rank of T_o - {j}, j) pairs
+};
+
+template <int K, int L, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) {
+  constexpr int E = binom_c(K, L - 1);  // input entries (row of level L-1)
+  constexpr int F = binom_c(K, L);      // output entries
+  using Sm = VertSmem<E, F, L, LAST>;
+  __shared__ Sm smem[kVWarps];
+  const CoefParams& P = A.P;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  Sm& S = smem[wib];
+  if (!LAST && lane == 0) {  // output pairs of the z map (colex order, coef_tables)
+    constexpr SubsetTab<K, L> TL{};
+    for (int o = 0; o < F; ++o) {
+      int c = 0;
+      for (int j = 0; j < K; ++j)
+        if (TL.less[o][j] >= 0) {
+          S.pin[o][c] = static_cast<uint8_t>(TL.less[o][j]);
+          S.pj[o][c] = static_cast<uint8_t>(j);
+          ++c;
+        }
+    }
+  }
+  const int64_t task = static_cast<int64_t>(blockIdx.x) * kVWarps + wib;
+  const int64_t idx = task * 32 + lane;
+  if (task * 32 >= A.nv) return;  // warp-uniform
+  const bool act = idx < A.nv;
+  const int32_t h = act ? __ldg(A.wl_head + idx) : 0;
+  const int64_t a0 = act ? __ldg(A.wl_start + idx) : 0;
+  const int cnt = act ? __ldg(A.wl_count + idx) : 0;
+  int32_t run = act ? __ldg(P.g.vtx_run_off + h) : 0;
+  const int steps = __reduce_max_sync(kFullV, cnt);
+  const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
+  const uint64_t yb = static_cast<uint64_t>(L - 1) + 0x165667b19e3779f9ull;
+  const uint64_t* __restrict__ rows = FIRST ? P.zj : P.s_prev;
+#pragma unroll
+  for (int e = 0; e < E; ++e) S.u[e][lane] = 0;
+  int qh = 0, qn = 0;  // ring head, queued count (warp-uniform)
+
+  // z map of `take` queued rows (one per lane), stored as S rows of F words:
+  // S[T] = XOR_{j in T} z_j * U[T - {j}], the L products of an output summed
+  // unreduced, one reduction per output
+  auto flush = [&](int take) {
+    __syncwarp();
+    if (lane < take) {
+      const int qi = (qh + lane) & (kQCap - 1);
+      const int32_t hd = S.q_head[qi];
+      uint64_t z[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) z[j] = __ldg(P.zj + static_cast<int64_t>(hd) * K + j);
+      uint64_t* out = P.ubuf + static_cast<int64_t>(S.q_slot[qi]) * F;
+#pragma unroll 1
+      for (int o = 0; o < F; ++o) {
+        u128 s = {0, 0};
+#pragma unroll
+        for (int c = 0; c < L; ++c) {
+          const int j = S.pj[o][c];
+          uint64_t zj = z[0];
+#pragma unroll
+          for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
+          clmul_acc(ksplit(zj), S.q[S.pin[o][c]][qi], s);
+        }
+        out[o] = gf_reduce_alu(s);
+      }
+    }
+    qh = (qh + take) & (kQCap - 1);
+    qn -= take;
+    __syncwarp();
+  };
+
+  // the next arc's source row goes to shared memory one step ahead (cp.async)
+  auto fetch = [&](int i, uint32_t& meta, bool& live) {
+    live = false;
+    meta = 0;
+    if (i < cnt) {
+      const int64_t a = a0 + i;
+      meta = __ldg(P.g.arc_meta + a);
+      const int32_t src = FIRST ? __ldg(P.g.arc_tail + a) : __ldg(P.g.arc_src + a);
+      live = src >= 0;
+      if (FIRST) live = live && (P.anchor_source < 0 || src == P.anchor_source);
+      if (live) {
+        const uint64_t* row = rows + static_cast<int64_t>(src) * E;
+#pragma unroll
+        for (int e = 0; e < E; ++e) cp_async8(&S.x[i & 1][e][lane], row + e);
+      }
+    }
+    cp_async_commit();
+  };
+  uint32_t nmeta;
+  bool nlive;
+  fetch(0, nmeta, nlive);
+  for (int i = 0; i < steps; ++i) {
+    const uint32_t meta = nmeta;
+    bool live = nlive;
+    cp_async_wait_all();  // row i has landed (lane-private slots: no barrier)
+    if (i + 1 < steps) fetch(i + 1, nmeta, nlive);
+    if (LAST && live) live = __ldg(P.g.run_ts + run) <= P.max_ts;
+    if (live) {
+      const KSplit ys = ksplit(draw_edge_y(pre, yb, meta & kEdgeMask));
+#pragma unroll 1
+      for (int e = 0; e < E; ++e)
+        S.u[e][lane] ^= gf_reduce_alu(clmul64_kara_s(ys, ksplit(S.x[i & 1][e][lane])));
+    }
+    const bool runend = i < cnt && (meta & kRunEnd);
+    if (!LAST) {
+      const int32_t slot = runend ? __ldg(P.g.run_slot + run) : -1;
+      const unsigned push = __ballot_sync(kFullV, slot >= 0);
+      if (push) {
+        if (slot >= 0) {
+          const int qi = (qh + qn + __popc(push & ((1u << lane) - 1u))) & (kQCap - 1);
+          S.q_slot[qi] = slot;
+          S.q_head[qi] = h;
+#pragma unroll
+          for (int e = 0; e < E; ++e) S.q[e][qi] = S.u[e][lane];
+        }
+        qn += __popc(push);
+        if (qn >= 32) flush(32);
+      }
+    }
+    if (runend) ++run;
+  }
+  if (!LAST) {
+    while (qn > 0) flush(qn < 32 ? qn : 32);
+  } else if (act && cnt > 0) {
+    // readout: acc[h] ^= det * XOR_j z_{h,j} * U_k[[k] - {j}]; U_k entries are
+    // the (k-1)-subsets, [k] - {j} has colex rank k-1-j
+    u128 r = {0, 0};
+#pragma unroll 1
+    for (int j = 0; j < K; ++j)
+      clmul_acc(ksplit(__ldg(P.zj + static_cast<int64_t>(h) * K + j)), S.u[K - 1 - j][lane], r);
+    uint64_t v = gf_reduce_alu(r);
+    if (A.det != 1) v = gf_mul(A.det, v);
+    if (v) A.acc[h] ^= v;
+  }
+}
+
+template <int K>
+void vertex_dispatch(const VertArgs& a, int l, cudaStream_t st) {
+  const unsigned blocks =
+      static_cast<unsigned>((a.nv + 32 * kVWarps - 1) / (32 * kVWarps));
+  if (!blocks) return;
+  const dim3 thr(kVWarps * 32);
+  if (l == 2 && l == K) k_coef_vertex<K, 2, true, true><<<blocks, thr, 0, st>>>(a);
+  else if (l == 2) k_coef_vertex<K, 2, true, false><<<blocks, thr, 0, st>>>(a);
+  else if (l == K) {
+    if constexpr (K >= 3) k_coef_vertex<K, K, false, true><<<blocks, thr, 0, st>>>(a);
+  } else {
+    if constexpr (K >= 4) {
+      if (l == 3) k_coef_vertex<K, 3, false, false><<<blocks, thr, 0, st>>>(a);
+      if constexpr (K >= 5)
+        if (l == 4) k_coef_vertex<K, 4, false, false><<<blocks, thr, 0, st>>>(a);
+    }
+  }
+}
+
+// ---- work list: vertices with arcs, sorted by arc count (descending) -------
+
+__global__ void k_vstart_pos(int64_t A, const uint32_t* __restrict__ meta,
+                             uint8_t* __restrict__ f) {
+  const int64_t a = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (a < A) f[a] = (meta[a] & kVStart) ? 1 : 0;
+}
+
+__global__ void k_has_runs(int32_t n, const int32_t* __restrict__ vro, uint8_t* __restrict__ f) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < n) f[x] = vro[x + 1] > vro[x] ? 1 : 0;
+}
+
+__global__ void k_counts(int64_t nv, int64_t A, const int64_t* __restrict__ start,
+                         int32_t* __restrict__ cnt, int32_t* __restrict__ pos) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  cnt[i] = static_cast<int32_t>((i + 1 < nv ? start[i + 1] : A) - start[i]);
+  pos[i] = static_cast<int32_t>(i);
+}
+
+__global__ void k_gather_start(int64_t nv, const int32_t* __restrict__ perm,
+                               const int64_t* __restrict__ start,
+                               const int32_t* __restrict__ head_in, int64_t* __restrict__ s_out,
+                               int32_t* __restrict__ h_out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const int32_t p = perm[i];
+  s_out[i] = start[p];
+  h_out[i] = head_in[p];
+}
+
+inline unsigned nblk_v(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
+
+}  // namespace
+
+bool vertex_engine_supports(int k) { return k >= 2 && k <= kVertexMaxK; }
+
+void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
+                       const std::function<void*(size_t)>& alloc,
+                       const std::function<void(void*)>& release) {
+  const int64_t A = g.A;
+  const int32_t n = g.n;
+  out = VertList{};
+  if (A == 0 || n == 0) return;
+  auto ck = [](cudaError_t e) {
+    if (e != cudaSuccess)
+      throw std::runtime_error(std::string("vertex list: ") + cudaGetErrorString(e));
+  };
+  // vertex starts in arc order (= increasing vertex id; at most n of them) ...
+  uint8_t* vf = static_cast<uint8_t*>(alloc(static_cast<size_t>(A)));
+  int64_t* vs = static_cast<int64_t*>(alloc((static_cast<size_t>(n) + 1) * 8));
+  int64_t* cnt64 = static_cast<int64_t*>(alloc(8));
+  k_vstart_pos<<<nblk_v(A), 256, 0, st>>>(A, g.arc_meta, vf);
+  cub::CountingInputIterator<int64_t> it(0);
+  size_t tmp = 0;
+  ck(cub::DeviceSelect::Flagged(nullptr, tmp, it, vf, vs, cnt64, A, st));
+  void* t = alloc(tmp ? tmp : 8);
+  ck(cub::DeviceSelect::Flagged(t, tmp, it, vf, vs, cnt64, A, st));
+  release(t);
+  int64_t nv = 0;
+  ck(cudaMemcpyAsync(&nv, cnt64, 8, cudaMemcpyDeviceToHost, st));
+  ck(cudaStreamSynchronize(st));
+  release(vf);
+  release(cnt64);
+  // ... which are the vertices with runs, in increasing id
+  uint8_t* hf = static_cast<uint8_t*>(alloc(static_cast<size_t>(n)));
+  int32_t* heads = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
+  int32_t* cnt32 = static_cast<int32_t*>(alloc(8));
+  k_has_runs<<<nblk_v(n), 256, 0, st>>>(n, g.vtx_run_off, hf);
+  cub::CountingInputIterator<int32_t> it32(0);
+  tmp = 0;
+  ck(cub::DeviceSelect::Flagged(nullptr, tmp, it32, hf, heads, cnt32, n, st));
+  t = alloc(tmp ? tmp : 8);
+  ck(cub::DeviceSelect::Flagged(t, tmp, it32, hf, heads, cnt32, n, st));
+  release(t);
+  release(hf);
+  release(cnt32);
+  // arc counts; sort by count (descending), carrying the list position
+  int32_t* counts = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
+  int32_t* pos = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
+  int32_t* counts_s = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
+  int32_t* pos_s = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
+  k_counts<<<nblk_v(nv), 256, 0, st>>>(nv, A, vs, counts, pos);
+  tmp = 0;
+  ck(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, counts, counts_s, pos, pos_s,
+                                               static_cast<int>(nv), 0, 32, st));
+  t = alloc(tmp ? tmp : 8);
+  ck(cub::DeviceRadixSort::SortPairsDescending(t, tmp, counts, counts_s, pos, pos_s,
+                                               static_cast<int>(nv), 0, 32, st));
+  release(t);
+  release(counts);
+  release(pos);
+  int64_t* start_s = static_cast<int64_t*>(alloc(static_cast<size_t>(nv) * 8 + 8));
+  int32_t* head_s = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
+  k_gather_start<<<nblk_v(nv), 256, 0, st>>>(nv, pos_s, vs, heads, start_s, head_s);
+  ck(cudaGetLastError());
+  ck(cudaStreamSynchronize(st));
+  release(pos_s);
+  release(vs);
+  release(heads);
+  out.nv = nv;
+  out.head = head_s;
+  out.start = start_s;
+  out.count = counts_s;
+}
+
+void launch_coef_vertex(const CoefParams& p, const VertList& vl, uint64_t det, uint64_t* acc,
+                        cudaStream_t st) {
+  if (vl.nv == 0) return;
+  VertArgs a;
+  a.P = p;
+  a.wl_head = vl.head;
+  a.wl_start = vl.start;
+  a.wl_count = vl.count;
+  a.nv = vl.nv;
+  a.det = det;
+  a.acc = acc;
+  prof_begin(p.last ? "coef_vertex_last" : p.ell == 2 ? "coef_vertex_first" : "coef_vertex", st);
+  switch (p.k) {
+    case 2: vertex_dispatch<2>(a, p.ell, st); break;
+    case 3: vertex_dispatch<3>(a, p.ell, st); break;
+    case 4: vertex_dispatch<4>(a, p.ell, st); break;
+    case 5: vertex_dispatch<5>(a, p.ell, st); break;
+    default: break;
+  }
+  prof_end(st);
+}
+
+}  // namespace tsv

@@ -225,11 +225,18 @@ struct tsv_graph {
   // stream of the synchronous entry points (created once per graph)
   mutable std::mutex stream_mu;
   mutable cudaStream_t api_stream = nullptr;
+  // work list of the vertex-lane coefficient engine (coef_vertex.cu), built
+  // on first use: 0 not built, 1 built, 2 not applicable (hub vertices)
+  mutable std::mutex vl_mu;
+  mutable int vl_state = 0;
+  mutable tsv::VertList vl;
+  mutable std::vector<void*> vl_owned;
   ~tsv_graph() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     if (api_stream) cudaStreamDestroy(api_stream);
+    for (void* p : vl_owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     cudaSetDevice(prev);
   }
@@ -448,6 +455,52 @@ const CoefConst& coef_const(int dev, int k, bool items) {
   return *cache[key];
 }
 
+// Largest in-degree the vertex-lane engine takes: a lane walks its vertex's
+// arcs serially, so power-law hubs go to the arc-parallel kernels.
+constexpr int32_t kVertexMaxArcs = 4096;
+
+// The vertex-lane work list of g (built once, on `st`), or nullptr when the
+// graph has hub vertices.
+const tsv::VertList* vertex_list(const tsv_graph* g, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g->vl_mu);
+  if (g->vl_state == 1) return &g->vl;
+  if (g->vl_state == 2) return nullptr;
+  std::vector<void*> live;
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+      throw CudaError("vertex list: out of device memory");
+    live.push_back(p);
+    return p;
+  };
+  auto release = [&](void* p) {
+    auto it = std::find(live.begin(), live.end(), p);
+    if (it != live.end()) live.erase(it);
+    cudaFreeAsync(p, st);
+  };
+  tsv::VertList vl;
+  try {
+    tsv::build_vertex_list(g->dev, vl, st, alloc, release);
+  } catch (...) {
+    for (void* p : live) cudaFreeAsync(p, st);
+    throw;
+  }
+  int32_t maxc = 0;
+  if (vl.nv) {
+    TSV_CUDA(cudaMemcpyAsync(&maxc, vl.count, 4, cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+  }
+  if (maxc > kVertexMaxArcs) {
+    for (void* p : live) cudaFreeAsync(p, st);
+    g->vl_state = 2;
+    return nullptr;
+  }
+  g->vl = vl;
+  g->vl_owned = live;
+  g->vl_state = 1;
+  return &g->vl;
+}
+
 // The coefficient (top-degree) engine, coef_kernels.cu: the XOR over ALL
 // 2^k sieve points in one pass per level, bit-identical to the point engine.
 // Used for full-range evaluations when its working set (two S x M state
@@ -534,6 +587,31 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                             vc ? nullptr : vsh.as<int8_t>(), mlist.as<int2>(),
                             mcount.as<int32_t>(), st);
   const int2* dp = cc.pairs;
+  // every shaded vertex multi-shade and small k (k-TempPath, C5): the
+  // vertex-lane engine (coef_vertex.cu) -- fused z map and readout
+  const char* vx_env = std::getenv("TSV_VERTEX");
+  const bool try_vertex = !vc && sh->single == 0 && tsv::vertex_engine_supports(k) &&
+                          !(vx_env && vx_env[0] == '0');
+  if (const tsv::VertList* vl = try_vertex ? vertex_list(g, st) : nullptr) {
+    uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
+    for (int l = 2; l <= k; ++l) {
+      tsv::CoefParams cp;
+      cp.g = g->dev;
+      cp.zj = d_zj.as<uint64_t>();
+      cp.k = k;
+      cp.ell = l;
+      cp.last = l == k;
+      cp.seed = cfg->seed;
+      cp.anchor_source = anchor_source;
+      cp.s_prev = A;
+      cp.ubuf = B;
+      cp.max_ts = max_ts;
+      tsv::launch_coef_vertex(cp, *vl, scale, d_acc, st);
+      TSV_CUDA(cudaGetLastError());
+      std::swap(A, B);
+    }
+    return true;
+  }
   // row strides: level l's rows hold its U row (C(k, l-1)) and then its S row (C(k, l))
   auto rs = [&](int l) { return static_cast<int>(std::max(T.count[l - 1], T.count[l])); };
   uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();

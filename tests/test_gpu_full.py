@@ -98,12 +98,12 @@ def run_engines(c, seed, max_ts, expect, monkeypatch):
     _native.Profile.enable(True)
     try:
         got = outcome(c.decide(seed, max_ts))
-        assert engine_ran("coef_arcs") or engine_ran("coef_arcs_last")
+        assert engine_ran("coef_arcs_last") or engine_ran("coef_vertex_last")
         assert got == expect, ("coefficient engine", seed, max_ts)
         monkeypatch.setenv("TSV_ENGINE", "points")
         _native.Profile.reset()
         got = outcome(c.decide(seed, max_ts))
-        assert not engine_ran("coef_arcs_last")
+        assert not engine_ran("coef_arcs_last") and not engine_ran("coef_vertex_last")
         assert engine_ran("level_last")
         assert got == expect, ("point engine", seed, max_ts)
     finally:
@@ -161,9 +161,13 @@ def test_full_c5_ktemppath_vs_oracle(cuda_device, full_golden, monkeypatch):
     _native.Profile.reset()
     _native.Profile.enable(True)
     got = outcome(c.decide(e["seed"], e["max_ts"]))
-    assert engine_ran("coef_arcs_last")
+    assert engine_ran("coef_vertex_last")       # the vertex-lane engine (coef_vertex.cu)
     _native.Profile.enable(False)
     assert got == want(e)
+    # and the arc-parallel coefficient kernels (TSV_VERTEX=0)
+    monkeypatch.setenv("TSV_VERTEX", "0")
+    assert outcome(c.decide(e["seed"], e["max_ts"])) == want(e)
+    monkeypatch.delenv("TSV_VERTEX")
     pts = {p["p_begin"]: p for p in rec["points"]}
     for p0 in (0, 7, 31):
         got = summary(c.points(1, p0, p0 + 1))

@@ -240,7 +240,7 @@ def test_partial_point_ranges_vs_oracle(cuda_device, ppb):
         _native.Profile.enable(False)
 
 
-@pytest.mark.parametrize("env", [{"TSV_ENGINE": "points"}, {"TSV_ITEMS": "0"},
+@pytest.mark.parametrize("env", [{"TSV_ENGINE": "points"}, {"TSV_ITEMS": "0"}, {"TSV_VERTEX": "0"},
                                  {"TSV_ITEMS": "1", "TSV_ITEMS_REG": "0"}, {"TSV_ITEMS": "1"},
                                  {"TSV_ZTRANS": "tab"}, {"TSV_SUBGRAPH": "0"},
                                  {"TSV_PERSIST": "0"}, {"TSV_WALK_SPLIT": "0"}])
@@ -280,6 +280,44 @@ def test_coefficient_engine_kernels_agree(cuda_device, monkeypatch, env):
         nz += bool(_oracle_vs_gpu(n, u, v, ts, True, one, [1] * k_, 29 + k_))
     nz += bool(_oracle_vs_gpu(n, u, v, ts, False, colors, [1, 1, 2, 3, 4, 2], 31, max_ts=20))
     assert nz >= 8
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
+def test_vertex_engine_vs_oracle(cuda_device, k):
+    """The vertex-lane coefficient engine (coef_vertex.cu; every shaded vertex
+    multi-shade, k <= 5 -- k-TempPath, C5's query): oracle accumulators for
+    directed and undirected graphs, (s,d) anchors, horizons below t, shadeless
+    vertices, and a graph with a hub above the engine's in-degree bound
+    (which must fall back to the arc-parallel kernels)."""
+    rng = np.random.default_rng(70 + k)
+    n, m, t = 300, 5000, 50
+    u = rng.integers(0, n, m)
+    v = rng.integers(0, n, m)
+    ts = rng.integers(1, t + 1, m)
+    ones = np.ones(n, np.int64)
+    two = rng.integers(1, 4, n)              # colors 1, 2 shaded twice; 3 shadeless
+    _native.Profile.reset()
+    _native.Profile.enable(True)
+    try:
+        nz = 0
+        for d, colors, motif, seed, mt, anchor in (
+                (True, ones, [1] * k, 3, None, (-1, -1)),
+                (False, ones, [1] * k, 5, 31, (-1, -1)),
+                (True, ones, [1] * k, 7, None, (4, 11)),
+                (True, two, {2: [1, 1], 3: [1, 1, 1], 4: [1, 1, 2, 2], 5: [1, 1, 2, 2, 2]}[k],
+                 9, 40, (-1, -1))):
+            nz += bool(_oracle_vs_gpu(n, u, v, ts, d, colors, motif, seed, anchor, mt))
+        assert nz >= 2
+        assert _native.Profile.get("coef_vertex_last")[0] > 0
+        # hub above the in-degree bound (4096 arcs): the arc kernels take over
+        hv = np.concatenate([v, np.zeros(5000, np.int64)])
+        hu = np.concatenate([u, rng.integers(1, n, 5000)])
+        hts = np.concatenate([ts, rng.integers(1, t + 1, 5000)])
+        _native.Profile.reset()
+        _oracle_vs_gpu(n, hu, hv, hts, True, ones, [1] * k, 13)
+        assert _native.Profile.get("coef_vertex_last")[0] == 0
+    finally:
+        _native.Profile.enable(False)
 
 
 @pytest.mark.parametrize("env", [{}, {"TSV_ENGINE": "points"}])
