@@ -43,7 +43,8 @@ def main():
     _native.Profile.enable(True)
     for _ in range(3):
         T.eval_temporal_sieve(g, k, full, sh, cfg, an)
-    names = ["coef_arcs_first", "coef_arcs", "coef_arcs_last", "coef_ztrans", "coef_fixup",
+    names = ["coef_vertex_first", "coef_vertex", "coef_vertex_last",
+             "coef_arcs_first", "coef_arcs", "coef_arcs_last", "coef_ztrans", "coef_fixup",
              "coef_readout", "level_first", "level", "level_last", "level_grouped_first",
              "level_grouped", "zbatch", "zj", "fixup"]
     kern = {}
