@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) 
 
   // z map of `take` queued rows (one per lane), stored as S rows of F words:
   // S[T] = XOR_{j in T} z_j * U[T - {j}], the L products of an output summed
-  // unreduced, one reduction per output
+  // in raw class form (gf_device.cuh ClassAcc): one Karatsuba combine, one
+  // class mask and one reduction per output
   auto flush = [&](int take) {
     __syncwarp();
     if (lane < take) {
@@ -188,16 +189,17 @@ __global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) 
       uint64_t* out = P.ubuf + static_cast<int64_t>(S.q_slot[qi]) * F;
 #pragma unroll 1
       for (int o = 0; o < F; ++o) {
-        u128 s = {0, 0};
+        ClassAcc ca;
+        class_zero(ca);
 #pragma unroll
         for (int c = 0; c < L; ++c) {
           const int j = S.pj[o][c];
           uint64_t zj = z[0];
 #pragma unroll
           for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
-          clmul_acc(ksplit(zj), S.q[S.pin[o][c]][qi], s);
+          class_acc(ksplit(zj), ksplit(S.q[S.pin[o][c]][qi]), ca);
         }
-        out[o] = gf_reduce_alu(s);
+        out[o] = gf_reduce_alu(class_finish(ca));
       }
     }
     qh = (qh + take) & (kQCap - 1);
@@ -261,11 +263,13 @@ __global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) 
   } else if (act && cnt > 0) {
     // readout: acc[h] ^= det * XOR_j z_{h,j} * U_k[[k] - {j}]; U_k entries are
     // the (k-1)-subsets, [k] - {j} has colex rank k-1-j
-    u128 r = {0, 0};
+    ClassAcc ca;
+    class_zero(ca);
 #pragma unroll 1
     for (int j = 0; j < K; ++j)
-      clmul_acc(ksplit(__ldg(P.zj + static_cast<int64_t>(h) * K + j)), S.u[K - 1 - j][lane], r);
-    uint64_t v = gf_reduce_alu(r);
+      class_acc(ksplit(__ldg(P.zj + static_cast<int64_t>(h) * K + j)), ksplit(S.u[K - 1 - j][lane]),
+                ca);
+    uint64_t v = gf_reduce_alu(class_finish(ca));
     if (A.det != 1) v = gf_mul(A.det, v);
     if (v) A.acc[h] ^= v;
   }

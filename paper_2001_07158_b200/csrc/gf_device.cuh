@@ -111,6 +111,46 @@ __device__ __forceinline__ u128 clmul64_kara_s(const KSplit& A, const KSplit& B)
   return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
 }
 
+// Sums of carry-less products in raw Karatsuba class form: the class
+// products L, H, M of every term are XORed as they come and combined, masked
+// (mask_class) and reduced ONCE for the whole sum -- all three steps are
+// linear over XOR.  For sums of several products (the z map's
+// S[T] = XOR_j z_j * U[T - {j}]) this saves the per-product combine and mask.
+struct ClassAcc {
+  uint64_t L[4], H[4], M[4];
+};
+
+__device__ __forceinline__ void class_zero(ClassAcc& c) {
+#pragma unroll
+  for (int r = 0; r < 4; ++r) c.L[r] = c.H[r] = c.M[r] = 0;
+}
+
+__device__ __forceinline__ void class_acc(const KSplit& A, const KSplit& B, ClassAcc& c) {
+  c.L[0] ^= class_prod<0>(A.l, B.l);
+  c.L[1] ^= class_prod<1>(A.l, B.l);
+  c.L[2] ^= class_prod<2>(A.l, B.l);
+  c.L[3] ^= class_prod<3>(A.l, B.l);
+  c.H[0] ^= class_prod<0>(A.h, B.h);
+  c.H[1] ^= class_prod<1>(A.h, B.h);
+  c.H[2] ^= class_prod<2>(A.h, B.h);
+  c.H[3] ^= class_prod<3>(A.h, B.h);
+  c.M[0] ^= class_prod<0>(A.m, B.m);
+  c.M[1] ^= class_prod<1>(A.m, B.m);
+  c.M[2] ^= class_prod<2>(A.m, B.m);
+  c.M[3] ^= class_prod<3>(A.m, B.m);
+}
+
+__device__ __forceinline__ u128 class_finish(const ClassAcc& c) {
+  uint64_t lo[4], hi[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint64_t M = c.M[r] ^ c.L[r] ^ c.H[r];
+    lo[r] = c.L[r] ^ (M << 32);
+    hi[r] = c.H[r] ^ (M >> 32);
+  }
+  return {mask_class(lo[0], lo[1], lo[2], lo[3]), mask_class(hi[0], hi[1], hi[2], hi[3])};
+}
+
 // Schoolbook over 32-bit halves with deferred class masking.
 __device__ __forceinline__ u128 clmul64_school(uint64_t a, uint64_t b) {
   const Split4 al = split4(lo32(a)), ah = split4(hi32(a));
