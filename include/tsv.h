@@ -205,6 +205,11 @@ int tsv_finalize(int32_t n, uint64_t* acc, int32_t anchor_sink,
 int tsv_finalize_device(uint64_t* d_acc, int64_t n, int32_t anchor_sink, void* stream,
                         tsv_outcome* out);
 
+/* Ascending indices of the nonzero words of acc[0..n) (the flagged list of
+ * finalize, sieve.cpp:136-159) into idx (capacity n), on all host threads.
+ * Returns the count. */
+int64_t tsv_nonzero_index(const uint64_t* acc, int64_t n, int32_t* idx);
+
 /* Per-kernel device-time profile (CUDA events on the launching stream).
  * names: "level", "level_first", "fixup", "readout", "zj" ... */
 int tsv_profile_enable(int on);

@@ -85,6 +85,8 @@ def lib():
                                          C.c_int32, C.c_uint64, C.c_uint64, vp, vp]
     L.tsv_xor_combine_device.argtypes = [vp, C.c_int, C.c_int64, vp, vp]
     L.tsv_finalize.argtypes = [C.c_int32, _u64p, C.c_int32, C.POINTER(Outcome)]
+    L.tsv_nonzero_index.restype = C.c_int64
+    L.tsv_nonzero_index.argtypes = [_u64p, C.c_int64, _i32p]
     L.tsv_finalize_device.argtypes = [vp, C.c_int64, C.c_int32, vp, C.POINTER(Outcome)]
     L.tsv_profile_enable.argtypes = [C.c_int]
     L.tsv_profile_get.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
@@ -143,6 +145,14 @@ def gf_mul_device(a, b, variant: int = 0):
     check(lib().tsv_gf_mul_device(variant, len(a), a if len(a) else out, b if len(b) else out,
                                   out))
     return out[:len(a)]
+
+
+def nonzero_index(acc) -> np.ndarray:
+    """Ascending indices of the nonzero words (multi-threaded, libtsv)."""
+    acc = np.ascontiguousarray(acc, dtype=np.uint64)
+    out = np.empty(max(len(acc), 1), np.int32)
+    c = lib().tsv_nonzero_index(acc if len(acc) else np.zeros(1, np.uint64), len(acc), out)
+    return out[:c]
 
 
 def finalize_device(d_acc_ptr: int, n: int, sink: int = -1, stream: int = 0):

@@ -1626,6 +1626,27 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
   });
 }
 
+int64_t tsv_nonzero_index(const uint64_t* acc, int64_t n, int32_t* idx) {
+  if (n <= 0 || !acc || !idx) return 0;
+  const int64_t block = int64_t{1} << 16;
+  const int64_t nb = (n + block - 1) / block;
+  std::vector<int64_t> cnt(static_cast<size_t>(nb) + 1, 0);
+#pragma omp parallel for schedule(static) if (n > (1 << 20))
+  for (int64_t b = 0; b < nb; ++b) {
+    int64_t c = 0;
+    for (int64_t x = b * block; x < std::min(n, (b + 1) * block); ++x) c += acc[x] != 0;
+    cnt[static_cast<size_t>(b) + 1] = c;
+  }
+  for (int64_t b = 0; b < nb; ++b) cnt[b + 1] += cnt[b];
+#pragma omp parallel for schedule(static) if (n > (1 << 20))
+  for (int64_t b = 0; b < nb; ++b) {
+    int64_t w = cnt[b];
+    for (int64_t x = b * block; x < std::min(n, (b + 1) * block); ++x)
+      if (acc[x]) idx[w++] = static_cast<int32_t>(x);
+  }
+  return cnt[nb];
+}
+
 int tsv_finalize_device(uint64_t* d_acc, int64_t n, int32_t anchor_sink, void* stream,
                         tsv_outcome* out) {
   return guard([&] {

@@ -159,7 +159,7 @@ def eval_temporal_sieve(g: TemporalGraph, k: int, max_ts: int, shades: ShadeAssi
     acc = acc[:n]
     res = SieveOutcome()
     res.accumulators = acc
-    res.flagged = np.nonzero(acc)[0].astype(np.int32)
+    res.flagged = _native.nonzero_index(acc)
     if config.localize:
         res.global_nonzero = len(res.flagged) > 0
     else:

@@ -142,3 +142,12 @@ def test_canonical_edges_carry_transition_times_like_reference():
         cu, cv, ct, ce = _native.canonical_edges_eps(n, u, v, ts, eps, directed)
         assert cu.tolist() == want["u"].tolist() and cv.tolist() == want["v"].tolist()
         assert ct.tolist() == want["ts"].tolist() and ce.tolist() == want["eps"].tolist()
+
+
+def test_nonzero_index_matches_numpy():
+    """tsv_nonzero_index (the flagged list on all host threads) == np.nonzero."""
+    from paper_2001_07158_b200 import _native
+    rng = np.random.default_rng(4)
+    for n, p in ((0, 0.5), (1, 1.0), (70_000, 0.3), (3_000_017, 0.9), (2_500_000, 0.0)):
+        a = (rng.random(n) < p).astype(np.uint64) * rng.integers(1, 2**63, n, dtype=np.uint64)
+        assert np.array_equal(_native.nonzero_index(a), np.nonzero(a)[0])
