@@ -395,7 +395,9 @@ def config_json(inst, world, args, cpu=False):
             "m": inst.m, "t": inst.t, "directed": inst.directed, "k_eff": k_eff,
             "sieve_points": 1 << k_eff, "repetitions": reps,
             "updates_per_step": inst.updates() * reps,
-            "parallelism": (f"repetitions / sieve points over {world} GPU(s) (shard.plan_units)"
+            "parallelism": (f"head-vertex partition of every evaluation over {world} GPU(s) "
+                            "(shard.vertex_partitioned_eval) when the vertex-lane engine applies, "
+                            "else repetitions / sieve points (shard.plan_units)"
                             if not cpu else
                             "reference CPU code on all host threads (rank 0)"),
             "l2": l2}
@@ -440,6 +442,11 @@ def main():
     ap.add_argument("--points-per-batch", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="-1 = per-config default")
+    ap.add_argument("--simulate-world", default="",
+                    help="comma-separated N: time each rank's share of the vertex-partitioned "
+                         "evaluation on this one GPU and project the N-GPU step (DESIGN.md 6)")
+    ap.add_argument("--nvlink-gbs", type=float, default=720.0,
+                    help="all-gather bandwidth per GPU assumed by the --simulate-world model")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent CUDA streams for the repetitions of a step "
                          "(at most one per work unit)")
@@ -487,6 +494,23 @@ def main():
                   "split_chunks": g.info.split_chunks, "device_bytes": g.info.device_bytes}
     acc = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
     total = torch.zeros((reps, n), dtype=torch.int64, device="cuda") if world > 1 else None
+    # N > 1 and a query the vertex-lane engine takes (k <= 5, every shaded
+    # vertex multi-shade, no hubs; C5): every repetition is split by head
+    # vertex over the ranks (shard.vertex_partitioned_eval), else the
+    # (repetition, point) units of plan_units
+    vertex_mode = False
+    if world > 1:
+        from paper_2001_07158_b200.shard import eval_vertex_partitioned_device
+        from paper_2001_07158_b200.sieve import vertex_partition
+        ok = torch.tensor([1 if vertex_partition(g, ds, k, rank, world).applicable else 0],
+                          device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        vertex_mode = bool(ok.item())
+    vbufs = None
+    if vertex_mode:
+        words = vertex_partition(g, ds, k, rank, world).state_words
+        vbufs = (torch.empty(words, dtype=torch.int64, device="cuda"),
+                 torch.empty(words, dtype=torch.int64, device="cuda"))
 
     # repetitions (independent evaluations) may run on concurrent streams so
     # one evaluation's tail wave overlaps the next one's launches
@@ -498,6 +522,11 @@ def main():
     def step(concurrent=True):
         l2_flush.zero_()
         acc.zero_()
+        if vertex_mode:
+            for r in range(reps):
+                total[r] = eval_vertex_partitioned_device(g, ds, k, g.t(), cfgs[r], anchor[0],
+                                                          acc[r], rank, world, bufs=vbufs)
+            return total
         if not side or not concurrent:
             for r, a, b in work:
                 T.eval_points_device(g, ds, k, g.t(), cfgs[r], anchor[0], a, b,
@@ -604,6 +633,45 @@ def main():
                 "launch_share_of_step": lvl_ms / max(all_ms, 1e-9),
                 "alg_bytes_per_launch": alg_bytes}
 
+    # --simulate-world: every rank's share of the vertex-partitioned
+    # evaluation timed on this GPU, the N-GPU step projected from it
+    simulated = None
+    if args.simulate_world and world == 1:
+        from paper_2001_07158_b200.shard import eval_vertex_simulated
+        simulated = {"model": ("per level: max over ranks of the rank's measured share + "
+                               "all-gather of the level's rows at --nvlink-gbs per GPU "
+                               "(modeled: one GPU here); + XOR combine of n words"),
+                     "nvlink_gbs": args.nvlink_gbs, "worlds": {}}
+        ref_acc = res[0].clone()
+        for N in (int(x) for x in args.simulate_world.split(",") if x):
+            a = torch.zeros(n, dtype=torch.int64, device="cuda")
+            try:
+                eval_vertex_simulated(g, ds, k, g.t(), cfgs[0], anchor[0], a, N)  # warm-up
+                a.zero_()
+                a, times, parts = eval_vertex_simulated(g, ds, k, g.t(), cfgs[0], anchor[0], a, N,
+                                                        timed=True)
+            except ValueError as e:
+                simulated["worlds"][str(N)] = {"unavailable": str(e)}
+                continue
+            if anchor[1] >= 0:
+                _native.finalize_device(a.data_ptr(), n, anchor[1], sp)
+            S = parts[0].slots
+            lv = {}
+            total_ms = 0.0
+            for level in range(2, k + 1):
+                per = [times[(level, q)] for q in range(N)]
+                xch = 0.0
+                if level < k and N > 1:
+                    xch = (N - 1) / N * S * parts[0].row_words[level] * 8 / (args.nvlink_gbs * 1e9) * 1e3
+                lv[str(level)] = {"rank_ms": per, "max_ms": max(per), "exchange_ms": xch}
+                total_ms += max(per) + xch
+            comb = 2 * (N - 1) / N * n * 8 / (args.nvlink_gbs * 1e9) * 1e3 if N > 1 else 0.0
+            total_ms += comb
+            simulated["worlds"][str(N)] = {
+                "levels": lv, "combine_ms": comb, "projected_ms_per_step": total_ms * reps,
+                "projected_value": upd_step / (total_ms * reps * 1e-3),
+                "parity_vs_n1": bool(torch.equal(a, ref_acc))}
+
     # the GPU's accumulators on the CPU sample's window (horizon max_ts on the
     # same graph), checked word for word against the CPU arm below
     gpu_window = None
@@ -621,7 +689,7 @@ def main():
     # accumulators back into a host buffer (tsv_eval_temporal_sieve).  The
     # timed graph is freed first so both fit in HBM.
     del ds, g
-    acc = total = None
+    acc = total = vbufs = None
     torch.cuda.synchronize()
     e2e = None
     e2e_parity = None
@@ -658,10 +726,15 @@ def main():
                 g2 = T.TemporalGraph(h, info)
                 ds2 = T.DeviceShades(g2, k, sh)
                 a2 = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
-                for r, a, b in work:
-                    T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], a, b,
-                                         a2[r].data_ptr(), sp)
-                a2 = xor_allreduce(a2)
+                if vertex_mode:
+                    for r in range(reps):
+                        a2[r] = eval_vertex_partitioned_device(g2, ds2, k, g2.t(), cfgs[r],
+                                                               anchor[0], a2[r], rank, world)
+                else:
+                    for r, a, b in work:
+                        T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], a, b,
+                                             a2[r].data_ptr(), sp)
+                    a2 = xor_allreduce(a2)
                 host_acc[:] = a2.cpu().numpy().view(np.uint64)
                 del ds2, g2
                 h = None
@@ -715,6 +788,7 @@ def main():
                 "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
                 "vs_baseline": None, "dtype": "u64", "data": "synthetic",
                 "config": config_json(inst, world, args), "parity": parity,
+                "simulated_world": simulated,
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "host_enqueue_ms_per_step": host_ms,
                 "clocks": clk.summary(), "decision": decisions, "checksums": checksums,

@@ -205,6 +205,34 @@ int tsv_finalize(int32_t n, uint64_t* acc, int32_t anchor_sink,
 int tsv_finalize_device(uint64_t* d_acc, int64_t n, int32_t anchor_sink, void* stream,
                         tsv_outcome* out);
 
+/* ---- Vertex-partitioned evaluation (multi-GPU) ----
+ * One full evaluation (all 2^k points, coefficient form) split by HEAD
+ * VERTEX: rank r of `world` owns the vertices [n r/world, n (r+1)/world)
+ * and computes their state rows level by level (vertex-lane engine,
+ * coef_vertex.cu: every shaded vertex multi-shade, k <= 5, no hubs).
+ * Between levels the caller makes every rank's rows visible to all ranks:
+ * rows of level l live at [slot_lo, slot_hi) x row_words[l] in each rank's
+ * full-size state buffer (an all-gather of those ranges; shard.py).  At
+ * level k every rank XORs the readout of its own vertices into d_acc. */
+typedef struct {
+  int32_t applicable;        /* 0: hub vertices or k out of range: use point sharding */
+  int32_t pad;
+  int64_t slot_lo, slot_hi;  /* this rank's state rows */
+  int64_t slots;             /* all state rows */
+  int64_t state_words;       /* words of each of the two state buffers */
+  int32_t row_words[32];     /* row stride of level l: C(k, l) */
+} tsv_partition;
+
+int tsv_vertex_partition(const tsv_graph* g, const tsv_shades* s, int k, int rank,
+                         int world, tsv_partition* out);
+/* Level `level` (2..k) of rank's share: reads level-1 rows from d_prev
+ * (unused at level 2), writes its level rows into d_cur (level < k) or XORs
+ * its vertices' readout into d_acc (level k).  Asynchronous on `stream`. */
+int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int level,
+                          int32_t max_ts, const tsv_config* cfg, int32_t anchor_source,
+                          int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
+                          uint64_t* d_acc, void* stream);
+
 /* Ascending indices of the nonzero words of acc[0..n) (the flagged list of
  * finalize, sieve.cpp:136-159) into idx (capacity n), on all host threads.
  * Returns the count. */

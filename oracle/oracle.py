@@ -73,6 +73,13 @@ def oracle_lib():
         lib.tsvo_big_eval.restype = C.c_int
         lib.tsvo_big_eval.argtypes = [C.c_void_p, C.c_int, _i32p, _i32p, C.c_uint64, C.c_int32,
                                       C.c_uint64, C.c_uint64, C.c_int, _u64p]
+        lib.tsvo_big_level.restype = C.c_int
+        lib.tsvo_big_level.argtypes = [C.c_void_p, C.c_int, C.c_int, _i32p, _i32p, C.c_uint64,
+                                       C.c_int32, C.c_uint64, C.c_int, C.c_int64, C.c_int64,
+                                       C.c_void_p, C.c_void_p, _u64p]
+        lib.tsvo_big_run_range.restype = None
+        lib.tsvo_big_run_range.argtypes = [C.c_void_p, C.c_int64, C.c_int64,
+                                           C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         lib.tsvo_set_threads.restype = None
         lib.tsvo_set_threads.argtypes = [C.c_int]
         lib.tsvo_max_threads.restype = C.c_int
@@ -219,6 +226,23 @@ class BigGraph:
         if rc != 0:
             raise ValueError("k out of range [1,30] or bad lane count")
         return acc[:self.n]
+
+    def run_range(self, v_lo, v_hi):
+        """Run-state indices [r_lo, r_hi) of the heads [v_lo, v_hi)."""
+        a, b = C.c_int64(0), C.c_int64(0)
+        oracle_lib().tsvo_big_run_range(self.h, int(v_lo), int(v_hi), C.byref(a), C.byref(b))
+        return a.value, b.value
+
+    def level(self, k, ell, vertex_off, vertex_shades, seed, anchor_source, p_begin, lanes,
+              v_lo, v_hi, prev, cur, acc):
+        """Level ell for heads [v_lo, v_hi), points [p_begin, p_begin+lanes):
+        prev/cur are uint64 run-state arrays (runs x lanes), acc n words."""
+        vs = _a32(vertex_shades) if len(vertex_shades) else np.zeros(1, np.int32)
+        rc = oracle_lib().tsvo_big_level(self.h, k, ell, _a32(vertex_off), vs, seed,
+                                         anchor_source, p_begin, lanes, int(v_lo), int(v_hi),
+                                         prev.ctypes.data, cur.ctypes.data, acc)
+        if rc != 0:
+            raise ValueError("bad level arguments")
 
     def close(self):
         if self.h:

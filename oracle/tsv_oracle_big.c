@@ -262,6 +262,114 @@ int64_t tsvo_big_runs(const void *p) { return ((const tsvo_big *)p)->nr; }
 #define MAXW 16
 
 /*
+ * One level ell (2..k) of the DP for the heads in [v_lo, v_hi): reads the
+ * level ell-1 run states `prev` (z at level 2), writes the level ell run
+ * states of these heads into `cur` (ell < k) or XORs their readout into acc
+ * (ell == k).  Heads are independent within a level (sieve.cpp:215-256).
+ */
+static void big_level(const tsvo_big *G, int ell, int k, const uint64_t *z, int W, int wn,
+                      uint64_t seed, int32_t anchor_source, int64_t v_lo, int64_t v_hi,
+                      const uint64_t *prev, uint64_t *cur, uint64_t *acc) {
+  const int last = ell == k;
+#pragma omp parallel for schedule(dynamic, 256)
+  for (int64_t h = v_lo; h < v_hi; ++h) {
+    int64_t a = G->hoff[h], ae = G->hoff[h + 1];
+    if (a == ae) continue;
+    uint64_t pfx[MAXW], tmp[MAXW];
+    const uint64_t *zh = z + h * W;
+    for (int w = 0; w < W; ++w) pfx[w] = 0;
+    int64_t r = G->roff[h];
+    while (a < ae) {
+      int32_t t = G->a_ts[a];
+      for (int w = 0; w < W; ++w) tmp[w] = 0;
+      for (; a < ae && G->a_ts[a] == t; ++a) {
+        if (ell > 2 && a + 16 < ae && G->a_src[a + 16] != NONE)
+          __builtin_prefetch(prev + (int64_t)G->a_src[a + 16] * W);
+        const uint64_t *src;
+        if (ell == 2) {
+          if (anchor_source >= 0 && G->a_tail[a] != anchor_source) continue;
+          src = z + (int64_t)G->a_tail[a] * W;
+        } else {
+          if (G->a_src[a] == NONE) continue;
+          src = prev + (int64_t)G->a_src[a] * W;
+        }
+        uint64_t y = draw_nonzero(seed, ROLE_EDGE_Y, (uint64_t)G->a_eid[a], (uint64_t)(ell - 1), 0);
+        for (int w = 0; w < wn; ++w) tmp[w] ^= gf_mul(y, src[w]);
+      }
+      for (int w = 0; w < wn; ++w) pfx[w] ^= gf_mul(zh[w], tmp[w]);
+      if (!last)
+        for (int w = 0; w < W; ++w) cur[r * W + w] = pfx[w];
+      ++r;
+    }
+    if (last) {
+      uint64_t s = 0;
+      for (int w = 0; w < wn; ++w) s ^= pfx[w];
+      acc[h] ^= s;
+    }
+  }
+}
+
+/* zj (n x k, sieve.cpp:83-101) and z_u^A for points [base, base+wn), W lanes */
+static void big_z(const tsvo_big *G, int k, const int32_t *vertex_off,
+                  const int32_t *vertex_shades, uint64_t seed, uint64_t base, int W, int wn,
+                  uint64_t *zj, uint64_t *z) {
+  const int64_t n = G->n;
+  uint64_t wtab[30 * 30];
+  for (int d = 1; d <= k; ++d)
+    for (int j = 1; j <= k; ++j)
+      wtab[(d - 1) * k + (j - 1)] = draw_nonzero(seed, ROLE_SHADE_W, (uint64_t)d, (uint64_t)j, 0);
+  memset(zj, 0, sizeof(uint64_t) * (size_t)n * (size_t)k);
+#pragma omp parallel for schedule(dynamic, 4096)
+  for (int64_t x = 0; x < n; ++x)
+    for (int32_t s = vertex_off[x]; s < vertex_off[x + 1]; ++s) {
+      int d = vertex_shades[s];
+      uint64_t vv = draw_nonzero(seed, ROLE_SHADE_V, (uint64_t)x, (uint64_t)d, 0);
+      for (int j = 0; j < k; ++j) zj[x * k + j] ^= gf_mul(vv, wtab[(d - 1) * k + j]);
+    }
+#pragma omp parallel for schedule(static)
+  for (int64_t x = 0; x < n; ++x)
+    for (int w = 0; w < W; ++w) {
+      uint64_t s = 0, A = base + (uint64_t)w;
+      if (w < wn)
+        for (int j = 0; j < k; ++j)
+          if ((A >> j) & 1) s ^= zj[x * k + j];
+      z[x * W + w] = s;
+    }
+}
+
+/*
+ * The vertex-partitioned form (the multi-GPU algorithm of DESIGN.md section
+ * 6, restated point by point): level ell for the heads [v_lo, v_hi) and the
+ * points [p_begin, p_begin + lanes); run states are `lanes` words per run.
+ * tsvo_big_run_range gives the run-state range a head range writes.
+ */
+int tsvo_big_level(const void *p, int k, int ell, const int32_t *vertex_off,
+                   const int32_t *vertex_shades, uint64_t seed, int32_t anchor_source,
+                   uint64_t p_begin, int lanes, int64_t v_lo, int64_t v_hi,
+                   const uint64_t *prev, uint64_t *cur, uint64_t *acc) {
+  const tsvo_big *G = p;
+  if (k < 2 || k > 30 || ell < 2 || ell > k || lanes < 1 || lanes > MAXW) return -1;
+  uint64_t *zj = malloc(sizeof(uint64_t) * ((size_t)G->n * (size_t)k + 1));
+  uint64_t *z = malloc(sizeof(uint64_t) * ((size_t)G->n * lanes + 1));
+  if (!zj || !z) {
+    free(zj);
+    free(z);
+    return -3;
+  }
+  big_z(G, k, vertex_off, vertex_shades, seed, p_begin, lanes, lanes, zj, z);
+  big_level(G, ell, k, z, lanes, lanes, seed, anchor_source, v_lo, v_hi, prev, cur, acc);
+  free(zj);
+  free(z);
+  return 0;
+}
+
+void tsvo_big_run_range(const void *p, int64_t v_lo, int64_t v_hi, int64_t *r_lo, int64_t *r_hi) {
+  const tsvo_big *G = p;
+  *r_lo = G->roff[v_lo];
+  *r_hi = G->roff[v_hi];
+}
+
+/*
  * XOR the sieve points [p_begin, p_end) into acc[0..n) (not cleared), `lanes`
  * points per pass (1..16).  Same contract as tsvo_eval_points.  Returns 0, or
  * -1 for k out of range / bad lanes, -3 when memory is short.
@@ -322,44 +430,7 @@ int tsvo_big_eval(const void *p, int k, const int32_t *vertex_off,
     }
     uint64_t *prev = S0, *cur = S1;
     for (int ell = 2; ell <= k; ++ell) {
-      const int last = ell == k;
-#pragma omp parallel for schedule(dynamic, 256)
-      for (int64_t h = 0; h < n; ++h) {
-        int64_t a = G->hoff[h], ae = G->hoff[h + 1];
-        if (a == ae) continue;
-        uint64_t pfx[MAXW], tmp[MAXW];
-        const uint64_t *zh = z + h * W;
-        for (int w = 0; w < W; ++w) pfx[w] = 0;
-        int64_t r = G->roff[h];
-        while (a < ae) {
-          int32_t t = G->a_ts[a];
-          for (int w = 0; w < W; ++w) tmp[w] = 0;
-          for (; a < ae && G->a_ts[a] == t; ++a) {
-            if (ell > 2 && a + 16 < ae && G->a_src[a + 16] != NONE)
-              __builtin_prefetch(prev + (int64_t)G->a_src[a + 16] * W);
-            const uint64_t *src;
-            if (ell == 2) {
-              if (anchor_source >= 0 && G->a_tail[a] != anchor_source) continue;
-              src = z + (int64_t)G->a_tail[a] * W;
-            } else {
-              if (G->a_src[a] == NONE) continue;
-              src = prev + (int64_t)G->a_src[a] * W;
-            }
-            uint64_t y = draw_nonzero(seed, ROLE_EDGE_Y, (uint64_t)G->a_eid[a],
-                                           (uint64_t)(ell - 1), 0);
-            for (int w = 0; w < wn; ++w) tmp[w] ^= gf_mul(y, src[w]);
-          }
-          for (int w = 0; w < wn; ++w) pfx[w] ^= gf_mul(zh[w], tmp[w]);
-          if (!last)
-            for (int w = 0; w < W; ++w) cur[r * W + w] = pfx[w];
-          ++r;
-        }
-        if (last) {
-          uint64_t s = 0;
-          for (int w = 0; w < wn; ++w) s ^= pfx[w];
-          acc[h] ^= s;
-        }
-      }
+      big_level(G, ell, k, z, W, wn, seed, anchor_source, 0, n, prev, cur, acc);
       uint64_t *sw = prev;
       prev = cur;
       cur = sw;

@@ -35,6 +35,12 @@ class Config(C.Structure):
                 ("memory_cap_words", C.c_uint64)]
 
 
+class Partition(C.Structure):
+    _fields_ = [("applicable", C.c_int32), ("pad", C.c_int32), ("slot_lo", C.c_int64),
+                ("slot_hi", C.c_int64), ("slots", C.c_int64), ("state_words", C.c_int64),
+                ("row_words", C.c_int32 * 32)]
+
+
 class Outcome(C.Structure):
     _fields_ = [("global_nonzero", C.c_int32), ("pad", C.c_int32), ("flagged", C.c_int64),
                 ("checksum", C.c_uint64), ("peak_field_words", C.c_uint64),
@@ -85,6 +91,9 @@ def lib():
                                          C.c_int32, C.c_uint64, C.c_uint64, vp, vp]
     L.tsv_xor_combine_device.argtypes = [vp, C.c_int, C.c_int64, vp, vp]
     L.tsv_finalize.argtypes = [C.c_int32, _u64p, C.c_int32, C.POINTER(Outcome)]
+    L.tsv_vertex_partition.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(Partition)]
+    L.tsv_eval_vertex_level.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int32, C.POINTER(Config),
+                                        C.c_int32, C.c_int, C.c_int, vp, vp, vp, vp]
     L.tsv_nonzero_index.restype = C.c_int64
     L.tsv_nonzero_index.argtypes = [_u64p, C.c_int64, _i32p]
     L.tsv_finalize_device.argtypes = [vp, C.c_int64, C.c_int32, vp, C.POINTER(Outcome)]

@@ -107,9 +107,15 @@ struct VertList {
   int32_t* count = nullptr;  // its arcs
 };
 bool vertex_engine_supports(int k);
+// The list of the vertices in [v_lo, v_hi) (v_hi < 0: all).
 void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
                        const std::function<void*(size_t)>& alloc,
-                       const std::function<void(void*)>& release);
+                       const std::function<void(void*)>& release, int32_t v_lo = 0,
+                       int32_t v_hi = -1);
+// State slots of the runs before run r (= the first slot of runs >= r).
+int64_t count_slots_before(const DevGraph& g, int64_t r, cudaStream_t st,
+                           const std::function<void*(size_t)>& alloc,
+                           const std::function<void(void*)>& release);
 // One level l of the vertex-lane engine: S_l rows (stride C(k, l)) at the
 // referenced slots into p.ubuf from p.s_prev (stride C(k, l-1)) or zj (l = 2);
 // at l = k the readout acc[h] ^= det * ... (no ulast).

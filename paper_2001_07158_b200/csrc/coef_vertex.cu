@@ -307,23 +307,60 @@ __global__ void k_has_runs(int32_t n, const int32_t* __restrict__ vro, uint8_t* 
   if (x < n) f[x] = vro[x + 1] > vro[x] ? 1 : 0;
 }
 
-__global__ void k_counts(int64_t nv, int64_t A, const int64_t* __restrict__ start,
-                         int32_t* __restrict__ cnt, int32_t* __restrict__ pos) {
+// list entries i0 .. i0+nv of the nvall vertex starts
+__global__ void k_counts(int64_t nv, int64_t i0, int64_t nvall, int64_t A,
+                         const int64_t* __restrict__ start, int32_t* __restrict__ cnt,
+                         int32_t* __restrict__ pos) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nv) return;
-  cnt[i] = static_cast<int32_t>((i + 1 < nv ? start[i + 1] : A) - start[i]);
+  const int64_t g = i0 + i;
+  cnt[i] = static_cast<int32_t>((g + 1 < nvall ? start[g + 1] : A) - start[g]);
   pos[i] = static_cast<int32_t>(i);
 }
 
-__global__ void k_gather_start(int64_t nv, const int32_t* __restrict__ perm,
+__global__ void k_gather_start(int64_t nv, int64_t i0, const int32_t* __restrict__ perm,
                                const int64_t* __restrict__ start,
                                const int32_t* __restrict__ head_in, int64_t* __restrict__ s_out,
                                int32_t* __restrict__ h_out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= nv) return;
-  const int32_t p = perm[i];
+  const int64_t p = i0 + perm[i];
   s_out[i] = start[p];
   h_out[i] = head_in[p];
+}
+
+// [lower_bound(heads, lo), lower_bound(heads, hi)) of the increasing list
+__global__ void k_list_range(const int32_t* __restrict__ heads, int64_t nv, int32_t lo,
+                             int32_t hi, int64_t* __restrict__ out) {
+  for (int w = 0; w < 2; ++w) {
+    const int32_t key = w ? hi : lo;
+    int64_t a = 0, b = nv;
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (heads[mid] < key) a = mid + 1;
+      else b = mid;
+    }
+    out[w] = a;
+  }
+}
+
+// referenced runs (state slots) among runs [0, r): slots are assigned in
+// run order, so this is the first slot of the runs from r on
+__global__ void k_count_slots(const int32_t* __restrict__ run_slot, int64_t r,
+                              unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long part[8];
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < r;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += run_slot[i] >= 0;
+  for (int d = 16; d; d >>= 1) c += __shfl_down_sync(0xffffffffu, c, d);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+    atomicAdd(out, s);
+  }
 }
 
 inline unsigned nblk_v(int64_t n) { return static_cast<unsigned>((n + 255) / 256); }
@@ -334,11 +371,12 @@ bool vertex_engine_supports(int k) { return k >= 2 && k <= kVertexMaxK; }
 
 void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
                        const std::function<void*(size_t)>& alloc,
-                       const std::function<void(void*)>& release) {
+                       const std::function<void(void*)>& release, int32_t v_lo, int32_t v_hi) {
   const int64_t A = g.A;
   const int32_t n = g.n;
   out = VertList{};
-  if (A == 0 || n == 0) return;
+  if (v_hi < 0) v_hi = n;
+  if (A == 0 || n == 0 || v_lo >= v_hi) return;
   auto ck = [](cudaError_t e) {
     if (e != cudaSuccess)
       throw std::runtime_error(std::string("vertex list: ") + cudaGetErrorString(e));
@@ -372,12 +410,27 @@ void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
   release(t);
   release(hf);
   release(cnt32);
+  // the vertices of [v_lo, v_hi): a contiguous range [i0, i1) of the list
+  int64_t* rng = static_cast<int64_t*>(alloc(16));
+  k_list_range<<<1, 1, 0, st>>>(heads, nv, v_lo, v_hi, rng);
+  int64_t hr[2] = {0, 0};
+  ck(cudaMemcpyAsync(hr, rng, 16, cudaMemcpyDeviceToHost, st));
+  ck(cudaStreamSynchronize(st));
+  release(rng);
+  const int64_t i0 = hr[0];
+  const int64_t nvall = nv;
+  nv = hr[1] - hr[0];
+  if (nv <= 0) {
+    release(vs);
+    release(heads);
+    return;
+  }
   // arc counts; sort by count (descending), carrying the list position
   int32_t* counts = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
   int32_t* pos = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
   int32_t* counts_s = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
   int32_t* pos_s = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
-  k_counts<<<nblk_v(nv), 256, 0, st>>>(nv, A, vs, counts, pos);
+  k_counts<<<nblk_v(nv), 256, 0, st>>>(nv, i0, nvall, A, vs, counts, pos);
   tmp = 0;
   ck(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, counts, counts_s, pos, pos_s,
                                                static_cast<int>(nv), 0, 32, st));
@@ -389,7 +442,7 @@ void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
   release(pos);
   int64_t* start_s = static_cast<int64_t*>(alloc(static_cast<size_t>(nv) * 8 + 8));
   int32_t* head_s = static_cast<int32_t*>(alloc(static_cast<size_t>(nv) * 4 + 4));
-  k_gather_start<<<nblk_v(nv), 256, 0, st>>>(nv, pos_s, vs, heads, start_s, head_s);
+  k_gather_start<<<nblk_v(nv), 256, 0, st>>>(nv, i0, pos_s, vs, heads, start_s, head_s);
   ck(cudaGetLastError());
   ck(cudaStreamSynchronize(st));
   release(pos_s);
@@ -399,6 +452,20 @@ void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
   out.head = head_s;
   out.start = start_s;
   out.count = counts_s;
+}
+
+int64_t count_slots_before(const DevGraph& g, int64_t r, cudaStream_t st,
+                           const std::function<void*(size_t)>& alloc,
+                           const std::function<void(void*)>& release) {
+  if (r <= 0) return 0;
+  auto* d = static_cast<unsigned long long*>(alloc(8));
+  cudaMemsetAsync(d, 0, 8, st);
+  k_count_slots<<<148 * 4, 256, 0, st>>>(g.run_slot, r, d);
+  unsigned long long h = 0;
+  cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, st);
+  cudaStreamSynchronize(st);
+  release(d);
+  return static_cast<int64_t>(h);
 }
 
 void launch_coef_vertex(const CoefParams& p, const VertList& vl, uint64_t det, uint64_t* acc,

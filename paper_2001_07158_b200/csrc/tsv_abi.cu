@@ -190,10 +190,20 @@ struct tsv_shades {
   };
   mutable std::mutex sub_mu;
   mutable std::vector<SubEntry> subs;
+  // the n x k table v_{u,d} of the shade basis per seed, with det(W), for the
+  // level-by-level (multi-GPU) entry point
+  struct ZjEntry {
+    uint64_t seed;
+    uint64_t* d;
+    uint64_t det;
+  };
+  mutable std::mutex zj_mu;
+  mutable std::vector<ZjEntry> zjs;
   ~tsv_shades() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
+    for (auto& z : zjs) cudaFree(z.d);
     cudaFree(off);
     cudaFree(shades);
     cudaSetDevice(prev);
@@ -225,18 +235,26 @@ struct tsv_graph {
   // stream of the synchronous entry points (created once per graph)
   mutable std::mutex stream_mu;
   mutable cudaStream_t api_stream = nullptr;
-  // work list of the vertex-lane coefficient engine (coef_vertex.cu), built
-  // on first use: 0 not built, 1 built, 2 not applicable (hub vertices)
+  // vertex-lane coefficient engine (coef_vertex.cu): per (rank, world)
+  // partition -- its work list and state-slot range -- built on first use;
+  // applicable = false when the graph has hub vertices
+  struct VertPart {
+    int rank = 0, world = 1;
+    bool applicable = false;
+    tsv::VertList vl;
+    int32_t v_lo = 0, v_hi = 0;
+    int64_t slot_lo = 0, slot_hi = 0;
+    std::vector<void*> owned;
+  };
   mutable std::mutex vl_mu;
-  mutable int vl_state = 0;
-  mutable tsv::VertList vl;
-  mutable std::vector<void*> vl_owned;
+  mutable std::vector<std::unique_ptr<VertPart>> parts;
   ~tsv_graph() {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
     if (api_stream) cudaStreamDestroy(api_stream);
-    for (void* p : vl_owned) cudaFree(p);
+    for (auto& vp : parts)
+      for (void* p : vp->owned) cudaFree(p);
     for (void* p : owned) cudaFree(p);
     cudaSetDevice(prev);
   }
@@ -459,13 +477,21 @@ const CoefConst& coef_const(int dev, int k, bool items) {
 // arcs serially, so power-law hubs go to the arc-parallel kernels.
 constexpr int32_t kVertexMaxArcs = 4096;
 
-// The vertex-lane work list of g (built once, on `st`), or nullptr when the
-// graph has hub vertices.
-const tsv::VertList* vertex_list(const tsv_graph* g, cudaStream_t st) {
+// The vertex-lane partition `rank` of `world` of g (built once, on `st`):
+// the vertices [n*rank/world, n*(rank+1)/world), their work list and state
+// slots.  applicable = false when the graph has hub vertices.
+const tsv_graph::VertPart& vertex_part(const tsv_graph* g, int rank, int world,
+                                       cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g->vl_mu);
-  if (g->vl_state == 1) return &g->vl;
-  if (g->vl_state == 2) return nullptr;
-  std::vector<void*> live;
+  for (auto& vp : g->parts)
+    if (vp->rank == rank && vp->world == world) return *vp;
+  auto vp = std::make_unique<tsv_graph::VertPart>();
+  vp->rank = rank;
+  vp->world = world;
+  const int64_t n = g->dev.n;
+  vp->v_lo = static_cast<int32_t>(n * rank / world);
+  vp->v_hi = static_cast<int32_t>(n * (rank + 1) / world);
+  std::vector<void*>& live = vp->owned;
   auto alloc = [&](size_t bytes) -> void* {
     void* p = nullptr;
     if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
@@ -478,27 +504,36 @@ const tsv::VertList* vertex_list(const tsv_graph* g, cudaStream_t st) {
     if (it != live.end()) live.erase(it);
     cudaFreeAsync(p, st);
   };
-  tsv::VertList vl;
   try {
-    tsv::build_vertex_list(g->dev, vl, st, alloc, release);
+    tsv::build_vertex_list(g->dev, vp->vl, st, alloc, release, vp->v_lo, vp->v_hi);
+    int32_t maxc = 0;
+    if (vp->vl.nv) {
+      TSV_CUDA(cudaMemcpyAsync(&maxc, vp->vl.count, 4, cudaMemcpyDeviceToHost, st));
+      TSV_CUDA(cudaStreamSynchronize(st));
+    }
+    // the largest in-degree of the whole graph decides applicability (every
+    // rank of a world must agree): the full list is partition (0, 1)
+    vp->applicable = maxc <= kVertexMaxArcs;
+    int32_t r0 = 0, r1 = 0;
+    TSV_CUDA(cudaMemcpyAsync(&r0, g->dev.vtx_run_off + vp->v_lo, 4, cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaMemcpyAsync(&r1, g->dev.vtx_run_off + vp->v_hi, 4, cudaMemcpyDeviceToHost, st));
+    TSV_CUDA(cudaStreamSynchronize(st));
+    vp->slot_lo = tsv::count_slots_before(g->dev, r0, st, alloc, release);
+    vp->slot_hi = tsv::count_slots_before(g->dev, r1, st, alloc, release);
   } catch (...) {
     for (void* p : live) cudaFreeAsync(p, st);
+    live.clear();
     throw;
   }
-  int32_t maxc = 0;
-  if (vl.nv) {
-    TSV_CUDA(cudaMemcpyAsync(&maxc, vl.count, 4, cudaMemcpyDeviceToHost, st));
-    TSV_CUDA(cudaStreamSynchronize(st));
-  }
-  if (maxc > kVertexMaxArcs) {
-    for (void* p : live) cudaFreeAsync(p, st);
-    g->vl_state = 2;
-    return nullptr;
-  }
-  g->vl = vl;
-  g->vl_owned = live;
-  g->vl_state = 1;
-  return &g->vl;
+  g->parts.push_back(std::move(vp));
+  return *g->parts.back();
+}
+
+// Largest in-degree the vertex-lane engine takes: a lane walks its vertex's
+// arcs serially, so power-law hubs go to the arc-parallel kernels.
+bool vertex_applicable(const tsv_graph* g, cudaStream_t st) {
+  if (!vertex_part(g, 0, 1, st).applicable) return false;
+  return true;
 }
 
 // The coefficient (top-degree) engine, coef_kernels.cu: the XOR over ALL
@@ -592,7 +627,8 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const char* vx_env = std::getenv("TSV_VERTEX");
   const bool try_vertex = !vc && sh->single == 0 && tsv::vertex_engine_supports(k) &&
                           !(vx_env && vx_env[0] == '0');
-  if (const tsv::VertList* vl = try_vertex ? vertex_list(g, st) : nullptr) {
+  if (try_vertex && vertex_applicable(g, st)) {
+    const tsv::VertList* vl = &vertex_part(g, 0, 1, st).vl;
     uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
     for (int l = 2; l <= k; ++l) {
       tsv::CoefParams cp;
@@ -1623,6 +1659,94 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     out->checksum = checksum;
     out->fn_bound = (2.0 * k - 1.0) / std::pow(2.0, 64);
     out->peak_field_words = peak;
+  });
+}
+
+int tsv_vertex_partition(const tsv_graph* g, const tsv_shades* s, int k, int rank,
+                         int world, tsv_partition* out) {
+  return guard([&] {
+    if (!g || !s || !out) throw std::invalid_argument("null argument");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank/world");
+    if (s->n != g->dev.n || s->k != k) throw std::invalid_argument("shade assignment built for a different graph");
+    std::memset(out, 0, sizeof(*out));
+    if (!tsv::vertex_engine_supports(k) || g->model != 0) return;
+    DeviceGuard dg(g->device);
+    cudaStream_t st = nullptr;
+    TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct Del {
+      cudaStream_t s;
+      ~Del() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    } del{st};
+    const tsv_graph::VertPart& vp = vertex_part(g, rank, world, st);
+    const tsv::CoefTables& T = coef_const_tables(k);
+    int64_t M = 1;
+    for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, T.count[l]);
+    out->applicable = vp.applicable && s->single == 0 ? 1 : 0;
+    out->slot_lo = vp.slot_lo;
+    out->slot_hi = vp.slot_hi;
+    out->slots = g->dev.S;
+    out->state_words = std::max<int64_t>(g->dev.S, 1) * M;
+    for (int l = 0; l <= k && l < 32; ++l) out->row_words[l] = static_cast<int32_t>(T.count[l]);
+  });
+}
+
+int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int level,
+                          int32_t max_ts, const tsv_config* cfg, int32_t anchor_source,
+                          int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
+                          uint64_t* d_acc, void* stream) {
+  return guard([&] {
+    if (!g || !s || !d_acc) throw std::invalid_argument("null argument");
+    check_config(cfg);
+    if (!tsv::vertex_engine_supports(k) || level < 2 || level > k)
+      throw std::invalid_argument("vertex-partitioned level: k must be 2..5, level 2..k");
+    if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
+    if (s->n != g->dev.n || s->k != k || s->device != g->device)
+      throw std::invalid_argument("shade assignment built for a different graph");
+    if (g->model != 0) throw std::invalid_argument("vertex-partitioned level: instant model only");
+    DeviceGuard dg(g->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const tsv_graph::VertPart& vp = vertex_part(g, rank, world, st);
+    if (!vp.applicable) throw std::invalid_argument("vertex partition not applicable (hub vertices)");
+    // v_{u,d} table and det(W) of this seed (cached with the shades)
+    uint64_t* zj = nullptr;
+    uint64_t det = 1;
+    {
+      std::lock_guard<std::mutex> lk(s->zj_mu);
+      for (auto& z : s->zjs)
+        if (z.seed == cfg->seed) zj = z.d, det = z.det;
+      if (!zj) {
+        TSV_CUDA(cudaMalloc(&zj, static_cast<size_t>(std::max<int32_t>(g->dev.n, 1)) * k * 8));
+        tsv::launch_zj_ident(g->dev.n, k, cfg->seed, s->off, s->shades, zj, st);
+        std::vector<uint64_t> W(static_cast<size_t>(k) * k);
+        const uint64_t pre = tsv::draw_prefix(cfg->seed, tsv::kRoleShadeW);
+        for (int d = 0; d < k; ++d)
+          for (int j = 0; j < k; ++j)
+            W[static_cast<size_t>(d) * k + j] = tsv::draw_nonzero_from(pre, d + 1, j + 1, 0);
+        det = tsv::gf_det_host(W.data(), k);
+        TSV_CUDA(cudaStreamSynchronize(st));
+        if (s->zjs.size() >= 4) {
+          cudaFree(s->zjs.front().d);
+          s->zjs.erase(s->zjs.begin());
+        }
+        s->zjs.push_back({cfg->seed, zj, det});
+      }
+    }
+    tsv::CoefParams cp;
+    cp.g = g->dev;
+    cp.zj = zj;
+    cp.k = k;
+    cp.ell = level;
+    cp.last = level == k;
+    cp.seed = cfg->seed;
+    cp.anchor_source = anchor_source;
+    cp.s_prev = d_prev;
+    cp.ubuf = d_cur;
+    cp.max_ts = max_ts;
+    tsv::launch_coef_vertex(cp, vp.vl, det, d_acc, st);
+    TSV_CUDA(cudaGetLastError());
   });
 }
 

@@ -104,3 +104,96 @@ def xor_allreduce(t, group=None, out=None):
         out.copy_(res)
         return out
     return res
+
+
+def vertex_partitioned_eval(level_fn, k, ranges, prev, cur, acc, group=None):
+    """One evaluation split by HEAD VERTEX across the ranks:
+    the multi-GPU form of the coefficient engine.
+
+    Rank r owns the heads [n r/N, n (r+1)/N).  Level l of the sieve needs
+    the level l-1 state rows of every tail, so after each level the ranks'
+    rows are made visible to all: `ranges(l)` gives, per rank, the element
+    range of `cur` holding its level-l rows (contiguous: state rows are in
+    vertex-major run order), and every range is broadcast from its owner
+    (an all-gather, in place, into the full-size buffers every rank holds).
+    `level_fn(l, prev, cur, acc)` computes this rank's share of level l;
+    at l = k it XORs its vertices' readout into acc, which the ranks
+    XOR-combine at the end (each vertex's word comes from its owner)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    for level in range(2, k + 1):
+        level_fn(level, prev, cur, acc)
+        if level < k and world > 1:
+            works = []
+            for q, (lo, hi) in enumerate(ranges(level)):
+                if hi > lo:
+                    src = dist.get_global_rank(group, q) if group is not None else q
+                    works.append(dist.broadcast(cur[lo:hi], src=src, group=group, async_op=True))
+            for w in works:
+                w.wait()
+        prev, cur = cur, prev
+    return xor_allreduce(acc, group) if world > 1 else acc
+
+
+def eval_vertex_partitioned_device(g, ds, k, max_ts, cfg, anchor_source, acc, rank, world,
+                                   group=None, bufs=None, stream=None):
+    """vertex_partitioned_eval with the device engine (tsv_eval_vertex_level)
+    on this rank's GPU; acc: int64 CUDA tensor of n words (XORed into)."""
+    import torch
+    from .sieve import eval_vertex_level, vertex_partition
+    parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
+    if not all(p.applicable for p in parts):
+        raise ValueError("vertex partition not applicable")
+    words = parts[0].state_words
+    if bufs is None:
+        bufs = (torch.empty(words, dtype=torch.int64, device=acc.device),
+                torch.empty(words, dtype=torch.int64, device=acc.device))
+    sp = (stream or torch.cuda.current_stream(acc.device)).cuda_stream
+
+    def level_fn(level, prev, cur, a):
+        eval_vertex_level(g, ds, k, level, max_ts, cfg, anchor_source, rank, world,
+                          prev.data_ptr(), cur.data_ptr(), a.data_ptr(), sp)
+
+    def ranges(level):
+        rw = parts[0].row_words[level]
+        return [(p.slot_lo * rw, p.slot_hi * rw) for p in parts]
+
+    return vertex_partitioned_eval(level_fn, k, ranges, bufs[0], bufs[1], acc, group)
+
+
+def eval_vertex_simulated(g, ds, k, max_ts, cfg, anchor_source, acc, world, bufs=None,
+                          timed=False):
+    """The `world`-rank vertex-partitioned evaluation run on ONE device: at
+    every level the ranks' shares run one after the other on the same
+    full-size buffers, so the all-gather between levels is the identity.
+    Returns acc and, with timed=True, the CUDA-event time of every
+    (level, rank) share in ms -- the per-rank compute of an N-GPU run
+    (bench.py --simulate-world)."""
+    import torch
+    from .sieve import eval_vertex_level, vertex_partition
+    parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
+    if not all(p.applicable for p in parts):
+        raise ValueError("vertex partition not applicable")
+    words = parts[0].state_words
+    if bufs is None:
+        bufs = (torch.empty(words, dtype=torch.int64, device=acc.device),
+                torch.empty(words, dtype=torch.int64, device=acc.device))
+    st = torch.cuda.current_stream(acc.device)
+    prev, cur = bufs
+    times = {}
+    for level in range(2, k + 1):
+        for q in range(world):
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+            eval_vertex_level(g, ds, k, level, max_ts, cfg, anchor_source, q, world,
+                              prev.data_ptr(), cur.data_ptr(), acc.data_ptr(), st.cuda_stream)
+            if timed:
+                e1.record(st)
+                times[(level, q)] = (e0, e1)
+        prev, cur = cur, prev
+    if timed:
+        torch.cuda.synchronize(acc.device)
+        times = {key: a.elapsed_time(b) for key, (a, b) in times.items()}
+    return acc, times, parts

@@ -215,3 +215,24 @@ def finalize(acc: np.ndarray, sink: int = -1):
     _native.check(_native.lib().tsv_finalize(len(a), a if len(a) else np.zeros(1, np.uint64),
                                              int(sink), C.byref(out)))
     return a, int(out.flagged), int(out.checksum)
+
+
+def vertex_partition(g: TemporalGraph, dshades: DeviceShades, k: int, rank: int = 0,
+                     world: int = 1) -> _native.Partition:
+    """tsv_vertex_partition: this rank's state-row range of the vertex-
+    partitioned evaluation (applicable = 0: use point sharding)."""
+    out = _native.Partition()
+    _native.check(_native.lib().tsv_vertex_partition(g.handle, dshades.handle, int(k), int(rank),
+                                                     int(world), C.byref(out)))
+    return out
+
+
+def eval_vertex_level(g: TemporalGraph, dshades: DeviceShades, k: int, level: int, max_ts: int,
+                      config: SieveConfig, anchor_source: int, rank: int, world: int,
+                      d_prev: int, d_cur: int, d_acc: int, stream_ptr: int = 0) -> None:
+    """tsv_eval_vertex_level: level `level` of this rank's vertices."""
+    cfg = config.to_native()
+    _native.check(_native.lib().tsv_eval_vertex_level(
+        g.handle, dshades.handle, int(k), int(level), int(max_ts), C.byref(cfg),
+        int(anchor_source), int(rank), int(world), C.c_void_p(d_prev), C.c_void_p(d_cur),
+        C.c_void_p(d_acc), C.c_void_p(stream_ptr)))

@@ -601,3 +601,36 @@ def test_edges_rebuilt_from_layout(cuda_device, monkeypatch):
         r2 = T.restrict_to(ref, keep, 30)
         for a, b in zip(r1.edges(), r2.edges()):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_vertex_partitioned_simulated_equals_single(cuda_device, world):
+    """The multi-GPU form of the vertex-lane engine (tsv_vertex_partition +
+    tsv_eval_vertex_level per rank; shard.eval_vertex_simulated runs the ranks
+    one after the other on this device, so the row all-gather is the identity)
+    gives the single-GPU accumulators and the oracle's, with anchors and
+    horizons; the ranks' state-row ranges tile [0, slots)."""
+    import torch
+    from paper_2001_07158_b200.shard import eval_vertex_simulated
+    rng = np.random.default_rng(90 + world)
+    n, m, t = 500, 8000, 60
+    u = rng.integers(0, n, m)
+    v = rng.integers(0, n, m)
+    ts = rng.integers(1, t + 1, m)
+    for k, seed, mt, anchor, directed in ((5, 3, None, (-1, -1), True), (4, 5, 40, (7, 9), True),
+                                          (3, 9, None, (-1, -1), False)):
+        g = T.TemporalGraph.build(n, (u, v, ts), directed)
+        cfg = T.SieveConfig(seed=seed)
+        sh = T.build_shades(T.MotifQuery.from_multiset([1] * k), T.VertexColoring.uniform(n),
+                            cfg)
+        ds = T.DeviceShades(g, k, sh)
+        mt = mt or g.t()
+        acc = torch.zeros(n, dtype=torch.int64, device="cuda")
+        acc, _, parts = eval_vertex_simulated(g, ds, k, mt, cfg, anchor[0], acc, world)
+        got = acc.cpu().numpy().view(np.uint64)
+        assert parts[0].slot_lo == 0 and parts[-1].slot_hi == parts[0].slots
+        assert all(a.slot_hi == b.slot_lo for a, b in zip(parts, parts[1:]))
+        cu, cv, ct = g.edges()
+        want = O.eval_points(n, cu, cv, ct, directed, k, mt, sh.vertex_off, sh.vertex_shades, seed,
+                             anchor[0])
+        assert np.array_equal(got, want), (k, world)
