@@ -48,7 +48,7 @@ namespace tsv {
 namespace {
 
 constexpr unsigned kFullV = 0xffffffffu;
-constexpr int kVWarps = 4;   // warps per block
+constexpr int kVWarps = 2;   // warps per block
 constexpr int kQCap = 64;    // queued rows per warp (ring)
 
 __host__ __device__ constexpr int binom_c(int n, int r) {
@@ -130,7 +130,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // keep every access conflict-free.
 template <int E, int F, int L, bool LAST>
 struct VertSmem {
-  uint64_t x[E][32];                    // the arc's source row (cp.async)
+  uint64_t x[2][E][32];                 // the next / current arc's source row (cp.async)
   uint64_t u[E][32];                    // the lane's running prefix U_L
   uint64_t q[LAST ? 1 : E][kQCap];      // queued U rows (ring)
   int32_t q_slot[kQCap], q_head[kQCap];
@@ -138,7 +138,7 @@ struct VertSmem {
 };
 
 template <int K, int L, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kVWarps * 32, 5) k_coef_vertex(const VertArgs A) {
+__global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) {
   constexpr int E = binom_c(K, L - 1);  // input entries (row of level L-1)
   constexpr int F = binom_c(K, L);      // output entries
   using Sm = VertSmem<E, F, L, LAST>;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kVWarps * 32, 5) k_coef_vertex(const VertArgs 
     __syncwarp();
   };
 
-  // the arc's source row goes to shared memory asynchronously (cp.async)
+  // the next arc's source row goes to shared memory one step ahead (cp.async)
   auto fetch = [&](int i, uint32_t& meta, bool& live) {
     live = false;
     meta = 0;
@@ -220,14 +220,11 @@ __global__ void __launch_bounds__(kVWarps * 32, 5) k_coef_vertex(const VertArgs 
       if (live) {
         const uint64_t* row = rows + static_cast<int64_t>(src) * E;
 #pragma unroll
-        for (int e = 0; e < E; ++e) cp_async8(&S.x[e][lane], row + e);
+        for (int e = 0; e < E; ++e) cp_async8(&S.x[i & 1][e][lane], row + e);
       }
     }
     cp_async_commit();
   };
-  // one staging row per lane: the next arc's row is requested as soon as
-  // the current one is consumed, and lands while the run end / z-map queue
-  // work of this step runs
   uint32_t nmeta;
   bool nlive;
   fetch(0, nmeta, nlive);
@@ -235,14 +232,14 @@ __global__ void __launch_bounds__(kVWarps * 32, 5) k_coef_vertex(const VertArgs 
     const uint32_t meta = nmeta;
     bool live = nlive;
     cp_async_wait_all();  // row i has landed (lane-private slots: no barrier)
+    if (i + 1 < steps) fetch(i + 1, nmeta, nlive);
     if (LAST && live) live = __ldg(P.g.run_ts + run) <= P.max_ts;
     if (live) {
       const KSplit ys = ksplit(draw_edge_y(pre, yb, meta & kEdgeMask));
 #pragma unroll 1
       for (int e = 0; e < E; ++e)
-        S.u[e][lane] ^= gf_reduce_alu(clmul64_kara_s(ys, ksplit(S.x[e][lane])));
+        S.u[e][lane] ^= gf_reduce_alu(clmul64_kara_s(ys, ksplit(S.x[i & 1][e][lane])));
     }
-    if (i + 1 < steps) fetch(i + 1, nmeta, nlive);
     const bool runend = i < cnt && (meta & kRunEnd);
     if (!LAST) {
       const int32_t slot = runend ? __ldg(P.g.run_slot + run) : -1;
