@@ -443,7 +443,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=-1, help="-1 = per-config default")
     ap.add_argument("--simulate-world", default="",
-                    help="comma-separated N: time each rank's share of the vertex-partitioned "
+                    help="N list (2,4,8 or 2+4+8): time each rank's share of the vertex-partitioned "
                          "evaluation on this one GPU and project the N-GPU step (DESIGN.md 6)")
     ap.add_argument("--nvlink-gbs", type=float, default=720.0,
                     help="all-gather bandwidth per GPU assumed by the --simulate-world model")
@@ -643,7 +643,7 @@ def main():
                                "(modeled: one GPU here); + XOR combine of n words"),
                      "nvlink_gbs": args.nvlink_gbs, "worlds": {}}
         ref_acc = res[0].clone()
-        for N in (int(x) for x in args.simulate_world.split(",") if x):
+        for N in (int(x) for x in args.simulate_world.replace("+", ",").split(",") if x):
             a = torch.zeros(n, dtype=torch.int64, device="cuda")
             try:
                 eval_vertex_simulated(g, ds, k, g.t(), cfgs[0], anchor[0], a, N)  # warm-up

@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--kinds", default="pageable,pinned")
     args = ap.parse_args()
     import torch
     import paper_2001_07158_b200 as T
@@ -52,7 +53,8 @@ def main():
         torch.cuda.synchronize()
         return r, (time.perf_counter() - t0) * 1e3
 
-    for kind, a in arrs.items():
+    for kind in args.kinds.split(","):
+        a = arrs[kind]
         rows = []
         for _ in range(args.iters):
             g, tb = t(lambda: T.TemporalGraph.build(inst.n, a, inst.directed, 0, 0))
@@ -66,6 +68,9 @@ def main():
             _, tf = t(lambda: g.__del__())
             rows.append((tb, ts_, te, td, tapi, tapi2, tf))
             del g
+        for r in rows:
+            print(f"  {kind} iter: " + " ".join(f"{x:.1f}" for x in r) +
+                  f"  free GB {torch.cuda.mem_get_info()[0] / 1e9:.1f}", flush=True)
         best = [min(r[i] for r in rows) for i in range(7)]
         print(f"{kind:9s} build {best[0]:.2f} ms  shades {best[1]:.2f}  eval(1 rep) {best[2]:.2f}"
               f"  d2h {best[3]:.2f}  C-ABI eval (shade upload) {best[4]:.2f}"
