@@ -53,7 +53,7 @@ def main():
         torch.cuda.synchronize()
         return r, (time.perf_counter() - t0) * 1e3
 
-    for kind in args.kinds.split(","):
+    for kind in args.kinds.replace("+", ",").split(","):
         a = arrs[kind]
         rows = []
         for _ in range(args.iters):
