@@ -638,9 +638,10 @@ def main():
     simulated = None
     if args.simulate_world and world == 1:
         from paper_2001_07158_b200.shard import eval_vertex_simulated
-        simulated = {"model": ("per level: max over ranks of the rank's measured share + "
-                               "all-gather of the level's rows at --nvlink-gbs per GPU "
-                               "(modeled: one GPU here); + XOR combine of n words"),
+        simulated = {"model": ("per level: max over ranks of the rank's measured share + the "
+                               "targeted row exchange (the largest rank's rows sent or received, "
+                               "from its exchange lists) at --nvlink-gbs per GPU (modeled: one "
+                               "GPU here); + XOR combine of n words"),
                      "nvlink_gbs": args.nvlink_gbs, "worlds": {}}
         ref_acc = res[0].clone()
         for N in (int(x) for x in args.simulate_world.replace("+", ",").split(",") if x):
@@ -656,20 +657,30 @@ def main():
             if anchor[1] >= 0:
                 _native.finalize_device(a.data_ptr(), n, anchor[1], sp)
             S = parts[0].slots
+            # targeted exchange: rows per rank from the exchange lists
+            from paper_2001_07158_b200.sieve import vertex_exchange_plan
+            rows_max = 0
+            if N > 1:
+                plans = [vertex_exchange_plan(g, ds, k, q, N) for q in range(N)]
+                rows_max = max(max(p.send_total, p.recv_total) for p in plans)
             lv = {}
             total_ms = 0.0
             for level in range(2, k + 1):
                 per = [times[(level, q)] for q in range(N)]
-                xch = 0.0
+                xch = xch_ag = 0.0
                 if level < k and N > 1:
-                    xch = (N - 1) / N * S * parts[0].row_words[level] * 8 / (args.nvlink_gbs * 1e9) * 1e3
-                lv[str(level)] = {"rank_ms": per, "max_ms": max(per), "exchange_ms": xch}
+                    F = parts[0].row_words[level]
+                    xch = rows_max * F * 8 / (args.nvlink_gbs * 1e9) * 1e3
+                    xch_ag = (N - 1) / N * S * F * 8 / (args.nvlink_gbs * 1e9) * 1e3
+                lv[str(level)] = {"rank_ms": per, "max_ms": max(per), "exchange_ms": xch,
+                                  "allgather_exchange_ms": xch_ag}
                 total_ms += max(per) + xch
             comb = 2 * (N - 1) / N * n * 8 / (args.nvlink_gbs * 1e9) * 1e3 if N > 1 else 0.0
             total_ms += comb
             simulated["worlds"][str(N)] = {
                 "levels": lv, "combine_ms": comb, "projected_ms_per_step": total_ms * reps,
                 "projected_value": upd_step / (total_ms * reps * 1e-3),
+                "exchange_rows_per_rank_max": rows_max, "slots": S,
                 "parity_vs_n1": bool(torch.equal(a, ref_acc))}
 
     # the GPU's accumulators on the CPU sample's window (horizon max_ts on the

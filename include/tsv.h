@@ -233,6 +233,24 @@ int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int le
                           int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
                           uint64_t* d_acc, void* stream);
 
+/* Targeted row exchange between levels (instead of an all-gather): rank
+ * sends to peer q exactly its rows some arc of q reads, receives likewise;
+ * the lists are fixed per graph.  plan: row counts per peer (world <= 32);
+ * pack: this rank's outgoing rows of level-l buffer d_rows (row_words =
+ * C(k, l)) into d_sendbuf, peers in rank order; unpack: d_recvbuf (peers in
+ * rank order) into d_rows.  The bytes in between move with one all-to-all
+ * (shard.py).  Asynchronous on `stream`. */
+typedef struct {
+  int64_t send_rows[32], recv_rows[32];
+  int64_t send_total, recv_total;
+} tsv_exchange;
+int tsv_vertex_exchange_plan(const tsv_graph* g, const tsv_shades* s, int k, int rank,
+                             int world, tsv_exchange* out);
+int tsv_vertex_exchange_pack(const tsv_graph* g, int rank, int world, int row_words,
+                             const uint64_t* d_rows, uint64_t* d_sendbuf, void* stream);
+int tsv_vertex_exchange_unpack(const tsv_graph* g, int rank, int world, int row_words,
+                               const uint64_t* d_recvbuf, uint64_t* d_rows, void* stream);
+
 /* Ascending indices of the nonzero words of acc[0..n) (the flagged list of
  * finalize, sieve.cpp:136-159) into idx (capacity n), on all host threads.
  * Returns the count. */

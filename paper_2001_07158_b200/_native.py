@@ -41,6 +41,11 @@ class Partition(C.Structure):
                 ("row_words", C.c_int32 * 32)]
 
 
+class Exchange(C.Structure):
+    _fields_ = [("send_rows", C.c_int64 * 32), ("recv_rows", C.c_int64 * 32),
+                ("send_total", C.c_int64), ("recv_total", C.c_int64)]
+
+
 class Outcome(C.Structure):
     _fields_ = [("global_nonzero", C.c_int32), ("pad", C.c_int32), ("flagged", C.c_int64),
                 ("checksum", C.c_uint64), ("peak_field_words", C.c_uint64),
@@ -94,6 +99,10 @@ def lib():
     L.tsv_vertex_partition.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(Partition)]
     L.tsv_eval_vertex_level.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int32, C.POINTER(Config),
                                         C.c_int32, C.c_int, C.c_int, vp, vp, vp, vp]
+    L.tsv_vertex_exchange_plan.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int,
+                                           C.POINTER(Exchange)]
+    L.tsv_vertex_exchange_pack.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]
+    L.tsv_vertex_exchange_unpack.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]
     L.tsv_nonzero_index.restype = C.c_int64
     L.tsv_nonzero_index.argtypes = [_u64p, C.c_int64, _i32p]
     L.tsv_finalize_device.argtypes = [vp, C.c_int64, C.c_int32, vp, C.POINTER(Outcome)]

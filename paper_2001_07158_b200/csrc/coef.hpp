@@ -112,6 +112,26 @@ void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
                        const std::function<void*(size_t)>& alloc,
                        const std::function<void(void*)>& release, int32_t v_lo = 0,
                        int32_t v_hi = -1);
+// Targeted row exchange of the vertex-partitioned engine: the state slots
+// this rank sends to / receives from every peer (rows some arc of the
+// receiving rank reads), peers in rank order; fixed per graph (the arcs
+// reading a slot are the same at every level).
+struct ExchangeLists {
+  std::vector<int64_t> send_count, recv_count;  // rows per peer
+  int64_t send_total = 0, recv_total = 0;
+  int32_t* send_slots = nullptr;  // device, send_total
+  int32_t* recv_slots = nullptr;  // device, recv_total
+};
+void build_exchange_lists(const DevGraph& g, const std::vector<const VertList*>& lists,
+                          const std::vector<int64_t>& slot_lo, const std::vector<int64_t>& slot_hi,
+                          int rank, ExchangeLists& out, cudaStream_t st,
+                          const std::function<void*(size_t)>& alloc,
+                          const std::function<void(void*)>& release);
+// rows (F words) of `slots` <-> a packed buffer
+void launch_rows_pack(const int32_t* slots, int64_t count, int F, const uint64_t* rows,
+                      uint64_t* buf, cudaStream_t st);
+void launch_rows_unpack(const int32_t* slots, int64_t count, int F, const uint64_t* buf,
+                        uint64_t* rows, cudaStream_t st);
 // State slots of the runs before run r (= the first slot of runs >= r).
 int64_t count_slots_before(const DevGraph& g, int64_t r, cudaStream_t st,
                            const std::function<void*(size_t)>& alloc,

@@ -39,6 +39,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "coef.hpp"
 #include "gf_device.cuh"
@@ -452,6 +453,138 @@ void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
   out.head = head_s;
   out.start = start_s;
   out.count = counts_s;
+}
+
+namespace {
+
+// reader mask of every state slot: bit q set when an arc whose head rank q
+// owns reads the slot (one byte per slot, packed four to a word)
+__global__ void k_reader_mask(const int64_t* __restrict__ wl_start,
+                              const int32_t* __restrict__ wl_count, int64_t nv,
+                              const int32_t* __restrict__ arc_src, int q,
+                              unsigned int* __restrict__ mask) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nv) return;
+  const int64_t a0 = wl_start[i];
+  const int c = wl_count[i];
+  const unsigned bit = 1u << q;
+  for (int j = 0; j < c; ++j) {
+    const int32_t s = arc_src[a0 + j];
+    if (s >= 0) atomicOr(mask + (s >> 2), bit << (8 * (s & 3)));
+  }
+}
+
+__global__ void k_mask_flags(const unsigned int* __restrict__ mask, int64_t lo, int64_t hi, int q,
+                             uint8_t* __restrict__ f) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= hi - lo) return;
+  const int64_t s = lo + i;
+  f[i] = ((mask[s >> 2] >> (8 * (s & 3))) >> q) & 1u;
+}
+
+template <bool PACK>
+__global__ void k_rows_move(const int32_t* __restrict__ slots, int64_t count, int F,
+                            const uint64_t* __restrict__ src, uint64_t* __restrict__ dst) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count * F) return;
+  const int64_t r = i / F;
+  const int e = static_cast<int>(i - r * F);
+  const int64_t s = slots[r];
+  if (PACK) dst[i] = src[s * F + e];
+  else dst[s * F + e] = src[i];
+}
+
+}  // namespace
+
+void build_exchange_lists(const DevGraph& g, const std::vector<const VertList*>& lists,
+                          const std::vector<int64_t>& slot_lo, const std::vector<int64_t>& slot_hi,
+                          int rank, ExchangeLists& out, cudaStream_t st,
+                          const std::function<void*(size_t)>& alloc,
+                          const std::function<void(void*)>& release) {
+  auto ck = [](cudaError_t e) {
+    if (e != cudaSuccess)
+      throw std::runtime_error(std::string("exchange lists: ") + cudaGetErrorString(e));
+  };
+  const int world = static_cast<int>(lists.size());
+  const int64_t S = std::max<int64_t>(g.S, 1);
+  auto* mask = static_cast<unsigned int*>(alloc(static_cast<size_t>((S + 3) / 4) * 4));
+  ck(cudaMemsetAsync(mask, 0, static_cast<size_t>((S + 3) / 4) * 4, st));
+  for (int q = 0; q < world; ++q) {
+    const VertList* vl = lists[q];
+    if (vl->nv)
+      k_reader_mask<<<nblk_v(vl->nv), 256, 0, st>>>(vl->start, vl->count, vl->nv,
+                                                     g.arc_src, q, mask);
+  }
+  out = ExchangeLists{};
+  out.send_count.assign(world, 0);
+  out.recv_count.assign(world, 0);
+  // send to q: my slots with bit q; receive from q: q's slots with my bit
+  std::vector<int32_t*> parts_s(world, nullptr), parts_r(world, nullptr);
+  int64_t* cnt = static_cast<int64_t*>(alloc(8));
+  auto select = [&](int64_t lo, int64_t hi, int bitq, int32_t** outp, int64_t* n) {
+    *outp = nullptr;
+    *n = 0;
+    if (hi <= lo) return;
+    uint8_t* f = static_cast<uint8_t*>(alloc(static_cast<size_t>(hi - lo)));
+    int32_t* o = static_cast<int32_t*>(alloc(static_cast<size_t>(hi - lo) * 4));
+    k_mask_flags<<<nblk_v(hi - lo), 256, 0, st>>>(mask, lo, hi, bitq, f);
+    cub::CountingInputIterator<int32_t> it(static_cast<int32_t>(lo));
+    size_t tmp = 0;
+    ck(cub::DeviceSelect::Flagged(nullptr, tmp, it, f, o, cnt, hi - lo, st));
+    void* t = alloc(tmp ? tmp : 8);
+    ck(cub::DeviceSelect::Flagged(t, tmp, it, f, o, cnt, hi - lo, st));
+    ck(cudaMemcpyAsync(n, cnt, 8, cudaMemcpyDeviceToHost, st));
+    ck(cudaStreamSynchronize(st));
+    release(t);
+    release(f);
+    *outp = o;
+  };
+  for (int q = 0; q < world; ++q) {
+    if (q == rank) continue;
+    select(slot_lo[rank], slot_hi[rank], q, &parts_s[q], &out.send_count[q]);
+    select(slot_lo[q], slot_hi[q], rank, &parts_r[q], &out.recv_count[q]);
+  }
+  release(cnt);
+  release(mask);
+  // one array per direction, peers in rank order
+  int64_t ts = 0, tr = 0;
+  for (int q = 0; q < world; ++q) ts += out.send_count[q], tr += out.recv_count[q];
+  out.send_slots = static_cast<int32_t*>(alloc(static_cast<size_t>(ts) * 4 + 4));
+  out.recv_slots = static_cast<int32_t*>(alloc(static_cast<size_t>(tr) * 4 + 4));
+  int64_t os = 0, orr = 0;
+  for (int q = 0; q < world; ++q) {
+    if (out.send_count[q])
+      ck(cudaMemcpyAsync(out.send_slots + os, parts_s[q], out.send_count[q] * 4,
+                         cudaMemcpyDeviceToDevice, st));
+    if (out.recv_count[q])
+      ck(cudaMemcpyAsync(out.recv_slots + orr, parts_r[q], out.recv_count[q] * 4,
+                         cudaMemcpyDeviceToDevice, st));
+    os += out.send_count[q];
+    orr += out.recv_count[q];
+  }
+  ck(cudaStreamSynchronize(st));
+  for (int q = 0; q < world; ++q) {
+    if (parts_s[q]) release(parts_s[q]);
+    if (parts_r[q]) release(parts_r[q]);
+  }
+  out.send_total = ts;
+  out.recv_total = tr;
+}
+
+void launch_rows_pack(const int32_t* slots, int64_t count, int F, const uint64_t* rows,
+                      uint64_t* buf, cudaStream_t st) {
+  if (count <= 0) return;
+  prof_begin("vertex_exchange", st);
+  k_rows_move<true><<<nblk_v(count * F), 256, 0, st>>>(slots, count, F, rows, buf);
+  prof_end(st);
+}
+
+void launch_rows_unpack(const int32_t* slots, int64_t count, int F, const uint64_t* buf,
+                        uint64_t* rows, cudaStream_t st) {
+  if (count <= 0) return;
+  prof_begin("vertex_exchange", st);
+  k_rows_move<false><<<nblk_v(count * F), 256, 0, st>>>(slots, count, F, buf, rows);
+  prof_end(st);
 }
 
 int64_t count_slots_before(const DevGraph& g, int64_t r, cudaStream_t st,

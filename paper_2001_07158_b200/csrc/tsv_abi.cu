@@ -245,6 +245,8 @@ struct tsv_graph {
     int32_t v_lo = 0, v_hi = 0;
     int64_t slot_lo = 0, slot_hi = 0;
     std::vector<void*> owned;
+    bool xlists = false;  // exchange lists built
+    tsv::ExchangeLists xl;
   };
   mutable std::mutex vl_mu;
   mutable std::vector<std::unique_ptr<VertPart>> parts;
@@ -1748,6 +1750,89 @@ int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int le
     tsv::launch_coef_vertex(cp, vp.vl, det, d_acc, st);
     TSV_CUDA(cudaGetLastError());
   });
+}
+
+int tsv_vertex_exchange_plan(const tsv_graph* g, const tsv_shades* s, int k, int rank,
+                             int world, tsv_exchange* out) {
+  return guard([&] {
+    if (!g || !s || !out) throw std::invalid_argument("null argument");
+    if (world < 1 || world > 32 || rank < 0 || rank >= world)
+      throw std::invalid_argument("bad rank/world");
+    std::memset(out, 0, sizeof(*out));
+    DeviceGuard dg(g->device);
+    cudaStream_t st = nullptr;
+    TSV_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct Del {
+      cudaStream_t s;
+      ~Del() {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+    } del{st};
+    std::vector<const tsv::VertList*> lists;
+    std::vector<int64_t> lo, hi;
+    for (int q = 0; q < world; ++q) {
+      const tsv_graph::VertPart& p = vertex_part(g, q, world, st);
+      lists.push_back(&p.vl);
+      lo.push_back(p.slot_lo);
+      hi.push_back(p.slot_hi);
+    }
+    auto& me = const_cast<tsv_graph::VertPart&>(vertex_part(g, rank, world, st));
+    std::lock_guard<std::mutex> lk(g->vl_mu);
+    if (!me.xlists) {
+      auto alloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+          throw CudaError("exchange lists: out of device memory");
+        me.owned.push_back(p);
+        return p;
+      };
+      auto release = [&](void* p) {
+        auto it = std::find(me.owned.begin(), me.owned.end(), p);
+        if (it != me.owned.end()) me.owned.erase(it);
+        cudaFreeAsync(p, st);
+      };
+      tsv::build_exchange_lists(g->dev, lists, lo, hi, rank, me.xl, st, alloc, release);
+      me.xlists = true;
+    }
+    for (int q = 0; q < world; ++q) {
+      out->send_rows[q] = me.xl.send_count[q];
+      out->recv_rows[q] = me.xl.recv_count[q];
+    }
+    out->send_total = me.xl.send_total;
+    out->recv_total = me.xl.recv_total;
+  });
+}
+
+static int exchange_move(const tsv_graph* g, int rank, int world, int row_words,
+                         const uint64_t* src, uint64_t* dst, void* stream, bool pack) {
+  return guard([&] {
+    if (!g || !src || !dst) throw std::invalid_argument("null argument");
+    DeviceGuard dg(g->device);
+    const tsv_graph::VertPart* me = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(g->vl_mu);
+      for (auto& vp : g->parts)
+        if (vp->rank == rank && vp->world == world) me = vp.get();
+    }
+    if (!me || !me->xlists) throw std::invalid_argument("call tsv_vertex_exchange_plan first");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (pack)
+      tsv::launch_rows_pack(me->xl.send_slots, me->xl.send_total, row_words, src, dst, st);
+    else
+      tsv::launch_rows_unpack(me->xl.recv_slots, me->xl.recv_total, row_words, src, dst, st);
+    TSV_CUDA(cudaGetLastError());
+  });
+}
+
+int tsv_vertex_exchange_pack(const tsv_graph* g, int rank, int world, int row_words,
+                             const uint64_t* d_rows, uint64_t* d_sendbuf, void* stream) {
+  return exchange_move(g, rank, world, row_words, d_rows, d_sendbuf, stream, true);
+}
+
+int tsv_vertex_exchange_unpack(const tsv_graph* g, int rank, int world, int row_words,
+                               const uint64_t* d_recvbuf, uint64_t* d_rows, void* stream) {
+  return exchange_move(g, rank, world, row_words, d_recvbuf, d_rows, stream, false);
 }
 
 int64_t tsv_nonzero_index(const uint64_t* acc, int64_t n, int32_t* idx) {

@@ -106,7 +106,7 @@ def xor_allreduce(t, group=None, out=None):
     return res
 
 
-def vertex_partitioned_eval(level_fn, k, ranges, prev, cur, acc, group=None):
+def vertex_partitioned_eval(level_fn, k, ranges, prev, cur, acc, group=None, exchange=None):
     """One evaluation split by HEAD VERTEX across the ranks:
     the multi-GPU form of the coefficient engine.
 
@@ -118,12 +118,16 @@ def vertex_partitioned_eval(level_fn, k, ranges, prev, cur, acc, group=None):
     (an all-gather, in place, into the full-size buffers every rank holds).
     `level_fn(l, prev, cur, acc)` computes this rank's share of level l;
     at l = k it XORs its vertices' readout into acc, which the ranks
-    XOR-combine at the end (each vertex's word comes from its owner)."""
+    XOR-combine at the end (each vertex's word comes from its owner).
+    `exchange(level, cur)`, when given, replaces the all-gather (the targeted
+    exchange of eval_vertex_partitioned_device)."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     for level in range(2, k + 1):
         level_fn(level, prev, cur, acc)
-        if level < k and world > 1:
+        if level < k and world > 1 and exchange is not None:
+            exchange(level, cur)
+        elif level < k and world > 1:
             works = []
             for q, (lo, hi) in enumerate(ranges(level)):
                 if hi > lo:
@@ -136,11 +140,18 @@ def vertex_partitioned_eval(level_fn, k, ranges, prev, cur, acc, group=None):
 
 
 def eval_vertex_partitioned_device(g, ds, k, max_ts, cfg, anchor_source, acc, rank, world,
-                                   group=None, bufs=None, stream=None):
+                                   group=None, bufs=None, stream=None, targeted=True):
     """vertex_partitioned_eval with the device engine (tsv_eval_vertex_level)
-    on this rank's GPU; acc: int64 CUDA tensor of n words (XORed into)."""
+    on this rank's GPU; acc: int64 CUDA tensor of n words (XORed into).
+
+    targeted=True: between levels each rank sends a peer only the rows some
+    arc of that peer reads (tsv_vertex_exchange_pack -> all_to_all_single ->
+    tsv_vertex_exchange_unpack; at C5 ~1.5 readers per row, so ~1.5/(N-1)
+    of the all-gather's bytes); else the all-gather of row ranges."""
     import torch
-    from .sieve import eval_vertex_level, vertex_partition
+    import torch.distributed as dist
+    from .sieve import (eval_vertex_level, vertex_exchange_move, vertex_exchange_plan,
+                        vertex_partition)
     parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
     if not all(p.applicable for p in parts):
         raise ValueError("vertex partition not applicable")
@@ -158,7 +169,23 @@ def eval_vertex_partitioned_device(g, ds, k, max_ts, cfg, anchor_source, acc, ra
         rw = parts[0].row_words[level]
         return [(p.slot_lo * rw, p.slot_hi * rw) for p in parts]
 
-    return vertex_partitioned_eval(level_fn, k, ranges, bufs[0], bufs[1], acc, group)
+    exchange = None
+    if targeted and world > 1:
+        plan = vertex_exchange_plan(g, ds, k, rank, world)
+        fmax = max(parts[0].row_words[lv] for lv in range(2, k))
+        sbuf = torch.empty(max(plan.send_total * fmax, 1), dtype=torch.int64, device=acc.device)
+        rbuf = torch.empty(max(plan.recv_total * fmax, 1), dtype=torch.int64, device=acc.device)
+
+        def exchange(level, cur):
+            F = parts[0].row_words[level]
+            vertex_exchange_move(g, rank, world, F, cur.data_ptr(), sbuf.data_ptr(), True, sp)
+            dist.all_to_all_single(rbuf[:plan.recv_total * F], sbuf[:plan.send_total * F],
+                                   output_split_sizes=[plan.recv_rows[q] * F for q in range(world)],
+                                   input_split_sizes=[plan.send_rows[q] * F for q in range(world)],
+                                   group=group)
+            vertex_exchange_move(g, rank, world, F, rbuf.data_ptr(), cur.data_ptr(), False, sp)
+
+    return vertex_partitioned_eval(level_fn, k, ranges, bufs[0], bufs[1], acc, group, exchange)
 
 
 def eval_vertex_simulated(g, ds, k, max_ts, cfg, anchor_source, acc, world, bufs=None,
@@ -197,3 +224,51 @@ def eval_vertex_simulated(g, ds, k, max_ts, cfg, anchor_source, acc, world, bufs
         torch.cuda.synchronize(acc.device)
         times = {key: a.elapsed_time(b) for key, (a, b) in times.items()}
     return acc, times, parts
+
+
+def eval_vertex_simulated_private(g, ds, k, max_ts, cfg, anchor_source, n, world):
+    """Test form of the targeted exchange on ONE device: every simulated rank
+    has its own full-size state buffers and accumulators, computes only its
+    vertices' rows, and receives only the rows its exchange lists name (the
+    all-to-all done as copies between the ranks' packed buffers).  A row
+    missing from the lists leaves a zero where a reader needs it, so equality
+    with the single-GPU result checks the lists."""
+    import torch
+    from .sieve import (eval_vertex_level, vertex_exchange_move, vertex_exchange_plan,
+                        vertex_partition)
+    parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
+    plans = [vertex_exchange_plan(g, ds, k, q, world) for q in range(world)]
+    words = parts[0].state_words
+    st = torch.cuda.current_stream().cuda_stream
+    bufs = [[torch.zeros(words, dtype=torch.int64, device="cuda") for _ in range(2)]
+            for _ in range(world)]
+    accs = [torch.zeros(n, dtype=torch.int64, device="cuda") for _ in range(world)]
+    cur_i = 1
+    for level in range(2, k + 1):
+        for q in range(world):
+            eval_vertex_level(g, ds, k, level, max_ts, cfg, anchor_source, q, world,
+                              bufs[q][1 - cur_i].data_ptr(), bufs[q][cur_i].data_ptr(),
+                              accs[q].data_ptr(), st)
+        if level < k and world > 1:
+            F = parts[0].row_words[level]
+            sends = []
+            for q in range(world):
+                sb = torch.zeros(max(plans[q].send_total * F, 1), dtype=torch.int64, device="cuda")
+                vertex_exchange_move(g, q, world, F, bufs[q][cur_i].data_ptr(), sb.data_ptr(),
+                                     True, st)
+                sends.append(sb)
+            for q in range(world):   # q receives from every r: r's segment for q
+                segs = []
+                for r in range(world):
+                    off = sum(plans[r].send_rows[p] for p in range(q)) * F
+                    segs.append(sends[r][off:off + plans[r].send_rows[q] * F])
+                    assert plans[r].send_rows[q] == plans[q].recv_rows[r]
+                rb = torch.cat(segs) if segs else torch.zeros(1, dtype=torch.int64, device="cuda")
+                if rb.numel():
+                    vertex_exchange_move(g, q, world, F, rb.data_ptr(), bufs[q][cur_i].data_ptr(),
+                                         False, st)
+        cur_i = 1 - cur_i
+    out = accs[0]
+    for a in accs[1:]:
+        torch.bitwise_xor(out, a, out=out)
+    return out

@@ -236,3 +236,20 @@ def eval_vertex_level(g: TemporalGraph, dshades: DeviceShades, k: int, level: in
         g.handle, dshades.handle, int(k), int(level), int(max_ts), C.byref(cfg),
         int(anchor_source), int(rank), int(world), C.c_void_p(d_prev), C.c_void_p(d_cur),
         C.c_void_p(d_acc), C.c_void_p(stream_ptr)))
+
+
+def vertex_exchange_plan(g: TemporalGraph, dshades: DeviceShades, k: int, rank: int,
+                         world: int) -> _native.Exchange:
+    """tsv_vertex_exchange_plan: rows this rank sends to / receives from each peer."""
+    out = _native.Exchange()
+    _native.check(_native.lib().tsv_vertex_exchange_plan(g.handle, dshades.handle, int(k),
+                                                         int(rank), int(world), C.byref(out)))
+    return out
+
+
+def vertex_exchange_move(g: TemporalGraph, rank: int, world: int, row_words: int, src: int,
+                         dst: int, pack: bool, stream_ptr: int = 0) -> None:
+    """tsv_vertex_exchange_pack (rows -> send buffer) / _unpack (receive buffer -> rows)."""
+    f = _native.lib().tsv_vertex_exchange_pack if pack else _native.lib().tsv_vertex_exchange_unpack
+    _native.check(f(g.handle, int(rank), int(world), int(row_words), C.c_void_p(src),
+                    C.c_void_p(dst), C.c_void_p(stream_ptr)))

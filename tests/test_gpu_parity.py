@@ -634,3 +634,7 @@ def test_vertex_partitioned_simulated_equals_single(cuda_device, world):
         want = O.eval_points(n, cu, cv, ct, directed, k, mt, sh.vertex_off, sh.vertex_shades, seed,
                              anchor[0])
         assert np.array_equal(got, want), (k, world)
+        if world > 1:   # targeted exchange: private buffers per simulated rank
+            from paper_2001_07158_b200.shard import eval_vertex_simulated_private
+            acc2 = eval_vertex_simulated_private(g, ds, k, mt, cfg, anchor[0], n, world)
+            assert np.array_equal(acc2.cpu().numpy().view(np.uint64), want), ("targeted", k, world)
