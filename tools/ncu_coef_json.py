@@ -3,7 +3,7 @@ launches (tools/gpu_profile_coef.sh) into profiles/coef_kernels_c<config>.json,
 which bench.py reads for the roofline `traffic` and instruction-issue figures.
 Per kernel family (middle-level k_coef_arcs, k_coef_ztrans_tab, ...): launches,
 mean duration, DRAM bytes, executed warp instructions, pipe utilizations.
-Usage: python tools/ncu_coef_json.py gpurun_out/prof_<tag>.ncu-rep <config> <tag>"""
+Usage: python tools/ncu_coef_json.py gpurun_out/prof_<tag>.ncu-rep <config> <tag> [OUT.json]"""
 import csv
 import io
 import json
@@ -31,6 +31,11 @@ KEYS = {"ncu_duration_ms": "gpu__time_duration.sum",
 
 
 def family(name):
+    m = re.search(r"k_coef_vertex<(\d+), (\d+), (\w+), (\w+)>", name)
+    if m:
+        first = m.group(3) in ("1", "true")
+        last = m.group(4) in ("1", "true")
+        return "coef_vertex_first" if first else "coef_vertex_last" if last else "coef_vertex"
     m = re.search(r"k_coef_arcs<(\d+), (\d+), (\w+), (\w+)>", name)
     if m:
         first = m.group(3) in ("1", "true")
@@ -49,6 +54,7 @@ def family(name):
 
 def main():
     rep, config, tag = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    dest = sys.argv[4] if len(sys.argv) > 4 else None
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -68,7 +74,7 @@ def main():
                 e[k] = sum(float(d[m]) for d in ds) / len(ds) * SCALE.get(units[m], 1.0)
         e["traffic_bytes_per_launch"] = e.get("dram_read_bytes", 0) + e.get("dram_write_bytes", 0)
         res["kernels"][f] = e
-    path = os.path.join(ROOT, "profiles", f"coef_kernels_c{config}.json")
+    path = dest or os.path.join(ROOT, "profiles", f"coef_kernels_c{config}.json")
     with open(path, "w") as fh:
         json.dump(res, fh, indent=1)
     print(json.dumps(res, indent=1))
