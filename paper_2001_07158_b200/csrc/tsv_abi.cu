@@ -1599,6 +1599,18 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
     const int32_t n = g->host.n;
     const int64_t cnt = vertex_off[n];
+    // TSV_TRACE_API=1: phase wall times of this call on stderr
+    const char* tre = std::getenv("TSV_TRACE_API");
+    const bool trace = tre && tre[0] == '1';
+    auto t_last = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what, cudaStream_t sync) {
+      if (!trace) return;
+      if (sync) cudaStreamSynchronize(sync);
+      const auto now = std::chrono::steady_clock::now();
+      std::fprintf(stderr, "[api] %-24s %9.1f ms\n", what,
+                   std::chrono::duration<double, std::milli>(now - t_last).count());
+      t_last = now;
+    };
     if (cnt < 0 || (cnt > 0 && !vertex_shades)) throw std::invalid_argument("null argument");
     // a repeated shade table (every probe of one query) is not uploaded
     // again: reuse the cached device copy when the CSR is word-for-word equal
@@ -1612,6 +1624,7 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
           equal_par(g->shade_vs_copy.data(), vertex_shades, static_cast<size_t>(cnt)))
         hold = g->shade_cache;
     }
+    mark(hold ? "shade compare (hit)" : "shade compare (miss)", nullptr);
     if (!hold) {
       tsv_shades* sh = nullptr;
       const int rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
@@ -1623,6 +1636,7 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
       g->shade_k = k;
       copy_par(g->shade_off_copy, vertex_off, static_cast<size_t>(n) + 1);
       copy_par(g->shade_vs_copy, vertex_shades, static_cast<size_t>(cnt));
+      mark("shade upload + host copy", nullptr);
     }
     DeviceGuard dg(g->device);
     // the graph's stream; a concurrent call on the same graph gets its own
@@ -1648,14 +1662,18 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     uint64_t peak = 0;
     DevBuf acc(static_cast<size_t>(n) * 8, st);
     TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8, st));
+    mark("stream + acc", st);
     eval_device(g, hold.get(), k, max_ts, cfg, anchor_source, 0, 1ull << k, acc.as<uint64_t>(),
                 st, &peak);
+    mark("sieve", st);
     // finalize on the device (sink restriction, flagged count, checksum),
     // then the accumulators to the caller through pinned staging buffers
     uint64_t checksum = 0;
     int64_t flagged = 0;
     tsv::device_finalize(acc.as<uint64_t>(), n, anchor_sink, st, &checksum, &flagged);
+    mark("device finalize", st);
     copy_to_host(accumulators, acc.p, static_cast<size_t>(n) * 8, st);
+    mark("accumulators to host", st);
     out->flagged = flagged;
     out->global_nonzero = flagged > 0;
     out->checksum = checksum;

@@ -61,6 +61,9 @@ def main():
             ds, ts_ = t(lambda: T.DeviceShades(g, k, sh))
             _, te = t(lambda: T.eval_points_device(g, ds, k, g.t(), cfg, anchor[0], 0, 1 << k,
                                                    acc.data_ptr(), sp))
+            _, te2 = t(lambda: T.eval_points_device(g, ds, k, g.t(), cfg, anchor[0], 0, 1 << k,
+                                                    acc.data_ptr(), sp))
+            print(f"  eval first {te:.1f} ms, again {te2:.1f} ms", flush=True)
             _, td = t(lambda: acc.cpu())
             del ds
             _, tapi = t(lambda: api(g))
