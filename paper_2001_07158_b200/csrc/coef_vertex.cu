@@ -45,6 +45,18 @@
 #include "gf_device.cuh"
 #include "layout.hpp"
 
+// z map form: 2 = paired (E + F products per row instead of L * F, below),
+// 0 = direct sums (measured at C5 x0.1: 70.2 ms -> 68.1 ms per evaluation;
+// fully unrolled pairing was slower, 87 ms: register spills)
+#ifndef TSV_ZPAIR
+#define TSV_ZPAIR 2
+#endif
+// resident blocks per SM the register budget is sized for (1: unbounded;
+// capping at 8 two-warp blocks spilled and ran slower)
+#ifndef TSV_VMINB
+#define TSV_VMINB 1
+#endif
+
 namespace tsv {
 namespace {
 
@@ -136,12 +148,18 @@ struct VertSmem {
   uint64_t q[LAST ? 1 : E][kQCap];      // queued U rows (ring)
   int32_t q_slot[kQCap], q_head[kQCap];
   uint8_t pin[F > 0 ? F : 1][L], pj[F > 0 ? F : 1][L];  // output o: (rank of T_o - {j}, j) pairs
+#if TSV_ZPAIR == 2
+  uint64_t w[LAST ? 1 : E][32];         // paired z map: W[P] = z_P * U[P] of the lane's row
+  uint8_t pmask[E];                     // input entry P's subset mask
+#endif
 };
 
 template <int K, int L, bool FIRST, bool LAST>
-__global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) {
+__global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const VertArgs A) {
   constexpr int E = binom_c(K, L - 1);  // input entries (row of level L-1)
   constexpr int F = binom_c(K, L);      // output entries
+  // the paired z map pays E + F products against L * F
+  constexpr bool kZPairOk = !LAST && E + F < L * F;
   using Sm = VertSmem<E, F, L, LAST>;
   __shared__ Sm smem[kVWarps];
   const CoefParams& P = A.P;
@@ -149,6 +167,10 @@ __global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) 
   Sm& S = smem[wib];
   if (!LAST && lane == 0) {  // output pairs of the z map (colex order, coef_tables)
     constexpr SubsetTab<K, L> TL{};
+#if TSV_ZPAIR == 2
+    constexpr SubsetTab<K, L - 1> TP{};
+    for (int p = 0; p < E; ++p) S.pmask[p] = static_cast<uint8_t>(TP.mask[p]);
+#endif
     for (int o = 0; o < F; ++o) {
       int c = 0;
       for (int j = 0; j < K; ++j)
@@ -188,19 +210,55 @@ __global__ void __launch_bounds__(kVWarps * 32) k_coef_vertex(const VertArgs A) 
 #pragma unroll
       for (int j = 0; j < K; ++j) z[j] = __ldg(P.zj + static_cast<int64_t>(hd) * K + j);
       uint64_t* out = P.ubuf + static_cast<int64_t>(S.q_slot[qi]) * F;
+#if TSV_ZPAIR == 2
+      // paired z map: with z_X = XOR_{j in X} z_j,
+      //   z_T * (XOR_{P in T, |P| = L-1} U[P])
+      //     = XOR_P XOR_{j in T} z_j U[P] = S[T] ^ XOR_{P in T} z_P U[P]
+      // (j = T - P gives S[T]'s terms, j in P the rest), so
+      //   S[T] = z_T * XOR_P U[P]  ^  XOR_P W[P],   W[P] = z_P * U[P]:
+      // one product per input entry and one per output (C5, L = 3: 20
+      // instead of 30).  W rides in shared memory, the loops stay rolled.
+      if constexpr (kZPairOk) {
 #pragma unroll 1
-      for (int o = 0; o < F; ++o) {
-        ClassAcc ca;
-        class_zero(ca);
+        for (int p = 0; p < E; ++p) {
+          const unsigned pm = S.pmask[p];
+          uint64_t zp = 0;
 #pragma unroll
-        for (int c = 0; c < L; ++c) {
-          const int j = S.pj[o][c];
-          uint64_t zj = z[0];
-#pragma unroll
-          for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
-          class_acc(ksplit(zj), ksplit(S.q[S.pin[o][c]][qi]), ca);
+          for (int j = 0; j < K; ++j) zp ^= ((pm >> j) & 1u) ? z[j] : 0ull;
+          S.w[p][lane] = gf_reduce_alu(clmul64_kara_s(ksplit(zp), ksplit(S.q[p][qi])));
         }
-        out[o] = gf_reduce_alu(class_finish(ca));
+#pragma unroll 1
+        for (int o = 0; o < F; ++o) {
+          uint64_t zt = 0, su = 0, sw = 0;
+#pragma unroll
+          for (int c = 0; c < L; ++c) {
+            const int j = S.pj[o][c], pi = S.pin[o][c];
+            uint64_t zj = z[0];
+#pragma unroll
+            for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
+            zt ^= zj;
+            su ^= S.q[pi][qi];
+            sw ^= S.w[pi][lane];
+          }
+          out[o] = gf_reduce_alu(clmul64_kara_s(ksplit(zt), ksplit(su))) ^ sw;
+        }
+      } else
+#endif
+      {
+#pragma unroll 1
+        for (int o = 0; o < F; ++o) {
+          ClassAcc ca;
+          class_zero(ca);
+#pragma unroll
+          for (int c = 0; c < L; ++c) {
+            const int j = S.pj[o][c];
+            uint64_t zj = z[0];
+#pragma unroll
+            for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
+            class_acc(ksplit(zj), ksplit(S.q[S.pin[o][c]][qi]), ca);
+          }
+          out[o] = gf_reduce_alu(class_finish(ca));
+        }
       }
     }
     qh = (qh + take) & (kQCap - 1);
