@@ -186,7 +186,13 @@ def coef_alg_bytes(g, sh, k):
         # metadata per arc (edge id, source slot) + 4 B per run (slot)
         vertex = sum(8 * (a_src * comb(k, l - 1) + S * comb(k, l)) + 8 * g.info.arcs +
                      4 * g.info.runs for l in range(3, k))
-        return {"coef_arcs": arcs, "coef_ztrans": ztrans, "coef_vertex": vertex}
+        # GF(2^64) products of the vertex-lane middle levels: C(k, l-1) per
+        # live arc (y times its source row) + C(k, l-1) + C(k, l) per
+        # referenced run (the paired z map, coef_vertex.cu)
+        products = sum(a_src * comb(k, l - 1) + S * (comb(k, l - 1) + comb(k, l))
+                       for l in range(3, k))
+        return {"coef_arcs": arcs, "coef_ztrans": ztrans, "coef_vertex": vertex,
+                "_products": {"coef_vertex": products}}
     cu, cv, ct = (np.asarray(x, dtype=np.int64) for x in g.edges())
     if not g.directed():
         cu, cv, ct = np.concatenate([cu, cv]), np.concatenate([cv, cu]), np.concatenate([ct, ct])
@@ -234,6 +240,7 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
     alg1 = coef_alg_bytes() of one evaluation; achieved = those bytes x the
     evaluations of the profile pass / the kernel family's CUDA-event time in
     that pass; int_pipe from the committed ncu capture of the same kernel."""
+    products = alg1.get("_products", {})
     alg = {nm: evals * b for nm, b in alg1.items() if nm in coef}
     name = max(coef, key=lambda nm: coef[nm][1])
     n_launch, tot_ms = coef[name]
@@ -268,6 +275,23 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
                             "peak": peak_issue, "frac": ach / peak_issue,
                             "alu_pipe_frac_ncu": prof["alu_pipe_pct_active"] / 100,
                             "capture": prof["capture"]}
+        if "fmaheavy_pipe_pct_elapsed" in prof:
+            # the carry-less products' IMAD.WIDE run on the FMA-heavy pipe
+            roof["int_pipe"]["fmaheavy_pipe_frac_ncu"] = prof["fmaheavy_pipe_pct_elapsed"] / 100
+    if name in products:
+        # GF(2^64) products per second of the family against the measured
+        # throughput of the same multiply alone (tsv_gf_bench, holes +
+        # Karatsuba, full grid: profiles/int_pipe_peaks.json)
+        rate = evals * products[name] / (tot_ms * 1e-3)
+        try:
+            with open(os.path.join(ROOT, "profiles", "int_pipe_peaks.json")) as f:
+                gpeak = json.load(f)["GF product, holes + Karatsuba"]
+        except Exception:
+            gpeak = None
+        roof["gf_products"] = {"unit": "products/s", "achieved": rate, "peak": gpeak,
+                               "frac": rate / gpeak if gpeak else None,
+                               "peak_kind": "measured microbenchmark (tsv_gf_bench variant 2)",
+                               "per_launch": products[name] * evals / n_launch}
     return roof
 
 

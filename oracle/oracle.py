@@ -307,9 +307,10 @@ def ref_build_shades(n, colors, motif, seed=1):
 
 
 def ref_eval(n, u, v, ts, directed, colors, motif, max_ts=0, seed=1, lanes=8, threads=1,
-             anchor=(-1, -1), t=0, repeats=1):
+             anchor=(-1, -1), t=0, repeats=1, field_bits=64):
     """Reference eval_temporal_sieve on raw edges.  Returns dict or None (infeasible)."""
     u, v, ts = _a32(u), _a32(v), _a32(ts)
+    ref_lib().ref_set_field_bits(int(field_bits))
     acc = np.zeros(max(n, 1), np.uint64)
     cs, nf, gl = C.c_uint64(0), C.c_int64(0), C.c_int32(0)
     sec = ref_lib().ref_eval_temporal(n, len(u), u, v, ts, int(directed), t, _a32(colors),

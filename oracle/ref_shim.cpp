@@ -190,6 +190,11 @@ int64_t ref_build_shades(int32_t n, const int32_t* colors, const int32_t* motif,
 // eval_temporal_sieve on a graph built from raw edges with a color-multiset
 // query.  acc_out receives the n accumulators.  Returns the seconds spent in
 // eval_temporal_sieve (>= 0), -1 on error, -2 if the query is infeasible.
+// field width of ref_eval_temporal (the reference's GF(2^b) dispatch,
+// sieve.cpp:637-649); 64 unless set
+static int g_field_bits = 64;
+void ref_set_field_bits(int32_t b) { g_field_bits = b; }
+
 double ref_eval_temporal(int32_t n, int64_t m, const int32_t* u,
                          const int32_t* v, const int32_t* ts, int directed,
                          int32_t t, const int32_t* colors,
@@ -208,6 +213,7 @@ double ref_eval_temporal(int32_t n, int64_t m, const int32_t* u,
     cfg.seed = seed;
     cfg.lane_width = lanes;
     cfg.threads = threads;
+    cfg.field_bits = g_field_bits;
     cfg.memory_cap_words = ~std::uint64_t{0};
     ShadeAssignment sh = build_shades(q, col, cfg);
     if (!sh.feasible) return -2;

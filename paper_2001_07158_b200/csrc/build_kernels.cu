@@ -619,6 +619,12 @@ __global__ void k_mark_src(int64_t A, const int32_t* __restrict__ arc_src,
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(counts, static_cast<unsigned long long>(c));
 }
 
+__global__ void k_mark_last_run(int32_t n, const int32_t* __restrict__ vro,
+                                int32_t* __restrict__ flag) {
+  const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (v < n && vro[v + 1] > vro[v]) flag[vro[v + 1] - 1] = 1;
+}
+
 __global__ void k_slots(int64_t R, const int32_t* __restrict__ flag,
                         const int32_t* __restrict__ excl, int32_t* __restrict__ slot,
                         unsigned long long* counts) {
@@ -691,7 +697,7 @@ void edges_from_layout(const DevGraph& g, bool directed, int32_t* eu, int32_t* e
 }
 
 SlotCounts build_run_slots(int64_t A, int64_t R, int32_t* arc_src, int32_t* run_slot,
-                           cudaStream_t st) {
+                           cudaStream_t st, const int32_t* vtx_run_off, int32_t n) {
   SlotCounts out;
   if (R == 0) return out;
   constexpr int kT = 256;
@@ -709,6 +715,7 @@ SlotCounts build_run_slots(int64_t A, int64_t R, int32_t* arc_src, int32_t* run_
   cudaMemsetAsync(flag, 0, R * 4, st);
   cudaMemsetAsync(counts, 0, 16, st);
   if (A) k_mark_src<<<nblk(A), kT, 0, st>>>(A, arc_src, flag, counts);
+  if (vtx_run_off && n > 0) k_mark_last_run<<<nblk(n), kT, 0, st>>>(n, vtx_run_off, flag);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, flag, excl, R, st);
   k_slots<<<nblk(R), kT, 0, st>>>(R, flag, excl, run_slot, counts);
   if (A) k_src_to_slot<<<nblk(A), kT, 0, st>>>(A, arc_src, run_slot);

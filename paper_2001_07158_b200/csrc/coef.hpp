@@ -54,6 +54,12 @@ struct CoefParams {
   int warp_words = 0;    // shared words per warp (table + frame accumulator)
   const int32_t* vc_color = nullptr;  // vertex-ordered sieve filter (as LevelParams)
   int32_t vc_head = 0, vc_tail = 0, vc_wild = -1;
+  // time windows (coef_window.cu, item-stream kernels): a vertex's prefix
+  // starts from its carried U row (carry_in[h * carry_cs], when carry_nz[h])
+  // instead of zero, so every window row already holds the carry
+  const uint64_t* carry_in = nullptr;
+  const uint8_t* carry_nz = nullptr;
+  int carry_cs = 0;
 };
 
 // Lanes per arc group for an entry slice of ne entries (4, 8, 16 or 32).
@@ -141,6 +147,36 @@ int64_t count_slots_before(const DevGraph& g, int64_t r, cudaStream_t st,
 // at l = k the readout acc[h] ^= det * ... (no ulast).
 void launch_coef_vertex(const CoefParams& p, const VertList& vl, uint64_t det, uint64_t* acc,
                         cudaStream_t st);
+
+// Time windows (coef_window.cu): arcs without a source in the window read
+// the tail's carry slot base + tail; window edge ids -> the original graph's
+// (oid[base + local], or base + local when oid is null).
+void launch_win_src(int64_t A, int32_t* arc_src, const int32_t* arc_tail, int64_t base,
+                    cudaStream_t st);
+void launch_win_edge_ids(int64_t A, uint32_t* meta, const int32_t* oid, int64_t base,
+                         cudaStream_t st);
+// One level of one window, after the arc pass and the chunk fix-up, before
+// the z map: carry slots from the carry (the state at the window start),
+// then the carry from each vertex's last window row.
+struct WinCarryArgs {
+  const int32_t* run_slot = nullptr;
+  const int32_t* vro = nullptr;  // window vtx_run_off (n+1)
+  int32_t n = 0;
+  int64_t Sw = 0;                // window slots (carry slots follow)
+  const int8_t* vsh = nullptr;
+  int frs = 0, frm = 0;          // U-row entries of single- / multi-shade vertices
+  uint64_t* rows = nullptr;      // level rows, stride rs
+  int rs = 0;
+  uint8_t* sflag = nullptr;
+  uint64_t* carry = nullptr;     // n x cs
+  int cs = 0;
+  uint8_t* cnz = nullptr;        // n: carry row nonzero
+};
+void launch_win_carry(const WinCarryArgs& a, cudaStream_t st);
+void launch_win_multi_list(int32_t n, int64_t Sw, const int8_t* vsh, int2* list, int32_t* count,
+                           cudaStream_t st);
+void launch_ts_group_start(const int32_t* ts, const int64_t* pos, int nb, int64_t* out,
+                           cudaStream_t st);
 
 // Host tables (colex order = increasing bit mask within a level).
 struct CoefTables {

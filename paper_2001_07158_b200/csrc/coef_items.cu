@@ -48,6 +48,12 @@ constexpr uint32_t kEvStart = 1u, kEvPush = 2u;
 constexpr int kBig = 24;
 constexpr int kSub = 4;   // rounds per super-round (loads in flight per lane)  // items from which an arc gets whole rounds (table products)
 
+// the prefix a vertex starts from: its carried U entry o (time windows), else 0
+__device__ __forceinline__ uint64_t carry_entry(const CoefParams& P, int32_t h, int o) {
+  if (!P.carry_in || h < 0 || !__ldg(P.carry_nz + h)) return 0ull;
+  return __ldg(P.carry_in + static_cast<int64_t>(h) * P.carry_cs + o);
+}
+
 __device__ __forceinline__ bool color_ok(const int32_t* __restrict__ colors, int32_t x,
                                          int32_t c, int32_t wild) {
   return c == wild || __ldg(colors + x) == c;
@@ -71,6 +77,7 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items(const CoefParams P) {
   __shared__ int32_t s_cnt[kIW][32];   // item counts
   __shared__ int32_t s_poff[kIW][32];  // item list offset
   __shared__ int32_t s_dst[kIW][32];   // slot (levels < k) or head (level k)
+  __shared__ int32_t s_hd[kIW][32];    // head
   __shared__ int16_t s_fr[kIW][32];    // head frame size
   __shared__ uint8_t s_ev[kIW][32];
 
@@ -168,6 +175,7 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items(const CoefParams P) {
       s_cnt[wib][ai] = nitem;
       s_poff[wib][ai] = poff;
       s_dst[wib][ai] = dst;
+      s_hd[wib][ai] = head;
       s_fr[wib][ai] = static_cast<int16_t>(hs >= 0 ? P.frame_single : P.frame_multi);
       s_ev[wib][ai] = (vst ? kEvStart : 0u) | (push ? kEvPush : 0u);
       s_y[wib][ai] = y;
@@ -260,7 +268,8 @@ __global__ void __launch_bounds__(kIW * 32) k_coef_items(const CoefParams P) {
         if ((ev & kEvStart) && sa >= q0) {  // first part of a new vertex: reset
           __syncwarp();
           frame = s_fr[wib][ea];
-          for (int o = lane; o < frame; o += 32) acc[o] = 0;
+          const int32_t hd = s_hd[wib][ea];
+          for (int o = lane; o < frame; o += 32) acc[o] = carry_entry(P, hd, o);
           __syncwarp();
         }
         if (ia == ea) acc[out] ^= prod;
@@ -484,8 +493,9 @@ __global__ void __launch_bounds__(kIW * 32, TSV_REG_MINB)
         const unsigned bit = on ? 1u << a : 0u;
         const int fra = __shfl_sync(kFull, myfr, a);
         const int32_t d = __shfl_sync(kFull, dst, a);
+        const int32_t hd = __shfl_sync(kFull, head, a);
         if (vstm & bit) {
-          acc0 = 0;
+          acc0 = o < fra ? carry_entry(P, hd, o) : 0ull;
           frame = fra;
         }
         if (livem & bit) {
@@ -515,9 +525,10 @@ __global__ void __launch_bounds__(kIW * 32, TSV_REG_MINB)
       ev &= ev - 1;
       const unsigned bit = 1u << a;
       if (vstm & bit) {
-        acc0 = 0;
-        if (NO > 1) acc1 = 0;
         frame = __shfl_sync(kFull, myfr, a);
+        const int32_t hd = __shfl_sync(kFull, head, a);
+        acc0 = lane < frame ? carry_entry(P, hd, lane) : 0ull;
+        if (NO > 1) acc1 = lane + 32 < frame ? carry_entry(P, hd, lane + 32) : 0ull;
       }
       if (livem & bit) {
         const uint64_t om = s_om[wib][a];

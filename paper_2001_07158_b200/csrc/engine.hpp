@@ -186,11 +186,14 @@ void edges_from_layout(const DevGraph& g, bool directed, int32_t* eu, int32_t* e
 // State slots (build_kernels.cu): run_slot[r] = rank of r among the runs
 // some arc reads (else -1) and arc_src rewritten from run indices to slots.
 // Returns {arcs with a src, referenced runs}; synchronizes `st`.
+// vtx_run_off (n+1, optional): also give every vertex's last run a slot
+// (time windows of the coefficient engine read each vertex's final state).
 struct SlotCounts {
   int64_t arcs_with_src = 0, slots = 0;
 };
 SlotCounts build_run_slots(int64_t A, int64_t R, int32_t* arc_src, int32_t* run_slot,
-                           cudaStream_t st);
+                           cudaStream_t st, const int32_t* vtx_run_off = nullptr,
+                           int32_t n = 0);
 void launch_xor_combine(const uint64_t* parts, int nparts, int64_t n,
                         uint64_t* out, cudaStream_t st);
 void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
@@ -206,6 +209,30 @@ void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges
 // Synchronizes `st`.
 void device_finalize(uint64_t* d_acc, int64_t n, int64_t sink, cudaStream_t st,
                      uint64_t* checksum, int64_t* flagged);
+
+// Temporal sieve over GF(2^8 / 2^16 / 2^32) (small_field.cu): points
+// [pb, pe) in batches of W, XORed (zero-extended) into acc; the vertex list
+// (head, start, count, nv) is build_vertex_list's.
+struct SmallFieldArgs {
+  int bits = 32;
+  DevGraph g;
+  const int32_t* head = nullptr;
+  const int64_t* start = nullptr;
+  const int32_t* count = nullptr;
+  int64_t nv = 0;
+  const int32_t* off = nullptr;     // shade CSR (device)
+  const int32_t* shades = nullptr;
+  int k = 0;
+  uint64_t seed = 1;
+  int32_t anchor = -1;
+  int32_t max_ts = 0;
+  uint64_t pb = 0, pe = 0;
+  int W = 1;
+  uint64_t* acc = nullptr;
+  std::function<void*(size_t)> alloc;
+  std::function<void(void*)> release;
+};
+void launch_small_field(const SmallFieldArgs& a, cudaStream_t st);
 
 void prof_begin(const char* name, cudaStream_t st);
 void prof_end(cudaStream_t st);

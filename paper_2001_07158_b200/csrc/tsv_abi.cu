@@ -272,14 +272,16 @@ const T* own_upload(tsv_graph* g, const std::vector<T>& v) {
   return p;
 }
 
-void check_config(const tsv_config* cfg) {
+// small_ok: the entry point evaluates GF(2^8 / 2^16 / 2^32) too (the
+// temporal sieve, small_field.cu); the others are GF(2^64) only.
+void check_config(const tsv_config* cfg, bool small_ok = false) {
   if (!cfg) throw std::invalid_argument("null config");
   if (cfg->field_bits != 8 && cfg->field_bits != 16 && cfg->field_bits != 32 &&
       cfg->field_bits != 64)
     throw std::invalid_argument("field_bits must be 8, 16, 32 or 64");
-  if (cfg->field_bits != 64)
+  if (cfg->field_bits != 64 && !small_ok)
     throw std::invalid_argument(
-        "the B200 engine evaluates GF(2^64) only (field_bits must be 64)");
+        "field_bits 8/16/32 are evaluated by the temporal sieve only (this sieve is GF(2^64))");
   const int W = cfg->lane_width;
   if (W < 1 || W > 256 || (W & (W - 1)))
     throw std::invalid_argument("lane_width must be a power of two in [1,256]");
@@ -387,6 +389,11 @@ struct VcSpec {
 };
 
 std::shared_ptr<tsv_graph> shaded_subgraph(const tsv_graph* g, const tsv_shades* sh);
+tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                              const int32_t* ts, bool directed, int32_t t, int device,
+                              bool canonical, bool on_device = false,
+                              const int32_t* eps = nullptr, const int32_t* delays = nullptr,
+                              int model = 0, bool force_last_runs = false);
 void copy_to_host(void* dst, const void* d_src, size_t bytes, cudaStream_t st);
 void copy_to_device(void* d_dst, const void* src, size_t bytes, cudaStream_t st);
 
@@ -538,17 +545,59 @@ bool vertex_applicable(const tsv_graph* g, cudaStream_t st) {
   return true;
 }
 
+// Time-window plan of a coefficient evaluation whose state rows do not fit
+// (coef_window.cu): the shaded edges with ts <= max_ts in canonical order
+// (ts-major, so a window is a contiguous range), split between distinct
+// timestamps into windows of at most `rows_cap` arcs.
+struct WindowPlan {
+  int64_t m = 0;                 // kept edges
+  std::unique_ptr<DevBuf> ku, kv, kts, koid;  // kept canonical edges, original edge ids
+  std::vector<int64_t> bounds;   // window w = edges [bounds[w], bounds[w+1])
+};
+
+// Splits [0, m) into windows of at most cap arcs (arcs_per_edge per edge),
+// boundaries moved down to the start of their timestamp group.  Returns
+// false when one timestamp alone exceeds the cap.
+bool plan_windows(const int32_t* d_ts, int64_t m, int arcs_per_edge, int64_t cap,
+                  std::vector<int64_t>& bounds, cudaStream_t st) {
+  const int64_t cap_e = std::max<int64_t>(cap / arcs_per_edge, 1);
+  int64_t nw = std::max<int64_t>((m + cap_e - 1) / cap_e, 1);
+  for (int attempt = 0; attempt < 16; ++attempt, nw = nw + nw / 4 + 1) {
+    bounds.assign(1, 0);
+    if (nw > 1) {
+      std::vector<int64_t> pos(static_cast<size_t>(nw - 1)), got(pos.size());
+      for (int64_t w = 1; w < nw; ++w) pos[w - 1] = w * m / nw;
+      DevBuf dp(pos.size() * 8, st), dg(pos.size() * 8, st);
+      TSV_CUDA(cudaMemcpyAsync(dp.p, pos.data(), pos.size() * 8, cudaMemcpyHostToDevice, st));
+      tsv::launch_ts_group_start(d_ts, dp.as<int64_t>(), static_cast<int>(pos.size()),
+                                 dg.as<int64_t>(), st);
+      TSV_CUDA(cudaMemcpyAsync(got.data(), dg.p, got.size() * 8, cudaMemcpyDeviceToHost, st));
+      TSV_CUDA(cudaStreamSynchronize(st));
+      for (int64_t x : got)
+        if (x > bounds.back()) bounds.push_back(x);
+    }
+    bounds.push_back(m);
+    bool ok = true;
+    for (size_t w = 0; w + 1 < bounds.size(); ++w)
+      ok = ok && (bounds[w + 1] - bounds[w]) <= cap_e;
+    if (ok) return true;
+  }
+  return false;
+}
+
 // The coefficient (top-degree) engine, coef_kernels.cu: the XOR over ALL
 // 2^k sieve points in one pass per level, bit-identical to the point engine.
-// Used for full-range evaluations when its working set (two S x M state
-// buffers, M = max_l C(k, l)) fits; TSV_ENGINE=points disables it.
-// Returns false (nothing launched) when not applicable.
+// Used for full-range evaluations; when its working set (two state buffers
+// of S rows) does not fit, the arcs run in time windows (coef_window.cu).
+// TSV_ENGINE=points disables it.  Returns false (nothing launched) when not
+// applicable.
 bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                const tsv_config* cfg, int32_t anchor_source, uint64_t* d_acc, cudaStream_t st,
                uint64_t* peak_out, const VcSpec* vc) {
   const char* eng = std::getenv("TSV_ENGINE");
   if (eng && std::strcmp(eng, "points") == 0) return false;
   if (k < 2 || k > 12) return false;  // C(k, l) <= tsv::kZAcc
+  const tsv_graph* g0 = g;  // the caller's graph (time windows restrict it)
   // arcs touching a shadeless vertex never carry a nonzero product (its z,
   // hence every S row, is zero): evaluate the shaded subgraph, which keeps
   // the vertex and edge ids (y draws) and gives the same accumulators
@@ -558,14 +607,118 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     if (sub_hold) g = sub_hold.get();
   }
   const tsv::CoefTables& T = coef_const_tables(k);
-  int64_t M = 1;
-  for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, T.count[l]);
+  const uint64_t n = static_cast<uint64_t>(g->dev.n);
+  // item-stream kernel (coef_items.cu) unless the vertex-ordered sieve's
+  // positional z (no shade structure) or TSV_ITEMS=0
+  // (measured: C3/C4, all single-shade, 1.3x faster; C5, no single-shade
+  // vertex, 1.2x slower than k_coef_arcs)
+  const char* it_env = std::getenv("TSV_ITEMS");
+  bool use_items = !vc && !(it_env && std::strcmp(it_env, "0") == 0) &&
+                   ((it_env && std::strcmp(it_env, "1") == 0) || sh->single * 4 >= n);
+  // U-row entries of level l (2..k-1) per vertex class, and the row stride:
+  // rows of multi-shade heads hold their U row, then (z map in place) their
+  // S row; without multi-shade rows a row is just the U frame (the single-
+  // shade compact frame C(k-1, l-1) in the item-stream layout)
+  const bool multi_rows = vc || sh->multi > 0;
+  auto fr_multi = [&](int l) { return static_cast<int>(T.count[l - 1]); };
+  auto fr_single = [&](int l) {
+    return use_items ? static_cast<int>(T.count[l - 1] * (k - l + 1) / k) : fr_multi(l);
+  };
+  auto rs = [&](int l) {
+    return multi_rows ? static_cast<int>(std::max(T.count[l - 1], T.count[l]))
+                      : (sh->single ? fr_single(l) : fr_multi(l));
+  };
+  int64_t M = 1;  // largest row stride; the chunk aggregates take C(k, l-1)
+  int64_t MA = 1;
+  for (int l = 2; l < k; ++l) M = std::max<int64_t>(M, rs(l));
+  for (int l = 2; l <= k; ++l) MA = std::max<int64_t>(MA, T.count[l - 1]);
   const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
   const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
-  const uint64_t n = static_cast<uint64_t>(g->dev.n);
-  const uint64_t words = 2 * S * M + C * M + 2 * n * k + 2 * n + S + (n + S) / 8 + 2;
-  if (words > cfg->memory_cap_words || !fits_device(words)) return false;
-  if (peak_out) *peak_out = words;
+  const uint64_t words = 2 * S * M + C * MA + 2 * n * k + 2 * n + S + (n + S) / 8 + 2;
+  const bool fits = words <= cfg->memory_cap_words && fits_device(words);
+  // time windows (coef_window.cu) when the state rows do not fit at once:
+  // instant edge model, shade structure (not the VC sieve's positional z)
+  const char* win_env = std::getenv("TSV_WINDOW_ROWS");  // (tests: force windows of <= N arcs)
+  const int64_t force_rows = win_env ? std::atoll(win_env) : 0;
+  const bool windowed = (!fits || force_rows > 0) && !vc && g0->model == 0;
+  if (!fits && !windowed) return false;
+  if (windowed && !use_items) {  // (the carried prefix is read by the item-stream kernels)
+    use_items = true;
+    M = 1;
+    for (int l = 2; l < k; ++l) M = std::max<int64_t>(M, rs(l));
+  }
+  WindowPlan wp;
+  std::vector<int64_t> cs_words(static_cast<size_t>(k) + 1, 0);  // carry stride per level
+  int64_t rows_cap = static_cast<int64_t>(S);
+  uint64_t fixed_words = 0;
+  if (windowed) {
+    for (int l = 2; l < k; ++l) cs_words[l] = multi_rows ? fr_multi(l) : fr_single(l);
+    for (int l = 2; l < k; ++l) fixed_words += n * static_cast<uint64_t>(cs_words[l]) + n / 8 + 1;
+    const uint64_t m0 = static_cast<uint64_t>(g0->m);
+    fixed_words += 2 * n * k + 2 * n + 2 * m0 + (g0->d_eu ? 0 : 2 * m0);
+    // per row (window arc): two state rows, flags, z-map list, the window
+    // graph and its build temporaries (~80 bytes per edge)
+    const uint64_t per_row = 2 * static_cast<uint64_t>(M) + 12;
+    const uint64_t budget = std::min<uint64_t>(cfg->memory_cap_words, device_budget_words());
+    if (budget <= fixed_words + (n + 1) * per_row) return false;
+    rows_cap = static_cast<int64_t>((budget - fixed_words) / per_row) - static_cast<int64_t>(n);
+    if (force_rows > 0) rows_cap = std::min<int64_t>(rows_cap, force_rows);
+    if (rows_cap < (force_rows > 0 ? 16 : 1024)) return false;
+    // the shaded edges of the caller's graph with ts <= max_ts, original ids
+    const int64_t m = g0->m;
+    std::vector<void*> tmp;
+    auto alloc = [&](size_t bytes) -> void* {
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+        throw CudaError("time windows: out of device memory");
+      tmp.push_back(p);
+      return p;
+    };
+    auto release = [&](void* p) {
+      auto it = std::find(tmp.begin(), tmp.end(), p);
+      if (it != tmp.end()) tmp.erase(it);
+      cudaFreeAsync(p, st);
+    };
+    try {
+      const int32_t *eu = g0->d_eu, *ev = g0->d_ev, *ets = g0->d_ets;
+      if (!eu) {
+        auto* a = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        auto* b = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        auto* c = static_cast<int32_t*>(alloc(std::max<int64_t>(m, 1) * 4));
+        if (g0->edges_in_layout) {
+          tsv::edges_from_layout(g0->dev, g0->host.directed, a, b, c, st);
+        } else if (m) {
+          TSV_CUDA(cudaMemcpyAsync(a, g0->host.eu.data(), m * 4, cudaMemcpyHostToDevice, st));
+          TSV_CUDA(cudaMemcpyAsync(b, g0->host.ev.data(), m * 4, cudaMemcpyHostToDevice, st));
+          TSV_CUDA(cudaMemcpyAsync(c, g0->host.ets.data(), m * 4, cudaMemcpyHostToDevice, st));
+        }
+        eu = a;
+        ev = b;
+        ets = c;
+      }
+      auto* keep = static_cast<uint8_t*>(alloc(std::max<uint64_t>(n, 1)));
+      tsv::launch_shaded_mask(static_cast<int32_t>(n), sh->off, keep, st);
+      const size_t eb = static_cast<size_t>(std::max<int64_t>(m, 1)) * 4;
+      wp.ku = std::make_unique<DevBuf>(eb, st);
+      wp.kv = std::make_unique<DevBuf>(eb, st);
+      wp.kts = std::make_unique<DevBuf>(eb, st);
+      wp.koid = std::make_unique<DevBuf>(eb, st);
+      wp.m = tsv::device_restrict(eu, ev, ets, m, keep, max_ts, wp.ku->as<int32_t>(),
+                                  wp.kv->as<int32_t>(), wp.kts->as<int32_t>(), st, alloc, release,
+                                  wp.koid->as<int32_t>());
+      for (void* p : tmp) cudaFreeAsync(p, st);
+      tmp.clear();
+    } catch (...) {
+      for (void* p : tmp) cudaFreeAsync(p, st);
+      throw;
+    }
+    if (!plan_windows(wp.kts->as<int32_t>(), wp.m, g0->host.directed ? 1 : 2, rows_cap,
+                      wp.bounds, st))
+      return false;
+    if (peak_out) *peak_out = fixed_words + (static_cast<uint64_t>(rows_cap) + n) * per_row;
+  } else if (peak_out) {
+    *peak_out = words;
+  }
   const int32_t nn = g->dev.n;
   int dev = 0, sms = 148;
   TSV_CUDA(cudaGetDevice(&dev));
@@ -589,46 +742,35 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     scale = tsv::gf_det_host(W.data(), k);
     tsv::launch_zj_ident(nn, k, cfg->seed, sh->off, sh->shades, d_zj.as<uint64_t>(), st);
   }
-  DevBuf X(S * M * 8, st), Y(S * M * 8, st), agg(C * M * 8, st);
+  // state rows: S slots, or per window its slots plus n carry slots
+  const uint64_t rows = windowed ? static_cast<uint64_t>(rows_cap) + n : S;
+  DevBuf X(rows * M * 8, st), Y(rows * M * 8, st);
   DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(std::getenv("TSV_ZTRANS") ? S * 4 : 8, st);
   // zero skipping and the single-shade form (CoefParams::vsh); positional z
   // keeps the plain z map
   DevBuf vsh(std::max<uint64_t>(n, 1), st), vsv(std::max<uint64_t>(n, 1) * 8, st);
-  DevBuf fl0(S, st), fl1(S, st);
+  DevBuf fl0(rows, st), fl1(rows, st);
   if (!vc) tsv::launch_vshade(nn, k, d_zj.as<uint64_t>(), vsh.as<int8_t>(), vsv.as<uint64_t>(), st);
   TSV_CUDA(cudaMemsetAsync(ulast.p, 0, std::max<uint64_t>(n, 1) * k * 8, st));
-  // item-stream kernel (coef_items.cu) unless the vertex-ordered sieve's
-  // positional z (no shade structure) or TSV_ITEMS=0
-  const char* it_env = std::getenv("TSV_ITEMS");
-  // (measured: C3/C4, all single-shade, 1.3x faster; C5, no single-shade
-  // vertex, 1.2x slower than k_coef_arcs)
-  const bool use_items = !vc && !(it_env && std::strcmp(it_env, "0") == 0) &&
-                         ((it_env && std::strcmp(it_env, "1") == 0) || sh->single * 4 >= n);
   // the index tables depend on (k, use_items) only: uploaded once per device
   const CoefConst& cc = coef_const(dev, k, use_items);
   const std::vector<size_t>&poff = cc.poff, &joff = cc.joff, &moff = cc.moff, &icoff = cc.icoff;
   // multi-shade rows: the direct z map over a (slot, head) list, or
   // (TSV_ZTRANS=tab) the warp-per-window table map over slot_head
   const char* zt_env = std::getenv("TSV_ZTRANS");
-  const bool zt_tab = zt_env && std::strcmp(zt_env, "tab") == 0;
-  DevBuf mlist(S * 8, st), mcount(4, st);
+  const bool zt_tab = zt_env && std::strcmp(zt_env, "tab") == 0 && !windowed;
+  DevBuf mlist(rows * 8, st), mcount(4, st);
   // expected listed rows: slots x the multi-shade share of the shaded vertices
   const int64_t rows_hint =
-      vc ? static_cast<int64_t>(S)
-         : static_cast<int64_t>(static_cast<double>(S) * static_cast<double>(sh->multi) /
+      vc ? static_cast<int64_t>(rows)
+         : static_cast<int64_t>(static_cast<double>(rows) * static_cast<double>(sh->multi) /
                                 static_cast<double>(std::max<int64_t>(sh->multi + sh->single, 1)));
-  if (zt_tab)
-    tsv::launch_slot_head(g->dev.R, g->dev.run_slot, g->dev.run_head, slot_head.as<int32_t>(), st);
-  else if (k > 2)
-    tsv::launch_multi_slots(g->dev.R, g->dev.run_slot, g->dev.run_head,
-                            vc ? nullptr : vsh.as<int8_t>(), mlist.as<int2>(),
-                            mcount.as<int32_t>(), st);
   const int2* dp = cc.pairs;
   // every shaded vertex multi-shade and small k (k-TempPath, C5): the
   // vertex-lane engine (coef_vertex.cu) -- fused z map and readout
   const char* vx_env = std::getenv("TSV_VERTEX");
-  const bool try_vertex = !vc && sh->single == 0 && tsv::vertex_engine_supports(k) &&
-                          !(vx_env && vx_env[0] == '0');
+  const bool try_vertex = !vc && !windowed && sh->single == 0 &&
+                          tsv::vertex_engine_supports(k) && !(vx_env && vx_env[0] == '0');
   if (try_vertex && vertex_applicable(g, st)) {
     const tsv::VertList* vl = &vertex_part(g, 0, 1, st).vl;
     uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
@@ -650,94 +792,225 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     }
     return true;
   }
-  // row strides: level l's rows hold its U row (C(k, l-1)) and then its S row (C(k, l))
-  auto rs = [&](int l) { return static_cast<int>(std::max(T.count[l - 1], T.count[l])); };
-  uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
-  uint8_t *fa = fl0.as<uint8_t>(), *fb = fl1.as<uint8_t>();
-  // chunk counters of the persistent item kernel, one per level
+  // chunk counters of the persistent item kernel, one per level and window
   const char* ps_env = std::getenv("TSV_PERSIST");
   const bool persist = !(ps_env && std::strcmp(ps_env, "0") == 0);
-  DevBuf ctrs(static_cast<size_t>(k + 1) * 4, st);
-  if (persist) TSV_CUDA(cudaMemsetAsync(ctrs.p, 0, static_cast<size_t>(k + 1) * 4, st));
-  for (int l = 2; l <= k; ++l) {
-    tsv::CoefParams cp;
-    cp.g = g->dev;
-    cp.zj = d_zj.as<uint64_t>();
-    cp.k = k;
-    cp.ell = l;
-    cp.last = l == k;
-    cp.seed = cfg->seed;
-    cp.anchor_source = anchor_source;
-    cp.E = static_cast<int>(T.count[l - 1]);
-    cp.s_prev = A;
-    cp.rs_in = l > 2 ? rs(l - 1) : 0;
-    cp.ubuf = B;
-    cp.rs_out = l < k ? rs(l) : 0;
-    cp.agg = agg.as<uint64_t>();
-    cp.ulast = ulast.as<uint64_t>();
-    cp.max_ts = max_ts;
-    cp.vsh = vc ? nullptr : vsh.as<int8_t>();
-    cp.vsv = vc ? nullptr : vsv.as<uint64_t>();
-    cp.sflag = fa;
-    cp.sflag_out = fb;
-    cp.smap = l > 2 ? cc.maps + moff[l - 1] : nullptr;
-    cp.chunk_ctr = persist ? ctrs.as<int32_t>() + l : nullptr;
-    cp.sms = sms;
-    if (use_items) {
-      const int K1 = k + 1;
-      cp.items = dp;  // offsets are absolute in d_pairs
-      cp.item_off = cc.maps + icoff[l];
-      cp.item_cnt = cp.item_off + K1 * K1;
-      cp.item_omask = cc.omask + cc.omoff[l];
-      cp.frame_multi = static_cast<int>(T.count[l - 1]);
-      cp.frame_single = static_cast<int>(T.count[l - 1] * (k - l + 1) / k);  // C(k-1, l-1)
-      cp.frame_max = sh->multi ? cp.frame_multi : cp.frame_single;
-      cp.warp_words = tsv::GfTable::kWords + (cp.frame_max + 31) / 32 * 32;
+  const size_t nwin = windowed ? wp.bounds.size() - 1 : 1;
+  DevBuf ctrs(static_cast<size_t>(k + 1) * nwin * 4, st);
+  if (persist) TSV_CUDA(cudaMemsetAsync(ctrs.p, 0, static_cast<size_t>(k + 1) * nwin * 4, st));
+  // carries of the windowed form: per level l < k, the U rows of every
+  // vertex as of the window start (stride cs_words[l]) and a nonzero flag
+  std::vector<std::unique_ptr<DevBuf>> carry(static_cast<size_t>(k) + 1),
+      cnz(static_cast<size_t>(k) + 1);
+  DevBuf cmlist(windowed ? std::max<uint64_t>(n, 1) * 8 : 8, st), cmcount(4, st);
+  if (windowed) {
+    for (int l = 2; l < k; ++l) {
+      carry[l] = std::make_unique<DevBuf>(std::max<uint64_t>(n, 1) * cs_words[l] * 8, st);
+      cnz[l] = std::make_unique<DevBuf>(std::max<uint64_t>(n, 1), st);
+      TSV_CUDA(cudaMemsetAsync(cnz[l]->p, 0, std::max<uint64_t>(n, 1), st));
     }
-    if (vc) {
-      cp.vc_color = vc->d_colors;
-      cp.vc_head = vc->order[l - 1];
-      cp.vc_tail = vc->order[l - 2];
-      cp.vc_wild = vc->wild;
-    }
-    if (!cp.last) TSV_CUDA(cudaMemsetAsync(fb, 0, S, st));
-    if (use_items) {
-      tsv::launch_coef_items(cp, st);
-    } else {
-      for (int e0 = 0; e0 < cp.E; e0 += tsv::kCoefSlice) {
-        cp.e0 = e0;
-        cp.ne = std::min(tsv::kCoefSlice, cp.E - e0);
-        tsv::launch_coef_arcs(cp, st);
-      }
-    }
-    if (cp.last) {
-      tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k],
-                               scale, use_items ? cp.vsh : nullptr,
-                               use_items ? cp.vsv : nullptr, d_acc, st);
-    } else {
-      tsv::launch_coef_fixup(cp, st);
-      if (zt_tab)
-        tsv::launch_coef_ztrans(g->dev.S, static_cast<int>(T.count[l]), l,
-                                slot_head.as<int32_t>(), d_zj.as<uint64_t>(), k, cp.E, B, rs(l),
-                                dp + joff[l], cp.vsh, fb, sms, st);
-      else
-        tsv::launch_coef_ztrans_direct(g->dev.S, static_cast<int>(T.count[l]), l,
-                                       mlist.as<int2>(), mcount.as<int32_t>(),
-                                       d_zj.as<uint64_t>(), k, B, rs(l), dp + poff[l],
-                                       vc ? nullptr : fb, sms, rows_hint, st);
-      std::swap(A, B);
-      std::swap(fa, fb);
-    }
-    TSV_CUDA(cudaGetLastError());
   }
+  for (size_t w = 0; w < nwin; ++w) {
+    // the graph of this pass: the whole (shaded) graph, or the window's edges
+    // with their original ids, every vertex's last run given a slot, and the
+    // arcs without a source in the window reading the tail's carry slot
+    std::unique_ptr<tsv_graph> gw;
+    tsv::DevGraph dg = g->dev;
+    int64_t Sw = 0;
+    if (windowed) {
+      const int64_t e0 = wp.bounds[w], e1 = wp.bounds[w + 1];
+      TSV_CUDA(cudaStreamSynchronize(st));
+      gw.reset(device_graph_build(nn, e1 - e0, wp.ku->as<int32_t>() + e0,
+                                  wp.kv->as<int32_t>() + e0, wp.kts->as<int32_t>() + e0,
+                                  g0->host.directed, g0->host.t, g0->device, /*canonical=*/true,
+                                  /*on_device=*/true, nullptr, nullptr, 0,
+                                  /*force_last_runs=*/true));
+      tsv::launch_win_edge_ids(gw->dev.A, const_cast<uint32_t*>(gw->dev.arc_meta),
+                               wp.koid->as<int32_t>(), e0, st);
+      Sw = gw->dev.S;
+      tsv::launch_win_src(gw->dev.A, const_cast<int32_t*>(gw->dev.arc_src), gw->dev.arc_tail, Sw,
+                          st);
+      dg = gw->dev;
+      dg.S = Sw + static_cast<int64_t>(n);
+      tsv::launch_win_multi_list(nn, Sw, vsh.as<int8_t>(), cmlist.as<int2>(),
+                                 cmcount.as<int32_t>(), st);
+    }
+    const uint64_t Cw = static_cast<uint64_t>(std::max<int64_t>(dg.C, 1));
+    DevBuf agg(Cw * MA * 8, st);
+    if (zt_tab)
+      tsv::launch_slot_head(dg.R, dg.run_slot, dg.run_head, slot_head.as<int32_t>(), st);
+    else if (k > 2)
+      tsv::launch_multi_slots(dg.R, dg.run_slot, dg.run_head, vc ? nullptr : vsh.as<int8_t>(),
+                              mlist.as<int2>(), mcount.as<int32_t>(), st);
+    uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
+    uint8_t *fa = fl0.as<uint8_t>(), *fb = fl1.as<uint8_t>();
+    const uint64_t S_pass = static_cast<uint64_t>(std::max<int64_t>(dg.S, 1));
+    for (int l = 2; l <= k; ++l) {
+      tsv::CoefParams cp;
+      cp.g = dg;
+      cp.zj = d_zj.as<uint64_t>();
+      cp.k = k;
+      cp.ell = l;
+      cp.last = l == k;
+      cp.seed = cfg->seed;
+      cp.anchor_source = anchor_source;
+      cp.E = static_cast<int>(T.count[l - 1]);
+      cp.s_prev = A;
+      cp.rs_in = l > 2 ? rs(l - 1) : 0;
+      cp.ubuf = B;
+      cp.rs_out = l < k ? rs(l) : 0;
+      cp.agg = agg.as<uint64_t>();
+      cp.ulast = ulast.as<uint64_t>();
+      cp.max_ts = max_ts;
+      cp.vsh = vc ? nullptr : vsh.as<int8_t>();
+      cp.vsv = vc ? nullptr : vsv.as<uint64_t>();
+      cp.sflag = fa;
+      cp.sflag_out = fb;
+      cp.smap = l > 2 ? cc.maps + moff[l - 1] : nullptr;
+      cp.chunk_ctr = persist ? ctrs.as<int32_t>() + w * (k + 1) + l : nullptr;
+      cp.sms = sms;
+      if (use_items) {
+        const int K1 = k + 1;
+        cp.items = dp;  // offsets are absolute in d_pairs
+        cp.item_off = cc.maps + icoff[l];
+        cp.item_cnt = cp.item_off + K1 * K1;
+        cp.item_omask = cc.omask + cc.omoff[l];
+        cp.frame_multi = static_cast<int>(T.count[l - 1]);
+        cp.frame_single = static_cast<int>(T.count[l - 1] * (k - l + 1) / k);  // C(k-1, l-1)
+        cp.frame_max = sh->multi ? cp.frame_multi : cp.frame_single;
+        cp.warp_words = tsv::GfTable::kWords + (cp.frame_max + 31) / 32 * 32;
+      }
+      if (windowed && !cp.last) {
+        cp.carry_in = carry[l]->as<uint64_t>();
+        cp.carry_nz = cnz[l]->as<uint8_t>();
+        cp.carry_cs = static_cast<int>(cs_words[l]);
+      }
+      if (vc) {
+        cp.vc_color = vc->d_colors;
+        cp.vc_head = vc->order[l - 1];
+        cp.vc_tail = vc->order[l - 2];
+        cp.vc_wild = vc->wild;
+      }
+      if (!cp.last) TSV_CUDA(cudaMemsetAsync(fb, 0, S_pass, st));
+      if (use_items) {
+        tsv::launch_coef_items(cp, st);
+      } else {
+        for (int e0 = 0; e0 < cp.E; e0 += tsv::kCoefSlice) {
+          cp.e0 = e0;
+          cp.ne = std::min(tsv::kCoefSlice, cp.E - e0);
+          tsv::launch_coef_arcs(cp, st);
+        }
+      }
+      if (!cp.last) {
+        tsv::launch_coef_fixup(cp, st);
+        if (windowed) {
+          tsv::WinCarryArgs wa;
+          wa.run_slot = dg.run_slot;
+          wa.vro = dg.vtx_run_off;
+          wa.n = nn;
+          wa.Sw = Sw;
+          wa.vsh = vsh.as<int8_t>();
+          wa.frs = fr_single(l);
+          wa.frm = fr_multi(l);
+          wa.rows = B;
+          wa.rs = rs(l);
+          wa.sflag = fb;
+          wa.carry = carry[l]->as<uint64_t>();
+          wa.cs = static_cast<int>(cs_words[l]);
+          wa.cnz = cnz[l]->as<uint8_t>();
+          tsv::launch_win_carry(wa, st);
+        }
+        if (zt_tab) {
+          tsv::launch_coef_ztrans(dg.S, static_cast<int>(T.count[l]), l, slot_head.as<int32_t>(),
+                                  d_zj.as<uint64_t>(), k, cp.E, B, rs(l), dp + joff[l], cp.vsh, fb,
+                                  sms, st);
+        } else {
+          tsv::launch_coef_ztrans_direct(dg.S, static_cast<int>(T.count[l]), l, mlist.as<int2>(),
+                                         mcount.as<int32_t>(), d_zj.as<uint64_t>(), k, B, rs(l),
+                                         dp + poff[l], vc ? nullptr : fb, sms, rows_hint, st);
+          if (windowed && sh->multi)
+            tsv::launch_coef_ztrans_direct(static_cast<int64_t>(n), static_cast<int>(T.count[l]),
+                                           l, cmlist.as<int2>(), cmcount.as<int32_t>(),
+                                           d_zj.as<uint64_t>(), k, B, rs(l), dp + poff[l], fb,
+                                           sms, sh->multi, st);
+        }
+        std::swap(A, B);
+        std::swap(fa, fb);
+      }
+      TSV_CUDA(cudaGetLastError());
+    }
+    if (gw) TSV_CUDA(cudaStreamSynchronize(st));  // the window graph is freed next
+  }
+  tsv::launch_coef_readout(nn, d_zj.as<uint64_t>(), k, ulast.as<uint64_t>(), dp + poff[k], scale,
+                           use_items ? vsh.as<int8_t>() : nullptr,
+                           use_items ? vsv.as<uint64_t>() : nullptr, d_acc, st);
+  TSV_CUDA(cudaGetLastError());
   return true;
+}
+
+// GF(2^8 / 2^16 / 2^32) temporal sieve (small_field.cu): the point form, one
+// thread per (head vertex, point), batches of W points.
+void eval_small_field(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
+                      const tsv_config* cfg, int32_t anchor_source, uint64_t p_begin,
+                      uint64_t p_end, uint64_t* d_acc, cudaStream_t st, uint64_t* peak_out) {
+  std::vector<void*> live;
+  auto alloc = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+      throw CudaError("small-field sieve: out of device memory");
+    live.push_back(p);
+    return p;
+  };
+  auto release = [&](void* p) {
+    auto it = std::find(live.begin(), live.end(), p);
+    if (it != live.end()) live.erase(it);
+    cudaFreeAsync(p, st);
+  };
+  const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
+  const uint64_t bytes = static_cast<uint64_t>(cfg->field_bits / 8);
+  int W = static_cast<int>(std::min<uint64_t>(p_end - p_begin, 64));
+  auto words = [&](int w) { return (2 * S * w * bytes + 7) / 8 + 2 * static_cast<uint64_t>(g->dev.n); };
+  while (W > 1 && (words(W) > cfg->memory_cap_words || !fits_device(words(W)))) W >>= 1;
+  if (words(W) > cfg->memory_cap_words)
+    throw CapError("sieve memory cap exceeded: needs " + std::to_string(words(W)) +
+                   " field words, cap " + std::to_string(cfg->memory_cap_words));
+  if (peak_out) *peak_out = words(W);
+  try {
+    tsv::VertList vl;
+    if (k >= 2) tsv::build_vertex_list(g->dev, vl, st, alloc, release);
+    tsv::SmallFieldArgs a;
+    a.bits = cfg->field_bits;
+    a.g = g->dev;
+    a.head = vl.head;
+    a.start = vl.start;
+    a.count = vl.count;
+    a.nv = vl.nv;
+    a.off = sh->off;
+    a.shades = sh->shades;
+    a.k = k;
+    a.seed = cfg->seed;
+    a.anchor = anchor_source;
+    a.max_ts = max_ts;
+    a.pb = p_begin;
+    a.pe = p_end;
+    a.W = W;
+    a.acc = d_acc;
+    a.alloc = alloc;
+    a.release = release;
+    tsv::launch_small_field(a, st);
+    TSV_CUDA(cudaGetLastError());
+  } catch (...) {
+    for (void* p : live) cudaFreeAsync(p, st);
+    throw;
+  }
+  for (void* p : live) cudaFreeAsync(p, st);
 }
 
 void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
                  const tsv_config* cfg, int32_t anchor_source, uint64_t p_begin,
                  uint64_t p_end, uint64_t* d_acc, cudaStream_t st,
                  uint64_t* peak_out, const VcSpec* vc = nullptr) {
-  check_config(cfg);
+  check_config(cfg, !vc);
   if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
   if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
   if (!vc && (!sh || sh->n != g->dev.n || sh->k != k))
@@ -754,6 +1027,10 @@ void eval_device(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts
   const uint64_t P = 1ull << k;
   p_end = std::min(p_end, P);
   if (p_begin >= p_end) return;
+  if (cfg->field_bits != 64) {
+    eval_small_field(g, sh, k, max_ts, cfg, anchor_source, p_begin, p_end, d_acc, st, peak_out);
+    return;
+  }
   if (p_begin == 0 && p_end == P &&
       eval_coef(g, sh, k, max_ts, cfg, anchor_source, d_acc, st, peak_out, vc))
     return;
@@ -901,9 +1178,8 @@ void finalize_host(int32_t n, uint64_t* acc, int32_t sink, int k, tsv_outcome* o
 // to the graph.
 tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                               const int32_t* ts, bool directed, int32_t t, int device,
-                              bool canonical, bool on_device = false,
-                              const int32_t* eps = nullptr, const int32_t* delays = nullptr,
-                              int model = 0) {
+                              bool canonical, bool on_device, const int32_t* eps,
+                              const int32_t* delays, int model, bool force_last_runs) {
   const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   DeviceGuard dg(device);
   int sm_count = 0;  // (cudaGetDeviceProperties costs milliseconds per call)
@@ -1036,7 +1312,8 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
     d.carry_list = L.carry_list;
     d.ncarry = L.ncarry;
     auto* slots = static_cast<int32_t*>(alloc(std::max<int64_t>(L.R, 1) * 4));
-    const tsv::SlotCounts sc = tsv::build_run_slots(L.A, L.R, L.arc_src, slots, st);
+    const tsv::SlotCounts sc = tsv::build_run_slots(L.A, L.R, L.arc_src, slots, st,
+                                                    force_last_runs ? L.vtx_run_off : nullptr, n);
     g->arcs_with_src = sc.arcs_with_src;
     g->runs_referenced = sc.slots;
     d.run_slot = slots;
@@ -1594,7 +1871,7 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
   return guard([&] {
     if (!g || !accumulators || !out || !vertex_off)
       throw std::invalid_argument("null argument");
-    check_config(cfg);
+    check_config(cfg, true);
     if (max_ts < 1 || max_ts > g->host.t) throw std::invalid_argument("max_ts outside [1..t]");
     if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
     const int32_t n = g->host.n;
@@ -1677,7 +1954,7 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     out->flagged = flagged;
     out->global_nonzero = flagged > 0;
     out->checksum = checksum;
-    out->fn_bound = (2.0 * k - 1.0) / std::pow(2.0, 64);
+    out->fn_bound = (2.0 * k - 1.0) / std::pow(2.0, cfg->field_bits);
     out->peak_field_words = peak;
   });
 }

@@ -146,8 +146,27 @@ def test_full_c4_sd_colorful_sampled_points(cuda_device, full_golden):
     for p in rec["points"]:
         got = summary(c.points(p["seed"], p["p_begin"], p["p_end"]))
         assert got == want(p), (p["p_begin"], p["p_end"])
+    _native.Profile.reset()
+    _native.Profile.enable(True)
     out = c.decide(1, c.g.t())
+    assert engine_ran("coef_win_carry")  # the coefficient engine in time windows
+    _native.Profile.enable(False)
     assert out.global_nonzero and out.flagged.tolist() == [c.n - 1]
+
+
+def test_full_c4_windows_equal_point_engine(cuda_device, monkeypatch):
+    """C4 at full size: the windowed coefficient engine (coef_window.cu; its
+    state rows do not fit at once) and the point engine over all 4096
+    points (pinned by the sampled blocks above) give the same accumulators
+    and checksum, at t and at a binary-search horizon."""
+    c = Cfg(4)
+    for mt in (c.g.t(), c.g.t() // 2):
+        coef = c.decide(1, mt)
+        monkeypatch.setenv("TSV_ENGINE", "points")
+        pts = c.decide(1, mt)
+        monkeypatch.delenv("TSV_ENGINE")
+        assert np.array_equal(coef.accumulators, pts.accumulators), mt
+        assert coef.checksum == pts.checksum
 
 
 def test_full_c5_ktemppath_vs_oracle(cuda_device, full_golden, monkeypatch):

@@ -282,6 +282,47 @@ def test_coefficient_engine_kernels_agree(cuda_device, monkeypatch, env):
     assert nz >= 8
 
 
+@pytest.mark.parametrize("rows,env", [(300, {}), (1200, {}), (700, {"TSV_ITEMS": "0"}),
+                                      (900, {"TSV_ITEMS": "1", "TSV_ITEMS_REG": "0"}),
+                                      (500, {"TSV_SUBGRAPH": "0"})])
+def test_time_windows_vs_oracle(cuda_device, monkeypatch, rows, env):
+    """The coefficient engine in time windows (coef_window.cu: arcs in
+    windows of consecutive timestamps, per-vertex carries of every level,
+    carry slots for sources before the window, ulast accumulated over the
+    windows) equals the oracle: single-, multi-shade and shadeless
+    vertices, horizons below t, (s,d) anchors, undirected graphs, k = 2..8,
+    item-stream and k_coef_arcs paths.  TSV_WINDOW_ROWS caps the arcs per
+    window (the engine windows by itself when the rows do not fit)."""
+    monkeypatch.setenv("TSV_WINDOW_ROWS", str(rows))
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    rng = np.random.default_rng(rows)
+    n, m, t = 150, 5000, 60
+    u = rng.integers(0, n, m)
+    v = np.where(rng.random(m) < 0.2, 0, rng.integers(0, n, m))
+    ts = rng.integers(1, t + 1, m)
+    colors = rng.integers(1, 6, n)            # color 5: shadeless vertices
+    _native.Profile.reset()
+    _native.Profile.enable(True)
+    try:
+        nz = 0
+        for motif, seed, mt, anchor, d in (([1, 2], 2, None, (-1, -1), True),
+                                           ([1, 2, 3], 4, 45, (-1, -1), True),
+                                           ([1, 1, 2, 3], 3, None, (-1, -1), True),
+                                           ([1, 2, 3, 4, 1], 8, 33, (-1, -1), True),
+                                           ([1, 1, 2, 3, 4, 2], 11, None, (-1, -1), True),
+                                           ([1, 2, 3, 4, 1, 2, 3, 4], 17, None, (-1, -1), True),
+                                           ([1, 2, 3, 4], 19, None, (3, 0), True),
+                                           ([1, 2, 3, 4, 2, 3], 23, 50, (5, 7), True),
+                                           ([1, 1, 2, 3, 4, 2], 31, 40, (-1, -1), False),
+                                           ([1, 2, 3, 4, 1], 37, None, (-1, -1), False)):
+            nz += bool(_oracle_vs_gpu(n, u, v, ts, d, colors, motif, seed, anchor, mt))
+        assert nz >= 6
+        assert _native.Profile.get("coef_win_carry")[0] > 0
+    finally:
+        _native.Profile.enable(False)
+
+
 @pytest.mark.parametrize("k", [2, 3, 4, 5])
 def test_vertex_engine_vs_oracle(cuda_device, k):
     """The vertex-lane coefficient engine (coef_vertex.cu; every shaded vertex

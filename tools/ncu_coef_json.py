@@ -23,6 +23,7 @@ KEYS = {"ncu_duration_ms": "gpu__time_duration.sum",
         "warp_inst_per_launch": "smsp__inst_executed.sum",
         "alu_pipe_pct_active": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
         "fma_pipe_pct_active": "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+        "fmaheavy_pipe_pct_elapsed": "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
         "lsu_pipe_pct_active": "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "issue_pct_active": "sm__inst_issued.avg.pct_of_peak_sustained_active",
         "warps_active_pct": "sm__warps_active.avg.pct_of_peak_sustained_active",
