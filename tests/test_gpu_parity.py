@@ -418,10 +418,51 @@ def test_argument_errors(cuda_device):
         T.eval_temporal_sieve(g, 3, 5, sh, T.SieveConfig())
     with pytest.raises(ValueError, match="field_bits"):
         T.eval_temporal_sieve(g, 3, 2, sh, T.SieveConfig(field_bits=12))
-    with pytest.raises(ValueError, match="GF\\(2\\^64\\) only"):
-        T.eval_temporal_sieve(g, 3, 2, sh, T.SieveConfig(field_bits=8))
     with pytest.raises(ValueError, match="endpoint out of range"):
         T.TemporalGraph.build(3, [(0, 4, 1)], True)
+
+
+@pytest.mark.parametrize("bits", [8, 16, 32])
+def test_small_fields_vs_reference(cuda_device, bits):
+    """GF(2^8 / 2^16 / 2^32) (small_field.cu; the reference's --field-bits,
+    tools/main.cpp:70) against the reference's own eval_temporal_sieve at the
+    same width (oracle/_ref, temporal_impl<Word> through sieve.cpp:637-649):
+    accumulators, checksum and the false-negative bound (2k-1)/2^b; small
+    fields do produce false negatives, so zero accumulators must agree too."""
+    assert O.ref_available()
+    rng = np.random.default_rng(bits)
+    nz = 0
+    try:
+        for i in range(40):
+            n, u, v, ts, d, colors, motif = synth.random_small(rng, n_max=40, m_max=200,
+                                                               t_max=12, k_max=6)
+            cu, _, ct = O.canonical_edges(n, u, v, ts, d)
+            if len(cu) == 0:
+                continue
+            tmax = int(ct.max())
+            mt = int(rng.integers(1, tmax + 1)) if i % 2 else tmax
+            anchor = (-1, -1)
+            if i % 4 == 1:
+                s_, dd = rng.choice(n, 2, replace=False)
+                anchor = (int(s_), int(dd))
+            seed = int(rng.integers(1, 1 << 40))
+            ref = O.ref_eval(n, u, v, ts, d, colors, motif, max_ts=mt, seed=seed, anchor=anchor,
+                             field_bits=bits)
+            if ref is None:
+                continue
+            g = T.TemporalGraph.build(n, (u, v, ts), d)
+            cfg = T.SieveConfig(seed=seed, field_bits=bits)
+            sh = T.build_shades(T.MotifQuery.from_multiset(motif),
+                                T.VertexColoring(colors, int(max(colors))), cfg)
+            out = T.eval_temporal_sieve(g, len(motif), mt, sh, cfg, T.AnchorSpec(*anchor))
+            assert np.array_equal(out.accumulators, ref["acc"]), (i, bits)
+            assert out.checksum == ref["checksum"]
+            assert out.fn_bound == (2 * len(motif) - 1) / 2.0 ** bits
+            assert int(out.accumulators.max(initial=0)) < (1 << bits)
+            nz += ref["nflagged"] > 0
+    finally:
+        O.ref_lib().ref_set_field_bits(64)
+    assert nz >= 5
 
 
 def test_device_points_api_shards_xor_to_full(cuda_device, golden):
