@@ -260,17 +260,24 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
     try:
         with open(os.path.join(ROOT, "profiles", f"coef_kernels_c{args.config}.json")) as f:
             prof = json.load(f)
-        if prof["config"] != args.config or args.scale != 1.0 or world != 1:
+        cscale = prof.get("capture_scale", 1.0)
+        if prof["config"] != args.config or world != 1:
             prof = None
         else:
-            prof = dict(prof["kernels"][name], capture=prof["capture"])
+            prof = dict(prof["kernels"][name], capture=prof["capture"], capture_scale=cscale)
     except Exception:
         prof = None
     if prof is not None:
-        roof["traffic"] = prof["traffic_bytes_per_launch"]
+        # a capture at another scale of the same config: per-launch DRAM
+        # bytes and instructions scaled by the arc count (both are per arc)
+        f = args.scale / prof["capture_scale"]
+        roof["traffic"] = prof["traffic_bytes_per_launch"] * f
+        if f != 1.0:
+            roof["traffic_source"] = (f"ncu --set full at scale {prof['capture_scale']:g} "
+                                      f"({prof['capture']}), x{f:g} by arcs")
         clk = sm_mhz or prof["sm_clock_ghz"] * 1e3
         peak_issue = 148 * 4 * clk * 1e6
-        ach = prof["warp_inst_per_launch"] / (roof["avg_launch_ms"] * 1e-3)
+        ach = prof["warp_inst_per_launch"] * f / (roof["avg_launch_ms"] * 1e-3)
         roof["int_pipe"] = {"bound": "issue", "unit": "warp-inst/s", "achieved": ach,
                             "peak": peak_issue, "frac": ach / peak_issue,
                             "alu_pipe_frac_ncu": prof["alu_pipe_pct_active"] / 100,

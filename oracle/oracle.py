@@ -376,8 +376,9 @@ def ref_solve_model(n, u, v, ts, eps, delays, edge_model, *args, **kw):
 
 
 def ref_solve(n, u, v, ts, directed, colors, problem, motif=(), k=0, source=-1, dest=-1,
-              seed=1, mode=0, extraction=0, preprocess=0, t=0):
+              seed=1, mode=0, extraction=0, preprocess=0, t=0, field_bits=64):
     u, v, ts = _a32(u), _a32(v), _a32(ts)
+    ref_lib().ref_set_field_bits(int(field_bits))
     buf = C.create_string_buffer(1 << 20)
     ml = len(motif)
     marr = _a32(motif) if ml else np.zeros(1, np.int32)

@@ -73,6 +73,10 @@ size_t put(char* buf, size_t cap, const std::string& s) {
 
 }  // namespace
 
+// field width of ref_eval_temporal / ref_solve (the reference's GF(2^b)
+// dispatch, sieve.cpp:637-649); 64 unless set
+static int g_field_bits = 64;
+
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -190,9 +194,6 @@ int64_t ref_build_shades(int32_t n, const int32_t* colors, const int32_t* motif,
 // eval_temporal_sieve on a graph built from raw edges with a color-multiset
 // query.  acc_out receives the n accumulators.  Returns the seconds spent in
 // eval_temporal_sieve (>= 0), -1 on error, -2 if the query is infeasible.
-// field width of ref_eval_temporal (the reference's GF(2^b) dispatch,
-// sieve.cpp:637-649); 64 unless set
-static int g_field_bits = 64;
 void ref_set_field_bits(int32_t b) { g_field_bits = b; }
 
 double ref_eval_temporal(int32_t n, int64_t m, const int32_t* u,
@@ -274,6 +275,7 @@ int64_t ref_solve(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
     req.dest = dest;
     req.config.seed = seed;
     req.config.threads = 1;
+    req.config.field_bits = g_field_bits;
     static const EdgeModel models[] = {EdgeModel::instant, EdgeModel::transition_only,
                                        EdgeModel::delay_only, EdgeModel::transition_delay};
     req.config.edge_model = models[g_model & 3];

@@ -13,11 +13,13 @@ using namespace tsieve;
 
 namespace {
 thread_local std::string g_err;
+int g_field_bits = 64;  // SieveConfig::field_bits of the solve calls below
 }
 
 extern "C" {
 
 const char* tsieve_last_error() { return g_err.c_str(); }
+void tsieve_set_field_bits(int32_t b) { g_field_bits = b; }
 
 int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
                              const int32_t* ts, const int32_t* eps, const int32_t* delays,
@@ -76,6 +78,7 @@ int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32
     req.source = source;
     req.dest = dest;
     req.config.seed = seed;
+    req.config.field_bits = g_field_bits;
     static const EdgeModel models[] = {EdgeModel::instant, EdgeModel::transition_only,
                                        EdgeModel::delay_only, EdgeModel::transition_delay};
     req.config.edge_model = models[edge_model & 3];

@@ -84,13 +84,14 @@ struct StaticLevel {
   uint64_t* out = nullptr;            // n x W, zeroed, XOR-accumulated
   uint64_t pb = 0, pe = 0;
   int ppt = 1;                        // W = 32 * ppt
+  int bits = 64;                      // field width (small_field.cuh for 8/16/32)
 };
 
 void launch_static_level(const StaticLevel& p, cudaStream_t st);
 void launch_static_base(int32_t n, const uint64_t* zj, int k, uint64_t pb, uint64_t pe, int ppt,
                         uint64_t* out, cudaStream_t st);
 void launch_static_readout(int32_t n, const uint64_t* a, const uint64_t* b, int ppt,
-                           uint64_t* acc, cudaStream_t st);
+                           uint64_t* acc, cudaStream_t st, int bits = 64);
 
 // ---- on-device graph build (build_kernels.cu) ------------------------------
 
@@ -233,6 +234,9 @@ struct SmallFieldArgs {
   std::function<void(void*)> release;
 };
 void launch_small_field(const SmallFieldArgs& a, cudaStream_t st);
+// n x k shade table z_{u,j} over GF(2^bits), bits 8/16/32, zero-extended
+void launch_small_zj64(int bits, int32_t n, int k, uint64_t seed, const int32_t* off,
+                       const int32_t* shades, uint64_t* zj, cudaStream_t st);
 
 void prof_begin(const char* name, cudaStream_t st);
 void prof_end(cudaStream_t st);

@@ -17,53 +17,10 @@
 #include "engine.hpp"
 #include "gf_device.cuh"
 #include "layout.hpp"
+#include "small_field.cuh"
 
 namespace tsv {
 namespace {
-
-template <typename Word>
-struct SmallField;
-template <>
-struct SmallField<uint8_t> {
-  static constexpr int kBits = 8;
-  static constexpr uint64_t kLow = 0x1b;
-};
-template <>
-struct SmallField<uint16_t> {
-  static constexpr int kBits = 16;
-  static constexpr uint64_t kLow = 0x2b;
-};
-template <>
-struct SmallField<uint32_t> {
-  static constexpr int kBits = 32;
-  static constexpr uint64_t kLow = 0x8d;
-};
-
-// gf::mul<Word> for b <= 32 (gf.hpp:85-97): 64-bit carry-less product (the
-// holes product of gf_device.cuh on 32-bit halves), overflow bits scanned
-// from the top and cleared with shifted copies of the modulus.
-template <typename Word>
-__device__ __forceinline__ Word smul(Word a, Word b) {
-  constexpr int nb = SmallField<Word>::kBits;
-  constexpr uint64_t poly = (uint64_t{1} << nb) | SmallField<Word>::kLow;
-  const Split4 sa = split4(a), sb = split4(b);
-  uint64_t p = mask_class(class_prod<0>(sa, sb), class_prod<1>(sa, sb), class_prod<2>(sa, sb),
-                          class_prod<3>(sa, sb));
-#pragma unroll
-  for (int bit = 2 * nb - 2; bit >= nb; --bit)
-    if ((p >> bit) & 1ull) p ^= poly << (bit - nb);
-  return static_cast<Word>(p);
-}
-
-// draw_nonzero<Word> (gf.hpp:147-153) with the (seed, role) rounds hoisted
-template <typename Word>
-__device__ __forceinline__ Word sdraw(uint64_t pre, uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t h = mix64(pre ^ (a + 0xc2b2ae3d27d4eb4full));
-  h = mix64(h ^ (b + 0x165667b19e3779f9ull));
-  h = mix64(h ^ (c + 0x27d4eb2f165667c5ull));
-  while (static_cast<Word>(h) == 0) h = mix64(h + 0x9e3779b97f4a7c15ull);
-  return static_cast<Word>(h);
-}
 
 // z_{u,j} = XOR_{d in S(u)} v_{u,d} * w_{d,j} (sieve.cpp:83-101); j, d 1-based
 template <typename Word>
@@ -204,7 +161,34 @@ void run_small(const SmallFieldArgs& a, cudaStream_t st) {
   a.release(zj);
 }
 
+template <typename Word>
+__global__ void k_small_zj64(int32_t n, int k, uint64_t pre_v, uint64_t pre_w,
+                             const int32_t* __restrict__ off, const int32_t* __restrict__ shades,
+                             uint64_t* __restrict__ zj) {
+  const int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  for (int j = 0; j < k; ++j) {
+    Word z = 0;
+    for (int32_t i = off[u]; i < off[u + 1]; ++i) {
+      const int d = shades[i];
+      z ^= smul<Word>(sdraw<Word>(pre_v, static_cast<uint64_t>(u), d, 0),
+                      sdraw<Word>(pre_w, static_cast<uint64_t>(d), j + 1, 0));
+    }
+    zj[u * k + j] = z;
+  }
+}
+
 }  // namespace
+
+void launch_small_zj64(int bits, int32_t n, int k, uint64_t seed, const int32_t* off,
+                       const int32_t* shades, uint64_t* zj, cudaStream_t st) {
+  if (n <= 0) return;
+  const uint64_t pv = draw_prefix(seed, kRoleShadeV), pw = draw_prefix(seed, kRoleShadeW);
+  const unsigned b = static_cast<unsigned>((n + 127) / 128);
+  if (bits == 8) k_small_zj64<uint8_t><<<b, 128, 0, st>>>(n, k, pv, pw, off, shades, zj);
+  else if (bits == 16) k_small_zj64<uint16_t><<<b, 128, 0, st>>>(n, k, pv, pw, off, shades, zj);
+  else k_small_zj64<uint32_t><<<b, 128, 0, st>>>(n, k, pv, pw, off, shades, zj);
+}
 
 void launch_small_field(const SmallFieldArgs& a, cudaStream_t st) {
   prof_begin("small_field", st);

@@ -15,6 +15,7 @@
 
 #include "engine.hpp"
 #include "gf_device.cuh"
+#include "small_field.cuh"
 
 namespace tsv {
 namespace {
@@ -40,7 +41,7 @@ __device__ __forceinline__ void zvals(const uint64_t* __restrict__ zj, int k, in
     if (pb + lane + 32 * p >= pe) z[p] = 0;
 }
 
-template <int PPT>
+template <int PPT, int BITS>
 __global__ void __launch_bounds__(kWarps * 32) k_static_level(const StaticLevel P) {
   constexpr int W = 32 * PPT;
   __shared__ uint64_t s_y[kWarps][32];
@@ -61,7 +62,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_static_level(const StaticLevel 
     if (lane < nb) {
       h = __ldg(P.arc_head + base + lane);
       t = __ldg(P.arc_tail + base + lane);
-      y = draw_edge_y(pre, yb, static_cast<uint32_t>(__ldg(P.arc_edge + base + lane)));
+      y = fdraw_y<BITS>(pre, yb, static_cast<uint64_t>(P.level),
+                        static_cast<uint32_t>(__ldg(P.arc_edge + base + lane)));
     }
     s_y[wib][lane] = y;
     s_head[wib][lane] = h;
@@ -81,18 +83,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_static_level(const StaticLevel 
         uint64_t z[PPT];
         zvals<PPT>(P.zj, P.k, tail, P.pb, P.pe, z);
 #pragma unroll
-        for (int p = 0; p < PPT; ++p) val[p] = P.src ? gf_mul(z[p], val[p]) : z[p];
+        for (int p = 0; p < PPT; ++p) val[p] = P.src ? fmul<BITS>(z[p], val[p]) : z[p];
       }
       const uint64_t yy = s_y[wib][i];
 #pragma unroll
-      for (int p = 0; p < PPT; ++p) acc[p] ^= gf_mul(yy, val[p]);
+      for (int p = 0; p < PPT; ++p) acc[p] ^= fmul<BITS>(yy, val[p]);
       const bool last = i + 1 >= nb || s_head[wib][i + 1] != head;  // flush per batch
       if (last) {
         if (P.head_times_z) {
           uint64_t z[PPT];
           zvals<PPT>(P.zj, P.k, head, P.pb, P.pe, z);
 #pragma unroll
-          for (int p = 0; p < PPT; ++p) acc[p] = gf_mul(z[p], acc[p]);
+          for (int p = 0; p < PPT; ++p) acc[p] = fmul<BITS>(z[p], acc[p]);
         }
 #pragma unroll
         for (int p = 0; p < PPT; ++p) {
@@ -121,7 +123,7 @@ __global__ void k_static_base(int32_t n, const uint64_t* __restrict__ zj, int k,
 }
 
 // acc[u] ^= XOR_w a[u][w] * b[u][w]  (b == nullptr: the all-ones layer)
-template <int PPT>
+template <int PPT, int BITS>
 __global__ void k_static_readout(int32_t n, const uint64_t* __restrict__ a,
                                  const uint64_t* __restrict__ b, uint64_t* __restrict__ acc) {
   const int64_t u = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -131,7 +133,7 @@ __global__ void k_static_readout(int32_t n, const uint64_t* __restrict__ a,
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     const int64_t i = u * 32 * PPT + lane + 32 * p;
-    x ^= b ? gf_mul(a[i], b[i]) : a[i];
+    x ^= b ? fmul<BITS>(a[i], b[i]) : a[i];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x ^= __shfl_xor_sync(kFull, x, o);
@@ -144,13 +146,23 @@ unsigned warps_blocks(int64_t warps) {
 
 }  // namespace
 
+template <int BITS>
+void static_level_bits(const StaticLevel& p, cudaStream_t st) {
+  if (p.ppt == 2)
+    k_static_level<2, BITS><<<warps_blocks(p.C), kWarps * 32, 0, st>>>(p);
+  else
+    k_static_level<1, BITS><<<warps_blocks(p.C), kWarps * 32, 0, st>>>(p);
+}
+
 void launch_static_level(const StaticLevel& p, cudaStream_t st) {
   if (p.C == 0) return;
   prof_begin("static_level", st);
-  if (p.ppt == 2)
-    k_static_level<2><<<warps_blocks(p.C), kWarps * 32, 0, st>>>(p);
-  else
-    k_static_level<1><<<warps_blocks(p.C), kWarps * 32, 0, st>>>(p);
+  switch (p.bits) {
+    case 8: static_level_bits<8>(p, st); break;
+    case 16: static_level_bits<16>(p, st); break;
+    case 32: static_level_bits<32>(p, st); break;
+    default: static_level_bits<64>(p, st); break;
+  }
   prof_end(st);
 }
 
@@ -165,14 +177,25 @@ void launch_static_base(int32_t n, const uint64_t* zj, int k, uint64_t pb, uint6
   prof_end(st);
 }
 
+template <int BITS>
+void static_readout_bits(int32_t n, const uint64_t* a, const uint64_t* b, int ppt, uint64_t* acc,
+                         cudaStream_t st) {
+  if (ppt == 2)
+    k_static_readout<2, BITS><<<warps_blocks(n), kWarps * 32, 0, st>>>(n, a, b, acc);
+  else
+    k_static_readout<1, BITS><<<warps_blocks(n), kWarps * 32, 0, st>>>(n, a, b, acc);
+}
+
 void launch_static_readout(int32_t n, const uint64_t* a, const uint64_t* b, int ppt,
-                           uint64_t* acc, cudaStream_t st) {
+                           uint64_t* acc, cudaStream_t st, int bits) {
   if (n == 0) return;
   prof_begin("static_readout", st);
-  if (ppt == 2)
-    k_static_readout<2><<<warps_blocks(n), kWarps * 32, 0, st>>>(n, a, b, acc);
-  else
-    k_static_readout<1><<<warps_blocks(n), kWarps * 32, 0, st>>>(n, a, b, acc);
+  switch (bits) {
+    case 8: static_readout_bits<8>(n, a, b, ppt, acc, st); break;
+    case 16: static_readout_bits<16>(n, a, b, ppt, acc, st); break;
+    case 32: static_readout_bits<32>(n, a, b, ppt, acc, st); break;
+    default: static_readout_bits<64>(n, a, b, ppt, acc, st); break;
+  }
   prof_end(st);
 }
 

@@ -597,6 +597,19 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const char* eng = std::getenv("TSV_ENGINE");
   if (eng && std::strcmp(eng, "points") == 0) return false;
   if (k < 2 || k > 12) return false;  // C(k, l) <= tsv::kZAcc
+  // TSV_TRACE_COEF=1: host microseconds per phase of this call on stderr
+  // (no synchronization added: enqueue cost and blocking calls)
+  static const bool trace = [] {
+    const char* e = std::getenv("TSV_TRACE_COEF");
+    return e && e[0] == '1';
+  }();
+  const auto tc0 = std::chrono::steady_clock::now();
+  auto tmark = [&](const char* what) {
+    if (!trace) return;
+    std::fprintf(stderr, "[coef] %-24s %9.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tc0)
+                     .count());
+  };
   const tsv_graph* g0 = g;  // the caller's graph (time windows restrict it)
   // arcs touching a shadeless vertex never carry a nonzero product (its z,
   // hence every S row, is zero): evaluate the shaded subgraph, which keeps
@@ -635,7 +648,9 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const uint64_t S = static_cast<uint64_t>(std::max<int64_t>(g->dev.S, 1));
   const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
   const uint64_t words = 2 * S * M + C * MA + 2 * n * k + 2 * n + S + (n + S) / 8 + 2;
+  tmark("tables, subgraph");
   const bool fits = words <= cfg->memory_cap_words && fits_device(words);
+  tmark("fits_device");
   // time windows (coef_window.cu) when the state rows do not fit at once:
   // instant edge model, shade structure (not the VC sieve's positional z)
   const char* win_env = std::getenv("TSV_WINDOW_ROWS");  // (tests: force windows of <= N arcs)
@@ -742,37 +757,20 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     scale = tsv::gf_det_host(W.data(), k);
     tsv::launch_zj_ident(nn, k, cfg->seed, sh->off, sh->shades, d_zj.as<uint64_t>(), st);
   }
+  tmark("shade table");
   // state rows: S slots, or per window its slots plus n carry slots
   const uint64_t rows = windowed ? static_cast<uint64_t>(rows_cap) + n : S;
   DevBuf X(rows * M * 8, st), Y(rows * M * 8, st);
-  DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(std::getenv("TSV_ZTRANS") ? S * 4 : 8, st);
-  // zero skipping and the single-shade form (CoefParams::vsh); positional z
-  // keeps the plain z map
-  DevBuf vsh(std::max<uint64_t>(n, 1), st), vsv(std::max<uint64_t>(n, 1) * 8, st);
-  DevBuf fl0(rows, st), fl1(rows, st);
-  if (!vc) tsv::launch_vshade(nn, k, d_zj.as<uint64_t>(), vsh.as<int8_t>(), vsv.as<uint64_t>(), st);
-  TSV_CUDA(cudaMemsetAsync(ulast.p, 0, std::max<uint64_t>(n, 1) * k * 8, st));
-  // the index tables depend on (k, use_items) only: uploaded once per device
-  const CoefConst& cc = coef_const(dev, k, use_items);
-  const std::vector<size_t>&poff = cc.poff, &joff = cc.joff, &moff = cc.moff, &icoff = cc.icoff;
-  // multi-shade rows: the direct z map over a (slot, head) list, or
-  // (TSV_ZTRANS=tab) the warp-per-window table map over slot_head
-  const char* zt_env = std::getenv("TSV_ZTRANS");
-  const bool zt_tab = zt_env && std::strcmp(zt_env, "tab") == 0 && !windowed;
-  DevBuf mlist(rows * 8, st), mcount(4, st);
-  // expected listed rows: slots x the multi-shade share of the shaded vertices
-  const int64_t rows_hint =
-      vc ? static_cast<int64_t>(rows)
-         : static_cast<int64_t>(static_cast<double>(rows) * static_cast<double>(sh->multi) /
-                                static_cast<double>(std::max<int64_t>(sh->multi + sh->single, 1)));
-  const int2* dp = cc.pairs;
   // every shaded vertex multi-shade and small k (k-TempPath, C5): the
-  // vertex-lane engine (coef_vertex.cu) -- fused z map and readout
+  // vertex-lane engine (coef_vertex.cu) -- fused z map and readout, so none
+  // of the buffers below (ulast, flags, z-map lists, chunk aggregates)
   const char* vx_env = std::getenv("TSV_VERTEX");
   const bool try_vertex = !vc && !windowed && sh->single == 0 &&
                           tsv::vertex_engine_supports(k) && !(vx_env && vx_env[0] == '0');
+  tmark("state buffers");
   if (try_vertex && vertex_applicable(g, st)) {
     const tsv::VertList* vl = &vertex_part(g, 0, 1, st).vl;
+    tmark("vertex list");
     uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
     for (int l = 2; l <= k; ++l) {
       tsv::CoefParams cp;
@@ -790,8 +788,31 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
       TSV_CUDA(cudaGetLastError());
       std::swap(A, B);
     }
+    tmark("levels enqueued");
     return true;
   }
+  DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(std::getenv("TSV_ZTRANS") ? S * 4 : 8, st);
+  // zero skipping and the single-shade form (CoefParams::vsh); positional z
+  // keeps the plain z map
+  DevBuf vsh(std::max<uint64_t>(n, 1), st), vsv(std::max<uint64_t>(n, 1) * 8, st);
+  DevBuf fl0(rows, st), fl1(rows, st);
+  if (!vc) tsv::launch_vshade(nn, k, d_zj.as<uint64_t>(), vsh.as<int8_t>(), vsv.as<uint64_t>(), st);
+  TSV_CUDA(cudaMemsetAsync(ulast.p, 0, std::max<uint64_t>(n, 1) * k * 8, st));
+  // the index tables depend on (k, use_items) only: uploaded once per device
+  tmark("buffers");
+  const CoefConst& cc = coef_const(dev, k, use_items);
+  const std::vector<size_t>&poff = cc.poff, &joff = cc.joff, &moff = cc.moff, &icoff = cc.icoff;
+  // multi-shade rows: the direct z map over a (slot, head) list, or
+  // (TSV_ZTRANS=tab) the warp-per-window table map over slot_head
+  const char* zt_env = std::getenv("TSV_ZTRANS");
+  const bool zt_tab = zt_env && std::strcmp(zt_env, "tab") == 0 && !windowed;
+  DevBuf mlist(rows * 8, st), mcount(4, st);
+  // expected listed rows: slots x the multi-shade share of the shaded vertices
+  const int64_t rows_hint =
+      vc ? static_cast<int64_t>(rows)
+         : static_cast<int64_t>(static_cast<double>(rows) * static_cast<double>(sh->multi) /
+                                static_cast<double>(std::max<int64_t>(sh->multi + sh->single, 1)));
+  const int2* dp = cc.pairs;
   // chunk counters of the persistent item kernel, one per level and window
   const char* ps_env = std::getenv("TSV_PERSIST");
   const bool persist = !(ps_env && std::strcmp(ps_env, "0") == 0);
@@ -2380,7 +2401,7 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
                                uint64_t* accumulators, tsv_outcome* out) {
   return guard([&] {
     if (!accumulators || !out || !vertex_off) throw std::invalid_argument("null argument");
-    check_config(cfg);
+    check_config(cfg, true);
     if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
     if (n < 0 || ms < 0) throw std::invalid_argument("negative size");
     // head-sorted arc lists of the projection: in-arcs (tail -> head) and
@@ -2464,8 +2485,12 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
         wtab[(d - 1) * k + (j - 1)] = tsv::draw_nonzero(cfg->seed, tsv::kRoleShadeW, d, j, 0);
     auto d_w = up(wtab);
     DevBuf zj(static_cast<size_t>(n) * k * 8, st), acc(static_cast<size_t>(n) * 8, st);
-    tsv::launch_zj(n, k, cfg->seed, d_off->as<int32_t>(), d_sh->as<int32_t>(),
-                   d_w->as<uint64_t>(), zj.as<uint64_t>(), st);
+    if (cfg->field_bits == 64)
+      tsv::launch_zj(n, k, cfg->seed, d_off->as<int32_t>(), d_sh->as<int32_t>(),
+                     d_w->as<uint64_t>(), zj.as<uint64_t>(), st);
+    else
+      tsv::launch_small_zj64(cfg->field_bits, n, k, cfg->seed, d_off->as<int32_t>(),
+                             d_sh->as<int32_t>(), zj.as<uint64_t>(), st);
     TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8, st));
     const size_t layer = static_cast<size_t>(n) * W;
     std::vector<std::unique_ptr<DevBuf>> ending;
@@ -2485,6 +2510,7 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
     in.role = tsv::kRoleEdgeY;
     in.head_times_z = true;
     in.ppt = ppt;
+    in.bits = cfg->field_bits;
     tsv::StaticLevel outl = in;
     outl.C = static_cast<int64_t>(oc.size()) - 1;
     outl.chunk_arc = d_oc->as<int64_t>();
@@ -2512,11 +2538,11 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
         tsv::launch_static_level(in, st);
       }
       if (!junction) {
-        tsv::launch_static_readout(n, E(k), nullptr, ppt, acc.as<uint64_t>(), st);
+        tsv::launch_static_readout(n, E(k), nullptr, ppt, acc.as<uint64_t>(), st, cfg->field_bits);
         continue;
       }
       // walks-starting family S_1 = 1, S_b from S_{b-1}; readout E_{k+1-b} * S_b
-      tsv::launch_static_readout(n, E(k), nullptr, ppt, acc.as<uint64_t>(), st);
+      tsv::launch_static_readout(n, E(k), nullptr, ppt, acc.as<uint64_t>(), st, cfg->field_bits);
       uint64_t* sp = nullptr;
       uint64_t* sc = s0.as<uint64_t>();
       for (int bb = 2; bb <= k; ++bb) {
@@ -2525,7 +2551,8 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
         outl.src = sp;
         outl.out = sc;
         tsv::launch_static_level(outl, st);
-        tsv::launch_static_readout(n, E(k + 1 - bb), sc, ppt, acc.as<uint64_t>(), st);
+        tsv::launch_static_readout(n, E(k + 1 - bb), sc, ppt, acc.as<uint64_t>(), st,
+                                   cfg->field_bits);
         sp = sc;
         sc = (sc == s0.as<uint64_t>()) ? s1.as<uint64_t>() : s0.as<uint64_t>();
       }
@@ -2537,6 +2564,7 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
     TSV_CUDA(cudaStreamSynchronize(st));
     *out = tsv_outcome{};
     finalize_host(n, accumulators, -1, k, out);
+    out->fn_bound = (2.0 * k - 1.0) / std::pow(2.0, cfg->field_bits);
     out->peak_field_words = words;
   });
 }

@@ -304,6 +304,31 @@ def test_default_preprocessing_matches_reference(cuda_device, golden):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("bits", [8, 16, 32])
+def test_solver_small_fields_match_reference(cuda_device, golden, bits):
+    """SieveConfig::field_bits 8 / 16 / 32 (the reference CLI's --field-bits,
+    tools/main.cpp:70): solve() records -- decisions, checksums, probes,
+    witnesses -- equal the reference's at the same width, with the default
+    preprocessing (junction sieve on the projection) and without; small
+    fields give false negatives, which must agree too."""
+    lib = dropin()
+    lib.tsieve_set_field_bits(bits)
+    try:
+        for c in golden["solve_sweep_preprocess"][:32]:
+            want = O.ref_solve(c["n"], c["u"], c["v"], c["ts"], c["directed"], c["colors"],
+                               c["problem"], c["motif"], c["k"], c["source"], c["dest"],
+                               seed=c["seed"], mode=c["mode"], extraction=c["extraction"],
+                               preprocess=c["preprocess"], field_bits=bits)
+            got = solve(c)
+            for key in ("decision", "certain", "optimum_ts", "checksum", "flagged", "witness",
+                        "extraction_failed", "oracle_calls", "preprocessed_n", "preprocessed_m"):
+                assert got[key] == want[key], (key, bits, c["problem"], got, want)
+    finally:
+        lib.tsieve_set_field_bits(64)
+        O.ref_lib().ref_set_field_bits(64)
+
+
+@pytest.mark.gpu
 def test_cli_reference_defaults(cuda_device, fig2, golden):
     """The reference CLI tests (test_cli.cpp:41-84) with DEFAULT flags
     (preprocess both, optimize on)."""

@@ -3,7 +3,9 @@ launches (tools/gpu_profile_coef.sh) into profiles/coef_kernels_c<config>.json,
 which bench.py reads for the roofline `traffic` and instruction-issue figures.
 Per kernel family (middle-level k_coef_arcs, k_coef_ztrans_tab, ...): launches,
 mean duration, DRAM bytes, executed warp instructions, pipe utilizations.
-Usage: python tools/ncu_coef_json.py gpurun_out/prof_<tag>.ncu-rep <config> <tag> [OUT.json]"""
+Usage: python tools/ncu_coef_json.py gpurun_out/prof_<tag>.ncu-rep <config> <tag> [OUT.json] [SCALE]
+(SCALE: the config scale the capture ran at; bench.py scales per-launch
+traffic and instructions by arcs when it runs at another scale)"""
 import csv
 import io
 import json
@@ -55,7 +57,8 @@ def family(name):
 
 def main():
     rep, config, tag = sys.argv[1], int(sys.argv[2]), sys.argv[3]
-    dest = sys.argv[4] if len(sys.argv) > 4 else None
+    dest = sys.argv[4] if len(sys.argv) > 4 and sys.argv[4] != "-" else None
+    scale = float(sys.argv[5]) if len(sys.argv) > 5 else 1.0
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -66,7 +69,8 @@ def main():
         f = family(d["Kernel Name"])
         if f:
             fams.setdefault(f, []).append(d)
-    res = {"config": config, "capture": os.path.basename(rep), "tag": tag, "kernels": {}}
+    res = {"config": config, "capture": os.path.basename(rep), "tag": tag, "capture_scale": scale,
+           "kernels": {}}
     for f, ds in fams.items():
         e = {"launches": len(ds), "kernel": ds[0]["Kernel Name"],
              "registers_per_thread": int(float(ds[0]["launch__registers_per_thread"]))}
