@@ -311,6 +311,7 @@ def test_solver_small_fields_match_reference(cuda_device, golden, bits):
     witnesses -- equal the reference's at the same width, with the default
     preprocessing (junction sieve on the projection) and without; small
     fields give false negatives, which must agree too."""
+    from oracle import oracle as O
     lib = dropin()
     lib.tsieve_set_field_bits(bits)
     try:
