@@ -302,6 +302,55 @@ def coef_roofline(coef, k, alg1, evals, hbm, peak_kind, args, world, sm_mhz):
     return roof
 
 
+def e2e_api_leg(inst, reps, steps, upd_step, gold):
+    """The same decide through the C++ drop-in API a reference user calls
+    (libtsieve: TemporalGraph::build from host vectors + solve() in decide
+    mode, --preprocess none, one call per repetition seed), host arrays in,
+    host outcome out.  The host vectors are staged outside the timed region
+    (a caller owns them); graph canonicalization, upload, shades, evaluation
+    and finalize are inside."""
+    import ctypes as C
+    lib = C.CDLL(os.path.join(ROOT, "paper_2001_07158_b200", "lib", "libtsieve.so"))
+    i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+    lib.tsieve_last_error.restype = C.c_char_p
+    lib.tsieve_e2e_stage.restype = C.c_int64
+    lib.tsieve_e2e_stage.argtypes = [C.c_int32, C.c_int64, i32p, i32p, i32p, C.c_int, i32p]
+    lib.tsieve_e2e_decide.restype = C.c_int64
+    lib.tsieve_e2e_decide.argtypes = [C.c_char_p, i32p, C.c_int32, C.c_int32, C.c_int32,
+                                      C.c_int32, C.c_uint64, C.c_int32,
+                                      np.ctypeslib.ndpointer(np.int32), np.ctypeslib.ndpointer(
+                                          np.uint64), np.ctypeslib.ndpointer(np.int64)]
+    a = lambda x: np.ascontiguousarray(np.asarray(x), dtype=np.int32)  # noqa: E731
+    u, v, ts = a(inst.u), a(inst.v), a(inst.ts)
+    colors = a(inst.colors) if inst.colors is not None else np.ones(max(inst.n, 1), np.int32)
+    motif = a(inst.motif) if inst.motif else np.zeros(1, np.int32)
+    dec = np.zeros(reps, np.int32)
+    cs = np.zeros(reps, np.uint64)
+    fl = np.zeros(reps, np.int64)
+    total = 0.0
+    for _ in range(steps):
+        if lib.tsieve_e2e_stage(inst.n, len(u), u, v, ts, int(inst.directed), colors) < 0:
+            raise RuntimeError(lib.tsieve_last_error().decode())
+        t0 = time.perf_counter()
+        r = lib.tsieve_e2e_decide(inst.problem.encode(), motif, len(inst.motif or []), inst.k,
+                                  inst.source, inst.dest, 1, reps, dec, cs, fl)
+        total += time.perf_counter() - t0
+        if r < 0:
+            raise RuntimeError(lib.tsieve_last_error().decode())
+    sec = total / steps
+    out = {"value": upd_step / sec, "unit": "updates/s", "ms_per_step": sec * 1e3,
+           "h2d_bytes_per_step": int(u.nbytes + v.nbytes + ts.nbytes),
+           "d2h_bytes_per_step": int(reps * inst.n * 8),
+           "path": ("C++ drop-in (libtsieve): TemporalGraph::build + solve(decide, "
+                    "--preprocess none, memory_cap_words 2^62 as the other legs) per "
+                    "repetition seed"),
+           "checksums": [f"{int(x):016x}" for x in cs]}
+    if gold is not None:
+        out["parity"] = all(f"{int(cs[r]):016x}" == gold[1][r]["checksum"] and
+                            int(fl[r]) == gold[1][r]["nflagged"] for r in range(reps))
+    return out
+
+
 # ------------------------------------------------------------------ CPU legs
 
 METRIC = "GF(2^64) edge x level x sieve-pt updates/s (decide)"
@@ -801,6 +850,8 @@ def main():
                         "XOR combine + D2H"),
                "parity": e2e_parity}
         del pinned, pu, pv, pt
+        if world == 1:
+            e2e["api"] = e2e_api_leg(inst, reps, e2e_steps, upd_step, gold)
 
     cpu = None
     if want_cpu:

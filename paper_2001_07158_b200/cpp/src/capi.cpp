@@ -1,11 +1,13 @@
 // capi.cpp -- a C entry point into the C++ drop-in solver, so the Python
 // tests can drive solve() on raw arrays exactly as oracle/ref_shim.cpp drives
 // the reference's (same argument meaning, same compact JSON record).
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
 #include <sstream>
 #include <string>
+#include <vector>
 
 #include "tsieve/solver.hpp"
 
@@ -121,6 +123,80 @@ int64_t tsieve_solve_json_ex(int32_t n, int64_t m, const int32_t* u, const int32
       buf[w] = 0;
     }
     return static_cast<int64_t>(s.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+// The C++ drop-in API as a reference user calls it, for the bench's e2e_api
+// leg: tsieve_e2e_stage copies raw arrays into the std::vectors a caller
+// would own (untimed); tsieve_e2e_decide then runs TemporalGraph::build on
+// them (moved in; device canonicalization for large inputs) and solve()
+// in decide mode with --preprocess none and no memory cap for seeds
+// seed0 .. seed0+reps-1 on that graph -- graph upload, shades, evaluation,
+// finalize and the host accumulators all inside.  Outputs per repetition:
+// decision, checksum.
+namespace {
+struct E2EStage {
+  int32_t n = 0;
+  bool directed = true;
+  std::vector<Vertex> u, v;
+  std::vector<Timestamp> ts;
+  std::vector<Color> colors;
+  Color q = 1;
+};
+E2EStage g_stage;
+}  // namespace
+
+int64_t tsieve_e2e_stage(int32_t n, int64_t m, const int32_t* u, const int32_t* v,
+                         const int32_t* ts, int directed, const int32_t* colors) {
+  try {
+    g_stage = E2EStage{};
+    g_stage.n = n;
+    g_stage.directed = directed != 0;
+    g_stage.u.assign(u, u + m);
+    g_stage.v.assign(v, v + m);
+    g_stage.ts.assign(ts, ts + m);
+    g_stage.colors.assign(static_cast<size_t>(n), 1);
+    for (int32_t i = 0; colors && i < n; ++i)
+      g_stage.q = std::max(g_stage.q, g_stage.colors[i] = colors[i]);
+    return m;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+int64_t tsieve_e2e_decide(const char* problem, const int32_t* motif, int32_t motif_len,
+                          int32_t k, int32_t source, int32_t dest, uint64_t seed0, int32_t reps,
+                          int32_t* decisions, uint64_t* checksums, int64_t* flagged) {
+  try {
+    TemporalGraph g = TemporalGraph::build(g_stage.n, std::move(g_stage.u), std::move(g_stage.v),
+                                           std::move(g_stage.ts), g_stage.directed);
+    VertexColoring col(g_stage.colors, g_stage.q);
+    SolveRequest req;
+    auto p = problem_from_name(problem);
+    if (!p) throw std::invalid_argument("unknown problem");
+    req.problem = *p;
+    const std::vector<Color> mcol(motif, motif + std::max(motif_len, 0));
+    req.query = motif_len > 0 ? MotifQuery::from_multiset(mcol) : MotifQuery::size_only(k);
+    req.source = source;
+    req.dest = dest;
+    req.preprocess = PreprocessLevel::none;
+    req.config.field_bits = g_field_bits;
+    // the bench's device-resident and C-ABI legs run uncapped too (the
+    // reference default of 2^31 words would send C5 to the point engine:
+    // the coefficient engine's working set is 1.4e10 words)
+    req.config.memory_cap_words = std::uint64_t{1} << 62;
+    for (int32_t r = 0; r < reps; ++r) {
+      req.config.seed = seed0 + static_cast<uint64_t>(r);
+      const SolveReport rep = solve(g, col, req, SolveMode::decide);
+      decisions[r] = rep.decision ? 1 : 0;
+      checksums[r] = rep.checksum;
+      flagged[r] = static_cast<int64_t>(rep.flagged.size());
+    }
+    return reps;
   } catch (const std::exception& e) {
     g_err = e.what();
     return -1;

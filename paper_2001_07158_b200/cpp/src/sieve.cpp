@@ -32,6 +32,12 @@ double false_negative_bound(int k, int field_bits) {
   return (2.0 * k - 1.0) / std::pow(2.0, field_bits);
 }
 
+// Shades (sieve.cpp:658-718): the query's colors in ascending order get
+// consecutive shade ids 1..k, multiplicity many each; a vertex carries the
+// shades of its primary color (plus those of the wildcard color when one is
+// active).  Every vertex's list is a run of consecutive ids, so the CSR is a
+// prefix sum of per-vertex counts, computed on all host threads (n = 1e8 at
+// C5).
 ShadeAssignment build_shades(const MotifQuery& query, const VertexColoring& coloring,
                              const SieveConfig& config) {
   check_config(config);
@@ -43,43 +49,74 @@ ShadeAssignment build_shades(const MotifQuery& query, const VertexColoring& colo
   ShadeAssignment sh;
   sh.k = query.k;
   sh.seed = config.seed;
-  const int n = coloring.n();
-  std::vector<std::int64_t> count(static_cast<size_t>(coloring.q()) + 2, 0);
-  for (Vertex x = 0; x < n; ++x) ++count[coloring.primary(x)];
-  if (coloring.wildcard_active()) count[coloring.wildcard_color()] = n;
-
+  const std::int64_t n = coloring.n();
+  const Color q = coloring.q();
+  // colors present among the primaries (every color when a wildcard is active)
+  std::vector<char> present(static_cast<size_t>(q) + 2, 0);
+  if (coloring.wildcard_active()) {
+    const Color w = coloring.wildcard_color();
+    if (w >= 0 && w < static_cast<Color>(present.size())) present[w] = 1;
+  }
+#pragma omp parallel for schedule(static) if (n > (1 << 20))
+  for (std::int64_t x = 0; x < n; ++x) {
+    const Color c = coloring.primary(static_cast<Vertex>(x));
+    if (c >= 0 && c < static_cast<Color>(present.size()) && !present[c]) present[c] = 1;
+  }
+  // per color: first shade id and how many (0: not in the query)
+  std::vector<std::int32_t> first(static_cast<size_t>(q) + 2, 0), many(first.size(), 0);
   int next = 1;
-  for (const auto& [c, mu] : query.multiset) {
+  for (const auto& [c, mu] : query.multiset) {  // std::map: ascending colors
     sh.colors.push_back(c);
-    std::vector<int> set(static_cast<size_t>(mu));
-    for (int& d : set) d = next++;
-    sh.shade_sets.push_back(std::move(set));
-    const bool present = c >= 1 && c < static_cast<Color>(count.size()) && count[c] > 0;
-    if (!present && sh.feasible) {
+    std::vector<int> ids(static_cast<size_t>(mu));
+    for (int i = 0; i < mu; ++i) ids[i] = next + i;
+    sh.shade_sets.push_back(std::move(ids));
+    if (c >= 0 && c < static_cast<Color>(first.size())) {
+      first[c] = next;
+      many[c] = mu;
+    }
+    next += mu;
+    const bool here = c >= 1 && c < static_cast<Color>(present.size()) && present[c];
+    if (!here && sh.feasible) {
       sh.feasible = false;
       sh.missing_color = c;
     }
   }
-  auto set_of = [&](Color c) -> const std::vector<int>* {
-    auto it = std::lower_bound(sh.colors.begin(), sh.colors.end(), c);
-    return (it == sh.colors.end() || *it != c) ? nullptr : &sh.shade_sets[it - sh.colors.begin()];
+  const Color wild = coloring.wildcard_active() ? coloring.wildcard_color() : -1;
+  const std::int32_t wf = wild >= 0 && wild < static_cast<Color>(first.size()) ? first[wild] : 0;
+  const std::int32_t wm = wild >= 0 && wild < static_cast<Color>(first.size()) ? many[wild] : 0;
+  auto own = [&](std::int64_t x, std::int32_t& f, std::int32_t& c) {
+    const Color col = coloring.primary(static_cast<Vertex>(x));
+    const bool in = col >= 0 && col < static_cast<Color>(first.size());
+    f = in ? first[col] : 0;
+    c = in ? many[col] : 0;
   };
   sh.vertex_off.assign(static_cast<size_t>(n) + 1, 0);
-  for (Vertex x = 0; x < n; ++x) {
-    int cnt = 0;
-    if (auto* s = set_of(coloring.primary(x))) cnt += static_cast<int>(s->size());
-    if (coloring.wildcard_active())
-      if (auto* s = set_of(coloring.wildcard_color())) cnt += static_cast<int>(s->size());
-    sh.vertex_off[x + 1] = sh.vertex_off[x] + cnt;
+  const std::int64_t block = std::int64_t{1} << 16;
+  const std::int64_t nb = (n + block - 1) / block;
+  std::vector<std::int64_t> part(static_cast<size_t>(nb) + 1, 0);
+#pragma omp parallel for schedule(static) if (n > (1 << 20))
+  for (std::int64_t b = 0; b < nb; ++b) {
+    std::int64_t acc = 0;
+    for (std::int64_t x = b * block; x < std::min(n, (b + 1) * block); ++x) {
+      std::int32_t f, c;
+      own(x, f, c);
+      acc += c + wm;
+      sh.vertex_off[x + 1] = static_cast<std::int32_t>(acc);  // block-local for now
+    }
+    part[b + 1] = acc;
   }
-  sh.vertex_shades.resize(static_cast<size_t>(sh.vertex_off[n]));
-  for (Vertex x = 0; x < n; ++x) {
-    std::int32_t at = sh.vertex_off[x];
-    if (auto* s = set_of(coloring.primary(x)))
-      for (int d : *s) sh.vertex_shades[at++] = d;
-    if (coloring.wildcard_active())
-      if (auto* s = set_of(coloring.wildcard_color()))
-        for (int d : *s) sh.vertex_shades[at++] = d;
+  for (std::int64_t b = 0; b < nb; ++b) part[b + 1] += part[b];
+  sh.vertex_shades.resize(static_cast<size_t>(part[nb]));
+#pragma omp parallel for schedule(static) if (n > (1 << 20))
+  for (std::int64_t b = 0; b < nb; ++b) {
+    for (std::int64_t x = b * block; x < std::min(n, (b + 1) * block); ++x) {
+      sh.vertex_off[x + 1] += static_cast<std::int32_t>(part[b]);
+      std::int32_t f, c;
+      own(x, f, c);
+      std::int32_t at = sh.vertex_off[x + 1] - c - wm;
+      for (std::int32_t i = 0; i < c; ++i) sh.vertex_shades[at++] = f + i;
+      for (std::int32_t i = 0; i < wm; ++i) sh.vertex_shades[at++] = wf + i;
+    }
   }
   return sh;
 }

@@ -169,9 +169,19 @@ std::vector<bool> preprocess_mask(const TemporalGraph& g, const Prep& p, Preproc
   return keep;
 }
 
+// TSIEVE_TRACE=1: phase wall times of solve() on stderr
+void solve_mark(const char* what, Clock::time_point t0) {
+  static const bool on = std::getenv("TSIEVE_TRACE") != nullptr;
+  if (on)
+    std::fprintf(stderr, "[solve] %-26s %9.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
+}
+
 Prep prepare(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req) {
   Prep p;
+  const auto pt0 = Clock::now();
   make_effective(g, col, req, p);
+  solve_mark("make_effective", pt0);
   const auto t0 = Clock::now();
   if (p.k > g.n()) {
     p.infeasible = true;
@@ -195,13 +205,16 @@ Prep prepare(const TemporalGraph& g, const VertexColoring& col, const SolveReque
       return p;
     }
   }
+  solve_mark("build_shades", pt0);
   PreprocessLevel level = req.preprocess;
   // the exact DP stays exact: only the lossless filter applies to it
   if (p.problem == Problem::vc_colorful_path &&
       (level == PreprocessLevel::static_sieve || level == PreprocessLevel::both))
     level = PreprocessLevel::color_filter;
   const std::vector<bool> keep = preprocess_mask(g, p, level, p.peak);
+  solve_mark("preprocess mask", pt0);
   p.graph = restrict_to(g, keep, g.t());
+  solve_mark("restrict_to", pt0);
   p.kept = static_cast<int>(std::count(keep.begin(), keep.end(), true));
   if (p.kept < p.k) {
     p.infeasible = true;
@@ -532,6 +545,7 @@ SolveReport solve_single(const TemporalGraph& g, const VertexColoring& col,
   const auto t0 = Clock::now();
   const Timestamp full = p.graph.t();
   const Probe whole_probe = probe(p, p.graph, full);
+  solve_mark("probe at t", t0);
   const SieveOutcome& whole = whole_probe.out;
   r.oracle_calls = 1;
   r.decision = whole.global_nonzero;

@@ -81,12 +81,12 @@ __global__ void k_validate_orient(int64_t m, int32_t n, const int32_t* __restric
     keep[i] = 0;
     return;
   }
-  atomicMax(&st->max_ts, t);
-  if (a == b) {
+  if (a == b) {  // (t = 0 takes the largest timestamp of the edges kept)
     atomicAdd(reinterpret_cast<unsigned long long*>(&st->self_loops), 1ull);
     keep[i] = 0;
     return;
   }
+  atomicMax(&st->max_ts, t);
   if (!directed && a > b) {
     const int32_t s = a;
     a = b;

@@ -2273,7 +2273,14 @@ int tsv_eval_edge_constrained(const tsv_graph* g, int k, const int32_t* times,
     size_t free_b = 0, total_b = 0;
     TSV_CUDA(cudaMemGetInfo(&free_b, &total_b));
     int W = static_cast<int>(std::min<uint64_t>(P, 128));
-    while (W > 1 && 3ull * n * W * 8 > free_b * 0.8) W >>= 1;
+    auto ec_words = [&](int w) {
+      return 3ull * n * w + static_cast<uint64_t>(n) * k + n;
+    };
+    while (W > 1 && (3ull * n * W * 8 > free_b * 0.8 || ec_words(W) > cfg->memory_cap_words))
+      W >>= 1;
+    if (ec_words(W) > cfg->memory_cap_words)  // (sieve.cpp:161-166's convention)
+      throw CapError("sieve memory cap exceeded: needs " + std::to_string(ec_words(W)) +
+                     " field words, cap " + std::to_string(cfg->memory_cap_words));
     DevBuf d_w(static_cast<size_t>(k) * k * 8, st), d_zj(static_cast<size_t>(n) * k * 8 + 8, st),
         acc(static_cast<size_t>(n) * 8 + 8, st), zb(static_cast<size_t>(n) * W * 8 + 8, st),
         s0(static_cast<size_t>(n) * W * 8 + 8, st), s1(static_cast<size_t>(n) * W * 8 + 8, st);
@@ -2310,7 +2317,7 @@ int tsv_eval_edge_constrained(const tsv_graph* g, int k, const int32_t* times,
                                cudaMemcpyDeviceToHost, st));
     TSV_CUDA(cudaStreamSynchronize(st));
     finalize_host(n, accumulators, -1, k, out);
-    out->peak_field_words = 3ull * n * W + static_cast<uint64_t>(n) * k + n;
+    out->peak_field_words = ec_words(W);
   });
   tsv_shades_free(sh);
   return rc;
