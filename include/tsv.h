@@ -108,6 +108,15 @@ int tsv_graph_get_info(const tsv_graph* g, tsv_graph_info* out);
 /* Copies the canonical edge list (m entries each) back to the host. */
 int tsv_graph_edges(const tsv_graph* g, int32_t* u, int32_t* v, int32_t* ts);
 
+/* The graph's static projection, computed on its device (replaces the host
+ * grouping of StaticProjection::project, graph.cpp:148-199 of the
+ * reference): *ms distinct (a, b) pairs in ascending order (a < b for
+ * undirected graphs) into a[], b[] (capacity m each), back_off[ms + 1] and
+ * back[m] = the temporal edge ids of each pair, increasing within a pair.
+ * Host arrays. */
+int tsv_graph_static_edges(const tsv_graph* g, int64_t* ms, int32_t* a, int32_t* b,
+                           int32_t* back_off, int32_t* back);
+
 /* Uploads a shade CSR: vertex_off[n+1], vertex_shades[vertex_off[n]] with
  * 1-based shade ids in [1..k] (build_shades, sieve.cpp:658-718). */
 int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,

@@ -86,6 +86,7 @@ def lib():
     L.tsv_graph_free.restype = None
     L.tsv_graph_get_info.argtypes = [vp, C.POINTER(GraphInfo)]
     L.tsv_graph_edges.argtypes = [vp, _i32p, _i32p, _i32p]
+    L.tsv_graph_static_edges.argtypes = [vp, C.POINTER(C.c_int64), _i32p, _i32p, _i32p, _i32p]
     L.tsv_shades_upload.argtypes = [vp, C.c_int, _i32p, _i32p, C.POINTER(vp)]
     L.tsv_shades_free.argtypes = [vp]
     L.tsv_shades_free.restype = None

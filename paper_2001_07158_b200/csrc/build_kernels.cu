@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+
+#include <functional>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -730,6 +732,91 @@ SlotCounts build_run_slots(int64_t A, int64_t R, int32_t* arc_src, int32_t* run_
   out.arcs_with_src = static_cast<int64_t>(hc[0]);
   out.slots = static_cast<int64_t>(hc[1]);
   return out;
+}
+
+
+// ---- static projection (graph.cpp:148-199): distinct (a, b) pairs of the
+// canonical edges (a < b for undirected graphs), ascending, each with the
+// ids of its temporal edges in increasing order ---------------------------
+
+namespace {
+
+__global__ void k_static_keys(int64_t m, int32_t n, int directed, const int32_t* __restrict__ u,
+                              const int32_t* __restrict__ v, uint64_t* __restrict__ key,
+                              int32_t* __restrict__ id) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  int32_t a = u[i], b = v[i];
+  if (!directed && a > b) {
+    const int32_t t = a;
+    a = b;
+    b = t;
+  }
+  key[i] = static_cast<uint64_t>(a) * static_cast<uint64_t>(n) + static_cast<uint64_t>(b);
+  id[i] = static_cast<int32_t>(i);
+}
+
+__global__ void k_static_heads(int64_t m, const uint64_t* __restrict__ key,
+                               int32_t* __restrict__ flag) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) flag[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+}
+
+__global__ void k_static_emit(int64_t m, int32_t n, const uint64_t* __restrict__ key,
+                              const int32_t* __restrict__ flag, const int32_t* __restrict__ rank,
+                              int32_t* __restrict__ a, int32_t* __restrict__ b,
+                              int32_t* __restrict__ off) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= m || !flag[i]) return;
+  const int32_t j = rank[i];
+  a[j] = static_cast<int32_t>(key[i] / static_cast<uint64_t>(n));
+  b[j] = static_cast<int32_t>(key[i] % static_cast<uint64_t>(n));
+  off[j] = static_cast<int32_t>(i);
+}
+
+}  // namespace
+
+int64_t static_projection(const int32_t* u, const int32_t* v, int64_t m, int32_t n, bool directed,
+                          int32_t* a, int32_t* b, int32_t* off, int32_t* back, cudaStream_t st,
+                          const std::function<void*(size_t)>& alloc,
+                          const std::function<void(void*)>& release) {
+  if (m == 0) return 0;
+  auto* k0 = static_cast<uint64_t*>(alloc(static_cast<size_t>(m) * 8));
+  auto* k1 = static_cast<uint64_t*>(alloc(static_cast<size_t>(m) * 8));
+  auto* i0 = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4));
+  k_static_keys<<<nblk(m), kT, 0, st>>>(m, n, directed ? 1 : 0, u, v, k0, i0);
+  // stable radix sort by key; ties keep edge-id order (std::stable_sort)
+  cub::DoubleBuffer<uint64_t> bk(k0, k1);
+  cub::DoubleBuffer<int32_t> bv(i0, back);
+  const uint64_t nn = static_cast<uint64_t>(n);
+  radix_pairs(bk, bv, m, bits_for(nn * nn ? nn * nn - 1 : 0), st);
+  if (bv.Current() != back)
+    cudaMemcpyAsync(back, bv.Current(), static_cast<size_t>(m) * 4, cudaMemcpyDeviceToDevice, st);
+  const uint64_t* ks = bk.Current();
+  auto* flag = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4));
+  auto* rank = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4));
+  k_static_heads<<<nblk(m), kT, 0, st>>>(m, ks, flag);
+  size_t tb = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tb, flag, rank, m, st);
+  void* t = alloc(tb ? tb : 8);
+  cub::DeviceScan::ExclusiveSum(t, tb, flag, rank, m, st);
+  release(t);
+  int32_t last[2] = {0, 0};
+  cudaMemcpyAsync(&last[0], rank + (m - 1), 4, cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&last[1], flag + (m - 1), 4, cudaMemcpyDeviceToHost, st);
+  k_static_emit<<<nblk(m), kT, 0, st>>>(m, n, ks, flag, rank, a, b, off);
+  if (cudaStreamSynchronize(st) != cudaSuccess)
+    throw std::runtime_error("static projection: device error");
+  const int64_t ms = static_cast<int64_t>(last[0]) + last[1];
+  const int32_t mm = static_cast<int32_t>(m);
+  cudaMemcpyAsync(off + ms, &mm, 4, cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);
+  release(k0);
+  release(k1);
+  release(i0);
+  release(flag);
+  release(rank);
+  return ms;
 }
 
 }  // namespace tsv

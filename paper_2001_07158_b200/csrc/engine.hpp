@@ -184,6 +184,16 @@ void launch_vc_dp_level(int64_t m, int directed, const int32_t* eu, const int32_
 void edges_from_layout(const DevGraph& g, bool directed, int32_t* eu, int32_t* ev, int32_t* ets,
                        cudaStream_t st);
 
+// Static projection of canonical edges (graph.cpp:148-199): writes the ms
+// distinct (a, b) pairs ascending (a < b when undirected) to a, b, the first
+// index of each into off (ms + 1 entries, off[ms] = m) and the temporal
+// edge ids grouped by pair, increasing within a pair, into back (m).  All
+// device arrays; returns ms (synchronizes st).
+int64_t static_projection(const int32_t* u, const int32_t* v, int64_t m, int32_t n, bool directed,
+                          int32_t* a, int32_t* b, int32_t* off, int32_t* back, cudaStream_t st,
+                          const std::function<void*(size_t)>& alloc,
+                          const std::function<void(void*)>& release);
+
 // State slots (build_kernels.cu): run_slot[r] = rank of r among the runs
 // some arc reads (else -1) and arc_src rewritten from run indices to slots.
 // Returns {arcs with a src, referenced runs}; synchronizes `st`.

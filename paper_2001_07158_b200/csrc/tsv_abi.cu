@@ -2241,6 +2241,65 @@ struct StreamGuard {
 
 }  // namespace
 
+int tsv_graph_static_edges(const tsv_graph* g, int64_t* ms, int32_t* a, int32_t* b,
+                           int32_t* back_off, int32_t* back) {
+  return guard([&] {
+    if (!g || !ms || !a || !b || !back_off || !back) throw std::invalid_argument("null argument");
+    if (g->model != 0)
+      throw std::invalid_argument("static projection of an edge-model graph: use the instant one");
+    DeviceGuard dg(g->device);
+    StreamGuard sg;
+    cudaStream_t st = sg.st;
+    const int64_t m = g->m;
+    std::vector<void*> live;
+    auto alloc = [&](size_t bytes) -> void* {
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+        throw CudaError("static projection: out of device memory");
+      live.push_back(p);
+      return p;
+    };
+    auto release = [&](void* p) {
+      auto it = std::find(live.begin(), live.end(), p);
+      if (it != live.end()) live.erase(it);
+      cudaFreeAsync(p, st);
+    };
+    try {
+      const int32_t *eu = g->d_eu, *ev = g->d_ev;
+      if (!eu) {
+        auto* x = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4 + 4));
+        auto* y = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4 + 4));
+        auto* z = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4 + 4));
+        if (g->edges_in_layout) {
+          tsv::edges_from_layout(g->dev, g->host.directed, x, y, z, st);
+        } else if (m) {
+          TSV_CUDA(cudaMemcpyAsync(x, g->host.eu.data(), m * 4, cudaMemcpyHostToDevice, st));
+          TSV_CUDA(cudaMemcpyAsync(y, g->host.ev.data(), m * 4, cudaMemcpyHostToDevice, st));
+        }
+        release(z);
+        eu = x;
+        ev = y;
+      }
+      auto* da = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4 + 4));
+      auto* db = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4 + 4));
+      auto* doff = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4 + 8));
+      auto* dback = static_cast<int32_t*>(alloc(static_cast<size_t>(m) * 4 + 4));
+      const int64_t s = tsv::static_projection(eu, ev, m, g->host.n, g->host.directed, da, db,
+                                               doff, dback, st, alloc, release);
+      copy_to_host(a, da, static_cast<size_t>(s) * 4, st);
+      copy_to_host(b, db, static_cast<size_t>(s) * 4, st);
+      copy_to_host(back_off, doff, static_cast<size_t>(s + 1) * 4, st);
+      copy_to_host(back, dback, static_cast<size_t>(m) * 4, st);
+      *ms = s;
+    } catch (...) {
+      for (void* p : live) cudaFreeAsync(p, st);
+      throw;
+    }
+    for (void* p : live) cudaFreeAsync(p, st);
+  });
+}
+
+
 int tsv_eval_edge_constrained(const tsv_graph* g, int k, const int32_t* times,
                               const int32_t* vertex_off, const int32_t* vertex_shades,
                               const tsv_config* cfg, uint64_t* accumulators, tsv_outcome* out) {

@@ -105,6 +105,19 @@ class TemporalGraph:
             self._edges = (u[:self.m()], v[:self.m()], ts[:self.m()])
         return self._edges
 
+    def static_projection(self):
+        """The static projection grouped on the device (tsv_graph_static_edges,
+        graph.cpp:148-199 of the reference): (a, b, back_off, back) -- the
+        distinct (a, b) pairs ascending (a < b when undirected) and, per pair,
+        its temporal edge ids in increasing order."""
+        m = max(self.m(), 1)
+        a, b, back = (np.zeros(m, np.int32) for _ in range(3))
+        off = np.zeros(m + 1, np.int32)
+        ms = C.c_int64(0)
+        _native.check(_native.lib().tsv_graph_static_edges(self._h, C.byref(ms), a, b, off, back))
+        s = ms.value
+        return a[:s], b[:s], off[:s + 1], back[:self.m()]
+
     @property
     def info(self) -> _native.GraphInfo:
         return self._info

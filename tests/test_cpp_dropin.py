@@ -330,6 +330,31 @@ def test_solver_small_fields_match_reference(cuda_device, golden, bits):
 
 
 @pytest.mark.gpu
+def test_default_preprocessing_large_graph_matches_reference(cuda_device):
+    """--preprocess both on a graph above 2^22 edges, where the C++
+    StaticProjection::project groups on the device (radix sort) and
+    TemporalGraph::build canonicalizes there: the solve() record equals the
+    reference's (its host stable_sort and build)."""
+    from oracle import oracle as O
+    rng = np.random.default_rng(23)
+    n, m = 3000, (1 << 22) + 5000
+    u = rng.integers(0, n, m).astype(np.int32)
+    v = rng.integers(0, n, m).astype(np.int32)
+    ts = rng.integers(1, 40, m).astype(np.int32)
+    colors = rng.integers(1, 6, n).astype(np.int32)
+    c = {"n": n, "u": u.tolist(), "v": v.tolist(), "ts": ts.tolist(), "directed": True,
+         "colors": colors,
+         "problem": "pathmotif", "motif": [1, 2, 2, 3], "k": 4, "source": -1, "dest": -1,
+         "seed": 3, "mode": 1, "extraction": 0, "preprocess": 3}
+    want = O.ref_solve(n, u, v, ts, True, colors, "pathmotif", [1, 2, 2, 3], 4, seed=3, mode=1,
+                       preprocess=3)
+    got = solve(c)
+    for key in ("decision", "certain", "optimum_ts", "checksum", "flagged", "oracle_calls",
+                "preprocessed_n", "preprocessed_m"):
+        assert got[key] == want[key], (key, got[key], want[key])
+
+
+@pytest.mark.gpu
 def test_cli_reference_defaults(cuda_device, fig2, golden):
     """The reference CLI tests (test_cli.cpp:41-84) with DEFAULT flags
     (preprocess both, optimize on)."""

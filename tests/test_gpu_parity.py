@@ -465,6 +465,34 @@ def test_small_fields_vs_reference(cuda_device, bits):
     assert nz >= 5
 
 
+@pytest.mark.parametrize("directed", [True, False])
+def test_device_static_projection_matches_host_grouping(cuda_device, directed):
+    """tsv_graph_static_edges (the radix-sorted projection the C++
+    StaticProjection::project uses from 2^22 edges on) equals the
+    reference's grouping (graph.cpp:148-199: stable sort of the canonical
+    edges by their oriented (u, v), pairs ascending, edge ids increasing
+    within a pair) -- here restated with numpy on the same canonical list;
+    repeated pairs (few vertices, many timestamps) and self-loops dropped by
+    the build."""
+    rng = np.random.default_rng(5 if directed else 6)
+    n, m = 300, 200_000
+    u, v = rng.integers(0, n, m), rng.integers(0, n, m)
+    ts = rng.integers(1, 5000, m)
+    g = T.TemporalGraph.build(n, (u, v, ts), directed)
+    a, b, off, back = g.static_projection()
+    cu, cv, _ = g.edges()
+    cu, cv = cu.astype(np.int64), cv.astype(np.int64)
+    if not directed:
+        cu, cv = np.minimum(cu, cv), np.maximum(cu, cv)
+    key = cu * n + cv
+    order = np.argsort(key, kind="stable")
+    uk, first = np.unique(key[order], return_index=True)
+    assert np.array_equal(a, uk // n) and np.array_equal(b, uk % n)
+    assert np.array_equal(off, np.append(first, len(key)))
+    assert np.array_equal(back, order)
+    assert len(uk) < g.m()  # repeated pairs were grouped
+
+
 def test_device_points_api_shards_xor_to_full(cuda_device, golden):
     """tsv_eval_points_device over disjoint point ranges + tsv_xor_combine_device
     reproduces the full evaluation (the multi-GPU sieve-point sharding path)."""
