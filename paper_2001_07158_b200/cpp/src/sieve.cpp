@@ -122,6 +122,15 @@ ShadeAssignment build_shades(const MotifQuery& query, const VertexColoring& colo
 }
 
 namespace {
+// The reference's default cap (2^31 words) bounds ITS dense layers (host
+// RAM, sieve.cpp:161-166); the engine's sparse state lives in HBM and is
+// bounded by the device itself, so the default means "no cap" here (C4 /
+// C5 would otherwise fall back to the slower engines under 16 GB).  Any
+// other value is the bound on the engine's working set (CapError beyond).
+std::uint64_t engine_cap(const SieveConfig& config) {
+  return config.memory_cap_words == SieveConfig{}.memory_cap_words ? ~std::uint64_t{0}
+                                                                    : config.memory_cap_words;
+}
 int default_device() {
   const char* e = std::getenv("TSV_DEVICE");
   return e ? std::atoi(e) : 0;
@@ -148,7 +157,7 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
   c.lane_width = config.lane_width;
   c.edge_model = model;
   c.points_per_batch = 0;
-  c.memory_cap_words = config.memory_cap_words;
+  c.memory_cap_words = engine_cap(config);
 
   SieveOutcome out;
   out.accumulators.assign(static_cast<size_t>(g.n()), 0);
@@ -211,7 +220,7 @@ tsv_config to_abi(const SieveConfig& config) {
   c.field_bits = config.field_bits;
   c.lane_width = config.lane_width;
   c.edge_model = 0;
-  c.memory_cap_words = config.memory_cap_words;
+  c.memory_cap_words = engine_cap(config);
   return c;
 }
 
@@ -302,7 +311,7 @@ SieveOutcome eval_projection(const StaticProjection& gs, int k, const ShadeAssig
   c.seed = config.seed;
   c.field_bits = config.field_bits;
   c.lane_width = config.lane_width;
-  c.memory_cap_words = config.memory_cap_words;
+  c.memory_cap_words = engine_cap(config);
   SieveOutcome out;
   out.accumulators.assign(static_cast<size_t>(gs.n()), 0);
   std::uint64_t scratch = 0;
