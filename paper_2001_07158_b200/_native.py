@@ -97,6 +97,9 @@ def lib():
                                          C.c_int32, C.c_uint64, C.c_uint64, vp, vp]
     L.tsv_xor_combine_device.argtypes = [vp, C.c_int, C.c_int64, vp, vp]
     L.tsv_finalize.argtypes = [C.c_int32, _u64p, C.c_int32, C.POINTER(Outcome)]
+    L.tsv_eval_static_projection.argtypes = [C.c_int32, C.c_int64, _i32p, _i32p, C.c_int, C.c_int,
+                                             C.c_int, _i32p, _i32p, C.POINTER(Config), C.c_int,
+                                             _u64p, C.POINTER(Outcome)]
     L.tsv_vertex_partition.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(Partition)]
     L.tsv_eval_vertex_level.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int32, C.POINTER(Config),
                                         C.c_int32, C.c_int, C.c_int, vp, vp, vp, vp]

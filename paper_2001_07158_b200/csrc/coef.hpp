@@ -178,6 +178,34 @@ void launch_win_multi_list(int32_t n, int64_t Sw, const int8_t* vsh, int2* list,
 void launch_ts_group_start(const int32_t* ts, const int64_t* pos, int nb, int64_t* out,
                            cudaStream_t st);
 
+// Static-projection sieves in coefficient form (coef_static.cu): the
+// junction sieve (junction = true) or the plain static sieve over the
+// projection's head-grouped in-arcs (tail -> head) and out-arcs (head =
+// the walk's current vertex, tail = the next one), both with per-head
+// offsets (n + 1); zj = the n x k shade-basis table (k_zj_ident), det =
+// det(W); XORs the accumulators into acc.
+struct StaticCoefInputs {
+  int32_t n = 0;
+  int k = 0;
+  bool junction = true;
+  uint64_t seed = 1;
+  const int64_t* in_off = nullptr;
+  const int32_t* in_tail = nullptr;
+  const int32_t* in_edge = nullptr;
+  const int64_t* out_off = nullptr;
+  const int32_t* out_tail = nullptr;
+  const int32_t* out_edge = nullptr;
+  const uint64_t* zj = nullptr;
+  uint64_t det = 1;
+  uint64_t* acc = nullptr;
+  const struct CoefTables* tables = nullptr;
+};
+bool static_coef_supported(int k);
+uint64_t static_coef_words(int32_t n, int k, bool junction);  // device words it allocates
+void eval_static_coef(const StaticCoefInputs& in, cudaStream_t st,
+                      const std::function<void*(size_t)>& alloc,
+                      const std::function<void(void*)>& release);
+
 // Host tables (colex order = increasing bit mask within a level).
 struct CoefTables {
   int k = 0;

@@ -2473,7 +2473,7 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
     // head-sorted arc lists of the projection: in-arcs (tail -> head) and
     // out-arcs (head = the walk's current vertex, tail = the next one)
     auto arcs = [&](bool incoming, std::vector<int32_t>& head, std::vector<int32_t>& tail,
-                    std::vector<int32_t>& edge) {
+                    std::vector<int32_t>& edge, std::vector<int64_t>* head_off = nullptr) {
       const int64_t A = directed ? ms : 2 * ms;
       std::vector<int64_t> off(static_cast<size_t>(n) + 1, 0);
       for (int64_t i = 0; i < ms; ++i) {
@@ -2483,6 +2483,7 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
         if (!directed) ++off[(incoming ? a[i] : b[i]) + 1];
       }
       for (int32_t x = 0; x < n; ++x) off[x + 1] += off[x];
+      if (head_off) *head_off = off;
       head.resize(static_cast<size_t>(A));
       tail.resize(static_cast<size_t>(A));
       edge.resize(static_cast<size_t>(A));
@@ -2518,6 +2519,84 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
                      " field words, cap " + std::to_string(cfg->memory_cap_words));
 
     std::vector<int32_t> ih, it, ie, oh, ot, oe;
+    // coefficient form (coef_static.cu): GF(2^64), k <= 12, when its rows fit
+    const char* se = std::getenv("TSV_STATIC_ENGINE");
+    const uint64_t cwords = tsv::static_coef_words(n, k, junction != 0);
+    if (cfg->field_bits == 64 && tsv::static_coef_supported(k) &&
+        !(se && std::strcmp(se, "points") == 0) && cwords <= cfg->memory_cap_words &&
+        fits_device(cwords)) {
+      std::vector<int64_t> ioff, ooff;
+      arcs(true, ih, it, ie, &ioff);
+      if (junction) arcs(false, oh, ot, oe, &ooff);
+      std::vector<int32_t> off(vertex_off, vertex_off + n + 1);
+      std::vector<int32_t> shv(vertex_shades, vertex_shades + vertex_off[n]);
+      for (int32_t s : shv)
+        if (s < 1 || s > k) throw std::invalid_argument("shade id outside [1..k]");
+      std::vector<void*> live;
+      auto alloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+          throw CudaError("static sieve: out of device memory");
+        live.push_back(p);
+        return p;
+      };
+      auto release = [&](void* p) {
+        auto itp = std::find(live.begin(), live.end(), p);
+        if (itp != live.end()) live.erase(itp);
+        cudaFreeAsync(p, st);
+      };
+      auto upv = [&](const auto& v) {
+        using Tv = typename std::decay_t<decltype(v)>::value_type;
+        void* d = alloc(std::max<size_t>(v.size(), 1) * sizeof(Tv));
+        if (!v.empty())
+          TSV_CUDA(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(Tv), cudaMemcpyHostToDevice, st));
+        return d;
+      };
+      try {
+        tsv::StaticCoefInputs ci;
+        ci.n = n;
+        ci.k = k;
+        ci.junction = junction != 0;
+        ci.seed = cfg->seed;
+        ci.in_off = static_cast<const int64_t*>(upv(ioff));
+        ci.in_tail = static_cast<const int32_t*>(upv(it));
+        ci.in_edge = static_cast<const int32_t*>(upv(ie));
+        if (junction) {
+          ci.out_off = static_cast<const int64_t*>(upv(ooff));
+          ci.out_tail = static_cast<const int32_t*>(upv(ot));
+          ci.out_edge = static_cast<const int32_t*>(upv(oe));
+        }
+        auto* d_off = static_cast<int32_t*>(upv(off));
+        auto* d_sh = static_cast<int32_t*>(upv(shv));
+        auto* zj = static_cast<uint64_t*>(alloc(static_cast<size_t>(n) * k * 8 + 8));
+        tsv::launch_zj_ident(n, k, cfg->seed, d_off, d_sh, zj, st);
+        std::vector<uint64_t> Wm(static_cast<size_t>(k) * k);
+        const uint64_t pre = tsv::draw_prefix(cfg->seed, tsv::kRoleShadeW);
+        for (int d = 0; d < k; ++d)
+          for (int j = 0; j < k; ++j)
+            Wm[static_cast<size_t>(d) * k + j] = tsv::draw_nonzero_from(pre, d + 1, j + 1, 0);
+        ci.det = tsv::gf_det_host(Wm.data(), k);
+        ci.zj = zj;
+        auto* acc = static_cast<uint64_t*>(alloc(static_cast<size_t>(n) * 8 + 8));
+        TSV_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(n) * 8 + 8, st));
+        ci.acc = acc;
+        ci.tables = &coef_const_tables(k);
+        tsv::eval_static_coef(ci, st, alloc, release);
+        TSV_CUDA(cudaGetLastError());
+        if (n)
+          TSV_CUDA(cudaMemcpyAsync(accumulators, acc, static_cast<size_t>(n) * 8,
+                                   cudaMemcpyDeviceToHost, st));
+        TSV_CUDA(cudaStreamSynchronize(st));
+      } catch (...) {
+        for (void* p : live) cudaFreeAsync(p, st);
+        throw;
+      }
+      for (void* p : live) cudaFreeAsync(p, st);
+      *out = tsv_outcome{};
+      finalize_host(n, accumulators, -1, k, out);
+      out->peak_field_words = cwords;
+      return;
+    }
     arcs(true, ih, it, ie);
     if (junction) arcs(false, oh, ot, oe);
     // chunks sized to give every SM several warps (a 256-arc chunk left the
@@ -2560,7 +2639,8 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
     TSV_CUDA(cudaMemsetAsync(acc.p, 0, static_cast<size_t>(n) * 8, st));
     const size_t layer = static_cast<size_t>(n) * W;
     std::vector<std::unique_ptr<DevBuf>> ending;
-    for (uint64_t i = 0; i <= static_cast<uint64_t>(k); ++i)
+    // (the static sieve ping-pongs E(l) over entries 1 and 2: at least 3, k = 1 too)
+    for (uint64_t i = 0; i <= std::max<uint64_t>(static_cast<uint64_t>(k), 2); ++i)
       ending.emplace_back(new DevBuf((junction || i <= 2 ? layer : 1) * 8, st));
     DevBuf s0(layer * 8, st), s1(layer * 8, st);
 

@@ -493,6 +493,56 @@ def test_device_static_projection_matches_host_grouping(cuda_device, directed):
     assert len(uk) < g.m()  # repeated pairs were grouped
 
 
+@pytest.mark.parametrize("junction", [1, 0])
+def test_static_coefficient_engine_equals_point_engine(cuda_device, monkeypatch, junction):
+    """The junction / static sieves on the projection in coefficient form
+    (coef_static.cu: walks-ending and walks-starting families as top-degree
+    rows, readout XOR_b E_{k+1-b} * S_b on complementary subsets) equal the
+    point form (static_kernels.cu, every sieve point; pinned against the
+    reference through test_default_preprocessing_matches_reference):
+    single-, multi-shade and shadeless vertices, directed and undirected
+    projections with repeated vertices, k = 1..8."""
+    import ctypes as C
+    L = _native.lib()
+    rng = np.random.default_rng(41 + junction)
+    nz = 0
+    for i in range(24):
+        n = int(rng.integers(3, 60))
+        ms = int(rng.integers(1, 400))
+        a = rng.integers(0, n, ms).astype(np.int32)
+        b = rng.integers(0, n, ms).astype(np.int32)
+        keep = a != b
+        a, b = a[keep], b[keep]
+        directed = int(i % 2)
+        k = int(rng.integers(1, 9))
+        q = int(rng.integers(1, 5))
+        colors = rng.integers(1, q + 2, n).astype(np.int32)  # color q+1: no shade
+        motif = sorted(int(x) for x in rng.integers(1, q + 1, k))
+        cfg = T.SieveConfig(seed=int(rng.integers(1, 1 << 30)), memory_cap_words=1 << 62)
+        sh = T.build_shades(T.MotifQuery.from_multiset(motif), T.VertexColoring(colors, q + 1),
+                            cfg)
+        vs = np.ascontiguousarray(sh.vertex_shades if len(sh.vertex_shades) else
+                                  np.zeros(1, np.int32), np.int32)
+        voff = np.ascontiguousarray(sh.vertex_off, np.int32)
+        res = []
+        for engine in ("coef", "points"):
+            if engine == "points":
+                monkeypatch.setenv("TSV_STATIC_ENGINE", "points")
+            acc = np.zeros(n, np.uint64)
+            o = _native.Outcome()
+            c = cfg.to_native()
+            _native.check(L.tsv_eval_static_projection(n, len(a), np.ascontiguousarray(a),
+                                                       np.ascontiguousarray(b), directed,
+                                                       junction, k, voff, vs, C.byref(c), 0,
+                                                       acc, C.byref(o)))
+            res.append((acc, o.checksum))
+            monkeypatch.delenv("TSV_STATIC_ENGINE", raising=False)
+        assert np.array_equal(res[0][0], res[1][0]), (i, k, directed, motif)
+        assert res[0][1] == res[1][1]
+        nz += int(res[0][0].any())
+    assert nz >= 8
+
+
 def test_device_points_api_shards_xor_to_full(cuda_device, golden):
     """tsv_eval_points_device over disjoint point ranges + tsv_xor_combine_device
     reproduces the full evaluation (the multi-GPU sieve-point sharding path)."""
