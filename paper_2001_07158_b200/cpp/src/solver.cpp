@@ -137,6 +137,14 @@ void make_effective(const TemporalGraph& g, const VertexColoring& col, const Sol
 // Kept-vertex mask (solver.cpp:458-497 of the reference): the exact color
 // filter, then the junction sieve on the static projection of what is left
 // (whp: flags exactly the vertices on a properly colored static k-path).
+// TSIEVE_TRACE=1: phase wall times of solve() on stderr
+void solve_mark(const char* what, Clock::time_point t0) {
+  static const bool on = std::getenv("TSIEVE_TRACE") != nullptr;
+  if (on)
+    std::fprintf(stderr, "[solve] %-26s %9.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
+}
+
 std::vector<bool> preprocess_mask(const TemporalGraph& g, const Prep& p, PreprocessLevel level,
                                   std::uint64_t& peak) {
   std::vector<bool> keep(static_cast<size_t>(g.n()), true);
@@ -157,24 +165,22 @@ std::vector<bool> preprocess_mask(const TemporalGraph& g, const Prep& p, Preproc
     relaxed.kind = QueryKind::multiset;
     relaxed.k = p.k;
     relaxed.multiset = p.query.multiset;
+    const auto jt0 = Clock::now();
     const ShadeAssignment sh = build_shades(relaxed, p.coloring, p.cfg);
     if (!sh.feasible) return std::vector<bool>(static_cast<size_t>(g.n()), false);
-    const StaticProjection proj = StaticProjection::project(restrict_to(g, keep, g.t()));
+    solve_mark("junction: shades", jt0);
+    const TemporalGraph filtered = restrict_to(g, keep, g.t());
+    solve_mark("junction: color filter", jt0);
+    const StaticProjection proj = StaticProjection::project(filtered);
+    solve_mark("junction: projection", jt0);
     const SieveOutcome jo = eval_junction_sieve(proj, p.k, sh, p.cfg);
+    solve_mark("junction: sieve", jt0);
     peak = std::max(peak, jo.peak_field_words);
     std::vector<bool> flagged(static_cast<size_t>(g.n()), false);
     for (Vertex x : jo.flagged) flagged[x] = true;
     for (Vertex x = 0; x < g.n(); ++x) keep[x] = keep[x] && flagged[x];
   }
   return keep;
-}
-
-// TSIEVE_TRACE=1: phase wall times of solve() on stderr
-void solve_mark(const char* what, Clock::time_point t0) {
-  static const bool on = std::getenv("TSIEVE_TRACE") != nullptr;
-  if (on)
-    std::fprintf(stderr, "[solve] %-26s %9.1f ms\n", what,
-                 std::chrono::duration<double, std::milli>(Clock::now() - t0).count());
 }
 
 Prep prepare(const TemporalGraph& g, const VertexColoring& col, const SolveRequest& req) {

@@ -195,6 +195,8 @@ struct StaticCoefInputs {
   const int64_t* out_off = nullptr;
   const int32_t* out_tail = nullptr;
   const int32_t* out_edge = nullptr;
+  const std::vector<int64_t>* h_in_off = nullptr;   // host copies of the offsets (tasks)
+  const std::vector<int64_t>* h_out_off = nullptr;
   const uint64_t* zj = nullptr;
   uint64_t det = 1;
   uint64_t* acc = nullptr;

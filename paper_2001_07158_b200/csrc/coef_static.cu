@@ -20,11 +20,14 @@
 // with zmap_h(U)[T] = XOR_{j in T} z_{h,j} U[T - {j}], a row of C(k, l)
 // words per vertex and level.  The static sieve is acc[u] = det * E_k[u][[k]].
 //
-// A warp owns a head vertex: per arc it builds the warp-uniform y's GfTable
-// (2 KB of shared memory, gf_device.cuh) and multiplies the tail's row by it
-// lane-strided; the z map takes z_{h,j} one j at a time, again as a table,
-// over the (T - {j} -> T) pairs of CoefTables::jpairs.  Work per arc and
-// level: C(k, l-1) table products instead of 2^k point products.
+// Arc pass: a warp owns a task of <= 256 arcs of one head (hubs of the
+// power-law configs span many tasks, combined with 64-bit atomic XOR): per
+// arc it builds the warp-uniform y's GfTable (2 KB of shared memory,
+// gf_device.cuh) and multiplies the tail's row by it lane-strided, eight
+// row loads in flight per lane.  z map pass: a warp per vertex takes
+// z_{h,j} one j at a time, again as a table, over the (T - {j} -> T) pairs
+// of CoefTables::jpairs.  Work per arc and level: C(k, l-1) table products
+// instead of 2^k point products.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,25 +45,81 @@ namespace {
 constexpr int kSW = 2;          // warps per block (2 x 17 KB of static shared memory)
 constexpr int kRowMax = 924;    // C(12, 6): the largest row (k <= 12)
 
-struct SLevel {
-  int64_t nlist = 0;                  // heads to process
-  const int32_t* list = nullptr;      // head ids (nullptr: 0 .. nlist-1)
-  const int64_t* off = nullptr;       // n+1: arcs of head h at [off[h], off[h+1]); nullptr: no arcs
+constexpr int kChunk = 256;     // arcs per task: hub vertices are split over warps
+
+// Arc pass: a warp per task (<= kChunk arcs of one head) XORs
+// XOR_{arcs} y(e) * src[tail] into dst[head] (zeroed; 64-bit atomics, since
+// a hub's tasks run on several warps).
+struct SArcs {
+  int64_t ntask = 0;
+  const int32_t* task_head = nullptr;
+  const int64_t* task_a0 = nullptr;
+  const int32_t* task_len = nullptr;
   const int32_t* tail = nullptr;
   const int32_t* edge = nullptr;
-  const uint64_t* src = nullptr;      // n x Ein
-  int Ein = 0;
-  uint64_t* dst = nullptr;            // n x Eout
-  int Eout = 0;
+  const uint64_t* src = nullptr;      // n x E
+  uint64_t* dst = nullptr;            // n x E
+  int E = 0;
   uint64_t pre = 0, yb = 0;           // draw prefix (seed, role), level + round constant
-  const uint64_t* zj = nullptr;       // n x k; nullptr: no z map (Eout == Ein)
-  int k = 0;
-  const int2* jp = nullptr;           // k blocks of C(k-1, Ein's size) (in rank, out rank)
-  int jcnt = 0;
-  bool self = false;                  // U = src[h] (vertex z map, no arcs)
 };
 
-__global__ void __launch_bounds__(kSW * 32) k_static_coef(const SLevel P) {
+__global__ void __launch_bounds__(kSW * 32) k_static_arcs(const SArcs P) {
+  __shared__ __align__(256) uint64_t tabs[kSW][GfTable::kWords];
+  __shared__ uint64_t su[kSW][kRowMax];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  GfTable T{tabs[w]};
+  uint64_t* U = su[w];
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * kSW;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kSW + w; i < P.ntask; i += nw) {
+    const int32_t h = __ldg(P.task_head + i);
+    const int64_t a0 = __ldg(P.task_a0 + i), a1 = a0 + __ldg(P.task_len + i);
+    for (int e = lane; e < P.E; e += 32) U[e] = 0;
+    for (int64_t a = a0; a < a1; ++a) {
+      const int32_t t = __ldg(P.tail + a);
+      const uint64_t y = draw_edge_y(P.pre, P.yb, static_cast<uint32_t>(__ldg(P.edge + a)));
+      const uint64_t* row = P.src + static_cast<int64_t>(t) * P.E;
+      __syncwarp();
+      T.build(y, lane);
+      __syncwarp();
+      // kLd independent row loads in flight per lane (a row is up to 924
+      // words; one load at a time left the pass latency-bound)
+      constexpr int kLd = 8;
+      for (int e0 = lane; e0 < P.E; e0 += 32 * kLd) {
+        uint64_t x[kLd];
+#pragma unroll
+        for (int r = 0; r < kLd; ++r) {
+          const int e = e0 + 32 * r;
+          x[r] = e < P.E ? __ldg(row + e) : 0ull;
+        }
+#pragma unroll
+        for (int r = 0; r < kLd; ++r)
+          if (x[r]) U[e0 + 32 * r] ^= T.mul(x[r]);
+      }
+    }
+    __syncwarp();
+    uint64_t* out = P.dst + static_cast<int64_t>(h) * P.E;
+    for (int e = lane; e < P.E; e += 32)
+      if (U[e])
+        atomicXor(reinterpret_cast<unsigned long long*>(out + e),
+                  static_cast<unsigned long long>(U[e]));
+  }
+}
+
+// z map per vertex: dst[h] = zmap_h(src[h]) (Ein -> Eout words), z_{h,j}
+// one j at a time as a warp-uniform table over the (T - {j} -> T) pairs.
+struct SZmap {
+  int32_t n = 0;
+  const uint64_t* src = nullptr;
+  int Ein = 0;
+  uint64_t* dst = nullptr;
+  int Eout = 0;
+  const uint64_t* zj = nullptr;
+  int k = 0;
+  const int2* jp = nullptr;  // k blocks of jcnt (in rank, out rank)
+  int jcnt = 0;
+};
+
+__global__ void __launch_bounds__(kSW * 32) k_static_zmap(const SZmap P) {
   __shared__ __align__(256) uint64_t tabs[kSW][GfTable::kWords];
   __shared__ uint64_t su[kSW][kRowMax], ss[kSW][kRowMax];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -68,47 +127,30 @@ __global__ void __launch_bounds__(kSW * 32) k_static_coef(const SLevel P) {
   uint64_t* U = su[w];
   uint64_t* S = ss[w];
   const int64_t nw = static_cast<int64_t>(gridDim.x) * kSW;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * kSW + w; i < P.nlist; i += nw) {
-    const int32_t h = P.list ? P.list[i] : static_cast<int32_t>(i);
-    if (P.self) {
-      for (int e = lane; e < P.Ein; e += 32) U[e] = P.src[static_cast<int64_t>(h) * P.Ein + e];
-    } else {
-      for (int e = lane; e < P.Ein; e += 32) U[e] = 0;
-      const int64_t a0 = P.off[h], a1 = P.off[h + 1];
-      for (int64_t a = a0; a < a1; ++a) {
-        const int32_t t = __ldg(P.tail + a);
-        const uint64_t y = draw_edge_y(P.pre, P.yb, static_cast<uint32_t>(__ldg(P.edge + a)));
-        const uint64_t* row = P.src + static_cast<int64_t>(t) * P.Ein;
+  for (int64_t h = static_cast<int64_t>(blockIdx.x) * kSW + w; h < P.n; h += nw) {
+    bool any = false;
+    for (int e = lane; e < P.Ein; e += 32) {
+      U[e] = __ldg(P.src + h * P.Ein + e);
+      any = any || U[e] != 0;
+    }
+    for (int e = lane; e < P.Eout; e += 32) S[e] = 0;
+    if (__any_sync(0xffffffffu, any)) {
+      for (int j = 0; j < P.k; ++j) {
+        const uint64_t z = __ldg(P.zj + h * P.k + j);
+        if (!z) continue;  // warp-uniform
         __syncwarp();
-        T.build(y, lane);
+        T.build(z, lane);
         __syncwarp();
-        for (int e = lane; e < P.Ein; e += 32) {
-          const uint64_t x = __ldg(row + e);
-          if (x) U[e] ^= T.mul(x);
+        const int2* pj = P.jp + static_cast<int64_t>(j) * P.jcnt;
+        for (int p = lane; p < P.jcnt; p += 32) {  // T' -> T' + {j}: distinct outputs
+          const int2 q = __ldg(pj + p);
+          const uint64_t x = U[q.x];
+          if (x) S[q.y] ^= T.mul(x);
         }
       }
     }
     __syncwarp();
-    uint64_t* out = P.dst + static_cast<int64_t>(h) * P.Eout;
-    if (!P.zj) {
-      for (int e = lane; e < P.Eout; e += 32) out[e] = U[e];
-      continue;
-    }
-    for (int e = lane; e < P.Eout; e += 32) S[e] = 0;
-    for (int j = 0; j < P.k; ++j) {
-      const uint64_t z = __ldg(P.zj + static_cast<int64_t>(h) * P.k + j);
-      if (!z) continue;  // warp-uniform
-      __syncwarp();
-      T.build(z, lane);
-      __syncwarp();
-      const int2* pj = P.jp + static_cast<int64_t>(j) * P.jcnt;
-      for (int p = lane; p < P.jcnt; p += 32) {  // T' -> T' + {j}: distinct outputs
-        const int2 q = __ldg(pj + p);
-        const uint64_t x = U[q.x];
-        if (x) S[q.y] ^= T.mul(x);
-      }
-    }
-    __syncwarp();
+    uint64_t* out = P.dst + h * P.Eout;
     for (int e = lane; e < P.Eout; e += 32) out[e] = S[e];
   }
 }
@@ -174,8 +216,8 @@ uint64_t static_coef_words(int32_t n, int k, bool junction) {
     if (c > mx) mx = c;
   }
   // + all S_b of the junction sieve (sum_b C(k, b-1), b = 2..k, kept for the
-  // readout) and one z-mapped buffer
-  const uint64_t srows = junction ? (uint64_t{1} << k) - 2 + mx : 0;
+  // readout) and the arc-pass / z-map buffer
+  const uint64_t srows = (junction ? (uint64_t{1} << k) - 2 : 0) + mx;
   return static_cast<uint64_t>(n) * (rows + srows + k);
 }
 
@@ -233,86 +275,79 @@ void eval_static_coef(const StaticCoefInputs& in, cudaStream_t st,
   const int64_t* d_coff = static_cast<const int64_t*>(up(comp_off.data(), comp_off.size() * 8));
   const int* d_cnt = static_cast<const int*>(up(cnt.data(), cnt.size() * sizeof(int)));
 
-  // walks-ending family E_2..E_k (E_1 = z)
+  // tasks: per head, chunks of <= kChunk of its arcs (offsets n + 1)
+  auto tasks = [&](const std::vector<int64_t>& off, SArcs& A) {
+    std::vector<int32_t> th, tl;
+    std::vector<int64_t> ta;
+    for (int32_t h = 0; h < n; ++h)
+      for (int64_t a = off[h]; a < off[h + 1]; a += kChunk) {
+        th.push_back(h);
+        ta.push_back(a);
+        tl.push_back(static_cast<int32_t>(std::min<int64_t>(kChunk, off[h + 1] - a)));
+      }
+    A.ntask = static_cast<int64_t>(th.size());
+    A.task_head = static_cast<const int32_t*>(up(th.data(), th.size() * 4));
+    A.task_a0 = static_cast<const int64_t*>(up(ta.data(), ta.size() * 8));
+    A.task_len = static_cast<const int32_t*>(up(tl.data(), tl.size() * 4));
+  };
+  int mx = 1;
+  for (int l = 1; l <= k; ++l) mx = std::max(mx, cnt[l]);
+  auto* ug = static_cast<uint64_t*>(alloc(static_cast<size_t>(n) * mx * 8));
+  auto zmap = [&](const uint64_t* src, int lin, uint64_t* dst) {  // lin = src's subset size
+    SZmap Z;
+    Z.n = n;
+    Z.src = src;
+    Z.Ein = cnt[lin];
+    Z.dst = dst;
+    Z.Eout = cnt[lin + 1];
+    Z.zj = in.zj;
+    Z.k = k;
+    Z.jp = jp[lin + 1];
+    Z.jcnt = cnt[lin] * (k - lin) / k;  // C(k-1, lin)
+    prof_begin("static_coef_zmap", st);
+    k_static_zmap<<<grid_for(n), kSW * 32, 0, st>>>(Z);
+    prof_end(st);
+  };
+  auto arcs = [&](SArcs A, const uint64_t* src, uint64_t* dst, int E, uint64_t role, int lvl) {
+    A.src = src;
+    A.dst = dst;
+    A.E = E;
+    A.pre = draw_prefix(in.seed, role);
+    A.yb = static_cast<uint64_t>(lvl) + 0x165667b19e3779f9ull;
+    cudaMemsetAsync(dst, 0, static_cast<size_t>(n) * E * 8, st);
+    if (!A.ntask) return;
+    prof_begin("static_coef_arcs", st);
+    k_static_arcs<<<grid_for(A.ntask), kSW * 32, 0, st>>>(A);
+    prof_end(st);
+  };
+
+  // walks-ending family E_2..E_k (E_1 = z): E_l = zmap(XOR_{t -> h} y E_{l-1}[t])
+  SArcs IN, OUT;
+  IN.tail = in.in_tail;
+  IN.edge = in.in_edge;
+  OUT.tail = in.out_tail;
+  OUT.edge = in.out_edge;
+  tasks(*in.h_in_off, IN);
   std::vector<uint64_t*> E(static_cast<size_t>(k) + 1, nullptr);
   E[1] = const_cast<uint64_t*>(in.zj);
-  SLevel L;
-  L.zj = in.zj;
-  L.k = k;
   for (int l = 2; l <= k; ++l) {
     E[l] = static_cast<uint64_t*>(alloc(static_cast<size_t>(n) * cnt[l] * 8));
-    cudaMemsetAsync(E[l], 0, static_cast<size_t>(n) * cnt[l] * 8, st);
-    L.nlist = n;  // heads without arcs write zero rows
-    L.list = nullptr;
-    L.off = in.in_off;
-    L.tail = in.in_tail;
-    L.edge = in.in_edge;
-    L.src = E[l - 1];
-    L.Ein = cnt[l - 1];
-    L.dst = E[l];
-    L.Eout = cnt[l];
-    L.pre = draw_prefix(in.seed, kRoleEdgeY);
-    L.yb = static_cast<uint64_t>(l - 1) + 0x165667b19e3779f9ull;
-    L.jp = jp[l];
-    L.jcnt = cnt[l - 1] * (k - l + 1) / k;  // C(k-1, l-1)
-    L.self = false;
-    if (L.nlist) {
-      prof_begin("static_coef", st);
-      k_static_coef<<<grid_for(L.nlist), kSW * 32, 0, st>>>(L);
-      prof_end(st);
-    }
+    arcs(IN, E[l - 1], ug, cnt[l - 1], kRoleEdgeY, l - 1);
+    zmap(ug, l - 1, E[l]);
   }
-  // walks-starting family S_2..S_k (S_1 = 1): Z_b = zmap_v(S_{b-1}) per
-  // vertex (Z_2 = z), then S_b[h] = XOR_{h -> v} y2 * Z_b[v]
+  // walks-starting family S_2..S_k (S_1 = 1): S_b[h] = XOR_{h -> v} y2 * zmap_v(S_{b-1}[v])
+  // (zmap(S_1) = z); every S_b is kept for the readout
   std::vector<uint64_t*> Sb(static_cast<size_t>(k) + 1, nullptr);
   if (in.junction) {
-    uint64_t* zbuf = nullptr;
+    tasks(*in.h_out_off, OUT);
     for (int b = 2; b <= k; ++b) {
-      const uint64_t* Z = in.zj;  // b = 2: zmap(1) = z
+      const uint64_t* Z = in.zj;
       if (b > 2) {
-        zbuf = static_cast<uint64_t*>(alloc(static_cast<size_t>(n) * cnt[b - 1] * 8));
-        SLevel V;
-        V.nlist = n;
-        V.src = Sb[b - 1];
-        V.Ein = cnt[b - 2];
-        V.dst = zbuf;
-        V.Eout = cnt[b - 1];
-        V.zj = in.zj;
-        V.k = k;
-        V.jp = jp[b - 1];
-        V.jcnt = cnt[b - 2] * (k - b + 2) / k;  // C(k-1, b-2)
-        V.self = true;
-        prof_begin("static_coef", st);
-        k_static_coef<<<grid_for(n), kSW * 32, 0, st>>>(V);
-        prof_end(st);
-        Z = zbuf;
+        zmap(Sb[b - 1], b - 2, ug);
+        Z = ug;
       }
       Sb[b] = static_cast<uint64_t*>(alloc(static_cast<size_t>(n) * cnt[b - 1] * 8));
-      cudaMemsetAsync(Sb[b], 0, static_cast<size_t>(n) * cnt[b - 1] * 8, st);
-      SLevel O;
-      O.nlist = n;
-      O.list = nullptr;
-      O.off = in.out_off;
-      O.tail = in.out_tail;
-      O.edge = in.out_edge;
-      O.src = Z;
-      O.Ein = cnt[b - 1];
-      O.dst = Sb[b];
-      O.Eout = cnt[b - 1];
-      O.pre = draw_prefix(in.seed, 4);  // Role::edge_y2 (gf.hpp:116)
-      O.yb = static_cast<uint64_t>(b - 1) + 0x165667b19e3779f9ull;
-      O.zj = nullptr;
-      if (O.nlist) {
-        prof_begin("static_coef", st);
-        k_static_coef<<<grid_for(O.nlist), kSW * 32, 0, st>>>(O);
-        prof_end(st);
-      }
-      if (zbuf) {
-        release(zbuf);
-        zbuf = nullptr;
-      }
-      // S_{b-1} is still needed by the readout: all S_b are kept (they are
-      // the smaller half of the rows: sum_b C(k, b-1) = 2^k - C(k, k))
+      arcs(OUT, Z, Sb[b], cnt[b - 1], 4 /* Role::edge_y2 */, b - 1);
     }
   }
   SReadout R;
@@ -337,6 +372,7 @@ void eval_static_coef(const StaticCoefInputs& in, cudaStream_t st,
   for (int l = 2; l <= k; ++l) release(E[l]);
   for (int b = 2; b <= k; ++b)
     if (Sb[b]) release(Sb[b]);
+  release(ug);
 }
 
 }  // namespace tsv

@@ -2472,27 +2472,36 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
     if (n < 0 || ms < 0) throw std::invalid_argument("negative size");
     // head-sorted arc lists of the projection: in-arcs (tail -> head) and
     // out-arcs (head = the walk's current vertex, tail = the next one)
+    // head-grouped arc lists (counting sort on all host threads; the order
+    // within a head is free: both engines XOR a head's arcs, so the placement
+    // races only over positions inside the head's range)
     auto arcs = [&](bool incoming, std::vector<int32_t>& head, std::vector<int32_t>& tail,
                     std::vector<int32_t>& edge, std::vector<int64_t>* head_off = nullptr) {
       const int64_t A = directed ? ms : 2 * ms;
       std::vector<int64_t> off(static_cast<size_t>(n) + 1, 0);
+      int64_t bad = 0;
+#pragma omp parallel for schedule(static) reduction(+ : bad) if (ms > (1 << 20))
       for (int64_t i = 0; i < ms; ++i) {
-        if (a[i] < 0 || a[i] >= n || b[i] < 0 || b[i] >= n)
-          throw std::invalid_argument("edge endpoint out of range");
-        ++off[(incoming ? b[i] : a[i]) + 1];
-        if (!directed) ++off[(incoming ? a[i] : b[i]) + 1];
+        if (a[i] < 0 || a[i] >= n || b[i] < 0 || b[i] >= n) {
+          ++bad;
+          continue;
+        }
+        __atomic_fetch_add(&off[(incoming ? b[i] : a[i]) + 1], 1, __ATOMIC_RELAXED);
+        if (!directed) __atomic_fetch_add(&off[(incoming ? a[i] : b[i]) + 1], 1, __ATOMIC_RELAXED);
       }
+      if (bad) throw std::invalid_argument("edge endpoint out of range");
       for (int32_t x = 0; x < n; ++x) off[x + 1] += off[x];
       if (head_off) *head_off = off;
       head.resize(static_cast<size_t>(A));
       tail.resize(static_cast<size_t>(A));
       edge.resize(static_cast<size_t>(A));
       auto put = [&](int32_t h, int32_t t, int64_t e) {
-        const int64_t p = off[h]++;
+        const int64_t p = __atomic_fetch_add(&off[h], 1, __ATOMIC_RELAXED);
         head[p] = h;
         tail[p] = t;
         edge[p] = static_cast<int32_t>(e);
       };
+#pragma omp parallel for schedule(static) if (ms > (1 << 20))
       for (int64_t i = 0; i < ms; ++i) {
         if (incoming) put(b[i], a[i], i); else put(a[i], b[i], i);
         if (!directed) { if (incoming) put(a[i], b[i], i); else put(b[i], a[i], i); }
@@ -2525,9 +2534,20 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
     if (cfg->field_bits == 64 && tsv::static_coef_supported(k) &&
         !(se && std::strcmp(se, "points") == 0) && cwords <= cfg->memory_cap_words &&
         fits_device(cwords)) {
+      const char* tre = std::getenv("TSV_TRACE_API");
+      const bool trace = tre && tre[0] == '1';
+      const auto t0 = std::chrono::steady_clock::now();
+      auto mark = [&](const char* what) {
+        if (!trace) return;
+        cudaStreamSynchronize(st);
+        std::fprintf(stderr, "[static] %-26s %9.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() -
+                                                               t0).count());
+      };
       std::vector<int64_t> ioff, ooff;
       arcs(true, ih, it, ie, &ioff);
       if (junction) arcs(false, oh, ot, oe, &ooff);
+      mark("host arc lists");
       std::vector<int32_t> off(vertex_off, vertex_off + n + 1);
       std::vector<int32_t> shv(vertex_shades, vertex_shades + vertex_off[n]);
       for (int32_t s : shv)
@@ -2559,6 +2579,8 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
         ci.junction = junction != 0;
         ci.seed = cfg->seed;
         ci.in_off = static_cast<const int64_t*>(upv(ioff));
+        ci.h_in_off = &ioff;
+        ci.h_out_off = &ooff;
         ci.in_tail = static_cast<const int32_t*>(upv(it));
         ci.in_edge = static_cast<const int32_t*>(upv(ie));
         if (junction) {
@@ -2581,7 +2603,9 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
         TSV_CUDA(cudaMemsetAsync(acc, 0, static_cast<size_t>(n) * 8 + 8, st));
         ci.acc = acc;
         ci.tables = &coef_const_tables(k);
+        mark("uploads, shade table");
         tsv::eval_static_coef(ci, st, alloc, release);
+        mark("coefficient sieve");
         TSV_CUDA(cudaGetLastError());
         if (n)
           TSV_CUDA(cudaMemcpyAsync(accumulators, acc, static_cast<size_t>(n) * 8,

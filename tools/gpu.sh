@@ -19,6 +19,8 @@
 #                            ncu --set full of `tools/one_eval.py CFG SCALE 2`
 #   launcheval:TAG,CFG[,SCALE]
 #                            ncu launch list (gpu__time_duration) of the same
+#   launchpy:TAG,SCRIPT[,ARGS]
+#                            ncu launch list (gpu__time_duration) of python SCRIPT ARGS
 #   sanitize:TOOL[,K]        compute-sanitizer --tool TOOL over pytest -m gpu -k K
 #   py:SCRIPT[,ARGS]         python SCRIPT ARGS                          -> py_<i>.log
 cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
@@ -81,6 +83,11 @@ for job in "$@"; do
       timeout 1800 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
           --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1
       echo "launcheval $tag rc=$?"; tail -3 gpurun_out/ncu_launch_$tag.log ;;
+    launchpy)
+      tag=${A[0]}; rest=("${A[@]:1}")
+      timeout 2400 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+          --log-file gpurun_out/launches_$tag.csv python "${rest[@]}" > gpurun_out/ncu_launch_$tag.log 2>&1
+      echo "launchpy $tag rc=$?"; tail -3 gpurun_out/ncu_launch_$tag.log ;;
     sanitize)
       tool=${A[0]}; k=${A[1]:-small}
       timeout 2400 compute-sanitizer --tool "$tool" --print-limit 20 \
