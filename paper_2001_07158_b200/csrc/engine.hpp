@@ -160,6 +160,9 @@ void launch_k1(int32_t n, const uint64_t* zj, Batch b, int32_t anchor_source,
                int32_t color = -1, int32_t wild = -1);
 // positional z_{u,j} = draw(seed, label_z, u, j+1) (build_zj_positional, sieve.cpp:103-113)
 // launch_zj with w = identity (the coefficient engine's shade basis)
+// the shade CSR of a table where every vertex has the same list `pattern` (c entries)
+void launch_uniform_csr(int32_t n, int c, const int32_t* pattern, int32_t* off, int32_t* shades,
+                        cudaStream_t st);
 void launch_zj_ident(int32_t n, int k, uint64_t seed, const int32_t* vertex_off,
                      const int32_t* vertex_shades, uint64_t* zj, cudaStream_t st);
 void launch_zj_positional(int32_t n, int k, uint64_t seed, uint64_t* zj, cudaStream_t st);

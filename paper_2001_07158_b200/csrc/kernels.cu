@@ -762,6 +762,18 @@ unsigned blocks_for(int64_t n, int threads) {
   return static_cast<unsigned>((n + threads - 1) / threads);
 }
 
+
+// Shade CSR in which every vertex carries the same shade list (k-TempPath:
+// all k shades; C5): off[i] = i * c, shades[i * c + j] = pattern[j].
+__global__ void k_uniform_csr(int32_t n, int c, const int32_t* __restrict__ pattern,
+                              int32_t* __restrict__ off, int32_t* __restrict__ shades) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  off[i] = static_cast<int32_t>(i * c);
+  if (i < n)
+    for (int j = 0; j < c; ++j) shades[i * c + j] = pattern[j];
+}
+
 }  // namespace
 
 void launch_level(const LevelParams& p, cudaStream_t st) {
@@ -879,6 +891,12 @@ void launch_draw_y(uint64_t seed, int32_t level, int64_t n, const int32_t* edges
                    uint64_t* out, cudaStream_t st) {
   if (n == 0) return;
   k_draw_y<<<blocks_for(n, 256), 256, 0, st>>>(seed, level, n, edges, out);
+}
+
+void launch_uniform_csr(int32_t n, int c, const int32_t* pattern, int32_t* off, int32_t* shades,
+                        cudaStream_t st) {
+  k_uniform_csr<<<blocks_for(static_cast<int64_t>(n) + 1, 256), 256, 0, st>>>(n, c, pattern, off,
+                                                                               shades);
 }
 
 }  // namespace tsv

@@ -232,6 +232,9 @@ struct tsv_graph {
   mutable std::shared_ptr<tsv_shades> shade_cache;
   mutable std::vector<int32_t> shade_off_copy, shade_vs_copy;
   mutable int shade_k = 0;
+  mutable bool shade_uniform = false;  // cached CSR = every vertex shade_upat
+  mutable int32_t shade_uc = 0;
+  mutable std::vector<int32_t> shade_upat;
   // stream of the synchronous entry points (created once per graph)
   mutable std::mutex stream_mu;
   mutable cudaStream_t api_stream = nullptr;
@@ -1823,6 +1826,31 @@ int tsv_graph_edges(const tsv_graph* g, int32_t* u, int32_t* v, int32_t* ts) {
   });
 }
 
+// Does every vertex carry the same shade list (k-TempPath: all k shades)?
+// Then the CSR is (c, pattern) -- one parallel read of the caller's arrays
+// instead of a 2.4 GB upload and host copy at C5.
+static bool uniform_shades(int32_t n, const int32_t* off, const int32_t* vs, int32_t* c_out,
+                           std::vector<int32_t>* pattern) {
+  if (n < 1 || off[0] != 0) return false;
+  const int32_t c = off[1] - off[0];
+  if (c < 0 || static_cast<int64_t>(n) * c > INT32_MAX) return false;
+  int bad = 0;
+#pragma omp parallel for schedule(static) reduction(| : bad) if (n > (1 << 16))
+  for (int32_t i = 0; i < n; ++i) {
+    if (bad) continue;
+    if (off[i + 1] - off[i] != c || off[i] != static_cast<int64_t>(i) * c) {
+      bad = 1;
+      continue;
+    }
+    for (int32_t j = 0; j < c; ++j)
+      if (vs[static_cast<int64_t>(i) * c + j] != vs[j]) bad = 1;
+  }
+  if (bad) return false;
+  *c_out = c;
+  pattern->assign(vs, vs + c);
+  return true;
+}
+
 int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
                       const int32_t* vertex_shades, tsv_shades** out) {
   return guard([&] {
@@ -1860,8 +1888,22 @@ int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
       TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->shades),
                                std::max<size_t>(static_cast<size_t>(cnt), 1) * 4, nullptr));
       TSV_CUDA(cudaStreamSynchronize(nullptr));
-      copy_to_device(s->off, vertex_off, (static_cast<size_t>(n) + 1) * 4, nullptr);
-      copy_to_device(s->shades, vertex_shades, static_cast<size_t>(cnt) * 4, nullptr);
+      int32_t c = 0;
+      std::vector<int32_t> pattern;
+      if (cnt > (int64_t{1} << 20) && uniform_shades(n, vertex_off, vertex_shades, &c, &pattern)) {
+        // every vertex the same list: expand (c, pattern) on the device
+        int32_t* dp = nullptr;
+        TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dp), std::max<size_t>(c, 1) * 4,
+                                 nullptr));
+        TSV_CUDA(cudaMemcpy(dp, pattern.data(), static_cast<size_t>(c) * 4,
+                            cudaMemcpyHostToDevice));
+        tsv::launch_uniform_csr(n, c, dp, s->off, s->shades, nullptr);
+        TSV_CUDA(cudaFreeAsync(dp, nullptr));
+        TSV_CUDA(cudaStreamSynchronize(nullptr));
+      } else {
+        copy_to_device(s->off, vertex_off, (static_cast<size_t>(n) + 1) * 4, nullptr);
+        copy_to_device(s->shades, vertex_shades, static_cast<size_t>(cnt) * 4, nullptr);
+      }
     } catch (...) {
       delete s;
       throw;
@@ -1912,15 +1954,23 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     if (cnt < 0 || (cnt > 0 && !vertex_shades)) throw std::invalid_argument("null argument");
     // a repeated shade table (every probe of one query) is not uploaded
     // again: reuse the cached device copy when the CSR is word-for-word equal
+    // (a uniform CSR -- every vertex the same list -- is kept as its pattern)
     std::shared_ptr<tsv_shades> hold;
+    int32_t uc = 0;
+    std::vector<int32_t> upat;
+    const bool uni = cnt > (int64_t{1} << 20) &&
+                     uniform_shades(n, vertex_off, vertex_shades, &uc, &upat);
     {
       std::lock_guard<std::mutex> lk(g->shade_mu);
-      if (g->shade_cache && g->shade_k == k &&
-          g->shade_off_copy.size() == static_cast<size_t>(n) + 1 &&
-          g->shade_vs_copy.size() == static_cast<size_t>(cnt) &&
-          equal_par(g->shade_off_copy.data(), vertex_off, static_cast<size_t>(n) + 1) &&
-          equal_par(g->shade_vs_copy.data(), vertex_shades, static_cast<size_t>(cnt)))
-        hold = g->shade_cache;
+      if (g->shade_cache && g->shade_k == k) {
+        if (g->shade_uniform)
+          hold = uni && uc == g->shade_uc && upat == g->shade_upat ? g->shade_cache : nullptr;
+        else if (!uni && g->shade_off_copy.size() == static_cast<size_t>(n) + 1 &&
+                 g->shade_vs_copy.size() == static_cast<size_t>(cnt) &&
+                 equal_par(g->shade_off_copy.data(), vertex_off, static_cast<size_t>(n) + 1) &&
+                 equal_par(g->shade_vs_copy.data(), vertex_shades, static_cast<size_t>(cnt)))
+          hold = g->shade_cache;
+      }
     }
     mark(hold ? "shade compare (hit)" : "shade compare (miss)", nullptr);
     if (!hold) {
@@ -1932,8 +1982,16 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
       std::lock_guard<std::mutex> lk(g->shade_mu);
       g->shade_cache = hold;
       g->shade_k = k;
-      copy_par(g->shade_off_copy, vertex_off, static_cast<size_t>(n) + 1);
-      copy_par(g->shade_vs_copy, vertex_shades, static_cast<size_t>(cnt));
+      g->shade_uniform = uni;
+      if (uni) {
+        g->shade_uc = uc;
+        g->shade_upat = upat;
+        std::vector<int32_t>().swap(g->shade_off_copy);
+        std::vector<int32_t>().swap(g->shade_vs_copy);
+      } else {
+        copy_par(g->shade_off_copy, vertex_off, static_cast<size_t>(n) + 1);
+        copy_par(g->shade_vs_copy, vertex_shades, static_cast<size_t>(cnt));
+      }
       mark("shade upload + host copy", nullptr);
     }
     DeviceGuard dg(g->device);
