@@ -53,6 +53,13 @@
 #endif
 // resident blocks per SM the register budget is sized for (1: unbounded;
 // capping at 8 two-warp blocks spilled and ran slower)
+// products interleaved per loop trip (arc products / z map); 1 = rolled
+#ifndef TSV_VUNROLL
+#define TSV_VUNROLL 1
+#endif
+#ifndef TSV_ZUNROLL
+#define TSV_ZUNROLL 1
+#endif
 #ifndef TSV_VMINB
 #define TSV_VMINB 1
 #endif
@@ -63,6 +70,7 @@ namespace {
 constexpr unsigned kFullV = 0xffffffffu;
 constexpr int kVWarps = 2;   // warps per block
 constexpr int kQCap = 64;    // queued rows per warp (ring)
+constexpr int kVUnroll = TSV_VUNROLL, kZUnroll = TSV_ZUNROLL;
 
 __host__ __device__ constexpr int binom_c(int n, int r) {
   if (r < 0 || r > n) return 0;
@@ -219,7 +227,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       // one product per input entry and one per output (C5, L = 3: 20
       // instead of 30).  W rides in shared memory, the loops stay rolled.
       if constexpr (kZPairOk) {
-#pragma unroll 1
+#pragma unroll kZUnroll
         for (int p = 0; p < E; ++p) {
           const unsigned pm = S.pmask[p];
           uint64_t zp = 0;
@@ -227,7 +235,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
           for (int j = 0; j < K; ++j) zp ^= ((pm >> j) & 1u) ? z[j] : 0ull;
           S.w[p][lane] = gf_reduce_alu(clmul64_kara_s(ksplit(zp), ksplit(S.q[p][qi])));
         }
-#pragma unroll 1
+#pragma unroll kZUnroll
         for (int o = 0; o < F; ++o) {
           uint64_t zt = 0, su = 0, sw = 0;
 #pragma unroll
@@ -295,7 +303,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
     if (LAST && live) live = __ldg(P.g.run_ts + run) <= P.max_ts;
     if (live) {
       const KSplit ys = ksplit(draw_edge_y(pre, yb, meta & kEdgeMask));
-#pragma unroll 1
+#pragma unroll kVUnroll
       for (int e = 0; e < E; ++e)
         S.u[e][lane] ^= gf_reduce_alu(clmul64_kara_s(ys, ksplit(S.x[i & 1][e][lane])));
     }
