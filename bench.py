@@ -865,6 +865,18 @@ def main():
             cpu = {"value": r["value"], "unit": "updates/s", "cores": r["threads"],
                    "kind": r["kind"], "sample": r["sample"], "seconds": r["seconds"],
                    "cpu_model": cpu_model(), "window_parity": r.get("window_parity")}
+            # calibration of the sampled rate: the whole evaluation's CPU time
+            # when the full-size golden was made (reference or OpenMP port,
+            # tests/golden/full_size.json; the build container's cores)
+            if gold is not None:
+                e0 = gold[1][0]
+                secs = e0.get("reference_seconds") or e0.get("oracle_seconds")
+                if secs:
+                    thr = e0.get("reference_threads") or e0.get("oracle_threads")
+                    cpu["full_run_calibration"] = {
+                        "seconds": secs, "threads": thr, "source": e0.get("source"),
+                        "updates_per_s": inst.updates() / secs,
+                        "note": "one whole evaluation on the golden-making host"}
         except Exception as e:  # reported, never fatal
             cpu = {"value": None, "unit": "updates/s", "cores": 0, "kind": "unavailable",
                    "sample": str(e)}
