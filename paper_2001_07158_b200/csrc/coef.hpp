@@ -113,6 +113,8 @@ struct VertList {
   int32_t* count = nullptr;  // its arcs
 };
 bool vertex_engine_supports(int k);
+// row stride (words) of the vertex-lane engine's level-l state rows
+int vertex_row_words(int k, int l);
 // The list of the vertices in [v_lo, v_hi) (v_hi < 0: all).
 void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
                        const std::function<void*(size_t)>& alloc,

@@ -70,6 +70,14 @@ namespace {
 constexpr unsigned kFullV = 0xffffffffu;
 constexpr int kVWarps = 2;   // warps per block
 constexpr int kQCap = 64;    // queued rows per warp (ring)
+
+// Row stride of level l's state rows: C(k, l) words padded to a multiple of
+// four (32 bytes, one DRAM sector) when TSV_VPAD, so that every row starts
+// on a sector and a row write never shares a sector with a neighbor row.
+#ifndef TSV_VPAD
+#define TSV_VPAD 0
+#endif
+__host__ __device__ constexpr int vpad(int w) { return TSV_VPAD ? (w + 3) & ~3 : w; }
 constexpr int kVUnroll = TSV_VUNROLL, kZUnroll = TSV_ZUNROLL;
 
 __host__ __device__ constexpr int binom_c(int n, int r) {
@@ -217,7 +225,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       uint64_t z[K];
 #pragma unroll
       for (int j = 0; j < K; ++j) z[j] = __ldg(P.zj + static_cast<int64_t>(hd) * K + j);
-      uint64_t* out = P.ubuf + static_cast<int64_t>(S.q_slot[qi]) * F;
+      uint64_t* out = P.ubuf + static_cast<int64_t>(S.q_slot[qi]) * vpad(F);
 #if TSV_ZPAIR == 2
       // paired z map: with z_X = XOR_{j in X} z_j,
       //   z_T * (XOR_{P in T, |P| = L-1} U[P])
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       live = src >= 0;
       if (FIRST) live = live && (P.anchor_source < 0 || src == P.anchor_source);
       if (live) {
-        const uint64_t* row = rows + static_cast<int64_t>(src) * E;
+        const uint64_t* row = rows + static_cast<int64_t>(src) * (FIRST ? E : vpad(E));
 #pragma unroll
         for (int e = 0; e < E; ++e) cp_async8(&S.x[i & 1][e][lane], row + e);
       }
@@ -435,6 +443,8 @@ inline unsigned nblk_v(int64_t n) { return static_cast<unsigned>((n + 255) / 256
 }  // namespace
 
 bool vertex_engine_supports(int k) { return k >= 2 && k <= kVertexMaxK; }
+
+int vertex_row_words(int k, int l) { return vpad(binom_c(k, l)); }
 
 void build_vertex_list(const DevGraph& g, VertList& out, cudaStream_t st,
                        const std::function<void*(size_t)>& alloc,

@@ -763,6 +763,8 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   tmark("shade table");
   // state rows: S slots, or per window its slots plus n carry slots
   const uint64_t rows = windowed ? static_cast<uint64_t>(rows_cap) + n : S;
+  if (!vc && !windowed && sh->single == 0 && tsv::vertex_engine_supports(k))
+    for (int l = 2; l < k; ++l) M = std::max<int64_t>(M, tsv::vertex_row_words(k, l));
   DevBuf X(rows * M * 8, st), Y(rows * M * 8, st);
   // every shaded vertex multi-shade and small k (k-TempPath, C5): the
   // vertex-lane engine (coef_vertex.cu) -- fused z map and readout, so none
@@ -2064,8 +2066,9 @@ int tsv_vertex_partition(const tsv_graph* g, const tsv_shades* s, int k, int ran
     out->slot_lo = vp.slot_lo;
     out->slot_hi = vp.slot_hi;
     out->slots = g->dev.S;
+    for (int l = 1; l < k; ++l) M = std::max<int64_t>(M, tsv::vertex_row_words(k, l));
     out->state_words = std::max<int64_t>(g->dev.S, 1) * M;
-    for (int l = 0; l <= k && l < 32; ++l) out->row_words[l] = static_cast<int32_t>(T.count[l]);
+    for (int l = 0; l <= k && l < 32; ++l) out->row_words[l] = tsv::vertex_row_words(k, l);
   });
 }
 
