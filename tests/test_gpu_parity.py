@@ -501,7 +501,7 @@ def test_static_coefficient_engine_equals_point_engine(cuda_device, monkeypatch,
     point form (static_kernels.cu, every sieve point; pinned against the
     reference through test_default_preprocessing_matches_reference):
     single-, multi-shade and shadeless vertices, directed and undirected
-    projections with repeated vertices, k = 1..8."""
+    projections with repeated vertices, k = 1..12."""
     import ctypes as C
     L = _native.lib()
     rng = np.random.default_rng(41 + junction)
@@ -514,7 +514,7 @@ def test_static_coefficient_engine_equals_point_engine(cuda_device, monkeypatch,
         keep = a != b
         a, b = a[keep], b[keep]
         directed = int(i % 2)
-        k = int(rng.integers(1, 9))
+        k = int(rng.integers(1, 9)) if i < 18 else int(rng.integers(9, 13))  # up to C4's 12
         q = int(rng.integers(1, 5))
         colors = rng.integers(1, q + 2, n).astype(np.int32)  # color q+1: no shade
         motif = sorted(int(x) for x in rng.integers(1, q + 1, k))
