@@ -111,6 +111,118 @@ struct DevBuf {
   }
 };
 
+// The coefficient engine's two big state buffers (C5: 2 x 38 GB) come from
+// a per-device cache that keeps them across evaluations -- also across
+// graphs: a fresh graph's evaluation would otherwise re-map tens of GB
+// through the stream-ordered pool (0.2-3 s at C5 in the end-to-end legs).
+// A buffer is reused when large enough and free; its last user's stream
+// work is ordered before the next user's by an event.  Small buffers go
+// through the pool as before.
+struct StateBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int dev = -1;
+  cudaStream_t st = nullptr;
+  StateBuf(size_t want, cudaStream_t s);
+  ~StateBuf();
+  StateBuf(const StateBuf&) = delete;
+  StateBuf& operator=(const StateBuf&) = delete;
+  template <typename T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+namespace {
+struct CachedState {
+  int dev;
+  void* p;
+  size_t bytes;
+  bool busy;
+  cudaEvent_t done;  // recorded on the last user's stream at release
+};
+std::mutex g_state_mu;
+std::vector<CachedState> g_state;
+constexpr size_t kStateCacheMin = size_t{1} << 30;  // cache buffers >= 1 GiB
+constexpr int kStateCacheMax = 8;
+}  // namespace
+
+StateBuf::StateBuf(size_t want, cudaStream_t s) : st(s) {
+  TSV_CUDA(cudaGetDevice(&dev));
+  want = want ? want : 8;
+  if (want >= kStateCacheMin && !std::getenv("TSV_NO_STATE_CACHE")) {
+    std::lock_guard<std::mutex> lk(g_state_mu);
+    int best = -1;
+    for (size_t i = 0; i < g_state.size(); ++i) {
+      const CachedState& c = g_state[i];
+      if (c.dev == dev && !c.busy && c.bytes >= want &&
+          (best < 0 || c.bytes < g_state[best].bytes))
+        best = static_cast<int>(i);
+    }
+    if (best >= 0) {
+      CachedState& c = g_state[best];
+      c.busy = true;
+      TSV_CUDA(cudaStreamWaitEvent(st, c.done, 0));
+      p = c.p;
+      bytes = c.bytes;
+      return;
+    }
+    // make room: drop free cached buffers of this device that are too small
+    for (size_t i = 0; i < g_state.size();) {
+      CachedState& c = g_state[i];
+      if (c.dev == dev && !c.busy) {
+        cudaEventSynchronize(c.done);
+        cudaEventDestroy(c.done);
+        cudaFree(c.p);
+        g_state.erase(g_state.begin() + static_cast<long>(i));
+      } else {
+        ++i;
+      }
+    }
+    if (static_cast<int>(g_state.size()) < kStateCacheMax) {
+      void* q = nullptr;
+      if (cudaMalloc(&q, want) != cudaSuccess) {
+        // the stream-ordered pool may hold the memory: trim it and retry,
+        // else fall back to a pool allocation
+        cudaGetLastError();
+        cudaMemPool_t pool = nullptr;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          cudaDeviceSynchronize();
+          cudaMemPoolTrimTo(pool, 0);
+        }
+        if (cudaMalloc(&q, want) != cudaSuccess) {
+          cudaGetLastError();
+          TSV_CUDA(cudaMallocAsync(&p, want, st));
+          bytes = 0;
+          return;
+        }
+      }
+      cudaEvent_t e = nullptr;
+      TSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      g_state.push_back({dev, q, want, true, e});
+      p = q;
+      bytes = want;
+      return;
+    }
+  }
+  TSV_CUDA(cudaMallocAsync(&p, want, st));
+  bytes = 0;  // pool allocation (not cached)
+}
+
+StateBuf::~StateBuf() {
+  if (!p) return;
+  if (!bytes) {
+    cudaFreeAsync(p, st);
+    return;
+  }
+  std::lock_guard<std::mutex> lk(g_state_mu);
+  for (CachedState& c : g_state)
+    if (c.p == p) {
+      cudaEventRecord(c.done, st);
+      c.busy = false;
+    }
+}
+
 // The state buffers (2*R*W words, up to ~130 GB at 1e9 edges) are stream-
 // ordered allocations; keep freed pool memory mapped so repeated
 // evaluations (probes, repetitions, steps) do not re-map it every time.
@@ -765,7 +877,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const uint64_t rows = windowed ? static_cast<uint64_t>(rows_cap) + n : S;
   if (!vc && !windowed && sh->single == 0 && tsv::vertex_engine_supports(k))
     for (int l = 2; l < k; ++l) M = std::max<int64_t>(M, tsv::vertex_row_words(k, l));
-  DevBuf X(rows * M * 8, st), Y(rows * M * 8, st);
+  std::unique_ptr<StateBuf> VX, VY;  // vertex path: cached state buffers
   // every shaded vertex multi-shade and small k (k-TempPath, C5): the
   // vertex-lane engine (coef_vertex.cu) -- fused z map and readout, so none
   // of the buffers below (ulast, flags, z-map lists, chunk aggregates)
@@ -776,7 +888,9 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   if (try_vertex && vertex_applicable(g, st)) {
     const tsv::VertList* vl = &vertex_part(g, 0, 1, st).vl;
     tmark("vertex list");
-    uint64_t *A = X.as<uint64_t>(), *B = Y.as<uint64_t>();
+    VX = std::make_unique<StateBuf>(rows * M * 8, st);
+    VY = std::make_unique<StateBuf>(rows * M * 8, st);
+    uint64_t *A = VX->as<uint64_t>(), *B = VY->as<uint64_t>();
     for (int l = 2; l <= k; ++l) {
       tsv::CoefParams cp;
       cp.g = g->dev;
@@ -796,6 +910,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     tmark("levels enqueued");
     return true;
   }
+  DevBuf X(rows * M * 8, st), Y(rows * M * 8, st);
   DevBuf ulast(std::max<uint64_t>(n, 1) * k * 8, st), slot_head(std::getenv("TSV_ZTRANS") ? S * 4 : 8, st);
   // zero skipping and the single-shade form (CoefParams::vsh); positional z
   // keeps the plain z map
