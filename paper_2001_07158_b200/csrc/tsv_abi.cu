@@ -147,6 +147,16 @@ constexpr size_t kStateCacheMin = size_t{1} << 30;  // cache buffers >= 1 GiB
 constexpr int kStateCacheMax = 8;
 }  // namespace
 
+// bytes of this device's free cached state buffers (a vertex-path
+// evaluation's state comes out of them, so they count as available)
+size_t cached_state_free(int dev) {
+  std::lock_guard<std::mutex> lk(g_state_mu);
+  size_t b = 0;
+  for (const CachedState& c : g_state)
+    if (c.dev == dev && !c.busy) b += c.bytes;
+  return b;
+}
+
 StateBuf::StateBuf(size_t want, cudaStream_t s) : st(s) {
   TSV_CUDA(cudaGetDevice(&dev));
   want = want ? want : 8;
@@ -764,7 +774,13 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
   const uint64_t C = static_cast<uint64_t>(std::max<int64_t>(g->dev.C, 1));
   const uint64_t words = 2 * S * M + C * MA + 2 * n * k + 2 * n + S + (n + S) / 8 + 2;
   tmark("tables, subgraph");
-  const bool fits = words <= cfg->memory_cap_words && fits_device(words);
+  // (the vertex path takes its two state buffers from the per-device cache)
+  int cur_dev = 0;
+  TSV_CUDA(cudaGetDevice(&cur_dev));
+  const uint64_t cached = static_cast<uint64_t>(cached_state_free(cur_dev)) / 8;
+  const bool vertex_like = !vc && sh->single == 0 && tsv::vertex_engine_supports(k);
+  const uint64_t need = vertex_like ? words - std::min<uint64_t>(cached, 2 * S * M) : words;
+  const bool fits = words <= cfg->memory_cap_words && fits_device(need);
   tmark("fits_device");
   // time windows (coef_window.cu) when the state rows do not fit at once:
   // instant edge model, shade structure (not the VC sieve's positional z)
