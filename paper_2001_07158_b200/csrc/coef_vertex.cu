@@ -63,6 +63,17 @@
 #ifndef TSV_VMINB
 #define TSV_VMINB 1
 #endif
+// arc products y * row through the lane table (gf_device.cuh LaneTable: the
+// arc's y multiplies C(k, l-1) entries, the table build is paid once per
+// arc; measured 1.96e11 products/s against 1.18e11 for the holes product);
+// 0 = holes + Karatsuba as in the z map
+#ifndef TSV_VTABLE
+#define TSV_VTABLE 1
+#endif
+// the lane table serves levels with at least this many input entries
+#ifndef TSV_VTABLE_MINE
+#define TSV_VTABLE_MINE 1
+#endif
 
 namespace tsv {
 namespace {
@@ -144,49 +155,63 @@ struct VertArgs {
   uint64_t* acc;             // level k: per-vertex accumulators (XORed into)
 };
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
+// Row entries are read once: keep them out of the small L1 that is left
+// next to the shared-memory carve-out (the arc metadata lives there).
+__device__ __forceinline__ uint64_t ld_row64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
 }
 
-// Per-warp shared state.  Lane-minor layouts ([entry][lane], [entry][slot])
-// keep every access conflict-free.
+// Per-warp shared state.  Lane-minor layouts ([entry][slot]) keep every
+// access conflict-free.  The lane's running prefix U and the current / next
+// source rows live in registers; the paired z map's W row and the lane
+// table share the warp's scratch block (the table is dead during a flush).
 template <int E, int F, int L, bool LAST>
 struct VertSmem {
-  uint64_t x[2][E][32];                 // the next / current arc's source row (cp.async)
-  uint64_t u[E][32];                    // the lane's running prefix U_L
   uint64_t q[LAST ? 1 : E][kQCap];      // queued U rows (ring)
   int32_t q_slot[kQCap], q_head[kQCap];
   uint8_t pin[F > 0 ? F : 1][L], pj[F > 0 ? F : 1][L];  // output o: (rank of T_o - {j}, j) pairs
-#if TSV_ZPAIR == 2
-  uint64_t w[LAST ? 1 : E][32];         // paired z map: W[P] = z_P * U[P] of the lane's row
-  uint8_t pmask[E];                     // input entry P's subset mask
-#endif
+  uint8_t pmask[E];                     // input entry P's subset mask (paired z map)
 };
+
+// scratch bytes per warp: the lane table (4 KB, 4 KB aligned) or, without
+// it, the W rows of the paired z map
+template <int E, bool TAB>
+constexpr unsigned vert_scratch() { return TAB ? 4096u : static_cast<unsigned>(E) * 256u; }
+
+template <int K, int L>
+constexpr bool vert_uses_table() {
+  return TSV_VTABLE && binom_c(K, L - 1) >= TSV_VTABLE_MINE;
+}
 
 template <int K, int L, bool FIRST, bool LAST>
 __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const VertArgs A) {
   constexpr int E = binom_c(K, L - 1);  // input entries (row of level L-1)
   constexpr int F = binom_c(K, L);      // output entries
+  constexpr bool kTab = vert_uses_table<K, L>();
   // the paired z map pays E + F products against L * F
   constexpr bool kZPairOk = !LAST && E + F < L * F;
   using Sm = VertSmem<E, F, L, LAST>;
-  __shared__ Sm smem[kVWarps];
   const CoefParams& P = A.P;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  Sm& S = smem[wib];
+  // dynamic shared memory: the warps' scratch blocks (4 KB aligned in the
+  // shared window when they hold lane tables), then their VertSmem blocks
+  extern __shared__ __align__(16) uint8_t vsm_raw[];
+  const uint32_t raw_s = static_cast<uint32_t>(__cvta_generic_to_shared(vsm_raw));
+  const uint32_t scr_s = kTab ? (raw_s + 4095u) & ~4095u : raw_s;
+  constexpr unsigned kScr = vert_scratch<E, kTab>();
+  uint8_t* const scr_g = vsm_raw + (scr_s - raw_s);
+  Sm& S = reinterpret_cast<Sm*>(scr_g + kScr * kVWarps)[wib];
+  // W[p][lane] of the paired z map: entries c = p + 1 of the lane's table
+  // column (entry 0 stays the table's zero)
+  uint64_t* const wrow = reinterpret_cast<uint64_t*>(scr_g + kScr * wib) + (kTab ? 32 : 0) + lane;
+  LaneTable LT;
+  if (kTab) LT.init(scr_s + kScr * wib, lane);
   if (!LAST && lane == 0) {  // output pairs of the z map (colex order, coef_tables)
     constexpr SubsetTab<K, L> TL{};
-#if TSV_ZPAIR == 2
     constexpr SubsetTab<K, L - 1> TP{};
     for (int p = 0; p < E; ++p) S.pmask[p] = static_cast<uint8_t>(TP.mask[p]);
-#endif
     for (int o = 0; o < F; ++o) {
       int c = 0;
       for (int j = 0; j < K; ++j)
@@ -209,8 +234,9 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
   const uint64_t pre = draw_prefix(P.seed, kRoleEdgeY);
   const uint64_t yb = static_cast<uint64_t>(L - 1) + 0x165667b19e3779f9ull;
   const uint64_t* __restrict__ rows = FIRST ? P.zj : P.s_prev;
+  uint64_t u[E];  // the lane's running prefix U_L
 #pragma unroll
-  for (int e = 0; e < E; ++e) S.u[e][lane] = 0;
+  for (int e = 0; e < E; ++e) u[e] = 0;
   int qh = 0, qn = 0;  // ring head, queued count (warp-uniform)
 
   // z map of `take` queued rows (one per lane), stored as S rows of F words:
@@ -241,7 +267,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
           uint64_t zp = 0;
 #pragma unroll
           for (int j = 0; j < K; ++j) zp ^= ((pm >> j) & 1u) ? z[j] : 0ull;
-          S.w[p][lane] = gf_reduce_alu(clmul64_kara_s(ksplit(zp), ksplit(S.q[p][qi])));
+          wrow[p * 32] = gf_reduce_alu(clmul64_kara_s(ksplit(zp), ksplit(S.q[p][qi])));
         }
 #pragma unroll kZUnroll
         for (int o = 0; o < F; ++o) {
@@ -254,7 +280,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
             for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
             zt ^= zj;
             su ^= S.q[pi][qi];
-            sw ^= S.w[pi][lane];
+            sw ^= wrow[pi * 32];
           }
           out[o] = gf_reduce_alu(clmul64_kara_s(ksplit(zt), ksplit(su))) ^ sw;
         }
@@ -282,42 +308,63 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
     __syncwarp();
   };
 
-  // the next arc's source row goes to shared memory one step ahead (cp.async)
-  auto fetch = [&](int i, uint32_t& meta, bool& live) {
-    live = false;
+  // Software pipeline over the lane's arcs, so that no global load is
+  // waited for where it is issued: step i's metadata is loaded two steps
+  // ahead, its source row (registers) and its run's slot one step ahead.
+  auto ld_meta = [&](int i, uint32_t& meta, int32_t& src) {
     meta = 0;
+    src = -1;
     if (i < cnt) {
       const int64_t a = a0 + i;
       meta = __ldg(P.g.arc_meta + a);
-      const int32_t src = FIRST ? __ldg(P.g.arc_tail + a) : __ldg(P.g.arc_src + a);
-      live = src >= 0;
-      if (FIRST) live = live && (P.anchor_source < 0 || src == P.anchor_source);
-      if (live) {
-        const uint64_t* row = rows + static_cast<int64_t>(src) * (FIRST ? E : vpad(E));
+      src = FIRST ? __ldg(P.g.arc_tail + a) : __ldg(P.g.arc_src + a);
+      if (FIRST && P.anchor_source >= 0 && src != P.anchor_source) src = -1;
+    }
+  };
+  auto ld_row = [&](int32_t src, uint64_t (&x)[E]) {
+    if (src >= 0) {
+      const uint64_t* row = rows + static_cast<int64_t>(src) * (FIRST ? E : vpad(E));
 #pragma unroll
-        for (int e = 0; e < E; ++e) cp_async8(&S.x[i & 1][e][lane], row + e);
+      for (int e = 0; e < E; ++e) x[e] = ld_row64(row + e);
+    }
+  };
+  // what a step needs of its run: the state slot at a run end (levels < k),
+  // the run's timestamp (level k, horizon test)
+  auto ld_run = [&](uint32_t meta, int32_t src, int32_t r) -> int32_t {
+    if (LAST) return src >= 0 ? __ldg(P.g.run_ts + r) : 0;
+    return (meta & kRunEnd) ? __ldg(P.g.run_slot + r) : -1;
+  };
+  uint32_t m0, m1;
+  int32_t s0, s1;
+  ld_meta(0, m0, s0);
+  ld_meta(1, m1, s1);
+  uint64_t xc[E], xn[E];
+  ld_row(s0, xc);
+  int32_t r0 = ld_run(m0, s0, run);
+  for (int i = 0; i < steps; ++i) {
+    uint32_t m2;
+    int32_t s2;
+    ld_meta(i + 2, m2, s2);
+    ld_row(s1, xn);
+    const bool runend = (m0 & kRunEnd) != 0;
+    const int32_t run1 = run + (runend ? 1 : 0);
+    const int32_t r1 = ld_run(m1, s1, run1);
+    bool live = s0 >= 0;
+    if (LAST) live = live && r0 <= P.max_ts;
+    if (live) {
+      const uint64_t y = draw_edge_y(pre, yb, m0 & kEdgeMask);
+      if constexpr (kTab) {
+        LT.build(y);
+#pragma unroll
+        for (int e = 0; e < E; ++e) u[e] ^= gf_reduce_shift(LT.clmul(xc[e], 0u));
+      } else {
+        const KSplit ys = ksplit(y);
+#pragma unroll kVUnroll
+        for (int e = 0; e < E; ++e) u[e] ^= gf_reduce_alu(clmul64_kara_s(ys, ksplit(xc[e])));
       }
     }
-    cp_async_commit();
-  };
-  uint32_t nmeta;
-  bool nlive;
-  fetch(0, nmeta, nlive);
-  for (int i = 0; i < steps; ++i) {
-    const uint32_t meta = nmeta;
-    bool live = nlive;
-    cp_async_wait_all();  // row i has landed (lane-private slots: no barrier)
-    if (i + 1 < steps) fetch(i + 1, nmeta, nlive);
-    if (LAST && live) live = __ldg(P.g.run_ts + run) <= P.max_ts;
-    if (live) {
-      const KSplit ys = ksplit(draw_edge_y(pre, yb, meta & kEdgeMask));
-#pragma unroll kVUnroll
-      for (int e = 0; e < E; ++e)
-        S.u[e][lane] ^= gf_reduce_alu(clmul64_kara_s(ys, ksplit(S.x[i & 1][e][lane])));
-    }
-    const bool runend = i < cnt && (meta & kRunEnd);
     if (!LAST) {
-      const int32_t slot = runend ? __ldg(P.g.run_slot + run) : -1;
+      const int32_t slot = r0;  // -1 unless a referenced run ends here
       const unsigned push = __ballot_sync(kFullV, slot >= 0);
       if (push) {
         if (slot >= 0) {
@@ -325,13 +372,20 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
           S.q_slot[qi] = slot;
           S.q_head[qi] = h;
 #pragma unroll
-          for (int e = 0; e < E; ++e) S.q[e][qi] = S.u[e][lane];
+          for (int e = 0; e < E; ++e) S.q[e][qi] = u[e];
         }
         qn += __popc(push);
         if (qn >= 32) flush(32);
       }
     }
-    if (runend) ++run;
+    run = run1;
+    m0 = m1;
+    s0 = s1;
+    m1 = m2;
+    s1 = s2;
+    r0 = r1;
+#pragma unroll
+    for (int e = 0; e < E; ++e) xc[e] = xn[e];
   }
   if (!LAST) {
     while (qn > 0) flush(qn < 32 ? qn : 32);
@@ -340,14 +394,26 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
     // the (k-1)-subsets, [k] - {j} has colex rank k-1-j
     ClassAcc ca;
     class_zero(ca);
-#pragma unroll 1
+#pragma unroll
     for (int j = 0; j < K; ++j)
-      class_acc(ksplit(__ldg(P.zj + static_cast<int64_t>(h) * K + j)), ksplit(S.u[K - 1 - j][lane]),
-                ca);
+      class_acc(ksplit(__ldg(P.zj + static_cast<int64_t>(h) * K + j)), ksplit(u[K - 1 - j]), ca);
     uint64_t v = gf_reduce_alu(class_finish(ca));
     if (A.det != 1) v = gf_mul(A.det, v);
     if (v) A.acc[h] ^= v;
   }
+}
+
+template <int K, int L, bool FIRST, bool LAST>
+void vertex_launch(const VertArgs& a, unsigned blocks, cudaStream_t st) {
+  constexpr int E = binom_c(K, L - 1);
+  constexpr bool kTab = vert_uses_table<K, L>();
+  using Sm = VertSmem<E, binom_c(K, L), L, LAST>;
+  const size_t dyn =
+      vert_scratch<E, kTab>() * kVWarps + (kTab ? 4096u : 0u) + sizeof(Sm) * kVWarps + 16;
+  if (dyn > 48u * 1024u)  // per device: set whenever the opt-in size is needed
+    cudaFuncSetAttribute(k_coef_vertex<K, L, FIRST, LAST>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dyn));
+  k_coef_vertex<K, L, FIRST, LAST><<<blocks, dim3(kVWarps * 32), dyn, st>>>(a);
 }
 
 template <int K>
@@ -355,16 +421,15 @@ void vertex_dispatch(const VertArgs& a, int l, cudaStream_t st) {
   const unsigned blocks =
       static_cast<unsigned>((a.nv + 32 * kVWarps - 1) / (32 * kVWarps));
   if (!blocks) return;
-  const dim3 thr(kVWarps * 32);
-  if (l == 2 && l == K) k_coef_vertex<K, 2, true, true><<<blocks, thr, 0, st>>>(a);
-  else if (l == 2) k_coef_vertex<K, 2, true, false><<<blocks, thr, 0, st>>>(a);
+  if (l == 2 && l == K) vertex_launch<K, 2, true, true>(a, blocks, st);
+  else if (l == 2) vertex_launch<K, 2, true, false>(a, blocks, st);
   else if (l == K) {
-    if constexpr (K >= 3) k_coef_vertex<K, K, false, true><<<blocks, thr, 0, st>>>(a);
+    if constexpr (K >= 3) vertex_launch<K, K, false, true>(a, blocks, st);
   } else {
     if constexpr (K >= 4) {
-      if (l == 3) k_coef_vertex<K, 3, false, false><<<blocks, thr, 0, st>>>(a);
+      if (l == 3) vertex_launch<K, 3, false, false>(a, blocks, st);
       if constexpr (K >= 5)
-        if (l == 4) k_coef_vertex<K, 4, false, false><<<blocks, thr, 0, st>>>(a);
+        if (l == 4) vertex_launch<K, 4, false, false>(a, blocks, st);
     }
   }
 }

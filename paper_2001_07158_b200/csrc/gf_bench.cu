@@ -100,6 +100,52 @@ __global__ void k_gf_bench_table(int64_t iters, uint64_t* sink) {
   sink[tid] = x;
 }
 
+// Lane-table products (LaneTable): per iteration every lane builds the table
+// of its own fresh y and multiplies PPT values by it.
+template <int PPT>
+__global__ void k_gf_bench_lanetab(int64_t iters, uint64_t* sink) {
+  extern __shared__ uint8_t dyn_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint32_t s0 = (static_cast<uint32_t>(__cvta_generic_to_shared(dyn_smem)) + 4095u) & ~4095u;
+  LaneTable T;
+  T.init(s0 + 4096u * w, lane);
+  uint64_t a[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) a[p] = mix64(tid * 16 + p);
+  uint64_t y = mix64(tid ^ 0x5555);
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) asm volatile("" ::"r"(lo32(a[p])));  // products done before the rebuild
+    T.build(y);
+    uint32_t gen;
+    asm volatile("mov.u32 %0, %1;" : "=r"(gen) : "r"(static_cast<uint32_t>(it)));
+#pragma unroll
+    for (int p = 0; p < PPT; ++p)
+      a[p] = gf_reduce_shift(T.clmul(a[p], gen)) ^ static_cast<uint64_t>(it);
+    y = y * 0x9e3779b97f4a7c15ull + 1;
+  }
+  uint64_t x = 0;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) x ^= a[p];
+  sink[tid] = x;
+}
+
+// self-test form: out[i] = a[i] * b[i] through the lane table
+__global__ void k_gf_mul_lanetab(int64_t n, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  extern __shared__ uint8_t dyn_smem[];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const uint32_t s0 = (static_cast<uint32_t>(__cvta_generic_to_shared(dyn_smem)) + 4095u) & ~4095u;
+  LaneTable T;
+  T.init(s0 + 4096u * w, lane);
+  T.build(i < n ? b[i] : 1);
+  uint32_t gen;
+  asm volatile("mov.u32 %0, %1;" : "=r"(gen) : "r"(0u));
+  const uint64_t r = gf_reduce_shift(T.clmul(i < n ? a[i] : 0, gen));
+  if (i < n) out[i] = r;
+}
+
 // Pipe probes: 8 independent mul.wide.u32 (V=7) or 3-input XORs (V=8) per
 // iteration and thread, to calibrate the instruction costs of the variants.
 template <int V>
@@ -133,6 +179,11 @@ void launch_gf_mul(int variant, int64_t n, const uint64_t* a, const uint64_t* b,
   if (n == 0) return;
   const int threads = 256;
   const int64_t blocks = (n + threads - 1) / threads;
+  if (variant == 10) {
+    k_gf_mul_lanetab<<<static_cast<unsigned>(blocks), threads, 4096 * (threads / 32 + 1), st>>>(
+        n, a, b, out);
+    return;
+  }
   k_gf_mul<<<static_cast<unsigned>(blocks), threads, 0, st>>>(variant, n, a, b, out);
 }
 
@@ -150,6 +201,23 @@ double launch_gf_bench(int variant, int64_t iters, uint64_t* sink, int blocks, i
     case 7: k_pipe_probe<7><<<blocks, threads, 0, st>>>(iters, sink); return 8.0 * iters * lanes;
     case 8: k_pipe_probe<8><<<blocks, threads, 0, st>>>(iters, sink); return 8.0 * iters * lanes;
     case 9: k_gf_bench<9><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
+    case 10: case 11: case 12: {
+      // lane tables: 1 / 5 / 10 products per table build
+      const size_t sm = 4096 * (static_cast<size_t>(threads) / 32 + 1);
+      if (variant == 10) {
+        cudaFuncSetAttribute(k_gf_bench_lanetab<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_gf_bench_lanetab<1><<<blocks, threads, sm, st>>>(iters, sink);
+        return 1.0 * iters * lanes;
+      }
+      if (variant == 11) {
+        cudaFuncSetAttribute(k_gf_bench_lanetab<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_gf_bench_lanetab<5><<<blocks, threads, sm, st>>>(iters, sink);
+        return 5.0 * iters * lanes;
+      }
+      cudaFuncSetAttribute(k_gf_bench_lanetab<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_gf_bench_lanetab<10><<<blocks, threads, sm, st>>>(iters, sink);
+      return 10.0 * iters * lanes;
+    }
     default: k_gf_bench<0><<<blocks, threads, 0, st>>>(iters, sink); return 4.0 * iters * lanes;
   }
 }

@@ -93,12 +93,18 @@ T* dupload(const std::vector<T>& v) {
   return p;
 }
 
+// Stream-ordered allocation that, when the device is full, gives the free
+// cached state buffers (below) and the pool's unused memory back and tries
+// once more: a vertex-path evaluation leaves tens of GB in that cache, which
+// another engine's state must be able to claim.
+bool alloc_retry(void** p, size_t bytes, cudaStream_t st);
+
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t st = nullptr;
   DevBuf() = default;
   DevBuf(size_t bytes, cudaStream_t s) : st(s) {
-    TSV_CUDA(cudaMallocAsync(&p, bytes ? bytes : 8, s));
+    if (!alloc_retry(&p, bytes ? bytes : 8, s)) TSV_CUDA(cudaErrorMemoryAllocation);
   }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, st);
@@ -155,6 +161,43 @@ size_t cached_state_free(int dev) {
   for (const CachedState& c : g_state)
     if (c.dev == dev && !c.busy) b += c.bytes;
   return b;
+}
+
+// Frees this device's cached state buffers that are not in use; returns
+// the bytes released.
+size_t drop_free_cached_state(int dev) {
+  std::lock_guard<std::mutex> lk(g_state_mu);
+  size_t b = 0;
+  for (size_t i = 0; i < g_state.size();) {
+    CachedState& c = g_state[i];
+    if (c.dev == dev && !c.busy) {
+      cudaEventSynchronize(c.done);
+      cudaEventDestroy(c.done);
+      cudaFree(c.p);
+      b += c.bytes;
+      g_state.erase(g_state.begin() + static_cast<long>(i));
+    } else {
+      ++i;
+    }
+  }
+  return b;
+}
+
+bool alloc_retry(void** p, size_t bytes, cudaStream_t st) {
+  if (cudaMallocAsync(p, bytes, st) == cudaSuccess) return true;
+  cudaGetLastError();
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  drop_free_cached_state(dev);
+  cudaMemPool_t pool = nullptr;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(pool, 0);
+  }
+  if (cudaMallocAsync(p, bytes, st) == cudaSuccess) return true;
+  cudaGetLastError();
+  *p = nullptr;
+  return false;
 }
 
 StateBuf::StateBuf(size_t want, cudaStream_t s) : st(s) {
@@ -215,7 +258,7 @@ StateBuf::StateBuf(size_t want, cudaStream_t s) : st(s) {
       return;
     }
   }
-  TSV_CUDA(cudaMallocAsync(&p, want, st));
+  if (!alloc_retry(&p, want, st)) TSV_CUDA(cudaErrorMemoryAllocation);
   bytes = 0;  // pool allocation (not cached)
 }
 
@@ -628,7 +671,7 @@ const tsv_graph::VertPart& vertex_part(const tsv_graph* g, int rank, int world,
   std::vector<void*>& live = vp->owned;
   auto alloc = [&](size_t bytes) -> void* {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+    if (!alloc_retry(&p, bytes ? bytes : 8, st))
       throw CudaError("vertex list: out of device memory");
     live.push_back(p);
     return p;
@@ -815,7 +858,7 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
     std::vector<void*> tmp;
     auto alloc = [&](size_t bytes) -> void* {
       void* p = nullptr;
-      if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+      if (!alloc_retry(&p, bytes ? bytes : 8, st))
         throw CudaError("time windows: out of device memory");
       tmp.push_back(p);
       return p;
@@ -1113,7 +1156,7 @@ void eval_small_field(const tsv_graph* g, const tsv_shades* sh, int k, int32_t m
   std::vector<void*> live;
   auto alloc = [&](size_t bytes) -> void* {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+    if (!alloc_retry(&p, bytes ? bytes : 8, st))
       throw CudaError("small-field sieve: out of device memory");
     live.push_back(p);
     return p;
@@ -1346,7 +1389,7 @@ tsv_graph* device_graph_build(int32_t n, int64_t m, const int32_t* u, const int3
   std::vector<void*> live;
   auto alloc = [&](size_t bytes) -> void* {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+    if (!alloc_retry(&p, bytes ? bytes : 8, st))
       throw CudaError("device graph build: out of device memory");
     live.push_back(p);
     return p;
@@ -1517,7 +1560,7 @@ std::shared_ptr<tsv_graph> shaded_subgraph(const tsv_graph* g, const tsv_shades*
   std::vector<void*> tmp;
   auto alloc = [&](size_t bytes) -> void* {
     void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+    if (!alloc_retry(&p, bytes ? bytes : 8, st))
       throw CudaError("shaded subgraph: out of device memory");
     tmp.push_back(p);
     return p;
@@ -1852,7 +1895,7 @@ int tsv_graph_restrict(const tsv_graph* g, const uint8_t* keep_vertex, int32_t m
     std::vector<void*> tmp;
     auto alloc = [&](size_t bytes) -> void* {
       void* p = nullptr;
-      if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+      if (!alloc_retry(&p, bytes ? bytes : 8, st))
         throw CudaError("restrict: out of device memory");
       tmp.push_back(p);
       return p;
@@ -2290,7 +2333,7 @@ int tsv_vertex_exchange_plan(const tsv_graph* g, const tsv_shades* s, int k, int
     if (!me.xlists) {
       auto alloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
-        if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+        if (!alloc_retry(&p, bytes ? bytes : 8, st))
           throw CudaError("exchange lists: out of device memory");
         me.owned.push_back(p);
         return p;
@@ -2446,7 +2489,7 @@ int tsv_graph_static_edges(const tsv_graph* g, int64_t* ms, int32_t* a, int32_t*
     std::vector<void*> live;
     auto alloc = [&](size_t bytes) -> void* {
       void* p = nullptr;
-      if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+      if (!alloc_retry(&p, bytes ? bytes : 8, st))
         throw CudaError("static projection: out of device memory");
       live.push_back(p);
       return p;
@@ -2747,7 +2790,7 @@ int tsv_eval_static_projection(int32_t n, int64_t ms, const int32_t* a, const in
       std::vector<void*> live;
       auto alloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
-        if (cudaMallocAsync(&p, bytes ? bytes : 8, st) != cudaSuccess)
+        if (!alloc_retry(&p, bytes ? bytes : 8, st))
           throw CudaError("static sieve: out of device memory");
         live.push_back(p);
         return p;

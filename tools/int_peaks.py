@@ -17,11 +17,23 @@ NAMES = {7: "mul.wide.u32 ops/s (FMA-heavy pipe)", 8: "LOP3 ops/s (ALU pipe)",
          3: "GF product, holes + schoolbook", 9: "GF product, holes period 5",
          4: "GF product, smem table, 1 per lane per table",
          5: "GF product, smem table, 2 per lane per table",
-         6: "GF product, smem table, 4 per lane per table"}
+         6: "GF product, smem table, 4 per lane per table",
+         10: "GF product, lane table, 1 per build",
+         11: "GF product, lane table, 5 per build",
+         12: "GF product, lane table, 10 per build"}
 
 
 def main():
     out = {}
+    import numpy as np
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 2**64 - 1, 100_000, dtype=np.uint64, endpoint=True)
+    b = rng.integers(0, 2**64 - 1, 100_000, dtype=np.uint64, endpoint=True)
+    a[:64] = 1 << np.arange(64, dtype=np.uint64)
+    b[:64] = np.uint64(2**64 - 1)
+    ok = bool(np.array_equal(_native.gf_mul_device(a, b, 10), _native.gf_mul_device(a, b, 1)))
+    print("lane table self-test vs bit-serial:", ok)
+    out["lane_table_selftest"] = ok
     for v, name in NAMES.items():
         best = max(_native.gf_bench(v, 4096) for _ in range(3))
         out[name] = best
