@@ -79,7 +79,10 @@ namespace tsv {
 namespace {
 
 constexpr unsigned kFullV = 0xffffffffu;
-constexpr int kVWarps = 2;   // warps per block
+#ifndef TSV_VWARPS
+#define TSV_VWARPS 2
+#endif
+constexpr int kVWarps = TSV_VWARPS;   // warps per block
 constexpr int kQCap = 64;    // queued rows per warp (ring)
 
 // Row stride of level l's state rows: C(k, l) words padded to a multiple of
@@ -155,12 +158,28 @@ struct VertArgs {
   uint64_t* acc;             // level k: per-vertex accumulators (XORed into)
 };
 
-// Row entries are read once: keep them out of the small L1 that is left
-// next to the shared-memory carve-out (the arc metadata lives there).
+// Row loads allocate in L1 (TSV_VROW_L1, default): a row spans two to four
+// 32-byte sectors and its entry loads merge there; without allocation every
+// entry load is its own L2 request (measured: level k 5.7 -> 9.2 ms at C5
+// x0.1).
+#ifndef TSV_VROW_L1
+#define TSV_VROW_L1 1
+#endif
 __device__ __forceinline__ uint64_t ld_row64(const uint64_t* p) {
   uint64_t v;
+#if TSV_VROW_L1
+  asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(p));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
+#endif
   return v;
+}
+__device__ __forceinline__ void ld_row128(const uint64_t* p, uint64_t& a, uint64_t& b) {
+#if TSV_VROW_L1
+  asm volatile("ld.global.nc.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+#else
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));
+#endif
 }
 
 // Per-warp shared state.  Lane-minor layouts ([entry][slot]) keep every
@@ -178,10 +197,10 @@ struct VertSmem {
 // scratch bytes per warp: the lane table (4 KB, 4 KB aligned) or, without
 // it, the W rows of the paired z map
 template <int E, bool TAB>
-constexpr unsigned vert_scratch() { return TAB ? 4096u : static_cast<unsigned>(E) * 256u; }
+__host__ __device__ constexpr unsigned vert_scratch() { return TAB ? 4096u : static_cast<unsigned>(E) * 256u; }
 
 template <int K, int L>
-constexpr bool vert_uses_table() {
+__host__ __device__ constexpr bool vert_uses_table() {
   return TSV_VTABLE && binom_c(K, L - 1) >= TSV_VTABLE_MINE;
 }
 
@@ -323,9 +342,16 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
   };
   auto ld_row = [&](int32_t src, uint64_t (&x)[E]) {
     if (src >= 0) {
-      const uint64_t* row = rows + static_cast<int64_t>(src) * (FIRST ? E : vpad(E));
+      constexpr int kStride = FIRST ? E : vpad(E);
+      const uint64_t* row = rows + static_cast<int64_t>(src) * kStride;
+      if constexpr (kStride % 2 == 0) {  // 16-byte aligned rows
 #pragma unroll
-      for (int e = 0; e < E; ++e) x[e] = ld_row64(row + e);
+        for (int e = 0; e + 1 < E; e += 2) ld_row128(row + e, x[e], x[e + 1]);
+        if constexpr (E % 2) x[E - 1] = ld_row64(row + E - 1);
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) x[e] = ld_row64(row + e);
+      }
     }
   };
   // what a step needs of its run: the state slot at a run end (levels < k),
