@@ -238,4 +238,46 @@ int64_t tsieve_load_graph_text(const char* edge_text, const char* color_text, in
   }
 }
 
+// load_graph_file with the binary ingest cache (graph.hpp); outputs as
+// tsieve_load_graph_text plus *cache_hit.  Returns m or -1.
+int64_t tsieve_load_graph_file(const char* edge_path, const char* color_text, int directed,
+                               const char* cache_path, int32_t* cache_hit, int32_t* n_out,
+                               int32_t* t_out, int32_t* out_u, int32_t* out_v, int32_t* out_ts,
+                               int64_t cap, int32_t* colors_out, int32_t ncap, char* names,
+                               int64_t names_cap, int64_t* stats3) {
+  try {
+    std::istringstream cs(color_text ? color_text : "");
+    bool hit = false;
+    LoadResult lr = load_graph_file(edge_path, color_text ? &cs : nullptr, directed != 0,
+                                    cache_path ? cache_path : "", &hit);
+    *cache_hit = hit ? 1 : 0;
+    *n_out = lr.graph.n();
+    *t_out = lr.graph.t();
+    const auto& e = lr.graph.edges();
+    for (int64_t i = 0; i < lr.graph.m() && i < cap; ++i) {
+      out_u[i] = e[i].u;
+      out_v[i] = e[i].v;
+      out_ts[i] = e[i].ts;
+    }
+    for (int32_t i = 0; i < lr.graph.n() && i < ncap; ++i) colors_out[i] = lr.coloring.primary(i);
+    std::string joined;
+    for (size_t i = 0; i < lr.vertex_names.size(); ++i)
+      joined += (i ? "\n" : "") + lr.vertex_names[i];
+    if (names && names_cap > 0) {
+      const size_t w = std::min<size_t>(static_cast<size_t>(names_cap - 1), joined.size());
+      std::memcpy(names, joined.data(), w);
+      names[w] = 0;
+    }
+    if (stats3) {
+      stats3[0] = lr.stats.raw_records;
+      stats3[1] = lr.stats.self_loops_dropped;
+      stats3[2] = lr.stats.duplicates_dropped;
+    }
+    return lr.graph.m();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 }  // extern "C"

@@ -243,6 +243,7 @@ class Reader {
 
 struct Opts {
   std::string graph_file, colors_file, delays_file;
+  std::string ingest_cache;  // binary ingest cache of --graph ("" = none); not a reference flag
   std::string problem = "pathmotif";
   std::string motif, order, times;
   int k = 0;
@@ -286,6 +287,7 @@ Opts parse_flags(const std::string& cmd, int argc, char** argv) {
     };
     if (f == "--graph") o.graph_file = val(), have_graph = true;
     else if (f == "--colors") o.colors_file = val();
+    else if (f == "--ingest-cache") o.ingest_cache = val();
     else if (f == "--delays") o.delays_file = val();
     else if (f == "--problem") o.problem = val();
     else if (f == "--motif") o.motif = val();
@@ -366,7 +368,7 @@ Instance load_instance(const Opts& o) {
     if (!*cf) throw std::invalid_argument("--colors: cannot open " + o.colors_file);
   }
   ef.close();
-  inst.loaded = load_graph_file(o.graph_file, cf ? &*cf : nullptr, o.directed);
+  inst.loaded = load_graph_file(o.graph_file, cf ? &*cf : nullptr, o.directed, o.ingest_cache);
   if (!o.delays_file.empty()) {
     std::ifstream df(o.delays_file);
     if (!df) throw std::invalid_argument("--delays: cannot open " + o.delays_file);

@@ -183,6 +183,93 @@ def test_load_graph_matches_reference_loader():
     assert str(our_err.value) == str(ref_err.value)
 
 
+def dropin_load_file(path, color_text, directed, cache):
+    lib = dropin()
+    f = lib.tsieve_load_graph_file
+    f.restype = C.c_int64
+    f.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_char_p, C.POINTER(C.c_int32),
+                  C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i32p, _i32p, _i32p, C.c_int64,
+                  _i32p, C.c_int32, C.c_char_p, C.c_int64,
+                  np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")]
+    with open(path) as fh:
+        cap = fh.read().count("\n") + 2
+    ou, ov, ot = (np.empty(cap, np.int32) for _ in range(3))
+    n, t, hit = C.c_int32(0), C.c_int32(0), C.c_int32(0)
+    cols = np.empty(2 * cap + 2, np.int32)
+    names = C.create_string_buffer(1 << 22)
+    stats = np.zeros(3, np.int64)
+    m = f(str(path).encode(), None if color_text is None else color_text.encode(), int(directed),
+          None if cache is None else str(cache).encode(), C.byref(hit), C.byref(n), C.byref(t),
+          ou, ov, ot, cap, cols, len(cols), names, len(names), stats)
+    if m < 0:
+        raise ValueError(lib.tsieve_last_error().decode())
+    nm = names.value.decode().split("\n") if n.value else []
+    return {"n": n.value, "t": t.value, "u": ou[:m].copy(), "v": ov[:m].copy(),
+            "ts": ot[:m].copy(), "colors": cols[:n.value].copy(), "names": nm,
+            "stats": stats.tolist()}, bool(hit.value)
+
+
+def _same_load(a, b):
+    return (a["n"] == b["n"] and a["t"] == b["t"] and a["names"] == b["names"] and
+            all(np.array_equal(a[k], b[k]) for k in ("u", "v", "ts", "colors")))
+
+
+def test_ingest_cache_reproduces_the_text_load(tmp_path):
+    """Binary ingest cache (graph.cpp): a load that hits the
+    cache equals the text parse (which test_load_graph_matches_reference_loader
+    pins to the reference's load_graph, graph.cpp:376-448) -- canonical edges,
+    names, colors, drop counts, for either directedness; a changed, truncated
+    or foreign cache file is a miss and is rewritten."""
+    import os
+    rng = np.random.default_rng(23)
+    hits = 0
+    for case in range(40):
+        text, colors = _random_text(rng)
+        nl = "" if not text or text.endswith("\n") else "\n"
+        if case % 4 == 0:  # transition times ride through the cache
+            text += nl + "a b 3 2\nb c 4 5\n"
+            nl = ""
+        src = tmp_path / f"g{case}.edges"
+        cache = tmp_path / f"g{case}.ingest"
+        src.write_text(text)
+        try:
+            want = dropin_load(text, colors, False)
+        except ValueError as e:
+            with pytest.raises(ValueError) as ei:
+                dropin_load_file(src, colors, False, cache)
+            assert str(ei.value) == str(e)
+            assert not cache.exists()        # a file that fails to parse leaves no cache
+            continue
+        plain, hit = dropin_load_file(src, colors, False, None)
+        assert not hit and _same_load(want, plain)
+        first, hit = dropin_load_file(src, colors, False, cache)
+        assert not hit and cache.exists()
+        assert _same_load(want, first) and first["stats"] == plain["stats"]
+        again, hit = dropin_load_file(src, colors, False, cache)
+        assert hit and _same_load(want, again) and again["stats"] == plain["stats"]
+        hits += 1
+        # the cache holds raw records: the other directedness is served from it too
+        wd = dropin_load(text, colors, True)
+        gd, hit = dropin_load_file(src, colors, True, cache)
+        assert hit and _same_load(wd, gd)
+        # a truncated cache is a miss (and is rewritten)
+        blob = cache.read_bytes()
+        cache.write_bytes(blob[:-1])
+        got, hit = dropin_load_file(src, colors, False, cache)
+        assert not hit and _same_load(want, got)
+        assert cache.read_bytes() == blob
+        # a changed source invalidates it
+        st = os.stat(src)
+        src.write_text(text + nl + "zz yy 7\n")
+        os.utime(src, ns=(st.st_atime_ns, st.st_mtime_ns + 5_000_000_000))
+        w2 = dropin_load(text + nl + "zz yy 7\n", colors, False)
+        g2, hit = dropin_load_file(src, colors, False, cache)
+        assert not hit and _same_load(w2, g2)
+        g3, hit = dropin_load_file(src, colors, False, cache)
+        assert hit and _same_load(w2, g3)
+    assert hits >= 20
+
+
 def test_load_graph_multi_chunk_matches_reference_loader():
     """A multi-megabyte edge file is parsed in parallel line-aligned chunks:
     interning order, ranks and the line number of a late error must still be
@@ -267,6 +354,16 @@ def test_cli_decide_extract_verify_optimum(cuda_device, fig2, tmp_path, golden):
     want = next(s for s in golden["solve_fig2"] if s["problem"] == "pathmotif" and s["mode"] == 0)
     assert rec["accumulator_checksum"] == want["result"]["checksum"]
     assert rec["flagged"] == want["result"]["flagged"]
+    # the same record from the binary ingest cache (written by the first run, hit by the second)
+    cache = tmp_path / "fig2.ingest"
+    for _ in range(2):
+        rc, out = cli(["decide"] + fig2 + ["--problem", "pathmotif", "--motif", "1,1,2,3",
+                                           "--preprocess", "none", "--format", "json",
+                                           "--ingest-cache", str(cache)])
+        assert rc == 0 and cache.exists()
+        again = json.loads(out)
+        assert again["accumulator_checksum"] == rec["accumulator_checksum"]
+        assert again["flagged"] == rec["flagged"]
 
     rc, out = cli(["extract"] + fig2 + ["--problem", "pathmotif", "--motif", "1,1,2,3",
                                         "--preprocess", "none", "--format", "json"])
