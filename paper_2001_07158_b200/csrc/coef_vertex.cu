@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       if constexpr (kTab) {
         LT.build(y);
 #pragma unroll
-        for (int e = 0; e < E; ++e) u[e] ^= gf_reduce_shift(LT.clmul(xc[e], 0u));
+        for (int e = 0; e < E; ++e) u[e] ^= gf_reduce124(LT.clmul(xc[e], 0u));
       } else {
         const KSplit ys = ksplit(y);
 #pragma unroll kVUnroll

@@ -122,7 +122,7 @@ __global__ void k_gf_bench_lanetab(int64_t iters, uint64_t* sink) {
     asm volatile("mov.u32 %0, %1;" : "=r"(gen) : "r"(static_cast<uint32_t>(it)));
 #pragma unroll
     for (int p = 0; p < PPT; ++p)
-      a[p] = gf_reduce_shift(T.clmul(a[p], gen)) ^ static_cast<uint64_t>(it);
+      a[p] = gf_reduce124(T.clmul(a[p], gen)) ^ static_cast<uint64_t>(it);
     y = y * 0x9e3779b97f4a7c15ull + 1;
   }
   uint64_t x = 0;
@@ -142,7 +142,7 @@ __global__ void k_gf_mul_lanetab(int64_t n, const uint64_t* a, const uint64_t* b
   T.build(i < n ? b[i] : 1);
   uint32_t gen;
   asm volatile("mov.u32 %0, %1;" : "=r"(gen) : "r"(0u));
-  const uint64_t r = gf_reduce_shift(T.clmul(i < n ? a[i] : 0, gen));
+  const uint64_t r = gf_reduce124(T.clmul(i < n ? a[i] : 0, gen));
   if (i < n) out[i] = r;
 }
 

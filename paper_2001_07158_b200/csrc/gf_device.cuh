@@ -467,6 +467,14 @@ struct LaneTable {
   }
 };
 
+// Reduction of a LaneTable::clmul product: it is below 2^124 (reduced
+// multiples shifted by at most 60 bits), so the high word has no bit above
+// 59 and one fold by x^4 + x^3 + x + 1 finishes it.
+__device__ __forceinline__ uint64_t gf_reduce124(u128 p) {
+  const uint64_t h = p.hi;
+  return p.lo ^ h ^ (h << 1) ^ (h << 3) ^ (h << 4);
+}
+
 // Reduction of a 128-bit carry-less product with ALU shifts only.
 __device__ __forceinline__ uint64_t gf_reduce_shift(u128 p) {
   const uint64_t h = p.hi;
