@@ -242,9 +242,23 @@ int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int le
                           int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
                           uint64_t* d_acc, void* stream);
 
+/* The same level with the row exchange inside the kernel: a
+ * row is stored into d_cur and, as it is formed, into peer_cur[q] of every
+ * OTHER rank q that reads it (its reader byte, fixed per graph) --
+ * peer_cur[0..world) are the ranks' level buffers as mapped on THIS device
+ * (NVLink peer memory, e.g. torch symmetric memory; peer_cur[rank] is
+ * ignored, a null entry is skipped), world <= 8.  After a barrier across
+ * the ranks every buffer holds the rows its rank reads; no pack / all-to-all
+ * / unpack.  Replaces the reference's per-block loop over one machine's
+ * lanes (sieve.cpp:199-304) across GPUs.  Asynchronous on `stream`. */
+int tsv_eval_vertex_level_peer(const tsv_graph* g, const tsv_shades* s, int k, int level,
+                               int32_t max_ts, const tsv_config* cfg, int32_t anchor_source,
+                               int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
+                               uint64_t* d_acc, uint64_t* const* peer_cur, void* stream);
+
 /* Targeted row exchange between levels (instead of an all-gather): rank
  * sends to peer q exactly its rows some arc of q reads, receives likewise;
- * the lists are fixed per graph.  plan: row counts per peer (world <= 32);
+ * the lists are fixed per graph.  plan: row counts per peer (world <= 8);
  * pack: this rank's outgoing rows of level-l buffer d_rows (row_words =
  * C(k, l)) into d_sendbuf, peers in rank order; unpack: d_recvbuf (peers in
  * rank order) into d_rows.  The bytes in between move with one all-to-all

@@ -103,6 +103,9 @@ def lib():
     L.tsv_vertex_partition.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.POINTER(Partition)]
     L.tsv_eval_vertex_level.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int32, C.POINTER(Config),
                                         C.c_int32, C.c_int, C.c_int, vp, vp, vp, vp]
+    L.tsv_eval_vertex_level_peer.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int32,
+                                             C.POINTER(Config), C.c_int32, C.c_int, C.c_int, vp,
+                                             vp, vp, C.POINTER(C.c_void_p), vp]
     L.tsv_vertex_exchange_plan.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int,
                                            C.POINTER(Exchange)]
     L.tsv_vertex_exchange_pack.argtypes = [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]

@@ -129,6 +129,18 @@ struct ExchangeLists {
   int64_t send_total = 0, recv_total = 0;
   int32_t* send_slots = nullptr;  // device, send_total
   int32_t* recv_slots = nullptr;  // device, recv_total
+  // one byte per state slot (packed four to a word): bit q = an arc whose
+  // head rank q owns reads the slot (kept for the peer-store level kernel)
+  const unsigned int* reader_mask = nullptr;
+};
+// Peer-store form of a level (coef_vertex.cu): every row is also stored
+// into the level buffer of each OTHER rank whose bit is set in its reader
+// byte -- peer[q] is rank q's buffer as mapped on this device (NVLink peer
+// memory) -- so the row exchange rides inside the level kernel.
+struct VertPeers {
+  const unsigned int* reader_mask = nullptr;
+  uint64_t* peer[8] = {};
+  int rank = 0;
 };
 void build_exchange_lists(const DevGraph& g, const std::vector<const VertList*>& lists,
                           const std::vector<int64_t>& slot_lo, const std::vector<int64_t>& slot_hi,
@@ -148,7 +160,7 @@ int64_t count_slots_before(const DevGraph& g, int64_t r, cudaStream_t st,
 // referenced slots into p.ubuf from p.s_prev (stride C(k, l-1)) or zj (l = 2);
 // at l = k the readout acc[h] ^= det * ... (no ulast).
 void launch_coef_vertex(const CoefParams& p, const VertList& vl, uint64_t det, uint64_t* acc,
-                        cudaStream_t st);
+                        cudaStream_t st, const VertPeers* peers = nullptr);
 
 // Time windows (coef_window.cu): arcs without a source in the window read
 // the tail's carry slot base + tail; window edge ids -> the original graph's

@@ -61,7 +61,7 @@
 #define TSV_ZUNROLL 1
 #endif
 #ifndef TSV_VMINB
-#define TSV_VMINB 1
+#define TSV_VMINB 7
 #endif
 // arc products y * row through the lane table (gf_device.cuh LaneTable: the
 // arc's y multiplies C(k, l-1) entries, the table build is paid once per
@@ -156,6 +156,12 @@ struct VertArgs {
   int64_t nv;                // vertices in the list
   uint64_t det;              // det(W) of the shade basis (readout)
   uint64_t* acc;             // level k: per-vertex accumulators (XORed into)
+  // peer stores (multi-GPU): the readers of every state slot
+  // (one byte per slot, own bit cleared by self_clear) and the ranks' level
+  // buffers as mapped on this device; rmask == nullptr: local rows only
+  const unsigned int* rmask;
+  uint64_t* peer[8];
+  unsigned self_clear;
 };
 
 // Row loads allocate in L1 (TSV_VROW_L1, default): a row spans two to four
@@ -270,7 +276,16 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       uint64_t z[K];
 #pragma unroll
       for (int j = 0; j < K; ++j) z[j] = __ldg(P.zj + static_cast<int64_t>(hd) * K + j);
-      uint64_t* out = P.ubuf + static_cast<int64_t>(S.q_slot[qi]) * vpad(F);
+      const int64_t out_off = static_cast<int64_t>(S.q_slot[qi]) * vpad(F);
+      uint64_t* out = P.ubuf + out_off;
+      // the other ranks that read this row get it now (NVLink peer stores)
+      unsigned pm = 0;
+      if (A.rmask)
+        pm = (__ldg(A.rmask + (S.q_slot[qi] >> 2)) >> (8 * (S.q_slot[qi] & 3))) & A.self_clear;
+      auto put = [&](int o, uint64_t v) {
+        out[o] = v;
+        for (unsigned m = pm; m; m &= m - 1) A.peer[__ffs(m) - 1][out_off + o] = v;
+      };
 #if TSV_ZPAIR == 2
       // paired z map: with z_X = XOR_{j in X} z_j,
       //   z_T * (XOR_{P in T, |P| = L-1} U[P])
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
             su ^= S.q[pi][qi];
             sw ^= wrow[pi * 32];
           }
-          out[o] = gf_reduce_alu(clmul64_kara_s(ksplit(zt), ksplit(su))) ^ sw;
+          put(o, gf_reduce_alu(clmul64_kara_s(ksplit(zt), ksplit(su))) ^ sw);
         }
       } else
 #endif
@@ -318,7 +333,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
             for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
             class_acc(ksplit(zj), ksplit(S.q[S.pin[o][c]][qi]), ca);
           }
-          out[o] = gf_reduce_alu(class_finish(ca));
+          put(o, gf_reduce_alu(class_finish(ca)));
         }
       }
     }
@@ -683,6 +698,7 @@ void build_exchange_lists(const DevGraph& g, const std::vector<const VertList*>&
                                                      g.arc_src, q, mask);
   }
   out = ExchangeLists{};
+  out.reader_mask = mask;
   out.send_count.assign(world, 0);
   out.recv_count.assign(world, 0);
   // send to q: my slots with bit q; receive from q: q's slots with my bit
@@ -712,7 +728,6 @@ void build_exchange_lists(const DevGraph& g, const std::vector<const VertList*>&
     select(slot_lo[q], slot_hi[q], rank, &parts_r[q], &out.recv_count[q]);
   }
   release(cnt);
-  release(mask);
   // one array per direction, peers in rank order
   int64_t ts = 0, tr = 0;
   for (int q = 0; q < world; ++q) ts += out.send_count[q], tr += out.recv_count[q];
@@ -769,9 +784,20 @@ int64_t count_slots_before(const DevGraph& g, int64_t r, cudaStream_t st,
 }
 
 void launch_coef_vertex(const CoefParams& p, const VertList& vl, uint64_t det, uint64_t* acc,
-                        cudaStream_t st) {
+                        cudaStream_t st, const VertPeers* peers) {
   if (vl.nv == 0) return;
   VertArgs a;
+  a.rmask = nullptr;
+  a.self_clear = 0xffu;
+  for (int q = 0; q < 8; ++q) a.peer[q] = nullptr;
+  if (peers && peers->reader_mask && !p.last) {
+    a.rmask = peers->reader_mask;
+    a.self_clear = 0xffu & ~(1u << peers->rank);
+    for (int q = 0; q < 8; ++q) {
+      a.peer[q] = peers->peer[q];
+      if (!a.peer[q]) a.self_clear &= ~(1u << q);  // no buffer given: not stored
+    }
+  }
   a.P = p;
   a.wl_head = vl.head;
   a.wl_start = vl.start;

@@ -2246,10 +2246,45 @@ int tsv_vertex_partition(const tsv_graph* g, const tsv_shades* s, int k, int ran
   });
 }
 
-int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int level,
-                          int32_t max_ts, const tsv_config* cfg, int32_t anchor_source,
-                          int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
-                          uint64_t* d_acc, void* stream) {
+// The partition `rank` of `world` with its exchange lists (and reader mask)
+// built on first use, on `st`.
+static const tsv_graph::VertPart& exchange_part(const tsv_graph* g, int rank, int world,
+                                                cudaStream_t st) {
+  if (world < 1 || world > 8 || rank < 0 || rank >= world)
+    throw std::invalid_argument("bad rank/world (the reader mask holds 8 ranks)");
+  std::vector<const tsv::VertList*> lists;
+  std::vector<int64_t> lo, hi;
+  for (int q = 0; q < world; ++q) {
+    const tsv_graph::VertPart& p = vertex_part(g, q, world, st);
+    lists.push_back(&p.vl);
+    lo.push_back(p.slot_lo);
+    hi.push_back(p.slot_hi);
+  }
+  auto& me = const_cast<tsv_graph::VertPart&>(vertex_part(g, rank, world, st));
+  std::lock_guard<std::mutex> lk(g->vl_mu);
+  if (!me.xlists) {
+    auto alloc = [&](size_t bytes) -> void* {
+      void* p = nullptr;
+      if (!alloc_retry(&p, bytes ? bytes : 8, st))
+        throw CudaError("exchange lists: out of device memory");
+      me.owned.push_back(p);
+      return p;
+    };
+    auto release = [&](void* p) {
+      auto it = std::find(me.owned.begin(), me.owned.end(), p);
+      if (it != me.owned.end()) me.owned.erase(it);
+      cudaFreeAsync(p, st);
+    };
+    tsv::build_exchange_lists(g->dev, lists, lo, hi, rank, me.xl, st, alloc, release);
+    me.xlists = true;
+  }
+  return me;
+}
+
+static int eval_vertex_level_impl(const tsv_graph* g, const tsv_shades* s, int k, int level,
+                                  int32_t max_ts, const tsv_config* cfg, int32_t anchor_source,
+                                  int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
+                                  uint64_t* d_acc, uint64_t* const* peer_cur, void* stream) {
   return guard([&] {
     if (!g || !s || !d_acc) throw std::invalid_argument("null argument");
     check_config(cfg);
@@ -2298,17 +2333,49 @@ int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int le
     cp.s_prev = d_prev;
     cp.ubuf = d_cur;
     cp.max_ts = max_ts;
-    tsv::launch_coef_vertex(cp, vp.vl, det, d_acc, st);
+    tsv::VertPeers peers;
+    if (peer_cur && world > 1 && level < k) {
+      // the reader byte of every slot comes with the exchange lists
+      const tsv_graph::VertPart& me = exchange_part(g, rank, world, st);
+      peers.reader_mask = me.xl.reader_mask;
+      peers.rank = rank;
+      for (int q = 0; q < world; ++q) peers.peer[q] = q == rank ? nullptr : peer_cur[q];
+    }
+    tsv::launch_coef_vertex(cp, vp.vl, det, d_acc, st, peers.reader_mask ? &peers : nullptr);
     TSV_CUDA(cudaGetLastError());
   });
 }
+
+int tsv_eval_vertex_level(const tsv_graph* g, const tsv_shades* s, int k, int level,
+                          int32_t max_ts, const tsv_config* cfg, int32_t anchor_source,
+                          int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
+                          uint64_t* d_acc, void* stream) {
+  return eval_vertex_level_impl(g, s, k, level, max_ts, cfg, anchor_source, rank, world, d_prev,
+                                d_cur, d_acc, nullptr, stream);
+}
+
+int tsv_eval_vertex_level_peer(const tsv_graph* g, const tsv_shades* s, int k, int level,
+                               int32_t max_ts, const tsv_config* cfg, int32_t anchor_source,
+                               int rank, int world, const uint64_t* d_prev, uint64_t* d_cur,
+                               uint64_t* d_acc, uint64_t* const* peer_cur, void* stream) {
+  if (!peer_cur) {
+    g_error = "null argument";
+    return TSV_ERR_INVALID;
+  }
+  if (world > 8) {
+    g_error = "peer stores take at most 8 ranks";
+    return TSV_ERR_INVALID;
+  }
+  return eval_vertex_level_impl(g, s, k, level, max_ts, cfg, anchor_source, rank, world, d_prev,
+                                d_cur, d_acc, peer_cur, stream);
+}
+
 
 int tsv_vertex_exchange_plan(const tsv_graph* g, const tsv_shades* s, int k, int rank,
                              int world, tsv_exchange* out) {
   return guard([&] {
     if (!g || !s || !out) throw std::invalid_argument("null argument");
-    if (world < 1 || world > 32 || rank < 0 || rank >= world)
-      throw std::invalid_argument("bad rank/world");
+    (void)k;
     std::memset(out, 0, sizeof(*out));
     DeviceGuard dg(g->device);
     cudaStream_t st = nullptr;
@@ -2320,32 +2387,7 @@ int tsv_vertex_exchange_plan(const tsv_graph* g, const tsv_shades* s, int k, int
         cudaStreamDestroy(s);
       }
     } del{st};
-    std::vector<const tsv::VertList*> lists;
-    std::vector<int64_t> lo, hi;
-    for (int q = 0; q < world; ++q) {
-      const tsv_graph::VertPart& p = vertex_part(g, q, world, st);
-      lists.push_back(&p.vl);
-      lo.push_back(p.slot_lo);
-      hi.push_back(p.slot_hi);
-    }
-    auto& me = const_cast<tsv_graph::VertPart&>(vertex_part(g, rank, world, st));
-    std::lock_guard<std::mutex> lk(g->vl_mu);
-    if (!me.xlists) {
-      auto alloc = [&](size_t bytes) -> void* {
-        void* p = nullptr;
-        if (!alloc_retry(&p, bytes ? bytes : 8, st))
-          throw CudaError("exchange lists: out of device memory");
-        me.owned.push_back(p);
-        return p;
-      };
-      auto release = [&](void* p) {
-        auto it = std::find(me.owned.begin(), me.owned.end(), p);
-        if (it != me.owned.end()) me.owned.erase(it);
-        cudaFreeAsync(p, st);
-      };
-      tsv::build_exchange_lists(g->dev, lists, lo, hi, rank, me.xl, st, alloc, release);
-      me.xlists = true;
-    }
+    const tsv_graph::VertPart& me = exchange_part(g, rank, world, st);
     for (int q = 0; q < world; ++q) {
       out->send_rows[q] = me.xl.send_count[q];
       out->recv_rows[q] = me.xl.recv_count[q];

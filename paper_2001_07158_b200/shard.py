@@ -139,6 +139,45 @@ def vertex_partitioned_eval(level_fn, k, ranges, prev, cur, acc, group=None, exc
     return xor_allreduce(acc, group) if world > 1 else acc
 
 
+def eval_vertex_partitioned_peer(g, ds, k, max_ts, cfg, anchor_source, acc, rank, world,
+                                 group=None, stream=None):
+    """The vertex-partitioned evaluation with the row exchange INSIDE the
+    level kernel (tsv_eval_vertex_level_peer): the two state buffers live in
+    symmetric memory (torch.distributed._symmetric_memory: every rank's
+    buffer is mapped on every GPU of the NVLink domain), a rank stores each
+    row it forms into its own buffer and into the buffers of the ranks whose
+    arcs read it, and the only step between levels is a barrier -- which also
+    guards the ping-pong: level l+1 overwrites, on the peers too, the buffer
+    level l read.  No pack / all-to-all / unpack, and the transfer overlaps
+    the level's products row by row."""
+    import torch
+    import torch.distributed as dist
+    import torch.distributed._symmetric_memory as symm
+    from .sieve import eval_vertex_level, vertex_partition
+    parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
+    if not all(p.applicable for p in parts):
+        raise ValueError("vertex partition not applicable")
+    if world > 8:
+        raise ValueError("peer stores take at most 8 ranks (one NVLink domain)")
+    words = parts[0].state_words
+    grp = group if group is not None else dist.group.WORLD
+    st = stream or torch.cuda.current_stream(acc.device)
+    with torch.cuda.stream(st):
+        bufs = [symm.empty(words, dtype=torch.int64, device=acc.device) for _ in range(2)]
+        hdls = [symm.rendezvous(b, grp) for b in bufs]
+        cur_i = 1
+        for level in range(2, k + 1):
+            prev, cur = bufs[1 - cur_i], bufs[cur_i]
+            peers = [int(p) for p in hdls[cur_i].buffer_ptrs] if level < k else None
+            eval_vertex_level(g, ds, k, level, max_ts, cfg, anchor_source, rank, world,
+                              prev.data_ptr(), cur.data_ptr(), acc.data_ptr(), st.cuda_stream,
+                              peer_cur=peers)
+            if level < k:
+                hdls[cur_i].barrier()   # every rank's level-l rows are in place everywhere
+            cur_i = 1 - cur_i
+    return xor_allreduce(acc, group) if world > 1 else acc
+
+
 def eval_vertex_partitioned_device(g, ds, k, max_ts, cfg, anchor_source, acc, rank, world,
                                    group=None, bufs=None, stream=None, targeted=True):
     """vertex_partitioned_eval with the device engine (tsv_eval_vertex_level)
@@ -224,6 +263,49 @@ def eval_vertex_simulated(g, ds, k, max_ts, cfg, anchor_source, acc, world, bufs
         torch.cuda.synchronize(acc.device)
         times = {key: a.elapsed_time(b) for key, (a, b) in times.items()}
     return acc, times, parts
+
+
+def eval_vertex_simulated_peer(g, ds, k, max_ts, cfg, anchor_source, n, world, timed=False):
+    """Test form of the peer-store levels on ONE device: every simulated rank
+    has its own zeroed state buffers; at a level the ranks run one after the
+    other, each storing its rows into its own buffer and -- through the
+    kernel's reader bytes -- into the buffers of the ranks that read them
+    (the other ranks' buffers stand in for NVLink peer mappings).  A row a
+    reader does not receive stays zero, so equality with the single-GPU
+    result checks the masks and the stores.  timed=True also returns the
+    CUDA-event time of every (level, rank) share, peer stores included."""
+    import torch
+    from .sieve import eval_vertex_level, vertex_partition
+    parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
+    words = parts[0].state_words
+    stream = torch.cuda.current_stream()
+    st = stream.cuda_stream
+    bufs = [[torch.zeros(words, dtype=torch.int64, device="cuda") for _ in range(2)]
+            for _ in range(world)]
+    accs = [torch.zeros(n, dtype=torch.int64, device="cuda") for _ in range(world)]
+    cur_i = 1
+    times = {}
+    for level in range(2, k + 1):
+        peers = [bufs[r][cur_i].data_ptr() for r in range(world)] if level < k else None
+        for q in range(world):
+            if timed:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            eval_vertex_level(g, ds, k, level, max_ts, cfg, anchor_source, q, world,
+                              bufs[q][1 - cur_i].data_ptr(), bufs[q][cur_i].data_ptr(),
+                              accs[q].data_ptr(), st, peer_cur=peers)
+            if timed:
+                e1.record(stream)
+                times[(level, q)] = (e0, e1)
+        cur_i = 1 - cur_i
+    out = accs[0]
+    for a in accs[1:]:
+        torch.bitwise_xor(out, a, out=out)
+    if timed:
+        torch.cuda.synchronize()
+        return out, {key: a.elapsed_time(b) for key, (a, b) in times.items()}
+    return out
 
 
 def eval_vertex_simulated_private(g, ds, k, max_ts, cfg, anchor_source, n, world):

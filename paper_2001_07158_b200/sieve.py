@@ -229,9 +229,20 @@ def vertex_partition(g: TemporalGraph, dshades: DeviceShades, k: int, rank: int 
 
 def eval_vertex_level(g: TemporalGraph, dshades: DeviceShades, k: int, level: int, max_ts: int,
                       config: SieveConfig, anchor_source: int, rank: int, world: int,
-                      d_prev: int, d_cur: int, d_acc: int, stream_ptr: int = 0) -> None:
-    """tsv_eval_vertex_level: level `level` of this rank's vertices."""
+                      d_prev: int, d_cur: int, d_acc: int, stream_ptr: int = 0,
+                      peer_cur=None) -> None:
+    """tsv_eval_vertex_level: level `level` of this rank's vertices.  With
+    peer_cur (the `world` ranks' level buffers as device pointers valid on
+    this GPU) the rows are also stored into the buffers of the ranks that
+    read them (tsv_eval_vertex_level_peer: the exchange inside the kernel)."""
     cfg = config.to_native()
+    if peer_cur is not None:
+        ptrs = (C.c_void_p * int(world))(*[C.c_void_p(int(x) if x else None) for x in peer_cur])
+        _native.check(_native.lib().tsv_eval_vertex_level_peer(
+            g.handle, dshades.handle, int(k), int(level), int(max_ts), C.byref(cfg),
+            int(anchor_source), int(rank), int(world), C.c_void_p(d_prev), C.c_void_p(d_cur),
+            C.c_void_p(d_acc), ptrs, C.c_void_p(stream_ptr)))
+        return
     _native.check(_native.lib().tsv_eval_vertex_level(
         g.handle, dshades.handle, int(k), int(level), int(max_ts), C.byref(cfg),
         int(anchor_source), int(rank), int(world), C.c_void_p(d_prev), C.c_void_p(d_cur),

@@ -798,3 +798,8 @@ def test_vertex_partitioned_simulated_equals_single(cuda_device, world):
             from paper_2001_07158_b200.shard import eval_vertex_simulated_private
             acc2 = eval_vertex_simulated_private(g, ds, k, mt, cfg, anchor[0], n, world)
             assert np.array_equal(acc2.cpu().numpy().view(np.uint64), want), ("targeted", k, world)
+            # peer stores: the exchange inside the level kernel
+            # (tsv_eval_vertex_level_peer), zeroed private buffers per rank
+            from paper_2001_07158_b200.shard import eval_vertex_simulated_peer
+            acc3 = eval_vertex_simulated_peer(g, ds, k, mt, cfg, anchor[0], n, world)
+            assert np.array_equal(acc3.cpu().numpy().view(np.uint64), want), ("peer", k, world)
