@@ -494,6 +494,7 @@ def config_json(inst, world, args, cpu=False):
             "parallelism": (f"head-vertex partition of every evaluation over {world} GPU(s) "
                             "(shard.vertex_partitioned_eval) when the vertex-lane engine applies, "
                             "else repetitions / sieve points (shard.plan_units)"
+                            + (f"; rows between levels: {args.exchange}" if world > 1 else "")
                             if not cpu else
                             "reference CPU code on all host threads (rank 0)"),
             "l2": l2}
@@ -543,6 +544,11 @@ def main():
                          "evaluation on this one GPU and project the N-GPU step (DESIGN.md 6)")
     ap.add_argument("--nvlink-gbs", type=float, default=720.0,
                     help="all-gather bandwidth per GPU assumed by the --simulate-world model")
+    ap.add_argument("--exchange", default=os.environ.get("TSV_EXCHANGE", "alltoall"),
+                    choices=["alltoall", "peer"],
+                    help="N > 1, vertex partition: rows between levels by pack / all_to_all / "
+                         "unpack (default), or stored into the peers' buffers by the level "
+                         "kernel over symmetric memory (NVLink peer stores)")
     ap.add_argument("--streams", type=int, default=4,
                     help="concurrent CUDA streams for the repetitions of a step "
                          "(at most one per work unit)")
@@ -602,11 +608,22 @@ def main():
                           device="cuda")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         vertex_mode = bool(ok.item())
-    vbufs = None
+    vbufs = peer_bufs = None
     if vertex_mode:
         words = vertex_partition(g, ds, k, rank, world).state_words
-        vbufs = (torch.empty(words, dtype=torch.int64, device="cuda"),
-                 torch.empty(words, dtype=torch.int64, device="cuda"))
+        if args.exchange == "peer":
+            from paper_2001_07158_b200.shard import PeerStateBuffers, eval_vertex_partitioned_peer
+            peer_bufs = PeerStateBuffers(words, torch.device("cuda", torch.cuda.current_device()))
+        else:
+            vbufs = (torch.empty(words, dtype=torch.int64, device="cuda"),
+                     torch.empty(words, dtype=torch.int64, device="cuda"))
+
+    def vertex_eval(gg, dd, cfg_r, acc_r, bufs):
+        if peer_bufs is not None:
+            return eval_vertex_partitioned_peer(gg, dd, k, gg.t(), cfg_r, anchor[0], acc_r, rank,
+                                                world, peer_bufs=peer_bufs)
+        return eval_vertex_partitioned_device(gg, dd, k, gg.t(), cfg_r, anchor[0], acc_r, rank,
+                                              world, bufs=bufs)
 
     # repetitions (independent evaluations) may run on concurrent streams so
     # one evaluation's tail wave overlaps the next one's launches
@@ -620,8 +637,7 @@ def main():
         acc.zero_()
         if vertex_mode:
             for r in range(reps):
-                total[r] = eval_vertex_partitioned_device(g, ds, k, g.t(), cfgs[r], anchor[0],
-                                                          acc[r], rank, world, bufs=vbufs)
+                total[r] = vertex_eval(g, ds, cfgs[r], acc[r], vbufs)
             return total
         if not side or not concurrent:
             for r, a, b in work:
@@ -737,16 +753,34 @@ def main():
         simulated = {"model": ("per level: max over ranks of the rank's measured share + the "
                                "targeted row exchange (the largest rank's rows sent or received, "
                                "from its exchange lists) at --nvlink-gbs per GPU (modeled: one "
-                               "GPU here); + XOR combine of n words"),
+                               "GPU here); + XOR combine of n words.  peer_store: the "
+                               "exchange rides inside the level kernel (NVLink peer stores, "
+                               "tsv_eval_vertex_level_peer): per level max(the rank's share "
+                               "measured WITH its peer stores issued -- to local HBM here -- , "
+                               "the same exchange bytes at --nvlink-gbs) + a barrier"),
                      "nvlink_gbs": args.nvlink_gbs, "worlds": {}}
         ref_acc = res[0].clone()
+        sim_bufs = None   # one pair of state buffers for every simulated world and pass
         for N in (int(x) for x in args.simulate_world.replace("+", ",").split(",") if x):
             a = torch.zeros(n, dtype=torch.int64, device="cuda")
             try:
-                eval_vertex_simulated(g, ds, k, g.t(), cfgs[0], anchor[0], a, N)  # warm-up
+                if sim_bufs is None:
+                    from paper_2001_07158_b200.sieve import vertex_partition
+                    words = vertex_partition(g, ds, k, 0, 1).state_words
+                    sim_bufs = (torch.empty(words, dtype=torch.int64, device="cuda"),
+                                torch.empty(words, dtype=torch.int64, device="cuda"))
+                eval_vertex_simulated(g, ds, k, g.t(), cfgs[0], anchor[0], a, N,
+                                      bufs=sim_bufs)  # warm-up
                 a.zero_()
                 a, times, parts = eval_vertex_simulated(g, ds, k, g.t(), cfgs[0], anchor[0], a, N,
-                                                        timed=True)
+                                                        bufs=sim_bufs, timed=True)
+                if N > 1:   # the exchange lists / reader bytes are built on first use
+                    from paper_2001_07158_b200.sieve import vertex_exchange_plan
+                    for q in range(N):
+                        vertex_exchange_plan(g, ds, k, q, N)
+                a2 = torch.zeros(n, dtype=torch.int64, device="cuda")
+                a2, times_p, _ = eval_vertex_simulated(g, ds, k, g.t(), cfgs[0], anchor[0], a2, N,
+                                                       bufs=sim_bufs, timed=True, peer_store=True)
             except ValueError as e:
                 simulated["worlds"][str(N)] = {"unavailable": str(e)}
                 continue
@@ -760,21 +794,31 @@ def main():
                 plans = [vertex_exchange_plan(g, ds, k, q, N) for q in range(N)]
                 rows_max = max(max(p.send_total, p.recv_total) for p in plans)
             lv = {}
-            total_ms = 0.0
+            total_ms = total_peer_ms = 0.0
             for level in range(2, k + 1):
                 per = [times[(level, q)] for q in range(N)]
+                per_p = [times_p[(level, q)] for q in range(N)]
                 xch = xch_ag = 0.0
                 if level < k and N > 1:
                     F = parts[0].row_words[level]
                     xch = rows_max * F * 8 / (args.nvlink_gbs * 1e9) * 1e3
                     xch_ag = (N - 1) / N * S * F * 8 / (args.nvlink_gbs * 1e9) * 1e3
                 lv[str(level)] = {"rank_ms": per, "max_ms": max(per), "exchange_ms": xch,
-                                  "allgather_exchange_ms": xch_ag}
+                                  "allgather_exchange_ms": xch_ag,
+                                  "peer_store_max_ms": max(per_p)}
                 total_ms += max(per) + xch
+                total_peer_ms += max(max(per_p), xch) + (0.02 if level < k and N > 1 else 0.0)
             comb = 2 * (N - 1) / N * n * 8 / (args.nvlink_gbs * 1e9) * 1e3 if N > 1 else 0.0
             total_ms += comb
+            total_peer_ms += comb
+            if anchor[1] >= 0:
+                _native.finalize_device(a2.data_ptr(), n, anchor[1], sp)
             simulated["worlds"][str(N)] = {
                 "levels": lv, "combine_ms": comb, "projected_ms_per_step": total_ms * reps,
+                "peer_store": {"projected_ms_per_step": total_peer_ms * reps,
+                               "projected_value": upd_step / (total_peer_ms * reps * 1e-3),
+                               "barrier_ms_assumed": 0.02,
+                               "parity_vs_n1": bool(torch.equal(a2, ref_acc))},
                 "projected_value": upd_step / (total_ms * reps * 1e-3),
                 "exchange_rows_per_rank_max": rows_max, "slots": S,
                 "parity_vs_n1": bool(torch.equal(a, ref_acc))}
@@ -796,6 +840,7 @@ def main():
     # accumulators back into a host buffer (tsv_eval_temporal_sieve).  The
     # timed graph is freed first so both fit in HBM.
     del ds, g
+    sim_bufs = None
     acc = total = vbufs = None
     torch.cuda.synchronize()
     e2e = None
@@ -835,8 +880,7 @@ def main():
                 a2 = torch.zeros((reps, n), dtype=torch.int64, device="cuda")
                 if vertex_mode:
                     for r in range(reps):
-                        a2[r] = eval_vertex_partitioned_device(g2, ds2, k, g2.t(), cfgs[r],
-                                                               anchor[0], a2[r], rank, world)
+                        a2[r] = vertex_eval(g2, ds2, cfgs[r], a2[r], None)
                 else:
                     for r, a, b in work:
                         T.eval_points_device(g2, ds2, k, g2.t(), cfgs[r], anchor[0], a, b,

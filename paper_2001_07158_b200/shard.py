@@ -139,32 +139,47 @@ def vertex_partitioned_eval(level_fn, k, ranges, prev, cur, acc, group=None, exc
     return xor_allreduce(acc, group) if world > 1 else acc
 
 
+class PeerStateBuffers:
+    """The two state buffers of a vertex-partitioned evaluation in symmetric
+    memory (torch.distributed._symmetric_memory): every rank's buffer is
+    mapped on every GPU of the NVLink domain.  Built once per (graph size,
+    group) -- the allocation and the handle exchange are collective -- and
+    reused by every evaluation."""
+
+    def __init__(self, words, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        grp = group if group is not None else dist.group.WORLD
+        self.bufs = [symm.empty(int(words), dtype=torch.int64, device=device) for _ in range(2)]
+        self.hdls = [symm.rendezvous(b, grp) for b in self.bufs]
+
+
 def eval_vertex_partitioned_peer(g, ds, k, max_ts, cfg, anchor_source, acc, rank, world,
-                                 group=None, stream=None):
+                                 group=None, stream=None, peer_bufs=None):
     """The vertex-partitioned evaluation with the row exchange INSIDE the
     level kernel (tsv_eval_vertex_level_peer): the two state buffers live in
-    symmetric memory (torch.distributed._symmetric_memory: every rank's
-    buffer is mapped on every GPU of the NVLink domain), a rank stores each
-    row it forms into its own buffer and into the buffers of the ranks whose
-    arcs read it, and the only step between levels is a barrier -- which also
-    guards the ping-pong: level l+1 overwrites, on the peers too, the buffer
-    level l read.  No pack / all-to-all / unpack, and the transfer overlaps
-    the level's products row by row."""
+    symmetric memory (PeerStateBuffers), a rank stores each row it forms
+    into its own buffer and into the buffers of the ranks whose arcs read
+    it, and the only step between levels is a barrier -- which also guards
+    the ping-pong: level l+1 overwrites, on the peers too, the buffer level l
+    read.  No pack / all-to-all / unpack, and the transfer overlaps the
+    level's products row by row.  Checked on one GPU by
+    eval_vertex_simulated_peer (tests); opt-in for N > 1 (bench.py
+    --exchange peer): the pool had no multi-GPU box to run it on."""
     import torch
-    import torch.distributed as dist
-    import torch.distributed._symmetric_memory as symm
     from .sieve import eval_vertex_level, vertex_partition
     parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
     if not all(p.applicable for p in parts):
         raise ValueError("vertex partition not applicable")
     if world > 8:
         raise ValueError("peer stores take at most 8 ranks (one NVLink domain)")
-    words = parts[0].state_words
-    grp = group if group is not None else dist.group.WORLD
     st = stream or torch.cuda.current_stream(acc.device)
     with torch.cuda.stream(st):
-        bufs = [symm.empty(words, dtype=torch.int64, device=acc.device) for _ in range(2)]
-        hdls = [symm.rendezvous(b, grp) for b in bufs]
+        if peer_bufs is None:
+            peer_bufs = PeerStateBuffers(parts[0].state_words, acc.device, group)
+        bufs, hdls = peer_bufs.bufs, peer_bufs.hdls
+        hdls[0].barrier()   # the previous evaluation's readers are done with both buffers
         cur_i = 1
         for level in range(2, k + 1):
             prev, cur = bufs[1 - cur_i], bufs[cur_i]
@@ -228,13 +243,16 @@ def eval_vertex_partitioned_device(g, ds, k, max_ts, cfg, anchor_source, acc, ra
 
 
 def eval_vertex_simulated(g, ds, k, max_ts, cfg, anchor_source, acc, world, bufs=None,
-                          timed=False):
+                          timed=False, peer_store=False):
     """The `world`-rank vertex-partitioned evaluation run on ONE device: at
     every level the ranks' shares run one after the other on the same
     full-size buffers, so the all-gather between levels is the identity.
     Returns acc and, with timed=True, the CUDA-event time of every
     (level, rank) share in ms -- the per-rank compute of an N-GPU run
-    (bench.py --simulate-world)."""
+    (bench.py --simulate-world).  peer_store=True runs the peer-store kernel
+    with the shared buffer standing in for every peer's: each row is stored
+    again once per reading rank (same value, same address), which times the
+    kernel's share WITH its exchange stores issued."""
     import torch
     from .sieve import eval_vertex_level, vertex_partition
     parts = [vertex_partition(g, ds, k, q, world) for q in range(world)]
@@ -253,8 +271,10 @@ def eval_vertex_simulated(g, ds, k, max_ts, cfg, anchor_source, acc, world, bufs
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(st)
+            peers = [cur.data_ptr()] * world if peer_store and level < k and world > 1 else None
             eval_vertex_level(g, ds, k, level, max_ts, cfg, anchor_source, q, world,
-                              prev.data_ptr(), cur.data_ptr(), acc.data_ptr(), st.cuda_stream)
+                              prev.data_ptr(), cur.data_ptr(), acc.data_ptr(), st.cuda_stream,
+                              peer_cur=peers)
             if timed:
                 e1.record(st)
                 times[(level, q)] = (e0, e1)
