@@ -42,10 +42,20 @@
 namespace tsv {
 namespace {
 
-constexpr int kIW = 4;  // warps per block
+// rounds per super-round of the deep levels (source loads in flight per lane)
+#ifndef TSV_ITEMS_SUB
+#define TSV_ITEMS_SUB 2
+#endif
+#ifndef TSV_ITEMS_WARPS
+#define TSV_ITEMS_WARPS 4
+#endif
+constexpr int kIW = TSV_ITEMS_WARPS;  // warps per block
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kEvStart = 1u, kEvPush = 2u;
-constexpr int kBig = 24;
+#ifndef TSV_ITEMS_BIG
+#define TSV_ITEMS_BIG 24
+#endif
+constexpr int kBig = TSV_ITEMS_BIG;
 constexpr int kSub = 4;   // rounds per super-round (loads in flight per lane)  // items from which an arc gets whole rounds (table products)
 
 // the prefix a vertex starts from: its carried U entry o (time windows), else 0
@@ -668,7 +678,7 @@ void launch_coef_items(const CoefParams& p, cudaStream_t st) {
   else if (last)
     go(k_coef_items<false, true, 1>);
   else if (deep)
-    go(k_coef_items<false, false, 4>);
+    go(k_coef_items<false, false, TSV_ITEMS_SUB>);
   else
     go(k_coef_items<false, false, 1>);
   prof_end(st);
