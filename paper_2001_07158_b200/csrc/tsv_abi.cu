@@ -2027,64 +2027,83 @@ static bool uniform_shades(int32_t n, const int32_t* off, const int32_t* vs, int
   return true;
 }
 
-int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
-                      const int32_t* vertex_shades, tsv_shades** out) {
-  return guard([&] {
-    if (!g || !out || !vertex_off) throw std::invalid_argument("null argument");
-    *out = nullptr;
-    if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
-    const int32_t n = g->host.n;
-    if (vertex_off[0] != 0) throw std::invalid_argument("vertex_off[0] must be 0");
+// The upload behind tsv_shades_upload.  known_uniform: the caller has already
+// found every vertex's list equal to `pattern` (c entries) with
+// uniform_shades, so the per-entry scans below are not repeated (at C5 they
+// read the 2.4 GB CSR three more times, ~80 ms of every fresh-graph decide).
+static void shades_upload_impl(const tsv_graph* g, int k, const int32_t* vertex_off,
+                               const int32_t* vertex_shades, bool known_uniform, int32_t c,
+                               std::vector<int32_t> pattern, tsv_shades** out) {
+  if (!g || !out || !vertex_off) throw std::invalid_argument("null argument");
+  *out = nullptr;
+  if (k < 1 || k > 30) throw std::invalid_argument("k out of range [1,30]");
+  const int32_t n = g->host.n;
+  if (vertex_off[0] != 0) throw std::invalid_argument("vertex_off[0] must be 0");
+  const int64_t cnt = vertex_off[n];
+  bool uni = known_uniform;
+  if (!uni && cnt > (int64_t{1} << 20))
+    uni = uniform_shades(n, vertex_off, vertex_shades, &c, &pattern);
+  int64_t single = 0, multi = 0;
+  if (uni) {
+    // off[i] = i * c was checked by uniform_shades; the entries are the pattern's
+    for (int32_t x : pattern)
+      if (x < 1 || x > k) throw std::invalid_argument("shade id outside [1..k]");
+    single = c == 1 ? n : 0;
+    multi = c > 1 ? n : 0;
+  } else {
     int bad_off = 0, bad_shade = 0;
 #pragma omp parallel for schedule(static) reduction(| : bad_off)
     for (int32_t i = 0; i < n; ++i) bad_off |= vertex_off[i + 1] < vertex_off[i];
     if (bad_off) throw std::invalid_argument("vertex_off must be non-decreasing");
-    const int64_t cnt = vertex_off[n];
 #pragma omp parallel for schedule(static) reduction(| : bad_shade)
     for (int64_t i = 0; i < cnt; ++i) bad_shade |= vertex_shades[i] < 1 || vertex_shades[i] > k;
     if (bad_shade) throw std::invalid_argument("shade id outside [1..k]");
-    int64_t single = 0, multi = 0;
 #pragma omp parallel for schedule(static) reduction(+ : single, multi)
     for (int32_t i = 0; i < n; ++i) {
       single += vertex_off[i + 1] - vertex_off[i] == 1;
       multi += vertex_off[i + 1] - vertex_off[i] > 1;
     }
-    DeviceGuard dg(g->device);
-    auto* s = new tsv_shades();
-    s->k = k;
-    s->n = n;
-    s->single = single;
-    s->multi = multi;
-    s->device = g->device;
-    try {
-      // pool allocations (cudaMalloc costs ~0.1 ms per call); the copies go
-      // through the pinned staging buffers and are complete on return
-      TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->off),
-                               (static_cast<size_t>(n) + 1) * 4, nullptr));
-      TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->shades),
-                               std::max<size_t>(static_cast<size_t>(cnt), 1) * 4, nullptr));
+  }
+  DeviceGuard dg(g->device);
+  auto* s = new tsv_shades();
+  s->k = k;
+  s->n = n;
+  s->single = single;
+  s->multi = multi;
+  s->device = g->device;
+  try {
+    // pool allocations (cudaMalloc costs ~0.1 ms per call); the copies go
+    // through the pinned staging buffers and are complete on return
+    TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->off), (static_cast<size_t>(n) + 1) * 4,
+                             nullptr));
+    TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&s->shades),
+                             std::max<size_t>(static_cast<size_t>(cnt), 1) * 4, nullptr));
+    TSV_CUDA(cudaStreamSynchronize(nullptr));
+    if (uni) {
+      // every vertex the same list: expand (c, pattern) on the device
+      int32_t* dp = nullptr;
+      TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dp), std::max<size_t>(c, 1) * 4,
+                               nullptr));
+      TSV_CUDA(cudaMemcpy(dp, pattern.data(), static_cast<size_t>(c) * 4,
+                          cudaMemcpyHostToDevice));
+      tsv::launch_uniform_csr(n, c, dp, s->off, s->shades, nullptr);
+      TSV_CUDA(cudaFreeAsync(dp, nullptr));
       TSV_CUDA(cudaStreamSynchronize(nullptr));
-      int32_t c = 0;
-      std::vector<int32_t> pattern;
-      if (cnt > (int64_t{1} << 20) && uniform_shades(n, vertex_off, vertex_shades, &c, &pattern)) {
-        // every vertex the same list: expand (c, pattern) on the device
-        int32_t* dp = nullptr;
-        TSV_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dp), std::max<size_t>(c, 1) * 4,
-                                 nullptr));
-        TSV_CUDA(cudaMemcpy(dp, pattern.data(), static_cast<size_t>(c) * 4,
-                            cudaMemcpyHostToDevice));
-        tsv::launch_uniform_csr(n, c, dp, s->off, s->shades, nullptr);
-        TSV_CUDA(cudaFreeAsync(dp, nullptr));
-        TSV_CUDA(cudaStreamSynchronize(nullptr));
-      } else {
-        copy_to_device(s->off, vertex_off, (static_cast<size_t>(n) + 1) * 4, nullptr);
-        copy_to_device(s->shades, vertex_shades, static_cast<size_t>(cnt) * 4, nullptr);
-      }
-    } catch (...) {
-      delete s;
-      throw;
+    } else {
+      copy_to_device(s->off, vertex_off, (static_cast<size_t>(n) + 1) * 4, nullptr);
+      copy_to_device(s->shades, vertex_shades, static_cast<size_t>(cnt) * 4, nullptr);
     }
-    *out = s;
+  } catch (...) {
+    delete s;
+    throw;
+  }
+  *out = s;
+}
+
+int tsv_shades_upload(const tsv_graph* g, int k, const int32_t* vertex_off,
+                      const int32_t* vertex_shades, tsv_shades** out) {
+  return guard([&] {
+    shades_upload_impl(g, k, vertex_off, vertex_shades, false, 0, {}, out);
   });
 }
 
@@ -2151,9 +2170,7 @@ int tsv_eval_temporal_sieve(const tsv_graph* g, int k, int32_t max_ts,
     mark(hold ? "shade compare (hit)" : "shade compare (miss)", nullptr);
     if (!hold) {
       tsv_shades* sh = nullptr;
-      const int rc = tsv_shades_upload(g, k, vertex_off, vertex_shades, &sh);
-      if (rc == TSV_ERR_INVALID) throw std::invalid_argument(g_error);
-      if (rc) throw CudaError(g_error);
+      shades_upload_impl(g, k, vertex_off, vertex_shades, uni, uc, upat, &sh);
       hold = std::shared_ptr<tsv_shades>(sh, tsv_shades_free);
       std::lock_guard<std::mutex> lk(g->shade_mu);
       g->shade_cache = hold;
