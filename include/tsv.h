@@ -287,8 +287,13 @@ int tsv_profile_reset(void);
 /* Number of engine kernels launched since the last reset. */
 int64_t tsv_kernel_launches(void);
 
-/* GF(2^64) on device: self-test of n products (a[i]*b[i] -> out[i], host
- * buffers) with the production multiply (variant 0) or another variant. */
+/* GF(2^64) on device (replaces gf::mul<uint64_t>, gf.hpp:85-106): self-test
+ * of n products (a[i]*b[i] -> out[i], host buffers) with the production
+ * general multiply (variant 0) or another form: 1 bit-serial, 2 holes +
+ * Karatsuba, 3 holes + schoolbook, 4-6 warp-uniform shared-memory tables, 9
+ * period-5 holes, 10 the per-lane shared-memory table of the vertex-lane
+ * engine's arc products (tsv_gf_bench: 10 / 11 / 12 = 1 / 5 / 10 products
+ * per table build). */
 int tsv_gf_mul_device(int variant, int64_t n, const uint64_t* a,
                       const uint64_t* b, uint64_t* out);
 /* Throughput microbenchmark: products/s of a variant (device only). */

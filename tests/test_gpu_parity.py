@@ -31,8 +31,8 @@ def test_gf_mul_device_matches_reference(cuda_device, golden):
     a = np.array([u64(x[0]) for x in golden["gf_mul"]], np.uint64)
     b = np.array([u64(x[1]) for x in golden["gf_mul"]], np.uint64)
     want = [u64(x[2]) for x in golden["gf_mul"]]
-    for variant in (0, 1):
-        assert _native.gf_mul_device(a, b, variant).tolist() == want
+    for variant in (0, 1, 2, 3, 10):   # production, bit-serial, holes (2 forms), lane table
+        assert _native.gf_mul_device(a, b, variant).tolist() == want, variant
     assert _native.gf_mul_device([1 << 63], [2]).tolist() == [0x1B]
 
 
@@ -46,6 +46,13 @@ def test_gf_mul_device_random_vs_oracle(cuda_device):
     idx = rng.choice(len(a), 3000, replace=False).tolist() + list(range(64))
     for i in idx:
         assert int(got[i]) == O.gf_mul(int(a[i]), int(b[i]))
+    # the lane-table product (gf_device.cuh LaneTable: the vertex-lane engine's
+    # arc products) and the holes forms, on every pair
+    for variant in (2, 3, 10):
+        assert np.array_equal(_native.gf_mul_device(a, b, variant), got), variant
+    assert _native.gf_mul_device([1 << 63], [2], 10).tolist() == [0x1B]
+    assert _native.gf_mul_device([2**64 - 1], [2**64 - 1], 10).tolist() == \
+        [O.gf_mul(2**64 - 1, 2**64 - 1)]
 
 
 def test_edge_y_draws_device(cuda_device):
