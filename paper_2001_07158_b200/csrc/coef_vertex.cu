@@ -198,12 +198,15 @@ struct VertSmem {
   int32_t q_slot[kQCap], q_head[kQCap];
   uint8_t pin[F > 0 ? F : 1][L], pj[F > 0 ? F : 1][L];  // output o: (rank of T_o - {j}, j) pairs
   uint8_t pmask[E];                     // input entry P's subset mask (paired z map)
+  uint8_t pmem[E][L > 1 ? L - 1 : 1];   // the members j of P, ascending
 };
 
 // scratch bytes per warp: the lane table (4 KB, 4 KB aligned) or, without
 // it, the W rows of the paired z map
 template <int E, bool TAB>
-__host__ __device__ constexpr unsigned vert_scratch() { return TAB ? 4096u : static_cast<unsigned>(E) * 256u; }
+__host__ __device__ constexpr unsigned vert_scratch() {
+  return TAB ? 4096u : static_cast<unsigned>(E + 8) * 256u;  // W rows + the row's z_j
+}
 
 template <int K, int L>
 __host__ __device__ constexpr bool vert_uses_table() {
@@ -236,7 +239,12 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
   if (!LAST && lane == 0) {  // output pairs of the z map (colex order, coef_tables)
     constexpr SubsetTab<K, L> TL{};
     constexpr SubsetTab<K, L - 1> TP{};
-    for (int p = 0; p < E; ++p) S.pmask[p] = static_cast<uint8_t>(TP.mask[p]);
+    for (int p = 0; p < E; ++p) {
+      S.pmask[p] = static_cast<uint8_t>(TP.mask[p]);
+      int c = 0;
+      for (int j = 0; j < K; ++j)
+        if ((TP.mask[p] >> j) & 1u) S.pmem[p][c++] = static_cast<uint8_t>(j);
+    }
     for (int o = 0; o < F; ++o) {
       int c = 0;
       for (int j = 0; j < K; ++j)
@@ -295,12 +303,16 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       // one product per input entry and one per output (C5, L = 3: 20
       // instead of 30).  W rides in shared memory, the loops stay rolled.
       if constexpr (kZPairOk) {
+        // the row's z_j next to its W entries (table entries E+1 .. E+K of
+        // the lane's column): the output loop picks them by a dynamic index
+        static_assert(E + K <= 15, "lane-table column holds W and z");
+#pragma unroll
+        for (int j = 0; j < K; ++j) wrow[(E + j) * 32] = z[j];
 #pragma unroll kZUnroll
         for (int p = 0; p < E; ++p) {
-          const unsigned pm = S.pmask[p];
           uint64_t zp = 0;
 #pragma unroll
-          for (int j = 0; j < K; ++j) zp ^= ((pm >> j) & 1u) ? z[j] : 0ull;
+          for (int c = 0; c < L - 1; ++c) zp ^= wrow[(E + S.pmem[p][c]) * 32];
           wrow[p * 32] = gf_reduce_alu(clmul64_kara_s(ksplit(zp), ksplit(S.q[p][qi])));
         }
 #pragma unroll kZUnroll
@@ -309,10 +321,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
 #pragma unroll
           for (int c = 0; c < L; ++c) {
             const int j = S.pj[o][c], pi = S.pin[o][c];
-            uint64_t zj = z[0];
-#pragma unroll
-            for (int jj = 1; jj < K; ++jj) zj = j == jj ? z[jj] : zj;
-            zt ^= zj;
+            zt ^= wrow[(E + j) * 32];  // z_j of this row (stored below)
             su ^= S.q[pi][qi];
             sw ^= wrow[pi * 32];
           }
