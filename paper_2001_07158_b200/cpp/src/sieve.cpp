@@ -3,6 +3,7 @@
 // eval_temporal_sieve replaces sieve.cpp:720-732 by the C-ABI call.
 #include <cstdlib>
 #include "tsieve/sieve.hpp"
+#include "tsieve/prefault.hpp"
 
 #include <algorithm>
 #include <bit>
@@ -90,6 +91,7 @@ ShadeAssignment build_shades(const MotifQuery& query, const VertexColoring& colo
     f = in ? first[col] : 0;
     c = in ? many[col] : 0;
   };
+  detail::reserve_prefaulted(sh.vertex_off, static_cast<size_t>(n) + 1);
   sh.vertex_off.assign(static_cast<size_t>(n) + 1, 0);
   const std::int64_t block = std::int64_t{1} << 16;
   const std::int64_t nb = (n + block - 1) / block;
@@ -106,6 +108,7 @@ ShadeAssignment build_shades(const MotifQuery& query, const VertexColoring& colo
     part[b + 1] = acc;
   }
   for (std::int64_t b = 0; b < nb; ++b) part[b + 1] += part[b];
+  detail::reserve_prefaulted(sh.vertex_shades, static_cast<size_t>(part[nb]));
   sh.vertex_shades.resize(static_cast<size_t>(part[nb]));
 #pragma omp parallel for schedule(static) if (n > (1 << 20))
   for (std::int64_t b = 0; b < nb; ++b) {
@@ -160,6 +163,7 @@ SieveOutcome eval_temporal_sieve(const TemporalGraph& g, int k, Timestamp max_ts
   c.memory_cap_words = engine_cap(config);
 
   SieveOutcome out;
+  detail::reserve_prefaulted(out.accumulators, static_cast<size_t>(g.n()));
   out.accumulators.assign(static_cast<size_t>(g.n()), 0);
   std::uint64_t scratch = 0;
   tsv_outcome o{};
@@ -197,6 +201,7 @@ void finish(SieveOutcome& out, int k, const SieveConfig& config, const tsv_outco
     cnt[static_cast<size_t>(b) + 1] = c;
   }
   for (int64_t b = 0; b < nb; ++b) cnt[b + 1] += cnt[b];
+  detail::reserve_prefaulted(out.flagged, static_cast<size_t>(cnt[nb]));
   out.flagged.resize(static_cast<size_t>(cnt[nb]));
 #pragma omp parallel for schedule(static) if (n > (1 << 20))
   for (int64_t b = 0; b < nb; ++b) {
@@ -247,6 +252,7 @@ SieveOutcome eval_edge_constrained_sieve(const TemporalGraph& g,
   }
   const int k = static_cast<int>(times.size()) + 1;
   SieveOutcome out;
+  detail::reserve_prefaulted(out.accumulators, static_cast<size_t>(g.n()));
   out.accumulators.assign(static_cast<size_t>(g.n()), 0);
   // a prescribed timestamp with no edge is a certain NO (sieve.cpp:767-774)
   for (Timestamp ts : times)
@@ -280,6 +286,7 @@ SieveOutcome eval_vertex_ordered_sieve(const TemporalGraph& g, const std::vector
   const int k = static_cast<int>(order.size());
   const tsv_config c = to_abi(config);
   SieveOutcome out;
+  detail::reserve_prefaulted(out.accumulators, static_cast<size_t>(g.n()));
   out.accumulators.assign(static_cast<size_t>(g.n()), 0);
   std::uint64_t scratch = 0;
   static const std::int32_t kNoColor = 0;
