@@ -174,7 +174,7 @@ int64_t tsieve_e2e_decide(const char* problem, const int32_t* motif, int32_t mot
   try {
     TemporalGraph g = TemporalGraph::build(g_stage.n, std::move(g_stage.u), std::move(g_stage.v),
                                            std::move(g_stage.ts), g_stage.directed);
-    VertexColoring col(g_stage.colors, g_stage.q);
+    VertexColoring col(std::move(g_stage.colors), g_stage.q);  // staged anew for every decide
     SolveRequest req;
     auto p = problem_from_name(problem);
     if (!p) throw std::invalid_argument("unknown problem");
