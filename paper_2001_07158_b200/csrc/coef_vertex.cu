@@ -35,6 +35,7 @@
 
 #include <cub/cub.cuh>
 
+#include <climits>
 #include <cstdint>
 #include <functional>
 #include <stdexcept>
@@ -391,6 +392,13 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
   uint64_t xc[E], xn[E];
   ld_row(s0, xc);
   int32_t r0 = ld_run(m0, s0, run);
+  // horizon below t (levels < k; level k tests r0): a vertex's arcs are in
+  // time order, so it is done at its first arc past max_ts -- an arc past
+  // the horizon only feeds rows that arcs past the horizon read -- and the
+  // warp stops when all its lanes are
+  const bool hz = !LAST && P.below_t;
+  int32_t t0 = INT32_MAX, t1 = INT32_MAX;
+  if (hz && cnt > 0) t0 = __ldg(P.g.run_ts + run);
   for (int i = 0; i < steps; ++i) {
     uint32_t m2;
     int32_t s2;
@@ -399,7 +407,10 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
     const bool runend = (m0 & kRunEnd) != 0;
     const int32_t run1 = run + (runend ? 1 : 0);
     const int32_t r1 = ld_run(m1, s1, run1);
-    bool live = s0 >= 0;
+    if (hz) t1 = i + 1 < cnt ? __ldg(P.g.run_ts + run1) : INT32_MAX;
+    const bool past = hz && t0 > P.max_ts;
+    if (hz && !__any_sync(kFullV, !past)) break;
+    bool live = s0 >= 0 && !past;
     if (LAST) live = live && r0 <= P.max_ts;
     if (live) {
       const uint64_t y = draw_edge_y(pre, yb, m0 & kEdgeMask);
@@ -414,7 +425,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       }
     }
     if (!LAST) {
-      const int32_t slot = r0;  // -1 unless a referenced run ends here
+      const int32_t slot = past ? -1 : r0;  // -1 unless a referenced run ends here
       const unsigned push = __ballot_sync(kFullV, slot >= 0);
       if (push) {
         if (slot >= 0) {
@@ -434,6 +445,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
     m1 = m2;
     s1 = s2;
     r0 = r1;
+    t0 = t1;
 #pragma unroll
     for (int e = 0; e < E; ++e) xc[e] = xn[e];
   }
