@@ -357,6 +357,12 @@ def test_vertex_engine_vs_oracle(cuda_device, k):
             nz += bool(_oracle_vs_gpu(n, u, v, ts, d, colors, motif, seed, anchor, mt))
         assert nz >= 2
         assert _native.Profile.get("coef_vertex_last")[0] > 0
+        # every kind of horizon (a probe below t stops each vertex at its first
+        # arc past it): the first timestamp, the middle, t - 1, with an anchor
+        for mt, anchor in ((1, (-1, -1)), (2, (-1, -1)), (t // 3, (-1, -1)), (t // 2, (4, 11)),
+                           (t - 1, (-1, -1)), (t, (4, 11))):
+            _oracle_vs_gpu(n, u, v, ts, True, ones, [1] * k, 21 + mt, anchor, mt)
+            _oracle_vs_gpu(n, u, v, ts, False, ones, [1] * k, 22 + mt, anchor, mt)
         # hub above the in-degree bound (4096 arcs): the arc kernels take over
         hv = np.concatenate([v, np.zeros(5000, np.int64)])
         hu = np.concatenate([u, rng.integers(1, n, 5000)])
