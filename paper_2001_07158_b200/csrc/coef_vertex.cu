@@ -379,10 +379,10 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
       }
     }
   };
-  // what a step needs of its run: the state slot at a run end (levels < k),
-  // the run's timestamp (level k, horizon test)
+  // what a step needs of its run: the state slot at a run end (levels < k)
   auto ld_run = [&](uint32_t meta, int32_t src, int32_t r) -> int32_t {
-    if (LAST) return src >= 0 ? __ldg(P.g.run_ts + r) : 0;
+    (void)src;
+    if (LAST) return -1;
     return (meta & kRunEnd) ? __ldg(P.g.run_slot + r) : -1;
   };
   uint32_t m0, m1;
@@ -392,11 +392,11 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
   uint64_t xc[E], xn[E];
   ld_row(s0, xc);
   int32_t r0 = ld_run(m0, s0, run);
-  // horizon below t (levels < k; level k tests r0): a vertex's arcs are in
-  // time order, so it is done at its first arc past max_ts -- an arc past
-  // the horizon only feeds rows that arcs past the horizon read -- and the
-  // warp stops when all its lanes are
-  const bool hz = !LAST && P.below_t;
+  // horizon below t: a vertex's arcs are in time order, so it is done at
+  // its first arc past max_ts -- an arc past the horizon only feeds rows
+  // that arcs past the horizon read, and no accumulator -- and the warp
+  // stops when all its lanes are.  At max_ts = t no timestamp is read.
+  const bool hz = P.below_t;
   int32_t t0 = INT32_MAX, t1 = INT32_MAX;
   if (hz && cnt > 0) t0 = __ldg(P.g.run_ts + run);
   for (int i = 0; i < steps; ++i) {
@@ -410,8 +410,7 @@ __global__ void __launch_bounds__(kVWarps * 32, TSV_VMINB) k_coef_vertex(const V
     if (hz) t1 = i + 1 < cnt ? __ldg(P.g.run_ts + run1) : INT32_MAX;
     const bool past = hz && t0 > P.max_ts;
     if (hz && !__any_sync(kFullV, !past)) break;
-    bool live = s0 >= 0 && !past;
-    if (LAST) live = live && r0 <= P.max_ts;
+    const bool live = s0 >= 0 && !past;
     if (live) {
       const uint64_t y = draw_edge_y(pre, yb, m0 & kEdgeMask);
       if constexpr (kTab) {
