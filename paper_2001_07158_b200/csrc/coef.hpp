@@ -28,9 +28,10 @@ struct CoefParams {
   uint64_t* agg = nullptr;           // C x E: chunk tail prefixes
   uint64_t* ulast = nullptr;         // n x k: level-k vertex sums (zeroed)
   int32_t max_ts = 0;
-  // max_ts is below the graph's last timestamp (a binary-search probe): the
-  // vertex-lane engine then stops a vertex at its first arc past the horizon
-  // at every level (false: no arc is past it, no timestamp is read)
+  // some arc may land past max_ts (a binary-search probe below t, or an edge
+  // model with transition times): the vertex-lane engine then stops a
+  // vertex at its first arc past the horizon at every level (false: no arc
+  // is past it, no timestamp is read)
   bool below_t = true;
   // per vertex: -1 no shade (S = 0), d = its only shade, -2 several
   // (nullptr: no zero skipping, no single-shade form)

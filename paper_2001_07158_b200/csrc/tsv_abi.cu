@@ -962,7 +962,8 @@ bool eval_coef(const tsv_graph* g, const tsv_shades* sh, int k, int32_t max_ts,
       cp.s_prev = A;
       cp.ubuf = B;
       cp.max_ts = max_ts;
-      cp.below_t = max_ts < g->host.t;
+      // (with transition times an arc can land past t: always test then)
+      cp.below_t = max_ts < g->host.t || g->model != 0;
       tsv::launch_coef_vertex(cp, *vl, scale, d_acc, st);
       TSV_CUDA(cudaGetLastError());
       std::swap(A, B);
@@ -2351,7 +2352,8 @@ static int eval_vertex_level_impl(const tsv_graph* g, const tsv_shades* s, int k
     cp.s_prev = d_prev;
     cp.ubuf = d_cur;
     cp.max_ts = max_ts;
-    cp.below_t = max_ts < g->host.t;
+    // (with transition times an arc can land past t: always test then)
+      cp.below_t = max_ts < g->host.t || g->model != 0;
     tsv::VertPeers peers;
     if (peer_cur && world > 1 && level < k) {
       // the reader byte of every slot comes with the exchange lists
